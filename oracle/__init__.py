@@ -1,0 +1,202 @@
+"""CPU oracle for the AJM hot path -- TEST INFRASTRUCTURE, not product code.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / ``--impl reference`` legs may
+import this package.  The product path (paper_2407_03272_b200) never imports it and shares no code
+with it.  The arithmetic lives in plain C (ajm_oracle.c, FP64, -ffp-contract=off); this module only
+builds it with gcc and marshals numpy arrays through ctypes.
+
+Each function cites the passage it follows (PAPER.md = P, SPEC.md = S, readings R#):
+  spmv            Q x, ascending-column row sums                       (P:463 Q y^t)
+  build_jdiag     eq-J-diag  J_kk = Q_kk + sum_{j!=k}|Q_kj|
+  diag            D = diag(Q)
+  alpha_next      alpha_{t+1} = (1 + sqrt(1 + 4 alpha_t^2))/2
+  objective       f(x) = 1/2<x,Qx> - <b,x>
+  rel_residual    ||b - Qx|| / ||b||
+  solve           Alg. 3, s = 1, literal two-SpMV form                 (R5-R10, R19)
+
+Pins: tests/test_oracle_pins.py ties every function above to something other than itself (SPEC
+worked values, dense Cholesky / pseudo-inverse solves, Thm 2.3 / Lemma 2.2 / Lemma 2.4 / Thm 2.5,
+the restart-count bound, the alpha identities, the Jacobi / weighted-Jacobi reductions and the
+§4.1 closed forms).  No function here is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+import subprocess
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "ajm_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "libajm_oracle.so")
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared", "-std=c11"]
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (building the checker is not using it)."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        P = ctypes.c_void_p
+        I64 = ctypes.c_int64
+        lib.oracle_spmv.argtypes = [I64, P, P, P, P, P]
+        lib.oracle_build_jdiag.argtypes = [I64, P, P, P, P]
+        lib.oracle_build_jdiag.restype = ctypes.c_int
+        lib.oracle_diag.argtypes = [I64, P, P, P, P]
+        lib.oracle_alpha_next.argtypes = [ctypes.c_double]
+        lib.oracle_alpha_next.restype = ctypes.c_double
+        lib.oracle_objective.argtypes = [I64, P, P, P, P, P]
+        lib.oracle_objective.restype = ctypes.c_double
+        lib.oracle_rel_residual.argtypes = [I64, P, P, P, P, P]
+        lib.oracle_rel_residual.restype = ctypes.c_double
+        lib.oracle_dot.argtypes = [I64, P, P]
+        lib.oracle_dot.restype = ctypes.c_double
+        lib.oracle_set_threads.argtypes = [ctypes.c_int]
+        lib.oracle_get_threads.restype = ctypes.c_int
+        lib.oracle_ajm_solve.argtypes = [I64, P, P, P, P, P, P, ctypes.c_double, I64, ctypes.c_int,
+                                         ctypes.c_int, I64, ctypes.c_int, P, P, P, P, P, P, P, P,
+                                         P, I64, P]
+        lib.oracle_ajm_solve.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _csr(Q):
+    rp = np.ascontiguousarray(Q.row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(Q.col, dtype=np.int32)
+    v = np.ascontiguousarray(Q.val, dtype=np.float64)
+    return rp, ci, v
+
+
+def _vec(x):
+    return np.ascontiguousarray(x, dtype=np.float64)
+
+
+def set_threads(nt: int) -> None:
+    _load().oracle_set_threads(int(nt))
+
+
+def get_threads() -> int:
+    return int(_load().oracle_get_threads())
+
+
+def spmv(Q, x) -> np.ndarray:
+    rp, ci, v = _csr(Q)
+    x = _vec(x)
+    y = np.empty(Q.n)
+    _load().oracle_spmv(Q.n, _p(rp), _p(ci), _p(v), _p(x), _p(y))
+    return y
+
+
+class OracleError(ValueError):
+    pass
+
+
+def build_jdiag(Q) -> np.ndarray:
+    rp, ci, v = _csr(Q)
+    J = np.empty(Q.n)
+    err = _load().oracle_build_jdiag(Q.n, _p(rp), _p(ci), _p(v), _p(J))
+    if err:
+        raise OracleError({1: "negative diagonal", 2: "zero row (J_kk = 0)", 3: "non-finite value"}[err])
+    return J
+
+
+def diag(Q) -> np.ndarray:
+    rp, ci, v = _csr(Q)
+    d = np.empty(Q.n)
+    _load().oracle_diag(Q.n, _p(rp), _p(ci), _p(v), _p(d))
+    return d
+
+
+def alpha_next(a: float) -> float:
+    return float(_load().oracle_alpha_next(float(a)))
+
+
+def objective(Q, b, x) -> float:
+    rp, ci, v = _csr(Q)
+    return float(_load().oracle_objective(Q.n, _p(rp), _p(ci), _p(v), _p(_vec(b)), _p(_vec(x))))
+
+
+def rel_residual(Q, b, x) -> float:
+    rp, ci, v = _csr(Q)
+    r = float(_load().oracle_rel_residual(Q.n, _p(rp), _p(ci), _p(v), _p(_vec(b)), _p(_vec(x))))
+    if np.isnan(r):
+        raise OracleError("||b|| = 0: stopping rule undefined")
+    return r
+
+
+STATUS = {0: "converged", 1: "maxiter", 2: "diverged"}
+
+
+@dataclasses.dataclass
+class OracleResult:
+    x: np.ndarray
+    status: str
+    iterations: int
+    n_restarts: int
+    x_is_prerestart: bool
+    restart_iters: list
+    res_hist: np.ndarray
+    f_hist: np.ndarray
+    d_hist: np.ndarray
+    dabs_hist: np.ndarray
+    xt_hist: np.ndarray | None
+    alpha_hist: np.ndarray | None
+
+
+def solve(Q, b, D=None, x0=None, tol=1e-6, maxit=1000, momentum=True, restart=True, k0=2,
+          mirror=False, forced=None, record_iterates=False, dmode="jdiag") -> OracleResult:
+    """Alg. 3.  D defaults to eq-J-diag; dmode='qdiag' uses diag(Q) (eq-jacobi)."""
+    rp, ci, v = _csr(Q)
+    n = Q.n
+    b = _vec(b)
+    if D is None:
+        D = build_jdiag(Q) if dmode == "jdiag" else diag(Q)
+    D = _vec(D)
+    x0a = None if x0 is None else _vec(x0)
+    m1 = maxit + 1
+    res_hist = np.zeros(m1)
+    f_hist = np.zeros(m1)
+    d_hist = np.zeros(m1)
+    dabs_hist = np.zeros(m1)
+    xt_hist = np.zeros(m1 * n) if record_iterates else None
+    alpha_hist = np.zeros(m1) if record_iterates else None
+    fa = None if forced is None else np.ascontiguousarray(forced, dtype=np.int8)
+    cap = 4096
+    rit = np.zeros(cap, dtype=np.int64)
+    info = np.zeros(6, dtype=np.int64)
+    x_out = np.empty(n)
+    rc = _load().oracle_ajm_solve(n, _p(rp), _p(ci), _p(v), _p(b), _p(D), _p(x0a), float(tol),
+                                  int(maxit), int(bool(momentum)), int(bool(restart)), int(k0),
+                                  int(bool(mirror)), _p(fa), _p(x_out), _p(res_hist), _p(f_hist),
+                                  _p(d_hist), _p(dabs_hist), _p(xt_hist), _p(alpha_hist), _p(rit),
+                                  cap, _p(info))
+    if rc == -1:
+        raise OracleError("invalid argument")
+    if rc == -2:
+        raise OracleError("||b|| = 0")
+    if rc != 0:
+        raise OracleError(f"oracle failure {rc}")
+    it = int(info[1])
+    k = it + 1
+    return OracleResult(
+        x=x_out, status=STATUS[int(info[0])], iterations=it, n_restarts=int(info[2]),
+        x_is_prerestart=bool(info[3]), restart_iters=[int(r) for r in rit[: int(info[4])]],
+        res_hist=res_hist[:k], f_hist=f_hist[:k], d_hist=d_hist[:k], dabs_hist=dabs_hist[:k],
+        xt_hist=None if xt_hist is None else xt_hist.reshape(m1, n)[:k],
+        alpha_hist=None if alpha_hist is None else alpha_hist[:k])
