@@ -434,3 +434,15 @@ def test_restart_tie_restarts_and_forcing():
     alt = oracle.solve(p.Q, p.b, tol=0.0, maxit=300, restart=True, forced=forced)
     assert t0 not in alt.restart_iters
     np.testing.assert_array_equal(alt.res_hist[:t0 + 1], base.res_hist[:t0 + 1])
+
+
+def test_restart_window_and_doubling():
+    """Alg. 3 lines 5-7: a restart needs t > K_re + K_l, then K_re = t and K_{l+1} = 2 K_l.
+    Forcing every decision to 'restart' makes restarts fire at the earliest admissible t:
+    K0 = 2 -> 3, 8, 17, 34, 67, 132 (t_{l+1} = t_l + 2^l K0 + 1)."""
+    p = synth.config_problem(1)
+    forced = np.ones(201, dtype=np.int8)
+    r = oracle.solve(p.Q, p.b, tol=0.0, maxit=200, restart=True, k0=2, forced=forced)
+    assert r.restart_iters == [3, 8, 17, 34, 67, 132]
+    r = oracle.solve(p.Q, p.b, tol=0.0, maxit=200, restart=True, k0=5, forced=forced)
+    assert r.restart_iters == [6, 17, 38, 79, 160]
