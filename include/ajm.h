@@ -1,0 +1,171 @@
+/*
+ * ajm.h -- C ABI of the B200-native accelerated Jacobi-type method (AJM) solver, arXiv 2407.03272.
+ *
+ * The library solves a consistent symmetric positive semidefinite system Q x = b
+ * (eq-linear-sys), equivalently min f(x) = 1/2<x,Qx> - <b,x> (PAPER.md:25-28,
+ * eq-qp), with the parallel Nesterov-accelerated Jacobi-type method with adaptive restart,
+ * Algorithm 3 on one GPU (s = 1 block: the GPU's row-parallel pass is the
+ * "for i parallel" loop of Alg. 3 line 3).  Everything is FP64.  Every step of every iteration runs
+ * in this library's own sm_100a kernels; there is no CPU fallback.
+ *
+ * Conventions shared by every entry point
+ *   - extern "C", plain pointers and sizes.  An array pointer may be HOST memory (pageable or
+ *     pinned) or DEVICE memory of the current CUDA device; the library detects which with
+ *     cudaPointerGetAttributes and copies accordingly (host<->device copies are stream-ordered on
+ *     `cuda_stream`).
+ *   - `cuda_stream` is a cudaStream_t (NULL = the legacy default stream); all device work of a call
+ *     is ordered on it.  ajm_create and ajm_solve return only after the stream reaches the end of
+ *     their work (their results are host-visible).
+ *   - A handle is not thread-safe; distinct handles are independent.
+ *   - On error a call returns a non-zero ajm_status_t and ajm_last_error() explains it; no output
+ *     argument is written except where stated.
+ */
+#ifndef AJM_H_
+#define AJM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AJM_ABI_VERSION 1
+
+typedef struct ajm_ctx* ajm_handle_t;
+
+typedef enum {
+    AJM_OK = 0,
+    AJM_ERR_INVALID_ARG = 1,   /* NULL / size mismatch, tol < 0 or NaN, maxit < 1, k0 < 2,
+                                  restart without momentum, n or nnz out of range */
+    AJM_ERR_CSR_INVALID = 2,   /* row_ptr[0] != 0, row_ptr decreasing, row_ptr[n] != nnz, column out of
+                                  range or not strictly increasing within a row            */
+    AJM_ERR_NOT_SYMMETRIC = 3, /* Q_ij != Q_ji (only checked with AJM_VALIDATE_SYMMETRY)   */
+    AJM_ERR_NONFINITE = 4,     /* NaN/Inf in Q, b, d or x0                                     */
+    AJM_ERR_NEGATIVE_DIAG = 5, /* some Q_kk < 0: Q cannot be SPSD                                     */
+    AJM_ERR_ZERO_DIAG = 6,     /* some D_kk = 0 (zero row / isolated node) or user d_k <= 0 */
+    AJM_ERR_ZERO_RHS = 7,      /* ||b|| = 0: the relative-residual stopping rule is undefined */
+    AJM_ERR_CUDA = 8,          /* a CUDA runtime call failed (message in ajm_last_error)              */
+    AJM_ERR_OOM = 9,           /* device allocation failed                                            */
+    AJM_ERR_UNSUPPORTED = 10   /* e.g. nnz >= 2^31 (device column/offset type is int32)              */
+} ajm_status_t;
+
+/* The diagonal metric D of the Jacobi-type step x = y + D^{-1}(b - Q y). */
+typedef enum {
+    AJM_D_JDIAG = 0, /* eq-J-diag: D_kk = J_kk = Q_kk + sum_{j != k}|Q_kj|, built on
+                        the device, summed in ascending column order.  S = J - Q is PSD,
+                        which is what Thm 2.3 / 2.5 need.  The default and the paper's experiments. */
+    AJM_D_USER = 1,  /* the caller's positive diagonal d[n], e.g. diag(Q)/omega for weighted Jacobi */
+    AJM_D_QDIAG = 2  /* D = diag(Q): classical Jacobi metric; no S >= 0 guarantee */
+} ajm_dmode_t;
+
+/* ajm_create flags */
+#define AJM_VALIDATE_SYMMETRY 0x1u /* also check Q_ij == Q_ji bitwise (O(nnz log rowlen) kernel)    */
+#define AJM_LOOP_HOST 0x10u        /* debug: host-driven loop of pass launches instead of the device
+                                      CUDA-graph WHILE loop (same kernels, same results)             */
+
+/* Iteration policy. */
+typedef struct {
+    int32_t momentum; /* 1: Nesterov alpha schedule alpha_{t+1} = (1 + sqrt(1 + 4 alpha_t^2))/2,
+                         beta_t = (alpha_t - 1)/alpha_{t+1} (Alg. 1/3);
+                         0: beta = 0, the variable-metric gradient / Jacobi step (eq-gd)   */
+    int32_t restart;  /* 1: adaptive restart = Alg. 3 IsRestart; 0: Alg. 1.
+                         restart = 1 with momentum = 0 -> AJM_ERR_INVALID_ARG                       */
+    int64_t k0;       /* K_0 >= 2, the first prohibition period ("K_l >= 2"); default 2      */
+} ajm_policy_t;
+
+typedef enum { AJM_CONVERGED = 0, AJM_MAXITER = 1, AJM_DIVERGED = 2 } ajm_term_t;
+
+typedef struct {
+    int32_t status;          /* ajm_term_t                                                          */
+    int32_t n_restarts;      /* restarts executed (Alg. 3 line 6 taken), ell at exit                */
+    int64_t iterations;      /* t at exit; 0 if x0 already satisfies the tolerance                  */
+    double rel_residual;     /* ||b - Q x~^t|| / ||b|| of the last evaluated iterate        */
+    double f;                /* f(x~^t) = 1/2<x,Qx> - <b,x> of the same iterate           */
+    int32_t x_is_prerestart; /* 1 if converged at an iteration whose restart test fired: x_out is the
+                                pre-restart x~^t (R5)                                     */
+    int32_t restarts_logged; /* entries written to restart_iters                                    */
+} ajm_result_t;
+
+/* Layout / launch facts of a handle (for benchmarks and tests). */
+typedef struct {
+    int64_t n, nnz;
+    int64_t units;            /* row units of <= 2048 nonzeros / <= 512 rows (or one long row)  */
+    int64_t long_rows;        /* rows with more than 2048 nonzeros (one CTA each)               */
+    int32_t grid;             /* CTAs of the fused pass kernel (persistent, multiple of #SMs)   */
+    int32_t block;            /* threads per CTA                                                */
+    int32_t sm_count;
+    int32_t ctas_per_sm;
+    double model_bytes_per_iter; /* nnz*12 + 7*n*8 + 4*(n+1)  */
+    double last_loop_ms;      /* device time of the last solve's iteration loop (CUDA events)  */
+    int64_t last_passes;      /* fused passes run by the last solve (= iterations + 1)        */
+    int64_t last_graph_launches; /* graph launches of the last solve (1 with the WHILE loop)    */
+} ajm_info_t;
+
+/*
+ * ajm_create -- validate Q, b (and d), build the device layout and the diagonal metric D.
+ *   out       : receives the handle (written only on AJM_OK)
+ *   n, nnz    : 1 <= n < 2^31, 0 <= nnz < 2^31
+ *   row_ptr   : int64[n+1], canonical CSR offsets (row_ptr[0] = 0, nondecreasing, row_ptr[n] = nnz)
+ *   col_idx   : int32[nnz], strictly increasing within each row, 0 <= col < n
+ *   vals      : double[nnz]; BOTH triangles of the symmetric Q are stored
+ *   b         : double[n], consistent right-hand side (b in range(Q) is assumed, not checked)
+ *   dmode     : ajm_dmode_t
+ *   d         : double[n] (> 0) for AJM_D_USER, otherwise ignored (may be NULL)
+ *   flags     : AJM_VALIDATE_SYMMETRY | AJM_LOOP_HOST
+ * Ownership: the handle deep-copies (and re-lays-out) Q, b and D into device memory it owns; the
+ * caller's buffers may be freed when the call returns.
+ */
+ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t* row_ptr,
+                        const int32_t* col_idx, const double* vals, const double* b,
+                        int32_t dmode, const double* d, uint32_t flags, void* cuda_stream);
+
+/*
+ * ajm_solve -- run Algorithm 3 from x0 until ||b - Q x~^t||/||b|| <= tol (converged; x_out = x~^t,
+ * R5), t = maxit (x_out = post-iteration x^t, R10) or divergence (res > 1e8 or non-finite, R19).
+ *   x0            : double[n] initial point (NULL = zeros, the paper's/configs' x0 = 0)
+ *   tol           : >= 0 (0 = run to maxit unless the residual is exactly 0)
+ *   maxit         : >= 1
+ *   policy        : see ajm_policy_t
+ *   x_out         : double[n] (host or device), receives the answer
+ *   res           : host, receives the ajm_result_t (may be NULL)
+ *   res_hist,f_hist : host double[maxit+1] or NULL; entry t (0 <= t <= iterations) is the relative
+ *                   residual / f of the pre-restart iterate x~^t; t = 0 is x0
+ *   restart_iters : host int64[restart_cap] or NULL; iterations t at which a restart executed, in
+ *                   order (ell <= log2(t+2) - 1 < 64)
+ * The whole iteration loop runs on the device (one CUDA-graph launch with a conditional WHILE
+ * node; the restart rule and the stopping test are evaluated on the device; there is no host
+ * round trip per iteration).  The handle's previous solve state is overwritten.
+ */
+ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t maxit,
+                       ajm_policy_t policy, double* x_out, ajm_result_t* res, double* res_hist,
+                       double* f_hist, int64_t* restart_iters, int64_t restart_cap,
+                       void* cuda_stream);
+
+/*
+ * ajm_get_trace -- copy a per-iteration trace of the last solve to host out[count]:
+ *   which = 0 res (as res_hist), 1 f (as f_hist), 2 the restart inner product
+ *   d_t = <Q y^t - b, x~^t - x^{t-1}> (entry 0 = 0), 3 sum_i |(Qy^t - b)_i (x~^t - x^{t-1})_i|
+ *   (the tie-ratio denominator of DESIGN.md R17).  count <= iterations + 1.
+ */
+ajm_status_t ajm_get_trace(ajm_handle_t h, int32_t which, double* out, int64_t count);
+
+/* ajm_get_diag -- copy the diagonal metric D actually used (J for AJM_D_JDIAG) to out[n] (host/device). */
+ajm_status_t ajm_get_diag(ajm_handle_t h, double* out);
+
+/* ajm_get_info -- layout and last-solve timing facts. */
+ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info);
+
+/* ajm_destroy -- free all device memory of the handle (h may be NULL). */
+ajm_status_t ajm_destroy(ajm_handle_t h);
+
+/* ajm_last_error -- message of the last failing call on h; h = NULL gives the calling thread's last
+ * ajm_create failure.  The string is owned by the library and valid until the next call. */
+const char* ajm_last_error(ajm_handle_t h);
+
+/* ajm_abi_version -- AJM_ABI_VERSION of the loaded library. */
+int32_t ajm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AJM_H_ */

@@ -1,0 +1,261 @@
+"""paper_2407_03272_b200 -- B200-native accelerated Jacobi-type method (arXiv 2407.03272, Alg. 3).
+
+Thin ctypes binding of libajm.so (C ABI in include/ajm.h).  Argument marshalling only: every step
+of the method runs in the library's sm_100a kernels.  There is no CPU fallback -- if libajm.so
+is missing, or no CUDA device is present when a solver is created, the calls raise.
+
+Names follow the ABI: ``ajm_create`` / ``ajm_solve`` / ``ajm_destroy`` (+ ``Solver``, a handle
+wrapper).  Arrays may be numpy arrays (host) or torch tensors (host or CUDA); PyTorch is only
+used for device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+
+import numpy as np
+
+__all__ = ["AjmError", "Result", "Solver", "ajm_create", "ajm_solve", "ajm_destroy", "lib",
+           "LIB_PATH", "STATUS_NAMES", "TERM_NAMES", "D_MODES", "model_bytes_per_iter"]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libajm.so")
+
+STATUS_NAMES = {0: "AJM_OK", 1: "AJM_ERR_INVALID_ARG", 2: "AJM_ERR_CSR_INVALID",
+                3: "AJM_ERR_NOT_SYMMETRIC", 4: "AJM_ERR_NONFINITE", 5: "AJM_ERR_NEGATIVE_DIAG",
+                6: "AJM_ERR_ZERO_DIAG", 7: "AJM_ERR_ZERO_RHS", 8: "AJM_ERR_CUDA", 9: "AJM_ERR_OOM",
+                10: "AJM_ERR_UNSUPPORTED"}
+TERM_NAMES = {0: "converged", 1: "maxiter", 2: "diverged"}
+D_MODES = {"jdiag": 0, "user": 1, "qdiag": 2}
+AJM_VALIDATE_SYMMETRY = 0x1
+AJM_LOOP_HOST = 0x10
+
+# every symbol include/ajm.h declares (tests check the .so exports all of them)
+ABI_SYMBOLS = ["ajm_create", "ajm_solve", "ajm_get_trace", "ajm_get_diag", "ajm_get_info",
+               "ajm_destroy", "ajm_last_error", "ajm_abi_version"]
+
+
+class AjmError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+        self.status_name = STATUS_NAMES.get(status, str(status))
+
+
+class ajm_policy_t(ctypes.Structure):
+    _fields_ = [("momentum", ctypes.c_int32), ("restart", ctypes.c_int32), ("k0", ctypes.c_int64)]
+
+
+class ajm_result_t(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("n_restarts", ctypes.c_int32),
+                ("iterations", ctypes.c_int64), ("rel_residual", ctypes.c_double),
+                ("f", ctypes.c_double), ("x_is_prerestart", ctypes.c_int32),
+                ("restarts_logged", ctypes.c_int32)]
+
+
+class ajm_info_t(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("nnz", ctypes.c_int64), ("units", ctypes.c_int64),
+                ("long_rows", ctypes.c_int64), ("grid", ctypes.c_int32), ("block", ctypes.c_int32),
+                ("sm_count", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32),
+                ("model_bytes_per_iter", ctypes.c_double), ("last_loop_ms", ctypes.c_double),
+                ("last_passes", ctypes.c_int64), ("last_graph_launches", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libajm.so (raises if it is missing: no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run __graft_entry__.build() or "
+                              "python paper_2407_03272_b200/build.py")
+        L = ctypes.CDLL(LIB_PATH)
+        P = ctypes.c_void_p
+        I64 = ctypes.c_int64
+        L.ajm_create.argtypes = [ctypes.POINTER(P), I64, I64, P, P, P, P, ctypes.c_int32, P,
+                                 ctypes.c_uint32, P]
+        L.ajm_create.restype = ctypes.c_int
+        L.ajm_solve.argtypes = [P, P, ctypes.c_double, I64, ajm_policy_t, P,
+                                ctypes.POINTER(ajm_result_t), P, P, P, I64, P]
+        L.ajm_solve.restype = ctypes.c_int
+        L.ajm_get_trace.argtypes = [P, ctypes.c_int32, P, I64]
+        L.ajm_get_trace.restype = ctypes.c_int
+        L.ajm_get_diag.argtypes = [P, P]
+        L.ajm_get_diag.restype = ctypes.c_int
+        L.ajm_get_info.argtypes = [P, ctypes.POINTER(ajm_info_t)]
+        L.ajm_get_info.restype = ctypes.c_int
+        L.ajm_destroy.argtypes = [P]
+        L.ajm_destroy.restype = ctypes.c_int
+        L.ajm_last_error.argtypes = [P]
+        L.ajm_last_error.restype = ctypes.c_char_p
+        L.ajm_abi_version.restype = ctypes.c_int32
+        _lib = L
+    return _lib
+
+
+def _ptr(a, dtype):
+    """(pointer, keepalive) of a numpy array or torch tensor with the given numpy dtype."""
+    if a is None:
+        return None, None
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            tdt = {np.float64: torch.float64, np.int64: torch.int64, np.int32: torch.int32}[dtype]
+            if a.dtype != tdt or not a.is_contiguous():
+                a = a.to(tdt).contiguous()
+            return ctypes.c_void_p(a.data_ptr()), a
+    except ImportError:  # pragma: no cover
+        pass
+    arr = np.ascontiguousarray(a, dtype=dtype)
+    return arr.ctypes.data_as(ctypes.c_void_p), arr
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _check(st: int, handle=None):
+    if st != 0:
+        msg = lib().ajm_last_error(handle)
+        raise AjmError(st, msg.decode() if msg else "")
+
+
+def model_bytes_per_iter(n: int, nnz: int) -> float:
+    """Algorithmic bytes of one fused pass: nnz*12 + 7 vectors * n * 8 + int32 row_ptr
+    (DESIGN.md §4)."""
+    return 12.0 * nnz + 56.0 * n + 4.0 * (n + 1)
+
+
+def ajm_create(n, nnz, row_ptr, col_idx, vals, b, dmode="jdiag", d=None, flags=0, stream=None):
+    """Marshal to ajm_create; returns the opaque handle (int)."""
+    keep = []
+    ptrs = []
+    for a, dt in ((row_ptr, np.int64), (col_idx, np.int32), (vals, np.float64), (b, np.float64),
+                  (d, np.float64)):
+        p, k = _ptr(a, dt)
+        ptrs.append(p)
+        keep.append(k)
+    h = ctypes.c_void_p()
+    dm = D_MODES[dmode] if isinstance(dmode, str) else int(dmode)
+    st = lib().ajm_create(ctypes.byref(h), int(n), int(nnz), ptrs[0], ptrs[1], ptrs[2], ptrs[3],
+                          dm, ptrs[4], int(flags), _stream(stream))
+    _check(st, None)
+    return h.value
+
+
+def ajm_solve(handle, x0, tol, maxit, momentum=True, restart=True, k0=2, x_out=None,
+              res_hist=None, f_hist=None, restart_iters=None, stream=None):
+    """Marshal to ajm_solve; returns the ajm_result_t."""
+    p0, k_0 = _ptr(x0, np.float64)
+    px, k_x = _ptr(x_out, np.float64)
+    pr, k_r = _ptr(res_hist, np.float64)
+    pf, k_f = _ptr(f_hist, np.float64)
+    pri, k_ri = _ptr(restart_iters, np.int64)
+    cap = 0 if restart_iters is None else len(restart_iters)
+    res = ajm_result_t()
+    pol = ajm_policy_t(int(bool(momentum)), int(bool(restart)), int(k0))
+    st = lib().ajm_solve(ctypes.c_void_p(handle), p0, float(tol), int(maxit), pol, px,
+                         ctypes.byref(res), pr, pf, pri, cap, _stream(stream))
+    _check(st, ctypes.c_void_p(handle))
+    return res
+
+
+def ajm_destroy(handle):
+    if handle:
+        _check(lib().ajm_destroy(ctypes.c_void_p(handle)))
+
+
+@dataclasses.dataclass
+class Result:
+    x: object
+    status: str
+    iterations: int
+    rel_residual: float
+    f: float
+    n_restarts: int
+    x_is_prerestart: bool
+    restart_iters: list
+    res_hist: np.ndarray | None
+    f_hist: np.ndarray | None
+
+
+class Solver:
+    """Handle wrapper: ``Solver(Q_csr_arrays, b, dmode, d).solve(x0, tol, maxit, policy)``.
+
+    row_ptr/col/val/b/d may be numpy arrays (copied host->device by the library) or torch tensors
+    (device arrays are copied device->device).  The solver owns its device copy afterwards."""
+
+    def __init__(self, n, row_ptr, col, val, b, dmode="jdiag", d=None, validate_symmetry=False,
+                 loop="graph", stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2407_03272_b200 needs a CUDA device (no CPU fallback)")
+        self.n = int(n)
+        self.nnz = int(row_ptr[-1])
+        flags = (AJM_VALIDATE_SYMMETRY if validate_symmetry else 0) | (AJM_LOOP_HOST if loop == "host" else 0)
+        self._stream = stream
+        self.handle = ajm_create(self.n, self.nnz, row_ptr, col, val, b, dmode, d, flags, stream)
+
+    @classmethod
+    def from_csr(cls, Q, b, **kw):
+        return cls(Q.n, Q.row_ptr, Q.col, Q.val, b, **kw)
+
+    def solve(self, x0=None, tol=1e-6, maxit=1000, momentum=True, restart=True, k0=2,
+              x_out=None, history=True, restart_cap=64) -> Result:
+        import torch
+        if x_out is None:
+            x_out = torch.empty(self.n, dtype=torch.float64, device="cuda")
+        rh = np.empty(maxit + 1) if history else None
+        fh = np.empty(maxit + 1) if history else None
+        ri = np.zeros(restart_cap, dtype=np.int64)
+        r = ajm_solve(self.handle, x0, tol, maxit, momentum, restart, k0, x_out, rh, fh, ri,
+                      self._stream)
+        k = r.iterations + 1
+        return Result(x=x_out, status=TERM_NAMES[r.status], iterations=int(r.iterations),
+                      rel_residual=r.rel_residual, f=r.f, n_restarts=int(r.n_restarts),
+                      x_is_prerestart=bool(r.x_is_prerestart),
+                      restart_iters=[int(v) for v in ri[: r.restarts_logged]],
+                      res_hist=None if rh is None else rh[:k], f_hist=None if fh is None else fh[:k])
+
+    def trace(self, which: str, count: int) -> np.ndarray:
+        out = np.empty(count)
+        w = {"res": 0, "f": 1, "d": 2, "dabs": 3}[which]
+        _check(lib().ajm_get_trace(ctypes.c_void_p(self.handle), w, out.ctypes.data_as(ctypes.c_void_p),
+                                   int(count)), ctypes.c_void_p(self.handle))
+        return out
+
+    def diag(self) -> np.ndarray:
+        out = np.empty(self.n)
+        _check(lib().ajm_get_diag(ctypes.c_void_p(self.handle), out.ctypes.data_as(ctypes.c_void_p)),
+               ctypes.c_void_p(self.handle))
+        return out
+
+    def info(self) -> dict:
+        inf = ajm_info_t()
+        _check(lib().ajm_get_info(ctypes.c_void_p(self.handle), ctypes.byref(inf)),
+               ctypes.c_void_p(self.handle))
+        return {f: getattr(inf, f) for f, _ in ajm_info_t._fields_}
+
+    def close(self):
+        if getattr(self, "handle", None):
+            ajm_destroy(self.handle)
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,67 @@
+"""Shared helpers for the -m gpu parity tests (GPU path via the C-ABI binding vs the CPU oracle)."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+PARITY_TOL = 1e-10  # north_star: max|x_gpu - x_cpu| / max|x_cpu| <= 1e-10 after 1000 FP64 iterations
+TIE_RATIO = 1e-10   # DESIGN.md R17: restart decisions with |d| / sum|terms| <= this may flip
+
+
+def cuda_ok():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+requires_cuda = pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")
+
+
+def oracle_threads():
+    oracle.set_threads(min(os.cpu_count() or 1, 32))
+
+
+def gpu_solve(Q, b, x0=None, tol=0.0, maxit=1000, restart=True, momentum=True, k0=2,
+              dmode="jdiag", d=None, loop="graph", device_inputs=False):
+    import torch
+    import paper_2407_03272_b200 as ajm
+    args = [Q.row_ptr, Q.col, Q.val, b, d, x0]
+    if device_inputs:
+        args = [None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in args]
+    with ajm.Solver(Q.n, args[0], args[1], args[2], args[3], dmode=dmode, d=args[4], loop=loop) as s:
+        r = s.solve(x0=args[5], tol=tol, maxit=maxit, momentum=momentum, restart=restart, k0=k0)
+        r.x = r.x.cpu().numpy()
+        r.d_trace = s.trace("d", r.iterations + 1)
+        r.dabs_trace = s.trace("dabs", r.iterations + 1)
+        r.D = s.diag()
+        r.info = s.info()
+    return r
+
+
+def max_rel(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def oracle_matching(Q, b, g, **kw):
+    """Oracle run that follows the GPU's restart decisions where (and only where) they are
+    near-ties (R17).  Returns (oracle result, number of forced decisions)."""
+    o = oracle.solve(Q, b, **kw)
+    forced_n = 0
+    for _ in range(8):
+        if o.restart_iters == g.restart_iters:
+            return o, forced_n
+        go, oo = set(g.restart_iters), set(o.restart_iters)
+        t = min(go.symmetric_difference(oo))
+        ratio = abs(o.d_hist[t]) / max(o.dabs_hist[t], 1e-300) if t < len(o.d_hist) else 0.0
+        assert ratio <= TIE_RATIO, f"restart decision differs at t={t} with tie ratio {ratio:.3e}"
+        forced = np.full(kw.get("maxit", 1000) + 1, -1, dtype=np.int8)
+        for tt in range(t, len(forced)):
+            forced[tt] = 1 if tt in go else 0
+        forced_n += 1
+        o = oracle.solve(Q, b, forced=forced, **kw)
+    raise AssertionError("restart schedules could not be matched")

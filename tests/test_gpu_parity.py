@@ -1,0 +1,186 @@
+"""GPU (C-ABI, sm_100a kernels) vs CPU oracle parity.  North-star bar: after 1000 FP64 iterations
+max|x_gpu - x_cpu| / max|x_cpu| <= 1e-10 and iterations-to-tol within +-1 (restart decisions may
+flip only at near-ties, R17).  Inputs: seeded synthetic configs (synth/) at sizes the
+oracle finishes in seconds, spanning many row units / CTAs and ragged tails."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from _gpu_helpers import (PARITY_TOL, gpu_solve, max_rel, oracle_matching, oracle_threads,
+                          requires_cuda)
+
+pytestmark = [pytest.mark.gpu, requires_cuda]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _threads():
+    oracle_threads()
+
+
+# (config, scale) pairs: oracle-sized versions of BASELINE configs 1-5
+CASES = [(1, 1.0), (2, 0.25), (3, 0.02), (4, 0.0125), (5, 0.09375)]
+
+
+@pytest.mark.parametrize("cfg,scale", CASES)
+@pytest.mark.parametrize("restart", [True, False])
+def test_parity_1000_iterations(cfg, scale, restart):
+    p = synth.config_problem(cfg, scale)
+    g = gpu_solve(p.Q, p.b, tol=0.0, maxit=1000, restart=restart)
+    o, nforced = oracle_matching(p.Q, p.b, g, tol=0.0, maxit=1000, restart=restart)
+    assert g.status == o.status and g.iterations == o.iterations
+    assert max_rel(g.x, o.x) <= PARITY_TOL, (cfg, max_rel(g.x, o.x), nforced)
+    np.testing.assert_array_equal(g.D, oracle.build_jdiag(p.Q))  # eq-J-diag bitwise
+    # residual history of the same iterates (rounding-level differences only)
+    k = min(len(g.res_hist), len(o.res_hist))
+    assert np.all(np.abs(g.res_hist[:k] - o.res_hist[:k]) <= 1e-9 * o.res_hist[:k] + 1e-12 * o.res_hist[0])
+
+
+@pytest.mark.parametrize("cfg,scale", CASES)
+def test_iterations_to_tol(cfg, scale):
+    """Iterations to 1e-6 within +-1 of the oracle (north_star)."""
+    p = synth.config_problem(cfg, scale)
+    g = gpu_solve(p.Q, p.b, tol=1e-6, maxit=5000, restart=True)
+    o = oracle.solve(p.Q, p.b, tol=1e-6, maxit=5000, restart=True)
+    assert g.status == "converged" and o.status == "converged"
+    assert abs(g.iterations - o.iterations) <= 1, (g.iterations, o.iterations)
+    assert g.res_hist[-1] <= 1e-6
+
+
+def test_bitwise_equal_to_mirror_oracle():
+    """Rows of <= 32 nonzeros are summed sequentially in ascending column order from 0.0 and no
+    FMA is contracted (R14), so the GPU iterates are BITWISE those of the oracle's mirror mode
+    (same single-SpMV algebra) whenever the restart decisions agree."""
+    p = synth.config_problem(1)
+    for restart in (False, True):
+        g = gpu_solve(p.Q, p.b, tol=0.0, maxit=2000, restart=restart)
+        m = oracle.solve(p.Q, p.b, tol=0.0, maxit=2000, restart=restart, mirror=True)
+        if g.restart_iters == m.restart_iters:
+            np.testing.assert_array_equal(g.x, m.x)
+        else:
+            t = min(set(g.restart_iters) ^ set(m.restart_iters))
+            assert m.res_hist[t] < 1e-13  # only at machine-precision residuals
+
+
+def test_determinism_and_loop_modes():
+    p = synth.config_problem(2, 0.25)
+    a = gpu_solve(p.Q, p.b, tol=0.0, maxit=300)
+    b = gpu_solve(p.Q, p.b, tol=0.0, maxit=300)
+    c = gpu_solve(p.Q, p.b, tol=0.0, maxit=300, loop="host")
+    d = gpu_solve(p.Q, p.b, tol=0.0, maxit=300, device_inputs=True)
+    for o in (b, c, d):
+        np.testing.assert_array_equal(a.x, o.x)
+        np.testing.assert_array_equal(a.res_hist, o.res_hist)
+        np.testing.assert_array_equal(a.f_hist, o.f_hist)
+    assert a.info["last_graph_launches"] == 1 and a.info["last_passes"] == 301
+
+
+# ------------------------------------------------------------------------------------------------
+# edge cases
+# ------------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [40, 600, 3000])
+def test_long_rows_sdd(n):
+    """§4.1 matrix: rows of length n exercise the warp-per-row (33..2048) and the
+    CTA-per-row (> 2048) reductions."""
+    Q = synth.sdd(n)
+    b = np.ones(n)
+    g = gpu_solve(Q, b, tol=1e-10, maxit=3000, restart=True)
+    o, _ = oracle_matching(Q, b, g, tol=1e-10, maxit=3000, restart=True)
+    assert abs(g.iterations - o.iterations) <= 1
+    assert max_rel(g.x, o.x) <= PARITY_TOL
+
+
+def test_tiny_and_ragged():
+    for n in (1, 2, 3, 31, 33, 513, 4097):
+        Q = synth.random_spd(n, seed=n, density=min(1.0, 4.0 / n)) if n <= 600 else synth.poisson2d(64)
+        if n == 4097:
+            Q = synth.er_laplacian(n, 4 * n, seed=5)
+        bb = np.random.Generator(np.random.PCG64(n)).uniform(-1, 1, Q.n)
+        b = Q.scipy() @ bb
+        g = gpu_solve(Q, b, tol=0.0, maxit=200)
+        o, _ = oracle_matching(Q, b, g, tol=0.0, maxit=200)
+        assert max_rel(g.x, o.x) <= PARITY_TOL, n
+
+
+def test_trivial_cases():
+    p = synth.config_problem(1)
+    g = gpu_solve(p.Q, p.b, x0=p.x_star, tol=1e-10)
+    assert g.status == "converged" and g.iterations == 0
+    np.testing.assert_array_equal(g.x, p.x_star)
+    d = np.array([1.0, 2.0, 4.0, 0.5])
+    Q = synth.diag_matrix(d)
+    b = np.array([3.0, -1.0, 2.0, 7.0])
+    g = gpu_solve(Q, b, tol=1e-15, maxit=5)
+    assert g.status == "converged" and g.iterations == 1
+    np.testing.assert_array_equal(g.x, b / d)
+    g = gpu_solve(p.Q, p.b, tol=0.0, maxit=1)
+    o = oracle.solve(p.Q, p.b, tol=0.0, maxit=1)
+    assert g.iterations == 1 and g.status == "maxiter"
+    assert max_rel(g.x, o.x) <= 1e-15
+
+
+def test_jacobi_and_weighted_jacobi_modes():
+    """momentum off with D = diag(Q) (AJM_D_QDIAG) / diag(Q)/omega (AJM_D_USER) is Jacobi / weighted
+    Jacobi; the oracle with the same D is pinned to the textbook forms."""
+    p = synth.config_problem(2, 0.125)
+    g = gpu_solve(p.Q, p.b, tol=0.0, maxit=200, momentum=False, restart=False, dmode="qdiag")
+    o = oracle.solve(p.Q, p.b, tol=0.0, maxit=200, momentum=False, restart=False, dmode="qdiag")
+    assert max_rel(g.x, o.x) <= 1e-13
+    dw = oracle.diag(p.Q) / 0.8
+    g = gpu_solve(p.Q, p.b, tol=0.0, maxit=200, momentum=False, restart=False, dmode="user", d=dw)
+    o = oracle.solve(p.Q, p.b, D=dw, tol=0.0, maxit=200, momentum=False, restart=False)
+    assert max_rel(g.x, o.x) <= 1e-13
+
+
+def test_divergence_guard():
+    """Weighted Jacobi with omega = 3.8 > 2/lambda_max(D^-1 Q) diverges; both sides stop
+    with Diverged at the same t (R19)."""
+    Q = synth.random_laplacian(40, seed=3)
+    b = Q.scipy() @ np.random.Generator(np.random.PCG64(1)).uniform(-1, 1, 40)
+    dw = oracle.diag(Q) / 3.8
+    g = gpu_solve(Q, b, tol=1e-8, maxit=5000, momentum=False, restart=False, dmode="user", d=dw)
+    o = oracle.solve(Q, b, D=dw, tol=1e-8, maxit=5000, momentum=False, restart=False)
+    assert g.status == o.status == "diverged"
+    assert abs(g.iterations - o.iterations) <= 1
+
+
+def test_create_errors():
+    import paper_2407_03272_b200 as ajm
+    Q = synth.poisson2d(4)
+    b = np.ones(16)
+
+    def create(rp, col, val, bb, **kw):
+        with pytest.raises(ajm.AjmError) as e:
+            ajm.Solver(16, rp, col, val, bb, **kw)
+        return e.value.status_name
+
+    bad = Q.col.copy()
+    bad[1], bad[2] = bad[2], bad[1]
+    assert create(Q.row_ptr, bad, Q.val, b) == "AJM_ERR_CSR_INVALID"
+    bad = Q.col.copy()
+    bad[0] = 99
+    assert create(Q.row_ptr, bad, Q.val, b) == "AJM_ERR_CSR_INVALID"
+    rp = Q.row_ptr.copy()
+    rp[-1] += 1
+    assert create(rp, Q.col, Q.val, b) == "AJM_ERR_CSR_INVALID"
+    v = Q.val.copy()
+    v[3] = np.nan
+    assert create(Q.row_ptr, Q.col, v, b) == "AJM_ERR_NONFINITE"
+    v = Q.val.copy()
+    v[0] = -4.0
+    assert create(Q.row_ptr, Q.col, v, b) == "AJM_ERR_NEGATIVE_DIAG"
+    assert create(Q.row_ptr, Q.col, Q.val, np.zeros(16)) == "AJM_ERR_ZERO_RHS"
+    v = Q.val.copy()
+    v[1] = -0.5
+    assert create(Q.row_ptr, Q.col, v, b, validate_symmetry=True) == "AJM_ERR_NOT_SYMMETRIC"
+    Z = synth.from_dense(np.diag([1.0, 0.0, 2.0]), drop_zeros=False)
+    assert create(Z.row_ptr, Z.col, Z.val, np.ones(3)) == "AJM_ERR_ZERO_DIAG"
+    assert create(Q.row_ptr, Q.col, Q.val, b, dmode="user", d=-np.ones(16)) == "AJM_ERR_ZERO_DIAG"
+    # solve-time argument errors
+    s = ajm.Solver(16, Q.row_ptr, Q.col, Q.val, b)
+    for kw in (dict(tol=-1.0), dict(maxit=0), dict(k0=1), dict(momentum=False, restart=True)):
+        with pytest.raises(ajm.AjmError) as e:
+            s.solve(**kw)
+        assert e.value.status_name == "AJM_ERR_INVALID_ARG"
+    s.close()
