@@ -89,8 +89,8 @@ typedef struct {
 /* Layout / launch facts of a handle (for benchmarks and tests). */
 typedef struct {
     int64_t n, nnz;
-    int64_t units;            /* row units of <= 2048 nonzeros / <= 512 rows (or one long row)  */
-    int64_t long_rows;        /* rows with more than 2048 nonzeros (one CTA each)               */
+    int64_t units;            /* work items: SELL chunks + warp-per-row rows + CTA-per-row rows */
+    int64_t long_rows;        /* rows with more than 8192 nonzeros (one CTA each)               */
     int32_t grid;             /* CTAs of the fused pass kernel (persistent, multiple of #SMs)   */
     int32_t block;            /* threads per CTA                                                */
     int32_t sm_count;

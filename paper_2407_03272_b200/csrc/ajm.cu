@@ -2,9 +2,12 @@
 //
 // create : validate (host row_ptr scan + device column/value kernel, optional symmetry kernel),
 //          D per dmode (eq-J-diag on the device), ||b|| (deterministic two-level
-//          reduction), row units of <= AJM_NNZ_CAP nonzeros / <= AJM_ROW_CAP rows (a longer row is
-//          its own unit), and a persistent grid of (#SMs x resident CTAs/SM) CTAs with contiguous
-//          cost-balanced unit ranges.
+//          reduction), and the row-length-binned layout:
+//            rows <= AJM_SELL_MAX nonzeros -> SELL-32-sigma chunks (sigma = 1 when natural order
+//              pads < 5%, else rows sorted by length inside windows of 4096), thread per row;
+//            rows <= AJM_WARP_MAX -> warp per row;  longer rows -> CTA per row;
+//          on a persistent grid of (#SMs x resident CTAs/SM) CTAs: long rows spread largest-first
+//          onto the least-loaded CTA, then mid rows and chunks in contiguous cost-balanced ranges.
 // solve  : init kernel -> one CUDA-graph launch whose WHILE conditional node re-runs the fused
 //          pass until the last CTA's finalize clears the condition (no host round trip per
 //          iteration) -> copy-out of the answer buffer, histories and the control block.
@@ -14,6 +17,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -25,10 +29,19 @@ namespace {
 
 thread_local std::string g_create_error;
 
-struct DevBuf {
-    void* p = nullptr;
-    size_t bytes = 0;
+typedef void (*PassFn)(AjmPass);
+struct PassVariant {
+    PassFn ident, general;
+    const char* name;
 };
+// SELL batch depth x min resident CTAs per SM (register budget); AJM_KVARIANT selects (tuning)
+const PassVariant kVariants[] = {
+    {ajm_pass_kernel<true, 8, 3>, ajm_pass_kernel<false, 8, 3>, "b8m3"},
+    {ajm_pass_kernel<true, 8, 2>, ajm_pass_kernel<false, 8, 2>, "b8m2"},
+    {ajm_pass_kernel<true, 6, 4>, ajm_pass_kernel<false, 6, 4>, "b6m4"},
+    {ajm_pass_kernel<true, 4, 4>, ajm_pass_kernel<false, 4, 4>, "b4m4"},
+};
+const int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 }  // namespace
 
@@ -37,7 +50,12 @@ struct ajm_ctx {
     int sm_count = 0;
     int ctas_per_sm = 0;
     int64_t n = 0, nnz = 0;
-    int64_t units = 0, long_rows = 0;
+    int64_t units = 0, long_rows = 0, mid_rows_n = 0, nchunks = 0, n_sell = 0;
+    int64_t sell_elems = 0;
+    int sigma = 1;
+    bool ident = true;
+    int variant = 0;
+    PassFn pass = nullptr;
     int grid = 0;
     uint32_t flags = 0;
     // device arrays
@@ -48,9 +66,15 @@ struct ajm_ctx {
     double* D = nullptr;
     double* X[3] = {nullptr, nullptr, nullptr};
     double* Qxp = nullptr;
-    int* unit_row = nullptr;
-    unsigned char* unit_flags = nullptr;
-    int* cta_unit = nullptr;
+    double* sval = nullptr;
+    int* scol = nullptr;
+    long long* chunk_off = nullptr;
+    int* perm = nullptr;
+    int* mid_rows = nullptr;
+    int* long_rows_d = nullptr;
+    int* cta_chunk = nullptr;
+    int* cta_mid = nullptr;
+    int* cta_long = nullptr;
     double* partials = nullptr;
     AjmCtrl* ctrl = nullptr;
     double* hist = nullptr;  // 4 x hist_cap: res, f, d, dabs
@@ -121,7 +145,8 @@ void free_all(ajm_ctx* h) {
     if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
     if (h->graph) cudaGraphDestroy(h->graph);
     void* ptrs[] = {h->rp, h->col, h->val, h->b, h->D, h->X[0], h->X[1], h->X[2], h->Qxp,
-                    h->unit_row, h->unit_flags, h->cta_unit, h->partials, h->ctrl, h->hist,
+                    h->sval, h->scol, h->chunk_off, h->perm, h->mid_rows, h->long_rows_d,
+                    h->cta_chunk, h->cta_mid, h->cta_long, h->partials, h->ctrl, h->hist,
                     h->scratch, h->err};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -141,9 +166,16 @@ AjmPass make_pass(ajm_ctx* h, int use_cond) {
     p.X1 = h->X[1];
     p.X2 = h->X[2];
     p.Qxp = h->Qxp;
-    p.unit_row = h->unit_row;
-    p.unit_flags = h->unit_flags;
-    p.cta_unit = h->cta_unit;
+    p.sval = h->sval;
+    p.scol = h->scol;
+    p.chunk_off = h->chunk_off;
+    p.perm = h->perm;
+    p.mid_rows = h->mid_rows;
+    p.long_rows = h->long_rows_d;
+    p.cta_chunk = h->cta_chunk;
+    p.cta_mid = h->cta_mid;
+    p.cta_long = h->cta_long;
+    p.n_sell = (int)h->n_sell;
     p.partials = h->partials;
     p.ctrl = h->ctrl;
     p.cond = h->cond;
@@ -166,7 +198,7 @@ ajm_status_t build_graph(ajm_ctx* h) {
     AjmPass p = make_pass(h, 1);
     void* args[] = {&p};
     cudaKernelNodeParams kp = {};
-    kp.func = (void*)ajm_pass_kernel;
+    kp.func = (void*)h->pass;
     kp.gridDim = dim3(h->grid);
     kp.blockDim = dim3(AJM_BLOCK);
     kp.sharedMemBytes = 0;
@@ -254,60 +286,122 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(cudaGetDevice(&h->device));
     CC(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
 
-    // ---- row units (host, O(n)) ----
-    std::vector<int> urow;
-    std::vector<unsigned char> uflag;
-    std::vector<double> ucost;
+    // ---- row-length-binned layout (host, O(n log sigma)) ----
+    std::vector<int> perm_h, mid_h, long_h;
+    std::vector<long long> choff;
+    std::vector<double> chcost;
     {
-        int64_t r = 0;
-        while (r < n) {
-            const int64_t len0 = hrp[r + 1] - hrp[r];
-            urow.push_back((int)r);
-            if (len0 > AJM_NNZ_CAP) {
-                uflag.push_back(0);
-                ucost.push_back(12.0 * len0 + 56.0);
-                h->long_rows++;
-                ++r;
-                continue;
+        std::vector<int> short_rows;
+        short_rows.reserve((size_t)n);
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t len = hrp[i + 1] - hrp[i];
+            if (len <= AJM_SELL_MAX) short_rows.push_back((int)i);
+            else if (len <= AJM_WARP_MAX) mid_h.push_back((int)i);
+            else long_h.push_back((int)i);
+        }
+        auto rlen = [&](int r) { return hrp[r + 1] - hrp[r]; };
+        auto padded = [&](const std::vector<int>& order) {
+            int64_t tot = 0;
+            for (size_t c0 = 0; c0 < order.size(); c0 += 32) {
+                int64_t w = 1;
+                for (size_t j = c0; j < std::min(order.size(), c0 + 32); ++j) w = std::max<int64_t>(w, rlen(order[j]));
+                tot += 32 * w;
             }
-            int64_t k = 0, rows = 0;
-            unsigned char fl = 0;
-            while (r < n && rows < AJM_ROW_CAP) {
-                const int64_t len = hrp[r + 1] - hrp[r];
-                if (len > AJM_NNZ_CAP || k + len > AJM_NNZ_CAP) break;
-                if (len > AJM_SEQ_ROW) fl |= 1;
-                k += len;
+            return tot;
+        };
+        int64_t short_nnz = 0;
+        for (int r : short_rows) short_nnz += rlen(r);
+        std::vector<int> order = short_rows;
+        h->sigma = 1;
+        if (!short_rows.empty() && (double)padded(order) > 1.05 * (double)std::max<int64_t>(short_nnz, 1)) {
+            // sort by decreasing length inside windows of 4096 consecutive row indices (stable)
+            h->sigma = 4096;
+            size_t lo = 0;
+            while (lo < order.size()) {
+                const int wbase = order[lo] / h->sigma;
+                size_t hi = lo;
+                while (hi < order.size() && order[hi] / h->sigma == wbase) ++hi;
+                std::stable_sort(order.begin() + lo, order.begin() + hi,
+                                 [&](int x, int y) { return rlen(x) > rlen(y); });
+                lo = hi;
+            }
+        }
+        h->n_sell = (int64_t)order.size();
+        h->nchunks = (h->n_sell + 31) / 32;
+        h->ident = (h->sigma == 1 && mid_h.empty() && long_h.empty());
+        perm_h.assign((size_t)h->nchunks * 32, -1);
+        for (size_t j = 0; j < order.size(); ++j) perm_h[j] = order[j];
+        choff.assign((size_t)h->nchunks + 1, 0);
+        chcost.assign((size_t)h->nchunks, 0.0);
+        for (int64_t c = 0; c < h->nchunks; ++c) {
+            int64_t w = 1, rows = 0;
+            for (int64_t j = c * 32; j < std::min<int64_t>(h->n_sell, c * 32 + 32); ++j) {
+                w = std::max<int64_t>(w, rlen(order[(size_t)j]));
                 ++rows;
-                ++r;
             }
-            uflag.push_back(fl);
-            ucost.push_back(12.0 * k + 56.0 * rows);
+            choff[(size_t)c + 1] = choff[(size_t)c] + 32 * w;
+            chcost[(size_t)c] = 12.0 * 32 * w + 56.0 * rows;
         }
-        urow.push_back((int)n);
+        h->sell_elems = choff.back();
+        if (h->sell_elems >= ((int64_t)1 << 40)) return bail(fail(h, AJM_ERR_UNSUPPORTED, "SELL layout too large"));
+        h->mid_rows_n = (int64_t)mid_h.size();
+        h->long_rows = (int64_t)long_h.size();
+        h->units = h->nchunks + h->mid_rows_n + h->long_rows;
     }
-    h->units = (int64_t)uflag.size();
+    std::vector<int> cta_chunk, cta_mid, cta_long, long_sorted;
     {
+        if (const char* ev = getenv("AJM_KVARIANT")) h->variant = std::max(0, std::min(kNumVariants - 1, atoi(ev)));
+        h->pass = h->ident ? kVariants[h->variant].ident : kVariants[h->variant].general;
         int occ = 0;
-        CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ajm_pass_kernel, AJM_BLOCK, 0));
+        CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->pass, AJM_BLOCK, 0));
         h->ctas_per_sm = std::max(occ, 1);
-        int64_t g = (int64_t)h->sm_count * h->ctas_per_sm;
-        h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(g, h->units));
-    }
-    std::vector<int> cta_unit((size_t)h->grid + 1);
-    {
-        double total = 0.0;
-        for (double c : ucost) total += c;
-        // contiguous split: CTA c gets the units whose cost prefix starts in [c, c+1) * total/grid
-        int64_t u = 0;
-        double pref = 0.0;
-        cta_unit[0] = 0;
-        for (int c = 1; c < h->grid; ++c) {
-            const double target = total * c / h->grid;
-            while (u < h->units && pref + 0.5 * ucost[u] < target) pref += ucost[u++];
-            // keep at least one unit per CTA where possible
-            cta_unit[c] = (int)std::max<int64_t>(u, cta_unit[c - 1]);
+        const int64_t g = (int64_t)h->sm_count * h->ctas_per_sm;
+        // at least ~8 work items per CTA (one per warp) before adding CTAs
+        const int64_t want = std::max<int64_t>(1, (h->nchunks + h->mid_rows_n) / 8 + h->long_rows);
+        h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(g, want));
+        const int G = h->grid;
+        std::vector<double> load((size_t)G, 0.0);
+        // long rows: largest first onto the least-loaded CTA (LPT)
+        std::vector<int> lr = long_h;
+        std::stable_sort(lr.begin(), lr.end(), [&](int x, int y) { return hrp[x + 1] - hrp[x] > hrp[y + 1] - hrp[y]; });
+        std::vector<std::vector<int>> per((size_t)G);
+        for (int r : lr) {
+            size_t best = 0;
+            for (size_t c = 1; c < (size_t)G; ++c)
+                if (load[c] < load[best]) best = c;
+            load[best] += 12.0 * (double)(hrp[r + 1] - hrp[r]) + 56.0;
+            per[best].push_back(r);
         }
-        cta_unit[h->grid] = (int)h->units;
+        cta_long.assign((size_t)G + 1, 0);
+        for (int c = 0; c < G; ++c) {
+            cta_long[(size_t)c + 1] = cta_long[(size_t)c] + (int)per[(size_t)c].size();
+            for (int r : per[(size_t)c]) long_sorted.push_back(r);
+        }
+        // mid rows then chunks as one sequence, contiguous ranges balancing total load
+        const int64_t nm = h->mid_rows_n, nc = h->nchunks, nseq = nm + nc;
+        auto cost = [&](int64_t i) {
+            if (i < nm) { const int r = mid_h[(size_t)i]; return 12.0 * (double)(hrp[r + 1] - hrp[r]) + 56.0 + 256.0; }
+            return chcost[(size_t)(i - nm)];
+        };
+        double total = 0.0;
+        for (double l : load) total += l;
+        for (int64_t i = 0; i < nseq; ++i) total += cost(i);
+        const double target = total / G;
+        std::vector<int64_t> start((size_t)G + 1, nseq);
+        int64_t i = 0;
+        for (int c = 0; c < G; ++c) {
+            start[(size_t)c] = i;
+            double acc = load[(size_t)c];
+            if (c == G - 1) { i = nseq; break; }
+            while (i < nseq && acc + 0.5 * cost(i) < target) acc += cost(i++);
+        }
+        start[(size_t)G] = nseq;
+        cta_mid.assign((size_t)G + 1, 0);
+        cta_chunk.assign((size_t)G + 1, 0);
+        for (int c = 0; c <= G; ++c) {
+            cta_mid[(size_t)c] = (int)std::min(start[(size_t)c], nm);
+            cta_chunk[(size_t)c] = (int)std::max<int64_t>(start[(size_t)c] - nm, 0);
+        }
     }
 
     // ---- device allocations ----
@@ -318,9 +412,15 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(dalloc(&h->D, n));
     for (int k = 0; k < 3; ++k) CC(dalloc(&h->X[k], n));
     CC(dalloc(&h->Qxp, n));
-    CC(dalloc(&h->unit_row, h->units + 1));
-    CC(dalloc(&h->unit_flags, h->units));
-    CC(dalloc(&h->cta_unit, h->grid + 1));
+    CC(dalloc(&h->sval, h->sell_elems));
+    CC(dalloc(&h->scol, h->sell_elems));
+    CC(dalloc(&h->chunk_off, h->nchunks + 1));
+    CC(dalloc(&h->perm, h->nchunks * 32));
+    CC(dalloc(&h->mid_rows, h->mid_rows_n));
+    CC(dalloc(&h->long_rows_d, h->long_rows));
+    CC(dalloc(&h->cta_chunk, h->grid + 1));
+    CC(dalloc(&h->cta_mid, h->grid + 1));
+    CC(dalloc(&h->cta_long, h->grid + 1));
     CC(dalloc(&h->partials, (size_t)h->grid * AJM_NPART));
     CC(dalloc(&h->ctrl, 1));
     CC(dalloc(&h->scratch, 512));
@@ -349,9 +449,16 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         CC(dalloc(&dtmp, n));
         CC(cudaMemcpyAsync(dtmp, d, sizeof(double) * n, kind_to_device(d), st));
     }
-    CC(cudaMemcpyAsync(h->unit_row, urow.data(), sizeof(int) * urow.size(), cudaMemcpyHostToDevice, st));
-    CC(cudaMemcpyAsync(h->unit_flags, uflag.data(), uflag.size(), cudaMemcpyHostToDevice, st));
-    CC(cudaMemcpyAsync(h->cta_unit, cta_unit.data(), sizeof(int) * cta_unit.size(), cudaMemcpyHostToDevice, st));
+    auto h2d = [&](void* dst, const void* src, size_t bytes) {
+        return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st) : cudaSuccess;
+    };
+    CC(h2d(h->chunk_off, choff.data(), sizeof(long long) * choff.size()));
+    CC(h2d(h->perm, perm_h.data(), sizeof(int) * perm_h.size()));
+    CC(h2d(h->mid_rows, mid_h.data(), sizeof(int) * mid_h.size()));
+    CC(h2d(h->long_rows_d, long_sorted.data(), sizeof(int) * long_sorted.size()));
+    CC(h2d(h->cta_chunk, cta_chunk.data(), sizeof(int) * cta_chunk.size()));
+    CC(h2d(h->cta_mid, cta_mid.data(), sizeof(int) * cta_mid.size()));
+    CC(h2d(h->cta_long, cta_long.data(), sizeof(int) * cta_long.size()));
     CC(cudaMemsetAsync(h->err, 0, sizeof(int), st));
 
     // ---- validation + D (device) ----
@@ -374,6 +481,13 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         CC(cudaMemcpyAsync(&herr, h->err, sizeof(int), cudaMemcpyDeviceToHost, st));
         CC(cudaStreamSynchronize(st));
         if (herr & AJM_EB_ASYM) return bail(fail(h, AJM_ERR_NOT_SYMMETRIC, "Q is not symmetric"));
+    }
+    // SELL copy of the short rows
+    if (h->nchunks > 0) {
+        const int ns = (int)(h->nchunks * 32);
+        ajm_sell_fill_kernel<<<(ns + 255) / 256, 256, 0, st>>>(ns, (int)h->n_sell, h->perm, h->ident ? 1 : 0,
+                                                               h->rp, h->col, h->val, h->chunk_off, h->sval, h->scol);
+        CC(cudaGetLastError());
     }
     // ||b||
     ajm_sumsq_partial_kernel<<<256, 256, 0, st>>>(n, h->b, h->scratch);
@@ -445,7 +559,7 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
         int64_t issued = 0;
         for (;;) {
             const int64_t chunk = std::min<int64_t>(64, maxit + 1 - issued);
-            for (int64_t i = 0; i < chunk; ++i) ajm_pass_kernel<<<h->grid, AJM_BLOCK, 0, st>>>(p);
+            for (int64_t i = 0; i < chunk; ++i) h->pass<<<h->grid, AJM_BLOCK, 0, st>>>(p);
             AJM_CUDA(h, cudaGetLastError());
             issued += chunk;
             AJM_CUDA(h, cudaMemcpyAsync(h->h_ctrl, h->ctrl, sizeof(AjmCtrl), cudaMemcpyDeviceToHost, st));

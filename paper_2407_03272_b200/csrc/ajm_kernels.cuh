@@ -22,9 +22,8 @@
 #include <stdint.h>
 
 #define AJM_BLOCK 256
-#define AJM_NNZ_CAP 2048  // nonzeros per row unit (8 per thread)
-#define AJM_ROW_CAP 512   // rows per row unit
-#define AJM_SEQ_ROW 32    // rows up to this length are summed by one thread, longer ones by a warp
+#define AJM_SELL_MAX 64     // rows up to this length go to SELL (thread per row)
+#define AJM_WARP_MAX 8192    // rows up to this length: one warp per row; longer: one CTA per row
 #define AJM_NPART 5       // rr, <x,q>, <b,x>, d, sum|d terms|
 #define AJM_LOG_CAP 64
 
@@ -56,23 +55,33 @@ struct AjmCtrl {
 };
 
 struct AjmPass {
+    // CSR (rows longer than AJM_SELL_MAX: warp- and CTA-per-row work)
     const int* __restrict__ rp;       // int32 row offsets [n+1]
     const int* __restrict__ col;      // int32 [nnz]
     const double* __restrict__ val;   // [nnz]
+    // SELL-32-sigma copy of the short rows (<= AJM_SELL_MAX nonzeros): chunk c holds 32 slots,
+    // element k of slot l at chunk_off[c] + 32 k + l (column-major: a warp's loads are coalesced)
+    const double* __restrict__ sval;
+    const int* __restrict__ scol;
+    const long long* __restrict__ chunk_off; // [nchunks+1]
+    const int* __restrict__ perm;     // slot -> row (-1 for tail slots); unused when identity
+    const int* __restrict__ mid_rows; // warp-per-row list, grouped by CTA
+    const int* __restrict__ long_rows;// CTA-per-row list, grouped by CTA
+    const int* __restrict__ cta_chunk;// [grid+1] chunk range of each CTA
+    const int* __restrict__ cta_mid;  // [grid+1]
+    const int* __restrict__ cta_long; // [grid+1]
     const double* __restrict__ b;     // [n]
     const double* __restrict__ D;     // [n]
     double* X0;
     double* X1;
     double* X2;
     double* Qxp;                      // Q x^{t-1} in, Q x^t out (in place per row)
-    const int* __restrict__ unit_row; // [units+1]
-    const unsigned char* __restrict__ unit_flags; // bit0: has a row longer than AJM_SEQ_ROW
-    const int* __restrict__ cta_unit; // [grid+1]
     double* partials;                 // [grid * AJM_NPART]
     AjmCtrl* ctrl;
     cudaGraphConditionalHandle cond;
     int use_cond;
     int n;
+    int n_sell;                       // slots holding a row
 };
 
 __device__ __forceinline__ double ajm_warp_sum(double v) {
@@ -86,16 +95,11 @@ struct AjmAcc {
     double rr, xq, bx, d, dabs;
 };
 
-// a3-a6 for one row i with q = (Q x~^t)_i
-__device__ __forceinline__ void ajm_row_epilogue(const AjmPass& p, int i, double q, double beta,
-                                                 int restart_t, const double* __restrict__ xc,
-                                                 const double* __restrict__ xp,
-                                                 double* __restrict__ xf, AjmAcc& a) {
-    const double bi = __ldg(p.b + i);
-    const double Di = __ldg(p.D + i);
-    const double xt = __ldg(xc + i);
-    const double xpi = __ldg(xp + i);
-    const double qxp = p.Qxp[i];
+// a3-a6 for one row i with q = (Q x~^t)_i; the five row operands are loaded by the caller
+__device__ __forceinline__ void ajm_row_update(double* __restrict__ Qxp, double* __restrict__ xf,
+                                               int i, double q, double bi, double Di, double xt,
+                                               double xpi, double qxp, double beta, int restart_t,
+                                               AjmAcc& a) {
     const double r = bi - q;
     a.rr += r * r;
     a.xq += xt * q;
@@ -104,7 +108,7 @@ __device__ __forceinline__ void ajm_row_epilogue(const AjmPass& p, int i, double
     if (!restart_t) {
         y = xt + beta * (xt - xpi);
         qy = q + beta * (q - qxp);
-        p.Qxp[i] = q;
+        Qxp[i] = q;
         xnow = xt;
     } else {
         y = xpi;
@@ -116,6 +120,14 @@ __device__ __forceinline__ void ajm_row_epilogue(const AjmPass& p, int i, double
     const double term = (qy - bi) * (xn - xnow);
     a.d += term;
     a.dabs += fabs(term);
+}
+
+__device__ __forceinline__ void ajm_row_epilogue(const AjmPass& p, int i, double q, double beta,
+                                                 int restart_t, const double* __restrict__ xc,
+                                                 const double* __restrict__ xp,
+                                                 double* __restrict__ xf, AjmAcc& a) {
+    ajm_row_update(p.Qxp, xf, i, q, __ldg(p.b + i), __ldg(p.D + i), __ldg(xc + i), __ldg(xp + i),
+                   p.Qxp[i], beta, restart_t, a);
 }
 
 __device__ __forceinline__ double* ajm_sel(const AjmPass& p, int k) {
@@ -211,91 +223,127 @@ __device__ void ajm_finalize_ctrl(const AjmPass& p, const double* tot) {
     if (p.use_cond) cudaGraphSetConditional(p.cond, stop ? 0u : 1u);
 }
 
-// The fused pass.  Persistent: CTA c owns row units [cta_unit[c], cta_unit[c+1]) (nnz-balanced,
-// contiguous, fixed at create time) so the per-CTA partials are run-to-run deterministic.
-__global__ void __launch_bounds__(AJM_BLOCK) ajm_pass_kernel(AjmPass p) {
-    __shared__ double s_prod[AJM_NNZ_CAP];
-    __shared__ double s_qx[AJM_ROW_CAP];
-    __shared__ int s_rp[AJM_ROW_CAP + 1];
+// The fused pass.  Persistent grid (#SMs x resident CTAs); CTA c owns, fixed at create time,
+//   (1) long rows  cta_long[c]..   : the whole CTA per row (strided sums + fixed CTA tree),
+//   (2) mid rows   cta_mid[c]..    : one warp per row (lane-strided sums + xor tree),
+//   (3) SELL chunks cta_chunk[c].. : one warp per chunk, one thread per row, sequential
+//       ascending-column sums (bitwise the oracle's per-row order).
+// Every assignment is static, so per-CTA partials and hence all reductions are deterministic.
+template <bool kIdent, int kBatch, int kMinCtas>
+__global__ void __launch_bounds__(AJM_BLOCK, kMinCtas) ajm_pass_kernel(AjmPass p) {
     __shared__ double s_red[AJM_BLOCK / 32][AJM_NPART];
+    __shared__ double s_w[AJM_BLOCK / 32];
     __shared__ double s_tot[AJM_NPART];
     __shared__ int s_last;
 
     AjmCtrl* c = p.ctrl;
     if (*(volatile int*)&c->done) return;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int restart_t = c->restart_t;
     const double beta = c->beta;
     const double* __restrict__ xc = ajm_sel(p, c->cur);
     const double* __restrict__ xp = ajm_sel(p, c->prev);
     double* __restrict__ xf = ajm_sel(p, c->fre);
-
     AjmAcc acc = {0.0, 0.0, 0.0, 0.0, 0.0};
-    const int ub = p.cta_unit[blockIdx.x], ue = p.cta_unit[blockIdx.x + 1];
-    for (int u = ub; u < ue; ++u) {
-        const int r0 = p.unit_row[u], r1 = p.unit_row[u + 1];
-        const int k0 = p.rp[r0], k1 = p.rp[r1];
-        const int nr = r1 - r0, nk = k1 - k0;
-        if (nk > AJM_NNZ_CAP) {
-            // one long row: strided per-thread sums then a fixed-order CTA tree
-            double s = 0.0;
-            for (int k = k0 + tid; k < k1; k += AJM_BLOCK) s += __ldg(p.val + k) * __ldg(xc + __ldg(p.col + k));
-            s = ajm_warp_sum(s);
-            if ((tid & 31) == 0) s_qx[tid >> 5] = s;
-            __syncthreads();
-            if (tid == 0) {
-                double q = 0.0;
-                for (int w = 0; w < AJM_BLOCK / 32; ++w) q += s_qx[w];
-                ajm_row_epilogue(p, r0, q, beta, restart_t, xc, xp, xf, acc);
-            }
-            __syncthreads();
-            continue;
-        }
-        // phase A: coalesced stream of val/col, gather x~, products to shared memory
+    const int bid = blockIdx.x;
+
+    // (1) long rows: whole CTA
+    for (int li = p.cta_long[bid]; li < p.cta_long[bid + 1]; ++li) {
+        const int row = p.long_rows[li];
+        const int k0 = p.rp[row], k1 = p.rp[row + 1];
+        double s = 0.0;
+        for (int k = k0 + tid; k < k1; k += 4 * AJM_BLOCK) {
+            double v[4], xg[4];
+            int cc[4];
 #pragma unroll
-        for (int j = 0; j < AJM_NNZ_CAP / AJM_BLOCK; ++j) {
-            const int k = tid + j * AJM_BLOCK;
-            if (k < nk) s_prod[k] = __ldg(p.val + k0 + k) * __ldg(xc + __ldg(p.col + k0 + k));
+            for (int j = 0; j < 4; ++j) {
+                const int kk = k + j * AJM_BLOCK;
+                v[j] = 0.0;
+                cc[j] = row;
+                if (kk < k1) { v[j] = __ldcs(p.val + kk); cc[j] = __ldcs(p.col + kk); }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) xg[j] = __ldg(xc + cc[j]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (k + j * AJM_BLOCK < k1) s += v[j] * xg[j];
         }
-        for (int i = tid; i <= nr; i += AJM_BLOCK) s_rp[i] = p.rp[r0 + i] - k0;
+        s = ajm_warp_sum(s);
+        if (lane == 0) s_w[warp] = s;
         __syncthreads();
-        // phase B: rows longer than AJM_SEQ_ROW, one warp each (lane-strided sums + xor tree)
-        if (p.unit_flags[u] & 1) {
-            const int lane = tid & 31, warp = tid >> 5;
-            for (int g = warp * 32; g < nr; g += AJM_BLOCK) {
-                const int i = g + lane;
-                const int len = (i < nr) ? s_rp[i + 1] - s_rp[i] : 0;
-                unsigned m = __ballot_sync(0xffffffffu, len > AJM_SEQ_ROW);
-                while (m) {
-                    const int row = g + __ffs(m) - 1;
-                    m &= m - 1;
-                    const int a = s_rp[row], e = s_rp[row + 1];
-                    double s = 0.0;
-                    for (int k = a + lane; k < e; k += 32) s += s_prod[k];
-                    s = ajm_warp_sum(s);
-                    if (lane == 0) s_qx[row] = s;
-                }
-            }
-            __syncthreads();
-        }
-        // phase C: per-row sums (sequential, ascending column, from 0.0) and the epilogue
-        for (int i = tid; i < nr; i += AJM_BLOCK) {
-            const int a = s_rp[i], e = s_rp[i + 1];
-            double q;
-            if (e - a <= AJM_SEQ_ROW) {
-                q = 0.0;
-                for (int k = a; k < e; ++k) q += s_prod[k];
-            } else {
-                q = s_qx[i];
-            }
-            ajm_row_epilogue(p, r0 + i, q, beta, restart_t, xc, xp, xf, acc);
+        if (tid == 0) {
+            double q = 0.0;
+            for (int w = 0; w < AJM_BLOCK / 32; ++w) q += s_w[w];
+            ajm_row_epilogue(p, row, q, beta, restart_t, xc, xp, xf, acc);
         }
         __syncthreads();
     }
 
+    // (2) mid rows: one warp per row
+    for (int mi = p.cta_mid[bid] + warp; mi < p.cta_mid[bid + 1]; mi += AJM_BLOCK / 32) {
+        const int row = p.mid_rows[mi];
+        const int k0 = p.rp[row], k1 = p.rp[row + 1];
+        double s = 0.0;
+        for (int k = k0 + lane; k < k1; k += 4 * 32) {
+            double v[4], xg[4];
+            int cc[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int kk = k + j * 32;
+                v[j] = 0.0;
+                cc[j] = row;
+                if (kk < k1) { v[j] = __ldcs(p.val + kk); cc[j] = __ldcs(p.col + kk); }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) xg[j] = __ldg(xc + cc[j]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (k + j * 32 < k1) s += v[j] * xg[j];
+        }
+        s = ajm_warp_sum(s);
+        if (lane == 0) ajm_row_epilogue(p, row, s, beta, restart_t, xc, xp, xf, acc);
+    }
+
+    // (3) SELL chunks: one warp per chunk of 32 rows, one thread per row
+    for (int ch = p.cta_chunk[bid] + warp; ch < p.cta_chunk[bid + 1]; ch += AJM_BLOCK / 32) {
+        const long long base = p.chunk_off[ch];
+        const int w = (int)((p.chunk_off[ch + 1] - base) >> 5);
+        const int slot = ch * 32 + lane;
+        const int row = kIdent ? (slot < p.n_sell ? slot : -1) : __ldg(p.perm + slot);
+        double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
+        if (row >= 0) {  // row operands first: independent of the SpMV, so they overlap it
+            bi = __ldcs(p.b + row);
+            Di = __ldcs(p.D + row);
+            xt = __ldg(xc + row);
+            xpi = __ldg(xp + row);
+            qxp = __ldcs(p.Qxp + row);
+        }
+        const double* __restrict__ sv = p.sval + base + lane;
+        const int* __restrict__ sc = p.scol + base + lane;
+        double s = 0.0;
+        for (int k0 = 0; k0 < w; k0 += kBatch) {
+            double v[kBatch], xg[kBatch];
+            int cc[kBatch];
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                if (k0 + j < w) {
+                    v[j] = __ldcs(sv + (size_t)(k0 + j) * 32);
+                    cc[j] = __ldcs(sc + (size_t)(k0 + j) * 32);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j)
+                if (k0 + j < w) xg[j] = __ldg(xc + cc[j]);
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j)
+                if (k0 + j < w) s += v[j] * xg[j];
+        }
+        if (row >= 0) ajm_row_update(p.Qxp, xf, row, s, bi, Di, xt, xpi, qxp, beta, restart_t, acc);
+    }
+
     ajm_block_reduce(acc, s_red);
     if (tid == 0) {
-        double* dst = p.partials + (size_t)blockIdx.x * AJM_NPART;
+        double* dst = p.partials + (size_t)bid * AJM_NPART;
         dst[0] = acc.rr; dst[1] = acc.xq; dst[2] = acc.bx; dst[3] = acc.d; dst[4] = acc.dabs;
         __threadfence();
         const unsigned v = atomicAdd(&c->ticket, 1u);
@@ -320,6 +368,28 @@ __global__ void __launch_bounds__(AJM_BLOCK) ajm_pass_kernel(AjmPass p) {
         s_tot[0] = t.rr; s_tot[1] = t.xq; s_tot[2] = t.bx; s_tot[3] = t.d; s_tot[4] = t.dabs;
         ajm_finalize_ctrl(p, s_tot);
         __threadfence();
+    }
+}
+
+// SELL fill: slot-parallel copy of each short row's entries into its chunk column; padding
+// (k >= row length, and tail slots) is val 0 / col = own row (or 0), appended AFTER the row's
+// entries so the sequential sum order is unchanged.
+__global__ void ajm_sell_fill_kernel(int nslots_padded, int n_sell, const int* __restrict__ perm,
+                                     int ident, const int* __restrict__ rp, const int* __restrict__ col,
+                                     const double* __restrict__ val, const long long* __restrict__ chunk_off,
+                                     double* __restrict__ sval, int* __restrict__ scol) {
+    const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+    if (slot >= nslots_padded) return;
+    const int ch = slot >> 5, lane = slot & 31;
+    const long long base = chunk_off[ch];
+    const int w = (int)((chunk_off[ch + 1] - base) >> 5);
+    const int row = ident ? (slot < n_sell ? slot : -1) : perm[slot];
+    int k0 = 0, len = 0;
+    if (row >= 0) { k0 = rp[row]; len = rp[row + 1] - k0; }
+    for (int k = 0; k < w; ++k) {
+        const long long e = base + (long long)k * 32 + lane;
+        if (k < len) { sval[e] = val[k0 + k]; scol[e] = col[k0 + k]; }
+        else { sval[e] = 0.0; scol[e] = row >= 0 ? row : 0; }
     }
 }
 
