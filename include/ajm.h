@@ -60,8 +60,9 @@ typedef enum {
 
 /* ajm_create flags */
 #define AJM_VALIDATE_SYMMETRY 0x1u /* also check Q_ij == Q_ji bitwise (O(nnz log rowlen) kernel)    */
-#define AJM_LOOP_HOST 0x10u        /* debug: host-driven loop of pass launches instead of the device
-                                      CUDA-graph WHILE loop (same kernels, same results)             */
+#define AJM_LOOP_HOST 0x10u        /* debug: one solver-kernel launch per pass, driven by the host,
+                                      instead of the single persistent launch (same kernel, same
+                                      results bit for bit)                                          */
 
 /* Iteration policy. */
 typedef struct {
@@ -89,16 +90,22 @@ typedef struct {
 /* Layout / launch facts of a handle (for benchmarks and tests). */
 typedef struct {
     int64_t n, nnz;
-    int64_t units;            /* work items: SELL chunks + warp-per-row rows + CTA-per-row rows */
-    int64_t long_rows;        /* rows with more than 8192 nonzeros (one CTA each)               */
-    int32_t grid;             /* CTAs of the fused pass kernel (persistent, multiple of #SMs)   */
+    int64_t units;            /* work items: SELL chunks + warp segments                         */
+    int64_t long_rows;        /* rows split into several warp segments (> 2048 nonzeros)        */
+    int32_t grid;             /* CTAs of the persistent solver kernel (#SMs x resident/SM)      */
     int32_t block;            /* threads per CTA                                                */
     int32_t sm_count;
     int32_t ctas_per_sm;
     double model_bytes_per_iter; /* nnz*12 + 7*n*8 + 4*(n+1)  */
     double last_loop_ms;      /* device time of the last solve's iteration loop (CUDA events)  */
     int64_t last_passes;      /* fused passes run by the last solve (= iterations + 1)        */
-    int64_t last_graph_launches; /* graph launches of the last solve (1 with the WHILE loop)    */
+    int64_t last_launches;    /* solver-kernel launches of the last solve (1: persistent loop) */
+    int64_t sell_rows;        /* rows in the SELL-32-sigma copy (<= 64 nonzeros)               */
+    int64_t seg_rows;         /* rows handled by warp segments                                 */
+    int64_t split_rows;       /* rows spanning several segments (finished by an owner CTA)     */
+    int64_t sell_elems;       /* SELL entries including padding                                */
+    int32_t sigma;            /* SELL sorting window (1 = natural order)                       */
+    int32_t variant;          /* kernel variant (SELL batch x min CTAs/SM)                      */
 } ajm_info_t;
 
 /*
@@ -132,9 +139,10 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
  *                   residual / f of the pre-restart iterate x~^t; t = 0 is x0
  *   restart_iters : host int64[restart_cap] or NULL; iterations t at which a restart executed, in
  *                   order (ell <= log2(t+2) - 1 < 64)
- * The whole iteration loop runs on the device (one CUDA-graph launch with a conditional WHILE
- * node; the restart rule and the stopping test are evaluated on the device; there is no host
- * round trip per iteration).  The handle's previous solve state is overwritten.
+ * The whole iteration loop runs on the device: ONE cooperative launch of a persistent kernel with a
+ * grid barrier per iteration; the restart rule, the alpha/beta schedule and the stopping test are
+ * evaluated on the device; there is no host round trip and no relaunch per iteration.  The
+ * handle's previous solve state is overwritten.
  */
 ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t maxit,
                        ajm_policy_t policy, double* x_out, ajm_result_t* res, double* res_hist,

@@ -58,7 +58,10 @@ class ajm_info_t(ctypes.Structure):
                 ("long_rows", ctypes.c_int64), ("grid", ctypes.c_int32), ("block", ctypes.c_int32),
                 ("sm_count", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32),
                 ("model_bytes_per_iter", ctypes.c_double), ("last_loop_ms", ctypes.c_double),
-                ("last_passes", ctypes.c_int64), ("last_graph_launches", ctypes.c_int64)]
+                ("last_passes", ctypes.c_int64), ("last_launches", ctypes.c_int64),
+                ("sell_rows", ctypes.c_int64), ("seg_rows", ctypes.c_int64),
+                ("split_rows", ctypes.c_int64), ("sell_elems", ctypes.c_int64),
+                ("sigma", ctypes.c_int32), ("variant", ctypes.c_int32)]
 
 
 _lib = None

@@ -5,15 +5,17 @@
 //          reduction), and the row-length-binned layout:
 //            rows <= AJM_SELL_MAX nonzeros -> SELL-32-sigma chunks (sigma = 1 when natural order
 //              pads < 5%, else rows sorted by length inside windows of 4096), thread per row;
-//            rows <= AJM_WARP_MAX -> warp per row;  longer rows -> CTA per row;
-//          on a persistent grid of (#SMs x resident CTAs/SM) CTAs: long rows spread largest-first
-//          onto the least-loaded CTA, then mid rows and chunks in contiguous cost-balanced ranges.
-// solve  : init kernel -> one CUDA-graph launch whose WHILE conditional node re-runs the fused
-//          pass until the last CTA's finalize clears the condition (no host round trip per
-//          iteration) -> copy-out of the answer buffer, histories and the control block.
+//            longer rows -> warp segments of <= AJM_SEG nonzeros (several segments: split row,
+//              finished by an owner CTA);
+//          all work items assigned to the warps of a persistent grid (#SMs x resident CTAs/SM) in
+//          contiguous cost-balanced ranges.
+// solve  : init kernel -> ONE cooperative launch of ajm_solve_kernel that runs every pass of
+//          Alg. 3 with a grid barrier per pass and device-side control (no host round trip, no
+//          relaunch) -> copy-out of the answer buffer, histories and the control block.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -29,17 +31,17 @@ namespace {
 
 thread_local std::string g_create_error;
 
-typedef void (*PassFn)(AjmPass);
-struct PassVariant {
-    PassFn ident, general;
+typedef void (*SolveFn)(AjmPass);
+struct SolveVariant {
+    SolveFn fn;
     const char* name;
 };
 // SELL batch depth x min resident CTAs per SM (register budget); AJM_KVARIANT selects (tuning)
-const PassVariant kVariants[] = {
-    {ajm_pass_kernel<true, 8, 3>, ajm_pass_kernel<false, 8, 3>, "b8m3"},
-    {ajm_pass_kernel<true, 8, 2>, ajm_pass_kernel<false, 8, 2>, "b8m2"},
-    {ajm_pass_kernel<true, 6, 4>, ajm_pass_kernel<false, 6, 4>, "b6m4"},
-    {ajm_pass_kernel<true, 4, 4>, ajm_pass_kernel<false, 4, 4>, "b4m4"},
+const SolveVariant kVariants[] = {
+    {ajm_solve_kernel<8, 2>, "b8m2"},
+    {ajm_solve_kernel<8, 3>, "b8m3"},
+    {ajm_solve_kernel<6, 4>, "b6m4"},
+    {ajm_solve_kernel<4, 4>, "b4m4"},
 };
 const int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -50,12 +52,12 @@ struct ajm_ctx {
     int sm_count = 0;
     int ctas_per_sm = 0;
     int64_t n = 0, nnz = 0;
-    int64_t units = 0, long_rows = 0, mid_rows_n = 0, nchunks = 0, n_sell = 0;
-    int64_t sell_elems = 0;
+    int64_t nchunks = 0, n_sell = 0, sell_elems = 0;
+    int64_t nseg = 0, nsplit = 0, seg_rows = 0, long_rows = 0;
     int sigma = 1;
     bool ident = true;
     int variant = 0;
-    PassFn pass = nullptr;
+    SolveFn fn = nullptr;
     int grid = 0;
     uint32_t flags = 0;
     // device arrays
@@ -70,11 +72,18 @@ struct ajm_ctx {
     int* scol = nullptr;
     long long* chunk_off = nullptr;
     int* perm = nullptr;
-    int* mid_rows = nullptr;
-    int* long_rows_d = nullptr;
-    int* cta_chunk = nullptr;
-    int* cta_mid = nullptr;
-    int* cta_long = nullptr;
+    int* seg_row = nullptr;
+    int* seg_k0 = nullptr;
+    int* seg_k1 = nullptr;
+    int* seg_split = nullptr;
+    double* seg_part = nullptr;
+    int* split_row = nullptr;
+    int* split_seg0 = nullptr;
+    unsigned* split_cnt = nullptr;
+    int* cta_split = nullptr;
+    int* owner_split = nullptr;
+    int* items = nullptr;
+    int* warp_item = nullptr;
     double* partials = nullptr;
     AjmCtrl* ctrl = nullptr;
     double* hist = nullptr;  // 4 x hist_cap: res, f, d, dabs
@@ -83,14 +92,10 @@ struct ajm_ctx {
     int* err = nullptr;
     AjmCtrl* h_ctrl = nullptr;  // pinned
     double nb = 0.0;
-    // graph
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t graph_exec = nullptr;
-    cudaGraphConditionalHandle cond = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double last_loop_ms = 0.0;
     int64_t last_passes = 0;
-    int64_t last_graph_launches = 0;
+    int64_t last_launches = 0;
     int64_t last_iterations = -1;
     std::string err_msg;
 };
@@ -142,12 +147,11 @@ cudaError_t dalloc(T** p, size_t count) {
 }
 
 void free_all(ajm_ctx* h) {
-    if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
-    if (h->graph) cudaGraphDestroy(h->graph);
     void* ptrs[] = {h->rp, h->col, h->val, h->b, h->D, h->X[0], h->X[1], h->X[2], h->Qxp,
-                    h->sval, h->scol, h->chunk_off, h->perm, h->mid_rows, h->long_rows_d,
-                    h->cta_chunk, h->cta_mid, h->cta_long, h->partials, h->ctrl, h->hist,
-                    h->scratch, h->err};
+                    h->sval, h->scol, h->chunk_off, h->perm, h->seg_row, h->seg_k0, h->seg_k1,
+                    h->seg_split, h->seg_part, h->split_row, h->split_seg0, h->split_cnt,
+                    h->cta_split, h->owner_split, h->items, h->warp_item, h->partials, h->ctrl,
+                    h->hist, h->scratch, h->err};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->h_ctrl) cudaFreeHost(h->h_ctrl);
@@ -155,58 +159,40 @@ void free_all(ajm_ctx* h) {
     if (h->ev1) cudaEventDestroy(h->ev1);
 }
 
-AjmPass make_pass(ajm_ctx* h, int use_cond) {
+AjmPass make_pass(ajm_ctx* h, int max_passes) {
     AjmPass p;
     p.rp = h->rp;
     p.col = h->col;
     p.val = h->val;
+    p.sval = h->sval;
+    p.scol = h->scol;
+    p.chunk_off = h->chunk_off;
+    p.perm = h->perm;
+    p.seg_row = h->seg_row;
+    p.seg_k0 = h->seg_k0;
+    p.seg_k1 = h->seg_k1;
+    p.seg_split = h->seg_split;
+    p.seg_part = h->seg_part;
+    p.split_row = h->split_row;
+    p.split_seg0 = h->split_seg0;
+    p.split_cnt = h->split_cnt;
+    p.cta_split = h->cta_split;
+    p.owner_split = h->owner_split;
+    p.items = h->items;
+    p.warp_item = h->warp_item;
     p.b = h->b;
     p.D = h->D;
     p.X0 = h->X[0];
     p.X1 = h->X[1];
     p.X2 = h->X[2];
     p.Qxp = h->Qxp;
-    p.sval = h->sval;
-    p.scol = h->scol;
-    p.chunk_off = h->chunk_off;
-    p.perm = h->perm;
-    p.mid_rows = h->mid_rows;
-    p.long_rows = h->long_rows_d;
-    p.cta_chunk = h->cta_chunk;
-    p.cta_mid = h->cta_mid;
-    p.cta_long = h->cta_long;
-    p.n_sell = (int)h->n_sell;
     p.partials = h->partials;
     p.ctrl = h->ctrl;
-    p.cond = h->cond;
-    p.use_cond = use_cond;
     p.n = (int)h->n;
+    p.n_sell = (int)h->n_sell;
+    p.ident = h->ident ? 1 : 0;
+    p.max_passes = max_passes;
     return p;
-}
-
-ajm_status_t build_graph(ajm_ctx* h) {
-    AJM_CUDA(h, cudaGraphCreate(&h->graph, 0));
-    AJM_CUDA(h, cudaGraphConditionalHandleCreate(&h->cond, h->graph, 1, cudaGraphCondAssignDefault));
-    cudaGraphNodeParams cp = {};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = h->cond;
-    cp.conditional.type = cudaGraphCondTypeWhile;
-    cp.conditional.size = 1;
-    cudaGraphNode_t cnode;
-    AJM_CUDA(h, cudaGraphAddNode(&cnode, h->graph, nullptr, 0, &cp));
-    cudaGraph_t body = cp.conditional.phGraph_out[0];
-    AjmPass p = make_pass(h, 1);
-    void* args[] = {&p};
-    cudaKernelNodeParams kp = {};
-    kp.func = (void*)h->pass;
-    kp.gridDim = dim3(h->grid);
-    kp.blockDim = dim3(AJM_BLOCK);
-    kp.sharedMemBytes = 0;
-    kp.kernelParams = args;
-    cudaGraphNode_t knode;
-    AJM_CUDA(h, cudaGraphAddKernelNode(&knode, body, nullptr, 0, &kp));
-    AJM_CUDA(h, cudaGraphInstantiate(&h->graph_exec, h->graph, 0));
-    return AJM_OK;
 }
 
 ajm_status_t ensure_hist(ajm_ctx* h, int64_t need) {
@@ -245,7 +231,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     if (dmode == AJM_D_USER && !d) return fail(nullptr, AJM_ERR_INVALID_ARG, "AJM_D_USER needs d");
     cudaStream_t st = (cudaStream_t)cuda_stream;
 
-    // host scan of row_ptr (needed anyway for the unit layout)
+    // host scan of row_ptr (needed anyway for the layout)
     std::vector<int64_t> hrp((size_t)n + 1);
     {
         cudaError_t e = cudaMemcpyAsync(hrp.data(), row_ptr, sizeof(int64_t) * (n + 1),
@@ -270,11 +256,6 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         delete h;
         return s;
     };
-#define CK(call)                                         \
-    do {                                                 \
-        ajm_status_t s__ = (call);                       \
-        if (s__ != AJM_OK) return bail(s__);             \
-    } while (0)
 #define CC(call)                                                                                   \
     do {                                                                                           \
         cudaError_t e_ = (call);                                                                   \
@@ -285,21 +266,27 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
 
     CC(cudaGetDevice(&h->device));
     CC(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
+    int coop = 0;
+    CC(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device));
+    if (!coop) return bail(fail(h, AJM_ERR_UNSUPPORTED, "device does not support cooperative launch"));
+    if (const char* ev = getenv("AJM_KVARIANT")) h->variant = std::max(0, std::min(kNumVariants - 1, atoi(ev)));
+    h->fn = kVariants[h->variant].fn;
 
     // ---- row-length-binned layout (host, O(n log sigma)) ----
-    std::vector<int> perm_h, mid_h, long_h;
+    auto rlen = [&](int64_t r) { return hrp[(size_t)r + 1] - hrp[(size_t)r]; };
+    std::vector<int> perm_h, seg_row_h, seg_k0_h, seg_k1_h, seg_split_h, split_row_h, split_seg0_h;
     std::vector<long long> choff;
     std::vector<double> chcost;
     {
-        std::vector<int> short_rows;
+        std::vector<int> short_rows, split_rows, whole_rows;
         short_rows.reserve((size_t)n);
         for (int64_t i = 0; i < n; ++i) {
-            const int64_t len = hrp[i + 1] - hrp[i];
+            const int64_t len = rlen(i);
             if (len <= AJM_SELL_MAX) short_rows.push_back((int)i);
-            else if (len <= AJM_WARP_MAX) mid_h.push_back((int)i);
-            else long_h.push_back((int)i);
+            else if (len <= AJM_SEG) whole_rows.push_back((int)i);
+            else split_rows.push_back((int)i);
         }
-        auto rlen = [&](int r) { return hrp[r + 1] - hrp[r]; };
+        h->long_rows = (int64_t)split_rows.size();
         auto padded = [&](const std::vector<int>& order) {
             int64_t tot = 0;
             for (size_t c0 = 0; c0 < order.size(); c0 += 32) {
@@ -328,7 +315,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         }
         h->n_sell = (int64_t)order.size();
         h->nchunks = (h->n_sell + 31) / 32;
-        h->ident = (h->sigma == 1 && mid_h.empty() && long_h.empty());
+        h->ident = (h->sigma == 1 && split_rows.empty() && whole_rows.empty());
         perm_h.assign((size_t)h->nchunks * 32, -1);
         for (size_t j = 0; j < order.size(); ++j) perm_h[j] = order[j];
         choff.assign((size_t)h->nchunks + 1, 0);
@@ -340,67 +327,82 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
                 ++rows;
             }
             choff[(size_t)c + 1] = choff[(size_t)c] + 32 * w;
-            chcost[(size_t)c] = 12.0 * 32 * w + 56.0 * rows;
+            chcost[(size_t)c] = 12.0 * 32 * w + 56.0 * rows + 64.0;
         }
         h->sell_elems = choff.back();
-        if (h->sell_elems >= ((int64_t)1 << 40)) return bail(fail(h, AJM_ERR_UNSUPPORTED, "SELL layout too large"));
-        h->mid_rows_n = (int64_t)mid_h.size();
-        h->long_rows = (int64_t)long_h.size();
-        h->units = h->nchunks + h->mid_rows_n + h->long_rows;
+        // segments: split rows first (consecutive per row), then whole rows
+        for (int r : split_rows) {
+            const int sidx = (int)split_row_h.size();
+            split_row_h.push_back(r);
+            split_seg0_h.push_back((int)seg_row_h.size());
+            for (int64_t k = hrp[(size_t)r]; k < hrp[(size_t)r + 1]; k += AJM_SEG) {
+                seg_row_h.push_back(r);
+                seg_k0_h.push_back((int)k);
+                seg_k1_h.push_back((int)std::min<int64_t>(k + AJM_SEG, hrp[(size_t)r + 1]));
+                seg_split_h.push_back(sidx);
+            }
+        }
+        split_seg0_h.push_back((int)seg_row_h.size());
+        for (int r : whole_rows) {
+            seg_row_h.push_back(r);
+            seg_k0_h.push_back((int)hrp[(size_t)r]);
+            seg_k1_h.push_back((int)hrp[(size_t)r + 1]);
+            seg_split_h.push_back(-1);
+        }
+        h->nseg = (int64_t)seg_row_h.size();
+        h->nsplit = (int64_t)split_row_h.size();
+        h->seg_rows = (int64_t)(split_rows.size() + whole_rows.size());
     }
-    std::vector<int> cta_chunk, cta_mid, cta_long, long_sorted;
+    // ---- persistent grid and the cost-balanced warp ranges ----
+    std::vector<int> items_h, warp_item_h, cta_split_h, owner_split_h;
     {
-        if (const char* ev = getenv("AJM_KVARIANT")) h->variant = std::max(0, std::min(kNumVariants - 1, atoi(ev)));
-        h->pass = h->ident ? kVariants[h->variant].ident : kVariants[h->variant].general;
         int occ = 0;
-        CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->pass, AJM_BLOCK, 0));
-        h->ctas_per_sm = std::max(occ, 1);
-        const int64_t g = (int64_t)h->sm_count * h->ctas_per_sm;
-        // at least ~8 work items per CTA (one per warp) before adding CTAs
-        const int64_t want = std::max<int64_t>(1, (h->nchunks + h->mid_rows_n) / 8 + h->long_rows);
+        CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->fn, AJM_BLOCK, 0));
+        if (occ < 1) return bail(fail(h, AJM_ERR_CUDA, "solver kernel cannot be resident"));
+        h->ctas_per_sm = occ;
+        const int64_t nitems = h->nseg + h->nchunks;
+        const int64_t g = (int64_t)h->sm_count * occ;
+        const int64_t want = std::max<int64_t>(1, (nitems + AJM_WARPS - 1) / AJM_WARPS);
         h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(g, want));
         const int G = h->grid;
-        std::vector<double> load((size_t)G, 0.0);
-        // long rows: largest first onto the least-loaded CTA (LPT)
-        std::vector<int> lr = long_h;
-        std::stable_sort(lr.begin(), lr.end(), [&](int x, int y) { return hrp[x + 1] - hrp[x] > hrp[y + 1] - hrp[y]; });
-        std::vector<std::vector<int>> per((size_t)G);
-        for (int r : lr) {
-            size_t best = 0;
-            for (size_t c = 1; c < (size_t)G; ++c)
-                if (load[c] < load[best]) best = c;
-            load[best] += 12.0 * (double)(hrp[r + 1] - hrp[r]) + 56.0;
-            per[best].push_back(r);
+        const int64_t W = (int64_t)G * AJM_WARPS;
+        items_h.reserve((size_t)nitems);
+        std::vector<double> cost;
+        cost.reserve((size_t)nitems);
+        for (int64_t s = 0; s < h->nseg; ++s) {
+            items_h.push_back((int)(-1 - s));
+            cost.push_back(12.0 * (seg_k1_h[(size_t)s] - seg_k0_h[(size_t)s]) + 56.0 + 256.0);
         }
-        cta_long.assign((size_t)G + 1, 0);
-        for (int c = 0; c < G; ++c) {
-            cta_long[(size_t)c + 1] = cta_long[(size_t)c] + (int)per[(size_t)c].size();
-            for (int r : per[(size_t)c]) long_sorted.push_back(r);
+        for (int64_t c = 0; c < h->nchunks; ++c) {
+            items_h.push_back((int)c);
+            cost.push_back(chcost[(size_t)c]);
         }
-        // mid rows then chunks as one sequence, contiguous ranges balancing total load
-        const int64_t nm = h->mid_rows_n, nc = h->nchunks, nseq = nm + nc;
-        auto cost = [&](int64_t i) {
-            if (i < nm) { const int r = mid_h[(size_t)i]; return 12.0 * (double)(hrp[r + 1] - hrp[r]) + 56.0 + 256.0; }
-            return chcost[(size_t)(i - nm)];
-        };
         double total = 0.0;
-        for (double l : load) total += l;
-        for (int64_t i = 0; i < nseq; ++i) total += cost(i);
-        const double target = total / G;
-        std::vector<int64_t> start((size_t)G + 1, nseq);
+        for (double x : cost) total += x;
+        const double target = total / (double)W;
+        // warp w takes items while its cumulative prefix stays within (w+1) * target (midpoints)
+        warp_item_h.assign((size_t)W + 1, (int)nitems);
         int64_t i = 0;
-        for (int c = 0; c < G; ++c) {
-            start[(size_t)c] = i;
-            double acc = load[(size_t)c];
-            if (c == G - 1) { i = nseq; break; }
-            while (i < nseq && acc + 0.5 * cost(i) < target) acc += cost(i++);
+        double pref = 0.0;
+        for (int64_t w = 0; w < W; ++w) {
+            warp_item_h[(size_t)w] = (int)i;
+            if (w == W - 1) break;
+            const double lim = target * (double)(w + 1);
+            while (i < nitems && pref + 0.5 * cost[(size_t)i] < lim) pref += cost[(size_t)i++];
         }
-        start[(size_t)G] = nseq;
-        cta_mid.assign((size_t)G + 1, 0);
-        cta_chunk.assign((size_t)G + 1, 0);
-        for (int c = 0; c <= G; ++c) {
-            cta_mid[(size_t)c] = (int)std::min(start[(size_t)c], nm);
-            cta_chunk[(size_t)c] = (int)std::max<int64_t>(start[(size_t)c] - nm, 0);
+        warp_item_h[(size_t)W] = (int)nitems;
+        // owner of a split row = the CTA that runs its last segment
+        std::vector<int> seg_cta((size_t)h->nseg, 0);
+        for (int64_t w = 0; w < W; ++w)
+            for (int k = warp_item_h[(size_t)w]; k < warp_item_h[(size_t)w + 1]; ++k)
+                if (items_h[(size_t)k] < 0) seg_cta[(size_t)(-1 - items_h[(size_t)k])] = (int)(w / AJM_WARPS);
+        std::vector<std::vector<int>> per((size_t)G);
+        for (int64_t sp = 0; sp < h->nsplit; ++sp)
+            per[(size_t)seg_cta[(size_t)split_seg0_h[(size_t)sp + 1] - 1]].push_back((int)sp);
+        cta_split_h.assign((size_t)G + 1, 0);
+        for (int c = 0; c < G; ++c) {
+            cta_split_h[(size_t)c + 1] = cta_split_h[(size_t)c] + (int)per[(size_t)c].size();
+            for (int sp : per[(size_t)c]) owner_split_h.push_back(sp);
         }
     }
 
@@ -416,12 +418,19 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(dalloc(&h->scol, h->sell_elems));
     CC(dalloc(&h->chunk_off, h->nchunks + 1));
     CC(dalloc(&h->perm, h->nchunks * 32));
-    CC(dalloc(&h->mid_rows, h->mid_rows_n));
-    CC(dalloc(&h->long_rows_d, h->long_rows));
-    CC(dalloc(&h->cta_chunk, h->grid + 1));
-    CC(dalloc(&h->cta_mid, h->grid + 1));
-    CC(dalloc(&h->cta_long, h->grid + 1));
-    CC(dalloc(&h->partials, (size_t)h->grid * AJM_NPART));
+    CC(dalloc(&h->seg_row, h->nseg));
+    CC(dalloc(&h->seg_k0, h->nseg));
+    CC(dalloc(&h->seg_k1, h->nseg));
+    CC(dalloc(&h->seg_split, h->nseg));
+    CC(dalloc(&h->seg_part, h->nseg));
+    CC(dalloc(&h->split_row, h->nsplit));
+    CC(dalloc(&h->split_seg0, h->nsplit + 1));
+    CC(dalloc(&h->split_cnt, h->nsplit));
+    CC(dalloc(&h->cta_split, h->grid + 1));
+    CC(dalloc(&h->owner_split, h->nsplit));
+    CC(dalloc(&h->items, items_h.size()));
+    CC(dalloc(&h->warp_item, warp_item_h.size()));
+    CC(dalloc(&h->partials, (size_t)2 * h->grid * AJM_NPART));
     CC(dalloc(&h->ctrl, 1));
     CC(dalloc(&h->scratch, 512));
     CC(dalloc(&h->err, 1));
@@ -454,11 +463,16 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     };
     CC(h2d(h->chunk_off, choff.data(), sizeof(long long) * choff.size()));
     CC(h2d(h->perm, perm_h.data(), sizeof(int) * perm_h.size()));
-    CC(h2d(h->mid_rows, mid_h.data(), sizeof(int) * mid_h.size()));
-    CC(h2d(h->long_rows_d, long_sorted.data(), sizeof(int) * long_sorted.size()));
-    CC(h2d(h->cta_chunk, cta_chunk.data(), sizeof(int) * cta_chunk.size()));
-    CC(h2d(h->cta_mid, cta_mid.data(), sizeof(int) * cta_mid.size()));
-    CC(h2d(h->cta_long, cta_long.data(), sizeof(int) * cta_long.size()));
+    CC(h2d(h->seg_row, seg_row_h.data(), sizeof(int) * seg_row_h.size()));
+    CC(h2d(h->seg_k0, seg_k0_h.data(), sizeof(int) * seg_k0_h.size()));
+    CC(h2d(h->seg_k1, seg_k1_h.data(), sizeof(int) * seg_k1_h.size()));
+    CC(h2d(h->seg_split, seg_split_h.data(), sizeof(int) * seg_split_h.size()));
+    CC(h2d(h->split_row, split_row_h.data(), sizeof(int) * split_row_h.size()));
+    CC(h2d(h->split_seg0, split_seg0_h.data(), sizeof(int) * split_seg0_h.size()));
+    CC(h2d(h->cta_split, cta_split_h.data(), sizeof(int) * cta_split_h.size()));
+    CC(h2d(h->owner_split, owner_split_h.data(), sizeof(int) * owner_split_h.size()));
+    CC(h2d(h->items, items_h.data(), sizeof(int) * items_h.size()));
+    CC(h2d(h->warp_item, warp_item_h.data(), sizeof(int) * warp_item_h.size()));
     CC(cudaMemsetAsync(h->err, 0, sizeof(int), st));
 
     // ---- validation + D (device) ----
@@ -498,9 +512,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(cudaStreamSynchronize(st));
     if (!(bb > 0.0)) return bail(fail(h, AJM_ERR_ZERO_RHS, "||b|| = 0: relative residual undefined"));
     h->nb = std::sqrt(bb);
-    if (!(flags & AJM_LOOP_HOST)) CK(build_graph(h));
     *out = h;
-#undef CK
 #undef CC
     return AJM_OK;
 }
@@ -514,6 +526,7 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
     if (!x_out) return fail(h, AJM_ERR_INVALID_ARG, "x_out is NULL");
     if (!(tol >= 0.0)) return fail(h, AJM_ERR_INVALID_ARG, "tol must be >= 0");
     if (maxit < 1) return fail(h, AJM_ERR_INVALID_ARG, "maxit must be >= 1");
+    if (maxit >= (int64_t)INT32_MAX) return fail(h, AJM_ERR_INVALID_ARG, "maxit must be < 2^31 - 1");
     if (policy.k0 < 2) return fail(h, AJM_ERR_INVALID_ARG, "k0 must be >= 2 (P:460)");
     if (policy.restart && !policy.momentum)
         return fail(h, AJM_ERR_INVALID_ARG, "restart requires momentum (Alg. 2/3)");
@@ -540,6 +553,7 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
         AJM_CUDA(h, cudaMemsetAsync(h->X[1], 0, sizeof(double) * n, st));
     }
     AJM_CUDA(h, cudaMemsetAsync(h->Qxp, 0, sizeof(double) * n, st));
+    if (h->nsplit) AJM_CUDA(h, cudaMemsetAsync(h->split_cnt, 0, sizeof(unsigned) * h->nsplit, st));
     double* hr = h->hist;
     double* hf = h->hist + h->hist_cap;
     double* hd = h->hist + 2 * h->hist_cap;
@@ -550,21 +564,25 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
 
     AJM_CUDA(h, cudaEventRecord(h->ev0, st));
     int64_t launches = 0;
-    if (h->graph_exec) {
-        AJM_CUDA(h, cudaGraphLaunch(h->graph_exec, st));
+    if (!(h->flags & AJM_LOOP_HOST)) {
+        // the whole Alg. 3 loop: one cooperative launch
+        AjmPass p = make_pass(h, (int)(maxit + 1));
+        void* args[] = {&p};
+        AJM_CUDA(h, cudaLaunchCooperativeKernel((const void*)h->fn, dim3(h->grid), dim3(AJM_BLOCK), args, 0, st));
         launches = 1;
     } else {
-        // debug host loop: chunks of passes, each pass exits at once when the control block is done
-        AjmPass p = make_pass(h, 0);
+        // debug host loop: one pass per launch, the control state round-trips through global memory
+        AjmPass p = make_pass(h, 1);
+        void* args[] = {&p};
         int64_t issued = 0;
         for (;;) {
             const int64_t chunk = std::min<int64_t>(64, maxit + 1 - issued);
-            for (int64_t i = 0; i < chunk; ++i) h->pass<<<h->grid, AJM_BLOCK, 0, st>>>(p);
-            AJM_CUDA(h, cudaGetLastError());
+            for (int64_t i = 0; i < chunk; ++i)
+                AJM_CUDA(h, cudaLaunchCooperativeKernel((const void*)h->fn, dim3(h->grid), dim3(AJM_BLOCK), args, 0, st));
             issued += chunk;
             AJM_CUDA(h, cudaMemcpyAsync(h->h_ctrl, h->ctrl, sizeof(AjmCtrl), cudaMemcpyDeviceToHost, st));
             AJM_CUDA(h, cudaStreamSynchronize(st));
-            if (h->h_ctrl->done || issued >= maxit + 1) break;
+            if (h->h_ctrl->s.done || issued >= maxit + 1) break;
         }
         launches = issued;
     }
@@ -572,28 +590,29 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
     AJM_CUDA(h, cudaMemcpyAsync(h->h_ctrl, h->ctrl, sizeof(AjmCtrl), cudaMemcpyDeviceToHost, st));
     AJM_CUDA(h, cudaStreamSynchronize(st));
     const AjmCtrl& c = *h->h_ctrl;
-    if (!c.done) return fail(h, AJM_ERR_CUDA, "iteration loop ended without a termination decision");
+    if (c.timeout_flag) return fail(h, AJM_ERR_CUDA, "device barrier wait timed out (internal error)");
+    if (!c.s.done) return fail(h, AJM_ERR_CUDA, "iteration loop ended without a termination decision");
     float ms = 0.f;
     AJM_CUDA(h, cudaEventElapsedTime(&ms, h->ev0, h->ev1));
     h->last_loop_ms = ms;
-    h->last_passes = c.iterations + 1;
-    h->last_graph_launches = launches;
-    h->last_iterations = c.iterations;
+    h->last_passes = c.s.iterations + 1;
+    h->last_launches = launches;
+    h->last_iterations = c.s.iterations;
 
-    AJM_CUDA(h, cudaMemcpyAsync(x_out, h->X[c.answer], sizeof(double) * n, kind_from_device(x_out), st));
-    const int64_t cnt = c.iterations + 1;
+    AJM_CUDA(h, cudaMemcpyAsync(x_out, h->X[c.s.answer], sizeof(double) * n, kind_from_device(x_out), st));
+    const int64_t cnt = c.s.iterations + 1;
     if (res_hist) AJM_CUDA(h, cudaMemcpyAsync(res_hist, hr, sizeof(double) * cnt, kind_from_device(res_hist), st));
     if (f_hist) AJM_CUDA(h, cudaMemcpyAsync(f_hist, hf, sizeof(double) * cnt, kind_from_device(f_hist), st));
     AJM_CUDA(h, cudaStreamSynchronize(st));
-    const int64_t nlog = std::min<int64_t>(c.nlogged, restart_iters ? restart_cap : 0);
+    const int64_t nlog = std::min<int64_t>(c.s.nlogged, restart_iters ? restart_cap : 0);
     for (int64_t i = 0; i < nlog; ++i) restart_iters[i] = c.restart_log[i];
     if (res) {
-        res->status = c.status;
-        res->n_restarts = c.nres;
-        res->iterations = c.iterations;
-        res->rel_residual = c.res_last;
-        res->f = c.f_last;
-        res->x_is_prerestart = c.prerestart;
+        res->status = c.s.status;
+        res->n_restarts = c.s.nres;
+        res->iterations = c.s.iterations;
+        res->rel_residual = c.s.res_last;
+        res->f = c.s.f_last;
+        res->x_is_prerestart = c.s.prerestart;
         res->restarts_logged = (int32_t)nlog;
     }
     return AJM_OK;
@@ -620,7 +639,7 @@ ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info) {
     if (!h || !info) return fail(h, AJM_ERR_INVALID_ARG, "NULL argument");
     info->n = h->n;
     info->nnz = h->nnz;
-    info->units = h->units;
+    info->units = h->nchunks + h->nseg;
     info->long_rows = h->long_rows;
     info->grid = h->grid;
     info->block = AJM_BLOCK;
@@ -629,7 +648,13 @@ ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info) {
     info->model_bytes_per_iter = 12.0 * (double)h->nnz + 56.0 * (double)h->n + 4.0 * (double)(h->n + 1);
     info->last_loop_ms = h->last_loop_ms;
     info->last_passes = h->last_passes;
-    info->last_graph_launches = h->last_graph_launches;
+    info->last_launches = h->last_launches;
+    info->sell_rows = h->n_sell;
+    info->seg_rows = h->seg_rows;
+    info->split_rows = h->nsplit;
+    info->sigma = h->sigma;
+    info->variant = h->variant;
+    info->sell_elems = h->sell_elems;
     return AJM_OK;
 }
 

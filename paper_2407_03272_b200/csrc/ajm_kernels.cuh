@@ -1,87 +1,114 @@
 // ajm_kernels.cuh -- sm_100a device code of the AJM hot path (arXiv 2407.03272, Alg. 3).
 //
-// One fused pass per iteration:
-//   a2  SpMV  q = Q x~^t                     (Alg. 3 line 4 Q y^t via the identity below)
-//   a3  partials of ||b - q||^2, <x~,q>, <b,x~>  (stopping rule P:505; f, eq-qp P:25-28)
-//   a4  restart branch or Nesterov extrapolation (Alg. 3 lines 6-13):
+// The whole iteration loop of Alg. 3 runs inside ONE persistent cooperative kernel
+// launch (one CTA per resident slot on every SM).  Each pass t:
+//   a2  SpMV  q = Q x~^t, Q streamed from HBM once  (realises Q y^t of Alg. 3 line 4 via the
+//       identity below, and Q x^t of the stopping rule)
+//   a3  partials of ||b - q||^2, <x~,q>, <b,x~>     (stopping rule P:505; f, eq-qp P:25-28)
+//   a4  restart branch or Nesterov extrapolation    (Alg. 3 lines 6-13):
 //         restart_t: y = x^{t-1}, Qy = Q x^{t-1}
 //         else     : y = x~ + beta_t (x~ - x^{t-1}),  Qy = q + beta_t (q - Q x^{t-1}),  Q x^t := q
-//   a5  Jacobi-type step x~^{t+1} = y + (b - Qy) / D   (IEEE division)
-//   a6  partials of d_{t+1} = <Qy - b, x~^{t+1} - x^t> and sum |terms|  (restart test P:465)
-//   a7  last-CTA finalize: fixed-order reduction of the per-CTA partials, residual / f history,
-//       stopping test, restart decision for t+1, alpha/beta schedule, buffer rotation, and the
-//       CUDA-graph WHILE condition.  Deterministic: no floating-point atomics anywhere.
-// Q is streamed from HBM exactly once per iteration; y and Qy are never stored.
+//   a5  Jacobi-type step x~^{t+1} = y + (b - Qy) / D (IEEE division)
+//   a6  partials of d_{t+1} = <Qy - b, x~^{t+1} - x^t> and sum |terms| (restart test P:465)
+//   a7  grid barrier; every CTA reduces all CTA partials in the same fixed order, so every CTA
+//       takes the same (bitwise) decisions: residual / f history, stopping test, restart decision
+//       for t+1, alpha/beta schedule, buffer rotation.  No floating-point atomics anywhere.
+//   a8  loop (no host round trip, no relaunch).
+// y and Qy are never stored.
 //
-// The translation unit is compiled with --fmad=false so that no multiply-add is contracted
-// (R14): the per-row sums of rows with <= 32 nonzeros run sequentially in ascending
-// column order from 0.0 exactly like the oracle's, and the elementwise update rounds like it.
+// Work layout (host-built, static => deterministic): rows <= AJM_SELL_MAX nonzeros live in a
+// SELL-32-sigma copy (warp per 32-row chunk, thread per row, sequential ascending-column sums =
+// the oracle's order); longer rows are cut into segments of <= AJM_SEG nonzeros (warp per
+// segment, lane-strided sums + xor tree).  A row of several segments is finished by a fixed
+// "owner" CTA after its segments' partials arrive (per-row arrival counters; all CTAs are
+// co-resident, so the wait cannot deadlock).  Items are assigned to warps in contiguous,
+// cost-balanced ranges.
+//
+// The translation unit is compiled with --fmad=false so no multiply-add is contracted (DESIGN.md
+// R14): SELL rows are summed exactly like the oracle's rows and the elementwise update rounds like
+// the oracle's mirror mode.
 #pragma once
 
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #define AJM_BLOCK 256
-#define AJM_SELL_MAX 64     // rows up to this length go to SELL (thread per row)
-#define AJM_WARP_MAX 8192    // rows up to this length: one warp per row; longer: one CTA per row
-#define AJM_NPART 5       // rr, <x,q>, <b,x>, d, sum|d terms|
+#define AJM_WARPS (AJM_BLOCK / 32)
+#define AJM_SELL_MAX 64  // rows up to this length go to SELL (thread per row)
+#define AJM_SEG 2048     // max nonzeros per warp segment of a longer row
+#define AJM_NPART 5      // rr, <x,q>, <b,x>, d, sum|d terms|
 #define AJM_LOG_CAP 64
 
-struct AjmCtrl {
+// Iteration state: identical copies in every CTA (shared memory) and in global memory.
+struct AjmState {
     long long t;        // index of the iterate x~^t the current pass multiplies
     long long maxit;
     long long K;        // K_l (prohibition period)
     long long Kre;      // K_re
+    long long iterations;
     double tol;
     double nb;          // ||b||_2
-    double alpha;       // alpha_t of the iteration whose y the current pass forms (see finalize)
+    double alpha;       // alpha of the iteration whose y the current pass forms
     double beta;        // beta_t used by the current pass
+    double res_last, f_last;
     int restart_t;      // restart decision for iteration t (applied by the current pass)
     int cur, prev, fre; // X buffer indices: x~^t, x^{t-1}, free (receives x~^{t+1})
     int momentum, restart_enabled;
     int done, status;
-    long long iterations;
     int answer;         // buffer index holding the answer when done
     int prerestart;
     int nres, nlogged;
-    unsigned int ticket;
-    int pad0;
-    double res_last, f_last;
+};
+
+struct AjmCtrl {
+    AjmState s;
     double* res_hist;
     double* f_hist;
     double* d_hist;
     double* dabs_hist;
+    unsigned int bar_count;        // grid barrier
+    unsigned int bar_gen;
+    unsigned int timeout_flag;     // set if a barrier/arrival wait timed out (never expected)
+    unsigned int pad;
     long long restart_log[AJM_LOG_CAP];
 };
 
 struct AjmPass {
-    // CSR (rows longer than AJM_SELL_MAX: warp- and CTA-per-row work)
-    const int* __restrict__ rp;       // int32 row offsets [n+1]
-    const int* __restrict__ col;      // int32 [nnz]
-    const double* __restrict__ val;   // [nnz]
-    // SELL-32-sigma copy of the short rows (<= AJM_SELL_MAX nonzeros): chunk c holds 32 slots,
-    // element k of slot l at chunk_off[c] + 32 k + l (column-major: a warp's loads are coalesced)
+    // CSR (segment rows)
+    const int* __restrict__ rp;
+    const int* __restrict__ col;
+    const double* __restrict__ val;
+    // SELL-32-sigma of the short rows: chunk c, element k of slot l at chunk_off[c] + 32 k + l
     const double* __restrict__ sval;
     const int* __restrict__ scol;
     const long long* __restrict__ chunk_off; // [nchunks+1]
-    const int* __restrict__ perm;     // slot -> row (-1 for tail slots); unused when identity
-    const int* __restrict__ mid_rows; // warp-per-row list, grouped by CTA
-    const int* __restrict__ long_rows;// CTA-per-row list, grouped by CTA
-    const int* __restrict__ cta_chunk;// [grid+1] chunk range of each CTA
-    const int* __restrict__ cta_mid;  // [grid+1]
-    const int* __restrict__ cta_long; // [grid+1]
-    const double* __restrict__ b;     // [n]
-    const double* __restrict__ D;     // [n]
+    const int* __restrict__ perm;            // slot -> row (-1 for tail slots); unused if identity
+    // segments of the longer rows
+    const int* __restrict__ seg_row;         // [nseg]
+    const int* __restrict__ seg_k0;          // [nseg] first nonzero
+    const int* __restrict__ seg_k1;          // [nseg] one past the last
+    const int* __restrict__ seg_split;       // [nseg] split-row index, or -1 (whole row)
+    double* seg_part;                        // [nseg] segment partial sums
+    const int* __restrict__ split_row;       // [nsplit] row
+    const int* __restrict__ split_seg0;      // [nsplit+1] its segments are split_seg0[i]..
+    unsigned int* split_cnt;                 // [nsplit] monotone arrival counters
+    const int* __restrict__ cta_split;       // [grid+1] split rows owned by each CTA
+    const int* __restrict__ owner_split;     // split-row ids grouped by owner CTA
+    // items: >= 0 SELL chunk id, < 0 segment (-1 - seg id); warp w runs warp_item[w]..[w+1]
+    const int* __restrict__ items;
+    const int* __restrict__ warp_item;       // [grid*AJM_WARPS + 1]
+    const double* __restrict__ b;
+    const double* __restrict__ D;
     double* X0;
     double* X1;
     double* X2;
-    double* Qxp;                      // Q x^{t-1} in, Q x^t out (in place per row)
-    double* partials;                 // [grid * AJM_NPART]
+    double* Qxp;                             // Q x^{t-1} in, Q x^t out (in place per row)
+    double* partials;                        // [2][grid][AJM_NPART], by pass parity
     AjmCtrl* ctrl;
-    cudaGraphConditionalHandle cond;
-    int use_cond;
     int n;
-    int n_sell;                       // slots holding a row
+    int n_sell;
+    int ident;                               // SELL slot == row
+    int max_passes;                          // passes this launch (debug host loop: 1)
 };
 
 __device__ __forceinline__ double ajm_warp_sum(double v) {
@@ -95,7 +122,10 @@ struct AjmAcc {
     double rr, xq, bx, d, dabs;
 };
 
-// a3-a6 for one row i with q = (Q x~^t)_i; the five row operands are loaded by the caller
+// coherent (L1-cached, invalidated by the post-barrier fence) load of data written in-kernel
+__device__ __forceinline__ double ajm_ld(const double* p) { return *p; }
+
+// a3-a6 for one row i with q = (Q x~^t)_i and the five row operands
 __device__ __forceinline__ void ajm_row_update(double* __restrict__ Qxp, double* __restrict__ xf,
                                                int i, double q, double bi, double Di, double xt,
                                                double xpi, double qxp, double beta, int restart_t,
@@ -123,15 +153,20 @@ __device__ __forceinline__ void ajm_row_update(double* __restrict__ Qxp, double*
 }
 
 __device__ __forceinline__ void ajm_row_epilogue(const AjmPass& p, int i, double q, double beta,
-                                                 int restart_t, const double* __restrict__ xc,
-                                                 const double* __restrict__ xp,
-                                                 double* __restrict__ xf, AjmAcc& a) {
-    ajm_row_update(p.Qxp, xf, i, q, __ldg(p.b + i), __ldg(p.D + i), __ldg(xc + i), __ldg(xp + i),
+                                                 int restart_t, const double* xc, const double* xp,
+                                                 double* xf, AjmAcc& a) {
+    ajm_row_update(p.Qxp, xf, i, q, __ldg(p.b + i), __ldg(p.D + i), ajm_ld(xc + i), ajm_ld(xp + i),
                    p.Qxp[i], beta, restart_t, a);
 }
 
 __device__ __forceinline__ double* ajm_sel(const AjmPass& p, int k) {
     return k == 0 ? p.X0 : (k == 1 ? p.X1 : p.X2);
+}
+
+__device__ __forceinline__ unsigned ajm_ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
 }
 
 // Fixed-order CTA reduction of the 5 accumulators; result valid in thread 0.
@@ -140,6 +175,7 @@ __device__ __forceinline__ void ajm_block_reduce(AjmAcc& a, double (*s_red)[AJM_
     double v[AJM_NPART] = {a.rr, a.xq, a.bx, a.d, a.dabs};
 #pragma unroll
     for (int j = 0; j < AJM_NPART; ++j) v[j] = ajm_warp_sum(v[j]);
+    __syncthreads();  // s_red may still be read by a previous reduction
     if (lane == 0) {
 #pragma unroll
         for (int j = 0; j < AJM_NPART; ++j) s_red[warp][j] = v[j];
@@ -147,250 +183,263 @@ __device__ __forceinline__ void ajm_block_reduce(AjmAcc& a, double (*s_red)[AJM_
     __syncthreads();
     if (threadIdx.x == 0) {
         double s[AJM_NPART] = {0, 0, 0, 0, 0};
-        for (int w = 0; w < AJM_BLOCK / 32; ++w)
+        for (int w = 0; w < AJM_WARPS; ++w)
 #pragma unroll
             for (int j = 0; j < AJM_NPART; ++j) s[j] += s_red[w][j];
         a.rr = s[0]; a.xq = s[1]; a.bx = s[2]; a.d = s[3]; a.dabs = s[4];
     }
 }
 
-// a7: executed by thread 0 of the last CTA with the grid-wide sums
-__device__ void ajm_finalize_ctrl(const AjmPass& p, const double* tot) {
-    AjmCtrl* c = p.ctrl;
-    const long long t = c->t;
-    const double res = sqrt(tot[0]) / c->nb;
+// a7 control step (thread 0 of every CTA, identical inputs -> identical outputs).  CTA 0 also
+// writes the histories and the restart log.
+__device__ void ajm_control_step(AjmState& s, const double* tot, AjmCtrl* c, bool writer) {
+    const long long t = s.t;
+    const double res = sqrt(tot[0]) / s.nb;
     const double f = 0.5 * tot[1] - tot[2];
-    c->res_hist[t] = res;
-    c->f_hist[t] = f;
-    c->d_hist[t + 1] = tot[3];
-    c->dabs_hist[t + 1] = tot[4];
-    c->res_last = res;
-    c->f_last = f;
+    if (writer) {
+        c->res_hist[t] = res;
+        c->f_hist[t] = f;
+        c->d_hist[t + 1] = tot[3];
+        c->dabs_hist[t + 1] = tot[4];
+    }
+    s.res_last = res;
+    s.f_last = f;
     int stop = 0;
-    if (res <= c->tol) {  // stopping rule on x~^t before the restart logic (R5)
-        c->status = 0;
-        c->answer = c->cur;
-        c->prerestart = (t >= 1) ? c->restart_t : 0;
+    if (res <= s.tol) {  // stopping rule on x~^t before the restart logic (R5)
+        s.status = 0;
+        s.answer = s.cur;
+        s.prerestart = (t >= 1) ? s.restart_t : 0;
         stop = 1;
     } else if (t >= 1 && !(res <= 1e8)) {  // divergence guard (R19), NaN included
-        c->status = 2;
-        c->answer = c->cur;
+        s.status = 2;
+        s.answer = s.cur;
         stop = 1;
     } else {
-        if (t >= 1 && c->restart_t) {  // the restart decided for t is executed now (counted here)
-            c->nres += 1;
-            if (c->nlogged < AJM_LOG_CAP) c->restart_log[c->nlogged++] = t;
+        if (t >= 1 && s.restart_t) {  // the restart decided for t is executed now (counted here)
+            if (writer && s.nlogged < AJM_LOG_CAP) c->restart_log[s.nlogged] = t;
+            s.nres += 1;
+            if (s.nlogged < AJM_LOG_CAP) s.nlogged += 1;
         }
-        if (t == c->maxit) {  // output the post-iteration x^t (R10)
-            c->status = 1;
-            c->answer = c->restart_t ? c->prev : c->cur;
+        if (t == s.maxit) {  // output the post-iteration x^t (R10)
+            s.status = 1;
+            s.answer = s.restart_t ? s.prev : s.cur;
             stop = 1;
         }
     }
     if (stop) {
-        c->iterations = t;
-        c->done = 1;
-    } else {
-        // restart decision for iteration t+1 (Alg. 3 line 5): d_{t+1} was formed by this pass
-        const long long tn = t + 1;
-        int rs = 0;
-        if (c->restart_enabled && tn > c->Kre + c->K) rs = (tot[3] >= 0.0);  // tie restarts (R7)
-        if (rs) {  // lines 6-10: K_re = t, K_{l+1} = 2 K_l, alpha_{t+1} = 1 (R9)
-            c->Kre = tn;
-            c->K = 2 * c->K;
-            c->alpha = 1.0;
-            c->beta = 0.0;
-        } else {   // lines 12-13: alpha_{t+1} = (1 + sqrt(1 + 4 alpha_t^2))/2, beta_t = (alpha_t - 1)/alpha_{t+1}
-            const double a = c->alpha;
-            const double an = (1.0 + sqrt(1.0 + 4.0 * a * a)) / 2.0;
-            c->beta = c->momentum ? (a - 1.0) / an : 0.0;
-            c->alpha = an;
-        }
-        // rotate: x^t = x~^t unless iteration t restarted (then x^t = x^{t-1})
-        const int cur = c->cur, prev = c->prev, fre = c->fre;
-        if (!c->restart_t) {
-            c->prev = cur;
-            c->cur = fre;
-            c->fre = prev;
-        } else {
-            c->cur = fre;
-            c->fre = cur;
-        }
-        c->restart_t = rs;
-        c->t = tn;
+        s.iterations = t;
+        s.done = 1;
+        return;
     }
-    c->ticket = 0;
-    if (p.use_cond) cudaGraphSetConditional(p.cond, stop ? 0u : 1u);
+    // restart decision for iteration t+1 (Alg. 3 line 5): d_{t+1} was formed by this pass
+    const long long tn = t + 1;
+    int rs = 0;
+    if (s.restart_enabled && tn > s.Kre + s.K) rs = (tot[3] >= 0.0);  // tie restarts (R7)
+    if (rs) {  // lines 6-10: K_re = t, K_{l+1} = 2 K_l, alpha_{t+1} = 1 (R9)
+        s.Kre = tn;
+        s.K = 2 * s.K;
+        s.alpha = 1.0;
+        s.beta = 0.0;
+    } else {   // lines 12-13: alpha_{t+1} = (1 + sqrt(1 + 4 alpha_t^2))/2, beta_t = (alpha_t - 1)/alpha_{t+1}
+        const double a = s.alpha;
+        const double an = (1.0 + sqrt(1.0 + 4.0 * a * a)) / 2.0;
+        s.beta = s.momentum ? (a - 1.0) / an : 0.0;
+        s.alpha = an;
+    }
+    // rotate: x^t = x~^t unless iteration t restarted (then x^t = x^{t-1})
+    const int cur = s.cur, prev = s.prev, fre = s.fre;
+    if (!s.restart_t) {
+        s.prev = cur;
+        s.cur = fre;
+        s.fre = prev;
+    } else {
+        s.cur = fre;
+        s.fre = cur;
+    }
+    s.restart_t = rs;
+    s.t = tn;
 }
 
-// The fused pass.  Persistent grid (#SMs x resident CTAs); CTA c owns, fixed at create time,
-//   (1) long rows  cta_long[c]..   : the whole CTA per row (strided sums + fixed CTA tree),
-//   (2) mid rows   cta_mid[c]..    : one warp per row (lane-strided sums + xor tree),
-//   (3) SELL chunks cta_chunk[c].. : one warp per chunk, one thread per row, sequential
-//       ascending-column sums (bitwise the oracle's per-row order).
-// Every assignment is static, so per-CTA partials and hence all reductions are deterministic.
-template <bool kIdent, int kBatch, int kMinCtas>
-__global__ void __launch_bounds__(AJM_BLOCK, kMinCtas) ajm_pass_kernel(AjmPass p) {
-    __shared__ double s_red[AJM_BLOCK / 32][AJM_NPART];
-    __shared__ double s_w[AJM_BLOCK / 32];
-    __shared__ double s_tot[AJM_NPART];
-    __shared__ int s_last;
-
-    AjmCtrl* c = p.ctrl;
-    if (*(volatile int*)&c->done) return;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int restart_t = c->restart_t;
-    const double beta = c->beta;
-    const double* __restrict__ xc = ajm_sel(p, c->cur);
-    const double* __restrict__ xp = ajm_sel(p, c->prev);
-    double* __restrict__ xf = ajm_sel(p, c->fre);
-    AjmAcc acc = {0.0, 0.0, 0.0, 0.0, 0.0};
-    const int bid = blockIdx.x;
-
-    // (1) long rows: whole CTA
-    for (int li = p.cta_long[bid]; li < p.cta_long[bid + 1]; ++li) {
-        const int row = p.long_rows[li];
-        const int k0 = p.rp[row], k1 = p.rp[row + 1];
-        double s = 0.0;
-        for (int k = k0 + tid; k < k1; k += 4 * AJM_BLOCK) {
-            double v[4], xg[4];
-            int cc[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int kk = k + j * AJM_BLOCK;
-                v[j] = 0.0;
-                cc[j] = row;
-                if (kk < k1) { v[j] = __ldcs(p.val + kk); cc[j] = __ldcs(p.col + kk); }
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) xg[j] = __ldg(xc + cc[j]);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (k + j * AJM_BLOCK < k1) s += v[j] * xg[j];
-        }
-        s = ajm_warp_sum(s);
-        if (lane == 0) s_w[warp] = s;
-        __syncthreads();
-        if (tid == 0) {
-            double q = 0.0;
-            for (int w = 0; w < AJM_BLOCK / 32; ++w) q += s_w[w];
-            ajm_row_epilogue(p, row, q, beta, restart_t, xc, xp, xf, acc);
-        }
-        __syncthreads();
-    }
-
-    // (2) mid rows: one warp per row
-    for (int mi = p.cta_mid[bid] + warp; mi < p.cta_mid[bid + 1]; mi += AJM_BLOCK / 32) {
-        const int row = p.mid_rows[mi];
-        const int k0 = p.rp[row], k1 = p.rp[row + 1];
-        double s = 0.0;
-        for (int k = k0 + lane; k < k1; k += 4 * 32) {
-            double v[4], xg[4];
-            int cc[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int kk = k + j * 32;
-                v[j] = 0.0;
-                cc[j] = row;
-                if (kk < k1) { v[j] = __ldcs(p.val + kk); cc[j] = __ldcs(p.col + kk); }
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) xg[j] = __ldg(xc + cc[j]);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (k + j * 32 < k1) s += v[j] * xg[j];
-        }
-        s = ajm_warp_sum(s);
-        if (lane == 0) ajm_row_epilogue(p, row, s, beta, restart_t, xc, xp, xf, acc);
-    }
-
-    // (3) SELL chunks: one warp per chunk of 32 rows, one thread per row
-    for (int ch = p.cta_chunk[bid] + warp; ch < p.cta_chunk[bid + 1]; ch += AJM_BLOCK / 32) {
-        const long long base = p.chunk_off[ch];
-        const int w = (int)((p.chunk_off[ch + 1] - base) >> 5);
-        const int slot = ch * 32 + lane;
-        const int row = kIdent ? (slot < p.n_sell ? slot : -1) : __ldg(p.perm + slot);
-        double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
-        if (row >= 0) {  // row operands first: independent of the SpMV, so they overlap it
-            bi = __ldcs(p.b + row);
-            Di = __ldcs(p.D + row);
-            xt = __ldg(xc + row);
-            xpi = __ldg(xp + row);
-            qxp = __ldcs(p.Qxp + row);
-        }
-        const double* __restrict__ sv = p.sval + base + lane;
-        const int* __restrict__ sc = p.scol + base + lane;
-        double s = 0.0;
-        for (int k0 = 0; k0 < w; k0 += kBatch) {
-            double v[kBatch], xg[kBatch];
-            int cc[kBatch];
-#pragma unroll
-            for (int j = 0; j < kBatch; ++j) {
-                if (k0 + j < w) {
-                    v[j] = __ldcs(sv + (size_t)(k0 + j) * 32);
-                    cc[j] = __ldcs(sc + (size_t)(k0 + j) * 32);
+// Sense-reversing-free generation barrier over all CTAs of the cooperative launch.  Release:
+// __threadfence before the arrival; acquire: ld.acquire on the generation, then a gpu-scope fence
+// (invalidates this SM's L1 so data written by other SMs this pass is re-read from L2).
+__device__ __forceinline__ void ajm_grid_barrier(AjmCtrl* c, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = ajm_ld_acquire(&c->bar_gen);
+        __threadfence();
+        const unsigned arrived = atomicAdd(&c->bar_count, 1u);
+        if (arrived == nblocks - 1) {
+            atomicExch(&c->bar_count, 0u);
+            __threadfence();
+            atomicAdd(&c->bar_gen, 1u);
+        } else {
+            long long spins = 0;
+            while (ajm_ld_acquire(&c->bar_gen) == g) {
+                __nanosleep(20);
+                if (++spins > (1LL << 28)) {  // ~ seconds: never expected; fail loudly, do not hang
+                    atomicExch(&c->timeout_flag, 1u);
+                    break;
                 }
             }
-#pragma unroll
-            for (int j = 0; j < kBatch; ++j)
-                if (k0 + j < w) xg[j] = __ldg(xc + cc[j]);
-#pragma unroll
-            for (int j = 0; j < kBatch; ++j)
-                if (k0 + j < w) s += v[j] * xg[j];
         }
-        if (row >= 0) ajm_row_update(p.Qxp, xf, row, s, bi, Di, xt, xpi, qxp, beta, restart_t, acc);
-    }
-
-    ajm_block_reduce(acc, s_red);
-    if (tid == 0) {
-        double* dst = p.partials + (size_t)bid * AJM_NPART;
-        dst[0] = acc.rr; dst[1] = acc.xq; dst[2] = acc.bx; dst[3] = acc.d; dst[4] = acc.dabs;
-        __threadfence();
-        const unsigned v = atomicAdd(&c->ticket, 1u);
-        s_last = (v == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    // last CTA: fixed-order reduction over all CTA partials
-    AjmAcc t = {0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int k = tid; k < (int)gridDim.x; k += AJM_BLOCK) {
-        const double* src = p.partials + (size_t)k * AJM_NPART;
-        t.rr += __ldcg(src + 0);
-        t.xq += __ldcg(src + 1);
-        t.bx += __ldcg(src + 2);
-        t.d += __ldcg(src + 3);
-        t.dabs += __ldcg(src + 4);
-    }
-    __syncthreads();
-    ajm_block_reduce(t, s_red);
-    if (tid == 0) {
-        s_tot[0] = t.rr; s_tot[1] = t.xq; s_tot[2] = t.bx; s_tot[3] = t.d; s_tot[4] = t.dabs;
-        ajm_finalize_ctrl(p, s_tot);
         __threadfence();
     }
+    __syncthreads();
 }
 
-// SELL fill: slot-parallel copy of each short row's entries into its chunk column; padding
-// (k >= row length, and tail slots) is val 0 / col = own row (or 0), appended AFTER the row's
-// entries so the sequential sum order is unchanged.
-__global__ void ajm_sell_fill_kernel(int nslots_padded, int n_sell, const int* __restrict__ perm,
-                                     int ident, const int* __restrict__ rp, const int* __restrict__ col,
-                                     const double* __restrict__ val, const long long* __restrict__ chunk_off,
-                                     double* __restrict__ sval, int* __restrict__ scol) {
-    const int slot = blockIdx.x * blockDim.x + threadIdx.x;
-    if (slot >= nslots_padded) return;
-    const int ch = slot >> 5, lane = slot & 31;
-    const long long base = chunk_off[ch];
-    const int w = (int)((chunk_off[ch + 1] - base) >> 5);
-    const int row = ident ? (slot < n_sell ? slot : -1) : perm[slot];
-    int k0 = 0, len = 0;
-    if (row >= 0) { k0 = rp[row]; len = rp[row + 1] - k0; }
-    for (int k = 0; k < w; ++k) {
-        const long long e = base + (long long)k * 32 + lane;
-        if (k < len) { sval[e] = val[k0 + k]; scol[e] = col[k0 + k]; }
-        else { sval[e] = 0.0; scol[e] = row >= 0 ? row : 0; }
+// warp-level dot of a CSR segment [k0, k1) against x (lane-strided, 8 loads in flight per lane)
+__device__ __forceinline__ double ajm_seg_dot(const AjmPass& p, int k0, int k1, const double* xc,
+                                              int lane) {
+    double s = 0.0;
+    for (int k = k0 + lane; k < k1; k += 8 * 32) {
+        double v[8], xg[8];
+        int cc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int kk = k + j * 32;
+            v[j] = 0.0;
+            cc[j] = 0;
+            if (kk < k1) { v[j] = __ldcs(p.val + kk); cc[j] = __ldcs(p.col + kk); }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) xg[j] = ajm_ld(xc + cc[j]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (k + j * 32 < k1) s += v[j] * xg[j];
     }
+    return ajm_warp_sum(s);
+}
+
+template <int kBatch>
+__device__ __forceinline__ void ajm_sell_chunk(const AjmPass& p, int ch, int lane, double beta,
+                                               int restart_t, const double* xc, const double* xp,
+                                               double* xf, AjmAcc& acc) {
+    const long long base = p.chunk_off[ch];
+    const int w = (int)((p.chunk_off[ch + 1] - base) >> 5);
+    const int slot = ch * 32 + lane;
+    const int row = p.ident ? (slot < p.n_sell ? slot : -1) : __ldg(p.perm + slot);
+    double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
+    if (row >= 0) {  // row operands first: independent of the SpMV, so they overlap it
+        bi = __ldcs(p.b + row);
+        Di = __ldcs(p.D + row);
+        xt = ajm_ld(xc + row);
+        xpi = ajm_ld(xp + row);
+        qxp = p.Qxp[row];
+    }
+    const double* __restrict__ sv = p.sval + base + lane;
+    const int* __restrict__ sc = p.scol + base + lane;
+    double s = 0.0;
+    for (int k0 = 0; k0 < w; k0 += kBatch) {
+        double v[kBatch], xg[kBatch];
+        int cc[kBatch];
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            if (k0 + j < w) {
+                v[j] = __ldcs(sv + (size_t)(k0 + j) * 32);
+                cc[j] = __ldcs(sc + (size_t)(k0 + j) * 32);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j)
+            if (k0 + j < w) xg[j] = ajm_ld(xc + cc[j]);
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j)
+            if (k0 + j < w) s += v[j] * xg[j];
+    }
+    if (row >= 0) ajm_row_update(p.Qxp, xf, row, s, bi, Di, xt, xpi, qxp, beta, restart_t, acc);
+}
+
+// The persistent solver kernel (cooperative launch; grid = resident CTAs).
+template <int kBatch, int kMinCtas>
+__global__ void __launch_bounds__(AJM_BLOCK, kMinCtas) ajm_solve_kernel(AjmPass p) {
+    __shared__ double s_red[AJM_WARPS][AJM_NPART];
+    __shared__ double s_tot[AJM_NPART];
+    __shared__ AjmState s_st;
+
+    AjmCtrl* c = p.ctrl;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, bid = blockIdx.x;
+    const unsigned G = gridDim.x;
+    if (tid == 0) s_st = c->s;
+    __syncthreads();
+    const int gw = bid * AJM_WARPS + warp;
+    const int it0 = p.warp_item[gw], it1 = p.warp_item[gw + 1];
+    const int sp0 = p.cta_split[bid], sp1 = p.cta_split[bid + 1];
+
+    for (int pass = 0; pass < p.max_passes; ++pass) {
+        if (s_st.done) break;
+        const long long t = s_st.t;
+        const int restart_t = s_st.restart_t;
+        const double beta = s_st.beta;
+        const double* xc = ajm_sel(p, s_st.cur);
+        const double* xp = ajm_sel(p, s_st.prev);
+        double* xf = ajm_sel(p, s_st.fre);
+        AjmAcc acc = {0.0, 0.0, 0.0, 0.0, 0.0};
+
+        // (1) this warp's items: SELL chunks and row segments
+        for (int it = it0; it < it1; ++it) {
+            const int item = __ldg(p.items + it);
+            if (item >= 0) {
+                ajm_sell_chunk<kBatch>(p, item, lane, beta, restart_t, xc, xp, xf, acc);
+            } else {
+                const int sg = -1 - item;
+                const int row = __ldg(p.seg_row + sg);
+                const double s = ajm_seg_dot(p, __ldg(p.seg_k0 + sg), __ldg(p.seg_k1 + sg), xc, lane);
+                const int sidx = __ldg(p.seg_split + sg);
+                if (lane == 0) {
+                    if (sidx < 0) {
+                        ajm_row_epilogue(p, row, s, beta, restart_t, xc, xp, xf, acc);
+                    } else {
+                        __stcg(p.seg_part + sg, s);
+                        __threadfence();
+                        atomicAdd(p.split_cnt + sidx, 1u);
+                    }
+                }
+            }
+        }
+        // (2) split rows owned by this CTA: wait for all segments of this pass, sum in order
+        for (int k = sp0 + warp; k < sp1; k += AJM_WARPS) {
+            const int sidx = __ldg(p.owner_split + k);
+            const int g0 = __ldg(p.split_seg0 + sidx), g1 = __ldg(p.split_seg0 + sidx + 1);
+            if (lane == 0) {
+                const unsigned target = (unsigned)(g1 - g0) * (unsigned)(t + 1);
+                long long spins = 0;
+                while (ajm_ld_acquire(p.split_cnt + sidx) < target) {
+                    __nanosleep(32);
+                    if (++spins > (1LL << 28)) { atomicExch(&c->timeout_flag, 1u); break; }
+                }
+                __threadfence();
+                double q = 0.0;
+                for (int g = g0; g < g1; ++g) q += __ldcg(p.seg_part + g);
+                ajm_row_epilogue(p, __ldg(p.split_row + sidx), q, beta, restart_t, xc, xp, xf, acc);
+            }
+        }
+        // (3) CTA partial -> grid barrier -> every CTA reduces all partials in the same order
+        ajm_block_reduce(acc, s_red);
+        double* part = p.partials + (size_t)(t & 1) * G * AJM_NPART;
+        if (tid == 0) {
+            double* dst = part + (size_t)bid * AJM_NPART;
+            dst[0] = acc.rr; dst[1] = acc.xq; dst[2] = acc.bx; dst[3] = acc.d; dst[4] = acc.dabs;
+        }
+        ajm_grid_barrier(c, G);
+        AjmAcc tt = {0.0, 0.0, 0.0, 0.0, 0.0};
+        for (int k = tid; k < (int)G; k += AJM_BLOCK) {
+            const double* src = part + (size_t)k * AJM_NPART;
+            tt.rr += __ldcg(src + 0);
+            tt.xq += __ldcg(src + 1);
+            tt.bx += __ldcg(src + 2);
+            tt.d += __ldcg(src + 3);
+            tt.dabs += __ldcg(src + 4);
+        }
+        ajm_block_reduce(tt, s_red);
+        if (tid == 0) {
+            s_tot[0] = tt.rr; s_tot[1] = tt.xq; s_tot[2] = tt.bx; s_tot[3] = tt.d; s_tot[4] = tt.dabs;
+            ajm_control_step(s_st, s_tot, c, bid == 0);
+            if (ajm_ld_acquire(&c->timeout_flag)) s_st.done = 1;
+        }
+        __syncthreads();
+    }
+    if (bid == 0 && tid == 0) c->s = s_st;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -493,40 +542,66 @@ __global__ void ajm_sum_final_kernel(int m, const double* __restrict__ part, dou
     }
 }
 
+
+// SELL fill: slot-parallel copy of each short row's entries into its chunk column; padding
+// (k >= row length, and tail slots) is val 0 / col = own row (or 0), appended AFTER the row's
+// entries so the sequential sum order is unchanged.
+__global__ void ajm_sell_fill_kernel(int nslots_padded, int n_sell, const int* __restrict__ perm,
+                                     int ident, const int* __restrict__ rp, const int* __restrict__ col,
+                                     const double* __restrict__ val, const long long* __restrict__ chunk_off,
+                                     double* __restrict__ sval, int* __restrict__ scol) {
+    const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+    if (slot >= nslots_padded) return;
+    const int ch = slot >> 5, lane = slot & 31;
+    const long long base = chunk_off[ch];
+    const int w = (int)((chunk_off[ch + 1] - base) >> 5);
+    const int row = ident ? (slot < n_sell ? slot : -1) : perm[slot];
+    int k0 = 0, len = 0;
+    if (row >= 0) { k0 = rp[row]; len = rp[row + 1] - k0; }
+    for (int k = 0; k < w; ++k) {
+        const long long e = base + (long long)k * 32 + lane;
+        if (k < len) { sval[e] = val[k0 + k]; scol[e] = col[k0 + k]; }
+        else { sval[e] = 0.0; scol[e] = row >= 0 ? row : 0; }
+    }
+}
+
 // Per-solve initialisation of the control block (t = 0: x~^0 = x0, x^{-1} := x0, beta_0 = 0,
 // alpha_1 = 1, K = K_0, K_re = 0, ell = 0).
 __global__ void ajm_init_ctrl_kernel(AjmCtrl* c, double tol, long long maxit, int momentum,
                                      int restart, long long k0, double nb, double* res_hist,
                                      double* f_hist, double* d_hist, double* dabs_hist) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    c->t = 0;
-    c->maxit = maxit;
-    c->K = k0;
-    c->Kre = 0;
-    c->tol = tol;
-    c->nb = nb;
-    c->alpha = 1.0;
-    c->beta = 0.0;
-    c->restart_t = 0;
-    c->cur = 0;
-    c->prev = 1;
-    c->fre = 2;
-    c->momentum = momentum;
-    c->restart_enabled = restart;
-    c->done = 0;
-    c->status = 1;
-    c->iterations = 0;
-    c->answer = 0;
-    c->prerestart = 0;
-    c->nres = 0;
-    c->nlogged = 0;
-    c->ticket = 0;
-    c->res_last = 0.0;
-    c->f_last = 0.0;
+    AjmState& s = c->s;
+    s.t = 0;
+    s.maxit = maxit;
+    s.K = k0;
+    s.Kre = 0;
+    s.iterations = 0;
+    s.tol = tol;
+    s.nb = nb;
+    s.alpha = 1.0;
+    s.beta = 0.0;
+    s.res_last = 0.0;
+    s.f_last = 0.0;
+    s.restart_t = 0;
+    s.cur = 0;
+    s.prev = 1;
+    s.fre = 2;
+    s.momentum = momentum;
+    s.restart_enabled = restart;
+    s.done = 0;
+    s.status = 1;
+    s.answer = 0;
+    s.prerestart = 0;
+    s.nres = 0;
+    s.nlogged = 0;
     c->res_hist = res_hist;
     c->f_hist = f_hist;
     c->d_hist = d_hist;
     c->dabs_hist = dabs_hist;
+    c->bar_count = 0;
+    c->bar_gen = 0;
+    c->timeout_flag = 0;
     d_hist[0] = 0.0;
     dabs_hist[0] = 0.0;
 }

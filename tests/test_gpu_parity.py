@@ -72,7 +72,7 @@ def test_determinism_and_loop_modes():
         np.testing.assert_array_equal(a.x, o.x)
         np.testing.assert_array_equal(a.res_hist, o.res_hist)
         np.testing.assert_array_equal(a.f_hist, o.f_hist)
-    assert a.info["last_graph_launches"] == 1 and a.info["last_passes"] == 301
+    assert a.info["last_launches"] == 1 and a.info["last_passes"] == 301
 
 
 # ------------------------------------------------------------------------------------------------
@@ -81,12 +81,13 @@ def test_determinism_and_loop_modes():
 
 @pytest.mark.parametrize("n", [40, 600, 3000])
 def test_long_rows_sdd(n):
-    """§4.1 matrix: rows of length n exercise the warp-per-row (33..2048) and the
-    CTA-per-row (> 2048) reductions."""
+    """§4.1 matrix: rows of length n exercise the SELL path (n <= 64), the single warp
+    segment (65..2048) and the split rows finished by an owner CTA (> 2048).  tol 1e-8 stays above
+    the rounding floor of these dense rows."""
     Q = synth.sdd(n)
     b = np.ones(n)
-    g = gpu_solve(Q, b, tol=1e-10, maxit=3000, restart=True)
-    o, _ = oracle_matching(Q, b, g, tol=1e-10, maxit=3000, restart=True)
+    g = gpu_solve(Q, b, tol=1e-8, maxit=3000, restart=True)
+    o, _ = oracle_matching(Q, b, g, tol=1e-8, maxit=3000, restart=True)
     assert abs(g.iterations - o.iterations) <= 1
     assert max_rel(g.x, o.x) <= PARITY_TOL
 
