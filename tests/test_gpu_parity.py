@@ -153,7 +153,7 @@ def test_create_errors():
 
     def create(rp, col, val, bb, **kw):
         with pytest.raises(ajm.AjmError) as e:
-            ajm.Solver(16, rp, col, val, bb, **kw)
+            ajm.Solver(len(rp) - 1, rp, col, val, bb, **kw)
         return e.value.status_name
 
     bad = Q.col.copy()
