@@ -7,8 +7,9 @@
 //              pads < 5%, else rows sorted by length inside windows of 4096), thread per row;
 //            longer rows -> warp segments of <= AJM_SEG nonzeros (several segments: split row,
 //              finished by an owner CTA);
-//          all work items assigned to the warps of a persistent grid (#SMs x resident CTAs/SM) in
-//          contiguous cost-balanced ranges.
+//          SELL chunks grouped into TMA staging units (<= 8 chunks, <= AJM_UNIT_EL elements);
+//          segments and units assigned to the CTAs of a persistent grid (#SMs x resident
+//          CTAs/SM) in contiguous cost-balanced ranges.
 // solve  : init kernel -> ONE cooperative launch of ajm_solve_kernel that runs every pass of
 //          Alg. 3 with a grid barrier per pass and device-side control (no host round trip, no
 //          relaunch) -> copy-out of the answer buffer, histories and the control block.
@@ -34,14 +35,16 @@ thread_local std::string g_create_error;
 typedef void (*SolveFn)(AjmPass);
 struct SolveVariant {
     SolveFn fn;
+    int stages;
     const char* name;
 };
-// SELL batch depth x min resident CTAs per SM (register budget); AJM_KVARIANT selects (tuning)
+// TMA ring depth x min resident CTAs per SM (shared memory / register budget); AJM_KVARIANT
+// selects one (tuning); the default is the measured best on B200
 const SolveVariant kVariants[] = {
-    {ajm_solve_kernel<8, 2>, "b8m2"},
-    {ajm_solve_kernel<8, 3>, "b8m3"},
-    {ajm_solve_kernel<6, 4>, "b6m4"},
-    {ajm_solve_kernel<4, 4>, "b4m4"},
+    {ajm_solve_kernel<4, 2>, 4, "s4m2"},
+    {ajm_solve_kernel<3, 3>, 3, "s3m3"},
+    {ajm_solve_kernel<2, 4>, 2, "s2m4"},
+    {ajm_solve_kernel<6, 1>, 6, "s6m1"},
 };
 const int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -58,6 +61,8 @@ struct ajm_ctx {
     bool ident = true;
     int variant = 0;
     SolveFn fn = nullptr;
+    size_t dyn_smem = 0;
+    int64_t nunits = 0;
     int grid = 0;
     uint32_t flags = 0;
     // device arrays
@@ -82,8 +87,9 @@ struct ajm_ctx {
     unsigned* split_cnt = nullptr;
     int* cta_split = nullptr;
     int* owner_split = nullptr;
-    int* items = nullptr;
-    int* warp_item = nullptr;
+    int* unit_c0 = nullptr;
+    int* cta_seg = nullptr;
+    int* cta_unit = nullptr;
     double* partials = nullptr;
     AjmCtrl* ctrl = nullptr;
     double* hist = nullptr;  // 4 x hist_cap: res, f, d, dabs
@@ -150,7 +156,7 @@ void free_all(ajm_ctx* h) {
     void* ptrs[] = {h->rp, h->col, h->val, h->b, h->D, h->X[0], h->X[1], h->X[2], h->Qxp,
                     h->sval, h->scol, h->chunk_off, h->perm, h->seg_row, h->seg_k0, h->seg_k1,
                     h->seg_split, h->seg_part, h->split_row, h->split_seg0, h->split_cnt,
-                    h->cta_split, h->owner_split, h->items, h->warp_item, h->partials, h->ctrl,
+                    h->cta_split, h->owner_split, h->unit_c0, h->cta_seg, h->cta_unit, h->partials, h->ctrl,
                     h->hist, h->scratch, h->err};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -178,8 +184,9 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.split_cnt = h->split_cnt;
     p.cta_split = h->cta_split;
     p.owner_split = h->owner_split;
-    p.items = h->items;
-    p.warp_item = h->warp_item;
+    p.unit_c0 = h->unit_c0;
+    p.cta_seg = h->cta_seg;
+    p.cta_unit = h->cta_unit;
     p.b = h->b;
     p.D = h->D;
     p.X0 = h->X[0];
@@ -271,6 +278,8 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     if (!coop) return bail(fail(h, AJM_ERR_UNSUPPORTED, "device does not support cooperative launch"));
     if (const char* ev = getenv("AJM_KVARIANT")) h->variant = std::max(0, std::min(kNumVariants - 1, atoi(ev)));
     h->fn = kVariants[h->variant].fn;
+    h->dyn_smem = (size_t)kVariants[h->variant].stages * AJM_UNIT_EL * (sizeof(double) + sizeof(int));
+    CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem));
 
     // ---- row-length-binned layout (host, O(n log sigma)) ----
     auto rlen = [&](int64_t r) { return hrp[(size_t)r + 1] - hrp[(size_t)r]; };
@@ -353,56 +362,70 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         h->nsplit = (int64_t)split_row_h.size();
         h->seg_rows = (int64_t)(split_rows.size() + whole_rows.size());
     }
-    // ---- persistent grid and the cost-balanced warp ranges ----
-    std::vector<int> items_h, warp_item_h, cta_split_h, owner_split_h;
+    // ---- TMA staging units, persistent grid, cost-balanced CTA ranges ----
+    std::vector<int> unit_c0_h, cta_seg_h, cta_unit_h, cta_split_h, owner_split_h;
     {
+        // units: consecutive chunks, <= AJM_WARPS chunks and <= AJM_UNIT_EL elements each
+        std::vector<double> ucost;
+        int64_t c = 0;
+        while (c < h->nchunks) {
+            unit_c0_h.push_back((int)c);
+            double cost = 0.0;
+            int64_t k = 0;
+            while (c < h->nchunks && k < AJM_WARPS &&
+                   choff[(size_t)c + 1] - choff[(size_t)unit_c0_h.back()] <= AJM_UNIT_EL) {
+                cost += chcost[(size_t)c];
+                ++c;
+                ++k;
+            }
+            ucost.push_back(cost);
+        }
+        unit_c0_h.push_back((int)h->nchunks);
+        h->nunits = (int64_t)ucost.size();
         int occ = 0;
-        CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->fn, AJM_BLOCK, 0));
+        CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->fn, AJM_BLOCK + 32, h->dyn_smem));
         if (occ < 1) return bail(fail(h, AJM_ERR_CUDA, "solver kernel cannot be resident"));
         h->ctas_per_sm = occ;
-        const int64_t nitems = h->nseg + h->nchunks;
+        const int64_t nitems = h->nseg + h->nunits;
         const int64_t g = (int64_t)h->sm_count * occ;
-        const int64_t want = std::max<int64_t>(1, (nitems + AJM_WARPS - 1) / AJM_WARPS);
-        h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(g, want));
+        h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(g, nitems));
         const int G = h->grid;
-        const int64_t W = (int64_t)G * AJM_WARPS;
-        items_h.reserve((size_t)nitems);
+        // one sequence: segments (split rows first), then units; contiguous CTA ranges by cost
         std::vector<double> cost;
         cost.reserve((size_t)nitems);
-        for (int64_t s = 0; s < h->nseg; ++s) {
-            items_h.push_back((int)(-1 - s));
-            cost.push_back(12.0 * (seg_k1_h[(size_t)s] - seg_k0_h[(size_t)s]) + 56.0 + 256.0);
-        }
-        for (int64_t c = 0; c < h->nchunks; ++c) {
-            items_h.push_back((int)c);
-            cost.push_back(chcost[(size_t)c]);
-        }
+        for (int64_t s2 = 0; s2 < h->nseg; ++s2)
+            cost.push_back(12.0 * (seg_k1_h[(size_t)s2] - seg_k0_h[(size_t)s2]) + 56.0 + 256.0);
+        for (double x : ucost) cost.push_back(x);
         double total = 0.0;
         for (double x : cost) total += x;
-        const double target = total / (double)W;
-        // warp w takes items while its cumulative prefix stays within (w+1) * target (midpoints)
-        warp_item_h.assign((size_t)W + 1, (int)nitems);
+        const double target = total / (double)G;
+        std::vector<int64_t> start((size_t)G + 1, nitems);
         int64_t i = 0;
         double pref = 0.0;
-        for (int64_t w = 0; w < W; ++w) {
-            warp_item_h[(size_t)w] = (int)i;
-            if (w == W - 1) break;
-            const double lim = target * (double)(w + 1);
+        for (int cc = 0; cc < G; ++cc) {
+            start[(size_t)cc] = i;
+            if (cc == G - 1) break;
+            const double lim = target * (double)(cc + 1);
             while (i < nitems && pref + 0.5 * cost[(size_t)i] < lim) pref += cost[(size_t)i++];
         }
-        warp_item_h[(size_t)W] = (int)nitems;
+        start[(size_t)G] = nitems;
+        cta_seg_h.assign((size_t)G + 1, 0);
+        cta_unit_h.assign((size_t)G + 1, 0);
+        for (int cc = 0; cc <= G; ++cc) {
+            cta_seg_h[(size_t)cc] = (int)std::min<int64_t>(start[(size_t)cc], h->nseg);
+            cta_unit_h[(size_t)cc] = (int)std::max<int64_t>(start[(size_t)cc] - h->nseg, 0);
+        }
         // owner of a split row = the CTA that runs its last segment
         std::vector<int> seg_cta((size_t)h->nseg, 0);
-        for (int64_t w = 0; w < W; ++w)
-            for (int k = warp_item_h[(size_t)w]; k < warp_item_h[(size_t)w + 1]; ++k)
-                if (items_h[(size_t)k] < 0) seg_cta[(size_t)(-1 - items_h[(size_t)k])] = (int)(w / AJM_WARPS);
+        for (int cc = 0; cc < G; ++cc)
+            for (int k2 = cta_seg_h[(size_t)cc]; k2 < cta_seg_h[(size_t)cc + 1]; ++k2) seg_cta[(size_t)k2] = cc;
         std::vector<std::vector<int>> per((size_t)G);
         for (int64_t sp = 0; sp < h->nsplit; ++sp)
             per[(size_t)seg_cta[(size_t)split_seg0_h[(size_t)sp + 1] - 1]].push_back((int)sp);
         cta_split_h.assign((size_t)G + 1, 0);
-        for (int c = 0; c < G; ++c) {
-            cta_split_h[(size_t)c + 1] = cta_split_h[(size_t)c] + (int)per[(size_t)c].size();
-            for (int sp : per[(size_t)c]) owner_split_h.push_back(sp);
+        for (int cc = 0; cc < G; ++cc) {
+            cta_split_h[(size_t)cc + 1] = cta_split_h[(size_t)cc] + (int)per[(size_t)cc].size();
+            for (int sp : per[(size_t)cc]) owner_split_h.push_back(sp);
         }
     }
 
@@ -428,8 +451,9 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(dalloc(&h->split_cnt, h->nsplit));
     CC(dalloc(&h->cta_split, h->grid + 1));
     CC(dalloc(&h->owner_split, h->nsplit));
-    CC(dalloc(&h->items, items_h.size()));
-    CC(dalloc(&h->warp_item, warp_item_h.size()));
+    CC(dalloc(&h->unit_c0, unit_c0_h.size()));
+    CC(dalloc(&h->cta_seg, cta_seg_h.size()));
+    CC(dalloc(&h->cta_unit, cta_unit_h.size()));
     CC(dalloc(&h->partials, (size_t)2 * h->grid * AJM_NPART));
     CC(dalloc(&h->ctrl, 1));
     CC(dalloc(&h->scratch, 512));
@@ -471,8 +495,9 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(h2d(h->split_seg0, split_seg0_h.data(), sizeof(int) * split_seg0_h.size()));
     CC(h2d(h->cta_split, cta_split_h.data(), sizeof(int) * cta_split_h.size()));
     CC(h2d(h->owner_split, owner_split_h.data(), sizeof(int) * owner_split_h.size()));
-    CC(h2d(h->items, items_h.data(), sizeof(int) * items_h.size()));
-    CC(h2d(h->warp_item, warp_item_h.data(), sizeof(int) * warp_item_h.size()));
+    CC(h2d(h->unit_c0, unit_c0_h.data(), sizeof(int) * unit_c0_h.size()));
+    CC(h2d(h->cta_seg, cta_seg_h.data(), sizeof(int) * cta_seg_h.size()));
+    CC(h2d(h->cta_unit, cta_unit_h.data(), sizeof(int) * cta_unit_h.size()));
     CC(cudaMemsetAsync(h->err, 0, sizeof(int), st));
 
     // ---- validation + D (device) ----
@@ -568,7 +593,7 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
         // the whole Alg. 3 loop: one cooperative launch
         AjmPass p = make_pass(h, (int)(maxit + 1));
         void* args[] = {&p};
-        AJM_CUDA(h, cudaLaunchCooperativeKernel((const void*)h->fn, dim3(h->grid), dim3(AJM_BLOCK), args, 0, st));
+        AJM_CUDA(h, cudaLaunchCooperativeKernel((const void*)h->fn, dim3(h->grid), dim3(AJM_BLOCK + 32), args, h->dyn_smem, st));
         launches = 1;
     } else {
         // debug host loop: one pass per launch, the control state round-trips through global memory
@@ -578,7 +603,7 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
         for (;;) {
             const int64_t chunk = std::min<int64_t>(64, maxit + 1 - issued);
             for (int64_t i = 0; i < chunk; ++i)
-                AJM_CUDA(h, cudaLaunchCooperativeKernel((const void*)h->fn, dim3(h->grid), dim3(AJM_BLOCK), args, 0, st));
+                AJM_CUDA(h, cudaLaunchCooperativeKernel((const void*)h->fn, dim3(h->grid), dim3(AJM_BLOCK + 32), args, h->dyn_smem, st));
             issued += chunk;
             AJM_CUDA(h, cudaMemcpyAsync(h->h_ctrl, h->ctrl, sizeof(AjmCtrl), cudaMemcpyDeviceToHost, st));
             AJM_CUDA(h, cudaStreamSynchronize(st));
@@ -639,7 +664,7 @@ ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info) {
     if (!h || !info) return fail(h, AJM_ERR_INVALID_ARG, "NULL argument");
     info->n = h->n;
     info->nnz = h->nnz;
-    info->units = h->nchunks + h->nseg;
+    info->units = h->nunits + h->nseg;
     info->long_rows = h->long_rows;
     info->grid = h->grid;
     info->block = AJM_BLOCK;

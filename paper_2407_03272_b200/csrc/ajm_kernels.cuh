@@ -37,6 +37,7 @@
 #define AJM_SELL_MAX 64  // rows up to this length go to SELL (thread per row)
 #define AJM_SEG 2048     // max nonzeros per warp segment of a longer row
 #define AJM_NPART 5      // rr, <x,q>, <b,x>, d, sum|d terms|
+#define AJM_UNIT_EL 2048 // SELL elements per TMA staging unit (24 KB of val + col)
 #define AJM_LOG_CAP 64
 
 // Iteration state: identical copies in every CTA (shared memory) and in global memory.
@@ -83,6 +84,7 @@ struct AjmPass {
     const int* __restrict__ scol;
     const long long* __restrict__ chunk_off; // [nchunks+1]
     const int* __restrict__ perm;            // slot -> row (-1 for tail slots); unused if identity
+    const int* __restrict__ unit_c0;         // [nunits+1] TMA staging units: chunks unit_c0[u]..
     // segments of the longer rows
     const int* __restrict__ seg_row;         // [nseg]
     const int* __restrict__ seg_k0;          // [nseg] first nonzero
@@ -94,9 +96,8 @@ struct AjmPass {
     unsigned int* split_cnt;                 // [nsplit] monotone arrival counters
     const int* __restrict__ cta_split;       // [grid+1] split rows owned by each CTA
     const int* __restrict__ owner_split;     // split-row ids grouped by owner CTA
-    // items: >= 0 SELL chunk id, < 0 segment (-1 - seg id); warp w runs warp_item[w]..[w+1]
-    const int* __restrict__ items;
-    const int* __restrict__ warp_item;       // [grid*AJM_WARPS + 1]
+    const int* __restrict__ cta_seg;         // [grid+1] segment range of each CTA
+    const int* __restrict__ cta_unit;        // [grid+1] unit range of each CTA
     const double* __restrict__ b;
     const double* __restrict__ D;
     double* X0;
@@ -169,18 +170,21 @@ __device__ __forceinline__ unsigned ajm_ld_acquire(const unsigned* p) {
     return v;
 }
 
-// Fixed-order CTA reduction of the 5 accumulators; result valid in thread 0.
+// barrier among the AJM_BLOCK consumer threads only (the TMA producer warp never joins)
+__device__ __forceinline__ void ajm_csync() { asm volatile("bar.sync 1, %0;" ::"n"(AJM_BLOCK) : "memory"); }
+
+// Fixed-order CTA reduction of the 5 accumulators over the consumer warps; valid in thread 0.
 __device__ __forceinline__ void ajm_block_reduce(AjmAcc& a, double (*s_red)[AJM_NPART]) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double v[AJM_NPART] = {a.rr, a.xq, a.bx, a.d, a.dabs};
 #pragma unroll
     for (int j = 0; j < AJM_NPART; ++j) v[j] = ajm_warp_sum(v[j]);
-    __syncthreads();  // s_red may still be read by a previous reduction
+    ajm_csync();  // s_red may still be read by a previous reduction
     if (lane == 0) {
 #pragma unroll
         for (int j = 0; j < AJM_NPART; ++j) s_red[warp][j] = v[j];
     }
-    __syncthreads();
+    ajm_csync();
     if (threadIdx.x == 0) {
         double s[AJM_NPART] = {0, 0, 0, 0, 0};
         for (int w = 0; w < AJM_WARPS; ++w)
@@ -264,7 +268,7 @@ __device__ void ajm_control_step(AjmState& s, const double* tot, AjmCtrl* c, boo
 // __threadfence before the arrival; acquire: ld.acquire on the generation, then a gpu-scope fence
 // (invalidates this SM's L1 so data written by other SMs this pass is re-read from L2).
 __device__ __forceinline__ void ajm_grid_barrier(AjmCtrl* c, unsigned nblocks) {
-    __syncthreads();
+    ajm_csync();
     if (threadIdx.x == 0) {
         const unsigned g = ajm_ld_acquire(&c->bar_gen);
         __threadfence();
@@ -285,7 +289,7 @@ __device__ __forceinline__ void ajm_grid_barrier(AjmCtrl* c, unsigned nblocks) {
         }
         __threadfence();
     }
-    __syncthreads();
+    ajm_csync();
 }
 
 // warp-level dot of a CSR segment [k0, k1) against x (lane-strided, 8 loads in flight per lane)
@@ -311,61 +315,134 @@ __device__ __forceinline__ double ajm_seg_dot(const AjmPass& p, int k0, int k1, 
     return ajm_warp_sum(s);
 }
 
-template <int kBatch>
-__device__ __forceinline__ void ajm_sell_chunk(const AjmPass& p, int ch, int lane, double beta,
-                                               int restart_t, const double* xc, const double* xp,
-                                               double* xf, AjmAcc& acc) {
-    const long long base = p.chunk_off[ch];
-    const int w = (int)((p.chunk_off[ch + 1] - base) >> 5);
-    const int slot = ch * 32 + lane;
-    const int row = p.ident ? (slot < p.n_sell ? slot : -1) : __ldg(p.perm + slot);
-    double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
-    if (row >= 0) {  // row operands first: independent of the SpMV, so they overlap it
-        bi = __ldcs(p.b + row);
-        Di = __ldcs(p.D + row);
-        xt = ajm_ld(xc + row);
-        xpi = ajm_ld(xp + row);
-        qxp = p.Qxp[row];
-    }
-    const double* __restrict__ sv = p.sval + base + lane;
-    const int* __restrict__ sc = p.scol + base + lane;
-    double s = 0.0;
-    for (int k0 = 0; k0 < w; k0 += kBatch) {
-        double v[kBatch], xg[kBatch];
-        int cc[kBatch];
-#pragma unroll
-        for (int j = 0; j < kBatch; ++j) {
-            if (k0 + j < w) {
-                v[j] = __ldcs(sv + (size_t)(k0 + j) * 32);
-                cc[j] = __ldcs(sc + (size_t)(k0 + j) * 32);
-            }
+// ---- mbarrier / bulk-copy (TMA engine) helpers --------------------------------------------------
+__device__ __forceinline__ uint32_t ajm_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void ajm_mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(ajm_smem(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void ajm_mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ajm_smem(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void ajm_mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ajm_smem(bar)) : "memory");
+}
+__device__ __forceinline__ bool ajm_mbar_try_wait(uint64_t* bar, unsigned parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok) : "r"(ajm_smem(bar)), "r"(parity) : "memory");
+    return ok != 0;
+}
+// bounded wait: a lost arrival must never hang the GPU; on timeout the flag aborts the solve
+__device__ __forceinline__ void ajm_mbar_wait(uint64_t* bar, unsigned parity, unsigned* timeout_flag) {
+    long long spins = 0;
+    while (!ajm_mbar_try_wait(bar, parity)) {
+        if (++spins > (1LL << 26)) {
+            atomicExch(timeout_flag, 1u);
+            return;
         }
-#pragma unroll
-        for (int j = 0; j < kBatch; ++j)
-            if (k0 + j < w) xg[j] = ajm_ld(xc + cc[j]);
-#pragma unroll
-        for (int j = 0; j < kBatch; ++j)
-            if (k0 + j < w) s += v[j] * xg[j];
     }
-    if (row >= 0) ajm_row_update(p.Qxp, xf, row, s, bi, Di, xt, xpi, qxp, beta, restart_t, acc);
+}
+// 1-D bulk copy global -> shared (cp.async.bulk, completes tx bytes on the mbarrier)
+__device__ __forceinline__ void ajm_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(ajm_smem(dst)),
+        "l"(src), "r"(bytes), "r"(ajm_smem(bar))
+        : "memory");
 }
 
-// The persistent solver kernel (cooperative launch; grid = resident CTAs).
-template <int kBatch, int kMinCtas>
-__global__ void __launch_bounds__(AJM_BLOCK, kMinCtas) ajm_solve_kernel(AjmPass p) {
+// One SELL chunk (32 rows, thread per row) whose val/col sit in shared memory (sv/sc already
+// offset to this chunk and lane; element k at [32 k]).  Row operands are loaded before the wait on
+// the stage's full barrier by the caller.
+__device__ __forceinline__ double ajm_chunk_dot(const double* sv, const int* sc, int w, const double* xc) {
+    double s = 0.0;
+    for (int k0 = 0; k0 < w; k0 += 8) {
+        double xg[8];
+        int cc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) cc[j] = (k0 + j < w) ? sc[(k0 + j) * 32] : 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (k0 + j < w) xg[j] = ajm_ld(xc + cc[j]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (k0 + j < w) s += sv[(k0 + j) * 32] * xg[j];  // ascending column order
+    }
+    return s;
+}
+
+// The persistent solver kernel (cooperative launch; grid = resident CTAs).  AJM_BLOCK consumer
+// threads + one producer warp that streams this CTA's SELL units (val and col of <= 8 chunks,
+// <= AJM_UNIT_EL elements) into a kStages-deep shared-memory ring with cp.async.bulk.  Q does not
+// change between passes, so the producer runs ahead across pass boundaries (it keeps the ring
+// full while the consumers sit in the grid barrier).
+template <int kStages, int kMinCtas>
+__global__ void __launch_bounds__(AJM_BLOCK + 32, kMinCtas) ajm_solve_kernel(AjmPass p) {
+    extern __shared__ __align__(128) unsigned char s_dyn[];
     __shared__ double s_red[AJM_WARPS][AJM_NPART];
     __shared__ double s_tot[AJM_NPART];
     __shared__ AjmState s_st;
+    __shared__ __align__(8) uint64_t s_full[kStages];
+    __shared__ __align__(8) uint64_t s_empty[kStages];
+    __shared__ volatile int s_stop;
+    __shared__ long long s_consumed;
 
     AjmCtrl* c = p.ctrl;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, bid = blockIdx.x;
     const unsigned G = gridDim.x;
-    if (tid == 0) s_st = c->s;
+    const int u0 = p.cta_unit[bid], u1 = p.cta_unit[bid + 1];
+    const int nunits = u1 - u0;
+    double* s_val = reinterpret_cast<double*>(s_dyn);
+    int* s_col = reinterpret_cast<int*>(s_dyn + (size_t)kStages * AJM_UNIT_EL * sizeof(double));
+    if (tid == 0) {
+        s_st = c->s;
+        s_stop = 0;
+        s_consumed = 0;
+        for (int k = 0; k < kStages; ++k) {
+            ajm_mbar_init(&s_full[k], 1);
+            ajm_mbar_init(&s_empty[k], AJM_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
-    const int gw = bid * AJM_WARPS + warp;
-    const int it0 = p.warp_item[gw], it1 = p.warp_item[gw + 1];
-    const int sp0 = p.cta_split[bid], sp1 = p.cta_split[bid + 1];
 
+    if (warp == AJM_WARPS) {
+        // ---------------- producer warp ----------------
+        if (lane == 0 && nunits > 0) {
+            long long cnt = 0;
+            const long long total = (long long)nunits * p.max_passes;
+            for (; cnt < total; ++cnt) {
+                const int stage = (int)(cnt % kStages);
+                const unsigned par = (unsigned)((cnt / kStages) & 1) ^ 1u;
+                bool stop = false;
+                long long spins = 0;
+                while (!ajm_mbar_try_wait(&s_empty[stage], par)) {
+                    if (s_stop) { stop = true; break; }
+                    if (++spins > (1LL << 26)) { atomicExch(&c->timeout_flag, 1u); stop = true; break; }
+                }
+                if (stop || s_stop) break;
+                const int u = u0 + (int)(cnt % nunits);
+                const long long e0 = p.chunk_off[p.unit_c0[u]], e1 = p.chunk_off[p.unit_c0[u + 1]];
+                const unsigned ne = (unsigned)(e1 - e0);
+                ajm_mbar_expect_tx(&s_full[stage], ne * 12u);
+                ajm_bulk_g2s(s_val + (size_t)stage * AJM_UNIT_EL, p.sval + e0, ne * 8u, &s_full[stage]);
+                ajm_bulk_g2s(s_col + (size_t)stage * AJM_UNIT_EL, p.scol + e0, ne * 4u, &s_full[stage]);
+            }
+            // drain: every issued copy must land before the CTA exits
+            long long spins = 0;
+            while (!s_stop) {
+                if (++spins > (1LL << 32)) break;
+            }
+            for (long long k = s_consumed; k < cnt; ++k)
+                ajm_mbar_wait(&s_full[k % kStages], (unsigned)((k / kStages) & 1), &c->timeout_flag);
+        }
+        return;
+    }
+
+    // ---------------- consumer warps ----------------
+    const int sg0 = p.cta_seg[bid], sg1 = p.cta_seg[bid + 1];
+    const int sp0 = p.cta_split[bid], sp1 = p.cta_split[bid + 1];
+    long long ucnt = 0;  // units consumed by this CTA (all passes)
     for (int pass = 0; pass < p.max_passes; ++pass) {
         if (s_st.done) break;
         const long long t = s_st.t;
@@ -376,28 +453,62 @@ __global__ void __launch_bounds__(AJM_BLOCK, kMinCtas) ajm_solve_kernel(AjmPass 
         double* xf = ajm_sel(p, s_st.fre);
         AjmAcc acc = {0.0, 0.0, 0.0, 0.0, 0.0};
 
-        // (1) this warp's items: SELL chunks and row segments
-        for (int it = it0; it < it1; ++it) {
-            const int item = __ldg(p.items + it);
-            if (item >= 0) {
-                ajm_sell_chunk<kBatch>(p, item, lane, beta, restart_t, xc, xp, xf, acc);
-            } else {
-                const int sg = -1 - item;
-                const int row = __ldg(p.seg_row + sg);
-                const double s = ajm_seg_dot(p, __ldg(p.seg_k0 + sg), __ldg(p.seg_k1 + sg), xc, lane);
-                const int sidx = __ldg(p.seg_split + sg);
-                if (lane == 0) {
-                    if (sidx < 0) {
-                        ajm_row_epilogue(p, row, s, beta, restart_t, xc, xp, xf, acc);
-                    } else {
-                        __stcg(p.seg_part + sg, s);
-                        __threadfence();
-                        atomicAdd(p.split_cnt + sidx, 1u);
-                    }
+        // (1) row segments (direct loads), split-row segments first
+        for (int sg = sg0 + warp; sg < sg1; sg += AJM_WARPS) {
+            const int row = __ldg(p.seg_row + sg);
+            const double s = ajm_seg_dot(p, __ldg(p.seg_k0 + sg), __ldg(p.seg_k1 + sg), xc, lane);
+            const int sidx = __ldg(p.seg_split + sg);
+            if (lane == 0) {
+                if (sidx < 0) {
+                    ajm_row_epilogue(p, row, s, beta, restart_t, xc, xp, xf, acc);
+                } else {
+                    __stcg(p.seg_part + sg, s);
+                    __threadfence();
+                    atomicAdd(p.split_cnt + sidx, 1u);
                 }
             }
         }
-        // (2) split rows owned by this CTA: wait for all segments of this pass, sum in order
+        // (2) SELL units from the shared-memory ring; chunk j of the CTA -> warp j % AJM_WARPS
+        {
+            int jc = warp;  // my next chunk, counted from the CTA's first chunk
+            const int cbase = nunits > 0 ? p.unit_c0[u0] : 0;
+            for (int uu = 0; uu < nunits; ++uu, ++ucnt) {
+                const int u = u0 + uu;
+                const int ca = p.unit_c0[u] - cbase, cb = p.unit_c0[u + 1] - cbase;
+                const int stage = (int)(ucnt % kStages);
+                const unsigned par = (unsigned)((ucnt / kStages) & 1);
+                const long long ebase = p.chunk_off[p.unit_c0[u]];
+                bool waited = false;
+                while (jc < cb) {
+                    const int ch = cbase + jc;
+                    const long long e0 = p.chunk_off[ch];
+                    const int w = (int)((p.chunk_off[ch + 1] - e0) >> 5);
+                    const int slot = ch * 32 + lane;
+                    const int row = p.ident ? (slot < p.n_sell ? slot : -1) : __ldg(p.perm + slot);
+                    double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
+                    if (row >= 0) {  // row operands first: independent of the stage data
+                        bi = __ldcs(p.b + row);
+                        Di = __ldcs(p.D + row);
+                        xt = ajm_ld(xc + row);
+                        xpi = ajm_ld(xp + row);
+                        qxp = p.Qxp[row];
+                    }
+                    if (!waited) {
+                        ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);
+                        waited = true;
+                    }
+                    const size_t off = (size_t)stage * AJM_UNIT_EL + (size_t)(e0 - ebase) + lane;
+                    const double q = ajm_chunk_dot(s_val + off, s_col + off, w, xc);
+                    if (row >= 0) ajm_row_update(p.Qxp, xf, row, q, bi, Di, xt, xpi, qxp, beta, restart_t, acc);
+                    jc += AJM_WARPS;
+                }
+                (void)ca;
+                if (!waited) ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);  // keep the phases in step
+                __syncwarp();
+                if (lane == 0) ajm_mbar_arrive(&s_empty[stage]);
+            }
+        }
+        // (3) split rows owned by this CTA: wait for all segments of this pass, sum in order
         for (int k = sp0 + warp; k < sp1; k += AJM_WARPS) {
             const int sidx = __ldg(p.owner_split + k);
             const int g0 = __ldg(p.split_seg0 + sidx), g1 = __ldg(p.split_seg0 + sidx + 1);
@@ -414,7 +525,7 @@ __global__ void __launch_bounds__(AJM_BLOCK, kMinCtas) ajm_solve_kernel(AjmPass 
                 ajm_row_epilogue(p, __ldg(p.split_row + sidx), q, beta, restart_t, xc, xp, xf, acc);
             }
         }
-        // (3) CTA partial -> grid barrier -> every CTA reduces all partials in the same order
+        // (4) CTA partial -> grid barrier -> every CTA reduces all partials in the same order
         ajm_block_reduce(acc, s_red);
         double* part = p.partials + (size_t)(t & 1) * G * AJM_NPART;
         if (tid == 0) {
@@ -436,10 +547,16 @@ __global__ void __launch_bounds__(AJM_BLOCK, kMinCtas) ajm_solve_kernel(AjmPass 
             s_tot[0] = tt.rr; s_tot[1] = tt.xq; s_tot[2] = tt.bx; s_tot[3] = tt.d; s_tot[4] = tt.dabs;
             ajm_control_step(s_st, s_tot, c, bid == 0);
             if (ajm_ld_acquire(&c->timeout_flag)) s_st.done = 1;
+            s_consumed = ucnt;
         }
-        __syncthreads();
+        ajm_csync();
     }
-    if (bid == 0 && tid == 0) c->s = s_st;
+    if (tid == 0) {
+        s_consumed = ucnt;
+        __threadfence_block();
+        s_stop = 1;
+        if (bid == 0) c->s = s_st;
+    }
 }
 
 // ------------------------------------------------------------------------------------------------
