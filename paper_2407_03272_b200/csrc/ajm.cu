@@ -63,6 +63,7 @@ struct ajm_ctx {
     SolveFn fn = nullptr;
     size_t dyn_smem = 0;
     int64_t nunits = 0;
+    int meta_units = 0, meta_chunks = 0;
     int grid = 0;
     uint32_t flags = 0;
     // device arrays
@@ -199,6 +200,8 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.n_sell = (int)h->n_sell;
     p.ident = h->ident ? 1 : 0;
     p.max_passes = max_passes;
+    p.meta_units = h->meta_units;
+    p.meta_chunks = h->meta_chunks;
     return p;
 }
 
@@ -382,15 +385,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         }
         unit_c0_h.push_back((int)h->nchunks);
         h->nunits = (int64_t)ucost.size();
-        int occ = 0;
-        CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->fn, AJM_BLOCK + 32, h->dyn_smem));
-        if (occ < 1) return bail(fail(h, AJM_ERR_CUDA, "solver kernel cannot be resident"));
-        h->ctas_per_sm = occ;
         const int64_t nitems = h->nseg + h->nunits;
-        const int64_t g = (int64_t)h->sm_count * occ;
-        h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(g, nitems));
-        const int G = h->grid;
-        // one sequence: segments (split rows first), then units; contiguous CTA ranges by cost
         std::vector<double> cost;
         cost.reserve((size_t)nitems);
         for (int64_t s2 = 0; s2 < h->nseg; ++s2)
@@ -398,23 +393,52 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         for (double x : ucost) cost.push_back(x);
         double total = 0.0;
         for (double x : cost) total += x;
-        const double target = total / (double)G;
-        std::vector<int64_t> start((size_t)G + 1, nitems);
-        int64_t i = 0;
-        double pref = 0.0;
-        for (int cc = 0; cc < G; ++cc) {
-            start[(size_t)cc] = i;
-            if (cc == G - 1) break;
-            const double lim = target * (double)(cc + 1);
-            while (i < nitems && pref + 0.5 * cost[(size_t)i] < lim) pref += cost[(size_t)i++];
+        // one sequence: segments (split rows first), then units; contiguous CTA ranges by cost
+        auto plan = [&](int G) {
+            const double target = total / (double)G;
+            std::vector<int64_t> start((size_t)G + 1, nitems);
+            int64_t i = 0;
+            double pref = 0.0;
+            for (int cc = 0; cc < G; ++cc) {
+                start[(size_t)cc] = i;
+                if (cc == G - 1) break;
+                const double lim = target * (double)(cc + 1);
+                while (i < nitems && pref + 0.5 * cost[(size_t)i] < lim) pref += cost[(size_t)i++];
+            }
+            start[(size_t)G] = nitems;
+            cta_seg_h.assign((size_t)G + 1, 0);
+            cta_unit_h.assign((size_t)G + 1, 0);
+            for (int cc = 0; cc <= G; ++cc) {
+                cta_seg_h[(size_t)cc] = (int)std::min<int64_t>(start[(size_t)cc], h->nseg);
+                cta_unit_h[(size_t)cc] = (int)std::max<int64_t>(start[(size_t)cc] - h->nseg, 0);
+            }
+            int mu = 1, mc = 1;
+            for (int cc = 0; cc < G; ++cc) {
+                const int ua = cta_unit_h[(size_t)cc], ub = cta_unit_h[(size_t)cc + 1];
+                mu = std::max(mu, ub - ua + 1);
+                if (ub > ua) mc = std::max(mc, unit_c0_h[(size_t)ub] - unit_c0_h[(size_t)ua] + 1);
+            }
+            h->meta_units = (mu + 3) & ~3;
+            h->meta_chunks = (mc + 3) & ~3;
+        };
+        const size_t ring = h->dyn_smem;
+        size_t meta = 4096;  // initial allowance, grown until the plan fits
+        for (int iter = 0;; ++iter) {
+            h->dyn_smem = ring + meta;
+            CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem));
+            int occ = 0;
+            CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->fn, AJM_BLOCK + 32, h->dyn_smem));
+            if (occ < 1) return bail(fail(h, AJM_ERR_UNSUPPORTED, "solver kernel cannot be resident (%zu B smem)", h->dyn_smem));
+            h->ctas_per_sm = occ;
+            const int64_t g = (int64_t)h->sm_count * occ;
+            h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(g, nitems));
+            plan(h->grid);
+            const size_t need = (size_t)(h->meta_units + h->meta_chunks) * sizeof(int);
+            if (need <= meta) break;
+            if (iter > 4) return bail(fail(h, AJM_ERR_UNSUPPORTED, "layout metadata does not fit shared memory"));
+            meta = need;
         }
-        start[(size_t)G] = nitems;
-        cta_seg_h.assign((size_t)G + 1, 0);
-        cta_unit_h.assign((size_t)G + 1, 0);
-        for (int cc = 0; cc <= G; ++cc) {
-            cta_seg_h[(size_t)cc] = (int)std::min<int64_t>(start[(size_t)cc], h->nseg);
-            cta_unit_h[(size_t)cc] = (int)std::max<int64_t>(start[(size_t)cc] - h->nseg, 0);
-        }
+        const int G = h->grid;
         // owner of a split row = the CTA that runs its last segment
         std::vector<int> seg_cta((size_t)h->nseg, 0);
         for (int cc = 0; cc < G; ++cc)

@@ -110,6 +110,8 @@ struct AjmPass {
     int n_sell;
     int ident;                               // SELL slot == row
     int max_passes;                          // passes this launch (debug host loop: 1)
+    int meta_units;                          // smem capacity for a CTA's unit table (+1)
+    int meta_chunks;                         // smem capacity for a CTA's chunk offsets (+1)
 };
 
 __device__ __forceinline__ double ajm_warp_sum(double v) {
@@ -394,6 +396,15 @@ __global__ void __launch_bounds__(AJM_BLOCK + 32, kMinCtas) ajm_solve_kernel(Ajm
     const int nunits = u1 - u0;
     double* s_val = reinterpret_cast<double*>(s_dyn);
     int* s_col = reinterpret_cast<int*>(s_dyn + (size_t)kStages * AJM_UNIT_EL * sizeof(double));
+    // static per-CTA SELL metadata, loaded once: unit -> first chunk, chunk -> element offset
+    // (relative to this CTA's first chunk / element), so the pass never chases global pointers
+    int* s_uc0 = s_col + (size_t)kStages * AJM_UNIT_EL;
+    int* s_coff = s_uc0 + p.meta_units;
+    const int cfirst = nunits > 0 ? p.unit_c0[u0] : 0;
+    const int nchk = nunits > 0 ? p.unit_c0[u1] - cfirst : 0;
+    const long long efirst = nunits > 0 ? p.chunk_off[cfirst] : 0;
+    for (int i = tid; i <= nunits; i += blockDim.x) s_uc0[i] = p.unit_c0[u0 + i] - cfirst;
+    for (int i = tid; i <= nchk; i += blockDim.x) s_coff[i] = (int)(p.chunk_off[cfirst + i] - efirst);
     if (tid == 0) {
         s_st = c->s;
         s_stop = 0;
@@ -421,12 +432,12 @@ __global__ void __launch_bounds__(AJM_BLOCK + 32, kMinCtas) ajm_solve_kernel(Ajm
                     if (++spins > (1LL << 26)) { atomicExch(&c->timeout_flag, 1u); stop = true; break; }
                 }
                 if (stop || s_stop) break;
-                const int u = u0 + (int)(cnt % nunits);
-                const long long e0 = p.chunk_off[p.unit_c0[u]], e1 = p.chunk_off[p.unit_c0[u + 1]];
+                const int uu = (int)(cnt % nunits);
+                const int e0 = s_coff[s_uc0[uu]], e1 = s_coff[s_uc0[uu + 1]];
                 const unsigned ne = (unsigned)(e1 - e0);
                 ajm_mbar_expect_tx(&s_full[stage], ne * 12u);
-                ajm_bulk_g2s(s_val + (size_t)stage * AJM_UNIT_EL, p.sval + e0, ne * 8u, &s_full[stage]);
-                ajm_bulk_g2s(s_col + (size_t)stage * AJM_UNIT_EL, p.scol + e0, ne * 4u, &s_full[stage]);
+                ajm_bulk_g2s(s_val + (size_t)stage * AJM_UNIT_EL, p.sval + efirst + e0, ne * 8u, &s_full[stage]);
+                ajm_bulk_g2s(s_col + (size_t)stage * AJM_UNIT_EL, p.scol + efirst + e0, ne * 4u, &s_full[stage]);
             }
             // drain: every issued copy must land before the CTA exits
             long long spins = 0;
@@ -471,18 +482,16 @@ __global__ void __launch_bounds__(AJM_BLOCK + 32, kMinCtas) ajm_solve_kernel(Ajm
         // (2) SELL units from the shared-memory ring; chunk j of the CTA -> warp j % AJM_WARPS
         {
             int jc = warp;  // my next chunk, counted from the CTA's first chunk
-            const int cbase = nunits > 0 ? p.unit_c0[u0] : 0;
             for (int uu = 0; uu < nunits; ++uu, ++ucnt) {
-                const int u = u0 + uu;
-                const int ca = p.unit_c0[u] - cbase, cb = p.unit_c0[u + 1] - cbase;
+                const int cb = s_uc0[uu + 1];
                 const int stage = (int)(ucnt % kStages);
                 const unsigned par = (unsigned)((ucnt / kStages) & 1);
-                const long long ebase = p.chunk_off[p.unit_c0[u]];
+                const int ebase = s_coff[s_uc0[uu]];
                 bool waited = false;
                 while (jc < cb) {
-                    const int ch = cbase + jc;
-                    const long long e0 = p.chunk_off[ch];
-                    const int w = (int)((p.chunk_off[ch + 1] - e0) >> 5);
+                    const int ch = cfirst + jc;
+                    const int e0 = s_coff[jc];
+                    const int w = (s_coff[jc + 1] - e0) >> 5;
                     const int slot = ch * 32 + lane;
                     const int row = p.ident ? (slot < p.n_sell ? slot : -1) : __ldg(p.perm + slot);
                     double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
@@ -502,7 +511,6 @@ __global__ void __launch_bounds__(AJM_BLOCK + 32, kMinCtas) ajm_solve_kernel(Ajm
                     if (row >= 0) ajm_row_update(p.Qxp, xf, row, q, bi, Di, xt, xpi, qxp, beta, restart_t, acc);
                     jc += AJM_WARPS;
                 }
-                (void)ca;
                 if (!waited) ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);  // keep the phases in step
                 __syncwarp();
                 if (lane == 0) ajm_mbar_arrive(&s_empty[stage]);
