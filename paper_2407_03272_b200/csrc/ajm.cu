@@ -64,6 +64,7 @@ struct ajm_ctx {
     size_t dyn_smem = 0;
     int64_t nunits = 0;
     int meta_units = 0, meta_chunks = 0;
+    int l2_mode = 2;
     int grid = 0;
     uint32_t flags = 0;
     // device arrays
@@ -202,6 +203,7 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.max_passes = max_passes;
     p.meta_units = h->meta_units;
     p.meta_chunks = h->meta_chunks;
+    p.l2_mode = h->l2_mode;
     return p;
 }
 
@@ -281,6 +283,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     if (!coop) return bail(fail(h, AJM_ERR_UNSUPPORTED, "device does not support cooperative launch"));
     if (const char* ev = getenv("AJM_KVARIANT")) h->variant = std::max(0, std::min(kNumVariants - 1, atoi(ev)));
     h->fn = kVariants[h->variant].fn;
+    if (const char* ev = getenv("AJM_L2MODE")) h->l2_mode = std::max(0, std::min(2, atoi(ev)));
     h->dyn_smem = (size_t)kVariants[h->variant].stages * AJM_UNIT_EL * (sizeof(double) + sizeof(int));
     CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem));
 

@@ -112,6 +112,7 @@ struct AjmPass {
     int max_passes;                          // passes this launch (debug host loop: 1)
     int meta_units;                          // smem capacity for a CTA's unit table (+1)
     int meta_chunks;                         // smem capacity for a CTA's chunk offsets (+1)
+    int l2_mode;                             // 0 none, 1 Q evict_first, 2 + vectors evict_last
 };
 
 __device__ __forceinline__ double ajm_warp_sum(double v) {
@@ -128,11 +129,32 @@ struct AjmAcc {
 // coherent (L1-cached, invalidated by the post-barrier fence) load of data written in-kernel
 __device__ __forceinline__ double ajm_ld(const double* p) { return *p; }
 
+// L2 eviction-priority policies (createpolicy): the Q stream is evict_first, the iterate vectors
+// evict_last, so the ~100 MB of vectors stay L2-resident across passes
+__device__ __forceinline__ uint64_t ajm_policy(int kind) {
+    uint64_t pol;
+    if (kind == 1)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    else if (kind == 2)
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ double ajm_ldp(const double* p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void ajm_stp(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 // a3-a6 for one row i with q = (Q x~^t)_i and the five row operands
 __device__ __forceinline__ void ajm_row_update(double* __restrict__ Qxp, double* __restrict__ xf,
                                                int i, double q, double bi, double Di, double xt,
                                                double xpi, double qxp, double beta, int restart_t,
-                                               AjmAcc& a) {
+                                               AjmAcc& a, uint64_t pol) {
     const double r = bi - q;
     a.rr += r * r;
     a.xq += xt * q;
@@ -141,7 +163,7 @@ __device__ __forceinline__ void ajm_row_update(double* __restrict__ Qxp, double*
     if (!restart_t) {
         y = xt + beta * (xt - xpi);
         qy = q + beta * (q - qxp);
-        Qxp[i] = q;
+        ajm_stp(Qxp + i, q, pol);
         xnow = xt;
     } else {
         y = xpi;
@@ -149,7 +171,7 @@ __device__ __forceinline__ void ajm_row_update(double* __restrict__ Qxp, double*
         xnow = xpi;
     }
     const double xn = y + (bi - qy) / Di;
-    xf[i] = xn;
+    ajm_stp(xf + i, xn, pol);
     const double term = (qy - bi) * (xn - xnow);
     a.d += term;
     a.dabs += fabs(term);
@@ -158,8 +180,9 @@ __device__ __forceinline__ void ajm_row_update(double* __restrict__ Qxp, double*
 __device__ __forceinline__ void ajm_row_epilogue(const AjmPass& p, int i, double q, double beta,
                                                  int restart_t, const double* xc, const double* xp,
                                                  double* xf, AjmAcc& a) {
-    ajm_row_update(p.Qxp, xf, i, q, __ldg(p.b + i), __ldg(p.D + i), ajm_ld(xc + i), ajm_ld(xp + i),
-                   p.Qxp[i], beta, restart_t, a);
+    const uint64_t pol = ajm_policy(p.l2_mode >= 2 ? 2 : 0);
+    ajm_row_update(p.Qxp, xf, i, q, ajm_ldp(p.b + i, pol), ajm_ldp(p.D + i, pol), ajm_ld(xc + i),
+                   ajm_ld(xp + i), ajm_ldp(p.Qxp + i, pol), beta, restart_t, a, pol);
 }
 
 __device__ __forceinline__ double* ajm_sel(const AjmPass& p, int k) {
@@ -345,11 +368,14 @@ __device__ __forceinline__ void ajm_mbar_wait(uint64_t* bar, unsigned parity, un
         }
     }
 }
-// 1-D bulk copy global -> shared (cp.async.bulk, completes tx bytes on the mbarrier)
-__device__ __forceinline__ void ajm_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+// 1-D bulk copy global -> shared (cp.async.bulk, completes tx bytes on the mbarrier), with an L2
+// eviction-priority hint
+__device__ __forceinline__ void ajm_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                             uint64_t pol) {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(ajm_smem(dst)),
-        "l"(src), "r"(bytes), "r"(ajm_smem(bar))
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            ajm_smem(dst)),
+        "l"(src), "r"(bytes), "r"(ajm_smem(bar)), "l"(pol)
         : "memory");
 }
 
@@ -420,6 +446,7 @@ __global__ void __launch_bounds__(AJM_BLOCK + 32, kMinCtas) ajm_solve_kernel(Ajm
     if (warp == AJM_WARPS) {
         // ---------------- producer warp ----------------
         if (lane == 0 && nunits > 0) {
+            const uint64_t qpol = ajm_policy(p.l2_mode >= 1 ? 1 : 0);
             long long cnt = 0;
             const long long total = (long long)nunits * p.max_passes;
             for (; cnt < total; ++cnt) {
@@ -436,8 +463,8 @@ __global__ void __launch_bounds__(AJM_BLOCK + 32, kMinCtas) ajm_solve_kernel(Ajm
                 const int e0 = s_coff[s_uc0[uu]], e1 = s_coff[s_uc0[uu + 1]];
                 const unsigned ne = (unsigned)(e1 - e0);
                 ajm_mbar_expect_tx(&s_full[stage], ne * 12u);
-                ajm_bulk_g2s(s_val + (size_t)stage * AJM_UNIT_EL, p.sval + efirst + e0, ne * 8u, &s_full[stage]);
-                ajm_bulk_g2s(s_col + (size_t)stage * AJM_UNIT_EL, p.scol + efirst + e0, ne * 4u, &s_full[stage]);
+                ajm_bulk_g2s(s_val + (size_t)stage * AJM_UNIT_EL, p.sval + efirst + e0, ne * 8u, &s_full[stage], qpol);
+                ajm_bulk_g2s(s_col + (size_t)stage * AJM_UNIT_EL, p.scol + efirst + e0, ne * 4u, &s_full[stage], qpol);
             }
             // drain: every issued copy must land before the CTA exits
             long long spins = 0;
@@ -451,6 +478,7 @@ __global__ void __launch_bounds__(AJM_BLOCK + 32, kMinCtas) ajm_solve_kernel(Ajm
     }
 
     // ---------------- consumer warps ----------------
+    const uint64_t vpol = ajm_policy(p.l2_mode >= 2 ? 2 : 0);
     const int sg0 = p.cta_seg[bid], sg1 = p.cta_seg[bid + 1];
     const int sp0 = p.cta_split[bid], sp1 = p.cta_split[bid + 1];
     long long ucnt = 0;  // units consumed by this CTA (all passes)
@@ -496,11 +524,11 @@ __global__ void __launch_bounds__(AJM_BLOCK + 32, kMinCtas) ajm_solve_kernel(Ajm
                     const int row = p.ident ? (slot < p.n_sell ? slot : -1) : __ldg(p.perm + slot);
                     double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
                     if (row >= 0) {  // row operands first: independent of the stage data
-                        bi = __ldcs(p.b + row);
-                        Di = __ldcs(p.D + row);
+                        bi = ajm_ldp(p.b + row, vpol);
+                        Di = ajm_ldp(p.D + row, vpol);
                         xt = ajm_ld(xc + row);
                         xpi = ajm_ld(xp + row);
-                        qxp = p.Qxp[row];
+                        qxp = ajm_ldp(p.Qxp + row, vpol);
                     }
                     if (!waited) {
                         ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);
@@ -508,7 +536,7 @@ __global__ void __launch_bounds__(AJM_BLOCK + 32, kMinCtas) ajm_solve_kernel(Ajm
                     }
                     const size_t off = (size_t)stage * AJM_UNIT_EL + (size_t)(e0 - ebase) + lane;
                     const double q = ajm_chunk_dot(s_val + off, s_col + off, w, xc);
-                    if (row >= 0) ajm_row_update(p.Qxp, xf, row, q, bi, Di, xt, xpi, qxp, beta, restart_t, acc);
+                    if (row >= 0) ajm_row_update(p.Qxp, xf, row, q, bi, Di, xt, xpi, qxp, beta, restart_t, acc, vpol);
                     jc += AJM_WARPS;
                 }
                 if (!waited) ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);  // keep the phases in step

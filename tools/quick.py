@@ -6,15 +6,18 @@ import synth, paper_2407_03272_b200 as ajm
 
 cfgs = [int(c) for c in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["1", "2"])]
 variants = [int(v) for v in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["0"])]
+l2modes = [int(v) for v in (sys.argv[3].split(",") if len(sys.argv) > 3 else ["2"])]
+variants = [(v, m) for v in variants for m in l2modes]
 for cfg in cfgs:
     t0 = time.time(); p = synth.config_problem(cfg); tg = time.time() - t0
-    for var in variants:
+    for var, l2m in variants:
         os.environ["AJM_KVARIANT"] = str(var)
+        os.environ["AJM_L2MODE"] = str(l2m)
         t0 = time.time()
         with ajm.Solver.from_csr(p.Q, p.b) as s:
             tc = time.time() - t0
             info = s.info()
-            print(f"cfg{cfg} var{var} n={p.Q.n} nnz={p.Q.nnz} gen={tg:.1f}s create={tc:.2f}s grid={info['grid']} "
+            print(f"cfg{cfg} var{var} l2m{l2m} n={p.Q.n} nnz={p.Q.nnz} gen={tg:.1f}s create={tc:.2f}s grid={info['grid']} "
                   f"occ={info['ctas_per_sm']} units={info['units']} sell={info['sell_rows']} seg={info['seg_rows']} split={info['split_rows']} sigma={info['sigma']} pad={info['sell_elems']}", flush=True)
             for rep in range(2):
                 r = s.solve(tol=1e-6, maxit=5000, restart=True)
