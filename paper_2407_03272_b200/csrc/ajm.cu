@@ -38,13 +38,13 @@ struct SolveVariant {
     int stages;
     const char* name;
 };
-// TMA ring depth x min resident CTAs per SM (shared memory / register budget); AJM_KVARIANT
-// selects one (tuning); the default is the measured best on B200
+// TMA ring depth x register cap (=> resident CTAs per SM with 288 threads); AJM_KVARIANT selects
+// one (tuning); the default is the measured best on B200
 const SolveVariant kVariants[] = {
-    {ajm_solve_kernel<4, 2>, 4, "s4m2"},
-    {ajm_solve_kernel<3, 3>, 3, "s3m3"},
-    {ajm_solve_kernel<2, 4>, 2, "s2m4"},
-    {ajm_solve_kernel<6, 1>, 6, "s6m1"},
+    {ajm_solve_kernel<4, 112>, 4, "s4r112"},  // 2 CTAs/SM
+    {ajm_solve_kernel<3, 72>, 3, "s3r72"},    // 3 CTAs/SM
+    {ajm_solve_kernel<6, 168>, 6, "s6r168"},  // 1 CTA/SM
+    {ajm_solve_kernel<3, 112>, 3, "s3r112"},  // 2 CTAs/SM, shallower ring
 };
 const int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 

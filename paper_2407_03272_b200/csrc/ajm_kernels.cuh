@@ -399,13 +399,50 @@ __device__ __forceinline__ double ajm_chunk_dot(const double* sv, const int* sc,
     return s;
 }
 
+// Two chunks' dots interleaved (twice the independent gathers in flight per warp).
+__device__ __forceinline__ void ajm_chunk_dot2(const double* svA, const int* scA, int wA, const double* svB,
+                                               const int* scB, int wB, const double* xc, double& qA,
+                                               double& qB) {
+    double sA = 0.0, sB = 0.0;
+    const int w = wA > wB ? wA : wB;
+    for (int k0 = 0; k0 < w; k0 += 4) {
+        double xa[4], xb[4];
+        int ca[4], cb[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            ca[j] = (k0 + j < wA) ? scA[(k0 + j) * 32] : 0;
+            cb[j] = (k0 + j < wB) ? scB[(k0 + j) * 32] : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (k0 + j < wA) xa[j] = ajm_ld(xc + ca[j]);
+            if (k0 + j < wB) xb[j] = ajm_ld(xc + cb[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (k0 + j < wA) sA += svA[(k0 + j) * 32] * xa[j];  // ascending column order
+            if (k0 + j < wB) sB += svB[(k0 + j) * 32] * xb[j];
+        }
+    }
+    qA = sA;
+    qB = sB;
+}
+
+// A SELL chunk whose row operands are in flight while the warp waits for the next stage.
+struct AjmPend {
+    int off;  // element offset of this lane's first entry in the shared-memory ring
+    int w;
+    int row;
+    double bi, Di, xt, xpi, qxp;
+};
+
 // The persistent solver kernel (cooperative launch; grid = resident CTAs).  AJM_BLOCK consumer
 // threads + one producer warp that streams this CTA's SELL units (val and col of <= 8 chunks,
 // <= AJM_UNIT_EL elements) into a kStages-deep shared-memory ring with cp.async.bulk.  Q does not
 // change between passes, so the producer runs ahead across pass boundaries (it keeps the ring
 // full while the consumers sit in the grid barrier).
-template <int kStages, int kMinCtas>
-__global__ void __launch_bounds__(AJM_BLOCK + 32, kMinCtas) ajm_solve_kernel(AjmPass p) {
+template <int kStages, int kMaxReg>
+__global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     extern __shared__ __align__(128) unsigned char s_dyn[];
     __shared__ double s_red[AJM_WARPS][AJM_NPART];
     __shared__ double s_tot[AJM_NPART];
@@ -507,42 +544,75 @@ __global__ void __launch_bounds__(AJM_BLOCK + 32, kMinCtas) ajm_solve_kernel(Ajm
                 }
             }
         }
-        // (2) SELL units from the shared-memory ring; chunk j of the CTA -> warp j % AJM_WARPS
+        // (2) SELL units from the shared-memory ring; chunk j of the CTA -> warp j % AJM_WARPS, so a
+        //     warp has at most one chunk per unit.  Chunks are processed in pairs (the first one's
+        //     row operands load while the warp waits for the next unit); a warp never holds more
+        //     than kStages-1 unreleased units, so the producer can always make progress.
         {
             int jc = warp;  // my next chunk, counted from the CTA's first chunk
-            for (int uu = 0; uu < nunits; ++uu, ++ucnt) {
-                const int cb = s_uc0[uu + 1];
-                const int stage = (int)(ucnt % kStages);
-                const unsigned par = (unsigned)((ucnt / kStages) & 1);
-                const int ebase = s_coff[s_uc0[uu]];
-                bool waited = false;
-                while (jc < cb) {
-                    const int ch = cfirst + jc;
-                    const int e0 = s_coff[jc];
-                    const int w = (s_coff[jc + 1] - e0) >> 5;
-                    const int slot = ch * 32 + lane;
-                    const int row = p.ident ? (slot < p.n_sell ? slot : -1) : __ldg(p.perm + slot);
-                    double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
-                    if (row >= 0) {  // row operands first: independent of the stage data
-                        bi = ajm_ldp(p.b + row, vpol);
-                        Di = ajm_ldp(p.D + row, vpol);
-                        xt = ajm_ld(xc + row);
-                        xpi = ajm_ld(xp + row);
-                        qxp = ajm_ldp(p.Qxp + row, vpol);
-                    }
-                    if (!waited) {
-                        ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);
-                        waited = true;
-                    }
-                    const size_t off = (size_t)stage * AJM_UNIT_EL + (size_t)(e0 - ebase) + lane;
-                    const double q = ajm_chunk_dot(s_val + off, s_col + off, w, xc);
-                    if (row >= 0) ajm_row_update(p.Qxp, xf, row, q, bi, Di, xt, xpi, qxp, beta, restart_t, acc, vpol);
-                    jc += AJM_WARPS;
+            int rel = 0;    // units [0, rel) released by this warp this pass
+            bool have = false;
+            int have_u = 0;
+            AjmPend pa;
+            auto release_to = [&](int upto) {  // arrive on units [rel, upto)
+                for (; rel < upto; ++rel) {
+                    __syncwarp();
+                    if (lane == 0) ajm_mbar_arrive(&s_empty[(int)((ucnt + rel) % kStages)]);
                 }
-                if (!waited) ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);  // keep the phases in step
-                __syncwarp();
-                if (lane == 0) ajm_mbar_arrive(&s_empty[stage]);
+            };
+            auto load_pend = [&](AjmPend& q, int j, int uu) {
+                const int ch = cfirst + j;
+                const int e0 = s_coff[j];
+                q.w = (s_coff[j + 1] - e0) >> 5;
+                q.off = (int)(((ucnt + uu) % kStages) * AJM_UNIT_EL) + (e0 - s_coff[s_uc0[uu]]) + lane;
+                const int slot = ch * 32 + lane;
+                q.row = p.ident ? (slot < p.n_sell ? slot : -1) : __ldg(p.perm + slot);
+                q.bi = 0.0; q.Di = 1.0; q.xt = 0.0; q.xpi = 0.0; q.qxp = 0.0;
+                if (q.row >= 0) {
+                    q.bi = ajm_ldp(p.b + q.row, vpol);
+                    q.Di = ajm_ldp(p.D + q.row, vpol);
+                    q.xt = ajm_ld(xc + q.row);
+                    q.xpi = ajm_ld(xp + q.row);
+                    q.qxp = ajm_ldp(p.Qxp + q.row, vpol);
+                }
+            };
+            auto finish = [&](const AjmPend& q, double dot) {
+                if (q.row >= 0)
+                    ajm_row_update(p.Qxp, xf, q.row, dot, q.bi, q.Di, q.xt, q.xpi, q.qxp, beta, restart_t, acc, vpol);
+            };
+            for (int uu = 0; uu < nunits; ++uu) {
+                if (have && uu - have_u >= kStages - 1) {  // look-ahead limit: run the pending chunk alone
+                    finish(pa, ajm_chunk_dot(s_val + pa.off, s_col + pa.off, pa.w, xc));
+                    have = false;
+                    release_to(uu);
+                }
+                const bool mine = jc < s_uc0[uu + 1];
+                AjmPend pb;
+                if (mine) load_pend(pb, jc, uu);  // operands in flight during the wait
+                ajm_mbar_wait(&s_full[(int)((ucnt + uu) % kStages)], (unsigned)(((ucnt + uu) / kStages) & 1),
+                              &c->timeout_flag);
+                if (mine) {
+                    jc += AJM_WARPS;
+                    if (have) {
+                        double qa, qb;
+                        ajm_chunk_dot2(s_val + pa.off, s_col + pa.off, pa.w, s_val + pb.off, s_col + pb.off, pb.w,
+                                       xc, qa, qb);
+                        finish(pa, qa);
+                        finish(pb, qb);
+                        have = false;
+                        release_to(uu + 1);
+                    } else {
+                        pa = pb;
+                        have = true;
+                        have_u = uu;
+                    }
+                } else if (!have) {
+                    release_to(uu + 1);
+                }
             }
+            if (have) finish(pa, ajm_chunk_dot(s_val + pa.off, s_col + pa.off, pa.w, xc));
+            release_to(nunits);
+            ucnt += nunits;
         }
         // (3) split rows owned by this CTA: wait for all segments of this pass, sum in order
         for (int k = sp0 + warp; k < sp1; k += AJM_WARPS) {
