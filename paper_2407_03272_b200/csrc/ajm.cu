@@ -41,10 +41,10 @@ struct SolveVariant {
 // TMA ring depth x register cap (=> resident CTAs per SM with 288 threads); AJM_KVARIANT selects
 // one (tuning); the default is the measured best on B200
 const SolveVariant kVariants[] = {
-    {ajm_solve_kernel<4, 112>, 4, "s4r112"},  // 2 CTAs/SM
-    {ajm_solve_kernel<3, 72>, 3, "s3r72"},    // 3 CTAs/SM
-    {ajm_solve_kernel<6, 168>, 6, "s6r168"},  // 1 CTA/SM
-    {ajm_solve_kernel<3, 112>, 3, "s3r112"},  // 2 CTAs/SM, shallower ring
+    {ajm_solve_kernel<3, 112>, 3, "s3r112"},  // 2 CTAs/SM
+    {ajm_solve_kernel<2, 72>, 2, "s2r72"},    // 3 CTAs/SM
+    {ajm_solve_kernel<6, 128>, 6, "s6r128"},  // 1 CTA/SM, deep ring
+    {ajm_solve_kernel<4, 112>, 4, "s4r112"},  // 1-2 CTAs/SM (shared-memory bound)
 };
 const int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -54,7 +54,7 @@ struct ajm_ctx {
     int device = 0;
     int sm_count = 0;
     int ctas_per_sm = 0;
-    int64_t n = 0, nnz = 0;
+    int64_t n = 0, nnz = 0, n_pad = 0;
     int64_t nchunks = 0, n_sell = 0, sell_elems = 0;
     int64_t nseg = 0, nsplit = 0, seg_rows = 0, long_rows = 0;
     int sigma = 1;
@@ -284,8 +284,6 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     if (const char* ev = getenv("AJM_KVARIANT")) h->variant = std::max(0, std::min(kNumVariants - 1, atoi(ev)));
     h->fn = kVariants[h->variant].fn;
     if (const char* ev = getenv("AJM_L2MODE")) h->l2_mode = std::max(0, std::min(2, atoi(ev)));
-    h->dyn_smem = (size_t)kVariants[h->variant].stages * AJM_UNIT_EL * (sizeof(double) + sizeof(int));
-    CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem));
 
     // ---- row-length-binned layout (host, O(n log sigma)) ----
     auto rlen = [&](int64_t r) { return hrp[(size_t)r + 1] - hrp[(size_t)r]; };
@@ -424,7 +422,9 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             h->meta_units = (mu + 3) & ~3;
             h->meta_chunks = (mc + 3) & ~3;
         };
-        const size_t ring = h->dyn_smem;
+        // ring: val/col of a unit (+ the rows' five vector slices for natural-order layouts)
+        const size_t ring = (size_t)kVariants[h->variant].stages *
+                            ((size_t)AJM_UNIT_EL * 12 + (h->ident ? (size_t)5 * AJM_UNIT_ROWS * 8 : 0));
         size_t meta = 4096;  // initial allowance, grown until the plan fits
         for (int iter = 0;; ++iter) {
             h->dyn_smem = ring + meta;
@@ -460,10 +460,15 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(dalloc(&h->rp, n + 1));
     CC(dalloc(&h->col, nnz));
     CC(dalloc(&h->val, nnz));
-    CC(dalloc(&h->b, n));
-    CC(dalloc(&h->D, n));
-    for (int k = 0; k < 3; ++k) CC(dalloc(&h->X[k], n));
-    CC(dalloc(&h->Qxp, n));
+    // vectors padded to whole SELL chunks (the TMA stages copy whole 32-row slices)
+    h->n_pad = std::max<int64_t>(n, h->nchunks * 32);
+    CC(dalloc(&h->b, h->n_pad));
+    CC(dalloc(&h->D, h->n_pad));
+    for (int k = 0; k < 3; ++k) CC(dalloc(&h->X[k], h->n_pad));
+    CC(dalloc(&h->Qxp, h->n_pad));
+    CC(cudaMemsetAsync(h->b, 0, sizeof(double) * h->n_pad, st));
+    CC(cudaMemsetAsync(h->D, 0, sizeof(double) * h->n_pad, st));
+    for (int k = 0; k < 3; ++k) CC(cudaMemsetAsync(h->X[k], 0, sizeof(double) * h->n_pad, st));
     CC(dalloc(&h->sval, h->sell_elems));
     CC(dalloc(&h->scol, h->sell_elems));
     CC(dalloc(&h->chunk_off, h->nchunks + 1));
@@ -601,10 +606,10 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
         if (herr) return fail(h, AJM_ERR_NONFINITE, "x0 has a non-finite entry");
         AJM_CUDA(h, cudaMemcpyAsync(h->X[1], h->X[0], sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     } else {
-        AJM_CUDA(h, cudaMemsetAsync(h->X[0], 0, sizeof(double) * n, st));
-        AJM_CUDA(h, cudaMemsetAsync(h->X[1], 0, sizeof(double) * n, st));
+        AJM_CUDA(h, cudaMemsetAsync(h->X[0], 0, sizeof(double) * h->n_pad, st));
+        AJM_CUDA(h, cudaMemsetAsync(h->X[1], 0, sizeof(double) * h->n_pad, st));
     }
-    AJM_CUDA(h, cudaMemsetAsync(h->Qxp, 0, sizeof(double) * n, st));
+    AJM_CUDA(h, cudaMemsetAsync(h->Qxp, 0, sizeof(double) * h->n_pad, st));
     if (h->nsplit) AJM_CUDA(h, cudaMemsetAsync(h->split_cnt, 0, sizeof(unsigned) * h->nsplit, st));
     double* hr = h->hist;
     double* hf = h->hist + h->hist_cap;

@@ -38,6 +38,7 @@
 #define AJM_SEG 2048     // max nonzeros per warp segment of a longer row
 #define AJM_NPART 5      // rr, <x,q>, <b,x>, d, sum|d terms|
 #define AJM_UNIT_EL 2048 // SELL elements per TMA staging unit (24 KB of val + col)
+#define AJM_UNIT_ROWS (AJM_WARPS * 32)  // rows per staging unit (<= 8 chunks)
 #define AJM_LOG_CAP 64
 
 // Iteration state: identical copies in every CTA (shared memory) and in global memory.
@@ -399,48 +400,14 @@ __device__ __forceinline__ double ajm_chunk_dot(const double* sv, const int* sc,
     return s;
 }
 
-// Two chunks' dots interleaved (twice the independent gathers in flight per warp).
-__device__ __forceinline__ void ajm_chunk_dot2(const double* svA, const int* scA, int wA, const double* svB,
-                                               const int* scB, int wB, const double* xc, double& qA,
-                                               double& qB) {
-    double sA = 0.0, sB = 0.0;
-    const int w = wA > wB ? wA : wB;
-    for (int k0 = 0; k0 < w; k0 += 4) {
-        double xa[4], xb[4];
-        int ca[4], cb[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            ca[j] = (k0 + j < wA) ? scA[(k0 + j) * 32] : 0;
-            cb[j] = (k0 + j < wB) ? scB[(k0 + j) * 32] : 0;
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (k0 + j < wA) xa[j] = ajm_ld(xc + ca[j]);
-            if (k0 + j < wB) xb[j] = ajm_ld(xc + cb[j]);
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (k0 + j < wA) sA += svA[(k0 + j) * 32] * xa[j];  // ascending column order
-            if (k0 + j < wB) sB += svB[(k0 + j) * 32] * xb[j];
-        }
-    }
-    qA = sA;
-    qB = sB;
-}
-
-// A SELL chunk whose row operands are in flight while the warp waits for the next stage.
-struct AjmPend {
-    int off;  // element offset of this lane's first entry in the shared-memory ring
-    int w;
-    int row;
-    double bi, Di, xt, xpi, qxp;
-};
-
 // The persistent solver kernel (cooperative launch; grid = resident CTAs).  AJM_BLOCK consumer
-// threads + one producer warp that streams this CTA's SELL units (val and col of <= 8 chunks,
-// <= AJM_UNIT_EL elements) into a kStages-deep shared-memory ring with cp.async.bulk.  Q does not
-// change between passes, so the producer runs ahead across pass boundaries (it keeps the ring
-// full while the consumers sit in the grid barrier).
+// threads + one producer warp.  The producer streams this CTA's SELL units into a kStages-deep
+// shared-memory ring with cp.async.bulk (TMA engine, mbarrier complete_tx):
+//   static part  -- val/col of <= 8 chunks (and, for natural-order layouts, the rows' b and D);
+//                   Q never changes, so this part runs ahead across pass boundaries;
+//   dynamic part -- (natural-order layouts) the rows' x~^t, x^{t-1}, Q x^{t-1} slices; issued
+//                   only once the pass that owns the unit has started (after the grid barrier).
+// A stage's full barrier completes when both parts have landed.
 template <int kStages, int kMaxReg>
 __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     extern __shared__ __align__(128) unsigned char s_dyn[];
@@ -450,18 +417,26 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     __shared__ __align__(8) uint64_t s_full[kStages];
     __shared__ __align__(8) uint64_t s_empty[kStages];
     __shared__ volatile int s_stop;
-    __shared__ long long s_consumed;
+    __shared__ volatile int s_pass;     // passes (of this launch) whose dynamic vectors may be staged
+    __shared__ volatile int s_bufc, s_bufp;  // x~^t / x^{t-1} buffer indices of pass s_pass
 
     AjmCtrl* c = p.ctrl;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, bid = blockIdx.x;
     const unsigned G = gridDim.x;
     const int u0 = p.cta_unit[bid], u1 = p.cta_unit[bid + 1];
     const int nunits = u1 - u0;
-    double* s_val = reinterpret_cast<double*>(s_dyn);
-    int* s_col = reinterpret_cast<int*>(s_dyn + (size_t)kStages * AJM_UNIT_EL * sizeof(double));
+    const bool vstage = p.ident != 0;  // natural order: the unit's rows are contiguous
+    // stage s: val[UNIT_EL] f64 | col[UNIT_EL] i32 | (vstage) b, D, x~, x^{t-1}, Qx^{t-1} [256] f64
+    const size_t stage_bytes = (size_t)AJM_UNIT_EL * 12 + (vstage ? (size_t)5 * AJM_UNIT_ROWS * 8 : 0);
+    auto st_val = [&](int k) { return reinterpret_cast<double*>(s_dyn + (size_t)k * stage_bytes); };
+    auto st_col = [&](int k) { return reinterpret_cast<int*>(s_dyn + (size_t)k * stage_bytes + (size_t)AJM_UNIT_EL * 8); };
+    auto st_vec = [&](int k, int which) {
+        return reinterpret_cast<double*>(s_dyn + (size_t)k * stage_bytes + (size_t)AJM_UNIT_EL * 12 +
+                                         (size_t)which * AJM_UNIT_ROWS * 8);
+    };
     // static per-CTA SELL metadata, loaded once: unit -> first chunk, chunk -> element offset
     // (relative to this CTA's first chunk / element), so the pass never chases global pointers
-    int* s_uc0 = s_col + (size_t)kStages * AJM_UNIT_EL;
+    int* s_uc0 = reinterpret_cast<int*>(s_dyn + (size_t)kStages * stage_bytes);
     int* s_coff = s_uc0 + p.meta_units;
     const int cfirst = nunits > 0 ? p.unit_c0[u0] : 0;
     const int nchk = nunits > 0 ? p.unit_c0[u1] - cfirst : 0;
@@ -471,7 +446,9 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     if (tid == 0) {
         s_st = c->s;
         s_stop = 0;
-        s_consumed = 0;
+        s_pass = 0;
+        s_bufc = s_st.cur;
+        s_bufp = s_st.prev;
         for (int k = 0; k < kStages; ++k) {
             ajm_mbar_init(&s_full[k], 1);
             ajm_mbar_init(&s_empty[k], AJM_WARPS);
@@ -481,35 +458,66 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     __syncthreads();
 
     if (warp == AJM_WARPS) {
-        // ---------------- producer warp ----------------
+        // ---------------- producer warp (one lane) ----------------
         if (lane == 0 && nunits > 0) {
             const uint64_t qpol = ajm_policy(p.l2_mode >= 1 ? 1 : 0);
-            long long cnt = 0;
+            const uint64_t vpol = ajm_policy(p.l2_mode >= 2 ? 2 : 0);
             const long long total = (long long)nunits * p.max_passes;
-            for (; cnt < total; ++cnt) {
-                const int stage = (int)(cnt % kStages);
-                const unsigned par = (unsigned)((cnt / kStages) & 1) ^ 1u;
-                bool stop = false;
-                long long spins = 0;
-                while (!ajm_mbar_try_wait(&s_empty[stage], par)) {
-                    if (s_stop) { stop = true; break; }
-                    if (++spins > (1LL << 26)) { atomicExch(&c->timeout_flag, 1u); stop = true; break; }
+            long long cnt = 0, vcnt = 0;  // units with static / dynamic parts issued
+            long long idle = 0;
+            auto issue_dynamic = [&](long long k) {
+                const int stage = (int)(k % kStages);
+                const int uu = (int)(k % nunits);
+                const int r0 = (cfirst + s_uc0[uu]) * 32;
+                const unsigned bytes = (unsigned)(s_uc0[uu + 1] - s_uc0[uu]) * 32u * 8u;
+                const double* xcur = ajm_sel(p, s_bufc);
+                const double* xprv = ajm_sel(p, s_bufp);
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                ajm_bulk_g2s(st_vec(stage, 2), xcur + r0, bytes, &s_full[stage], vpol);
+                ajm_bulk_g2s(st_vec(stage, 3), xprv + r0, bytes, &s_full[stage], vpol);
+                ajm_bulk_g2s(st_vec(stage, 4), p.Qxp + r0, bytes, &s_full[stage], vpol);
+            };
+            while (vcnt < total) {
+                bool progressed = false;
+                if (vstage && vcnt < cnt && vcnt / nunits <= (long long)s_pass) {
+                    issue_dynamic(vcnt++);
+                    progressed = true;
+                } else if (!vstage && vcnt < cnt) {
+                    vcnt = cnt;
                 }
-                if (stop || s_stop) break;
-                const int uu = (int)(cnt % nunits);
-                const int e0 = s_coff[s_uc0[uu]], e1 = s_coff[s_uc0[uu + 1]];
-                const unsigned ne = (unsigned)(e1 - e0);
-                ajm_mbar_expect_tx(&s_full[stage], ne * 12u);
-                ajm_bulk_g2s(s_val + (size_t)stage * AJM_UNIT_EL, p.sval + efirst + e0, ne * 8u, &s_full[stage], qpol);
-                ajm_bulk_g2s(s_col + (size_t)stage * AJM_UNIT_EL, p.scol + efirst + e0, ne * 4u, &s_full[stage], qpol);
+                if (cnt < total) {
+                    const int stage = (int)(cnt % kStages);
+                    const unsigned par = (unsigned)((cnt / kStages) & 1) ^ 1u;
+                    if (ajm_mbar_try_wait(&s_empty[stage], par)) {
+                        const int uu = (int)(cnt % nunits);
+                        const int e0 = s_coff[s_uc0[uu]], e1 = s_coff[s_uc0[uu + 1]];
+                        const unsigned ne = (unsigned)(e1 - e0);
+                        const unsigned vbytes = vstage ? (unsigned)(s_uc0[uu + 1] - s_uc0[uu]) * 32u * 8u : 0u;
+                        ajm_mbar_expect_tx(&s_full[stage], ne * 12u + 5u * vbytes);
+                        ajm_bulk_g2s(st_val(stage), p.sval + efirst + e0, ne * 8u, &s_full[stage], qpol);
+                        ajm_bulk_g2s(st_col(stage), p.scol + efirst + e0, ne * 4u, &s_full[stage], qpol);
+                        if (vstage) {
+                            const int r0 = (cfirst + s_uc0[uu]) * 32;
+                            ajm_bulk_g2s(st_vec(stage, 0), p.b + r0, vbytes, &s_full[stage], vpol);
+                            ajm_bulk_g2s(st_vec(stage, 1), p.D + r0, vbytes, &s_full[stage], vpol);
+                        }
+                        ++cnt;
+                        progressed = true;
+                    }
+                }
+                if (s_stop) break;
+                if (progressed) idle = 0;
+                else if (++idle > (1LL << 28)) { atomicExch(&c->timeout_flag, 1u); break; }
             }
-            // drain: every issued copy must land before the CTA exits
+            // complete every issued stage (dynamic parts of never-consumed units read stale but
+            // valid memory), then wait for all copies to land before the CTA exits
+            while (vstage && vcnt < cnt) issue_dynamic(vcnt++);
             long long spins = 0;
             while (!s_stop) {
                 if (++spins > (1LL << 32)) break;
             }
-            for (long long k = s_consumed; k < cnt; ++k)
-                ajm_mbar_wait(&s_full[k % kStages], (unsigned)((k / kStages) & 1), &c->timeout_flag);
+            for (long long k = (long long)s_pass * nunits; k < cnt; ++k)
+                if (k >= 0) ajm_mbar_wait(&s_full[k % kStages], (unsigned)((k / kStages) & 1), &c->timeout_flag);
         }
         return;
     }
@@ -519,7 +527,8 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     const int sg0 = p.cta_seg[bid], sg1 = p.cta_seg[bid + 1];
     const int sp0 = p.cta_split[bid], sp1 = p.cta_split[bid + 1];
     long long ucnt = 0;  // units consumed by this CTA (all passes)
-    for (int pass = 0; pass < p.max_passes; ++pass) {
+    int pass = 0;
+    for (; pass < p.max_passes; ++pass) {
         if (s_st.done) break;
         const long long t = s_st.t;
         const int restart_t = s_st.restart_t;
@@ -544,74 +553,51 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                 }
             }
         }
-        // (2) SELL units from the shared-memory ring; chunk j of the CTA -> warp j % AJM_WARPS, so a
-        //     warp has at most one chunk per unit.  Chunks are processed in pairs (the first one's
-        //     row operands load while the warp waits for the next unit); a warp never holds more
-        //     than kStages-1 unreleased units, so the producer can always make progress.
+        // (2) SELL units from the ring; chunk j of the CTA -> warp j % AJM_WARPS (at most one
+        //     chunk per unit per warp)
         {
-            int jc = warp;  // my next chunk, counted from the CTA's first chunk
-            int rel = 0;    // units [0, rel) released by this warp this pass
-            bool have = false;
-            int have_u = 0;
-            AjmPend pa;
-            auto release_to = [&](int upto) {  // arrive on units [rel, upto)
-                for (; rel < upto; ++rel) {
-                    __syncwarp();
-                    if (lane == 0) ajm_mbar_arrive(&s_empty[(int)((ucnt + rel) % kStages)]);
-                }
-            };
-            auto load_pend = [&](AjmPend& q, int j, int uu) {
-                const int ch = cfirst + j;
-                const int e0 = s_coff[j];
-                q.w = (s_coff[j + 1] - e0) >> 5;
-                q.off = (int)(((ucnt + uu) % kStages) * AJM_UNIT_EL) + (e0 - s_coff[s_uc0[uu]]) + lane;
-                const int slot = ch * 32 + lane;
-                q.row = p.ident ? (slot < p.n_sell ? slot : -1) : __ldg(p.perm + slot);
-                q.bi = 0.0; q.Di = 1.0; q.xt = 0.0; q.xpi = 0.0; q.qxp = 0.0;
-                if (q.row >= 0) {
-                    q.bi = ajm_ldp(p.b + q.row, vpol);
-                    q.Di = ajm_ldp(p.D + q.row, vpol);
-                    q.xt = ajm_ld(xc + q.row);
-                    q.xpi = ajm_ld(xp + q.row);
-                    q.qxp = ajm_ldp(p.Qxp + q.row, vpol);
-                }
-            };
-            auto finish = [&](const AjmPend& q, double dot) {
-                if (q.row >= 0)
-                    ajm_row_update(p.Qxp, xf, q.row, dot, q.bi, q.Di, q.xt, q.xpi, q.qxp, beta, restart_t, acc, vpol);
-            };
+            int jc = warp;
             for (int uu = 0; uu < nunits; ++uu) {
-                if (have && uu - have_u >= kStages - 1) {  // look-ahead limit: run the pending chunk alone
-                    finish(pa, ajm_chunk_dot(s_val + pa.off, s_col + pa.off, pa.w, xc));
-                    have = false;
-                    release_to(uu);
-                }
-                const bool mine = jc < s_uc0[uu + 1];
-                AjmPend pb;
-                if (mine) load_pend(pb, jc, uu);  // operands in flight during the wait
-                ajm_mbar_wait(&s_full[(int)((ucnt + uu) % kStages)], (unsigned)(((ucnt + uu) / kStages) & 1),
-                              &c->timeout_flag);
-                if (mine) {
+                const int stage = (int)((ucnt + uu) % kStages);
+                const unsigned par = (unsigned)(((ucnt + uu) / kStages) & 1);
+                if (jc < s_uc0[uu + 1]) {
+                    const int j = jc;
                     jc += AJM_WARPS;
-                    if (have) {
-                        double qa, qb;
-                        ajm_chunk_dot2(s_val + pa.off, s_col + pa.off, pa.w, s_val + pb.off, s_col + pb.off, pb.w,
-                                       xc, qa, qb);
-                        finish(pa, qa);
-                        finish(pb, qb);
-                        have = false;
-                        release_to(uu + 1);
+                    const int e0 = s_coff[j];
+                    const int w = (s_coff[j + 1] - e0) >> 5;
+                    const int slot = (cfirst + j) * 32 + lane;
+                    int row;
+                    double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
+                    if (vstage) {
+                        row = slot < p.n_sell ? slot : -1;
                     } else {
-                        pa = pb;
-                        have = true;
-                        have_u = uu;
+                        row = __ldg(p.perm + slot);
+                        if (row >= 0) {  // operands in flight during the stage wait
+                            bi = ajm_ldp(p.b + row, vpol);
+                            Di = ajm_ldp(p.D + row, vpol);
+                            xt = ajm_ld(xc + row);
+                            xpi = ajm_ld(xp + row);
+                            qxp = ajm_ldp(p.Qxp + row, vpol);
+                        }
                     }
-                } else if (!have) {
-                    release_to(uu + 1);
+                    ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);
+                    if (vstage) {
+                        const int ri = (j - s_uc0[uu]) * 32 + lane;
+                        bi = st_vec(stage, 0)[ri];
+                        Di = st_vec(stage, 1)[ri];
+                        xt = st_vec(stage, 2)[ri];
+                        xpi = st_vec(stage, 3)[ri];
+                        qxp = st_vec(stage, 4)[ri];
+                    }
+                    const int off = (e0 - s_coff[s_uc0[uu]]) + lane;
+                    const double q = ajm_chunk_dot(st_val(stage) + off, st_col(stage) + off, w, xc);
+                    if (row >= 0) ajm_row_update(p.Qxp, xf, row, q, bi, Di, xt, xpi, qxp, beta, restart_t, acc, vpol);
+                } else {
+                    ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);  // keep the phases in step
                 }
+                __syncwarp();
+                if (lane == 0) ajm_mbar_arrive(&s_empty[stage]);
             }
-            if (have) finish(pa, ajm_chunk_dot(s_val + pa.off, s_col + pa.off, pa.w, xc));
-            release_to(nunits);
             ucnt += nunits;
         }
         // (3) split rows owned by this CTA: wait for all segments of this pass, sum in order
@@ -653,12 +639,18 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
             s_tot[0] = tt.rr; s_tot[1] = tt.xq; s_tot[2] = tt.bx; s_tot[3] = tt.d; s_tot[4] = tt.dabs;
             ajm_control_step(s_st, s_tot, c, bid == 0);
             if (ajm_ld_acquire(&c->timeout_flag)) s_st.done = 1;
-            s_consumed = ucnt;
+            if (!s_st.done) {  // the next pass may stage its dynamic vectors now
+                s_bufc = s_st.cur;
+                s_bufp = s_st.prev;
+                __threadfence_block();
+                s_pass = pass + 1;
+            }
         }
         ajm_csync();
     }
     if (tid == 0) {
-        s_consumed = ucnt;
+        __threadfence_block();
+        s_pass = pass;  // units of passes >= pass were never consumed
         __threadfence_block();
         s_stop = 1;
         if (bid == 0) c->s = s_st;
