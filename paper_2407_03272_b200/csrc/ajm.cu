@@ -41,10 +41,10 @@ struct SolveVariant {
 // TMA ring depth x register cap (=> resident CTAs per SM with 288 threads); AJM_KVARIANT selects
 // one (tuning); the default is the measured best on B200
 const SolveVariant kVariants[] = {
-    {ajm_solve_kernel<3, 112>, 3, "s3r112"},  // 2 CTAs/SM
-    {ajm_solve_kernel<2, 72>, 2, "s2r72"},    // 3 CTAs/SM
+    {ajm_solve_kernel<4, 112>, 4, "s4r112"},  // 2 CTAs/SM
+    {ajm_solve_kernel<3, 72>, 3, "s3r72"},    // 3 CTAs/SM
+    {ajm_solve_kernel<2, 56>, 2, "s2r56"},    // 4 CTAs/SM
     {ajm_solve_kernel<6, 128>, 6, "s6r128"},  // 1 CTA/SM, deep ring
-    {ajm_solve_kernel<4, 112>, 4, "s4r112"},  // 1-2 CTAs/SM (shared-memory bound)
 };
 const int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -65,6 +65,7 @@ struct ajm_ctx {
     int64_t nunits = 0;
     int meta_units = 0, meta_chunks = 0;
     int l2_mode = 2;
+    int vstage = 0;
     int grid = 0;
     uint32_t flags = 0;
     // device arrays
@@ -204,6 +205,7 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.meta_units = h->meta_units;
     p.meta_chunks = h->meta_chunks;
     p.l2_mode = h->l2_mode;
+    p.vstage = h->vstage;
     return p;
 }
 
@@ -284,6 +286,8 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     if (const char* ev = getenv("AJM_KVARIANT")) h->variant = std::max(0, std::min(kNumVariants - 1, atoi(ev)));
     h->fn = kVariants[h->variant].fn;
     if (const char* ev = getenv("AJM_L2MODE")) h->l2_mode = std::max(0, std::min(2, atoi(ev)));
+    if (const char* ev = getenv("AJM_VSTAGE")) h->vstage = atoi(ev) ? 1 : 0;
+    CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
 
     // ---- row-length-binned layout (host, O(n log sigma)) ----
     auto rlen = [&](int64_t r) { return hrp[(size_t)r + 1] - hrp[(size_t)r]; };
@@ -422,9 +426,10 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             h->meta_units = (mu + 3) & ~3;
             h->meta_chunks = (mc + 3) & ~3;
         };
+        if (!h->ident) h->vstage = 0;
         // ring: val/col of a unit (+ the rows' five vector slices for natural-order layouts)
         const size_t ring = (size_t)kVariants[h->variant].stages *
-                            ((size_t)AJM_UNIT_EL * 12 + (h->ident ? (size_t)5 * AJM_UNIT_ROWS * 8 : 0));
+                            ((size_t)AJM_UNIT_EL * 12 + (h->vstage ? (size_t)5 * AJM_UNIT_ROWS * 8 : 0));
         size_t meta = 4096;  // initial allowance, grown until the plan fits
         for (int iter = 0;; ++iter) {
             h->dyn_smem = ring + meta;

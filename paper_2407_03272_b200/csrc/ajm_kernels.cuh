@@ -114,6 +114,7 @@ struct AjmPass {
     int meta_units;                          // smem capacity for a CTA's unit table (+1)
     int meta_chunks;                         // smem capacity for a CTA's chunk offsets (+1)
     int l2_mode;                             // 0 none, 1 Q evict_first, 2 + vectors evict_last
+    int vstage;                              // stage the rows' vector slices too (needs ident)
 };
 
 __device__ __forceinline__ double ajm_warp_sum(double v) {
@@ -425,7 +426,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     const unsigned G = gridDim.x;
     const int u0 = p.cta_unit[bid], u1 = p.cta_unit[bid + 1];
     const int nunits = u1 - u0;
-    const bool vstage = p.ident != 0;  // natural order: the unit's rows are contiguous
+    const bool vstage = p.vstage != 0;  // natural order only: the unit's rows are contiguous
     // stage s: val[UNIT_EL] f64 | col[UNIT_EL] i32 | (vstage) b, D, x~, x^{t-1}, Qx^{t-1} [256] f64
     const size_t stage_bytes = (size_t)AJM_UNIT_EL * 12 + (vstage ? (size_t)5 * AJM_UNIT_ROWS * 8 : 0);
     auto st_val = [&](int k) { return reinterpret_cast<double*>(s_dyn + (size_t)k * stage_bytes); };

@@ -7,6 +7,7 @@ import synth, paper_2407_03272_b200 as ajm
 cfgs = [int(c) for c in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["1", "2"])]
 variants = [int(v) for v in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["0"])]
 l2modes = [int(v) for v in (sys.argv[3].split(",") if len(sys.argv) > 3 else ["2"])]
+os.environ["AJM_VSTAGE"] = sys.argv[4] if len(sys.argv) > 4 else "0"
 variants = [(v, m) for v in variants for m in l2modes]
 for cfg in cfgs:
     t0 = time.time(); p = synth.config_problem(cfg); tg = time.time() - t0
