@@ -20,6 +20,8 @@ __all__ = ["AjmError", "Result", "Solver", "ajm_create", "ajm_solve", "ajm_destr
            "LIB_PATH", "STATUS_NAMES", "TERM_NAMES", "D_MODES", "model_bytes_per_iter"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libajm.so")
+if os.environ.get("AJM_LIB_OVERRIDE"):  # A/B experiments against another build of the same ABI
+    LIB_PATH = os.environ["AJM_LIB_OVERRIDE"]
 
 STATUS_NAMES = {0: "AJM_OK", 1: "AJM_ERR_INVALID_ARG", 2: "AJM_ERR_CSR_INVALID",
                 3: "AJM_ERR_NOT_SYMMETRIC", 4: "AJM_ERR_NONFINITE", 5: "AJM_ERR_NEGATIVE_DIAG",

@@ -409,7 +409,7 @@ __device__ __forceinline__ double ajm_chunk_dot(const double* sv, const int* sc,
 //   dynamic part -- (natural-order layouts) the rows' x~^t, x^{t-1}, Q x^{t-1} slices; issued
 //                   only once the pass that owns the unit has started (after the grid barrier).
 // A stage's full barrier completes when both parts have landed.
-template <int kStages, int kMaxReg>
+template <int kStages, int kMaxReg, bool kVStage>
 __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     extern __shared__ __align__(128) unsigned char s_dyn[];
     __shared__ double s_red[AJM_WARPS][AJM_NPART];
@@ -426,7 +426,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     const unsigned G = gridDim.x;
     const int u0 = p.cta_unit[bid], u1 = p.cta_unit[bid + 1];
     const int nunits = u1 - u0;
-    const bool vstage = p.vstage != 0;  // natural order only: the unit's rows are contiguous
+    constexpr bool vstage = kVStage;  // natural order only: the unit's rows are contiguous
     // stage s: val[UNIT_EL] f64 | col[UNIT_EL] i32 | (vstage) b, D, x~, x^{t-1}, Qx^{t-1} [256] f64
     const size_t stage_bytes = (size_t)AJM_UNIT_EL * 12 + (vstage ? (size_t)5 * AJM_UNIT_ROWS * 8 : 0);
     auto st_val = [&](int k) { return reinterpret_cast<double*>(s_dyn + (size_t)k * stage_bytes); };
