@@ -572,7 +572,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                     if (vstage) {
                         row = slot < p.n_sell ? slot : -1;
                     } else {
-                        row = __ldg(p.perm + slot);
+                        row = p.ident ? (slot < p.n_sell ? slot : -1) : __ldg(p.perm + slot);
                         if (row >= 0) {  // operands in flight during the stage wait
                             bi = ajm_ldp(p.b + row, vpol);
                             Di = ajm_ldp(p.D + row, vpol);
