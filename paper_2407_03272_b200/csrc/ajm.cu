@@ -376,32 +376,17 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     // ---- TMA staging units, persistent grid, cost-balanced CTA ranges ----
     std::vector<int> unit_c0_h, cta_seg_h, cta_unit_h, cta_split_h, owner_split_h;
     {
-        // units: consecutive chunks, <= AJM_WARPS chunks and <= AJM_UNIT_EL elements each
-        std::vector<double> ucost;
-        int64_t c = 0;
-        while (c < h->nchunks) {
-            unit_c0_h.push_back((int)c);
-            double cost = 0.0;
-            int64_t k = 0;
-            while (c < h->nchunks && k < AJM_WARPS &&
-                   choff[(size_t)c + 1] - choff[(size_t)unit_c0_h.back()] <= AJM_UNIT_EL) {
-                cost += chcost[(size_t)c];
-                ++c;
-                ++k;
-            }
-            ucost.push_back(cost);
-        }
-        unit_c0_h.push_back((int)h->nchunks);
-        h->nunits = (int64_t)ucost.size();
-        const int64_t nitems = h->nseg + h->nunits;
+        // one item sequence: segments (split rows first), then SELL chunks; contiguous CTA ranges
+        // balanced by cost at chunk granularity; each CTA's chunks are then grouped into TMA
+        // staging units of <= AJM_WARPS chunks and <= AJM_UNIT_EL elements
+        const int64_t nitems = h->nseg + h->nchunks;
         std::vector<double> cost;
         cost.reserve((size_t)nitems);
         for (int64_t s2 = 0; s2 < h->nseg; ++s2)
             cost.push_back(12.0 * (seg_k1_h[(size_t)s2] - seg_k0_h[(size_t)s2]) + 56.0 + 256.0);
-        for (double x : ucost) cost.push_back(x);
+        for (int64_t c2 = 0; c2 < h->nchunks; ++c2) cost.push_back(chcost[(size_t)c2]);
         double total = 0.0;
         for (double x : cost) total += x;
-        // one sequence: segments (split rows first), then units; contiguous CTA ranges by cost
         auto plan = [&](int G) {
             const double target = total / (double)G;
             std::vector<int64_t> start((size_t)G + 1, nitems);
@@ -416,16 +401,29 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             start[(size_t)G] = nitems;
             cta_seg_h.assign((size_t)G + 1, 0);
             cta_unit_h.assign((size_t)G + 1, 0);
-            for (int cc = 0; cc <= G; ++cc) {
-                cta_seg_h[(size_t)cc] = (int)std::min<int64_t>(start[(size_t)cc], h->nseg);
-                cta_unit_h[(size_t)cc] = (int)std::max<int64_t>(start[(size_t)cc] - h->nseg, 0);
-            }
+            unit_c0_h.clear();
             int mu = 1, mc = 1;
+            for (int cc = 0; cc <= G; ++cc) cta_seg_h[(size_t)cc] = (int)std::min<int64_t>(start[(size_t)cc], h->nseg);
             for (int cc = 0; cc < G; ++cc) {
-                const int ua = cta_unit_h[(size_t)cc], ub = cta_unit_h[(size_t)cc + 1];
-                mu = std::max(mu, ub - ua + 1);
-                if (ub > ua) mc = std::max(mc, unit_c0_h[(size_t)ub] - unit_c0_h[(size_t)ua] + 1);
+                cta_unit_h[(size_t)cc] = (int)unit_c0_h.size();
+                const int64_t c0 = std::max<int64_t>(start[(size_t)cc] - h->nseg, 0);
+                const int64_t c1 = std::max<int64_t>(start[(size_t)cc + 1] - h->nseg, 0);
+                int64_t c2 = c0;
+                while (c2 < c1) {
+                    const int64_t ub = c2;
+                    unit_c0_h.push_back((int)ub);
+                    int64_t k = 0;
+                    while (c2 < c1 && k < AJM_WARPS && choff[(size_t)c2 + 1] - choff[(size_t)ub] <= AJM_UNIT_EL) {
+                        ++c2;
+                        ++k;
+                    }
+                }
+                mu = std::max(mu, (int)(unit_c0_h.size() - cta_unit_h[(size_t)cc]) + 1);
+                mc = std::max(mc, (int)(c1 - c0) + 1);
             }
+            cta_unit_h[(size_t)G] = (int)unit_c0_h.size();
+            unit_c0_h.push_back((int)h->nchunks);
+            h->nunits = (int64_t)unit_c0_h.size() - 1;
             h->meta_units = (mu + 3) & ~3;
             h->meta_chunks = (mc + 3) & ~3;
         };

@@ -10,7 +10,13 @@ l2modes = [int(v) for v in (sys.argv[3].split(",") if len(sys.argv) > 3 else ["2
 os.environ["AJM_VSTAGE"] = sys.argv[4] if len(sys.argv) > 4 else "0"
 variants = [(v, m) for v in variants for m in l2modes]
 for cfg in cfgs:
-    t0 = time.time(); p = synth.config_problem(cfg); tg = time.time() - t0
+    t0 = time.time()
+    if cfg == 0:  # per-pass fixed-overhead probe: diagonal matrix, one 1-wide chunk per warp
+        d = 1.0 + (np.arange(148 * 2 * 8 * 32) % 7)
+        p = synth.make_problem("diag", synth.diag_matrix(d), 7)
+    else:
+        p = synth.config_problem(cfg)
+    tg = time.time() - t0
     for var, l2m in variants:
         os.environ["AJM_KVARIANT"] = str(var)
         os.environ["AJM_L2MODE"] = str(l2m)
