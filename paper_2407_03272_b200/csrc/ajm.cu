@@ -34,19 +34,20 @@ thread_local std::string g_create_error;
 
 typedef void (*SolveFn)(AjmPass);
 struct SolveVariant {
-    SolveFn fn;   // plain ring (val/col)
+    SolveFn fn;   // plain ring (val/col), natural-order layouts
     int stages;
     SolveFn fnv;  // ring that also stages the rows' vector slices (natural-order layouts)
     int vstages;
+    SolveFn fnd;  // no ring: SELL read directly (sorted-window layouts)
     const char* name;
 };
 // TMA ring depth x register cap (=> resident CTAs per SM with 288 threads); AJM_KVARIANT selects
 // one (tuning); the default is the measured best on B200
 const SolveVariant kVariants[] = {
-    {ajm_solve_kernel<4, 96, false>, 4, ajm_solve_kernel<3, 96, true>, 3, "s4r96"},    // 2 CTAs/SM
-    {ajm_solve_kernel<3, 72, false>, 3, ajm_solve_kernel<2, 72, true>, 2, "s3r72"},    // 3 CTAs/SM
-    {ajm_solve_kernel<2, 56, false>, 2, ajm_solve_kernel<2, 56, true>, 2, "s2r56"},    // 4 CTAs/SM
-    {ajm_solve_kernel<6, 128, false>, 6, ajm_solve_kernel<6, 128, true>, 6, "s6r128"}, // 1 CTA/SM
+    {ajm_solve_kernel<4, 96, 0>, 4, ajm_solve_kernel<3, 96, 1>, 3, ajm_solve_kernel<1, 96, 2>, "s4r96"},     // 2 CTAs/SM
+    {ajm_solve_kernel<3, 72, 0>, 3, ajm_solve_kernel<2, 72, 1>, 2, ajm_solve_kernel<1, 72, 2>, "s3r72"},     // 3 CTAs/SM
+    {ajm_solve_kernel<2, 56, 0>, 2, ajm_solve_kernel<2, 56, 1>, 2, ajm_solve_kernel<1, 56, 2>, "s2r56"},     // 4 CTAs/SM
+    {ajm_solve_kernel<6, 128, 0>, 6, ajm_solve_kernel<6, 128, 1>, 6, ajm_solve_kernel<1, 128, 2>, "s6r128"}, // 1 CTA/SM
 };
 const int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -68,6 +69,7 @@ struct ajm_ctx {
     int meta_units = 0, meta_chunks = 0;
     int l2_mode = 2;
     int vstage = 0;
+    int direct = 0;
     int grid = 0;
     uint32_t flags = 0;
     // device arrays
@@ -291,6 +293,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     if (const char* ev = getenv("AJM_VSTAGE")) h->vstage = atoi(ev) ? 1 : 0;
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fnv, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fnd, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
 
     // ---- row-length-binned layout (host, O(n log sigma)) ----
     auto rlen = [&](int64_t r) { return hrp[(size_t)r + 1] - hrp[(size_t)r]; };
@@ -428,9 +431,15 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             h->meta_chunks = (mc + 3) & ~3;
         };
         if (!h->ident) h->vstage = 0;
+        h->direct = (h->sigma > 1) ? 1 : 0;
+        if (const char* ev = getenv("AJM_DIRECT")) h->direct = atoi(ev) ? 1 : 0;
         if (h->vstage) h->fn = kVariants[h->variant].fnv;
+        if (h->direct) {
+            h->fn = kVariants[h->variant].fnd;
+            h->vstage = 0;
+        }
         // ring: val/col of a unit (+ the rows' five vector slices for natural-order layouts)
-        const size_t ring = (size_t)(h->vstage ? kVariants[h->variant].vstages : kVariants[h->variant].stages) *
+        const size_t ring = h->direct ? 0 : (size_t)(h->vstage ? kVariants[h->variant].vstages : kVariants[h->variant].stages) *
                             ((size_t)AJM_UNIT_EL * 12 + (h->vstage ? (size_t)5 * AJM_UNIT_ROWS * 8 : 0));
         size_t meta = 4096;  // initial allowance, grown until the plan fits
         for (int iter = 0;; ++iter) {

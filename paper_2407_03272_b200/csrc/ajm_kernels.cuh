@@ -401,6 +401,44 @@ __device__ __forceinline__ double ajm_chunk_dot(const double* sv, const int* sc,
     return s;
 }
 
+// A SELL chunk read directly from global memory (no staging): used for sorted-window layouts,
+// whose variable chunk widths make the shared-memory units small.
+__device__ __forceinline__ void ajm_chunk_direct(const AjmPass& p, int ch, int w, long long base, int lane,
+                                                 double beta, int restart_t, const double* xc,
+                                                 const double* xp, double* xf, AjmAcc& acc, uint64_t vpol) {
+    const int slot = ch * 32 + lane;
+    const int row = p.ident ? (slot < p.n_sell ? slot : -1) : __ldg(p.perm + slot);
+    double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
+    if (row >= 0) {
+        bi = ajm_ldp(p.b + row, vpol);
+        Di = ajm_ldp(p.D + row, vpol);
+        xt = ajm_ld(xc + row);
+        xpi = ajm_ld(xp + row);
+        qxp = ajm_ldp(p.Qxp + row, vpol);
+    }
+    const double* __restrict__ sv = p.sval + base + lane;
+    const int* __restrict__ sc = p.scol + base + lane;
+    double s = 0.0;
+    for (int k0 = 0; k0 < w; k0 += 8) {
+        double v[8], xg[8];
+        int cc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (k0 + j < w) {
+                v[j] = __ldcs(sv + (size_t)(k0 + j) * 32);
+                cc[j] = __ldcs(sc + (size_t)(k0 + j) * 32);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (k0 + j < w) xg[j] = ajm_ld(xc + cc[j]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (k0 + j < w) s += v[j] * xg[j];  // ascending column order
+    }
+    if (row >= 0) ajm_row_update(p.Qxp, xf, row, s, bi, Di, xt, xpi, qxp, beta, restart_t, acc, vpol);
+}
+
 // The persistent solver kernel (cooperative launch; grid = resident CTAs).  AJM_BLOCK consumer
 // threads + one producer warp.  The producer streams this CTA's SELL units into a kStages-deep
 // shared-memory ring with cp.async.bulk (TMA engine, mbarrier complete_tx):
@@ -409,7 +447,9 @@ __device__ __forceinline__ double ajm_chunk_dot(const double* sv, const int* sc,
 //   dynamic part -- (natural-order layouts) the rows' x~^t, x^{t-1}, Q x^{t-1} slices; issued
 //                   only once the pass that owns the unit has started (after the grid barrier).
 // A stage's full barrier completes when both parts have landed.
-template <int kStages, int kMaxReg, bool kVStage>
+// kMode: 0 TMA ring of val/col; 1 ring + the rows' vector slices (natural order only);
+//        2 no ring, SELL read directly by the consumer warps (sorted-window layouts).
+template <int kStages, int kMaxReg, int kMode>
 __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     extern __shared__ __align__(128) unsigned char s_dyn[];
     __shared__ double s_red[AJM_WARPS][AJM_NPART];
@@ -426,7 +466,8 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     const unsigned G = gridDim.x;
     const int u0 = p.cta_unit[bid], u1 = p.cta_unit[bid + 1];
     const int nunits = u1 - u0;
-    constexpr bool vstage = kVStage;  // natural order only: the unit's rows are contiguous
+    constexpr bool vstage = (kMode == 1);  // natural order only: the unit's rows are contiguous
+    constexpr bool direct = (kMode == 2);
     // stage s: val[UNIT_EL] f64 | col[UNIT_EL] i32 | (vstage) b, D, x~, x^{t-1}, Qx^{t-1} [256] f64
     const size_t stage_bytes = (size_t)AJM_UNIT_EL * 12 + (vstage ? (size_t)5 * AJM_UNIT_ROWS * 8 : 0);
     auto st_val = [&](int k) { return reinterpret_cast<double*>(s_dyn + (size_t)k * stage_bytes); };
@@ -437,7 +478,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     };
     // static per-CTA SELL metadata, loaded once: unit -> first chunk, chunk -> element offset
     // (relative to this CTA's first chunk / element), so the pass never chases global pointers
-    int* s_uc0 = reinterpret_cast<int*>(s_dyn + (size_t)kStages * stage_bytes);
+    int* s_uc0 = reinterpret_cast<int*>(s_dyn + (direct ? (size_t)0 : (size_t)kStages * stage_bytes));
     int* s_coff = s_uc0 + p.meta_units;
     const int cfirst = nunits > 0 ? p.unit_c0[u0] : 0;
     const int nchk = nunits > 0 ? p.unit_c0[u1] - cfirst : 0;
@@ -460,7 +501,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
 
     if (warp == AJM_WARPS) {
         // ---------------- producer warp (one lane) ----------------
-        if (lane == 0 && nunits > 0) {
+        if (!direct && lane == 0 && nunits > 0) {
             const uint64_t qpol = ajm_policy(p.l2_mode >= 1 ? 1 : 0);
             const uint64_t vpol = ajm_policy(p.l2_mode >= 2 ? 2 : 0);
             const long long total = (long long)nunits * p.max_passes;
@@ -554,6 +595,14 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                 }
             }
         }
+        if (direct) {
+            // (2') SELL chunks straight from global memory; chunk j of the CTA -> warp j % 8
+            for (int j = warp; j < nchk; j += AJM_WARPS) {
+                const int e0 = s_coff[j];
+                ajm_chunk_direct(p, cfirst + j, (s_coff[j + 1] - e0) >> 5, efirst + e0, lane, beta, restart_t,
+                                 xc, xp, xf, acc, vpol);
+            }
+        } else
         // (2) SELL units from the ring; chunk j of the CTA -> warp j % AJM_WARPS (at most one
         //     chunk per unit per warp)
         {

@@ -11,9 +11,9 @@ os.environ["AJM_VSTAGE"] = sys.argv[4] if len(sys.argv) > 4 else "0"
 variants = [(v, m) for v in variants for m in l2modes]
 for cfg in cfgs:
     t0 = time.time()
-    if cfg == 0:  # per-pass fixed-overhead probe: diagonal matrix, one 1-wide chunk per warp
-        d = 1.0 + (np.arange(148 * 2 * 8 * 32) % 7)
-        p = synth.make_problem("diag", synth.diag_matrix(d), 7)
+    if cfg == 0:  # per-pass fixed-overhead probe: 1D Laplacian + I, one 3-wide chunk per warp
+        Q = synth._stencil(148 * 2 * 8 * 32, 1, [((1,), -1.0), ((-1,), -1.0)], "const", 3.0)
+        p = synth.make_problem("tridiag", Q, 7)
     else:
         p = synth.config_problem(cfg)
     tg = time.time() - t0
