@@ -68,8 +68,7 @@ struct AjmCtrl {
     double* f_hist;
     double* d_hist;
     double* dabs_hist;
-    unsigned int bar_count;        // grid barrier
-    unsigned int bar_gen;
+    unsigned long long bar_count;  // grid barrier: monotone arrival counter (reset per solve)
     unsigned int timeout_flag;     // set if a barrier/arrival wait timed out (never expected)
     unsigned int pad;
     long long restart_log[AJM_LOG_CAP];
@@ -291,32 +290,37 @@ __device__ void ajm_control_step(AjmState& s, const double* tot, AjmCtrl* c, boo
     s.t = tn;
 }
 
-// Sense-reversing-free generation barrier over all CTAs of the cooperative launch.  Release:
-// __threadfence before the arrival; acquire: ld.acquire on the generation, then a gpu-scope fence
-// (invalidates this SM's L1 so data written by other SMs this pass is re-read from L2).
-__device__ __forceinline__ void ajm_grid_barrier(AjmCtrl* c, unsigned nblocks) {
+// Grid barrier over all CTAs of the cooperative launch: a monotone 64-bit arrival counter (reset
+// per solve); pass t completes when it reaches (t+1)*G, so nobody has to reset or publish anything
+// (one atomic per CTA, no extra round trip for the last arriver).  Release: __threadfence before
+// the arrival; acquire: ld.acquire on the counter, then a gpu-scope fence (which also invalidates
+// this SM's L1, so data written by other SMs this pass is re-read from L2).
+__device__ __forceinline__ unsigned long long ajm_ld_acquire64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ bool ajm_grid_barrier(AjmCtrl* c, unsigned nblocks, long long t) {
     ajm_csync();
+    __shared__ int s_to;
     if (threadIdx.x == 0) {
-        const unsigned g = ajm_ld_acquire(&c->bar_gen);
+        s_to = 0;
+        const unsigned long long target = (unsigned long long)(t + 1) * nblocks;
         __threadfence();
-        const unsigned arrived = atomicAdd(&c->bar_count, 1u);
-        if (arrived == nblocks - 1) {
-            atomicExch(&c->bar_count, 0u);
-            __threadfence();
-            atomicAdd(&c->bar_gen, 1u);
-        } else {
-            long long spins = 0;
-            while (ajm_ld_acquire(&c->bar_gen) == g) {
-                __nanosleep(20);
-                if (++spins > (1LL << 28)) {  // ~ seconds: never expected; fail loudly, do not hang
-                    atomicExch(&c->timeout_flag, 1u);
-                    break;
-                }
+        atomicAdd(&c->bar_count, 1ull);
+        long long spins = 0;
+        while (ajm_ld_acquire64(&c->bar_count) < target) {
+            __nanosleep(16);
+            if (++spins > (1LL << 27)) {  // ~ seconds: never expected; fail loudly, do not hang
+                atomicExch(&c->timeout_flag, 1u);
+                s_to = 1;
+                break;
             }
         }
         __threadfence();
     }
     ajm_csync();
+    return s_to != 0;
 }
 
 // warp-level dot of a CSR segment [k0, k1) against x (lane-strided, 8 loads in flight per lane)
@@ -674,7 +678,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
             double* dst = part + (size_t)bid * AJM_NPART;
             dst[0] = acc.rr; dst[1] = acc.xq; dst[2] = acc.bx; dst[3] = acc.d; dst[4] = acc.dabs;
         }
-        ajm_grid_barrier(c, G);
+        const bool timed_out = ajm_grid_barrier(c, G, t);
         AjmAcc tt = {0.0, 0.0, 0.0, 0.0, 0.0};
         for (int k = tid; k < (int)G; k += AJM_BLOCK) {
             const double* src = part + (size_t)k * AJM_NPART;
@@ -688,7 +692,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         if (tid == 0) {
             s_tot[0] = tt.rr; s_tot[1] = tt.xq; s_tot[2] = tt.bx; s_tot[3] = tt.d; s_tot[4] = tt.dabs;
             ajm_control_step(s_st, s_tot, c, bid == 0);
-            if (ajm_ld_acquire(&c->timeout_flag)) s_st.done = 1;
+            if (timed_out) s_st.done = 1;
             if (!s_st.done) {  // the next pass may stage its dynamic vectors now
                 s_bufc = s_st.cur;
                 s_bufp = s_st.prev;
@@ -864,8 +868,7 @@ __global__ void ajm_init_ctrl_kernel(AjmCtrl* c, double tol, long long maxit, in
     c->f_hist = f_hist;
     c->d_hist = d_hist;
     c->dabs_hist = dabs_hist;
-    c->bar_count = 0;
-    c->bar_gen = 0;
+    c->bar_count = 0ull;
     c->timeout_flag = 0;
     d_hist[0] = 0.0;
     dabs_hist[0] = 0.0;
