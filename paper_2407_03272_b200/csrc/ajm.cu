@@ -70,6 +70,7 @@ struct ajm_ctx {
     int l2_mode = 2;
     int vstage = 0;
     int direct = 0;
+    unsigned long long* ts = nullptr;  // debug phase timestamps (AJM_TS=1)
     int grid = 0;
     uint32_t flags = 0;
     // device arrays
@@ -164,7 +165,7 @@ void free_all(ajm_ctx* h) {
                     h->sval, h->scol, h->chunk_off, h->perm, h->seg_row, h->seg_k0, h->seg_k1,
                     h->seg_split, h->seg_part, h->split_row, h->split_seg0, h->split_cnt,
                     h->cta_split, h->owner_split, h->unit_c0, h->cta_seg, h->cta_unit, h->partials, h->ctrl,
-                    h->hist, h->scratch, h->err};
+                    h->hist, h->scratch, h->err, h->ts};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->h_ctrl) cudaFreeHost(h->h_ctrl);
@@ -210,6 +211,7 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.meta_chunks = h->meta_chunks;
     p.l2_mode = h->l2_mode;
     p.vstage = h->vstage;
+    p.ts = h->ts;
     return p;
 }
 
@@ -506,6 +508,10 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(dalloc(&h->ctrl, 1));
     CC(dalloc(&h->scratch, 512));
     CC(dalloc(&h->err, 1));
+    if (getenv("AJM_TS")) {
+        CC(dalloc(&h->ts, 64 * 8));
+        CC(cudaMemsetAsync(h->ts, 0, 64 * 8 * sizeof(unsigned long long), st));
+    }
     CC(cudaMallocHost((void**)&h->h_ctrl, sizeof(AjmCtrl)));
     CC(cudaEventCreate(&h->ev0));
     CC(cudaEventCreate(&h->ev1));
@@ -671,6 +677,22 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
     h->last_passes = c.s.iterations + 1;
     h->last_launches = launches;
     h->last_iterations = c.s.iterations;
+    if (h->ts) {  // debug: mean phase durations of CTA 0 over the first passes
+        unsigned long long hts[64 * 8];
+        AJM_CUDA(h, cudaMemcpy(hts, h->ts, sizeof(hts), cudaMemcpyDeviceToHost));
+        double acc[5] = {0, 0, 0, 0, 0};
+        int np = 0;
+        for (int k = 2; k < 64 && k + 1 <= c.s.iterations; ++k) {
+            if (!hts[k * 8 + 5] || !hts[(k + 1) * 8]) break;
+            for (int j = 0; j < 4; ++j) acc[j] += (double)(hts[k * 8 + j + 1] - hts[k * 8 + j]);
+            acc[4] += (double)(hts[(k + 1) * 8] - hts[k * 8 + 4]);
+            ++np;
+        }
+        if (np)
+            fprintf(stderr, "[ajm ts] passes %d: work %.2f us, block-reduce %.2f, grid-barrier %.2f, "
+                            "partials %.2f, control+sync %.2f\n", np, acc[0] / np / 1e3, acc[1] / np / 1e3,
+                    acc[2] / np / 1e3, acc[3] / np / 1e3, acc[4] / np / 1e3);
+    }
 
     AJM_CUDA(h, cudaMemcpyAsync(x_out, h->X[c.s.answer], sizeof(double) * n, kind_from_device(x_out), st));
     const int64_t cnt = c.s.iterations + 1;

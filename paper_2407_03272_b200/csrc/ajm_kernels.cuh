@@ -114,7 +114,14 @@ struct AjmPass {
     int meta_chunks;                         // smem capacity for a CTA's chunk offsets (+1)
     int l2_mode;                             // 0 none, 1 Q evict_first, 2 + vectors evict_last
     int vstage;                              // stage the rows' vector slices too (needs ident)
+    unsigned long long* ts;                  // debug: per-pass phase timestamps of CTA 0 (or null)
 };
+
+__device__ __forceinline__ unsigned long long ajm_gtime() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+    return v;
+}
 
 __device__ __forceinline__ double ajm_warp_sum(double v) {
     // xor butterfly: a + b == b + a in IEEE, so every lane ends with the same bits
@@ -583,6 +590,8 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         const double* xp = ajm_sel(p, s_st.prev);
         double* xf = ajm_sel(p, s_st.fre);
         AjmAcc acc = {0.0, 0.0, 0.0, 0.0, 0.0};
+        const bool tsw = p.ts && bid == 0 && tid == 0 && pass < 64;
+        if (tsw) p.ts[pass * 8 + 0] = ajm_gtime();
 
         // (1) row segments (direct loads), split-row segments first
         for (int sg = sg0 + warp; sg < sg1; sg += AJM_WARPS) {
@@ -672,13 +681,16 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
             }
         }
         // (4) CTA partial -> grid barrier -> every CTA reduces all partials in the same order
+        if (tsw) p.ts[pass * 8 + 1] = ajm_gtime();
         ajm_block_reduce(acc, s_red);
+        if (tsw) p.ts[pass * 8 + 2] = ajm_gtime();
         double* part = p.partials + (size_t)(t & 1) * G * AJM_NPART;
         if (tid == 0) {
             double* dst = part + (size_t)bid * AJM_NPART;
             dst[0] = acc.rr; dst[1] = acc.xq; dst[2] = acc.bx; dst[3] = acc.d; dst[4] = acc.dabs;
         }
         const bool timed_out = ajm_grid_barrier(c, G, t);
+        if (tsw) p.ts[pass * 8 + 3] = ajm_gtime();
         AjmAcc tt = {0.0, 0.0, 0.0, 0.0, 0.0};
         for (int k = tid; k < (int)G; k += AJM_BLOCK) {
             const double* src = part + (size_t)k * AJM_NPART;
@@ -689,10 +701,12 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
             tt.dabs += __ldcg(src + 4);
         }
         ajm_block_reduce(tt, s_red);
+        if (tsw) p.ts[pass * 8 + 4] = ajm_gtime();
         if (tid == 0) {
             s_tot[0] = tt.rr; s_tot[1] = tt.xq; s_tot[2] = tt.bx; s_tot[3] = tt.d; s_tot[4] = tt.dabs;
             ajm_control_step(s_st, s_tot, c, bid == 0);
             if (timed_out) s_st.done = 1;
+            if (tsw) p.ts[pass * 8 + 5] = ajm_gtime();
             if (!s_st.done) {  // the next pass may stage its dynamic vectors now
                 s_bufc = s_st.cur;
                 s_bufp = s_st.prev;
