@@ -682,7 +682,7 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
         AJM_CUDA(h, cudaMemcpy(hts, h->ts, sizeof(hts), cudaMemcpyDeviceToHost));
         double acc[5] = {0, 0, 0, 0, 0};
         int np = 0;
-        for (int k = 2; k < 64 && k + 1 <= c.s.iterations; ++k) {
+        for (int k = 2; k + 1 < 64 && k + 1 <= c.s.iterations; ++k) {
             if (!hts[k * 8 + 5] || !hts[(k + 1) * 8]) break;
             for (int j = 0; j < 4; ++j) acc[j] += (double)(hts[k * 8 + j + 1] - hts[k * 8 + j]);
             acc[4] += (double)(hts[(k + 1) * 8] - hts[k * 8 + 4]);

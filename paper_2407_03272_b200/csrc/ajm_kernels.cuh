@@ -229,7 +229,8 @@ __device__ __forceinline__ void ajm_block_reduce(AjmAcc& a, double (*s_red)[AJM_
 
 // a7 control step (thread 0 of every CTA, identical inputs -> identical outputs).  CTA 0 also
 // writes the histories and the restart log.
-__device__ void ajm_control_step(AjmState& s, const double* tot, AjmCtrl* c, bool writer) {
+__device__ void ajm_control_step(AjmState& s, const double* tot, AjmCtrl* c, bool writer, double an_c,
+                                 double beta_c) {
     const long long t = s.t;
     const double res = sqrt(tot[0]) / s.nb;
     const double f = 0.5 * tot[1] - tot[2];
@@ -278,10 +279,8 @@ __device__ void ajm_control_step(AjmState& s, const double* tot, AjmCtrl* c, boo
         s.alpha = 1.0;
         s.beta = 0.0;
     } else {   // lines 12-13: alpha_{t+1} = (1 + sqrt(1 + 4 alpha_t^2))/2, beta_t = (alpha_t - 1)/alpha_{t+1}
-        const double a = s.alpha;
-        const double an = (1.0 + sqrt(1.0 + 4.0 * a * a)) / 2.0;
-        s.beta = s.momentum ? (a - 1.0) / an : 0.0;
-        s.alpha = an;
+        s.beta = beta_c;  // computed from s.alpha before the barrier, same expression
+        s.alpha = an_c;
     }
     // rotate: x^t = x~^t unless iteration t restarted (then x^t = x^{t-1})
     const int cur = s.cur, prev = s.prev, fre = s.fre;
@@ -317,8 +316,7 @@ __device__ __forceinline__ bool ajm_grid_barrier(AjmCtrl* c, unsigned nblocks, l
         atomicAdd(&c->bar_count, 1ull);
         long long spins = 0;
         while (ajm_ld_acquire64(&c->bar_count) < target) {
-            __nanosleep(16);
-            if (++spins > (1LL << 27)) {  // ~ seconds: never expected; fail loudly, do not hang
+            if (++spins > (1LL << 30)) {  // ~ seconds: never expected; fail loudly, do not hang
                 atomicExch(&c->timeout_flag, 1u);
                 s_to = 1;
                 break;
@@ -684,27 +682,41 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         if (tsw) p.ts[pass * 8 + 1] = ajm_gtime();
         ajm_block_reduce(acc, s_red);
         if (tsw) p.ts[pass * 8 + 2] = ajm_gtime();
+        // partials as 5 arrays of G (SoA) so the all-CTA read below is coalesced
         double* part = p.partials + (size_t)(t & 1) * G * AJM_NPART;
+        double an_c = 0.0, beta_c = 0.0;
         if (tid == 0) {
-            double* dst = part + (size_t)bid * AJM_NPART;
-            dst[0] = acc.rr; dst[1] = acc.xq; dst[2] = acc.bx; dst[3] = acc.d; dst[4] = acc.dabs;
+            part[0 * G + bid] = acc.rr;
+            part[1 * G + bid] = acc.xq;
+            part[2 * G + bid] = acc.bx;
+            part[3 * G + bid] = acc.d;
+            part[4 * G + bid] = acc.dabs;
+            // the non-restart alpha/beta candidates do not depend on this pass: compute them while
+            // the barrier is pending (Alg. 3 line 13)
+            const double a = s_st.alpha;
+            an_c = (1.0 + sqrt(1.0 + 4.0 * a * a)) / 2.0;
+            beta_c = s_st.momentum ? (a - 1.0) / an_c : 0.0;
         }
         const bool timed_out = ajm_grid_barrier(c, G, t);
         if (tsw) p.ts[pass * 8 + 3] = ajm_gtime();
-        AjmAcc tt = {0.0, 0.0, 0.0, 0.0, 0.0};
-        for (int k = tid; k < (int)G; k += AJM_BLOCK) {
-            const double* src = part + (size_t)k * AJM_NPART;
-            tt.rr += __ldcg(src + 0);
-            tt.xq += __ldcg(src + 1);
-            tt.bx += __ldcg(src + 2);
-            tt.d += __ldcg(src + 3);
-            tt.dabs += __ldcg(src + 4);
+        if (warp == 0) {
+            // warp 0 reduces all CTA partials: lane l sums records l, l+32, ... in order, then a
+            // fixed xor tree (identical bits in every CTA)
+            double v[AJM_NPART] = {0.0, 0.0, 0.0, 0.0, 0.0};
+            for (int k = lane; k < (int)G; k += 32) {
+#pragma unroll
+                for (int j = 0; j < AJM_NPART; ++j) v[j] += __ldcg(part + (size_t)j * G + k);
+            }
+#pragma unroll
+            for (int j = 0; j < AJM_NPART; ++j) v[j] = ajm_warp_sum(v[j]);
+            if (lane == 0) {
+#pragma unroll
+                for (int j = 0; j < AJM_NPART; ++j) s_tot[j] = v[j];
+            }
         }
-        ajm_block_reduce(tt, s_red);
         if (tsw) p.ts[pass * 8 + 4] = ajm_gtime();
         if (tid == 0) {
-            s_tot[0] = tt.rr; s_tot[1] = tt.xq; s_tot[2] = tt.bx; s_tot[3] = tt.d; s_tot[4] = tt.dabs;
-            ajm_control_step(s_st, s_tot, c, bid == 0);
+            ajm_control_step(s_st, s_tot, c, bid == 0, an_c, beta_c);
             if (timed_out) s_st.done = 1;
             if (tsw) p.ts[pass * 8 + 5] = ajm_gtime();
             if (!s_st.done) {  // the next pass may stage its dynamic vectors now
