@@ -699,21 +699,23 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         }
         const bool timed_out = ajm_grid_barrier(c, G, t);
         if (tsw) p.ts[pass * 8 + 3] = ajm_gtime();
-        if (warp == 0) {
-            // warp 0 reduces all CTA partials: lane l sums records l, l+32, ... in order, then a
-            // fixed xor tree (identical bits in every CTA)
-            double v[AJM_NPART] = {0.0, 0.0, 0.0, 0.0, 0.0};
-            for (int k = lane; k < (int)G; k += 32) {
+        if (warp < AJM_NPART) {
+            // warp j reduces component j of all CTA partials: lane l sums records l, l+32, ... in
+            // order (8 loads in flight), then a fixed xor tree -- identical bits in every CTA
+            const double* src = part + (size_t)warp * G;
+            double v = 0.0;
+            for (int k0 = lane; k0 < (int)G; k0 += 8 * 32) {
+                double r[8];
 #pragma unroll
-                for (int j = 0; j < AJM_NPART; ++j) v[j] += __ldcg(part + (size_t)j * G + k);
+                for (int j = 0; j < 8; ++j) r[j] = (k0 + j * 32 < (int)G) ? __ldcg(src + k0 + j * 32) : 0.0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (k0 + j * 32 < (int)G) v += r[j];
             }
-#pragma unroll
-            for (int j = 0; j < AJM_NPART; ++j) v[j] = ajm_warp_sum(v[j]);
-            if (lane == 0) {
-#pragma unroll
-                for (int j = 0; j < AJM_NPART; ++j) s_tot[j] = v[j];
-            }
+            v = ajm_warp_sum(v);
+            if (lane == 0) s_tot[warp] = v;
         }
+        ajm_csync();
         if (tsw) p.ts[pass * 8 + 4] = ajm_gtime();
         if (tid == 0) {
             ajm_control_step(s_st, s_tot, c, bid == 0, an_c, beta_c);
