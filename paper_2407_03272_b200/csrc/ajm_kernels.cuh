@@ -212,7 +212,7 @@ __device__ __forceinline__ void ajm_block_reduce(AjmAcc& a, double (*s_red)[AJM_
     double v[AJM_NPART] = {a.rr, a.xq, a.bx, a.d, a.dabs};
 #pragma unroll
     for (int j = 0; j < AJM_NPART; ++j) v[j] = ajm_warp_sum(v[j]);
-    ajm_csync();  // s_red may still be read by a previous reduction
+    // (s_red was last read by thread 0 in the previous pass, several CTA barriers ago)
     if (lane == 0) {
 #pragma unroll
         for (int j = 0; j < AJM_NPART; ++j) s_red[warp][j] = v[j];
@@ -306,26 +306,27 @@ __device__ __forceinline__ unsigned long long ajm_ld_acquire64(const unsigned lo
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ bool ajm_grid_barrier(AjmCtrl* c, unsigned nblocks, long long t) {
-    ajm_csync();
-    __shared__ int s_to;
-    if (threadIdx.x == 0) {
-        s_to = 0;
-        const unsigned long long target = (unsigned long long)(t + 1) * nblocks;
-        __threadfence();
-        atomicAdd(&c->bar_count, 1ull);
-        long long spins = 0;
-        while (ajm_ld_acquire64(&c->bar_count) < target) {
-            if (++spins > (1LL << 30)) {  // ~ seconds: never expected; fail loudly, do not hang
-                atomicExch(&c->timeout_flag, 1u);
-                s_to = 1;
-                break;
-            }
+// Arrival (thread 0, right after ajm_block_reduce, whose CTA barrier already ordered every thread's
+// stores of this pass): a release-add orders them before the arrival without waiting for the
+// atomic's round trip.
+__device__ __forceinline__ void ajm_grid_arrive(AjmCtrl* c) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&c->bar_count) : "memory");
+}
+// Wait (thread 0) until pass t's arrivals reach (t+1)*G; the trailing gpu-scope fence also
+// invalidates this SM's L1.  Returns true on a (never expected) timeout.
+__device__ __forceinline__ bool ajm_grid_wait(AjmCtrl* c, unsigned nblocks, long long t) {
+    const unsigned long long target = (unsigned long long)(t + 1) * nblocks;
+    long long spins = 0;
+    bool to = false;
+    while (ajm_ld_acquire64(&c->bar_count) < target) {
+        if (++spins > (1LL << 30)) {  // ~ seconds: fail loudly, do not hang
+            atomicExch(&c->timeout_flag, 1u);
+            to = true;
+            break;
         }
-        __threadfence();
     }
-    ajm_csync();
-    return s_to != 0;
+    __threadfence();
+    return to;
 }
 
 // warp-level dot of a CSR segment [k0, k1) against x (lane-strided, 8 loads in flight per lane)
@@ -469,6 +470,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     __shared__ volatile int s_stop;
     __shared__ volatile int s_pass;     // passes (of this launch) whose dynamic vectors may be staged
     __shared__ volatile int s_bufc, s_bufp;  // x~^t / x^{t-1} buffer indices of pass s_pass
+    __shared__ int s_to;
 
     AjmCtrl* c = p.ctrl;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, bid = blockIdx.x;
@@ -691,13 +693,16 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
             part[2 * G + bid] = acc.bx;
             part[3 * G + bid] = acc.d;
             part[4 * G + bid] = acc.dabs;
+            ajm_grid_arrive(c);
             // the non-restart alpha/beta candidates do not depend on this pass: compute them while
             // the barrier is pending (Alg. 3 line 13)
             const double a = s_st.alpha;
             an_c = (1.0 + sqrt(1.0 + 4.0 * a * a)) / 2.0;
             beta_c = s_st.momentum ? (a - 1.0) / an_c : 0.0;
+            s_to = ajm_grid_wait(c, G, t) ? 1 : 0;
         }
-        const bool timed_out = ajm_grid_barrier(c, G, t);
+        ajm_csync();
+        const bool timed_out = s_to != 0;
         if (tsw) p.ts[pass * 8 + 3] = ajm_gtime();
         if (warp < AJM_NPART) {
             // warp j reduces component j of all CTA partials: lane l sums records l, l+32, ... in
