@@ -105,7 +105,11 @@ typedef struct {
     int64_t split_rows;       /* rows spanning several segments (finished by an owner CTA)     */
     int64_t sell_elems;       /* SELL entries including padding                                */
     int32_t sigma;            /* SELL sorting window (1 = natural order)                       */
-    int32_t variant;          /* kernel variant (SELL batch x min CTAs/SM)                      */
+    int32_t variant;          /* kernel variant (TMA ring depth x register cap)                 */
+    int64_t l2_window_bytes;  /* iterate vectors covered by the persisting-L2 access window     */
+    double l2_hit_ratio;      /* persisting fraction of that window                            */
+    int32_t mode;             /* 0 TMA ring, 1 ring + vector slices, 2 direct SELL loads       */
+    int32_t pad0;
 } ajm_info_t;
 
 /*

@@ -71,6 +71,10 @@ struct ajm_ctx {
     int vstage = 0;
     int direct = 0;
     unsigned long long* ts = nullptr;  // debug phase timestamps (AJM_TS=1)
+    double* vecs = nullptr;            // X0 X1 X2 Qxp b D, one allocation
+    int l2persist = 1;
+    size_t win_bytes = 0;
+    float win_hit = 0.f;
     int grid = 0;
     uint32_t flags = 0;
     // device arrays
@@ -161,7 +165,7 @@ cudaError_t dalloc(T** p, size_t count) {
 }
 
 void free_all(ajm_ctx* h) {
-    void* ptrs[] = {h->rp, h->col, h->val, h->b, h->D, h->X[0], h->X[1], h->X[2], h->Qxp,
+    void* ptrs[] = {h->rp, h->col, h->val, h->vecs,
                     h->sval, h->scol, h->chunk_off, h->perm, h->seg_row, h->seg_k0, h->seg_k1,
                     h->seg_split, h->seg_part, h->split_row, h->split_seg0, h->split_cnt,
                     h->cta_split, h->owner_split, h->unit_c0, h->cta_seg, h->cta_unit, h->partials, h->ctrl,
@@ -213,6 +217,32 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.vstage = h->vstage;
     p.ts = h->ts;
     return p;
+}
+
+// cooperative launch of the persistent solver kernel, with the L2 access-policy window over the
+// iterate vectors (persisting hits, streaming misses)
+cudaError_t launch_solver(ajm_ctx* h, AjmPass& p, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(h->grid);
+    cfg.blockDim = dim3(AJM_BLOCK + 32);
+    cfg.dynamicSmemBytes = h->dyn_smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    int na = 1;
+    if (h->win_bytes) {
+        at[1].id = cudaLaunchAttributeAccessPolicyWindow;
+        at[1].val.accessPolicyWindow.base_ptr = h->vecs;
+        at[1].val.accessPolicyWindow.num_bytes = h->win_bytes;
+        at[1].val.accessPolicyWindow.hitRatio = h->win_hit;
+        at[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        at[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        na = 2;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, h->fn, p);
 }
 
 ajm_status_t ensure_hist(ajm_ctx* h, int64_t need) {
@@ -293,6 +323,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     h->fn = kVariants[h->variant].fn;
     if (const char* ev = getenv("AJM_L2MODE")) h->l2_mode = std::max(0, std::min(2, atoi(ev)));
     if (const char* ev = getenv("AJM_VSTAGE")) h->vstage = atoi(ev) ? 1 : 0;
+    if (const char* ev = getenv("AJM_L2PERSIST")) h->l2persist = atoi(ev) ? 1 : 0;
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fnv, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fnd, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -478,15 +509,33 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(dalloc(&h->rp, n + 1));
     CC(dalloc(&h->col, nnz));
     CC(dalloc(&h->val, nnz));
-    // vectors padded to whole SELL chunks (the TMA stages copy whole 32-row slices)
-    h->n_pad = std::max<int64_t>(n, h->nchunks * 32);
-    CC(dalloc(&h->b, h->n_pad));
-    CC(dalloc(&h->D, h->n_pad));
-    for (int k = 0; k < 3; ++k) CC(dalloc(&h->X[k], h->n_pad));
-    CC(dalloc(&h->Qxp, h->n_pad));
-    CC(cudaMemsetAsync(h->b, 0, sizeof(double) * h->n_pad, st));
-    CC(cudaMemsetAsync(h->D, 0, sizeof(double) * h->n_pad, st));
-    for (int k = 0; k < 3; ++k) CC(cudaMemsetAsync(h->X[k], 0, sizeof(double) * h->n_pad, st));
+    // the six n-vectors in ONE allocation [X0 X1 X2 Qxp b D] (each padded to whole SELL chunks,
+    // 256-byte aligned): the L2 persistence window below covers them with a single range
+    h->n_pad = (std::max<int64_t>(n, h->nchunks * 32) + 31) / 32 * 32;
+    CC(dalloc(&h->vecs, (size_t)6 * h->n_pad));
+    CC(cudaMemsetAsync(h->vecs, 0, sizeof(double) * 6 * h->n_pad, st));
+    for (int k = 0; k < 3; ++k) h->X[k] = h->vecs + (size_t)k * h->n_pad;
+    h->Qxp = h->vecs + (size_t)3 * h->n_pad;
+    h->b = h->vecs + (size_t)4 * h->n_pad;
+    h->D = h->vecs + (size_t)5 * h->n_pad;
+    // L2 residency: keep as much of the iterate vectors as the device allows in a
+    // persisting L2 carve-out; the matrix stream goes through with evict_first hints
+    h->win_bytes = 0;
+    if (h->l2persist) {
+        int maxp = 0, maxw = 0;
+        CC(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device));
+        CC(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, h->device));
+        const size_t vec_bytes = sizeof(double) * 6 * (size_t)h->n_pad;
+        if (maxp > 0 && maxw > 0) {
+            size_t persist = std::min<size_t>((size_t)maxp, vec_bytes);
+            size_t cur = 0;
+            CC(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+            if (cur < persist) CC(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
+            CC(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+            h->win_bytes = std::min<size_t>(vec_bytes, (size_t)maxw);
+            h->win_hit = (float)std::min(1.0, (double)cur / (double)h->win_bytes);
+        }
+    }
     CC(dalloc(&h->sval, h->sell_elems));
     CC(dalloc(&h->scol, h->sell_elems));
     CC(dalloc(&h->chunk_off, h->nchunks + 1));
@@ -646,18 +695,15 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
     if (!(h->flags & AJM_LOOP_HOST)) {
         // the whole Alg. 3 loop: one cooperative launch
         AjmPass p = make_pass(h, (int)(maxit + 1));
-        void* args[] = {&p};
-        AJM_CUDA(h, cudaLaunchCooperativeKernel((const void*)h->fn, dim3(h->grid), dim3(AJM_BLOCK + 32), args, h->dyn_smem, st));
+        AJM_CUDA(h, launch_solver(h, p, st));
         launches = 1;
     } else {
         // debug host loop: one pass per launch, the control state round-trips through global memory
         AjmPass p = make_pass(h, 1);
-        void* args[] = {&p};
         int64_t issued = 0;
         for (;;) {
             const int64_t chunk = std::min<int64_t>(64, maxit + 1 - issued);
-            for (int64_t i = 0; i < chunk; ++i)
-                AJM_CUDA(h, cudaLaunchCooperativeKernel((const void*)h->fn, dim3(h->grid), dim3(AJM_BLOCK + 32), args, h->dyn_smem, st));
+            for (int64_t i = 0; i < chunk; ++i) AJM_CUDA(h, launch_solver(h, p, st));
             issued += chunk;
             AJM_CUDA(h, cudaMemcpyAsync(h->h_ctrl, h->ctrl, sizeof(AjmCtrl), cudaMemcpyDeviceToHost, st));
             AJM_CUDA(h, cudaStreamSynchronize(st));
@@ -749,6 +795,9 @@ ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info) {
     info->split_rows = h->nsplit;
     info->sigma = h->sigma;
     info->variant = h->variant;
+    info->l2_window_bytes = (int64_t)h->win_bytes;
+    info->l2_hit_ratio = h->win_hit;
+    info->mode = h->direct ? 2 : (h->vstage ? 1 : 0);
     info->sell_elems = h->sell_elems;
     return AJM_OK;
 }

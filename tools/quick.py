@@ -25,7 +25,7 @@ for cfg in cfgs:
             tc = time.time() - t0
             info = s.info()
             print(f"cfg{cfg} var{var} l2m{l2m} n={p.Q.n} nnz={p.Q.nnz} gen={tg:.1f}s create={tc:.2f}s grid={info['grid']} "
-                  f"occ={info['ctas_per_sm']} units={info['units']} sell={info['sell_rows']} seg={info['seg_rows']} split={info['split_rows']} sigma={info['sigma']} pad={info['sell_elems']}", flush=True)
+                  f"occ={info['ctas_per_sm']} mode={info['mode']} l2win={info['l2_window_bytes']/1e6:.0f}MB hit={info['l2_hit_ratio']:.2f} units={info['units']} sell={info['sell_rows']} seg={info['seg_rows']} split={info['split_rows']} sigma={info['sigma']} pad={info['sell_elems']}", flush=True)
             for rep in range(2):
                 r = s.solve(tol=1e-6, maxit=5000, restart=True)
                 info = s.info(); ms = info["last_loop_ms"]
