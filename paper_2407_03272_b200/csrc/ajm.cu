@@ -44,7 +44,7 @@ struct SolveVariant {
 // TMA ring depth x register cap (=> resident CTAs per SM with 288 threads); AJM_KVARIANT selects
 // one (tuning); the default is the measured best on B200
 const SolveVariant kVariants[] = {
-    {ajm_solve_kernel<4, 96, 0>, 4, ajm_solve_kernel<3, 96, 1>, 3, ajm_solve_kernel<1, 96, 2>, "s4r96"},     // 2 CTAs/SM
+    {ajm_solve_kernel<4, 96, 0>, 4, ajm_solve_kernel<3, 96, 1>, 3, ajm_solve_kernel<1, 128, 2>, "s4r96"},    // 2 CTAs/SM
     {ajm_solve_kernel<3, 72, 0>, 3, ajm_solve_kernel<2, 72, 1>, 2, ajm_solve_kernel<1, 72, 2>, "s3r72"},     // 3 CTAs/SM
     {ajm_solve_kernel<2, 56, 0>, 2, ajm_solve_kernel<2, 56, 1>, 2, ajm_solve_kernel<1, 56, 2>, "s2r56"},     // 4 CTAs/SM
     {ajm_solve_kernel<6, 128, 0>, 6, ajm_solve_kernel<6, 128, 1>, 6, ajm_solve_kernel<1, 128, 2>, "s6r128"}, // 1 CTA/SM
@@ -224,7 +224,7 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
 cudaError_t launch_solver(ajm_ctx* h, AjmPass& p, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(h->grid);
-    cfg.blockDim = dim3(AJM_BLOCK + 32);
+    cfg.blockDim = dim3(h->direct ? AJM_BLOCK : AJM_BLOCK + 32);  // direct mode: no producer warp
     cfg.dynamicSmemBytes = h->dyn_smem;
     cfg.stream = st;
     cudaLaunchAttribute at[2];
@@ -479,7 +479,8 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             h->dyn_smem = ring + meta;
             CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem));
             int occ = 0;
-            CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->fn, AJM_BLOCK + 32, h->dyn_smem));
+            CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->fn, h->direct ? AJM_BLOCK : AJM_BLOCK + 32,
+                                                             h->dyn_smem));
             if (occ < 1) return bail(fail(h, AJM_ERR_UNSUPPORTED, "solver kernel cannot be resident (%zu B smem)", h->dyn_smem));
             h->ctas_per_sm = occ;
             const int64_t g = (int64_t)h->sm_count * occ;
