@@ -216,6 +216,7 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.l2_mode = h->l2_mode;
     p.vstage = h->vstage;
     p.ts = h->ts;
+    p.direct_interleave = getenv("AJM_DIRECT_INTERLEAVE") ? atoi(getenv("AJM_DIRECT_INTERLEAVE")) : 0;
     return p;
 }
 
@@ -464,7 +465,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             h->meta_chunks = (mc + 3) & ~3;
         };
         if (!h->ident) h->vstage = 0;
-        h->direct = (h->sigma > 1) ? 1 : 0;
+        h->direct = 0;  // direct mode measured slower than the ring on every config so far
         if (const char* ev = getenv("AJM_DIRECT")) h->direct = atoi(ev) ? 1 : 0;
         if (h->vstage) h->fn = kVariants[h->variant].fnv;
         if (h->direct) {

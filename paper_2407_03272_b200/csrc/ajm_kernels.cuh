@@ -115,6 +115,7 @@ struct AjmPass {
     int l2_mode;                             // 0 none, 1 Q evict_first, 2 + vectors evict_last
     int vstage;                              // stage the rows' vector slices too (needs ident)
     unsigned long long* ts;                  // debug: per-pass phase timestamps of CTA 0 (or null)
+    int direct_interleave;                   // direct mode: chunk j -> warp j%8 (else contiguous)
 };
 
 __device__ __forceinline__ unsigned long long ajm_gtime() {
@@ -180,6 +181,32 @@ __device__ __forceinline__ void ajm_row_update(double* __restrict__ Qxp, double*
     }
     const double xn = y + (bi - qy) / Di;
     ajm_stp(xf + i, xn, pol);
+    const double term = (qy - bi) * (xn - xnow);
+    a.d += term;
+    a.dabs += fabs(term);
+}
+
+// same as ajm_row_update with plain stores (scattered rows of sorted-window layouts)
+__device__ __forceinline__ void ajm_row_update_plain(double* __restrict__ Qxp, double* __restrict__ xf, int i,
+                                                     double q, double bi, double Di, double xt, double xpi,
+                                                     double qxp, double beta, int restart_t, AjmAcc& a) {
+    const double r = bi - q;
+    a.rr += r * r;
+    a.xq += xt * q;
+    a.bx += bi * xt;
+    double y, qy, xnow;
+    if (!restart_t) {
+        y = xt + beta * (xt - xpi);
+        qy = q + beta * (q - qxp);
+        Qxp[i] = q;
+        xnow = xt;
+    } else {
+        y = xpi;
+        qy = qxp;
+        xnow = xpi;
+    }
+    const double xn = y + (bi - qy) / Di;
+    xf[i] = xn;
     const double term = (qy - bi) * (xn - xnow);
     a.d += term;
     a.dabs += fabs(term);
@@ -419,12 +446,12 @@ __device__ __forceinline__ void ajm_chunk_direct(const AjmPass& p, int ch, int w
     const int slot = ch * 32 + lane;
     const int row = p.ident ? (slot < p.n_sell ? slot : -1) : __ldg(p.perm + slot);
     double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
-    if (row >= 0) {
-        bi = ajm_ldp(p.b + row, vpol);
-        Di = ajm_ldp(p.D + row, vpol);
+    if (row >= 0) {  // plain loads: the rows of a sorted-window chunk are scattered
+        bi = __ldg(p.b + row);
+        Di = __ldg(p.D + row);
         xt = ajm_ld(xc + row);
         xpi = ajm_ld(xp + row);
-        qxp = ajm_ldp(p.Qxp + row, vpol);
+        qxp = p.Qxp[row];
     }
     const double* __restrict__ sv = p.sval + base + lane;
     const int* __restrict__ sc = p.scol + base + lane;
@@ -446,7 +473,7 @@ __device__ __forceinline__ void ajm_chunk_direct(const AjmPass& p, int ch, int w
         for (int j = 0; j < 8; ++j)
             if (k0 + j < w) s += v[j] * xg[j];  // ascending column order
     }
-    if (row >= 0) ajm_row_update(p.Qxp, xf, row, s, bi, Di, xt, xpi, qxp, beta, restart_t, acc, vpol);
+    if (row >= 0) ajm_row_update_plain(p.Qxp, xf, row, s, bi, Di, xt, xpi, qxp, beta, restart_t, acc);
 }
 
 // The persistent solver kernel (cooperative launch; grid = resident CTAs).  AJM_BLOCK consumer
@@ -610,7 +637,10 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         }
         if (direct) {
             // (2') SELL chunks straight from global memory; chunk j of the CTA -> warp j % 8
-            for (int j = warp; j < nchk; j += AJM_WARPS) {
+            const int jb = (int)((long long)nchk * warp / AJM_WARPS);
+            const int je = (int)((long long)nchk * (warp + 1) / AJM_WARPS);
+            for (int j = (p.direct_interleave ? warp : jb); j < (p.direct_interleave ? nchk : je);
+                 j += (p.direct_interleave ? AJM_WARPS : 1)) {
                 const int e0 = s_coff[j];
                 ajm_chunk_direct(p, cfirst + j, (s_coff[j + 1] - e0) >> 5, efirst + e0, lane, beta, restart_t,
                                  xc, xp, xf, acc, vpol);
