@@ -101,6 +101,7 @@ struct ajm_ctx {
     int* owner_split = nullptr;
     int* unit_c0 = nullptr;
     int* cta_seg = nullptr;
+    int* seg_list = nullptr;
     int* cta_unit = nullptr;
     double* partials = nullptr;
     AjmCtrl* ctrl = nullptr;
@@ -168,7 +169,7 @@ void free_all(ajm_ctx* h) {
     void* ptrs[] = {h->rp, h->col, h->val, h->vecs,
                     h->sval, h->scol, h->chunk_off, h->perm, h->seg_row, h->seg_k0, h->seg_k1,
                     h->seg_split, h->seg_part, h->split_row, h->split_seg0, h->split_cnt,
-                    h->cta_split, h->owner_split, h->unit_c0, h->cta_seg, h->cta_unit, h->partials, h->ctrl,
+                    h->cta_split, h->owner_split, h->unit_c0, h->cta_seg, h->seg_list, h->cta_unit, h->partials, h->ctrl,
                     h->hist, h->scratch, h->err, h->ts};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -198,6 +199,7 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.owner_split = h->owner_split;
     p.unit_c0 = h->unit_c0;
     p.cta_seg = h->cta_seg;
+    p.seg_list = h->seg_list;
     p.cta_unit = h->cta_unit;
     p.b = h->b;
     p.D = h->D;
@@ -411,7 +413,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         h->seg_rows = (int64_t)(split_rows.size() + whole_rows.size());
     }
     // ---- TMA staging units, persistent grid, cost-balanced CTA ranges ----
-    std::vector<int> unit_c0_h, cta_seg_h, cta_unit_h, cta_split_h, owner_split_h;
+    std::vector<int> unit_c0_h, cta_seg_h, cta_unit_h, cta_split_h, owner_split_h, seg_list_h;
     {
         // one item sequence: segments (split rows first), then SELL chunks; contiguous CTA ranges
         // balanced by cost at chunk granularity; each CTA's chunks are then grouped into TMA
@@ -419,32 +421,63 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         const int64_t nitems = h->nseg + h->nchunks;
         std::vector<double> cost;
         cost.reserve((size_t)nitems);
+        // segments are latency-bound (one warp, direct loads): weight their bytes twice
         for (int64_t s2 = 0; s2 < h->nseg; ++s2)
-            cost.push_back(12.0 * (seg_k1_h[(size_t)s2] - seg_k0_h[(size_t)s2]) + 56.0 + 256.0);
+            cost.push_back(24.0 * (seg_k1_h[(size_t)s2] - seg_k0_h[(size_t)s2]) + 56.0 + 512.0);
         for (int64_t c2 = 0; c2 < h->nchunks; ++c2) cost.push_back(chcost[(size_t)c2]);
         double total = 0.0;
         for (double x : cost) total += x;
         auto plan = [&](int G) {
+            // (a) segments: largest first onto the least-loaded CTA (LPT), so the latency-bound
+            //     long rows spread over every SM; (b) SELL chunks: contiguous ranges topping every
+            //     CTA up to the same cumulative cost
             const double target = total / (double)G;
-            std::vector<int64_t> start((size_t)G + 1, nitems);
-            int64_t i = 0;
-            double pref = 0.0;
-            for (int cc = 0; cc < G; ++cc) {
-                start[(size_t)cc] = i;
-                if (cc == G - 1) break;
-                const double lim = target * (double)(cc + 1);
-                while (i < nitems && pref + 0.5 * cost[(size_t)i] < lim) pref += cost[(size_t)i++];
+            std::vector<double> segload((size_t)G, 0.0);
+            std::vector<std::vector<int>> segs((size_t)G);
+            {
+                std::vector<int64_t> order((size_t)h->nseg);
+                for (int64_t k = 0; k < h->nseg; ++k) order[(size_t)k] = k;
+                std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return cost[(size_t)x] > cost[(size_t)y]; });
+                std::vector<std::pair<double, int>> heap;
+                for (int cc = 0; cc < G; ++cc) heap.push_back({0.0, cc});
+                auto cmp = [](const std::pair<double, int>& x, const std::pair<double, int>& y) {
+                    return x.first > y.first || (x.first == y.first && x.second > y.second);
+                };
+                std::make_heap(heap.begin(), heap.end(), cmp);
+                for (int64_t k : order) {
+                    std::pop_heap(heap.begin(), heap.end(), cmp);
+                    auto& top = heap.back();
+                    top.first += cost[(size_t)k];
+                    segload[(size_t)top.second] += cost[(size_t)k];
+                    segs[(size_t)top.second].push_back((int)k);
+                    std::push_heap(heap.begin(), heap.end(), cmp);
+                }
             }
-            start[(size_t)G] = nitems;
+            seg_list_h.clear();
             cta_seg_h.assign((size_t)G + 1, 0);
+            for (int cc = 0; cc < G; ++cc) {
+                std::sort(segs[(size_t)cc].begin(), segs[(size_t)cc].end());  // split-row segments first
+                cta_seg_h[(size_t)cc] = (int)seg_list_h.size();
+                for (int k : segs[(size_t)cc]) seg_list_h.push_back(k);
+            }
+            cta_seg_h[(size_t)G] = (int)seg_list_h.size();
+            std::vector<int64_t> cstart((size_t)G + 1, h->nchunks);
+            int64_t i = 0;
+            double pref = 0.0, cumseg = 0.0;
+            for (int cc = 0; cc < G; ++cc) {
+                cstart[(size_t)cc] = i;
+                cumseg += segload[(size_t)cc];
+                if (cc == G - 1) break;
+                const double lim = target * (double)(cc + 1) - cumseg;
+                while (i < h->nchunks && pref + 0.5 * cost[(size_t)(h->nseg + i)] < lim) pref += cost[(size_t)(h->nseg + i++)];
+            }
+            cstart[(size_t)G] = h->nchunks;
             cta_unit_h.assign((size_t)G + 1, 0);
             unit_c0_h.clear();
             int mu = 1, mc = 1;
-            for (int cc = 0; cc <= G; ++cc) cta_seg_h[(size_t)cc] = (int)std::min<int64_t>(start[(size_t)cc], h->nseg);
             for (int cc = 0; cc < G; ++cc) {
                 cta_unit_h[(size_t)cc] = (int)unit_c0_h.size();
-                const int64_t c0 = std::max<int64_t>(start[(size_t)cc] - h->nseg, 0);
-                const int64_t c1 = std::max<int64_t>(start[(size_t)cc + 1] - h->nseg, 0);
+                const int64_t c0 = cstart[(size_t)cc], c1 = cstart[(size_t)cc + 1];
                 int64_t c2 = c0;
                 while (c2 < c1) {
                     const int64_t ub = c2;
@@ -496,7 +529,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         // owner of a split row = the CTA that runs its last segment
         std::vector<int> seg_cta((size_t)h->nseg, 0);
         for (int cc = 0; cc < G; ++cc)
-            for (int k2 = cta_seg_h[(size_t)cc]; k2 < cta_seg_h[(size_t)cc + 1]; ++k2) seg_cta[(size_t)k2] = cc;
+            for (int k2 = cta_seg_h[(size_t)cc]; k2 < cta_seg_h[(size_t)cc + 1]; ++k2) seg_cta[(size_t)seg_list_h[(size_t)k2]] = cc;
         std::vector<std::vector<int>> per((size_t)G);
         for (int64_t sp = 0; sp < h->nsplit; ++sp)
             per[(size_t)seg_cta[(size_t)split_seg0_h[(size_t)sp + 1] - 1]].push_back((int)sp);
@@ -554,6 +587,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(dalloc(&h->owner_split, h->nsplit));
     CC(dalloc(&h->unit_c0, unit_c0_h.size()));
     CC(dalloc(&h->cta_seg, cta_seg_h.size()));
+    CC(dalloc(&h->seg_list, seg_list_h.size()));
     CC(dalloc(&h->cta_unit, cta_unit_h.size()));
     CC(dalloc(&h->partials, (size_t)2 * h->grid * AJM_NPART));
     CC(dalloc(&h->ctrl, 1));
@@ -602,6 +636,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(h2d(h->owner_split, owner_split_h.data(), sizeof(int) * owner_split_h.size()));
     CC(h2d(h->unit_c0, unit_c0_h.data(), sizeof(int) * unit_c0_h.size()));
     CC(h2d(h->cta_seg, cta_seg_h.data(), sizeof(int) * cta_seg_h.size()));
+    CC(h2d(h->seg_list, seg_list_h.data(), sizeof(int) * seg_list_h.size()));
     CC(h2d(h->cta_unit, cta_unit_h.data(), sizeof(int) * cta_unit_h.size()));
     CC(cudaMemsetAsync(h->err, 0, sizeof(int), st));
 

@@ -96,7 +96,8 @@ struct AjmPass {
     unsigned int* split_cnt;                 // [nsplit] monotone arrival counters
     const int* __restrict__ cta_split;       // [grid+1] split rows owned by each CTA
     const int* __restrict__ owner_split;     // split-row ids grouped by owner CTA
-    const int* __restrict__ cta_seg;         // [grid+1] segment range of each CTA
+    const int* __restrict__ cta_seg;         // [grid+1] range of each CTA in seg_list
+    const int* __restrict__ seg_list;        // segment ids grouped by CTA
     const int* __restrict__ cta_unit;        // [grid+1] unit range of each CTA
     const double* __restrict__ b;
     const double* __restrict__ D;
@@ -621,7 +622,8 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         if (tsw) p.ts[pass * 8 + 0] = ajm_gtime();
 
         // (1) row segments (direct loads), split-row segments first
-        for (int sg = sg0 + warp; sg < sg1; sg += AJM_WARPS) {
+        for (int sk = sg0 + warp; sk < sg1; sk += AJM_WARPS) {
+            const int sg = __ldg(p.seg_list + sk);
             const int row = __ldg(p.seg_row + sg);
             const double s = ajm_seg_dot(p, __ldg(p.seg_k0 + sg), __ldg(p.seg_k1 + sg), xc, lane);
             const int sidx = __ldg(p.seg_split + sg);
