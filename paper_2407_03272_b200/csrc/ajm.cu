@@ -763,18 +763,21 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
     if (h->ts) {  // debug: mean phase durations of CTA 0 over the first passes
         unsigned long long hts[64 * 8];
         AJM_CUDA(h, cudaMemcpy(hts, h->ts, sizeof(hts), cudaMemcpyDeviceToHost));
-        double acc[5] = {0, 0, 0, 0, 0};
+        double acc[5] = {0, 0, 0, 0, 0}, seg = 0, chk = 0;
         int np = 0;
         for (int k = 2; k + 1 < 64 && k + 1 <= c.s.iterations; ++k) {
             if (!hts[k * 8 + 5] || !hts[(k + 1) * 8]) break;
             for (int j = 0; j < 4; ++j) acc[j] += (double)(hts[k * 8 + j + 1] - hts[k * 8 + j]);
             acc[4] += (double)(hts[(k + 1) * 8] - hts[k * 8 + 4]);
+            seg += (double)(hts[k * 8 + 6] - hts[k * 8 + 0]);
+            chk += (double)(hts[k * 8 + 7] - hts[k * 8 + 6]);
             ++np;
         }
         if (np)
             fprintf(stderr, "[ajm ts] passes %d: work %.2f us, block-reduce %.2f, grid-barrier %.2f, "
-                            "partials %.2f, control+sync %.2f\n", np, acc[0] / np / 1e3, acc[1] / np / 1e3,
-                    acc[2] / np / 1e3, acc[3] / np / 1e3, acc[4] / np / 1e3);
+                            "partials %.2f, control+sync %.2f | segments %.2f, chunks %.2f\n", np, acc[0] / np / 1e3,
+                    acc[1] / np / 1e3, acc[2] / np / 1e3, acc[3] / np / 1e3, acc[4] / np / 1e3, seg / np / 1e3,
+                    chk / np / 1e3);
     }
 
     AJM_CUDA(h, cudaMemcpyAsync(x_out, h->X[c.s.answer], sizeof(double) * n, kind_from_device(x_out), st));

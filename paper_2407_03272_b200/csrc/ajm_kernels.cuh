@@ -637,6 +637,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                 }
             }
         }
+        if (tsw) p.ts[pass * 8 + 6] = ajm_gtime();
         if (direct) {
             // (2') SELL chunks straight from global memory; chunk j of the CTA -> warp j % 8
             const int jb = (int)((long long)nchk * warp / AJM_WARPS);
@@ -695,6 +696,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
             }
             ucnt += nunits;
         }
+        if (tsw) p.ts[pass * 8 + 7] = ajm_gtime();
         // (3) split rows owned by this CTA: wait for all segments of this pass, sum in order
         for (int k = sp0 + warp; k < sp1; k += AJM_WARPS) {
             const int sidx = __ldg(p.owner_split + k);
