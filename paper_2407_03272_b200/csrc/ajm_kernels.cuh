@@ -357,25 +357,43 @@ __device__ __forceinline__ bool ajm_grid_wait(AjmCtrl* c, unsigned nblocks, long
     return to;
 }
 
-// warp-level dot of a CSR segment [k0, k1) against x (lane-strided, 8 loads in flight per lane)
+// warp-level dot of a CSR segment [k0, k1) against x: lane-strided, 8 elements per lane per step,
+// software-pipelined so the next step's val/col stream in while this step's gathers are in flight
 __device__ __forceinline__ double ajm_seg_dot(const AjmPass& p, int k0, int k1, const double* xc,
                                               int lane) {
     double s = 0.0;
-    for (int k = k0 + lane; k < k1; k += 8 * 32) {
-        double v[8], xg[8];
-        int cc[8];
+    double v[8];
+    int cc[8];
+    int k = k0 + lane;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int kk = k + j * 32;
-            v[j] = 0.0;
-            cc[j] = 0;
-            if (kk < k1) { v[j] = __ldcs(p.val + kk); cc[j] = __ldcs(p.col + kk); }
-        }
+    for (int j = 0; j < 8; ++j) {
+        const int kk = k + j * 32;
+        v[j] = 0.0;
+        cc[j] = 0;
+        if (kk < k1) { v[j] = __ldcs(p.val + kk); cc[j] = __ldcs(p.col + kk); }
+    }
+    for (; k < k1; k += 8 * 32) {
+        double xg[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) xg[j] = ajm_ld(xc + cc[j]);
+        double vn[8];
+        int cn[8];
+        const int kn = k + 8 * 32;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int kk = kn + j * 32;
+            vn[j] = 0.0;
+            cn[j] = 0;
+            if (kk < k1) { vn[j] = __ldcs(p.val + kk); cn[j] = __ldcs(p.col + kk); }
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j)
             if (k + j * 32 < k1) s += v[j] * xg[j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            v[j] = vn[j];
+            cc[j] = cn[j];
+        }
     }
     return ajm_warp_sum(s);
 }
@@ -424,16 +442,16 @@ __device__ __forceinline__ void ajm_bulk_g2s(void* dst, const void* src, unsigne
 // the stage's full barrier by the caller.
 __device__ __forceinline__ double ajm_chunk_dot(const double* sv, const int* sc, int w, const double* xc) {
     double s = 0.0;
-    for (int k0 = 0; k0 < w; k0 += 8) {
-        double xg[8];
-        int cc[8];
+    for (int k0 = 0; k0 < w; k0 += 16) {  // 16 independent gathers in flight per lane
+        double xg[16];
+        int cc[16];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) cc[j] = (k0 + j < w) ? sc[(k0 + j) * 32] : 0;
+        for (int j = 0; j < 16; ++j) cc[j] = (k0 + j < w) ? sc[(k0 + j) * 32] : 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < 16; ++j)
             if (k0 + j < w) xg[j] = ajm_ld(xc + cc[j]);
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < 16; ++j)
             if (k0 + j < w) s += sv[(k0 + j) * 32] * xg[j];  // ascending column order
     }
     return s;
