@@ -442,16 +442,16 @@ __device__ __forceinline__ void ajm_bulk_g2s(void* dst, const void* src, unsigne
 // the stage's full barrier by the caller.
 __device__ __forceinline__ double ajm_chunk_dot(const double* sv, const int* sc, int w, const double* xc) {
     double s = 0.0;
-    for (int k0 = 0; k0 < w; k0 += 16) {  // 16 independent gathers in flight per lane
-        double xg[16];
-        int cc[16];
+    for (int k0 = 0; k0 < w; k0 += 8) {
+        double xg[8];
+        int cc[8];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) cc[j] = (k0 + j < w) ? sc[(k0 + j) * 32] : 0;
+        for (int j = 0; j < 8; ++j) cc[j] = (k0 + j < w) ? sc[(k0 + j) * 32] : 0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
+        for (int j = 0; j < 8; ++j)
             if (k0 + j < w) xg[j] = ajm_ld(xc + cc[j]);
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
+        for (int j = 0; j < 8; ++j)
             if (k0 + j < w) s += sv[(k0 + j) * 32] * xg[j];  // ascending column order
     }
     return s;
