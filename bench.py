@@ -317,7 +317,7 @@ def run_ours(args):
         "model_gbs": achieved,
         "pct_of_8tbs_nominal": 100.0 * achieved / NOMINAL_HBM_GBS,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_basis": "ncu dram read+write per pass (profiles/ncu_traffic.json) x passes per launch", "peak_source": peak_src,
                      "kernel": "ajm_solve_kernel (persistent; one launch per solve)",
                      "achieved_basis": "algorithmic bytes nnz*12+7n*8+4(n+1) per pass x passes / "
                                        "launch duration (CUDA events on the launch stream)"},
