@@ -28,9 +28,31 @@ sys.path.insert(0, ROOT)
 
 METRIC = "AJM iterations/s + achieved HBM GB/s (% of B200 peak); time to 1e-6 rel. residual"
 UNIT = "iterations/s"
-WORKLOAD = "poisson3d_128: 3D 7-pt Dirichlet Laplacian 128^3 (n=2097152, nnz=14581760), FP64 CSR, " \
-           "x*~U(-1,1) seed 2, b=Qx*, x0=0, eq-J-diag, restart on, K0=2, solve to 1e-6 rel. residual " \
-           "(BASELINE.json configs[1])"
+# BASELINE.json configs; the default (configs[1], the config the metric is quoted on) is the bench
+# line; the others are reported with --config K (every config as a roofline fraction, north_star)
+WORKLOADS = {
+    1: dict(tol=0.0, maxit=2000, bound="latency",
+            workload="poisson2d_64: 2D 5-pt Dirichlet Laplacian 64^2 (n=4096, nnz=20224), FP64 CSR, "
+                     "x*~U(-1,1) seed 1, b=Qx*, x0=0, eq-J-diag, restart on, K0=2, 2000 iterations "
+                     "(BASELINE.json configs[0]; 0.49 MB per pass: L2/latency-bound, not HBM)"),
+    2: dict(tol=1e-6, maxit=5000, bound="hbm",
+            workload="poisson3d_128: 3D 7-pt Dirichlet Laplacian 128^3 (n=2097152, nnz=14581760), FP64 CSR, "
+                     "x*~U(-1,1) seed 2, b=Qx*, x0=0, eq-J-diag, restart on, K0=2, solve to 1e-6 rel. residual "
+                     "(BASELINE.json configs[1])"),
+    3: dict(tol=1e-6, maxit=5000, bound="hbm",
+            workload="er_1m_deg16: weighted Erdos-Renyi Laplacian n=1M, 8M edges, w~U(0.1,1), singular SPSD, "
+                     "x*~N(0,1)-mean seed 1003, b=Lx*, x0=0, eq-J-diag, restart on, solve to 1e-6 "
+                     "(BASELINE.json configs[2])"),
+    4: dict(tol=1e-6, maxit=5000, bound="hbm",
+            workload="chunglu_4m_deg20: Chung-Lu gamma=2.1 Laplacian n=4M mean degree 20 (max row ~1e5) "
+                     "+1e-3 I, w~U(0.1,1), x*~U(-1,1) seed 1004, x0=0, eq-J-diag, restart on, solve to 1e-6 "
+                     "(BASELINE.json configs[3])"),
+    5: dict(tol=1e-6, maxit=5000, bound="hbm",
+            workload="aniso27_256: anisotropic 27-pt stencil 256^3 (n=16777216, nnz=449455096), w=(1,1,1e-2), "
+                     "diag=row-abs-sum+1e-6, x*~U(-1,1) seed 5, x0=0, eq-J-diag, restart on, solve to 1e-6 "
+                     "(BASELINE.json configs[4])"),
+}
+WORKLOAD = WORKLOADS[2]["workload"]
 NOMINAL_HBM_GBS = 8000.0
 
 
@@ -43,13 +65,19 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic():
-    """ncu DRAM bytes per pass of the solver kernel on this workload (profiles/, committed)."""
+def load_traffic(workload: str):
+    """ncu DRAM bytes per pass of the solver kernel on this workload (profiles/ncu_traffic.json,
+    committed from an `ncu --set full` capture; one record per workload name)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f)
+            tr = json.load(f)
     except Exception:
         return None
+    recs = tr if isinstance(tr, list) else [tr]
+    for r in recs:
+        if r.get("workload") == workload:
+            return r
+    return None
 
 
 # ------------------------------------------------------------------------------------------------
@@ -153,12 +181,12 @@ class ClockSampler:
 # workload
 # ------------------------------------------------------------------------------------------------
 
-def make_problem():
+def make_problem(cfg=2):
     import synth
-    return synth.config_problem(2)
+    return synth.config_problem(cfg)
 
 
-def cpu_baseline_run(p, budget_s=12.0, nthreads=None):
+def cpu_baseline_run(p, cfg=2, budget_s=12.0, nthreads=None):
     """The oracle as it stands (literal two-SpMV Alg. 3), on host cores, on a bounded sample of the
     workload: the first T iterations of the same solve, T sized to ~budget_s seconds."""
     import oracle
@@ -172,7 +200,7 @@ def cpu_baseline_run(p, budget_s=12.0, nthreads=None):
     r = oracle.solve(p.Q, p.b, tol=0.0, maxit=T, restart=True)
     dt = time.perf_counter() - t0
     return {"value": r.iterations / dt, "unit": UNIT, "cores": nt, "kind": "oracle",
-            "sample": f"first {T} iterations of the config-2 solve (literal two-SpMV Alg. 3, "
+            "sample": f"first {T} iterations of the config-{cfg} solve (literal two-SpMV Alg. 3, "
                       f"plain C FP64, {nt} OpenMP threads), {dt:.2f} s wall"}
 
 
@@ -180,7 +208,8 @@ def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
         return 0  # rank 0 alone runs the CPU reference arm
-    p = make_problem()
+    W = WORKLOADS[args.config]
+    p = make_problem(args.config)
     import oracle
     nt = os.cpu_count() or 1
     oracle.set_threads(nt)
@@ -202,9 +231,9 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": WORKLOAD, "sample_iterations_per_step": S},
+        "data": "synthetic", "config": {"workload": W["workload"], "sample_iterations_per_step": S},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": nt, "kind": "oracle",
-                         "sample": f"{S} iterations of the config-2 solve per step (literal two-SpMV "
+                         "sample": f"{S} iterations of the config-{args.config} solve per step (literal two-SpMV "
                                    f"Alg. 3, plain C FP64, {nt} OpenMP threads)"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -223,13 +252,16 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = init_dist(world, "nccl")
-    p = make_problem()
+    W = WORKLOADS[args.config]
+    tol = W["tol"] if args.tol is None else args.tol
+    maxit = W["maxit"] if args.maxit is None else args.maxit
+    p = make_problem(args.config)
     stream = torch.cuda.current_stream()
     # inputs resident in HBM before timing
     Qd = [torch.from_numpy(a).to(dev) for a in (p.Q.row_ptr, p.Q.col, p.Q.val, p.b)]
     solver = ajm.Solver(p.Q.n, *Qd[:3], Qd[3])
     x_out = torch.empty(p.Q.n, dtype=torch.float64, device=dev)
-    kw = dict(tol=args.tol, maxit=args.maxit, restart=True, x_out=x_out, history=False)
+    kw = dict(tol=tol, maxit=maxit, restart=True, x_out=x_out, history=False)
     for _ in range(args.warmup):
         solver.solve(**kw)
     torch.cuda.synchronize()
@@ -257,7 +289,7 @@ def run_ours(args):
     ms = e0.elapsed_time(e1)
     job_iters, job_ms = reduce_job(float(iters), ms, dist, dev)
     info = solver.info()
-    assert all(r.status == "converged" for r in results)
+    assert all(r.status == ("converged" if tol > 0 else "maxiter") for r in results)
 
     # ---- e2e: the public API from pinned host buffers (create + solve + x to host + destroy) ----
     host = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
@@ -271,7 +303,7 @@ def run_ours(args):
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record(stream)
         with ajm.Solver(p.Q.n, host[0], host[1], host[2], host[3]) as s2:
-            r2 = s2.solve(tol=args.tol, maxit=args.maxit, restart=True, x_out=x_host, history=True)
+            r2 = s2.solve(tol=tol, maxit=maxit, restart=True, x_out=x_host, history=True)
         a1.record(stream)
         torch.cuda.synchronize()
         if k == 0:
@@ -287,11 +319,14 @@ def run_ours(args):
     peak, peak_src = load_peaks()
     model_bytes = info["model_bytes_per_iter"]
     achieved = model_bytes * passes / (loop_ms * 1e-3) / 1e9  # GB/s, per-launch average
-    tr = load_traffic()
-    traffic = None
-    if tr and tr.get("workload") == "poisson3d_128":
-        traffic = tr["dram_bytes_per_pass"] * passes / args.steps
-    cpu = cpu_baseline_run(p) if (world == 1 and not args.no_cpu_baseline) else None
+    tr = load_traffic(p.name)
+    traffic = None if tr is None else tr["dram_bytes_per_pass"] * passes / args.steps
+    cpu = cpu_baseline_run(p, args.config) if (world == 1 and not args.no_cpu_baseline) else None
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    l2_note = (f"inputs larger than L2: {model_bytes / 1e6:.1f} MB algorithmic traffic per pass vs "
+               f"{l2_bytes / 1e6:.0f} MB L2" if model_bytes > l2_bytes else
+               f"L2-resident: {model_bytes / 1e6:.2f} MB per pass fits the {l2_bytes / 1e6:.0f} MB L2, "
+               "so the HBM fraction is not the bound (latency-bound: grid barrier per pass)")
     line = {
         "metric": METRIC,
         "value": job_iters / (job_ms * 1e-3),
@@ -305,9 +340,9 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n": p.Q.n, "nnz": p.Q.nnz, "tol": args.tol,
+        "config": {"workload": W["workload"], "n": p.Q.n, "nnz": p.Q.nnz, "tol": tol, "maxit": maxit,
                    "parallelism": f"replicas x{world} (the method does not shard: DESIGN.md §6)",
-                   "l2": "inputs larger than L2: 300.8 MB algorithmic traffic per pass vs 126 MB L2",
+                   "l2": l2_note,
                    "kernel_variant": info["variant"], "grid": info["grid"],
                    "ctas_per_sm": info["ctas_per_sm"]},
         "iterations_per_solve": iters / args.steps,
@@ -316,7 +351,7 @@ def run_ours(args):
         "model_bytes_per_iteration": model_bytes,
         "model_gbs": achieved,
         "pct_of_8tbs_nominal": 100.0 * achieved / NOMINAL_HBM_GBS,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "roofline": {"bound": W["bound"] if W["bound"] != "latency" else "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_basis": "ncu dram read+write per pass (profiles/ncu_traffic.json) x passes per launch", "peak_source": peak_src,
                      "kernel": "ajm_solve_kernel (persistent; one launch per solve)",
                      "achieved_basis": "algorithmic bytes nnz*12+7n*8+4(n+1) per pass x passes / "
@@ -340,8 +375,10 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--tol", type=float, default=1e-6)
-    ap.add_argument("--maxit", type=int, default=5000)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(WORKLOADS),
+                    help="BASELINE.json configs[K-1]; default 2 = the metric's config")
+    ap.add_argument("--tol", type=float, default=None, help="default: the workload's")
+    ap.add_argument("--maxit", type=int, default=None, help="default: the workload's")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)

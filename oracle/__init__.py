@@ -8,6 +8,7 @@ builds it with gcc and marshals numpy arrays through ctypes.
 Each function cites the passage it follows (PAPER.md = P, SPEC.md = S, readings R#):
   spmv            Q x, ascending-column row sums                       (P:463 Q y^t)
   build_jdiag     eq-J-diag  J_kk = Q_kk + sum_{j!=k}|Q_kj|
+  build_jblock    eq-J-blkdiag J^{ii} = Q^{ii} + sum_{j!=i}||Q^{ij}||_2 I  (R23)
   diag            D = diag(Q)
   alpha_next      alpha_{t+1} = (1 + sqrt(1 + 4 alpha_t^2))/2
   objective       f(x) = 1/2<x,Qx> - <b,x>
@@ -65,8 +66,8 @@ def _load():
         lib.oracle_set_threads.argtypes = [ctypes.c_int]
         lib.oracle_get_threads.restype = ctypes.c_int
         lib.oracle_ajm_solve.argtypes = [I64, P, P, P, P, P, P, ctypes.c_double, I64, ctypes.c_int,
-                                         ctypes.c_int, I64, ctypes.c_int, P, P, P, P, P, P, P, P,
-                                         P, I64, P]
+                                         ctypes.c_int, I64, ctypes.c_int, P, I64, P, P, P, P, P, P,
+                                         P, P, P, I64, P]
         lib.oracle_ajm_solve.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -116,6 +117,62 @@ def build_jdiag(Q) -> np.ndarray:
     return J
 
 
+def build_jblock(Q, bs: int, batch: int = 1 << 16) -> np.ndarray:
+    """eq-J-blkdiag: J = diag(J^{1,1}, ..., J^{s,s}) over contiguous row blocks of bs
+    rows (block i = rows [i*bs, min((i+1)*bs, n)), the last one ragged -- DESIGN.md R23), with
+        J^{ii} = Q^{ii} + (sum_{j != i} ||Q^{ij}||_2) I.
+    ||Q^{ij}||_2 is the largest singular value of the dense off-diagonal block (numpy's LAPACK
+    SVD); the shifts are summed in ascending j.  Returns the dense blocks, shape (s, bs, bs); the
+    ragged last block is padded with the identity (which leaves J^{-1} on its rows unchanged)."""
+    n = int(Q.n)
+    bs = int(bs)
+    if bs < 1:
+        raise OracleError("block size must be >= 1")
+    nblk = (n + bs - 1) // bs
+    rp = np.asarray(Q.row_ptr, dtype=np.int64)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp))
+    cols = np.asarray(Q.col, dtype=np.int64)
+    vals = np.asarray(Q.val, dtype=np.float64)
+    if not np.all(np.isfinite(vals)):
+        raise OracleError("non-finite value")
+    bi, bj = rows // bs, cols // bs
+    J = np.zeros((nblk, bs, bs))
+    on = bi == bj
+    J[bi[on], rows[on] % bs, cols[on] % bs] = vals[on]       # Q^{ii}
+    off = ~on
+    key = bi[off] * nblk + bj[off]                           # sorted by (i, j): CSR order
+    order = np.argsort(key, kind="stable")
+    key, r_off, c_off, v_off = key[order], rows[off][order], cols[off][order], vals[off][order]
+    uniq, first, inv = np.unique(key, return_index=True, return_inverse=True)
+    norms = np.empty(len(uniq))
+    for s0 in range(0, len(uniq), batch):                   # ||Q^{ij}||_2, batched SVDs
+        s1 = min(s0 + batch, len(uniq))
+        lo, hi = first[s0], (first[s1] if s1 < len(uniq) else len(key))
+        B = np.zeros((s1 - s0, bs, bs))
+        B[inv[lo:hi] - s0, r_off[lo:hi] % bs, c_off[lo:hi] % bs] = v_off[lo:hi]
+        norms[s0:s1] = np.linalg.svd(B, compute_uv=False)[:, 0] if s1 > s0 else 0.0
+    shift = np.zeros(nblk)
+    for blk, nv in zip(uniq // nblk, norms):                 # ascending j within each i
+        shift[blk] += nv
+    idx = np.arange(bs)
+    J[:, idx, idx] += shift[:, None]
+    m = n - (nblk - 1) * bs                                  # ragged last block: identity pad
+    for k in range(m, bs):
+        J[nblk - 1, k, :] = 0.0
+        J[nblk - 1, :, k] = 0.0
+        J[nblk - 1, k, k] = 1.0
+    return J
+
+
+def jblock_factor(J: np.ndarray) -> np.ndarray:
+    """Per-block lower Cholesky factors (LAPACK) of an eq-J-blkdiag J; an SPD failure raises
+    (impossible for SPSD Q with exact norms)."""
+    try:
+        return np.ascontiguousarray(np.linalg.cholesky(J))
+    except np.linalg.LinAlgError as e:
+        raise OracleError(f"J block not SPD: {e}")
+
+
 def diag(Q) -> np.ndarray:
     rp, ci, v = _csr(Q)
     d = np.empty(Q.n)
@@ -160,11 +217,17 @@ class OracleResult:
 
 
 def solve(Q, b, D=None, x0=None, tol=1e-6, maxit=1000, momentum=True, restart=True, k0=2,
-          mirror=False, forced=None, record_iterates=False, dmode="jdiag") -> OracleResult:
-    """Alg. 3.  D defaults to eq-J-diag; dmode='qdiag' uses diag(Q) (eq-jacobi)."""
+          mirror=False, forced=None, record_iterates=False, dmode="jdiag",
+          jblock: int | None = None) -> OracleResult:
+    """Alg. 3 (P:458-480).  D defaults to eq-J-diag; dmode='qdiag' uses diag(Q) (eq-jacobi);
+    jblock=bs uses the block-diagonal J of eq-J-blkdiag with bs-row blocks (D is then ignored)."""
     rp, ci, v = _csr(Q)
     n = Q.n
     b = _vec(b)
+    Lfac = None
+    if jblock is not None:
+        Lfac = jblock_factor(build_jblock(Q, jblock))
+        D = np.ones(n)
     if D is None:
         D = build_jdiag(Q) if dmode == "jdiag" else diag(Q)
     D = _vec(D)
@@ -183,7 +246,7 @@ def solve(Q, b, D=None, x0=None, tol=1e-6, maxit=1000, momentum=True, restart=Tr
     x_out = np.empty(n)
     rc = _load().oracle_ajm_solve(n, _p(rp), _p(ci), _p(v), _p(b), _p(D), _p(x0a), float(tol),
                                   int(maxit), int(bool(momentum)), int(bool(restart)), int(k0),
-                                  int(bool(mirror)), _p(fa), _p(x_out), _p(res_hist), _p(f_hist),
+                                  int(bool(mirror)), _p(fa), int(jblock or 0), _p(Lfac), _p(x_out), _p(res_hist), _p(f_hist),
                                   _p(d_hist), _p(dabs_hist), _p(xt_hist), _p(alpha_hist), _p(rit),
                                   cap, _p(info))
     if rc == -1:

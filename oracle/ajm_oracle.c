@@ -9,6 +9,11 @@
  *
  * What it computes (PAPER.md = P, SPEC.md = S; DESIGN.md §2 lists the readings R1..R21):
  *   - eq-J-diag (§3):  J_kk = Q_kk + sum_{j != k} |Q_kj|   (ascending j)
+ *   - eq-J-blkdiag (§3): block-diagonal J with J^{ii} = Q^{ii} + sum_{j != i}||Q^{ij}||_2 I
+ *     over contiguous row blocks of bs rows (the last block ragged).  The blocks themselves are
+ *     built in oracle/__init__.py (numpy: dense blocks, LAPACK SVD for ||.||_2, LAPACK Cholesky);
+ *     this file applies J^{-1} per block by forward and back substitution with the Cholesky factor
+ *     (Alg. 3 line 4: (x^t)^i = (y^t)^i + (J^{ii})^{-1}(b^i - sum_j Q^{ij}(y^t)^j)).
  *   - eq-qp:            f(x) = 1/2 <x, Qx> - <b, x>
  *   - stopping rule (§4):  ||b - Qx^t||_2 / ||b||_2 <= tol   (R3)
  *   - Alg. 3 with s = 1, LITERALLY: every iteration does the SpMV Q y^t for the step
@@ -168,6 +173,30 @@ void oracle_diag(int64_t n, const int64_t* rp, const int32_t* ci, const double* 
 /* Alg. 1 line 4 / Alg. 3 line 13: alpha_{t+1} = (1 + sqrt(1 + 4 alpha_t^2)) / 2 */
 double oracle_alpha_next(double a) { return (1.0 + sqrt(1.0 + 4.0 * a * a)) / 2.0; }
 
+/* z = J^{-1} r for block-diagonal J given its per-block lower Cholesky factors L (J^{ii} = L L^T,
+ * row-major bs x bs per block; the ragged last block uses its leading m x m corner).
+ * Forward substitution L w = r, then back substitution L^T z = w, textbook order. */
+static void block_chol_solve(int64_t n, int64_t bs, const double* L, const double* r, double* z) {
+    int64_t nblk = (n + bs - 1) / bs, blk;
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+    for (blk = 0; blk < nblk; ++blk) {
+        const int64_t base = blk * bs;
+        const int64_t m = (base + bs <= n) ? bs : n - base;
+        const double* Lb = L + (size_t)blk * (size_t)(bs * bs);
+        double* w = z + base;
+        for (int64_t k = 0; k < m; ++k) { /* L w = r */
+            double s = r[base + k];
+            for (int64_t j = 0; j < k; ++j) s -= Lb[k * bs + j] * w[j];
+            w[k] = s / Lb[k * bs + k];
+        }
+        for (int64_t k = m - 1; k >= 0; --k) { /* L^T z = w (in place) */
+            double s = w[k];
+            for (int64_t j = k + 1; j < m; ++j) s -= Lb[j * bs + k] * w[j];
+            w[k] = s / Lb[k * bs + k];
+        }
+    }
+}
+
 enum { OR_CONVERGED = 0, OR_MAXITER = 1, OR_DIVERGED = 2 };
 
 /*
@@ -176,7 +205,9 @@ enum { OR_CONVERGED = 0, OR_MAXITER = 1, OR_DIVERGED = 2 };
  * inputs : CSR Q (n, rp, ci, v), b[n], D[n] (> 0), x0[n] (NULL = zeros), tol (>= 0), maxit (>= 1),
  *          momentum (0/1), restart (0/1 = IsRestart), k0 (K_0 >= 2), mirror (0 literal / 1 identity),
  *          forced[maxit+1] (NULL, or per-t forced restart decision: -1 none, 0 no, 1 yes; R17 tie
- *          protocol -- the t > K_re + K_l window is still required).
+ *          protocol -- the t > K_re + K_l window is still required);
+ *          bs, Lfac: block-diagonal J (eq-J-blkdiag) -- if Lfac != NULL the step applies J^{-1} by
+ *          per-block Cholesky solves (block_chol_solve) and D is ignored.
  * outputs: x_out[n]; res_hist/f_hist[maxit+1] (entry t is for x~^t, the pre-restart iterate);
  *          d_hist/dabs_hist[maxit+1] (restart inner product <Qy^t - b, x~^t - x^{t-1}> and the sum of
  *          |terms| for the tie ratio, entry 0 unused = 0); xt_hist[(maxit+1)*n] post-iteration x^t
@@ -189,10 +220,11 @@ enum { OR_CONVERGED = 0, OR_MAXITER = 1, OR_DIVERGED = 2 };
 int oracle_ajm_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
                      const double* b, const double* D, const double* x0, double tol, int64_t maxit,
                      int momentum, int restart, int64_t k0, int mirror, const int8_t* forced,
-                     double* x_out, double* res_hist, double* f_hist, double* d_hist,
+                     int64_t bs, const double* Lfac, double* x_out, double* res_hist, double* f_hist, double* d_hist,
                      double* dabs_hist, double* xt_hist, double* alpha_hist,
                      int64_t* restart_iters, int64_t restart_cap, int64_t* info) {
     if (n < 1 || maxit < 1 || !(tol >= 0.0) || k0 < 2 || (restart && !momentum)) return -1;
+    if (Lfac && bs < 1) return -1;
     size_t bytes = sizeof(double) * (size_t)n;
     double *x = malloc(bytes), *x_prev = malloc(bytes), *y = malloc(bytes), *xt = malloc(bytes);
     double *qy = malloc(bytes), *qx = malloc(bytes), *qx_prev = malloc(bytes);
@@ -233,7 +265,13 @@ int oracle_ajm_solve(int64_t n, const int64_t* rp, const int32_t* ci, const doub
         if (alpha_hist) alpha_hist[t] = alpha;
         /* Alg. 3 line 4: x~^t = y^t + D^{-1}(b - Q y^t) */
         if (!mirror) oracle_spmv(n, rp, ci, v, y, qy);
-        for (int64_t i = 0; i < n; ++i) xt[i] = y[i] + (b[i] - qy[i]) / D[i];
+        if (!Lfac) {
+            for (int64_t i = 0; i < n; ++i) xt[i] = y[i] + (b[i] - qy[i]) / D[i];
+        } else { /* eq-J-blkdiag: x~ = y + J^{-1}(b - Q y), block by block */
+            for (int64_t i = 0; i < n; ++i) xt[i] = b[i] - qy[i];
+            block_chol_solve(n, bs, Lfac, xt, xt);
+            for (int64_t i = 0; i < n; ++i) xt[i] = y[i] + xt[i];
+        }
 
         /* stopping rule on x~^t (R5) and trace */
         oracle_spmv(n, rp, ci, v, xt, qx);

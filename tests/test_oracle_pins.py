@@ -74,8 +74,10 @@ def test_golden_residual_objective(golden):
 def test_golden_one_step(golden):
     for e in golden["one_step"]:
         Q = GOLDEN_MATRICES[e["matrix"]]()
+        jb = int(e["dmode"][6:]) if e["dmode"].startswith("jblock") else None
         r = oracle.solve(Q, np.array(e["b"], float), tol=0.0, maxit=1, restart=False,
-                         momentum=(e["dmode"] == "jdiag"), dmode=e["dmode"])
+                         momentum=(e["dmode"] != "qdiag"), dmode=e["dmode"] if jb is None else "jdiag",
+                         jblock=jb)
         np.testing.assert_allclose(r.x, e["expected_x1"], rtol=1e-15, err_msg=e["cite"])
 
 
@@ -446,3 +448,96 @@ def test_restart_window_and_doubling():
     assert r.restart_iters == [3, 8, 17, 34, 67, 132]
     r = oracle.solve(p.Q, p.b, tol=0.0, maxit=200, restart=True, k0=5, forced=forced)
     assert r.restart_iters == [6, 17, 38, 79, 160]
+
+
+# ------------------------------------------------------------------------------------------------
+# eq-J-blkdiag: block-diagonal J (R23)
+# ------------------------------------------------------------------------------------------------
+
+def _assemble(J, n):
+    """Dense n x n block-diagonal matrix from the (s, bs, bs) blocks (drops the identity pad)."""
+    s, bs, _ = J.shape
+    M = np.zeros((s * bs, s * bs))
+    for i in range(s):
+        M[i * bs:(i + 1) * bs, i * bs:(i + 1) * bs] = J[i]
+    return M[:n, :n]
+
+
+def test_golden_jblock(golden):
+    for e in golden["jblock"]:
+        J = oracle.build_jblock(GOLDEN_MATRICES[e["matrix"]](), e["bs"])
+        np.testing.assert_allclose(J, np.array(e["expected_blocks"]), rtol=0, atol=1e-14,
+                                   err_msg=e["cite"])
+
+
+def test_jblock_bs1_is_jdiag():
+    """bs = 1: ||[Q_ij]||_2 = |Q_ij|, so eq-J-blkdiag reduces to eq-J-diag, bitwise."""
+    for kind, Q in _instances("all")[::3] + [("p", synth.poisson3d(5)), ("a", synth.aniso27(4))]:
+        np.testing.assert_array_equal(oracle.build_jblock(Q, 1)[:, 0, 0], oracle.build_jdiag(Q))
+
+
+def test_jblock_single_block_is_q_and_solves_in_one_step():
+    """s = 1 (bs >= n): J = Q with no shift, so Alg. 3 line 4 from any y gives
+    y + Q^{-1}(b - Qy) = Q^{-1} b: converged after one iteration (dense Cholesky x*)."""
+    for k, n in enumerate([5, 12, 30]):
+        Q = synth.random_spd(n, seed=400 + k)
+        A = synth.to_dense(Q)
+        J = oracle.build_jblock(Q, n)
+        np.testing.assert_array_equal(J[0], A)
+        b = _rhs(A, k)
+        r = oracle.solve(Q, b, tol=1e-12, maxit=3, jblock=n)
+        assert r.status == "converged" and r.iterations == 1
+        np.testing.assert_allclose(r.x, sla.cho_solve(sla.cho_factor(A), b), rtol=1e-11, atol=1e-12)
+
+
+def test_jblock_stencil_closed_form():
+    """2D / 3D Dirichlet Laplacians with blocks of bs consecutive x-rows (bs | m): every
+    off-diagonal block is either -I (y/z neighbours) or a single -1 (x neighbour), both of
+    2-norm 1, so J^{ii} = Q^{ii} + (number of neighbouring blocks) I -- no SVD needed."""
+    for m, dim, bs in [(8, 2, 4), (8, 2, 2), (6, 3, 3), (8, 3, 8)]:
+        Q = synth.poisson2d(m) if dim == 2 else synth.poisson3d(m)
+        J = oracle.build_jblock(Q, bs)
+        A = synth.to_dense(Q)
+        nb = m // bs
+        for blk in range(Q.n // bs):
+            r0 = blk * bs
+            coords = np.unravel_index(r0, (m,) * dim)  # coords[-1] is the fastest (x) axis
+            cnt = 0
+            for ax in range(dim):
+                lim = nb if ax == dim - 1 else m
+                c = coords[ax] // bs if ax == dim - 1 else coords[ax]
+                cnt += int(c > 0) + int(c < lim - 1)
+            expect = A[r0:r0 + bs, r0:r0 + bs] + cnt * np.eye(bs)
+            np.testing.assert_array_equal(J[blk], expect)
+
+
+def test_jblock_s_psd_and_one_step_dense():
+    """S = J - Q is PSD for every tested block size, and the oracle's block
+    Cholesky step equals a dense solve with the assembled J (brute force)."""
+    for kind, Q in _instances("all")[::2]:
+        A = synth.to_dense(Q)
+        for bs in (2, 3, 4, 8):
+            Jd = _assemble(oracle.build_jblock(Q, bs), Q.n)
+            lam = np.linalg.eigvalsh(Jd - A)
+            assert lam.min() >= -1e-10 * max(1.0, np.abs(A).max()), (kind, Q.n, bs, lam.min())
+            b = _rhs(A, bs)
+            r = oracle.solve(Q, b, tol=0.0, maxit=1, restart=False, jblock=bs)
+            np.testing.assert_allclose(r.x, np.linalg.solve(Jd, b), rtol=1e-12, atol=1e-13)
+
+
+def test_jblock_thm23_bound():
+    """Thm 2.3 with the block-diagonal J of eq-J-blkdiag: S = J - Q."""
+    for kind, Q in _instances("all")[::2]:
+        A = synth.to_dense(Q)
+        b = _rhs(A, 17)
+        xs = _xstar(kind, A, b)
+        for bs in (2, 4):
+            S = _assemble(oracle.build_jblock(Q, bs), Q.n) - A
+            r = oracle.solve(Q, b, tol=0.0, maxit=300, restart=False, jblock=bs, record_iterates=True)
+            gap = _gap(A, b, xs, r.xt_hist)
+            fstar = -0.5 * b @ xs
+            slack = 1e-10 * max(1.0, abs(fstar))
+            e0 = r.xt_hist[0] - xs
+            t = np.arange(1, len(gap))
+            assert np.all(gap[1:] <= 2 * (e0 @ S @ e0) / (t + 1) ** 2 + slack), (kind, Q.n, bs)
+            assert np.all(gap[1:] >= -slack)
