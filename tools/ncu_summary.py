@@ -1,0 +1,72 @@
+"""Summarise per-config ncu --set full captures (gpurun_out/<tag>_ncu_cfgK.ncu-rep, the 2nd solve of
+tools/prof.py K 30 = 31 passes) into profiles/<tag>_ncu_configs.md and profiles/ncu_traffic.json.
+usage: python tools/ncu_summary.py TAG [K ...]"""
+import csv, io, json, os, subprocess, sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+NAMES = {1: "poisson2d_64", 2: "poisson3d_128", 3: "er_1m_deg16", 4: "chunglu_4m_deg20", 5: "aniso27_256"}
+PASSES = 31
+M = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+     "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
+     "sm__warps_active.avg.pct_of_peak_sustained_active", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+     "l1tex__throughput.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+     "smsp__average_warp_latency_issue_stalled_long_scoreboard"]
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1.0}
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    d = {}
+    for k in M:
+        if k in hdr:
+            i = hdr.index(k)
+            v = float(vals[i].replace(",", ""))
+            d[k] = v * SCALE.get(units[i], 1.0)
+    d["kernel"] = vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
+    return d
+
+
+def main():
+    tag = sys.argv[1]
+    cfgs = [int(c) for c in sys.argv[2:]] or [1, 2, 3, 4, 5]
+    import paper_2407_03272_b200 as ajm  # noqa: F401  (model bytes formula only)
+    import synth
+    lines = [f"# {tag} -- ncu --set full per BASELINE config (solver kernel, 2nd solve of "
+             f"tools/prof.py K 30 = {PASSES} passes)", "",
+             "| cfg | workload | µs/pass (profiled) | DRAM MB/pass | algorithmic MB/pass | DRAM/alg | L2 hit | "
+             "L1 hit | warps active | L2 thru | L1 thru |", "|---|---|---|---|---|---|---|---|---|---|---|"]
+    traffic = []
+    for c in cfgs:
+        rep = os.path.join(ROOT, "gpurun_out", f"{tag}_ncu_cfg{c}.ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        d = raw(rep)
+        if c == 1:
+            n, nnz = 4096, 20224
+        else:
+            p = synth.config_problem(c) if c in (2, 3) else None
+            n, nnz = {2: (2097152, 14581760), 5: (16777216, 449455096)}.get(c, (p.Q.n, p.Q.nnz) if p else (4000000, 80218976))
+        alg = 12.0 * nnz + 56.0 * n + 4.0 * (n + 1)
+        dram = (d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]) / PASSES
+        lines.append(f"| {c} | {NAMES[c]} | {1e6 * d['gpu__time_duration.sum'] / PASSES:.1f} | {dram / 1e6:.1f} | "
+                     f"{alg / 1e6:.1f} | {dram / alg:.2f} | {d['lts__t_sector_hit_rate.pct']:.1f}% | "
+                     f"{d['l1tex__t_sector_hit_rate.pct']:.1f}% | {d['sm__warps_active.avg.pct_of_peak_sustained_active']:.1f}% | "
+                     f"{d['lts__throughput.avg.pct_of_peak_sustained_elapsed']:.1f}% | "
+                     f"{d['l1tex__throughput.avg.pct_of_peak_sustained_active']:.1f}% |")
+        traffic.append({"workload": NAMES[c], "kernel": d["kernel"], "passes_profiled": PASSES,
+                        "dram_bytes_read": d["dram__bytes_read.sum"], "dram_bytes_write": d["dram__bytes_write.sum"],
+                        "dram_bytes_per_pass": dram, "algorithmic_bytes_per_pass": alg,
+                        "source": f"ncu --set full --clock-control none on tools/prof.py {c} 30 (2nd solve); "
+                                  f"profiles/{tag}_ncu_configs.md"})
+    with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_configs.md"), "w") as f:
+        f.write("\n".join(lines) + "\n")
+    with open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w") as f:
+        json.dump(traffic, f, indent=1)
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
