@@ -62,6 +62,9 @@ struct ajm_ctx {
     int64_t nseg = 0, nsplit = 0, seg_rows = 0, long_rows = 0;
     int sigma = 1;
     bool ident = true;
+    bool relabel = false;           // SELL slot order != caller's row order: vectors live in slot order
+    int* perm_fwd = nullptr;        // [n] internal (layout) index -> caller's row
+    int* perm_inv = nullptr;        // [n] caller's row -> internal index
     int variant = 0;
     SolveFn fn = nullptr;
     size_t dyn_smem = 0;
@@ -170,7 +173,7 @@ void free_all(ajm_ctx* h) {
                     h->sval, h->scol, h->chunk_off, h->perm, h->seg_row, h->seg_k0, h->seg_k1,
                     h->seg_split, h->seg_part, h->split_row, h->split_seg0, h->split_cnt,
                     h->cta_split, h->owner_split, h->unit_c0, h->cta_seg, h->seg_list, h->cta_unit, h->partials, h->ctrl,
-                    h->hist, h->scratch, h->err, h->ts};
+                    h->hist, h->scratch, h->err, h->ts, h->perm_fwd, h->perm_inv};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->h_ctrl) cudaFreeHost(h->h_ctrl);
@@ -374,9 +377,25 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         }
         h->n_sell = (int64_t)order.size();
         h->nchunks = (h->n_sell + 31) / 32;
-        h->ident = (h->sigma == 1 && split_rows.empty() && whole_rows.empty());
-        perm_h.assign((size_t)h->nchunks * 32, -1);
+        // Relabelling: the solver works in "internal" row numbering -- SELL rows in
+        // slot order, then the segment rows (split rows first) -- so every row operand of a SELL
+        // chunk is contiguous (coalesced / TMA-stageable) whatever the sorting window.  Values
+        // and the order of each row's entries are unchanged (the row sums are the same).
+        h->relabel = !(h->sigma == 1 && split_rows.empty() && whole_rows.empty());
+        h->ident = true;  // SELL slot == internal row
+        perm_h.assign((size_t)n, 0);
         for (size_t j = 0; j < order.size(); ++j) perm_h[j] = order[j];
+        {
+            size_t k = order.size();
+            for (int r : split_rows) perm_h[k++] = r;
+            for (int r : whole_rows) perm_h[k++] = r;
+        }
+        std::vector<int> inv_h;
+        if (h->relabel) {
+            inv_h.assign((size_t)n, 0);
+            for (int64_t k = 0; k < n; ++k) inv_h[(size_t)perm_h[(size_t)k]] = (int)k;
+        }
+        auto irow = [&](int r) { return h->relabel ? inv_h[(size_t)r] : r; };
         choff.assign((size_t)h->nchunks + 1, 0);
         chcost.assign((size_t)h->nchunks, 0.0);
         for (int64_t c = 0; c < h->nchunks; ++c) {
@@ -392,10 +411,10 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         // segments: split rows first (consecutive per row), then whole rows
         for (int r : split_rows) {
             const int sidx = (int)split_row_h.size();
-            split_row_h.push_back(r);
+            split_row_h.push_back(irow(r));
             split_seg0_h.push_back((int)seg_row_h.size());
             for (int64_t k = hrp[(size_t)r]; k < hrp[(size_t)r + 1]; k += AJM_SEG) {
-                seg_row_h.push_back(r);
+                seg_row_h.push_back(irow(r));
                 seg_k0_h.push_back((int)k);
                 seg_k1_h.push_back((int)std::min<int64_t>(k + AJM_SEG, hrp[(size_t)r + 1]));
                 seg_split_h.push_back(sidx);
@@ -403,7 +422,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         }
         split_seg0_h.push_back((int)seg_row_h.size());
         for (int r : whole_rows) {
-            seg_row_h.push_back(r);
+            seg_row_h.push_back(irow(r));
             seg_k0_h.push_back((int)hrp[(size_t)r]);
             seg_k1_h.push_back((int)hrp[(size_t)r + 1]);
             seg_split_h.push_back(-1);
@@ -411,6 +430,13 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         h->nseg = (int64_t)seg_row_h.size();
         h->nsplit = (int64_t)split_row_h.size();
         h->seg_rows = (int64_t)(split_rows.size() + whole_rows.size());
+        if (h->relabel) {
+            CC(dalloc(&h->perm_fwd, n));
+            CC(dalloc(&h->perm_inv, n));
+            CC(cudaMemcpyAsync(h->perm_fwd, perm_h.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+            CC(cudaMemcpyAsync(h->perm_inv, inv_h.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+            CC(cudaStreamSynchronize(st));
+        }
     }
     // ---- TMA staging units, persistent grid, cost-balanced CTA ranges ----
     std::vector<int> unit_c0_h, cta_seg_h, cta_unit_h, cta_split_h, owner_split_h, seg_list_h;
@@ -574,7 +600,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(dalloc(&h->sval, h->sell_elems));
     CC(dalloc(&h->scol, h->sell_elems));
     CC(dalloc(&h->chunk_off, h->nchunks + 1));
-    CC(dalloc(&h->perm, h->nchunks * 32));
+    CC(dalloc(&h->perm, 1));
     CC(dalloc(&h->seg_row, h->nseg));
     CC(dalloc(&h->seg_k0, h->nseg));
     CC(dalloc(&h->seg_k1, h->nseg));
@@ -615,7 +641,13 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         CC(cudaMemcpyAsync(h->col, col_idx, sizeof(int32_t) * nnz, kind_to_device(col_idx), st));
         CC(cudaMemcpyAsync(h->val, vals, sizeof(double) * nnz, kind_to_device(vals), st));
     }
-    CC(cudaMemcpyAsync(h->b, b, sizeof(double) * n, kind_to_device(b), st));
+    // b (and below D) arrive in the caller's row order; with relabelling they are gathered into
+    // internal order through the X[2] scratch buffer (free until the first solve)
+    CC(cudaMemcpyAsync(h->relabel ? h->X[2] : h->b, b, sizeof(double) * n, kind_to_device(b), st));
+    if (h->relabel) {
+        ajm_gather_kernel<<<1024, 256, 0, st>>>(n, h->perm_fwd, h->X[2], h->b);
+        CC(cudaGetLastError());
+    }
     double* dtmp = nullptr;
     if (dmode == AJM_D_USER) {
         CC(dalloc(&dtmp, n));
@@ -625,7 +657,6 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st) : cudaSuccess;
     };
     CC(h2d(h->chunk_off, choff.data(), sizeof(long long) * choff.size()));
-    CC(h2d(h->perm, perm_h.data(), sizeof(int) * perm_h.size()));
     CC(h2d(h->seg_row, seg_row_h.data(), sizeof(int) * seg_row_h.size()));
     CC(h2d(h->seg_k0, seg_k0_h.data(), sizeof(int) * seg_k0_h.size()));
     CC(h2d(h->seg_k1, seg_k1_h.data(), sizeof(int) * seg_k1_h.size()));
@@ -642,8 +673,13 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
 
     // ---- validation + D (device) ----
     const int nblk = (int)((n + 255) / 256);
-    ajm_validate_diag_kernel<<<nblk, 256, 0, st>>>((int)n, h->rp, h->col, h->val, dmode, dtmp, h->D, h->err);
+    ajm_validate_diag_kernel<<<nblk, 256, 0, st>>>((int)n, h->rp, h->col, h->val, dmode, dtmp,
+                                                   h->relabel ? h->X[2] : h->D, h->err);
     CC(cudaGetLastError());
+    if (h->relabel) {
+        ajm_gather_kernel<<<1024, 256, 0, st>>>(n, h->perm_fwd, h->X[2], h->D);
+        CC(cudaGetLastError());
+    }
     ajm_finite_kernel<<<1024, 256, 0, st>>>(n, h->b, h->err);
     CC(cudaGetLastError());
     int herr = 0;
@@ -661,10 +697,15 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         CC(cudaStreamSynchronize(st));
         if (herr & AJM_EB_ASYM) return bail(fail(h, AJM_ERR_NOT_SYMMETRIC, "Q is not symmetric"));
     }
-    // SELL copy of the short rows
+    // columns in internal numbering (after validation, which needs the caller's order)
+    if (h->relabel && nnz > 0) {
+        ajm_remap_kernel<<<2048, 256, 0, st>>>(nnz, h->perm_inv, h->col);
+        CC(cudaGetLastError());
+    }
+    // SELL copy of the short rows (slot -> caller's row through perm_fwd when relabelled)
     if (h->nchunks > 0) {
         const int ns = (int)(h->nchunks * 32);
-        ajm_sell_fill_kernel<<<(ns + 255) / 256, 256, 0, st>>>(ns, (int)h->n_sell, h->perm, h->ident ? 1 : 0,
+        ajm_sell_fill_kernel<<<(ns + 255) / 256, 256, 0, st>>>(ns, (int)h->n_sell, h->perm_fwd, h->relabel ? 0 : 1,
                                                                h->rp, h->col, h->val, h->chunk_off, h->sval, h->scol);
         CC(cudaGetLastError());
     }
@@ -704,7 +745,13 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
     // x~^0 = x0 and x^{-1} := x0 (beta_0 = 0 makes it unused); Q x^{-1} := 0 (finite, times 0)
     if (x0) {
         const cudaMemcpyKind k = kind_to_device(x0);
-        AJM_CUDA(h, cudaMemcpyAsync(h->X[0], x0, sizeof(double) * n, k, st));
+        if (h->relabel) {  // caller's order -> internal order (X[2] is free at this point)
+            AJM_CUDA(h, cudaMemcpyAsync(h->X[2], x0, sizeof(double) * n, k, st));
+            ajm_gather_kernel<<<1024, 256, 0, st>>>(n, h->perm_fwd, h->X[2], h->X[0]);
+            AJM_CUDA(h, cudaGetLastError());
+        } else {
+            AJM_CUDA(h, cudaMemcpyAsync(h->X[0], x0, sizeof(double) * n, k, st));
+        }
         AJM_CUDA(h, cudaMemsetAsync(h->err, 0, sizeof(int), st));
         ajm_finite_kernel<<<1024, 256, 0, st>>>(n, h->X[0], h->err);
         AJM_CUDA(h, cudaGetLastError());
@@ -780,7 +827,14 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
                     chk / np / 1e3);
     }
 
-    AJM_CUDA(h, cudaMemcpyAsync(x_out, h->X[c.s.answer], sizeof(double) * n, kind_from_device(x_out), st));
+    if (h->relabel) {  // internal order -> caller's order, through a buffer that is not the answer
+        double* tmp = h->X[(c.s.answer + 1) % 3];
+        ajm_gather_kernel<<<1024, 256, 0, st>>>(n, h->perm_inv, h->X[c.s.answer], tmp);
+        AJM_CUDA(h, cudaGetLastError());
+        AJM_CUDA(h, cudaMemcpyAsync(x_out, tmp, sizeof(double) * n, kind_from_device(x_out), st));
+    } else {
+        AJM_CUDA(h, cudaMemcpyAsync(x_out, h->X[c.s.answer], sizeof(double) * n, kind_from_device(x_out), st));
+    }
     const int64_t cnt = c.s.iterations + 1;
     if (res_hist) AJM_CUDA(h, cudaMemcpyAsync(res_hist, hr, sizeof(double) * cnt, kind_from_device(res_hist), st));
     if (f_hist) AJM_CUDA(h, cudaMemcpyAsync(f_hist, hf, sizeof(double) * cnt, kind_from_device(f_hist), st));
@@ -812,6 +866,16 @@ ajm_status_t ajm_get_trace(ajm_handle_t h, int32_t which, double* out, int64_t c
 
 ajm_status_t ajm_get_diag(ajm_handle_t h, double* out) {
     if (!h || !out) return fail(h, AJM_ERR_INVALID_ARG, "NULL argument");
+    if (h->relabel) {
+        double* tmp = nullptr;
+        AJM_CUDA(h, dalloc(&tmp, h->n));
+        ajm_gather_kernel<<<1024, 256>>>(h->n, h->perm_inv, h->D, tmp);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaMemcpy(out, tmp, sizeof(double) * h->n, kind_from_device(out));
+        cudaFree(tmp);
+        AJM_CUDA(h, e);
+        return AJM_OK;
+    }
     AJM_CUDA(h, cudaMemcpy(out, h->D, sizeof(double) * h->n, kind_from_device(out)));
     return AJM_OK;
 }

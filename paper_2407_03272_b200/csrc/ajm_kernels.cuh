@@ -919,6 +919,19 @@ __global__ void ajm_sell_fill_kernel(int nslots_padded, int n_sell, const int* _
     }
 }
 
+// dst[i] = src[idx[i]] (relabelling of n-vectors between the caller's row order and the layout's)
+__global__ void ajm_gather_kernel(long long n, const int* __restrict__ idx, const double* __restrict__ src,
+                                  double* __restrict__ dst) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+
+// col[k] = inv[col[k]]: column indices in the layout's row numbering (values and entry order unchanged)
+__global__ void ajm_remap_kernel(long long nnz, const int* __restrict__ inv, int* __restrict__ col) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < nnz; k += (long long)gridDim.x * blockDim.x)
+        col[k] = inv[col[k]];
+}
+
 // Per-solve initialisation of the control block (t = 0: x~^0 = x0, x^{-1} := x0, beta_0 = 0,
 // alpha_1 = 1, K = K_0, K_re = 0, ell = 0).
 __global__ void ajm_init_ctrl_kernel(AjmCtrl* c, double tol, long long maxit, int momentum,
