@@ -40,14 +40,16 @@ struct SolveVariant {
     int vstages;
     SolveFn fnd;  // no ring: SELL read directly (sorted-window layouts)
     const char* name;
+    SolveFn fng;  // gather ring (kMode 3): x~ gathers as cp.async into the stage, 1 CTA/SM
+    int gstages;
 };
 // TMA ring depth x register cap (=> resident CTAs per SM with 288 threads); AJM_KVARIANT selects
 // one (tuning); the default is the measured best on B200
 const SolveVariant kVariants[] = {
-    {ajm_solve_kernel<4, 96, 0>, 4, ajm_solve_kernel<3, 96, 1>, 3, ajm_solve_kernel<1, 128, 2>, "s4r96"},    // 2 CTAs/SM
-    {ajm_solve_kernel<3, 72, 0>, 3, ajm_solve_kernel<2, 72, 1>, 2, ajm_solve_kernel<1, 72, 2>, "s3r72"},     // 3 CTAs/SM
-    {ajm_solve_kernel<2, 56, 0>, 2, ajm_solve_kernel<2, 56, 1>, 2, ajm_solve_kernel<1, 56, 2>, "s2r56"},     // 4 CTAs/SM
-    {ajm_solve_kernel<6, 128, 0>, 6, ajm_solve_kernel<6, 128, 1>, 6, ajm_solve_kernel<1, 128, 2>, "s6r128"}, // 1 CTA/SM
+    {ajm_solve_kernel<4, 96, 0>, 4, ajm_solve_kernel<3, 96, 1>, 3, ajm_solve_kernel<1, 128, 2>, "s4r96", ajm_solve_kernel<4, 128, 3>, 4},    // 2 CTAs/SM
+    {ajm_solve_kernel<3, 72, 0>, 3, ajm_solve_kernel<2, 72, 1>, 2, ajm_solve_kernel<1, 72, 2>, "s3r72", ajm_solve_kernel<3, 128, 3>, 3},     // 3 CTAs/SM
+    {ajm_solve_kernel<2, 56, 0>, 2, ajm_solve_kernel<2, 56, 1>, 2, ajm_solve_kernel<1, 56, 2>, "s2r56", ajm_solve_kernel<2, 128, 3>, 2},     // 4 CTAs/SM
+    {ajm_solve_kernel<6, 128, 0>, 6, ajm_solve_kernel<6, 128, 1>, 6, ajm_solve_kernel<1, 128, 2>, "s6r128", ajm_solve_kernel<4, 128, 3>, 4}, // 1 CTA/SM
 };
 const int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -73,6 +75,7 @@ struct ajm_ctx {
     int l2_mode = 2;
     int vstage = 0;
     int direct = 0;
+    int gring = 0;                     // kMode 3 gather ring
     unsigned long long* ts = nullptr;  // debug phase timestamps (AJM_TS=1)
     double* vecs = nullptr;            // X0 X1 X2 Qxp b D, one allocation
     int l2persist = 1;
@@ -221,16 +224,20 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.l2_mode = h->l2_mode;
     p.vstage = h->vstage;
     p.ts = h->ts;
+    p.bid_rev = getenv("AJM_BID_REV") ? atoi(getenv("AJM_BID_REV")) : 0;
     p.direct_interleave = getenv("AJM_DIRECT_INTERLEAVE") ? atoi(getenv("AJM_DIRECT_INTERLEAVE")) : 0;
     return p;
 }
+
+// consumer warps + producer warp (+ gather warp in kMode 3); direct mode has no producer
+int block_threads(const ajm_ctx* h) { return h->direct ? AJM_BLOCK : (h->gring ? AJM_BLOCK + 32 + 32 * AJM_GWARPS : AJM_BLOCK + 32); }
 
 // cooperative launch of the persistent solver kernel, with the L2 access-policy window over the
 // iterate vectors (persisting hits, streaming misses)
 cudaError_t launch_solver(ajm_ctx* h, AjmPass& p, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(h->grid);
-    cfg.blockDim = dim3(h->direct ? AJM_BLOCK : AJM_BLOCK + 32);  // direct mode: no producer warp
+    cfg.blockDim = dim3(block_threads(h));
     cfg.dynamicSmemBytes = h->dyn_smem;
     cfg.stream = st;
     cudaLaunchAttribute at[2];
@@ -333,6 +340,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fnv, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fnd, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fng, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
 
     // ---- row-length-binned layout (host, O(n log sigma)) ----
     auto rlen = [&](int64_t r) { return hrp[(size_t)r + 1] - hrp[(size_t)r]; };
@@ -526,20 +534,27 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         if (!h->ident) h->vstage = 0;
         h->direct = 0;  // direct mode measured slower than the ring on every config so far
         if (const char* ev = getenv("AJM_DIRECT")) h->direct = atoi(ev) ? 1 : 0;
+        if (const char* ev = getenv("AJM_GRING")) h->gring = atoi(ev) ? 1 : 0;
         if (h->vstage) h->fn = kVariants[h->variant].fnv;
+        if (h->gring) {
+            h->fn = kVariants[h->variant].fng;
+            h->vstage = 0;
+            h->direct = 0;
+        }
         if (h->direct) {
             h->fn = kVariants[h->variant].fnd;
             h->vstage = 0;
         }
         // ring: val/col of a unit (+ the rows' five vector slices for natural-order layouts)
-        const size_t ring = h->direct ? 0 : (size_t)(h->vstage ? kVariants[h->variant].vstages : kVariants[h->variant].stages) *
+        const size_t ring = h->direct ? 0 : h->gring ? (size_t)kVariants[h->variant].gstages * ((size_t)AJM_UNIT_EL * 20 + (size_t)5 * AJM_UNIT_ROWS * 8)
+                          : (size_t)(h->vstage ? kVariants[h->variant].vstages : kVariants[h->variant].stages) *
                             ((size_t)AJM_UNIT_EL * 12 + (h->vstage ? (size_t)5 * AJM_UNIT_ROWS * 8 : 0));
         size_t meta = 4096;  // initial allowance, grown until the plan fits
         for (int iter = 0;; ++iter) {
             h->dyn_smem = ring + meta;
             CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem));
             int occ = 0;
-            CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->fn, h->direct ? AJM_BLOCK : AJM_BLOCK + 32,
+            CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->fn, block_threads(h),
                                                              h->dyn_smem));
             if (occ < 1) return bail(fail(h, AJM_ERR_UNSUPPORTED, "solver kernel cannot be resident (%zu B smem)", h->dyn_smem));
             h->ctas_per_sm = occ;
@@ -620,8 +635,8 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(dalloc(&h->scratch, 512));
     CC(dalloc(&h->err, 1));
     if (getenv("AJM_TS")) {
-        CC(dalloc(&h->ts, 64 * 8));
-        CC(cudaMemsetAsync(h->ts, 0, 64 * 8 * sizeof(unsigned long long), st));
+        CC(dalloc(&h->ts, 512 + 2 * (size_t)h->grid));
+        CC(cudaMemsetAsync(h->ts, 0, (512 + 2 * (size_t)h->grid) * sizeof(unsigned long long), st));
     }
     CC(cudaMallocHost((void**)&h->h_ctrl, sizeof(AjmCtrl)));
     CC(cudaEventCreate(&h->ev0));
@@ -820,6 +835,23 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
             chk += (double)(hts[k * 8 + 7] - hts[k * 8 + 6]);
             ++np;
         }
+        std::vector<unsigned long long> cta((size_t)2 * h->grid);
+        AJM_CUDA(h, cudaMemcpy(cta.data(), h->ts + 512, sizeof(unsigned long long) * cta.size(), cudaMemcpyDeviceToHost));
+        if (c.s.iterations >= 6 && hts[5 * 8]) {  // pass-5 work-end of every CTA relative to the pass start
+            std::vector<std::pair<double, int>> endt;
+            for (int g = 0; g < h->grid; ++g)
+                endt.push_back({(double)(cta[(size_t)2 * g] - hts[5 * 8]) / 1e3, (int)cta[(size_t)2 * g + 1]});
+            std::sort(endt.begin(), endt.end());
+            auto q = [&](double f) { return endt[(size_t)std::min<double>(endt.size() - 1, f * (endt.size() - 1))]; };
+            fprintf(stderr, "[ajm ts] pass 5 CTA work-end us: min %.2f (sm %d) p10 %.2f p50 %.2f p90 %.2f max %.2f (sm %d)\n",
+                    endt.front().first, endt.front().second, q(0.1).first, q(0.5).first, q(0.9).first,
+                    endt.back().first, endt.back().second);
+            if (getenv("AJM_TS_ALL")) {
+                for (int g = 0; g < h->grid; ++g)
+                    fprintf(stderr, "[ajm cta] %d sm %d end %.2f\n", g, (int)cta[(size_t)2 * g + 1],
+                            (double)(cta[(size_t)2 * g] - hts[5 * 8]) / 1e3);
+            }
+        }
         if (np)
             fprintf(stderr, "[ajm ts] passes %d: work %.2f us, block-reduce %.2f, grid-barrier %.2f, "
                             "partials %.2f, control+sync %.2f | segments %.2f, chunks %.2f\n", np, acc[0] / np / 1e3,
@@ -901,7 +933,7 @@ ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info) {
     info->variant = h->variant;
     info->l2_window_bytes = (int64_t)h->win_bytes;
     info->l2_hit_ratio = h->win_hit;
-    info->mode = h->direct ? 2 : (h->vstage ? 1 : 0);
+    info->mode = h->gring ? 3 : h->direct ? 2 : (h->vstage ? 1 : 0);
     info->sell_elems = h->sell_elems;
     return AJM_OK;
 }

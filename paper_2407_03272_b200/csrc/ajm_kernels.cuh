@@ -40,6 +40,7 @@
 #define AJM_UNIT_EL 2048 // SELL elements per TMA staging unit (24 KB of val + col)
 #define AJM_UNIT_ROWS (AJM_WARPS * 32)  // rows per staging unit (<= 8 chunks)
 #define AJM_LOG_CAP 64
+#define AJM_GWARPS 4     // gather warps per CTA in kMode 3
 
 // Iteration state: identical copies in every CTA (shared memory) and in global memory.
 struct AjmState {
@@ -117,6 +118,7 @@ struct AjmPass {
     int vstage;                              // stage the rows' vector slices too (needs ident)
     unsigned long long* ts;                  // debug: per-pass phase timestamps of CTA 0 (or null)
     int direct_interleave;                   // direct mode: chunk j -> warp j%8 (else contiguous)
+    int bid_rev;                             // experiment: CTA g takes work range G-1-g
 };
 
 __device__ __forceinline__ unsigned long long ajm_gtime() {
@@ -504,7 +506,28 @@ __device__ __forceinline__ void ajm_chunk_direct(const AjmPass& p, int ch, int w
 //                   only once the pass that owns the unit has started (after the grid barrier).
 // A stage's full barrier completes when both parts have landed.
 // kMode: 0 TMA ring of val/col; 1 ring + the rows' vector slices (natural order only);
-//        2 no ring, SELL read directly by the consumer warps (sorted-window layouts).
+//        2 no ring, SELL read directly by the consumer warps (sorted-window layouts);
+//        3 "gather ring": as 1, plus a gather warp that, once a unit's columns have landed and
+//          its pass has started, issues the unit's x~ gathers as asynchronous 8-byte copies
+//          (cp.async, LDGSTS) straight into the stage, and the bulk copies of the rows'
+//          x~^t / x^{t-1} / Q x^{t-1} slices; both complete on the stage's "gathered" mbarrier.
+//          The consumer warps then run from shared memory only (no register-bound gather
+//          batches: every gather of a unit is in flight at once).
+__device__ __forceinline__ void ajm_cp_async8(void* dst_smem, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(ajm_smem(dst_smem)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void ajm_cp_async_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(ajm_smem(bar)) : "memory");
+}
+
+// SELL chunk dot from shared memory: val and the gathered x~ values side by side in the stage
+__device__ __forceinline__ double ajm_chunk_dot_smem(const double* sv, const double* sx, int w) {
+    double s = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < w; ++k) s += sv[k * 32] * sx[k * 32];  // ascending column order
+    return s;
+}
+
 template <int kStages, int kMaxReg, int kMode>
 __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     extern __shared__ __align__(128) unsigned char s_dyn[];
@@ -516,22 +539,33 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     __shared__ volatile int s_stop;
     __shared__ volatile int s_pass;     // passes (of this launch) whose dynamic vectors may be staged
     __shared__ volatile int s_bufc, s_bufp;  // x~^t / x^{t-1} buffer indices of pass s_pass
+    __shared__ volatile int s_endpass;       // (kMode 3) first pass that never runs, -1 while running
+    __shared__ __align__(8) uint64_t s_gath[kStages];
     __shared__ int s_to;
 
     AjmCtrl* c = p.ctrl;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, bid = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int bid = p.bid_rev ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x;  // (experiment knob)
     const unsigned G = gridDim.x;
     const int u0 = p.cta_unit[bid], u1 = p.cta_unit[bid + 1];
     const int nunits = u1 - u0;
-    constexpr bool vstage = (kMode == 1);  // natural order only: the unit's rows are contiguous
+    constexpr bool gring = (kMode == 3);
+    constexpr bool vstage = (kMode == 1);  // the unit's rows are contiguous (internal numbering)
+    constexpr bool vecs = vstage || gring; // row operands staged in shared memory
     constexpr bool direct = (kMode == 2);
-    // stage s: val[UNIT_EL] f64 | col[UNIT_EL] i32 | (vstage) b, D, x~, x^{t-1}, Qx^{t-1} [256] f64
-    const size_t stage_bytes = (size_t)AJM_UNIT_EL * 12 + (vstage ? (size_t)5 * AJM_UNIT_ROWS * 8 : 0);
+    // stage s: val[UNIT_EL] f64 | col[UNIT_EL] i32 | (vecs) b, D, x~, x^{t-1}, Qx^{t-1} [256] f64
+    //          | (gring) gathered x~[col] [UNIT_EL] f64
+    const size_t stage_bytes = (size_t)AJM_UNIT_EL * 12 + (vecs ? (size_t)5 * AJM_UNIT_ROWS * 8 : 0) +
+                               (gring ? (size_t)AJM_UNIT_EL * 8 : 0);
     auto st_val = [&](int k) { return reinterpret_cast<double*>(s_dyn + (size_t)k * stage_bytes); };
     auto st_col = [&](int k) { return reinterpret_cast<int*>(s_dyn + (size_t)k * stage_bytes + (size_t)AJM_UNIT_EL * 8); };
     auto st_vec = [&](int k, int which) {
         return reinterpret_cast<double*>(s_dyn + (size_t)k * stage_bytes + (size_t)AJM_UNIT_EL * 12 +
                                          (size_t)which * AJM_UNIT_ROWS * 8);
+    };
+    auto st_xg = [&](int k) {
+        return reinterpret_cast<double*>(s_dyn + (size_t)k * stage_bytes + (size_t)AJM_UNIT_EL * 12 +
+                                         (size_t)5 * AJM_UNIT_ROWS * 8);
     };
     // static per-CTA SELL metadata, loaded once: unit -> first chunk, chunk -> element offset
     // (relative to this CTA's first chunk / element), so the pass never chases global pointers
@@ -548,9 +582,11 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         s_pass = 0;
         s_bufc = s_st.cur;
         s_bufp = s_st.prev;
+        s_endpass = -1;
         for (int k = 0; k < kStages; ++k) {
             ajm_mbar_init(&s_full[k], 1);
             ajm_mbar_init(&s_empty[k], AJM_WARPS);
+            ajm_mbar_init(&s_gath[k], AJM_GWARPS * 32 + 1);  // cp.async arrivals + one expect_tx arrival
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -591,11 +627,11 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                         const int uu = (int)(cnt % nunits);
                         const int e0 = s_coff[s_uc0[uu]], e1 = s_coff[s_uc0[uu + 1]];
                         const unsigned ne = (unsigned)(e1 - e0);
-                        const unsigned vbytes = vstage ? (unsigned)(s_uc0[uu + 1] - s_uc0[uu]) * 32u * 8u : 0u;
-                        ajm_mbar_expect_tx(&s_full[stage], ne * 12u + 5u * vbytes);
+                        const unsigned vbytes = vecs ? (unsigned)(s_uc0[uu + 1] - s_uc0[uu]) * 32u * 8u : 0u;
+                        ajm_mbar_expect_tx(&s_full[stage], ne * 12u + (vstage ? 5u : 2u) * vbytes);
                         ajm_bulk_g2s(st_val(stage), p.sval + efirst + e0, ne * 8u, &s_full[stage], qpol);
                         ajm_bulk_g2s(st_col(stage), p.scol + efirst + e0, ne * 4u, &s_full[stage], qpol);
-                        if (vstage) {
+                        if (vecs) {
                             const int r0 = (cfirst + s_uc0[uu]) * 32;
                             ajm_bulk_g2s(st_vec(stage, 0), p.b + r0, vbytes, &s_full[stage], vpol);
                             ajm_bulk_g2s(st_vec(stage, 1), p.D + r0, vbytes, &s_full[stage], vpol);
@@ -617,6 +653,57 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
             }
             for (long long k = (long long)s_pass * nunits; k < cnt; ++k)
                 if (k >= 0) ajm_mbar_wait(&s_full[k % kStages], (unsigned)((k / kStages) & 1), &c->timeout_flag);
+        }
+        return;
+    }
+
+    if (gring && warp > AJM_WARPS) {
+        // ---------------- gather warp (kMode 3) ----------------
+        // unit k (this CTA's k-th staged unit, pass k / nunits): once its columns have landed
+        // (full) and its pass has started (x~ final after the grid barrier), lane 0 bulk-copies
+        // the rows' x~^t, x^{t-1}, Q x^{t-1} slices and all 32 lanes issue the unit's gathers
+        // x~[col[e]] -> stage as 8-byte cp.async; everything completes on s_gath[stage].
+        if (nunits > 0) {
+            const uint64_t vpol = ajm_policy(p.l2_mode >= 2 ? 2 : 0);
+            const long long total = (long long)nunits * p.max_passes;
+            for (long long k = 0; k < total; ++k) {
+                const long long kp = k / nunits;
+                long long spins = 0;
+                bool quit = false;
+                while ((long long)s_pass < kp) {
+                    if (s_stop || ++spins > (1LL << 31)) { quit = true; break; }
+                }
+                if (quit || (s_endpass >= 0 && kp >= (long long)s_endpass)) break;
+                const int stage = (int)(k % kStages);
+                ajm_mbar_wait(&s_full[stage], (unsigned)((k / kStages) & 1), &c->timeout_flag);
+                const int uu = (int)(k % nunits);
+                const int e0 = s_coff[s_uc0[uu]], ne = s_coff[s_uc0[uu + 1]] - e0;
+                const double* xcur = ajm_sel(p, s_bufc);
+                const int gt = (warp - AJM_WARPS - 1) * 32 + lane;
+                if (gt == 0) {
+                    const int r0 = (cfirst + s_uc0[uu]) * 32;
+                    const unsigned bytes = (unsigned)(s_uc0[uu + 1] - s_uc0[uu]) * 32u * 8u;
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    ajm_mbar_expect_tx(&s_gath[stage], 3u * bytes);
+                    ajm_bulk_g2s(st_vec(stage, 2), xcur + r0, bytes, &s_gath[stage], vpol);
+                    ajm_bulk_g2s(st_vec(stage, 3), ajm_sel(p, s_bufp) + r0, bytes, &s_gath[stage], vpol);
+                    ajm_bulk_g2s(st_vec(stage, 4), p.Qxp + r0, bytes, &s_gath[stage], vpol);
+                }
+                const int* sc = st_col(stage);
+                double* xg = st_xg(stage);
+                constexpr int GS = AJM_GWARPS * 32;
+                int e = gt;
+                for (; e + 3 * GS < ne; e += 4 * GS) {
+                    const int c0 = sc[e], c1 = sc[e + GS], c2 = sc[e + 2 * GS], c3 = sc[e + 3 * GS];
+                    ajm_cp_async8(xg + e, xcur + c0);
+                    ajm_cp_async8(xg + e + GS, xcur + c1);
+                    ajm_cp_async8(xg + e + 2 * GS, xcur + c2);
+                    ajm_cp_async8(xg + e + 3 * GS, xcur + c3);
+                }
+                for (; e < ne; e += GS) ajm_cp_async8(xg + e, xcur + sc[e]);
+                ajm_cp_async_arrive_noinc(&s_gath[stage]);
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
         }
         return;
     }
@@ -682,7 +769,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                     const int slot = (cfirst + j) * 32 + lane;
                     int row;
                     double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
-                    if (vstage) {
+                    if (vecs) {
                         row = slot < p.n_sell ? slot : -1;
                     } else {
                         row = p.ident ? (slot < p.n_sell ? slot : -1) : __ldg(p.perm + slot);
@@ -695,7 +782,8 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                         }
                     }
                     ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);
-                    if (vstage) {
+                    if (gring) ajm_mbar_wait(&s_gath[stage], par, &c->timeout_flag);
+                    if (vecs) {
                         const int ri = (j - s_uc0[uu]) * 32 + lane;
                         bi = st_vec(stage, 0)[ri];
                         Di = st_vec(stage, 1)[ri];
@@ -704,7 +792,8 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                         qxp = st_vec(stage, 4)[ri];
                     }
                     const int off = (e0 - s_coff[s_uc0[uu]]) + lane;
-                    const double q = ajm_chunk_dot(st_val(stage) + off, st_col(stage) + off, w, xc);
+                    const double q = gring ? ajm_chunk_dot_smem(st_val(stage) + off, st_xg(stage) + off, w)
+                                           : ajm_chunk_dot(st_val(stage) + off, st_col(stage) + off, w, xc);
                     if (row >= 0) ajm_row_update(p.Qxp, xf, row, q, bi, Di, xt, xpi, qxp, beta, restart_t, acc, vpol);
                 } else {
                     ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);  // keep the phases in step
@@ -734,6 +823,12 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         }
         // (4) CTA partial -> grid barrier -> every CTA reduces all partials in the same order
         if (tsw) p.ts[pass * 8 + 1] = ajm_gtime();
+        if (p.ts && tid == 0 && pass == 5) {  // debug: every CTA's work-end time and SM of pass 5
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            p.ts[512 + 2 * bid] = ajm_gtime();
+            p.ts[512 + 2 * bid + 1] = smid;
+        }
         ajm_block_reduce(acc, s_red);
         if (tsw) p.ts[pass * 8 + 2] = ajm_gtime();
         // partials as 5 arrays of G (SoA) so the all-CTA read below is coalesced
@@ -788,6 +883,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         ajm_csync();
     }
     if (tid == 0) {
+        s_endpass = pass;  // (kMode 3) the gather warp must not start pass >= pass
         __threadfence_block();
         s_pass = pass;  // units of passes >= pass were never consumed
         __threadfence_block();
