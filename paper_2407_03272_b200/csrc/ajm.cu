@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdarg>
@@ -115,7 +116,8 @@ struct ajm_ctx {
     int64_t hist_cap = 0;
     double* scratch = nullptr;  // reductions at create
     int* err = nullptr;
-    AjmCtrl* h_ctrl = nullptr;  // pinned
+    AjmCtrl* h_ctrl = nullptr;  // host copy of the control block
+    double* b_in = nullptr;     // b as given (caller's order), until the layout exists
     double nb = 0.0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double last_loop_ms = 0.0;
@@ -166,9 +168,42 @@ cudaMemcpyKind kind_from_device(const void* dst) {
     return is_device_ptr(dst) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
 }
 
+// Device memory comes from a library-owned stream-ordered pool that keeps freed memory (release
+// threshold = max), so the allocations of a create after a destroy cost no cudaMalloc and a
+// destroy costs no synchronising cudaFree.
+cudaMemPool_t ajm_pool(int dev) {
+    static cudaMemPool_t pools[64] = {};
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (!pools[dev]) {
+        cudaMemPoolProps pp = {};
+        pp.allocType = cudaMemAllocationTypePinned;
+        pp.handleTypes = cudaMemHandleTypeNone;
+        pp.location.type = cudaMemLocationTypeDevice;
+        pp.location.id = dev;
+        cudaMemPool_t mp = nullptr;
+        if (cudaMemPoolCreate(&mp, &pp) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+        pools[dev] = mp;
+    }
+    return pools[dev];
+}
+
 template <class T>
-cudaError_t dalloc(T** p, size_t count) {
-    return cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T));
+cudaError_t dalloc(T** p, size_t count, cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t mp = ajm_pool(dev);
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    if (!mp) return cudaMalloc((void**)p, bytes);
+    return cudaMallocFromPoolAsync((void**)p, bytes, mp, s);
+}
+
+void dfree(void* p) {
+    if (p) cudaFreeAsync(p, 0);  // nothing of the handle is in flight when it is freed
 }
 
 void free_all(ajm_ctx* h) {
@@ -176,10 +211,9 @@ void free_all(ajm_ctx* h) {
                     h->sval, h->scol, h->chunk_off, h->perm, h->seg_row, h->seg_k0, h->seg_k1,
                     h->seg_split, h->seg_part, h->split_row, h->split_seg0, h->split_cnt,
                     h->cta_split, h->owner_split, h->unit_c0, h->cta_seg, h->seg_list, h->cta_unit, h->partials, h->ctrl,
-                    h->hist, h->scratch, h->err, h->ts, h->perm_fwd, h->perm_inv};
-    for (void* p : ptrs)
-        if (p) cudaFree(p);
-    if (h->h_ctrl) cudaFreeHost(h->h_ctrl);
+                    h->hist, h->scratch, h->err, h->ts, h->perm_fwd, h->perm_inv, h->b_in};
+    for (void* p : ptrs) dfree(p);
+    if (h->h_ctrl) free(h->h_ctrl);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
 }
@@ -258,14 +292,14 @@ cudaError_t launch_solver(ajm_ctx* h, AjmPass& p, cudaStream_t st) {
     return cudaLaunchKernelEx(&cfg, h->fn, p);
 }
 
-ajm_status_t ensure_hist(ajm_ctx* h, int64_t need) {
+ajm_status_t ensure_hist(ajm_ctx* h, int64_t need, cudaStream_t st) {
     if (need <= h->hist_cap) return AJM_OK;
     if (h->hist) {
-        AJM_CUDA(h, cudaFree(h->hist));
+        dfree(h->hist);
         h->hist = nullptr;
     }
     int64_t cap = std::max<int64_t>(need, 1024);
-    AJM_CUDA(h, dalloc(&h->hist, (size_t)cap * 4));
+    AJM_CUDA(h, dalloc(&h->hist, (size_t)cap * 4, st));
     h->hist_cap = cap;
     return AJM_OK;
 }
@@ -284,6 +318,19 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
                         const int32_t* col_idx, const double* vals, const double* b, int32_t dmode,
                         const double* d, uint32_t flags, void* cuda_stream) {
     g_create_error.clear();
+    // debug (AJM_TS): host wall time of each create phase
+    const bool tsc = getenv("AJM_TS") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    std::string tsc_log;
+    auto mark = [&](const char* what, cudaStream_t s_) {
+        if (!tsc) return;
+        if (s_ != (cudaStream_t)-1) cudaStreamSynchronize(s_);
+        auto now = std::chrono::steady_clock::now();
+        char b[96];
+        snprintf(b, sizeof b, " %s %.2f", what, std::chrono::duration<double, std::milli>(now - t_last).count());
+        tsc_log += b;
+        t_last = now;
+    };
     if (!out) return fail(nullptr, AJM_ERR_INVALID_ARG, "out is NULL");
     if (n < 1 || nnz < 0) return fail(nullptr, AJM_ERR_INVALID_ARG, "n must be >= 1 and nnz >= 0");
     if (n >= (int64_t)1 << 31 || nnz >= (int64_t)1 << 31)
@@ -294,13 +341,16 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     if (dmode == AJM_D_USER && !d) return fail(nullptr, AJM_ERR_INVALID_ARG, "AJM_D_USER needs d");
     cudaStream_t st = (cudaStream_t)cuda_stream;
 
-    // host scan of row_ptr (needed anyway for the layout)
-    std::vector<int64_t> hrp((size_t)n + 1);
-    {
-        cudaError_t e = cudaMemcpyAsync(hrp.data(), row_ptr, sizeof(int64_t) * (n + 1),
-                                        is_device_ptr(row_ptr) ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost, st);
+    // host scan of row_ptr (needed anyway for the layout); read in place when it is host memory
+    const bool rp_dev = is_device_ptr(row_ptr);
+    std::vector<int64_t> hrp_copy;
+    const int64_t* hrp = row_ptr;
+    if (rp_dev) {
+        hrp_copy.resize((size_t)n + 1);
+        cudaError_t e = cudaMemcpyAsync(hrp_copy.data(), row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return fail(nullptr, AJM_ERR_CUDA, "row_ptr copy: %s", cudaGetErrorString(e));
+        hrp = hrp_copy.data();
     }
     if (hrp[0] != 0) return fail(nullptr, AJM_ERR_CSR_INVALID, "row_ptr[0] = %lld != 0", (long long)hrp[0]);
     for (int64_t i = 0; i < n; ++i)
@@ -309,6 +359,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     if (hrp[n] != nnz)
         return fail(nullptr, AJM_ERR_CSR_INVALID, "row_ptr[n] = %lld != nnz = %lld", (long long)hrp[n], (long long)nnz);
 
+    mark("rowptr", st);
     ajm_ctx* h = new ajm_ctx();
     h->n = n;
     h->nnz = nnz;
@@ -334,7 +385,8 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     if (!coop) return bail(fail(h, AJM_ERR_UNSUPPORTED, "device does not support cooperative launch"));
     if (const char* ev = getenv("AJM_KVARIANT")) h->variant = std::max(0, std::min(kNumVariants - 1, atoi(ev)));
     h->fn = kVariants[h->variant].fn;
-    if (const char* ev = getenv("AJM_L2MODE")) h->l2_mode = std::max(0, std::min(2, atoi(ev)));
+    int l2_env = -1;
+    if (const char* ev = getenv("AJM_L2MODE")) l2_env = std::max(0, std::min(3, atoi(ev)));
     if (const char* ev = getenv("AJM_VSTAGE")) h->vstage = atoi(ev) ? 1 : 0;
     if (const char* ev = getenv("AJM_L2PERSIST")) h->l2persist = atoi(ev) ? 1 : 0;
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -342,12 +394,67 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fnd, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fng, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
 
+    // ---- the CSR arrays and b go to the device now; the copies overlap the host planning ----
+    CC(dalloc(&h->rp, n + 1, st));
+    CC(dalloc(&h->col, nnz + 8, st));
+    CC(dalloc(&h->val, nnz + 8, st));
+    CC(dalloc(&h->b_in, n, st));
+    if (rp_dev) {
+        ajm_rowptr_narrow_kernel<<<1024, 256, 0, st>>>(n + 1, (const long long*)row_ptr, h->rp);
+        CC(cudaGetLastError());
+    } else {
+        int64_t* rp64 = nullptr;
+        CC(dalloc(&rp64, n + 1, st));
+        CC(cudaMemcpyAsync(rp64, hrp, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
+        ajm_rowptr_narrow_kernel<<<1024, 256, 0, st>>>(n + 1, (const long long*)rp64, h->rp);
+        CC(cudaGetLastError());
+        CC(cudaFreeAsync(rp64, st));
+    }
+    if (nnz > 0) {
+        CC(cudaMemcpyAsync(h->col, col_idx, sizeof(int32_t) * nnz, kind_to_device(col_idx), st));
+        CC(cudaMemcpyAsync(h->val, vals, sizeof(double) * nnz, kind_to_device(vals), st));
+    }
+    CC(cudaMemcpyAsync(h->b_in, b, sizeof(double) * n, kind_to_device(b), st));
+    mark("h2d-issue", st);
+
     // ---- row-length-binned layout (host, O(n log sigma)) ----
     auto rlen = [&](int64_t r) { return hrp[(size_t)r + 1] - hrp[(size_t)r]; };
     std::vector<int> perm_h, seg_row_h, seg_k0_h, seg_k1_h, seg_split_h, split_row_h, split_seg0_h;
     std::vector<long long> choff;
     std::vector<double> chcost;
+    // fast path (stencil-like matrices): every row short and natural order pads < 5% -> SELL-32
+    // in natural order, no relabelling, no segments; one pass over the row lengths
+    bool fast = false;
     {
+        const int64_t nch = (n + 31) / 32;
+        std::vector<long long> fo((size_t)nch + 1, 0);
+        std::vector<double> fc((size_t)nch, 0.0);
+        int64_t maxlen = 0;
+        for (int64_t c = 0; c < nch; ++c) {
+            int64_t w = 1;
+            const int64_t r1 = std::min<int64_t>(n, c * 32 + 32);
+            for (int64_t r = c * 32; r < r1; ++r) w = std::max<int64_t>(w, rlen(r));
+            maxlen = std::max(maxlen, w);
+            fo[(size_t)c + 1] = fo[(size_t)c] + 32 * w;
+            fc[(size_t)c] = 12.0 * 32 * w + 56.0 * (double)(r1 - c * 32) + 64.0;
+        }
+        if (maxlen <= AJM_SELL_MAX && (double)fo.back() <= 1.05 * (double)std::max<int64_t>(nnz, 1)) {
+            fast = true;
+            h->long_rows = 0;
+            h->sigma = 1;
+            h->n_sell = n;
+            h->nchunks = nch;
+            h->relabel = false;
+            h->ident = true;
+            choff.swap(fo);
+            chcost.swap(fc);
+            h->sell_elems = choff.back();
+            split_seg0_h.push_back(0);
+            h->nseg = h->nsplit = h->seg_rows = 0;
+        }
+        mark("L-fast", (cudaStream_t)-1);
+    }
+    if (!fast) {
         std::vector<int> short_rows, split_rows, whole_rows;
         short_rows.reserve((size_t)n);
         for (int64_t i = 0; i < n; ++i) {
@@ -357,6 +464,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             else split_rows.push_back((int)i);
         }
         h->long_rows = (int64_t)split_rows.size();
+        mark("L-bins", (cudaStream_t)-1);
         auto padded = [&](const std::vector<int>& order) {
             int64_t tot = 0;
             for (size_t c0 = 0; c0 < order.size(); c0 += 32) {
@@ -383,6 +491,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
                 lo = hi;
             }
         }
+        mark("L-sort", (cudaStream_t)-1);
         h->n_sell = (int64_t)order.size();
         h->nchunks = (h->n_sell + 31) / 32;
         // Relabelling: the solver works in "internal" row numbering -- SELL rows in
@@ -404,6 +513,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             for (int64_t k = 0; k < n; ++k) inv_h[(size_t)perm_h[(size_t)k]] = (int)k;
         }
         auto irow = [&](int r) { return h->relabel ? inv_h[(size_t)r] : r; };
+        mark("L-perm", (cudaStream_t)-1);
         choff.assign((size_t)h->nchunks + 1, 0);
         chcost.assign((size_t)h->nchunks, 0.0);
         for (int64_t c = 0; c < h->nchunks; ++c) {
@@ -416,6 +526,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             chcost[(size_t)c] = 12.0 * 32 * w + 56.0 * rows + 64.0;
         }
         h->sell_elems = choff.back();
+        mark("L-chunks", (cudaStream_t)-1);
         // segments: split rows first (consecutive per row), then whole rows
         for (int r : split_rows) {
             const int sidx = (int)split_row_h.size();
@@ -439,13 +550,14 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         h->nsplit = (int64_t)split_row_h.size();
         h->seg_rows = (int64_t)(split_rows.size() + whole_rows.size());
         if (h->relabel) {
-            CC(dalloc(&h->perm_fwd, n));
-            CC(dalloc(&h->perm_inv, n));
+            CC(dalloc(&h->perm_fwd, n, st));
+            CC(dalloc(&h->perm_inv, n, st));
             CC(cudaMemcpyAsync(h->perm_fwd, perm_h.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
             CC(cudaMemcpyAsync(h->perm_inv, inv_h.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
             CC(cudaStreamSynchronize(st));
         }
     }
+    mark("layout", st);
     // ---- TMA staging units, persistent grid, cost-balanced CTA ranges ----
     std::vector<int> unit_c0_h, cta_seg_h, cta_unit_h, cta_split_h, owner_split_h, seg_list_h;
     {
@@ -581,14 +693,12 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         }
     }
 
+    mark("plan", st);
     // ---- device allocations ----
-    CC(dalloc(&h->rp, n + 1));
-    CC(dalloc(&h->col, nnz));
-    CC(dalloc(&h->val, nnz));
     // the six n-vectors in ONE allocation [X0 X1 X2 Qxp b D] (each padded to whole SELL chunks,
     // 256-byte aligned): the L2 persistence window below covers them with a single range
     h->n_pad = (std::max<int64_t>(n, h->nchunks * 32) + 31) / 32 * 32;
-    CC(dalloc(&h->vecs, (size_t)6 * h->n_pad));
+    CC(dalloc(&h->vecs, (size_t)6 * h->n_pad, st));
     CC(cudaMemsetAsync(h->vecs, 0, sizeof(double) * 6 * h->n_pad, st));
     for (int k = 0; k < 3; ++k) h->X[k] = h->vecs + (size_t)k * h->n_pad;
     h->Qxp = h->vecs + (size_t)3 * h->n_pad;
@@ -608,64 +718,65 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             CC(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
             if (cur < persist) CC(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
             CC(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
-            h->win_bytes = std::min<size_t>(vec_bytes, (size_t)maxw);
+            // all six vectors when they (nearly) fit the carve-out; otherwise only the three
+            // rotating iterate buffers X0..X2 (the gathered x~ lives there) and b, D, Qx are
+            // streamed with evict_first (l2_mode 3)
+            // measured: mode 2 when all six vectors fit the carve-out, else mode 3
+            h->l2_mode = vec_bytes <= cur ? 2 : 3;
+            if (l2_env >= 0) h->l2_mode = l2_env;
+            const size_t wb = h->l2_mode == 3 ? sizeof(double) * 3 * (size_t)h->n_pad : vec_bytes;
+            h->win_bytes = std::min<size_t>(wb, (size_t)maxw);
             h->win_hit = (float)std::min(1.0, (double)cur / (double)h->win_bytes);
         }
+    } else if (l2_env >= 0) {
+        h->l2_mode = l2_env;
     }
-    CC(dalloc(&h->sval, h->sell_elems));
-    CC(dalloc(&h->scol, h->sell_elems));
-    CC(dalloc(&h->chunk_off, h->nchunks + 1));
-    CC(dalloc(&h->perm, 1));
-    CC(dalloc(&h->seg_row, h->nseg));
-    CC(dalloc(&h->seg_k0, h->nseg));
-    CC(dalloc(&h->seg_k1, h->nseg));
-    CC(dalloc(&h->seg_split, h->nseg));
-    CC(dalloc(&h->seg_part, h->nseg));
-    CC(dalloc(&h->split_row, h->nsplit));
-    CC(dalloc(&h->split_seg0, h->nsplit + 1));
-    CC(dalloc(&h->split_cnt, h->nsplit));
-    CC(dalloc(&h->cta_split, h->grid + 1));
-    CC(dalloc(&h->owner_split, h->nsplit));
-    CC(dalloc(&h->unit_c0, unit_c0_h.size()));
-    CC(dalloc(&h->cta_seg, cta_seg_h.size()));
-    CC(dalloc(&h->seg_list, seg_list_h.size()));
-    CC(dalloc(&h->cta_unit, cta_unit_h.size()));
-    CC(dalloc(&h->partials, (size_t)2 * h->grid * AJM_NPART));
-    CC(dalloc(&h->ctrl, 1));
-    CC(dalloc(&h->scratch, 512));
-    CC(dalloc(&h->err, 1));
+    CC(dalloc(&h->sval, h->sell_elems, st));
+    CC(dalloc(&h->scol, h->sell_elems, st));
+    CC(dalloc(&h->chunk_off, h->nchunks + 1, st));
+    CC(dalloc(&h->perm, 1, st));
+    CC(dalloc(&h->seg_row, h->nseg, st));
+    CC(dalloc(&h->seg_k0, h->nseg, st));
+    CC(dalloc(&h->seg_k1, h->nseg, st));
+    CC(dalloc(&h->seg_split, h->nseg, st));
+    CC(dalloc(&h->seg_part, h->nseg, st));
+    CC(dalloc(&h->split_row, h->nsplit, st));
+    CC(dalloc(&h->split_seg0, h->nsplit + 1, st));
+    CC(dalloc(&h->split_cnt, h->nsplit, st));
+    CC(dalloc(&h->cta_split, h->grid + 1, st));
+    CC(dalloc(&h->owner_split, h->nsplit, st));
+    CC(dalloc(&h->unit_c0, unit_c0_h.size(), st));
+    CC(dalloc(&h->cta_seg, cta_seg_h.size(), st));
+    CC(dalloc(&h->seg_list, seg_list_h.size(), st));
+    CC(dalloc(&h->cta_unit, cta_unit_h.size(), st));
+    CC(dalloc(&h->partials, (size_t)2 * h->grid * AJM_NPART, st));
+    CC(dalloc(&h->ctrl, 1, st));
+    CC(dalloc(&h->scratch, 512, st));
+    CC(dalloc(&h->err, 1, st));
     if (getenv("AJM_TS")) {
-        CC(dalloc(&h->ts, 512 + 2 * (size_t)h->grid));
+        CC(dalloc(&h->ts, 512 + 2 * (size_t)h->grid, st));
         CC(cudaMemsetAsync(h->ts, 0, (512 + 2 * (size_t)h->grid) * sizeof(unsigned long long), st));
     }
-    CC(cudaMallocHost((void**)&h->h_ctrl, sizeof(AjmCtrl)));
+    h->h_ctrl = (AjmCtrl*)malloc(sizeof(AjmCtrl));
+    if (!h->h_ctrl) return bail(fail(h, AJM_ERR_OOM, "host allocation failed"));
     CC(cudaEventCreate(&h->ev0));
     CC(cudaEventCreate(&h->ev1));
 
+    mark("alloc", st);
     // ---- copies ----
-    {
-        int64_t* rp64 = nullptr;
-        CC(dalloc(&rp64, n + 1));
-        CC(cudaMemcpyAsync(rp64, hrp.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
-        ajm_rowptr_narrow_kernel<<<1024, 256, 0, st>>>(n + 1, (const long long*)rp64, h->rp);
-        CC(cudaGetLastError());
-        CC(cudaStreamSynchronize(st));
-        cudaFree(rp64);
-    }
-    if (nnz > 0) {
-        CC(cudaMemcpyAsync(h->col, col_idx, sizeof(int32_t) * nnz, kind_to_device(col_idx), st));
-        CC(cudaMemcpyAsync(h->val, vals, sizeof(double) * nnz, kind_to_device(vals), st));
-    }
     // b (and below D) arrive in the caller's row order; with relabelling they are gathered into
-    // internal order through the X[2] scratch buffer (free until the first solve)
-    CC(cudaMemcpyAsync(h->relabel ? h->X[2] : h->b, b, sizeof(double) * n, kind_to_device(b), st));
+    // internal order (D through the X[2] scratch buffer, free until the first solve)
     if (h->relabel) {
-        ajm_gather_kernel<<<1024, 256, 0, st>>>(n, h->perm_fwd, h->X[2], h->b);
+        ajm_gather_kernel<<<1024, 256, 0, st>>>(n, h->perm_fwd, h->b_in, h->b);
         CC(cudaGetLastError());
+    } else {
+        CC(cudaMemcpyAsync(h->b, h->b_in, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     }
+    CC(cudaFreeAsync(h->b_in, st));
+    h->b_in = nullptr;
     double* dtmp = nullptr;
     if (dmode == AJM_D_USER) {
-        CC(dalloc(&dtmp, n));
+        CC(dalloc(&dtmp, n, st));
         CC(cudaMemcpyAsync(dtmp, d, sizeof(double) * n, kind_to_device(d), st));
     }
     auto h2d = [&](void* dst, const void* src, size_t bytes) {
@@ -686,6 +797,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(h2d(h->cta_unit, cta_unit_h.data(), sizeof(int) * cta_unit_h.size()));
     CC(cudaMemsetAsync(h->err, 0, sizeof(int), st));
 
+    mark("copies", st);
     // ---- validation + D (device) ----
     const int nblk = (int)((n + 255) / 256);
     ajm_validate_diag_kernel<<<nblk, 256, 0, st>>>((int)n, h->rp, h->col, h->val, dmode, dtmp,
@@ -700,7 +812,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     int herr = 0;
     CC(cudaMemcpyAsync(&herr, h->err, sizeof(int), cudaMemcpyDeviceToHost, st));
     CC(cudaStreamSynchronize(st));
-    if (dtmp) cudaFree(dtmp);
+    if (dtmp) cudaFreeAsync(dtmp, st);
     if (herr & AJM_EB_CSR) return bail(fail(h, AJM_ERR_CSR_INVALID, "column index out of range or not strictly increasing"));
     if (herr & AJM_EB_NONFINITE) return bail(fail(h, AJM_ERR_NONFINITE, "non-finite value in Q, b or d"));
     if (herr & AJM_EB_NEGDIAG) return bail(fail(h, AJM_ERR_NEGATIVE_DIAG, "negative diagonal entry: Q is not SPSD"));
@@ -733,6 +845,8 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(cudaStreamSynchronize(st));
     if (!(bb > 0.0)) return bail(fail(h, AJM_ERR_ZERO_RHS, "||b|| = 0: relative residual undefined"));
     h->nb = std::sqrt(bb);
+    mark("validate+fill+norm", st);
+    if (tsc) fprintf(stderr, "[ajm create ms]%s\n", tsc_log.c_str());
     *out = h;
 #undef CC
     return AJM_OK;
@@ -754,7 +868,7 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
     if (restart_iters && restart_cap < 0) return fail(h, AJM_ERR_INVALID_ARG, "restart_cap < 0");
     cudaStream_t st = (cudaStream_t)cuda_stream;
     const int64_t n = h->n;
-    ajm_status_t s = ensure_hist(h, maxit + 2);
+    ajm_status_t s = ensure_hist(h, maxit + 2, st);
     if (s != AJM_OK) return s;
 
     // x~^0 = x0 and x^{-1} := x0 (beta_0 = 0 makes it unused); Q x^{-1} := 0 (finite, times 0)
@@ -900,11 +1014,11 @@ ajm_status_t ajm_get_diag(ajm_handle_t h, double* out) {
     if (!h || !out) return fail(h, AJM_ERR_INVALID_ARG, "NULL argument");
     if (h->relabel) {
         double* tmp = nullptr;
-        AJM_CUDA(h, dalloc(&tmp, h->n));
+        AJM_CUDA(h, dalloc(&tmp, h->n, (cudaStream_t)0));
         ajm_gather_kernel<<<1024, 256>>>(h->n, h->perm_inv, h->D, tmp);
         cudaError_t e = cudaGetLastError();
         if (e == cudaSuccess) e = cudaMemcpy(out, tmp, sizeof(double) * h->n, kind_from_device(out));
-        cudaFree(tmp);
+        dfree(tmp);
         AJM_CUDA(h, e);
         return AJM_OK;
     }

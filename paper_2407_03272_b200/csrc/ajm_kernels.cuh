@@ -114,7 +114,9 @@ struct AjmPass {
     int max_passes;                          // passes this launch (debug host loop: 1)
     int meta_units;                          // smem capacity for a CTA's unit table (+1)
     int meta_chunks;                         // smem capacity for a CTA's chunk offsets (+1)
-    int l2_mode;                             // 0 none, 1 Q evict_first, 2 + vectors evict_last
+    int l2_mode;                             // 0 none, 1 Q evict_first, 2 + vectors evict_last,
+                                             // 3 = 1 + only the iterate x~ evict_last (b, D, Qx streamed
+                                             //     evict_first): vectors larger than the L2 carve-out
     int vstage;                              // stage the rows' vector slices too (needs ident)
     unsigned long long* ts;                  // debug: per-pass phase timestamps of CTA 0 (or null)
     int direct_interleave;                   // direct mode: chunk j -> warp j%8 (else contiguous)
@@ -166,7 +168,7 @@ __device__ __forceinline__ void ajm_stp(double* p, double v, uint64_t pol) {
 __device__ __forceinline__ void ajm_row_update(double* __restrict__ Qxp, double* __restrict__ xf,
                                                int i, double q, double bi, double Di, double xt,
                                                double xpi, double qxp, double beta, int restart_t,
-                                               AjmAcc& a, uint64_t pol) {
+                                               AjmAcc& a, uint64_t pol, uint64_t xpol) {
     const double r = bi - q;
     a.rr += r * r;
     a.xq += xt * q;
@@ -183,7 +185,7 @@ __device__ __forceinline__ void ajm_row_update(double* __restrict__ Qxp, double*
         xnow = xpi;
     }
     const double xn = y + (bi - qy) / Di;
-    ajm_stp(xf + i, xn, pol);
+    ajm_stp(xf + i, xn, xpol);
     const double term = (qy - bi) * (xn - xnow);
     a.d += term;
     a.dabs += fabs(term);
@@ -218,9 +220,10 @@ __device__ __forceinline__ void ajm_row_update_plain(double* __restrict__ Qxp, d
 __device__ __forceinline__ void ajm_row_epilogue(const AjmPass& p, int i, double q, double beta,
                                                  int restart_t, const double* xc, const double* xp,
                                                  double* xf, AjmAcc& a) {
-    const uint64_t pol = ajm_policy(p.l2_mode >= 2 ? 2 : 0);
+    const uint64_t pol = ajm_policy(p.l2_mode == 3 ? 1 : (p.l2_mode >= 2 ? 2 : 0));
+    const uint64_t xpol = ajm_policy(p.l2_mode >= 2 ? 2 : 0);
     ajm_row_update(p.Qxp, xf, i, q, ajm_ldp(p.b + i, pol), ajm_ldp(p.D + i, pol), ajm_ld(xc + i),
-                   ajm_ld(xp + i), ajm_ldp(p.Qxp + i, pol), beta, restart_t, a, pol);
+                   ajm_ld(xp + i), ajm_ldp(p.Qxp + i, pol), beta, restart_t, a, pol, xpol);
 }
 
 __device__ __forceinline__ double* ajm_sel(const AjmPass& p, int k) {
@@ -709,7 +712,8 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     }
 
     // ---------------- consumer warps ----------------
-    const uint64_t vpol = ajm_policy(p.l2_mode >= 2 ? 2 : 0);
+    const uint64_t vpol = ajm_policy(p.l2_mode == 3 ? 1 : (p.l2_mode >= 2 ? 2 : 0));  // b, D, Qx
+    const uint64_t xpol = ajm_policy(p.l2_mode >= 2 ? 2 : 0);                         // x~^{t+1}
     const int sg0 = p.cta_seg[bid], sg1 = p.cta_seg[bid + 1];
     const int sp0 = p.cta_split[bid], sp1 = p.cta_split[bid + 1];
     long long ucnt = 0;  // units consumed by this CTA (all passes)
@@ -794,7 +798,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                     const int off = (e0 - s_coff[s_uc0[uu]]) + lane;
                     const double q = gring ? ajm_chunk_dot_smem(st_val(stage) + off, st_xg(stage) + off, w)
                                            : ajm_chunk_dot(st_val(stage) + off, st_col(stage) + off, w, xc);
-                    if (row >= 0) ajm_row_update(p.Qxp, xf, row, q, bi, Di, xt, xpi, qxp, beta, restart_t, acc, vpol);
+                    if (row >= 0) ajm_row_update(p.Qxp, xf, row, q, bi, Di, xt, xpi, qxp, beta, restart_t, acc, vpol, xpol);
                 } else {
                     ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);  // keep the phases in step
                 }
