@@ -55,7 +55,14 @@ typedef enum {
                         the device, summed in ascending column order.  S = J - Q is PSD,
                         which is what Thm 2.3 / 2.5 need.  The default and the paper's experiments. */
     AJM_D_USER = 1,  /* the caller's positive diagonal d[n], e.g. diag(Q)/omega for weighted Jacobi */
-    AJM_D_QDIAG = 2  /* D = diag(Q): classical Jacobi metric; no S >= 0 guarantee */
+    AJM_D_QDIAG = 2, /* D = diag(Q): classical Jacobi metric; no S >= 0 guarantee */
+    AJM_D_JBLOCK = 3 /* block-diagonal J of eq-J-blkdiag: contiguous row blocks of bs rows
+                        (bs = AJM_JBLOCK_SIZE in the create flags; the last block ragged),
+                        J^{ii} = Q^{ii} + (sum_{j != i} ||Q^{ij}||_2) I, the spectral norms summed in
+                        ascending j; the step applies J^{-1} block by block (Alg. 3 line 4).  S = J - Q
+                        is PSD.  Requires every row to have <= 64 nonzeros (the blocks are
+                        solved inside a warp); otherwise AJM_ERR_UNSUPPORTED.  A block that is not SPD
+                        gives AJM_ERR_ZERO_DIAG.  DESIGN.md R23. */
 } ajm_dmode_t;
 
 /* ajm_create flags */
@@ -63,6 +70,9 @@ typedef enum {
 #define AJM_LOOP_HOST 0x10u        /* debug: one solver-kernel launch per pass, driven by the host,
                                       instead of the single persistent launch (same kernel, same
                                       results bit for bit)                                          */
+/* block size of AJM_D_JBLOCK, bits 8..15 of the flags: bs in {1, 2, 4, 8, 16, 32} */
+#define AJM_JBLOCK_SIZE(bs) (((uint32_t)(bs) & 0xffu) << 8)
+#define AJM_JBLOCK_SIZE_OF(flags) (((uint32_t)(flags) >> 8) & 0xffu)
 
 /* Iteration policy. */
 typedef struct {
@@ -122,7 +132,7 @@ typedef struct {
  *   b         : double[n], consistent right-hand side (b in range(Q) is assumed, not checked)
  *   dmode     : ajm_dmode_t
  *   d         : double[n] (> 0) for AJM_D_USER, otherwise ignored (may be NULL)
- *   flags     : AJM_VALIDATE_SYMMETRY | AJM_LOOP_HOST
+ *   flags     : AJM_VALIDATE_SYMMETRY | AJM_LOOP_HOST | AJM_JBLOCK_SIZE(bs) (AJM_D_JBLOCK only)
  * Ownership: the handle deep-copies (and re-lays-out) Q, b and D into device memory it owns; the
  * caller's buffers may be freed when the call returns.
  */
@@ -161,8 +171,14 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
  */
 ajm_status_t ajm_get_trace(ajm_handle_t h, int32_t which, double* out, int64_t count);
 
-/* ajm_get_diag -- copy the diagonal metric D actually used (J for AJM_D_JDIAG) to out[n] (host/device). */
+/* ajm_get_diag -- copy the diagonal metric D actually used (J for AJM_D_JDIAG; the diagonal of the
+ * block J for AJM_D_JBLOCK) to out[n] (host/device). */
 ajm_status_t ajm_get_diag(ajm_handle_t h, double* out);
+
+/* ajm_get_jblock -- AJM_D_JBLOCK handles only: copy the blocks J^{ii} of eq-J-blkdiag to
+ * out[s * bs * bs] (host/device), s = ceil(n / bs), block i row-major at out + i*bs*bs; the ragged
+ * last block is padded with the identity.  Other handles: AJM_ERR_INVALID_ARG. */
+ajm_status_t ajm_get_jblock(ajm_handle_t h, double* out);
 
 /* ajm_get_info -- layout and last-solve timing facts. */
 ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info);

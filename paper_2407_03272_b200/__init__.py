@@ -28,13 +28,18 @@ STATUS_NAMES = {0: "AJM_OK", 1: "AJM_ERR_INVALID_ARG", 2: "AJM_ERR_CSR_INVALID",
                 6: "AJM_ERR_ZERO_DIAG", 7: "AJM_ERR_ZERO_RHS", 8: "AJM_ERR_CUDA", 9: "AJM_ERR_OOM",
                 10: "AJM_ERR_UNSUPPORTED"}
 TERM_NAMES = {0: "converged", 1: "maxiter", 2: "diverged"}
-D_MODES = {"jdiag": 0, "user": 1, "qdiag": 2}
+D_MODES = {"jdiag": 0, "user": 1, "qdiag": 2, "jblock": 3}
 AJM_VALIDATE_SYMMETRY = 0x1
 AJM_LOOP_HOST = 0x10
 
+
+def AJM_JBLOCK_SIZE(bs: int) -> int:
+    """Create-flag bits carrying the eq-J-blkdiag block size (include/ajm.h)."""
+    return (int(bs) & 0xFF) << 8
+
 # every symbol include/ajm.h declares (tests check the .so exports all of them)
-ABI_SYMBOLS = ["ajm_create", "ajm_solve", "ajm_get_trace", "ajm_get_diag", "ajm_get_info",
-               "ajm_destroy", "ajm_last_error", "ajm_abi_version"]
+ABI_SYMBOLS = ["ajm_create", "ajm_solve", "ajm_get_trace", "ajm_get_diag", "ajm_get_jblock",
+               "ajm_get_info", "ajm_destroy", "ajm_last_error", "ajm_abi_version"]
 
 
 class AjmError(RuntimeError):
@@ -91,6 +96,8 @@ def lib():
         L.ajm_get_trace.restype = ctypes.c_int
         L.ajm_get_diag.argtypes = [P, P]
         L.ajm_get_diag.restype = ctypes.c_int
+        L.ajm_get_jblock.argtypes = [P, P]
+        L.ajm_get_jblock.restype = ctypes.c_int
         L.ajm_get_info.argtypes = [P, ctypes.POINTER(ajm_info_t)]
         L.ajm_get_info.restype = ctypes.c_int
         L.ajm_destroy.argtypes = [P]
@@ -200,13 +207,18 @@ class Solver:
     (device arrays are copied device->device).  The solver owns its device copy afterwards."""
 
     def __init__(self, n, row_ptr, col, val, b, dmode="jdiag", d=None, validate_symmetry=False,
-                 loop="graph", stream=None):
+                 loop="graph", stream=None, jblock=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2407_03272_b200 needs a CUDA device (no CPU fallback)")
         self.n = int(n)
         self.nnz = int(row_ptr[-1])
         flags = (AJM_VALIDATE_SYMMETRY if validate_symmetry else 0) | (AJM_LOOP_HOST if loop == "host" else 0)
+        self.jblock = None
+        if jblock is not None:  # eq-J-blkdiag with bs-row blocks (AJM_D_JBLOCK)
+            dmode = "jblock"
+            flags |= AJM_JBLOCK_SIZE(jblock)
+            self.jblock = int(jblock)
         self._stream = stream
         self.handle = ajm_create(self.n, self.nnz, row_ptr, col, val, b, dmode, d, flags, stream)
 
@@ -243,6 +255,17 @@ class Solver:
         _check(lib().ajm_get_diag(ctypes.c_void_p(self.handle), out.ctypes.data_as(ctypes.c_void_p)),
                ctypes.c_void_p(self.handle))
         return out
+
+    def jblocks(self) -> np.ndarray:
+        """The blocks J^{ii} of eq-J-blkdiag built by the library, shape (s, bs, bs)."""
+        if not self.jblock:
+            raise ValueError("solver was not created with jblock=bs")
+        bs = self.jblock
+        s = (self.n + bs - 1) // bs
+        out = np.empty(s * bs * bs)
+        _check(lib().ajm_get_jblock(ctypes.c_void_p(self.handle), out.ctypes.data_as(ctypes.c_void_p)),
+               ctypes.c_void_p(self.handle))
+        return out.reshape(s, bs, bs)
 
     def info(self) -> dict:
         inf = ajm_info_t()

@@ -118,6 +118,10 @@ struct ajm_ctx {
     int* err = nullptr;
     AjmCtrl* h_ctrl = nullptr;  // host copy of the control block
     double* b_in = nullptr;     // b as given (caller's order), until the layout exists
+    int dmode = 0;
+    int jbs = 0;                // AJM_D_JBLOCK block size (0: diagonal metric)
+    double* Jblk = nullptr;     // [s][bs][bs] blocks of eq-J-blkdiag
+    double* Jinv = nullptr;     // rows of their inverses, per SELL chunk [bs][32]
     double nb = 0.0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double last_loop_ms = 0.0;
@@ -211,7 +215,7 @@ void free_all(ajm_ctx* h) {
                     h->sval, h->scol, h->chunk_off, h->perm, h->seg_row, h->seg_k0, h->seg_k1,
                     h->seg_split, h->seg_part, h->split_row, h->split_seg0, h->split_cnt,
                     h->cta_split, h->owner_split, h->unit_c0, h->cta_seg, h->seg_list, h->cta_unit, h->partials, h->ctrl,
-                    h->hist, h->scratch, h->err, h->ts, h->perm_fwd, h->perm_inv, h->b_in};
+                    h->hist, h->scratch, h->err, h->ts, h->perm_fwd, h->perm_inv, h->b_in, h->Jblk, h->Jinv};
     for (void* p : ptrs) dfree(p);
     if (h->h_ctrl) free(h->h_ctrl);
     if (h->ev0) cudaEventDestroy(h->ev0);
@@ -259,6 +263,8 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.vstage = h->vstage;
     p.ts = h->ts;
     p.bid_rev = getenv("AJM_BID_REV") ? atoi(getenv("AJM_BID_REV")) : 0;
+    p.Jinv = h->Jinv;
+    p.jbs = h->jbs;
     p.direct_interleave = getenv("AJM_DIRECT_INTERLEAVE") ? atoi(getenv("AJM_DIRECT_INTERLEAVE")) : 0;
     return p;
 }
@@ -337,7 +343,10 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         return fail(nullptr, AJM_ERR_UNSUPPORTED, "n and nnz must be < 2^31 (int32 device offsets)");
     if (!row_ptr || !b || (nnz > 0 && (!col_idx || !vals)))
         return fail(nullptr, AJM_ERR_INVALID_ARG, "NULL array argument");
-    if (dmode < 0 || dmode > 2) return fail(nullptr, AJM_ERR_INVALID_ARG, "bad dmode %d", dmode);
+    if (dmode < 0 || dmode > 3) return fail(nullptr, AJM_ERR_INVALID_ARG, "bad dmode %d", dmode);
+    const int jbs = dmode == AJM_D_JBLOCK ? (int)AJM_JBLOCK_SIZE_OF(flags) : 0;
+    if (dmode == AJM_D_JBLOCK && (jbs < 1 || jbs > 32 || (jbs & (jbs - 1))))
+        return fail(nullptr, AJM_ERR_INVALID_ARG, "AJM_D_JBLOCK needs AJM_JBLOCK_SIZE(bs) with bs in {1,2,4,8,16,32}");
     if (dmode == AJM_D_USER && !d) return fail(nullptr, AJM_ERR_INVALID_ARG, "AJM_D_USER needs d");
     cudaStream_t st = (cudaStream_t)cuda_stream;
 
@@ -364,6 +373,8 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     h->n = n;
     h->nnz = nnz;
     h->flags = flags;
+    h->dmode = dmode;
+    h->jbs = jbs;
     auto bail = [&](ajm_status_t s) {
         g_create_error = h->err_msg;
         free_all(h);
@@ -438,7 +449,11 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             fo[(size_t)c + 1] = fo[(size_t)c] + 32 * w;
             fc[(size_t)c] = 12.0 * 32 * w + 56.0 * (double)(r1 - c * 32) + 64.0;
         }
-        if (maxlen <= AJM_SELL_MAX && (double)fo.back() <= 1.05 * (double)std::max<int64_t>(nnz, 1)) {
+        if (jbs && maxlen > AJM_SELL_MAX)
+            return bail(fail(h, AJM_ERR_UNSUPPORTED, "AJM_D_JBLOCK needs every row to have <= %d nonzeros "
+                                                       "(the longest has %lld)", AJM_SELL_MAX, (long long)maxlen));
+        // block-diagonal J solves each block inside a warp: natural order whatever the padding
+        if (maxlen <= AJM_SELL_MAX && (jbs || (double)fo.back() <= 1.05 * (double)std::max<int64_t>(nnz, 1))) {
             fast = true;
             h->long_rows = 0;
             h->sigma = 1;
@@ -648,6 +663,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         if (const char* ev = getenv("AJM_DIRECT")) h->direct = atoi(ev) ? 1 : 0;
         if (const char* ev = getenv("AJM_GRING")) h->gring = atoi(ev) ? 1 : 0;
         if (h->vstage) h->fn = kVariants[h->variant].fnv;
+        if (h->jbs) h->gring = 0, h->direct = 0;
         if (h->gring) {
             h->fn = kVariants[h->variant].fng;
             h->vstage = 0;
@@ -800,7 +816,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     mark("copies", st);
     // ---- validation + D (device) ----
     const int nblk = (int)((n + 255) / 256);
-    ajm_validate_diag_kernel<<<nblk, 256, 0, st>>>((int)n, h->rp, h->col, h->val, dmode, dtmp,
+    ajm_validate_diag_kernel<<<nblk, 256, 0, st>>>((int)n, h->rp, h->col, h->val, dmode == AJM_D_JBLOCK ? 0 : dmode, dtmp,
                                                    h->relabel ? h->X[2] : h->D, h->err);
     CC(cudaGetLastError());
     if (h->relabel) {
@@ -823,6 +839,27 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         CC(cudaMemcpyAsync(&herr, h->err, sizeof(int), cudaMemcpyDeviceToHost, st));
         CC(cudaStreamSynchronize(st));
         if (herr & AJM_EB_ASYM) return bail(fail(h, AJM_ERR_NOT_SYMMETRIC, "Q is not symmetric"));
+    }
+    // eq-J-blkdiag: blocks, their inverses (per-chunk rows) and D = diag(J)
+    if (h->jbs) {
+        const int64_t sblk = (n + jbs - 1) / jbs;
+        CC(dalloc(&h->Jblk, (size_t)sblk * jbs * jbs, st));
+        CC(dalloc(&h->Jinv, (size_t)h->nchunks * jbs * 32, st));
+        CC(cudaMemsetAsync(h->Jinv, 0, sizeof(double) * (size_t)h->nchunks * jbs * 32, st));
+        const int tb = 64, gb = (int)((sblk + tb - 1) / tb);
+        switch (jbs) {
+            case 1: ajm_jblock_build_kernel<1><<<gb, tb, 0, st>>>((int)n, h->rp, h->col, h->val, h->Jblk, h->Jinv, h->D, h->err); break;
+            case 2: ajm_jblock_build_kernel<2><<<gb, tb, 0, st>>>((int)n, h->rp, h->col, h->val, h->Jblk, h->Jinv, h->D, h->err); break;
+            case 4: ajm_jblock_build_kernel<4><<<gb, tb, 0, st>>>((int)n, h->rp, h->col, h->val, h->Jblk, h->Jinv, h->D, h->err); break;
+            case 8: ajm_jblock_build_kernel<8><<<gb, tb, 0, st>>>((int)n, h->rp, h->col, h->val, h->Jblk, h->Jinv, h->D, h->err); break;
+            case 16: ajm_jblock_build_kernel<16><<<gb, tb, 0, st>>>((int)n, h->rp, h->col, h->val, h->Jblk, h->Jinv, h->D, h->err); break;
+            default: ajm_jblock_build_kernel<32><<<gb, tb, 0, st>>>((int)n, h->rp, h->col, h->val, h->Jblk, h->Jinv, h->D, h->err); break;
+        }
+        CC(cudaGetLastError());
+        CC(cudaMemcpyAsync(&herr, h->err, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CC(cudaStreamSynchronize(st));
+        if (herr & AJM_EB_JBLOCK)
+            return bail(fail(h, AJM_ERR_ZERO_DIAG, "a block J^{ii} of eq-J-blkdiag is not positive definite"));
     }
     // columns in internal numbering (after validation, which needs the caller's order)
     if (h->relabel && nnz > 0) {
@@ -1026,6 +1063,14 @@ ajm_status_t ajm_get_diag(ajm_handle_t h, double* out) {
     return AJM_OK;
 }
 
+ajm_status_t ajm_get_jblock(ajm_handle_t h, double* out) {
+    if (!h || !out) return fail(h, AJM_ERR_INVALID_ARG, "NULL argument");
+    if (!h->jbs) return fail(h, AJM_ERR_INVALID_ARG, "handle was not created with AJM_D_JBLOCK");
+    const size_t cnt = (size_t)((h->n + h->jbs - 1) / h->jbs) * h->jbs * h->jbs;
+    AJM_CUDA(h, cudaMemcpy(out, h->Jblk, sizeof(double) * cnt, kind_from_device(out)));
+    return AJM_OK;
+}
+
 ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info) {
     if (!h || !info) return fail(h, AJM_ERR_INVALID_ARG, "NULL argument");
     info->n = h->n;
@@ -1036,7 +1081,9 @@ ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info) {
     info->block = AJM_BLOCK;
     info->sm_count = h->sm_count;
     info->ctas_per_sm = h->ctas_per_sm;
-    info->model_bytes_per_iter = 12.0 * (double)h->nnz + 56.0 * (double)h->n + 4.0 * (double)(h->n + 1);
+    // the diagonal D (8 B/row) is replaced by bs doubles per row of J^{-1} for AJM_D_JBLOCK
+    info->model_bytes_per_iter = 12.0 * (double)h->nnz + (48.0 + 8.0 * (h->jbs ? h->jbs : 1)) * (double)h->n +
+                                 4.0 * (double)(h->n + 1);
     info->last_loop_ms = h->last_loop_ms;
     info->last_passes = h->last_passes;
     info->last_launches = h->last_launches;

@@ -30,6 +30,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <climits>
 #include <stdint.h>
 
 #define AJM_BLOCK 256
@@ -121,6 +122,8 @@ struct AjmPass {
     unsigned long long* ts;                  // debug: per-pass phase timestamps of CTA 0 (or null)
     int direct_interleave;                   // direct mode: chunk j -> warp j%8 (else contiguous)
     int bid_rev;                             // experiment: CTA g takes work range G-1-g
+    const double* __restrict__ Jinv;         // AJM_D_JBLOCK: rows of the block inverses, per chunk [bs][32]
+    int jbs;                                 // AJM_D_JBLOCK block size (0: diagonal D)
 };
 
 __device__ __forceinline__ unsigned long long ajm_gtime() {
@@ -212,6 +215,45 @@ __device__ __forceinline__ void ajm_row_update_plain(double* __restrict__ Qxp, d
     }
     const double xn = y + (bi - qy) / Di;
     xf[i] = xn;
+    const double term = (qy - bi) * (xn - xnow);
+    a.d += term;
+    a.dabs += fabs(term);
+}
+
+// a3-a6 with the block-diagonal J of eq-J-blkdiag: x~^{t+1} = y + J^{-1}(b - Qy),
+// J^{-1} applied inside the warp -- the bs rows of a block are bs consecutive lanes of one SELL
+// chunk (natural order), lane l holds row l of its block's inverse (jr[32 k], k < bs) and gathers
+// the block's residuals by shuffles; z_l = sum_k (J^{-1})_{lk} r_k in ascending k.  Called by all
+// 32 lanes (row < 0: tail slot, every operand 0, nothing stored).
+__device__ __forceinline__ void ajm_row_update_blk(double* __restrict__ Qxp, double* __restrict__ xf, int i,
+                                                   double q, double bi, const double* __restrict__ jr, int bs,
+                                                   double xt, double xpi, double qxp, double beta,
+                                                   int restart_t, AjmAcc& a, uint64_t pol, uint64_t xpol) {
+    const int lane = threadIdx.x & 31;
+    const double rq = bi - q;
+    a.rr += rq * rq;
+    a.xq += xt * q;
+    a.bx += bi * xt;
+    double y, qy, xnow;
+    if (!restart_t) {
+        y = xt + beta * (xt - xpi);
+        qy = q + beta * (q - qxp);
+        if (i >= 0) ajm_stp(Qxp + i, q, pol);
+        xnow = xt;
+    } else {
+        y = xpi;
+        qy = qxp;
+        xnow = xpi;
+    }
+    const double r = bi - qy;
+    const int base = lane & ~(bs - 1);
+    double z = 0.0;
+    for (int k = 0; k < bs; ++k) {
+        const double rk = __shfl_sync(0xffffffffu, r, base + k);
+        z += __ldcs(jr + 32 * k) * rk;
+    }
+    const double xn = y + z;
+    if (i >= 0) ajm_stp(xf + i, xn, xpol);
     const double term = (qy - bi) * (xn - xnow);
     a.d += term;
     a.dabs += fabs(term);
@@ -798,7 +840,11 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                     const int off = (e0 - s_coff[s_uc0[uu]]) + lane;
                     const double q = gring ? ajm_chunk_dot_smem(st_val(stage) + off, st_xg(stage) + off, w)
                                            : ajm_chunk_dot(st_val(stage) + off, st_col(stage) + off, w, xc);
-                    if (row >= 0) ajm_row_update(p.Qxp, xf, row, q, bi, Di, xt, xpi, qxp, beta, restart_t, acc, vpol, xpol);
+                    if (p.jbs)  // block-diagonal J: warp-uniform branch, every lane takes part
+                        ajm_row_update_blk(p.Qxp, xf, row, q, bi, p.Jinv + (size_t)(cfirst + j) * p.jbs * 32 + lane,
+                                           p.jbs, xt, xpi, qxp, beta, restart_t, acc, vpol, xpol);
+                    else if (row >= 0)
+                        ajm_row_update(p.Qxp, xf, row, q, bi, Di, xt, xpi, qxp, beta, restart_t, acc, vpol, xpol);
                 } else {
                     ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);  // keep the phases in step
                 }
@@ -1016,6 +1062,144 @@ __global__ void ajm_sell_fill_kernel(int nslots_padded, int n_sell, const int* _
         const long long e = base + (long long)k * 32 + lane;
         if (k < len) { sval[e] = val[k0 + k]; scol[e] = col[k0 + k]; }
         else { sval[e] = 0.0; scol[e] = row >= 0 ? row : 0; }
+    }
+}
+
+// eq-J-blkdiag setup ("setup J"), one thread per row block of BS rows:
+//   J^{ii} = Q^{ii} + (sum_{j != i} ||Q^{ij}||_2) I
+// The off-diagonal blocks Q^{ij} of the block's rows are visited in ascending column-block j by a
+// merge over the rows' (sorted) columns; ||B||_2 = sqrt(lambda_max(B^T B)) with lambda_max from a
+// cyclic Jacobi eigenvalue iteration on the small symmetric B^T B (converged to rounding).  Then
+// J^{ii} = L L^T (Cholesky; a non-positive pivot flags AJM_EB_ZERODIAG) and (J^{ii})^{-1} by
+// triangular solves.  Outputs: J blocks (row-major, ragged last block padded with I), the rows of
+// the inverses in the solver's per-chunk [bs][32] layout, and D = diag(J).
+#define AJM_EB_JBLOCK 32
+template <int BS>
+__device__ double ajm_spectral_norm(const double* B) {
+    double C[BS * BS];
+    for (int a = 0; a < BS; ++a)
+        for (int b = 0; b < BS; ++b) {
+            double t = 0.0;
+            for (int k = 0; k < BS; ++k) t += B[k * BS + a] * B[k * BS + b];
+            C[a * BS + b] = t;
+        }
+    for (int sweep = 0; sweep < 64; ++sweep) {
+        double off = 0.0, dmax = 0.0;
+        for (int a = 0; a < BS; ++a)
+            for (int b = 0; b < BS; ++b) {
+                if (a < b) off += C[a * BS + b] * C[a * BS + b] + C[b * BS + a] * C[b * BS + a];
+                else dmax = fmax(dmax, fabs(C[a * BS + a]));
+            }
+        // converged when the off-diagonal mass is below 1e-15 of the largest diagonal (Weyl: the
+        // largest eigenvalue is then exact to that relative accuracy)
+        if (!(off > 1e-30 * dmax * dmax)) break;
+        for (int pp = 0; pp < BS - 1; ++pp)
+            for (int qq = pp + 1; qq < BS; ++qq) {
+                const double apq = C[pp * BS + qq];
+                if (apq == 0.0) continue;
+                const double app = C[pp * BS + pp], aqq = C[qq * BS + qq];
+                if (fabs(apq) <= 1e-18 * dmax) {  // negligible against the spectrum: drop it
+                    C[pp * BS + qq] = C[qq * BS + pp] = 0.0;
+                    continue;
+                }
+                const double theta = (aqq - app) / (2.0 * apq);
+                const double tt = fabs(theta) > 1e150 ? 0.5 / theta
+                                : (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                const double cs = 1.0 / sqrt(tt * tt + 1.0), sn = tt * cs;
+                for (int k = 0; k < BS; ++k) {  // C <- C G  (columns p, q)
+                    const double ckp = C[k * BS + pp], ckq = C[k * BS + qq];
+                    C[k * BS + pp] = cs * ckp - sn * ckq;
+                    C[k * BS + qq] = sn * ckp + cs * ckq;
+                }
+                for (int k = 0; k < BS; ++k) {  // C <- G^T C  (rows p, q)
+                    const double cpk = C[pp * BS + k], cqk = C[qq * BS + k];
+                    C[pp * BS + k] = cs * cpk - sn * cqk;
+                    C[qq * BS + k] = sn * cpk + cs * cqk;
+                }
+                C[pp * BS + qq] = C[qq * BS + pp] = 0.0;  // the annihilated pair (exact in theory)
+            }
+    }
+    double lmax = 0.0;
+    for (int a = 0; a < BS; ++a) lmax = fmax(lmax, C[a * BS + a]);
+    return sqrt(lmax);
+}
+
+template <int BS>
+__global__ void ajm_jblock_build_kernel(int n, const int* __restrict__ rp, const int* __restrict__ col,
+                                        const double* __restrict__ val, double* __restrict__ Jout,
+                                        double* __restrict__ Jinv, double* __restrict__ D, int* __restrict__ err) {
+    const int blk = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nblk = (n + BS - 1) / BS;
+    if (blk >= nblk) return;
+    const int r0 = blk * BS;
+    const int m = min(BS, n - r0);
+    double A[BS * BS], B[BS * BS];
+    int cur[BS], end[BS];
+    for (int k = 0; k < BS * BS; ++k) A[k] = 0.0;
+    for (int r = 0; r < BS; ++r) {
+        cur[r] = r < m ? rp[r0 + r] : 0;
+        end[r] = r < m ? rp[r0 + r + 1] : 0;
+    }
+    double shift = 0.0;
+    for (;;) {
+        int bj = INT_MAX;  // smallest column block still unvisited in any of the rows
+        for (int r = 0; r < m; ++r)
+            if (cur[r] < end[r]) bj = min(bj, col[cur[r]] / BS);
+        if (bj == INT_MAX) break;
+        double* T = (bj == blk) ? A : B;
+        if (bj != blk)
+            for (int k = 0; k < BS * BS; ++k) B[k] = 0.0;
+        for (int r = 0; r < m; ++r)
+            while (cur[r] < end[r] && col[cur[r]] / BS == bj) {
+                T[r * BS + (col[cur[r]] - bj * BS)] = val[cur[r]];
+                ++cur[r];
+            }
+        if (bj != blk) shift += ajm_spectral_norm<BS>(B);  // ascending j
+    }
+    for (int k = 0; k < BS; ++k) {
+        if (k < m) A[k * BS + k] += shift;
+        else {
+            for (int j = 0; j < BS; ++j) A[k * BS + j] = A[j * BS + k] = 0.0;
+            A[k * BS + k] = 1.0;
+        }
+    }
+    for (int k = 0; k < BS * BS; ++k) Jout[(size_t)blk * BS * BS + k] = A[k];
+    for (int k = 0; k < m; ++k) D[r0 + k] = A[k * BS + k];
+    // Cholesky A = L L^T (L in B, lower)
+    for (int k = 0; k < BS * BS; ++k) B[k] = 0.0;
+    bool ok = true;
+    for (int j = 0; j < BS; ++j) {
+        double d = A[j * BS + j];
+        for (int k = 0; k < j; ++k) d -= B[j * BS + k] * B[j * BS + k];
+        if (!(d > 0.0)) { ok = false; break; }
+        const double ljj = sqrt(d);
+        B[j * BS + j] = ljj;
+        for (int i = j + 1; i < BS; ++i) {
+            double t = A[i * BS + j];
+            for (int k = 0; k < j; ++k) t -= B[i * BS + k] * B[j * BS + k];
+            B[i * BS + j] = t / ljj;
+        }
+    }
+    if (!ok) { atomicOr(err, AJM_EB_JBLOCK); return; }
+    // inverse column by column: L y = e_c, L^T x = y  (A reused for the inverse)
+    for (int c = 0; c < BS; ++c) {
+        double x[BS];
+        for (int i = 0; i < BS; ++i) {
+            double t = (i == c) ? 1.0 : 0.0;
+            for (int k = 0; k < i; ++k) t -= B[i * BS + k] * x[k];
+            x[i] = t / B[i * BS + i];
+        }
+        for (int i = BS - 1; i >= 0; --i) {
+            double t = x[i];
+            for (int k = i + 1; k < BS; ++k) t -= B[k * BS + i] * x[k];
+            x[i] = t / B[i * BS + i];
+        }
+        for (int i = 0; i < BS; ++i) A[i * BS + c] = x[i];
+    }
+    for (int k = 0; k < m; ++k) {  // row r0+k of the inverse -> chunk layout [chunk][c][lane]
+        const int row = r0 + k;
+        double* dst = Jinv + (size_t)(row >> 5) * BS * 32 + (row & 31);
+        for (int c = 0; c < BS; ++c) dst[32 * c] = A[k * BS + c];
     }
 }
 

@@ -29,19 +29,21 @@ def oracle_threads():
 
 
 def gpu_solve(Q, b, x0=None, tol=0.0, maxit=1000, restart=True, momentum=True, k0=2,
-              dmode="jdiag", d=None, loop="graph", device_inputs=False):
+              dmode="jdiag", d=None, loop="graph", device_inputs=False, jblock=None):
     import torch
     import paper_2407_03272_b200 as ajm
     args = [Q.row_ptr, Q.col, Q.val, b, d, x0]
     if device_inputs:
         args = [None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in args]
-    with ajm.Solver(Q.n, args[0], args[1], args[2], args[3], dmode=dmode, d=args[4], loop=loop) as s:
+    with ajm.Solver(Q.n, args[0], args[1], args[2], args[3], dmode=dmode, d=args[4], loop=loop,
+                    jblock=jblock) as s:
         r = s.solve(x0=args[5], tol=tol, maxit=maxit, momentum=momentum, restart=restart, k0=k0)
         r.x = r.x.cpu().numpy()
         r.d_trace = s.trace("d", r.iterations + 1)
         r.dabs_trace = s.trace("dabs", r.iterations + 1)
         r.D = s.diag()
         r.info = s.info()
+        r.J = s.jblocks() if jblock else None
     return r
 
 
