@@ -259,7 +259,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     # inputs resident in HBM before timing
     Qd = [torch.from_numpy(a).to(dev) for a in (p.Q.row_ptr, p.Q.col, p.Q.val, p.b)]
-    solver = ajm.Solver(p.Q.n, *Qd[:3], Qd[3])
+    solver = ajm.Solver(p.Q.n, *Qd[:3], Qd[3], jblock=args.jblock)
     x_out = torch.empty(p.Q.n, dtype=torch.float64, device=dev)
     kw = dict(tol=tol, maxit=maxit, restart=True, x_out=x_out, history=False)
     for _ in range(args.warmup):
@@ -302,7 +302,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record(stream)
-        with ajm.Solver(p.Q.n, host[0], host[1], host[2], host[3]) as s2:
+        with ajm.Solver(p.Q.n, host[0], host[1], host[2], host[3], jblock=args.jblock) as s2:
             r2 = s2.solve(tol=tol, maxit=maxit, restart=True, x_out=x_host, history=True)
         a1.record(stream)
         torch.cuda.synchronize()
@@ -319,7 +319,7 @@ def run_ours(args):
     peak, peak_src = load_peaks()
     model_bytes = info["model_bytes_per_iter"]
     achieved = model_bytes * passes / (loop_ms * 1e-3) / 1e9  # GB/s, per-launch average
-    tr = load_traffic(p.name)
+    tr = None if args.jblock else load_traffic(p.name)
     traffic = None if tr is None else tr["dram_bytes_per_pass"] * passes / args.steps
     cpu = cpu_baseline_run(p, args.config) if (world == 1 and not args.no_cpu_baseline) else None
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -340,7 +340,9 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": W["workload"], "n": p.Q.n, "nnz": p.Q.nnz, "tol": tol, "maxit": maxit,
+        "config": {"workload": W["workload"] + (f"; block-diagonal J (eq-J-blkdiag), bs={args.jblock}"
+                                                 if args.jblock else ""),
+                   "n": p.Q.n, "nnz": p.Q.nnz, "tol": tol, "maxit": maxit,
                    "parallelism": f"replicas x{world} (the method does not shard: DESIGN.md §6)",
                    "l2": l2_note,
                    "kernel_variant": info["variant"], "grid": info["grid"],
@@ -354,8 +356,9 @@ def run_ours(args):
         "roofline": {"bound": W["bound"] if W["bound"] != "latency" else "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_basis": "ncu dram read+write per pass (profiles/ncu_traffic.json) x passes per launch", "peak_source": peak_src,
                      "kernel": "ajm_solve_kernel (persistent; one launch per solve)",
-                     "achieved_basis": "algorithmic bytes nnz*12+7n*8+4(n+1) per pass x passes / "
-                                       "launch duration (CUDA events on the launch stream)"},
+                     "achieved_basis": "algorithmic bytes nnz*12+7n*8+4(n+1) per pass (D replaced by bs "
+                                       "doubles of J^-1 per row with --jblock) x passes / launch duration "
+                                       "(CUDA events on the launch stream)"},
         "e2e": {"value": e2e_iters / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "note": "ajm_create from pinned host CSR+b (H2D + layout build) + ajm_solve to 1e-6 "
@@ -380,6 +383,8 @@ def main(argv=None):
     ap.add_argument("--tol", type=float, default=None, help="default: the workload's")
     ap.add_argument("--maxit", type=int, default=None, help="default: the workload's")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--jblock", type=int, default=None,
+                    help="block-diagonal J of eq-J-blkdiag with this block size (default: eq-J-diag)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
     if args.warmup < 3:

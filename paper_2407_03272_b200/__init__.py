@@ -96,8 +96,9 @@ def lib():
         L.ajm_get_trace.restype = ctypes.c_int
         L.ajm_get_diag.argtypes = [P, P]
         L.ajm_get_diag.restype = ctypes.c_int
-        L.ajm_get_jblock.argtypes = [P, P]
-        L.ajm_get_jblock.restype = ctypes.c_int
+        if hasattr(L, "ajm_get_jblock"):  # (AJM_LIB_OVERRIDE A/B builds may predate it)
+            L.ajm_get_jblock.argtypes = [P, P]
+            L.ajm_get_jblock.restype = ctypes.c_int
         L.ajm_get_info.argtypes = [P, ctypes.POINTER(ajm_info_t)]
         L.ajm_get_info.restype = ctypes.c_int
         L.ajm_destroy.argtypes = [P]

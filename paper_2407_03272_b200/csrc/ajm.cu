@@ -44,8 +44,9 @@ struct SolveVariant {
     SolveFn fng;  // gather ring (kMode 3): x~ gathers as cp.async into the stage, 1 CTA/SM
     int gstages;
 };
-// TMA ring depth x register cap (=> resident CTAs per SM with 288 threads); AJM_KVARIANT selects
-// one (tuning); the default is the measured best on B200
+// TMA ring depth x register cap (=> resident CTAs per SM with 288 threads; above 96 registers two
+// 9-warp CTAs no longer fit the per-SMSP register files); AJM_KVARIANT selects one (tuning); the
+// default is the measured best on B200
 const SolveVariant kVariants[] = {
     {ajm_solve_kernel<4, 96, 0>, 4, ajm_solve_kernel<3, 96, 1>, 3, ajm_solve_kernel<1, 128, 2>, "s4r96", ajm_solve_kernel<4, 128, 3>, 4},    // 2 CTAs/SM
     {ajm_solve_kernel<3, 72, 0>, 3, ajm_solve_kernel<2, 72, 1>, 2, ajm_solve_kernel<1, 72, 2>, "s3r72", ajm_solve_kernel<3, 128, 3>, 3},     // 3 CTAs/SM
