@@ -119,7 +119,7 @@ typedef struct {
     int64_t l2_window_bytes;  /* iterate vectors covered by the persisting-L2 access window     */
     double l2_hit_ratio;      /* persisting fraction of that window                            */
     int32_t mode;             /* 0 TMA ring, 1 ring + vector slices, 2 direct SELL loads       */
-    int32_t pad0;
+    int32_t l2_mode;          /* L2 policy: 2 all vectors persist, 3 only the x~ buffers persist */
 } ajm_info_t;
 
 /*

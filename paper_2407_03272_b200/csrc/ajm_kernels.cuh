@@ -1216,6 +1216,14 @@ __global__ void ajm_remap_kernel(long long nnz, const int* __restrict__ inv, int
         col[k] = inv[col[k]];
 }
 
+// L2 priming: read every line of the vectors once (launched under an access-policy window)
+__global__ void ajm_l2_touch_kernel(const double* __restrict__ v, long long n, double* __restrict__ sink) {
+    double s = 0.0;
+    for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * 4; i < n; i += (long long)gridDim.x * blockDim.x * 4)
+        s += v[i];  // one load per 32-byte sector
+    if (s == 1.2345e300) *sink = s;
+}
+
 // Per-solve initialisation of the control block (t = 0: x~^0 = x0, x^{-1} := x0, beta_0 = 0,
 // alpha_1 = 1, K = K_0, K_re = 0, ell = 0).
 __global__ void ajm_init_ctrl_kernel(AjmCtrl* c, double tol, long long maxit, int momentum,

@@ -19,13 +19,16 @@ for cfg in cfgs:
     tg = time.time() - t0
     for var, l2m in variants:
         os.environ["AJM_KVARIANT"] = str(var)
-        os.environ["AJM_L2MODE"] = str(l2m)
+        if l2m >= 0:
+            os.environ["AJM_L2MODE"] = str(l2m)
+        else:
+            os.environ.pop("AJM_L2MODE", None)
         t0 = time.time()
         with ajm.Solver.from_csr(p.Q, p.b) as s:
             tc = time.time() - t0
             info = s.info()
             print(f"cfg{cfg} var{var} l2m{l2m} n={p.Q.n} nnz={p.Q.nnz} gen={tg:.1f}s create={tc:.2f}s grid={info['grid']} "
-                  f"occ={info['ctas_per_sm']} mode={info['mode']} l2win={info['l2_window_bytes']/1e6:.0f}MB hit={info['l2_hit_ratio']:.2f} units={info['units']} sell={info['sell_rows']} seg={info['seg_rows']} split={info['split_rows']} sigma={info['sigma']} pad={info['sell_elems']}", flush=True)
+                  f"occ={info['ctas_per_sm']} mode={info['mode']} l2auto={info['l2_mode']} l2win={info['l2_window_bytes']/1e6:.0f}MB hit={info['l2_hit_ratio']:.2f} units={info['units']} sell={info['sell_rows']} seg={info['seg_rows']} split={info['split_rows']} sigma={info['sigma']} pad={info['sell_elems']}", flush=True)
             for rep in range(2):
                 r = s.solve(tol=1e-6, maxit=5000, restart=True)
                 info = s.info(); ms = info["last_loop_ms"]
