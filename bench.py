@@ -363,7 +363,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": d2h,
                 "note": "ajm_create from pinned host CSR+b (H2D + layout build) + ajm_solve to 1e-6 "
                         "+ x and histories to host + ajm_destroy"},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": int(info["launches_per_solve"]) * args.steps,
         "clocks": clk,
         "cpu_baseline": cpu,
     }

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define AJM_ABI_VERSION 1
+#define AJM_ABI_VERSION 2  /* 2: AJM_D_JBLOCK, ajm_get_jblock, ajm_info_t.l2_mode / launches_per_solve */
 
 typedef struct ajm_ctx* ajm_handle_t;
 
@@ -120,6 +120,8 @@ typedef struct {
     double l2_hit_ratio;      /* persisting fraction of that window                            */
     int32_t mode;             /* 0 TMA ring, 1 ring + vector slices, 2 direct SELL loads       */
     int32_t l2_mode;          /* L2 policy: 2 all vectors persist, 3 only the x~ buffers persist */
+    int32_t launches_per_solve; /* kernel launches of one ajm_solve (L2 priming + init + solver)   */
+    int32_t pad1;
 } ajm_info_t;
 
 /*

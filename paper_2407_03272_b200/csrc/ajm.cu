@@ -1126,6 +1126,8 @@ ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info) {
     info->mode = h->gring ? 3 : h->direct ? 2 : (h->vstage ? 1 : 0);
     info->sell_elems = h->sell_elems;
     info->l2_mode = h->l2_mode;
+    info->launches_per_solve = (int32_t)(1 + (h->prime_bytes ? 1 : 0) + std::max<int64_t>(h->last_launches, 1));
+    info->pad1 = 0;
     return AJM_OK;
 }
 

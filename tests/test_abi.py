@@ -22,7 +22,7 @@ def test_library_built_and_loads():
     from paper_2407_03272_b200 import build
     build.build()
     L = ajm.lib()
-    assert L.ajm_abi_version() == 1
+    assert L.ajm_abi_version() == 2
 
 
 def test_exports_every_header_symbol():
