@@ -63,8 +63,17 @@ def main():
                                   f"profiles/{tag}_ncu_configs.md"})
     with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_configs.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
-    with open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w") as f:
-        json.dump(traffic, f, indent=1)
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:  # merge: replace the records of the workloads captured now, keep the others
+        with open(path) as f:
+            old = json.load(f)
+        old = old if isinstance(old, list) else [old]
+    except Exception:
+        old = []
+    new_names = {t["workload"] for t in traffic}
+    merged = [o for o in old if o.get("workload") not in new_names] + traffic
+    with open(path, "w") as f:
+        json.dump(merged, f, indent=1)
     print("\n".join(lines))
 
 
