@@ -726,34 +726,36 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     // L2 residency: keep as much of the iterate vectors as the device allows in a
     // persisting L2 carve-out; the matrix stream goes through with evict_first hints
     h->win_bytes = 0;
+    int l2size = 0;
+    CC(cudaDeviceGetAttribute(&l2size, cudaDevAttrL2CacheSize, h->device));
+    const size_t vec_bytes = sizeof(double) * 6 * (size_t)h->n_pad;
+    // vectors larger than the whole L2 (configs 4, 5): a persisting carve-out only takes L2 away
+    // from everything else (measured 1138 -> 919 us/pass on config 4): eviction hints only
+    if (vec_bytes > (size_t)l2size && l2_env < 0 && !getenv("AJM_FORCE_WINDOW")) {
+        h->l2persist = 0;
+        h->l2_mode = 3;
+    }
     if (h->l2persist) {
         int maxp = 0, maxw = 0;
         CC(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device));
         CC(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, h->device));
-        const size_t vec_bytes = sizeof(double) * 6 * (size_t)h->n_pad;
         if (maxp > 0 && maxw > 0) {
             size_t persist = std::min<size_t>((size_t)maxp, vec_bytes);
             size_t cur = 0;
             CC(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
             if (cur < persist) CC(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
             CC(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
-            // all six vectors when they (nearly) fit the carve-out; otherwise only the three
-            // rotating iterate buffers X0..X2 (the gathered x~ lives there) and b, D, Qx are
-            // streamed with evict_first (l2_mode 3)
-            // measured: mode 2 when all six vectors fit the carve-out, else mode 3
+            // mode 2: all six vectors in the window (they fit 3/4 of the carve-out: config 3);
+            // mode 3: only the three rotating iterate buffers X0..X2 (the gathered x~ lives there),
+            // b, D, Qx streamed with evict_first
             h->l2_mode = (double)vec_bytes <= 0.75 * (double)maxp ? 2 : 3;
             if (l2_env >= 0) h->l2_mode = l2_env;
             const size_t wb = h->l2_mode == 3 ? sizeof(double) * 3 * (size_t)h->n_pad : vec_bytes;
             h->win_bytes = std::min<size_t>(wb, (size_t)maxw);
             h->win_hit = (float)std::min(1.0, (double)cur / (double)h->win_bytes);
-            // mode 3 on vectors that fit the L2: before each solve one touch pass over all six
-            // vectors under a window covering them (the carve-out's share persists), then the
-            // solver's own window keeps the x~ buffers at hit ratio 1 (measured: DESIGN.md §5)
-            int l2size = 0;
-            CC(cudaDeviceGetAttribute(&l2size, cudaDevAttrL2CacheSize, h->device));
-            // vectors larger than the whole L2 (configs 4, 5): a persisting carve-out only takes
-            // L2 away from everything else (measured 1138 -> 919 us/pass on config 4): hints only
-            if (vec_bytes > (size_t)l2size && l2_env < 0 && !getenv("AJM_FORCE_WINDOW")) h->win_bytes = 0;
+            // mode 3 on vectors that fit the L2 (config 2): before each solve one touch pass over
+            // all six vectors under a window covering them (the carve-out's share persists), then
+            // the solver's own window keeps the x~ buffers at hit ratio 1 (55.3 -> 47.0 us/pass)
             if (h->l2_mode == 3 && vec_bytes <= (size_t)l2size && !getenv("AJM_NO_PRIME")) {
                 h->prime_bytes = std::min<size_t>(vec_bytes, (size_t)maxw);
                 h->prime_hit = (float)std::min(1.0, (double)cur / (double)h->prime_bytes);
