@@ -185,3 +185,29 @@ def test_create_errors():
             s.solve(**kw)
         assert e.value.status_name == "AJM_ERR_INVALID_ARG"
     s.close()
+
+
+@pytest.mark.parametrize("n", [1000, 3000])
+def test_sdd_paper_experiment(n):
+    """§4.1: on Q = (n+1)I - 11^T, b = 1, tol 1e-4, maxiter 5000, the GPU's Jacobi and
+    weighted Jacobi (omega_opt = 2n/(n+2)) follow their closed forms (1-1/n)^t and (1-2/(n+2))^t
+    and AJM with restart follows the exact scalar recurrence of Alg. 3 on span{1} (the models are
+    pinned against the oracle in test_oracle_pins.py); rows of n nonzeros run on the warp-segment
+    and split-row path."""
+    import sys, os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import exp_sdd
+    Q = synth.sdd(n)
+    b = np.ones(n)
+    t = np.arange(5001)
+    g = gpu_solve(Q, b, tol=1e-4, maxit=5000, momentum=False, restart=False, dmode="qdiag")
+    assert (g.iterations, g.status) == exp_sdd.closed_form_iters(1 - 1 / n, 1e-4, 5000)
+    np.testing.assert_allclose(g.res_hist, (1 - 1 / n) ** t[: len(g.res_hist)], rtol=1e-9)
+    w = 2 * n / (n + 2)
+    g = gpu_solve(Q, b, tol=1e-4, maxit=5000, momentum=False, restart=False, dmode="user", d=np.full(n, n / w))
+    it, st = exp_sdd.closed_form_iters(1 - 2 / (n + 2), 1e-4, 5000)
+    assert g.status == st and abs(g.iterations - it) <= 1
+    np.testing.assert_allclose(g.res_hist, (1 - 2 / (n + 2)) ** t[: len(g.res_hist)], rtol=1e-8)
+    g = gpu_solve(Q, b, tol=1e-4, maxit=5000, restart=True)
+    it, res = exp_sdd.scalar_ajm(n, 1e-4, 5000)
+    assert g.status == "converged" and abs(g.iterations - it) <= 1
