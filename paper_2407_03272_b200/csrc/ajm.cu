@@ -43,15 +43,16 @@ struct SolveVariant {
     const char* name;
     SolveFn fng;  // gather ring (kMode 3): x~ gathers as cp.async into the stage, 1 CTA/SM
     int gstages;
+    SolveFn fn0;  // as fn, compiled without the segment phases (layouts without long rows)
 };
 // TMA ring depth x register cap (=> resident CTAs per SM with 288 threads; above 96 registers two
 // 9-warp CTAs no longer fit the per-SMSP register files); AJM_KVARIANT selects one (tuning); the
 // default is the measured best on B200
 const SolveVariant kVariants[] = {
-    {ajm_solve_kernel<4, 96, 0>, 4, ajm_solve_kernel<3, 96, 1>, 3, ajm_solve_kernel<1, 128, 2>, "s4r96", ajm_solve_kernel<4, 128, 3>, 4},    // 2 CTAs/SM
-    {ajm_solve_kernel<3, 72, 0>, 3, ajm_solve_kernel<2, 72, 1>, 2, ajm_solve_kernel<1, 72, 2>, "s3r72", ajm_solve_kernel<3, 128, 3>, 3},     // 3 CTAs/SM
-    {ajm_solve_kernel<2, 56, 0>, 2, ajm_solve_kernel<2, 56, 1>, 2, ajm_solve_kernel<1, 56, 2>, "s2r56", ajm_solve_kernel<2, 128, 3>, 2},     // 4 CTAs/SM
-    {ajm_solve_kernel<6, 128, 0>, 6, ajm_solve_kernel<6, 128, 1>, 6, ajm_solve_kernel<1, 128, 2>, "s6r128", ajm_solve_kernel<4, 128, 3>, 4}, // 1 CTA/SM
+    {ajm_solve_kernel<4, 96, 0>, 4, ajm_solve_kernel<3, 96, 1>, 3, ajm_solve_kernel<1, 128, 2>, "s4r96", ajm_solve_kernel<4, 128, 3>, 4, ajm_solve_kernel<4, 96, 0, false>},    // 2 CTAs/SM
+    {ajm_solve_kernel<3, 72, 0>, 3, ajm_solve_kernel<2, 72, 1>, 2, ajm_solve_kernel<1, 72, 2>, "s3r72", ajm_solve_kernel<3, 128, 3>, 3, ajm_solve_kernel<3, 72, 0, false>},     // 3 CTAs/SM
+    {ajm_solve_kernel<2, 56, 0>, 2, ajm_solve_kernel<2, 56, 1>, 2, ajm_solve_kernel<1, 56, 2>, "s2r56", ajm_solve_kernel<2, 128, 3>, 2, ajm_solve_kernel<2, 56, 0, false>},     // 4 CTAs/SM
+    {ajm_solve_kernel<6, 128, 0>, 6, ajm_solve_kernel<6, 128, 1>, 6, ajm_solve_kernel<1, 128, 2>, "s6r128", ajm_solve_kernel<4, 128, 3>, 4, ajm_solve_kernel<6, 128, 0, false>}, // 1 CTA/SM
 };
 const int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -112,6 +113,10 @@ struct ajm_ctx {
     int* unit_c0 = nullptr;
     int* cta_seg = nullptr;
     int* seg_list = nullptr;
+    int* seg_order = nullptr;       // dynamic segment queue: segments in claim order (longest first)
+    int* seg_grp = nullptr;         // claim g -> seg_order[seg_grp[g] .. seg_grp[g+1])
+    int64_t nsegq = 0;              // claim groups
+    int dynseg = 0;                 // segments claimed dynamically by warps (else static LPT plan)
     int* cta_unit = nullptr;
     double* partials = nullptr;
     AjmCtrl* ctrl = nullptr;
@@ -218,7 +223,7 @@ void free_all(ajm_ctx* h) {
                     h->sval, h->scol, h->chunk_off, h->perm, h->seg_row, h->seg_k0, h->seg_k1,
                     h->seg_split, h->seg_part, h->split_row, h->split_seg0, h->split_cnt,
                     h->cta_split, h->owner_split, h->unit_c0, h->cta_seg, h->seg_list, h->cta_unit, h->partials, h->ctrl,
-                    h->hist, h->scratch, h->err, h->ts, h->perm_fwd, h->perm_inv, h->b_in, h->Jblk, h->Jinv};
+                    h->hist, h->scratch, h->err, h->ts, h->perm_fwd, h->perm_inv, h->b_in, h->Jblk, h->Jinv, h->seg_order, h->seg_grp};
     for (void* p : ptrs) dfree(p);
     if (h->h_ctrl) free(h->h_ctrl);
     if (h->ev0) cudaEventDestroy(h->ev0);
@@ -247,6 +252,10 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.unit_c0 = h->unit_c0;
     p.cta_seg = h->cta_seg;
     p.seg_list = h->seg_list;
+    p.seg_order = h->seg_order;
+    p.dynseg = h->dynseg;
+    p.nseg = (int)h->nsegq;
+    p.seg_grp = h->seg_grp;
     p.cta_unit = h->cta_unit;
     p.b = h->b;
     p.D = h->D;
@@ -407,6 +416,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fnv, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fnd, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fng, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fn0, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
 
     // ---- the CSR arrays and b go to the device now; the copies overlap the host planning ----
     CC(dalloc(&h->rp, n + 1, st));
@@ -473,12 +483,24 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         mark("L-fast", (cudaStream_t)-1);
     }
     if (!fast) {
+        int64_t seg_len = AJM_SEG;  // nonzeros per warp segment (AJM_SEGLEN: tuning experiments)
+        if (const char* ev = getenv("AJM_SEGLEN")) seg_len = std::max<int64_t>(AJM_SELL_MAX + 1, atoll(ev));
         std::vector<int> short_rows, split_rows, whole_rows;
         short_rows.reserve((size_t)n);
+        // dynamic segment queue when long rows carry >= 90% of the nonzeros (e.g. the §4.1 dense
+        // SDD matrix: 1.2-1.3x faster); with a SELL majority (config 4) the static LPT plan is
+        // faster (873 vs 964 us/pass).  AJM_DYNSEG overrides.
+        {
+            int64_t long_nnz = 0;
+            for (int64_t i = 0; i < n; ++i)
+                if (rlen(i) > AJM_SELL_MAX) long_nnz += rlen(i);
+            h->dynseg = (double)long_nnz >= 0.9 * (double)std::max<int64_t>(nnz, 1) ? 1 : 0;
+            if (const char* ev = getenv("AJM_DYNSEG")) h->dynseg = atoi(ev) ? 1 : 0;
+        }
         for (int64_t i = 0; i < n; ++i) {
             const int64_t len = rlen(i);
             if (len <= AJM_SELL_MAX) short_rows.push_back((int)i);
-            else if (len <= AJM_SEG) whole_rows.push_back((int)i);
+            else if (len <= seg_len) whole_rows.push_back((int)i);
             else split_rows.push_back((int)i);
         }
         h->long_rows = (int64_t)split_rows.size();
@@ -550,20 +572,27 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             const int sidx = (int)split_row_h.size();
             split_row_h.push_back(irow(r));
             split_seg0_h.push_back((int)seg_row_h.size());
-            for (int64_t k = hrp[(size_t)r]; k < hrp[(size_t)r + 1]; k += AJM_SEG) {
+            for (int64_t k = hrp[(size_t)r]; k < hrp[(size_t)r + 1]; k += seg_len) {
                 seg_row_h.push_back(irow(r));
                 seg_k0_h.push_back((int)k);
-                seg_k1_h.push_back((int)std::min<int64_t>(k + AJM_SEG, hrp[(size_t)r + 1]));
+                seg_k1_h.push_back((int)std::min<int64_t>(k + seg_len, hrp[(size_t)r + 1]));
                 seg_split_h.push_back(sidx);
             }
         }
-        split_seg0_h.push_back((int)seg_row_h.size());
+        if (!h->dynseg) split_seg0_h.push_back((int)seg_row_h.size());
         for (int r : whole_rows) {
+            // dynamic segments: every segment row is finished by a fixed owner CTA (one segment)
+            const int sidx = h->dynseg ? (int)split_row_h.size() : -1;
+            if (h->dynseg) {
+                split_row_h.push_back(irow(r));
+                split_seg0_h.push_back((int)seg_row_h.size());
+            }
             seg_row_h.push_back(irow(r));
             seg_k0_h.push_back((int)hrp[(size_t)r]);
             seg_k1_h.push_back((int)hrp[(size_t)r + 1]);
-            seg_split_h.push_back(-1);
+            seg_split_h.push_back(sidx);
         }
+        if (h->dynseg) split_seg0_h.push_back((int)seg_row_h.size());
         h->nseg = (int64_t)seg_row_h.size();
         h->nsplit = (int64_t)split_row_h.size();
         h->seg_rows = (int64_t)(split_rows.size() + whole_rows.size());
@@ -577,7 +606,30 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     }
     mark("layout", st);
     // ---- TMA staging units, persistent grid, cost-balanced CTA ranges ----
-    std::vector<int> unit_c0_h, cta_seg_h, cta_unit_h, cta_split_h, owner_split_h, seg_list_h;
+    std::vector<int> unit_c0_h, cta_seg_h, cta_unit_h, cta_split_h, owner_split_h, seg_list_h, seg_order_h, seg_grp_h;
+    if (h->dynseg) {  // claim order of the dynamic segment queue: longest first (LPT-like)
+        seg_order_h.resize((size_t)h->nseg);
+        for (int64_t k = 0; k < h->nseg; ++k) seg_order_h[(size_t)k] = (int)k;
+        std::stable_sort(seg_order_h.begin(), seg_order_h.end(), [&](int x, int y) {
+            return seg_k1_h[(size_t)x] - seg_k0_h[(size_t)x] > seg_k1_h[(size_t)y] - seg_k0_h[(size_t)y];
+        });
+        // claim groups: consecutive segments of the order with >= seg_group_nnz nonzeros (<= 16
+        // segments), so the queue costs one atomic per ~1k nonzeros, not per short row
+        int64_t gnnz = 1024;
+        if (const char* ev = getenv("AJM_SEGGROUP")) gnnz = std::max<int64_t>(1, atoll(ev));
+        int64_t acc = 0, cntg = 0;
+        seg_grp_h.push_back(0);
+        for (int64_t k = 0; k < h->nseg; ++k) {
+            const int sg = seg_order_h[(size_t)k];
+            acc += seg_k1_h[(size_t)sg] - seg_k0_h[(size_t)sg];
+            ++cntg;
+            if (acc >= gnnz || cntg >= 16 || k + 1 == h->nseg) {
+                seg_grp_h.push_back((int)(k + 1));
+                acc = cntg = 0;
+            }
+        }
+        h->nsegq = (int64_t)seg_grp_h.size() - 1;
+    }
     {
         // one item sequence: segments (split rows first), then SELL chunks; contiguous CTA ranges
         // balanced by cost at chunk granularity; each CTA's chunks are then grouped into TMA
@@ -586,8 +638,8 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         std::vector<double> cost;
         cost.reserve((size_t)nitems);
         // segments are latency-bound (one warp, direct loads): weight their bytes twice
-        for (int64_t s2 = 0; s2 < h->nseg; ++s2)
-            cost.push_back(24.0 * (seg_k1_h[(size_t)s2] - seg_k0_h[(size_t)s2]) + 56.0 + 512.0);
+        for (int64_t s2 = 0; s2 < h->nseg; ++s2)  // (dynamic segments are outside the static plan)
+            cost.push_back(h->dynseg ? 0.0 : 24.0 * (seg_k1_h[(size_t)s2] - seg_k0_h[(size_t)s2]) + 56.0 + 512.0);
         for (int64_t c2 = 0; c2 < h->nchunks; ++c2) cost.push_back(chcost[(size_t)c2]);
         double total = 0.0;
         for (double x : cost) total += x;
@@ -598,7 +650,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             const double target = total / (double)G;
             std::vector<double> segload((size_t)G, 0.0);
             std::vector<std::vector<int>> segs((size_t)G);
-            {
+            if (!h->dynseg) {
                 std::vector<int64_t> order((size_t)h->nseg);
                 for (int64_t k = 0; k < h->nseg; ++k) order[(size_t)k] = k;
                 std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return cost[(size_t)x] > cost[(size_t)y]; });
@@ -664,6 +716,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         if (!h->ident) h->vstage = 0;
         h->direct = 0;  // direct mode measured slower than the ring on every config so far
         if (const char* ev = getenv("AJM_DIRECT")) h->direct = atoi(ev) ? 1 : 0;
+        if (h->nseg == 0 && !h->vstage && !getenv("AJM_NO_NOSEG")) h->fn = kVariants[h->variant].fn0;
         if (const char* ev = getenv("AJM_GRING")) h->gring = atoi(ev) ? 1 : 0;
         if (h->vstage) h->fn = kVariants[h->variant].fnv;
         if (h->jbs) h->gring = 0, h->direct = 0;
@@ -703,8 +756,12 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         for (int cc = 0; cc < G; ++cc)
             for (int k2 = cta_seg_h[(size_t)cc]; k2 < cta_seg_h[(size_t)cc + 1]; ++k2) seg_cta[(size_t)seg_list_h[(size_t)k2]] = cc;
         std::vector<std::vector<int>> per((size_t)G);
-        for (int64_t sp = 0; sp < h->nsplit; ++sp)
-            per[(size_t)seg_cta[(size_t)split_seg0_h[(size_t)sp + 1] - 1]].push_back((int)sp);
+        for (int64_t sp = 0; sp < h->nsplit; ++sp) {
+            // static: the CTA that runs the row's last segment; dynamic: contiguous equal shares
+            const int own = h->dynseg ? (int)(sp * G / std::max<int64_t>(h->nsplit, 1))
+                                      : seg_cta[(size_t)split_seg0_h[(size_t)sp + 1] - 1];
+            per[(size_t)own].push_back((int)sp);
+        }
         cta_split_h.assign((size_t)G + 1, 0);
         for (int cc = 0; cc < G; ++cc) {
             cta_split_h[(size_t)cc + 1] = cta_split_h[(size_t)cc] + (int)per[(size_t)cc].size();
@@ -781,6 +838,8 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(dalloc(&h->unit_c0, unit_c0_h.size(), st));
     CC(dalloc(&h->cta_seg, cta_seg_h.size(), st));
     CC(dalloc(&h->seg_list, seg_list_h.size(), st));
+    CC(dalloc(&h->seg_order, seg_order_h.size(), st));
+    CC(dalloc(&h->seg_grp, seg_grp_h.size(), st));
     CC(dalloc(&h->cta_unit, cta_unit_h.size(), st));
     CC(dalloc(&h->partials, (size_t)2 * h->grid * AJM_NPART, st));
     CC(dalloc(&h->ctrl, 1, st));
@@ -827,6 +886,8 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(h2d(h->unit_c0, unit_c0_h.data(), sizeof(int) * unit_c0_h.size()));
     CC(h2d(h->cta_seg, cta_seg_h.data(), sizeof(int) * cta_seg_h.size()));
     CC(h2d(h->seg_list, seg_list_h.data(), sizeof(int) * seg_list_h.size()));
+    CC(h2d(h->seg_order, seg_order_h.data(), sizeof(int) * seg_order_h.size()));
+    CC(h2d(h->seg_grp, seg_grp_h.data(), sizeof(int) * seg_grp_h.size()));
     CC(h2d(h->cta_unit, cta_unit_h.data(), sizeof(int) * cta_unit_h.size()));
     CC(cudaMemsetAsync(h->err, 0, sizeof(int), st));
 

@@ -71,6 +71,7 @@ struct AjmCtrl {
     double* d_hist;
     double* dabs_hist;
     unsigned long long bar_count;  // grid barrier: monotone arrival counter (reset per solve)
+    unsigned seg_q[2];             // dynamic segment queues, by pass parity
     unsigned int timeout_flag;     // set if a barrier/arrival wait timed out (never expected)
     unsigned int pad;
     long long restart_log[AJM_LOG_CAP];
@@ -99,7 +100,11 @@ struct AjmPass {
     const int* __restrict__ cta_split;       // [grid+1] split rows owned by each CTA
     const int* __restrict__ owner_split;     // split-row ids grouped by owner CTA
     const int* __restrict__ cta_seg;         // [grid+1] range of each CTA in seg_list
-    const int* __restrict__ seg_list;        // segment ids grouped by CTA
+    const int* __restrict__ seg_list;        // segment ids grouped by CTA (static mode)
+    const int* __restrict__ seg_order;       // dynamic mode: segment ids in claim order (longest first)
+    const int* __restrict__ seg_grp;         // claim g covers seg_order[seg_grp[g] .. seg_grp[g+1])
+    int dynseg;                              // 1: warps claim segment groups from a per-pass queue
+    int nseg;                                // dynamic mode: number of claim groups
     const int* __restrict__ cta_unit;        // [grid+1] unit range of each CTA
     const double* __restrict__ b;
     const double* __restrict__ D;
@@ -573,7 +578,9 @@ __device__ __forceinline__ double ajm_chunk_dot_smem(const double* sv, const dou
     return s;
 }
 
-template <int kStages, int kMaxReg, int kMode>
+// kSeg = false: layouts without warp segments (all rows in SELL, e.g. stencils) -- phases (1) and
+// (3) are compiled out of the hot loop.
+template <int kStages, int kMaxReg, int kMode, bool kSeg = true>
 __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     extern __shared__ __align__(128) unsigned char s_dyn[];
     __shared__ double s_red[AJM_WARPS][AJM_NPART];
@@ -772,9 +779,30 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         const bool tsw = p.ts && bid == 0 && tid == 0 && pass < 64;
         if (tsw) p.ts[pass * 8 + 0] = ajm_gtime();
 
-        // (1) row segments (direct loads), split-row segments first
-        for (int sk = sg0 + warp; sk < sg1; sk += AJM_WARPS) {
-            const int sg = __ldg(p.seg_list + sk);
+        if (kSeg) {
+        // (1) row segments (direct loads).  Dynamic mode: every warp of every CTA claims segments
+        //     (longest first) from this pass's queue until it is empty; results go to seg_part and
+        //     the rows are finished by their fixed owner CTA in (3), so the arithmetic does not
+        //     depend on which warp ran a segment.  The other parity's queue was last used in pass
+        //     t-1 (finished before the last grid barrier) and is reset here for pass t+1.
+        if (p.dynseg && bid == 0 && tid == 0) c->seg_q[(t + 1) & 1] = 0u;
+        int gk = 0, gend = 0;  // dynamic mode: current claim group [gk, gend) of seg_order
+        for (int sk = sg0 + warp;; sk += AJM_WARPS) {
+            int sg;
+            if (p.dynseg) {
+                if (gk >= gend) {
+                    unsigned k = 0;
+                    if (lane == 0) k = atomicAdd(&c->seg_q[t & 1], 1u);
+                    k = __shfl_sync(0xffffffffu, k, 0);
+                    if ((int)k >= p.nseg) break;
+                    gk = __ldg(p.seg_grp + k);
+                    gend = __ldg(p.seg_grp + k + 1);
+                }
+                sg = __ldg(p.seg_order + gk++);
+            } else {
+                if (sk >= sg1) break;
+                sg = __ldg(p.seg_list + sk);
+            }
             const int row = __ldg(p.seg_row + sg);
             const double s = ajm_seg_dot(p, __ldg(p.seg_k0 + sg), __ldg(p.seg_k1 + sg), xc, lane);
             const int sidx = __ldg(p.seg_split + sg);
@@ -787,6 +815,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                     atomicAdd(p.split_cnt + sidx, 1u);
                 }
             }
+        }
         }
         if (tsw) p.ts[pass * 8 + 6] = ajm_gtime();
         if (direct) {
@@ -854,22 +883,22 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
             ucnt += nunits;
         }
         if (tsw) p.ts[pass * 8 + 7] = ajm_gtime();
-        // (3) split rows owned by this CTA: wait for all segments of this pass, sum in order
-        for (int k = sp0 + warp; k < sp1; k += AJM_WARPS) {
+        if (kSeg) {
+        // (3) segment rows owned by this CTA (one per lane, 256 in flight per CTA): wait for all
+        //     segments of this pass, sum their partials in segment order, run the row epilogue
+        for (int k = sp0 + tid; k < sp1; k += AJM_BLOCK) {
             const int sidx = __ldg(p.owner_split + k);
             const int g0 = __ldg(p.split_seg0 + sidx), g1 = __ldg(p.split_seg0 + sidx + 1);
-            if (lane == 0) {
-                const unsigned target = (unsigned)(g1 - g0) * (unsigned)(t + 1);
-                long long spins = 0;
-                while (ajm_ld_acquire(p.split_cnt + sidx) < target) {
-                    __nanosleep(32);
-                    if (++spins > (1LL << 28)) { atomicExch(&c->timeout_flag, 1u); break; }
-                }
-                __threadfence();
-                double q = 0.0;
-                for (int g = g0; g < g1; ++g) q += __ldcg(p.seg_part + g);
-                ajm_row_epilogue(p, __ldg(p.split_row + sidx), q, beta, restart_t, xc, xp, xf, acc);
+            const unsigned target = (unsigned)(g1 - g0) * (unsigned)(t + 1);
+            long long spins = 0;
+            while (ajm_ld_acquire(p.split_cnt + sidx) < target) {
+                __nanosleep(32);
+                if (++spins > (1LL << 28)) { atomicExch(&c->timeout_flag, 1u); break; }
             }
+            double q = 0.0;
+            for (int g = g0; g < g1; ++g) q += __ldcg(p.seg_part + g);
+            ajm_row_epilogue(p, __ldg(p.split_row + sidx), q, beta, restart_t, xc, xp, xf, acc);
+        }
         }
         // (4) CTA partial -> grid barrier -> every CTA reduces all partials in the same order
         if (tsw) p.ts[pass * 8 + 1] = ajm_gtime();
@@ -1259,6 +1288,7 @@ __global__ void ajm_init_ctrl_kernel(AjmCtrl* c, double tol, long long maxit, in
     c->d_hist = d_hist;
     c->dabs_hist = dabs_hist;
     c->bar_count = 0ull;
+    c->seg_q[0] = c->seg_q[1] = 0u;
     c->timeout_flag = 0;
     d_hist[0] = 0.0;
     dabs_hist[0] = 0.0;
