@@ -716,7 +716,11 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         if (!h->ident) h->vstage = 0;
         h->direct = 0;  // direct mode measured slower than the ring on every config so far
         if (const char* ev = getenv("AJM_DIRECT")) h->direct = atoi(ev) ? 1 : 0;
-        if (h->nseg == 0 && !h->vstage && !getenv("AJM_NO_NOSEG")) h->fn = kVariants[h->variant].fn0;
+        // no long rows: the variant without the segment phases -- measured faster for narrow
+        // chunks (config 2, width 7: 47.5 -> 45.5 us/pass) but not for wide ones (config 5,
+        // width 27: 1174 -> 1197), so only below an average width of 16
+        const double avg_w = h->nchunks ? (double)h->sell_elems / (32.0 * (double)h->nchunks) : 0.0;
+        if (h->nseg == 0 && !h->vstage && avg_w < 16.0 && !getenv("AJM_NO_NOSEG")) h->fn = kVariants[h->variant].fn0;
         if (const char* ev = getenv("AJM_GRING")) h->gring = atoi(ev) ? 1 : 0;
         if (h->vstage) h->fn = kVariants[h->variant].fnv;
         if (h->jbs) h->gring = 0, h->direct = 0;
