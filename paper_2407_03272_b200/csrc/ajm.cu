@@ -520,14 +520,20 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         h->sigma = 1;
         if (!short_rows.empty() && (double)padded(order) > 1.05 * (double)std::max<int64_t>(short_nnz, 1)) {
             // sort by decreasing length inside windows of 4096 consecutive row indices (stable)
+            // (a stable counting sort: row lengths are <= AJM_SELL_MAX here)
             h->sigma = 4096;
+            std::vector<int> tmp;
             size_t lo = 0;
             while (lo < order.size()) {
                 const int wbase = order[lo] / h->sigma;
                 size_t hi = lo;
                 while (hi < order.size() && order[hi] / h->sigma == wbase) ++hi;
-                std::stable_sort(order.begin() + lo, order.begin() + hi,
-                                 [&](int x, int y) { return rlen(x) > rlen(y); });
+                int cnt[AJM_SELL_MAX + 2] = {0};
+                for (size_t j = lo; j < hi; ++j) ++cnt[AJM_SELL_MAX - rlen(order[j]) + 1];
+                for (int b2 = 1; b2 <= AJM_SELL_MAX + 1; ++b2) cnt[b2] += cnt[b2 - 1];
+                tmp.resize(hi - lo);
+                for (size_t j = lo; j < hi; ++j) tmp[(size_t)cnt[AJM_SELL_MAX - rlen(order[j])]++] = order[j];
+                std::copy(tmp.begin(), tmp.end(), order.begin() + lo);
                 lo = hi;
             }
         }
