@@ -417,6 +417,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fnd, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fng, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fn0, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CC(cudaFuncSetAttribute((const void*)ajm_solve_kernel<4, 96, 4, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
 
     // ---- the CSR arrays and b go to the device now; the copies overlap the host planning ----
     CC(dalloc(&h->rp, n + 1, st));
@@ -729,7 +730,12 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         if (h->nseg == 0 && !h->vstage && avg_w < 16.0 && !getenv("AJM_NO_NOSEG")) h->fn = kVariants[h->variant].fn0;
         if (const char* ev = getenv("AJM_GRING")) h->gring = atoi(ev) ? 1 : 0;
         if (h->vstage) h->fn = kVariants[h->variant].fnv;
-        if (h->jbs) h->gring = 0, h->direct = 0;
+        if (h->jbs) {  // block-diagonal J: its own instantiation (natural order, no segments)
+            h->gring = 0;
+            h->direct = 0;
+            h->vstage = 0;
+            h->fn = ajm_solve_kernel<4, 96, 4, false>;
+        }
         if (h->gring) {
             h->fn = kVariants[h->variant].fng;
             h->vstage = 0;

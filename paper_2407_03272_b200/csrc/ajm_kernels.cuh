@@ -232,8 +232,9 @@ __device__ __forceinline__ void ajm_row_update_plain(double* __restrict__ Qxp, d
 // 32 lanes (row < 0: tail slot, every operand 0, nothing stored).
 __device__ __forceinline__ void ajm_row_update_blk(double* __restrict__ Qxp, double* __restrict__ xf, int i,
                                                    double q, double bi, const double* __restrict__ jr, int bs,
-                                                   double xt, double xpi, double qxp, double beta,
-                                                   int restart_t, AjmAcc& a, uint64_t pol, uint64_t xpol) {
+                                                   const double (&jv)[8], double xt, double xpi, double qxp,
+                                                   double beta, int restart_t, AjmAcc& a, uint64_t pol,
+                                                   uint64_t xpol) {
     const int lane = threadIdx.x & 31;
     const double rq = bi - q;
     a.rr += rq * rq;
@@ -253,9 +254,17 @@ __device__ __forceinline__ void ajm_row_update_blk(double* __restrict__ Qxp, dou
     const double r = bi - qy;
     const int base = lane & ~(bs - 1);
     double z = 0.0;
-    for (int k = 0; k < bs; ++k) {
-        const double rk = __shfl_sync(0xffffffffu, r, base + k);
-        z += __ldcs(jr + 32 * k) * rk;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {  // row entries k < 8 were loaded before the stage wait (jv)
+        const double rk = __shfl_sync(0xffffffffu, r, base + (k & (bs - 1)));
+        if (k < bs) z += jv[k] * rk;
+    }
+    for (int k0 = 8; k0 < bs; k0 += 8) {  // bs = 16, 32: 8 independent loads per batch
+        double jw[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) jw[k] = __ldcs(jr + 32 * (k0 + k));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) z += jw[k] * __shfl_sync(0xffffffffu, r, base + k0 + k);
     }
     const double xn = y + z;
     if (i >= 0) ajm_stp(xf + i, xn, xpol);
@@ -602,6 +611,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     const int u0 = p.cta_unit[bid], u1 = p.cta_unit[bid + 1];
     const int nunits = u1 - u0;
     constexpr bool gring = (kMode == 3);
+    constexpr bool jblk = (kMode == 4);    // as 0 with the block-diagonal J of eq-J-blkdiag
     constexpr bool vstage = (kMode == 1);  // the unit's rows are contiguous (internal numbering)
     constexpr bool vecs = vstage || gring; // row operands staged in shared memory
     constexpr bool direct = (kMode == 2);
@@ -850,11 +860,17 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                         row = p.ident ? (slot < p.n_sell ? slot : -1) : __ldg(p.perm + slot);
                         if (row >= 0) {  // operands in flight during the stage wait
                             bi = ajm_ldp(p.b + row, vpol);
-                            Di = ajm_ldp(p.D + row, vpol);
+                            if (!jblk) Di = ajm_ldp(p.D + row, vpol);
                             xt = ajm_ld(xc + row);
                             xpi = ajm_ld(xp + row);
                             qxp = ajm_ldp(p.Qxp + row, vpol);
                         }
+                    }
+                    double jv[8];  // (jblk) this row's first 8 entries of J^{-1}, also in flight
+                    const double* jr = jblk ? p.Jinv + (size_t)(cfirst + j) * p.jbs * 32 + lane : nullptr;
+                    if (jblk) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) jv[k] = (k < p.jbs) ? __ldcs(jr + 32 * k) : 0.0;
                     }
                     ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);
                     if (gring) ajm_mbar_wait(&s_gath[stage], par, &c->timeout_flag);
@@ -869,9 +885,9 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                     const int off = (e0 - s_coff[s_uc0[uu]]) + lane;
                     const double q = gring ? ajm_chunk_dot_smem(st_val(stage) + off, st_xg(stage) + off, w)
                                            : ajm_chunk_dot(st_val(stage) + off, st_col(stage) + off, w, xc);
-                    if (p.jbs)  // block-diagonal J: warp-uniform branch, every lane takes part
-                        ajm_row_update_blk(p.Qxp, xf, row, q, bi, p.Jinv + (size_t)(cfirst + j) * p.jbs * 32 + lane,
-                                           p.jbs, xt, xpi, qxp, beta, restart_t, acc, vpol, xpol);
+                    if (jblk)  // every lane takes part (shuffles); tail lanes store nothing
+                        ajm_row_update_blk(p.Qxp, xf, row, q, bi, jr, p.jbs, jv, xt, xpi, qxp, beta, restart_t, acc,
+                                           vpol, xpol);
                     else if (row >= 0)
                         ajm_row_update(p.Qxp, xf, row, q, bi, Di, xt, xpi, qxp, beta, restart_t, acc, vpol, xpol);
                 } else {
