@@ -54,6 +54,7 @@ WORKLOADS = {
 }
 WORKLOAD = WORKLOADS[2]["workload"]
 NOMINAL_HBM_GBS = 8000.0
+GATHER_PEAK_GPS = 282.0  # random 8-byte gathers/s from an L2-resident array, measured
 
 
 def load_peaks():
@@ -359,6 +360,14 @@ def run_ours(args):
                      "achieved_basis": "algorithmic bytes nnz*12+7n*8+4(n+1) per pass (D replaced by bs "
                                        "doubles of J^-1 per row with --jblock) x passes / launch duration "
                                        "(CUDA events on the launch stream)"},
+        # second roof for the x~ gathers: one random 8-byte load per stored nonzero and pass,
+        # against the measured ceiling of random 8-byte gathers from an L2-resident array
+        # (tools/ubench/gather_mlp.cu, profiles/r1_ubench_gather_mlp.jsonl); binding for the
+        # graph Laplacians (configs 3, 4), not for the stencils (whose gathers mostly hit L1)
+        "roofline_gather": {"bound": "l2_random_gather", "achieved": p.Q.nnz * passes / (loop_ms * 1e-3) / 1e9,
+                            "peak": GATHER_PEAK_GPS, "unit": "G gathers/s",
+                            "frac": p.Q.nnz * passes / (loop_ms * 1e-3) / 1e9 / GATHER_PEAK_GPS,
+                            "peak_source": "measured on this pool: tools/ubench/gather_mlp.cu (8-32 MB array)"},
         "e2e": {"value": e2e_iters / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "note": "ajm_create from pinned host CSR+b (H2D + layout build) + ajm_solve to 1e-6 "
