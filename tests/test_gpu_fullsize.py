@@ -86,3 +86,14 @@ def test_config5_full_bounded_and_thm23():
     slack = 1e-9 * max(1.0, abs(fstar))
     assert np.all(gap <= bound + slack)
     assert np.all(gap >= -slack)
+
+
+def test_config2_full_block_j_1000_iterations(cfg2):
+    """eq-J-blkdiag at the full 128^3 size, bs = 4: blocks 1e-13, iterates 1e-10."""
+    p = cfg2
+    g = gpu_solve(p.Q, p.b, tol=0.0, maxit=1000, restart=True, jblock=4)
+    Jo = oracle.build_jblock(p.Q, 4)
+    np.testing.assert_allclose(g.J, Jo, rtol=1e-13, atol=1e-13 * np.abs(Jo).max())
+    o, nforced = oracle_matching(p.Q, p.b, g, tol=0.0, maxit=1000, restart=True, jblock=4)
+    assert g.iterations == o.iterations == 1000
+    assert max_rel(g.x, o.x) <= PARITY_TOL, (max_rel(g.x, o.x), nforced)

@@ -211,3 +211,29 @@ def test_sdd_paper_experiment(n):
     g = gpu_solve(Q, b, tol=1e-4, maxit=5000, restart=True)
     it, res = exp_sdd.scalar_ajm(n, 1e-4, 5000)
     assert g.status == "converged" and abs(g.iterations - it) <= 1
+
+
+@pytest.mark.parametrize("dynseg", ["0", "1"])
+def test_segment_queue_modes(dynseg, monkeypatch):
+    """Both segment schedules (static LPT plan / dynamic claim queue, AJM_DYNSEG) give the same
+    iterates as the oracle on a Chung-Lu graph with split rows and on the dense §4.1 rows; each is
+    deterministic run to run (the queue only decides which warp runs a segment)."""
+    monkeypatch.setenv("AJM_DYNSEG", dynseg)
+    for p in (synth.config_problem(4, 0.0125), synth.make_problem("sdd", synth.sdd(2600), 3)):
+        a = gpu_solve(p.Q, p.b, tol=0.0, maxit=300, restart=True)
+        b = gpu_solve(p.Q, p.b, tol=0.0, maxit=300, restart=True)
+        np.testing.assert_array_equal(a.x, b.x)
+        o, _ = oracle_matching(p.Q, p.b, a, tol=0.0, maxit=300, restart=True)
+        assert max_rel(a.x, o.x) <= PARITY_TOL
+
+
+def test_relabelled_layout_x0_and_diag():
+    """Sorted-window layouts solve in an internal row order; x0, x and D cross the boundary in the
+    caller's order (non-zero x0, ER graph)."""
+    p = synth.config_problem(3, 0.01)
+    x0 = synth.random_vector(p.Q.n, 77)
+    g = gpu_solve(p.Q, p.b, x0=x0, tol=0.0, maxit=200, restart=True)
+    assert g.info["sigma"] > 1
+    np.testing.assert_array_equal(g.D, oracle.build_jdiag(p.Q))
+    o, _ = oracle_matching(p.Q, p.b, g, x0=x0, tol=0.0, maxit=200, restart=True)
+    assert max_rel(g.x, o.x) <= PARITY_TOL
