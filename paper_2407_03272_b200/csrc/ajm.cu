@@ -79,6 +79,7 @@ struct ajm_ctx {
     int vstage = 0;
     int direct = 0;
     int gring = 0;                     // kMode 3 gather ring
+    int cluster = 0;                   // grid <= 16 CTAs launched as one cluster (DSMEM barrier)
     unsigned long long* ts = nullptr;  // debug phase timestamps (AJM_TS=1)
     double* vecs = nullptr;            // X0 X1 X2 Qxp b D, one allocation
     int l2persist = 1;
@@ -293,8 +294,15 @@ cudaError_t launch_solver(ajm_ctx* h, AjmPass& p, cudaStream_t st) {
     cfg.dynamicSmemBytes = h->dyn_smem;
     cfg.stream = st;
     cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
+    if (h->cluster) {  // the grid is one thread-block cluster (co-scheduled by construction)
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)h->grid;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+    } else {
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+    }
     int na = 1;
     if (h->win_bytes) {
         at[1].id = cudaLaunchAttributeAccessPolicyWindow;
@@ -760,6 +768,10 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             h->ctas_per_sm = occ;
             const int64_t g = (int64_t)h->sm_count * occ;
             h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(g, nitems));
+            // <= 128 work items: one item per consumer warp on <= 16 CTAs, launched below as a
+            // single cluster whose barrier lives in distributed shared memory
+            if (nitems <= 16 * AJM_WARPS && h->variant == 0 && !getenv("AJM_NO_CLUSTER"))
+                h->grid = (int)std::max<int64_t>(1, (nitems + AJM_WARPS - 1) / AJM_WARPS);
             plan(h->grid);
             const size_t need = (size_t)(h->meta_units + h->meta_chunks) * sizeof(int);
             if (need <= meta) break;
@@ -767,6 +779,36 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             meta = need;
         }
         const int G = h->grid;
+        // small problems: the grid as ONE thread-block cluster, barrier and partial exchange in
+        // distributed shared memory (variant 0 kernels only; AJM_NO_CLUSTER disables)
+        if (G <= 16 && h->variant == 0 && !h->direct && !h->gring && !h->vstage && !getenv("AJM_NO_CLUSTER")) {
+            SolveFn cf = nullptr;
+            if (h->jbs) cf = ajm_solve_kernel<4, 96, 4, false, true>;
+            else if (h->fn == kVariants[0].fn0) cf = ajm_solve_kernel<4, 96, 0, false, true>;
+            else if (h->fn == kVariants[0].fn) cf = ajm_solve_kernel<4, 96, 0, true, true>;
+            if (cf) {
+                cudaFuncSetAttribute((const void*)cf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem);
+                cudaFuncSetAttribute((const void*)cf, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+                if (G > 8) cudaFuncSetAttribute((const void*)cf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                cudaLaunchConfig_t qc = {};
+                qc.gridDim = dim3(G);
+                qc.blockDim = dim3(block_threads(h));
+                qc.dynamicSmemBytes = h->dyn_smem;
+                cudaLaunchAttribute qa[1];
+                qa[0].id = cudaLaunchAttributeClusterDimension;
+                qa[0].val.clusterDim.x = (unsigned)G;
+                qa[0].val.clusterDim.y = 1;
+                qa[0].val.clusterDim.z = 1;
+                qc.attrs = qa;
+                qc.numAttrs = 1;
+                int ncl = 0;
+                if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)cf, &qc) == cudaSuccess && ncl >= 1) {
+                    h->fn = cf;
+                    h->cluster = 1;
+                }
+                cudaGetLastError();
+            }
+        }
         // owner of a split row = the CTA that runs its last segment
         std::vector<int> seg_cta((size_t)h->nseg, 0);
         for (int cc = 0; cc < G; ++cc)
@@ -1087,7 +1129,7 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
     if (h->ts) {  // debug: mean phase durations of CTA 0 over the first passes
         unsigned long long hts[64 * 8];
         AJM_CUDA(h, cudaMemcpy(hts, h->ts, sizeof(hts), cudaMemcpyDeviceToHost));
-        double acc[5] = {0, 0, 0, 0, 0}, seg = 0, chk = 0;
+        double acc[5] = {0, 0, 0, 0, 0}, seg = 0, chk = 0, ctl = 0;
         int np = 0;
         for (int k = 2; k + 1 < 64 && k + 1 <= c.s.iterations; ++k) {
             if (!hts[k * 8 + 5] || !hts[(k + 1) * 8]) break;
@@ -1095,6 +1137,7 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
             acc[4] += (double)(hts[(k + 1) * 8] - hts[k * 8 + 4]);
             seg += (double)(hts[k * 8 + 6] - hts[k * 8 + 0]);
             chk += (double)(hts[k * 8 + 7] - hts[k * 8 + 6]);
+            ctl += (double)(hts[k * 8 + 5] - hts[k * 8 + 4]);
             ++np;
         }
         std::vector<unsigned long long> cta((size_t)2 * h->grid);
@@ -1116,8 +1159,8 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
         }
         if (np)
             fprintf(stderr, "[ajm ts] passes %d: work %.2f us, block-reduce %.2f, grid-barrier %.2f, "
-                            "partials %.2f, control+sync %.2f | segments %.2f, chunks %.2f\n", np, acc[0] / np / 1e3,
-                    acc[1] / np / 1e3, acc[2] / np / 1e3, acc[3] / np / 1e3, acc[4] / np / 1e3, seg / np / 1e3,
+                            "partials %.2f, control+sync %.2f (control %.2f) | segments %.2f, chunks %.2f\n", np, acc[0] / np / 1e3,
+                    acc[1] / np / 1e3, acc[2] / np / 1e3, acc[3] / np / 1e3, acc[4] / np / 1e3, ctl / np / 1e3, seg / np / 1e3,
                     chk / np / 1e3);
     }
 
@@ -1205,7 +1248,7 @@ ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info) {
     info->variant = h->variant;
     info->l2_window_bytes = (int64_t)h->win_bytes;
     info->l2_hit_ratio = h->win_hit;
-    info->mode = h->gring ? 3 : h->direct ? 2 : (h->vstage ? 1 : 0);
+    info->mode = h->gring ? 3 : h->direct ? 2 : h->vstage ? 1 : (h->cluster ? 5 : 0);
     info->sell_elems = h->sell_elems;
     info->l2_mode = h->l2_mode;
     info->launches_per_solve = (int32_t)(1 + (h->prime_bytes ? 1 : 0) + std::max<int64_t>(h->last_launches, 1));

@@ -556,6 +556,38 @@ __device__ __forceinline__ void ajm_chunk_direct(const AjmPass& p, int ch, int w
     if (row >= 0) ajm_row_update_plain(p.Qxp, xf, row, s, bi, Di, xt, xpi, qxp, beta, restart_t, acc);
 }
 
+// ---- distributed shared memory (single-cluster variant) ----
+// arrive (release at cluster scope) on the mbarrier at the same smem offset in CTA `rank`
+__device__ __forceinline__ void ajm_cluster_arrive(uint64_t* bar, unsigned rank) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(ajm_smem(bar)), "r"(rank)
+        : "memory");
+}
+// wait (acquire at cluster scope) for the local mbarrier's phase with the given parity; bounded
+__device__ __forceinline__ bool ajm_cluster_wait(uint64_t* bar, unsigned parity, unsigned* timeout_flag) {
+    long long spins = 0;
+    for (;;) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(ajm_smem(bar)), "r"(parity) : "memory");
+        if (ok) return false;
+        if (++spins > (1LL << 28)) {
+            atomicExch(timeout_flag, 1u);
+            return true;
+        }
+    }
+}
+// load a double at the same smem offset in CTA `rank`
+__device__ __forceinline__ double ajm_ld_cluster(const double* local, unsigned rank) {
+    double v;
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %1, %2;\n\tld.shared::cluster.f64 %0, [ra];\n\t}"
+        : "=d"(v) : "r"(ajm_smem(local)), "r"(rank) : "memory");
+    return v;
+}
+
 // The persistent solver kernel (cooperative launch; grid = resident CTAs).  AJM_BLOCK consumer
 // threads + one producer warp.  The producer streams this CTA's SELL units into a kStages-deep
 // shared-memory ring with cp.async.bulk (TMA engine, mbarrier complete_tx):
@@ -589,7 +621,11 @@ __device__ __forceinline__ double ajm_chunk_dot_smem(const double* sv, const dou
 
 // kSeg = false: layouts without warp segments (all rows in SELL, e.g. stencils) -- phases (1) and
 // (3) are compiled out of the hot loop.
-template <int kStages, int kMaxReg, int kMode, bool kSeg = true>
+// kCluster = true: the whole grid is ONE thread-block cluster (<= 16 CTAs, small problems): the
+// per-pass barrier and the exchange of the CTA partials go through distributed shared memory
+// (remote mbarrier arrivals, ld.shared::cluster) instead of global memory.  Same reduction order
+// as the global path, so the results are bitwise those of the cooperative launch with the same grid.
+template <int kStages, int kMaxReg, int kMode, bool kSeg = true, bool kCluster = false>
 __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     extern __shared__ __align__(128) unsigned char s_dyn[];
     __shared__ double s_red[AJM_WARPS][AJM_NPART];
@@ -602,6 +638,9 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     __shared__ volatile int s_bufc, s_bufp;  // x~^t / x^{t-1} buffer indices of pass s_pass
     __shared__ volatile int s_endpass;       // (kMode 3) first pass that never runs, -1 while running
     __shared__ __align__(8) uint64_t s_gath[kStages];
+    __shared__ __align__(8) uint64_t s_cbar;   // (kCluster) per-pass barrier: G arrivals per phase
+    __shared__ __align__(8) uint64_t s_cexit;  // (kCluster) every CTA done with the others' smem
+    __shared__ double s_part[2][AJM_NPART];    // (kCluster) this CTA's partials by pass parity
     __shared__ int s_to;
 
     AjmCtrl* c = p.ctrl;
@@ -650,9 +689,16 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
             ajm_mbar_init(&s_empty[k], AJM_WARPS);
             ajm_mbar_init(&s_gath[k], AJM_GWARPS * 32 + 1);  // cp.async arrivals + one expect_tx arrival
         }
+        if (kCluster) {
+            ajm_mbar_init(&s_cbar, gridDim.x);
+            ajm_mbar_init(&s_cexit, gridDim.x);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    if (kCluster) {  // every CTA's barriers initialised before any remote arrival
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
 
     if (warp == AJM_WARPS) {
         // ---------------- producer warp (one lane) ----------------
@@ -929,7 +975,27 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         // partials as 5 arrays of G (SoA) so the all-CTA read below is coalesced
         double* part = p.partials + (size_t)(t & 1) * G * AJM_NPART;
         double an_c = 0.0, beta_c = 0.0;
-        if (tid == 0) {
+        if (kCluster && warp == 0) {
+            if (lane == 0) {
+                double* sp = s_part[t & 1];
+                sp[0] = acc.rr;
+                sp[1] = acc.xq;
+                sp[2] = acc.bx;
+                sp[3] = acc.d;
+                sp[4] = acc.dabs;
+            }
+            __syncwarp();
+            // lane r arrives (release, cluster scope: this CTA's x~/Qx stores and partials) on CTA
+            // r's barrier -- the G remote arrivals go out in parallel
+            if (lane < (int)G) ajm_cluster_arrive(&s_cbar, (unsigned)lane);
+        }
+        if (kCluster && tid == 0) {
+            const double a = s_st.alpha;
+            an_c = (1.0 + sqrt(1.0 + 4.0 * a * a)) / 2.0;
+            beta_c = s_st.momentum ? (a - 1.0) / an_c : 0.0;
+            s_to = ajm_cluster_wait(&s_cbar, (unsigned)(t & 1), &c->timeout_flag) ? 1 : 0;
+            __threadfence();  // invalidate this SM's L1 before re-reading x~ written by other SMs
+        } else if (!kCluster && tid == 0) {
             part[0 * G + bid] = acc.rr;
             part[1 * G + bid] = acc.xq;
             part[2 * G + bid] = acc.bx;
@@ -951,6 +1017,9 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
             // order (8 loads in flight), then a fixed xor tree -- identical bits in every CTA
             const double* src = part + (size_t)warp * G;
             double v = 0.0;
+            if (kCluster) {  // G <= 16: lane l holds CTA l's record (the global path's order)
+                if (lane < (int)G) v = ajm_ld_cluster(&s_part[t & 1][warp], (unsigned)lane);
+            } else
             for (int k0 = lane; k0 < (int)G; k0 += 8 * 32) {
                 double r[8];
 #pragma unroll
@@ -984,6 +1053,12 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         __threadfence_block();
         s_stop = 1;
         if (bid == 0) c->s = s_st;
+    }
+    if (kCluster && warp == 0) {  // no CTA leaves while another may still read its partials
+        __syncwarp();
+        if (lane < (int)G) ajm_cluster_arrive(&s_cexit, (unsigned)lane);
+        if (lane == 0) ajm_cluster_wait(&s_cexit, 0u, &c->timeout_flag);
+        __syncwarp();
     }
 }
 
