@@ -319,9 +319,8 @@ __device__ __forceinline__ void ajm_block_reduce(AjmAcc& a, double (*s_red)[AJM_
 // a7 control step (thread 0 of every CTA, identical inputs -> identical outputs).  CTA 0 also
 // writes the histories and the restart log.
 __device__ void ajm_control_step(AjmState& s, const double* tot, AjmCtrl* c, bool writer, double an_c,
-                                 double beta_c) {
+                                 double beta_c, double res) {
     const long long t = s.t;
-    const double res = sqrt(tot[0]) / s.nb;
     const double f = 0.5 * tot[1] - tot[2];
     if (writer) {
         c->res_hist[t] = res;
@@ -630,6 +629,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     extern __shared__ __align__(128) unsigned char s_dyn[];
     __shared__ double s_red[AJM_WARPS][AJM_NPART];
     __shared__ double s_tot[AJM_NPART];
+    __shared__ double s_res;
     __shared__ AjmState s_st;
     __shared__ __align__(8) uint64_t s_full[kStages];
     __shared__ __align__(8) uint64_t s_empty[kStages];
@@ -1030,11 +1030,15 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
             }
             v = ajm_warp_sum(v);
             if (lane == 0) s_tot[warp] = v;
+            // the relative residual ||b - Q x~||/||b|| off the serial control path
+            if (warp == 0 && lane == 0) s_res = sqrt(v) / s_st.nb;
         }
         ajm_csync();
         if (tsw) p.ts[pass * 8 + 4] = ajm_gtime();
         if (tid == 0) {
-            ajm_control_step(s_st, s_tot, c, bid == 0, an_c, beta_c);
+            AjmState ls = s_st;  // the control step on a register copy of the shared state
+            ajm_control_step(ls, s_tot, c, bid == 0, an_c, beta_c, s_res);
+            s_st = ls;
             if (timed_out) s_st.done = 1;
             if (tsw) p.ts[pass * 8 + 5] = ajm_gtime();
             if (!s_st.done) {  // the next pass may stage its dynamic vectors now
