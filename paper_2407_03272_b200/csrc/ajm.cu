@@ -214,7 +214,11 @@ cudaError_t dalloc(T** p, size_t count, cudaStream_t s) {
     cudaMemPool_t mp = ajm_pool(dev);
     const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
     if (!mp) return cudaMalloc((void**)p, bytes);
-    return cudaMallocFromPoolAsync((void**)p, bytes, mp, s);
+    cudaError_t e = cudaMallocFromPoolAsync((void**)p, bytes, mp, s);
+    // AJM_POISON (tests): fill new allocations with 0xff so a read of memory the library never
+    // wrote shows up deterministically instead of depending on what the pool hands back
+    if (e == cudaSuccess && getenv("AJM_POISON")) cudaMemsetAsync(*p, 0xff, bytes, s);
+    return e;
 }
 
 void dfree(void* p) {
@@ -352,7 +356,10 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     std::string tsc_log;
     auto mark = [&](const char* what, cudaStream_t s_) {
         if (!tsc) return;
-        if (s_ != (cudaStream_t)-1) cudaStreamSynchronize(s_);
+        if (s_ != (cudaStream_t)-1) {
+            cudaError_t e_ = cudaStreamSynchronize(s_);
+            if (e_ != cudaSuccess) fprintf(stderr, "[ajm create] error after phase before '%s': %s\n", what, cudaGetErrorString(e_));
+        }
         auto now = std::chrono::steady_clock::now();
         char b[96];
         snprintf(b, sizeof b, " %s %.2f", what, std::chrono::duration<double, std::milli>(now - t_last).count());

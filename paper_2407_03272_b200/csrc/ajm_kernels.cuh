@@ -1168,8 +1168,8 @@ __global__ void ajm_sum_final_kernel(int m, const double* __restrict__ part, dou
 
 
 // SELL fill: slot-parallel copy of each short row's entries into its chunk column; padding
-// (k >= row length, and tail slots) is val 0 / col = own row (or 0), appended AFTER the row's
-// entries so the sequential sum order is unchanged.
+// (k >= row length, and tail slots) is val 0 / col = the slot's own internal row (or 0),
+// appended AFTER the row's entries so the sequential sum order is unchanged.
 __global__ void ajm_sell_fill_kernel(int nslots_padded, int n_sell, const int* __restrict__ perm,
                                      int ident, const int* __restrict__ rp, const int* __restrict__ col,
                                      const double* __restrict__ val, const long long* __restrict__ chunk_off,
@@ -1179,13 +1179,14 @@ __global__ void ajm_sell_fill_kernel(int nslots_padded, int n_sell, const int* _
     const int ch = slot >> 5, lane = slot & 31;
     const long long base = chunk_off[ch];
     const int w = (int)((chunk_off[ch + 1] - base) >> 5);
-    const int row = ident ? (slot < n_sell ? slot : -1) : perm[slot];
+    // slot -> caller's row (perm has n_sell entries; slots past them are chunk tail padding)
+    const int row = slot < n_sell ? (ident ? slot : perm[slot]) : -1;
     int k0 = 0, len = 0;
     if (row >= 0) { k0 = rp[row]; len = rp[row + 1] - k0; }
     for (int k = 0; k < w; ++k) {
         const long long e = base + (long long)k * 32 + lane;
         if (k < len) { sval[e] = val[k0 + k]; scol[e] = col[k0 + k]; }
-        else { sval[e] = 0.0; scol[e] = row >= 0 ? row : 0; }
+        else { sval[e] = 0.0; scol[e] = slot < n_sell ? slot : 0; }  // padding: own (internal) row
     }
 }
 

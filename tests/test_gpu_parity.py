@@ -237,3 +237,20 @@ def test_relabelled_layout_x0_and_diag():
     np.testing.assert_array_equal(g.D, oracle.build_jdiag(p.Q))
     o, _ = oracle_matching(p.Q, p.b, g, x0=x0, tol=0.0, maxit=200, restart=True)
     assert max_rel(g.x, o.x) <= PARITY_TOL
+
+
+def test_many_handles_pool_reuse(monkeypatch):
+    """Create / solve / destroy cycles of mixed layouts (natural order, sorted windows with
+    relabelling, single-cluster and cooperative grids) with every new allocation poisoned
+    (AJM_POISON): the pooled memory a handle gets back is never read before it is written
+    (regression: chunk-tail slots once read past the slot->row map)."""
+    monkeypatch.setenv("AJM_POISON", "1")
+    for rep in range(3):
+        for n in (1, 2, 3, 31, 33, 513, 4097):
+            Q = synth.random_spd(n, seed=n, density=min(1.0, 4.0 / n)) if n <= 600 else \
+                synth.er_laplacian(n, 4 * n, seed=5)
+            b = Q.scipy() @ np.random.Generator(np.random.PCG64(n)).uniform(-1, 1, Q.n)
+            g = gpu_solve(Q, b, tol=0.0, maxit=100)
+            if rep == 0:
+                o, _ = oracle_matching(Q, b, g, tol=0.0, maxit=100)
+                assert max_rel(g.x, o.x) <= PARITY_TOL, n
