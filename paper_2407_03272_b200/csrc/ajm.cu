@@ -435,6 +435,9 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fng, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fn0, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     CC(cudaFuncSetAttribute((const void*)ajm_solve_kernel<4, 96, 4, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CC(cudaFuncSetAttribute((const void*)ajm_solve_kernel<4, 96, 4, false, false, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CC(cudaFuncSetAttribute((const void*)ajm_solve_kernel<4, 96, 4, false, false, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CC(cudaFuncSetAttribute((const void*)ajm_solve_kernel<4, 96, 4, false, false, 8>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
 
     // ---- the CSR arrays and b go to the device now; the copies overlap the host planning ----
     CC(dalloc(&h->rp, n + 1, st));
@@ -751,7 +754,10 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             h->gring = 0;
             h->direct = 0;
             h->vstage = 0;
-            h->fn = ajm_solve_kernel<4, 96, 4, false>;
+            h->fn = h->jbs == 2 ? ajm_solve_kernel<4, 96, 4, false, false, 2>
+                  : h->jbs == 4 ? ajm_solve_kernel<4, 96, 4, false, false, 4>
+                  : h->jbs == 8 ? ajm_solve_kernel<4, 96, 4, false, false, 8>
+                                : ajm_solve_kernel<4, 96, 4, false>;
         }
         if (h->gring) {
             h->fn = kVariants[h->variant].fng;
@@ -792,7 +798,10 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         // distributed shared memory (variant 0 kernels only; AJM_NO_CLUSTER disables)
         if (G <= 16 && h->variant == 0 && !h->direct && !h->gring && !h->vstage && !getenv("AJM_NO_CLUSTER")) {
             SolveFn cf = nullptr;
-            if (h->jbs) cf = ajm_solve_kernel<4, 96, 4, false, true>;
+            if (h->jbs) cf = h->jbs == 2 ? ajm_solve_kernel<4, 96, 4, false, true, 2>
+                           : h->jbs == 4 ? ajm_solve_kernel<4, 96, 4, false, true, 4>
+                           : h->jbs == 8 ? ajm_solve_kernel<4, 96, 4, false, true, 8>
+                                         : ajm_solve_kernel<4, 96, 4, false, true>;
             else if (h->fn == kVariants[0].fn0) cf = ajm_solve_kernel<4, 96, 0, false, true>;
             else if (h->fn == kVariants[0].fn) cf = ajm_solve_kernel<4, 96, 0, true, true>;
             if (cf) {

@@ -230,11 +230,13 @@ __device__ __forceinline__ void ajm_row_update_plain(double* __restrict__ Qxp, d
 // chunk (natural order), lane l holds row l of its block's inverse (jr[32 k], k < bs) and gathers
 // the block's residuals by shuffles; z_l = sum_k (J^{-1})_{lk} r_k in ascending k.  Called by all
 // 32 lanes (row < 0: tail slot, every operand 0, nothing stored).
+template <int JB>  // JB > 0: compile-time block size (<= 8); JB = 0: runtime bs (jv holds 8)
 __device__ __forceinline__ void ajm_row_update_blk(double* __restrict__ Qxp, double* __restrict__ xf, int i,
-                                                   double q, double bi, const double* __restrict__ jr, int bs,
-                                                   const double (&jv)[8], double xt, double xpi, double qxp,
+                                                   double q, double bi, const double* __restrict__ jr, int bs_rt,
+                                                   const double* jv, double xt, double xpi, double qxp,
                                                    double beta, int restart_t, AjmAcc& a, uint64_t pol,
                                                    uint64_t xpol) {
+    const int bs = JB > 0 ? JB : bs_rt;
     const int lane = threadIdx.x & 31;
     const double rq = bi - q;
     a.rr += rq * rq;
@@ -254,11 +256,13 @@ __device__ __forceinline__ void ajm_row_update_blk(double* __restrict__ Qxp, dou
     const double r = bi - qy;
     const int base = lane & ~(bs - 1);
     double z = 0.0;
+    constexpr int KP = JB > 0 ? JB : 8;  // row entries k < KP were loaded before the stage wait (jv)
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {  // row entries k < 8 were loaded before the stage wait (jv)
+    for (int k = 0; k < KP; ++k) {
         const double rk = __shfl_sync(0xffffffffu, r, base + (k & (bs - 1)));
         if (k < bs) z += jv[k] * rk;
     }
+    if (JB == 0)
     for (int k0 = 8; k0 < bs; k0 += 8) {  // bs = 16, 32: 8 independent loads per batch
         double jw[8];
 #pragma unroll
@@ -624,7 +628,7 @@ __device__ __forceinline__ double ajm_chunk_dot_smem(const double* sv, const dou
 // per-pass barrier and the exchange of the CTA partials go through distributed shared memory
 // (remote mbarrier arrivals, ld.shared::cluster) instead of global memory.  Same reduction order
 // as the global path, so the results are bitwise those of the cooperative launch with the same grid.
-template <int kStages, int kMaxReg, int kMode, bool kSeg = true, bool kCluster = false>
+template <int kStages, int kMaxReg, int kMode, bool kSeg = true, bool kCluster = false, int kJB = 0>
 __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     extern __shared__ __align__(128) unsigned char s_dyn[];
     __shared__ double s_red[AJM_WARPS][AJM_NPART];
@@ -912,11 +916,13 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                             qxp = ajm_ldp(p.Qxp + row, vpol);
                         }
                     }
-                    double jv[8];  // (jblk) this row's first 8 entries of J^{-1}, also in flight
-                    const double* jr = jblk ? p.Jinv + (size_t)(cfirst + j) * p.jbs * 32 + lane : nullptr;
+                    constexpr int JV = kJB > 0 ? kJB : 8;
+                    double jv[JV];  // (jblk) this row's first entries of J^{-1}, also in flight
+                    const int jbs = kJB > 0 ? kJB : p.jbs;
+                    const double* jr = jblk ? p.Jinv + (size_t)(cfirst + j) * jbs * 32 + lane : nullptr;
                     if (jblk) {
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) jv[k] = (k < p.jbs) ? __ldcs(jr + 32 * k) : 0.0;
+                        for (int k = 0; k < JV; ++k) jv[k] = (k < jbs) ? __ldcs(jr + 32 * k) : 0.0;
                     }
                     ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);
                     if (gring) ajm_mbar_wait(&s_gath[stage], par, &c->timeout_flag);
@@ -932,8 +938,8 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                     const double q = gring ? ajm_chunk_dot_smem(st_val(stage) + off, st_xg(stage) + off, w)
                                            : ajm_chunk_dot(st_val(stage) + off, st_col(stage) + off, w, xc);
                     if (jblk)  // every lane takes part (shuffles); tail lanes store nothing
-                        ajm_row_update_blk(p.Qxp, xf, row, q, bi, jr, p.jbs, jv, xt, xpi, qxp, beta, restart_t, acc,
-                                           vpol, xpol);
+                        ajm_row_update_blk<kJB>(p.Qxp, xf, row, q, bi, jr, jbs, jv, xt, xpi, qxp, beta, restart_t,
+                                                acc, vpol, xpol);
                     else if (row >= 0)
                         ajm_row_update(p.Qxp, xf, row, q, bi, Di, xt, xpi, qxp, beta, restart_t, acc, vpol, xpol);
                 } else {
