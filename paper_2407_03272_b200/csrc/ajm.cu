@@ -26,12 +26,20 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges visible to nsys / ncu, no link dependency
+
 #include "ajm.h"
 #include "ajm_kernels.cuh"
 
 namespace {
 
 thread_local std::string g_create_error;
+
+// NVTX range for the duration of a scope (SURVEY §5 tracing: create / solve / destroy)
+struct NvtxScope {
+    explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+    ~NvtxScope() { nvtxRangePop(); }
+};
 
 typedef void (*SolveFn)(AjmPass);
 struct SolveVariant {
@@ -349,6 +357,7 @@ const char* ajm_last_error(ajm_handle_t h) {
 ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t* row_ptr,
                         const int32_t* col_idx, const double* vals, const double* b, int32_t dmode,
                         const double* d, uint32_t flags, void* cuda_stream) {
+    NvtxScope nvtx_scope_("ajm_create");
     g_create_error.clear();
     // debug (AJM_TS): host wall time of each create phase
     const bool tsc = getenv("AJM_TS") != nullptr;
@@ -1055,6 +1064,7 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
                        ajm_policy_t policy, double* x_out, ajm_result_t* res, double* res_hist,
                        double* f_hist, int64_t* restart_iters, int64_t restart_cap,
                        void* cuda_stream) {
+    NvtxScope nvtx_scope_("ajm_solve");
     if (!h) return fail(nullptr, AJM_ERR_INVALID_ARG, "NULL handle");
     h->err_msg.clear();
     if (!x_out) return fail(h, AJM_ERR_INVALID_ARG, "x_out is NULL");
@@ -1283,6 +1293,7 @@ ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info) {
 }
 
 ajm_status_t ajm_destroy(ajm_handle_t h) {
+    NvtxScope nvtx_scope_("ajm_destroy");
     if (!h) return AJM_OK;
     free_all(h);
     delete h;
