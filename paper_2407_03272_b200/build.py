@@ -18,8 +18,8 @@ NVCC_FLAGS = [
     "-lineinfo",
     "--fmad=false",          # no multiply-add contraction anywhere (R14)
     "-Xptxas", "-v",
-    "-Xcompiler", "-fPIC,-O2",
-    "-shared", "-cudart", "static",
+    "-Xcompiler", "-fPIC,-O2,-fopenmp",  # OpenMP: the host layout planner's O(n) passes
+    "-shared", "-cudart", "static", "-lgomp",
 ]
 
 

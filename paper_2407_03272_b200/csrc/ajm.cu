@@ -478,20 +478,23 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     std::vector<double> chcost;
     // fast path (stencil-like matrices): every row short and natural order pads < 5% -> SELL-32
     // in natural order, no relabelling, no segments; one pass over the row lengths
+    // (host loops below are OpenMP-parallel where the result does not depend on the split)
     bool fast = false;
     {
         const int64_t nch = (n + 31) / 32;
         std::vector<long long> fo((size_t)nch + 1, 0);
         std::vector<double> fc((size_t)nch, 0.0);
         int64_t maxlen = 0;
+#pragma omp parallel for schedule(static) reduction(max : maxlen)
         for (int64_t c = 0; c < nch; ++c) {
             int64_t w = 1;
             const int64_t r1 = std::min<int64_t>(n, c * 32 + 32);
             for (int64_t r = c * 32; r < r1; ++r) w = std::max<int64_t>(w, rlen(r));
             maxlen = std::max(maxlen, w);
-            fo[(size_t)c + 1] = fo[(size_t)c] + 32 * w;
+            fo[(size_t)c + 1] = 32 * w;
             fc[(size_t)c] = 12.0 * 32 * w + 56.0 * (double)(r1 - c * 32) + 64.0;
         }
+        for (int64_t c = 0; c < nch; ++c) fo[(size_t)c + 1] += fo[(size_t)c];
         if (jbs && maxlen > AJM_SELL_MAX)
             return bail(fail(h, AJM_ERR_UNSUPPORTED, "AJM_D_JBLOCK needs every row to have <= %d nonzeros "
                                                        "(the longest has %lld)", AJM_SELL_MAX, (long long)maxlen));
@@ -522,6 +525,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         // faster (873 vs 964 us/pass).  AJM_DYNSEG overrides.
         {
             int64_t long_nnz = 0;
+#pragma omp parallel for schedule(static) reduction(+ : long_nnz)
             for (int64_t i = 0; i < n; ++i)
                 if (rlen(i) > AJM_SELL_MAX) long_nnz += rlen(i);
             h->dynseg = (double)long_nnz >= 0.9 * (double)std::max<int64_t>(nnz, 1) ? 1 : 0;
@@ -537,34 +541,47 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         mark("L-bins", (cudaStream_t)-1);
         auto padded = [&](const std::vector<int>& order) {
             int64_t tot = 0;
-            for (size_t c0 = 0; c0 < order.size(); c0 += 32) {
+            const int64_t nc = ((int64_t)order.size() + 31) / 32;
+#pragma omp parallel for schedule(static) reduction(+ : tot)
+            for (int64_t c = 0; c < nc; ++c) {
                 int64_t w = 1;
-                for (size_t j = c0; j < std::min(order.size(), c0 + 32); ++j) w = std::max<int64_t>(w, rlen(order[j]));
+                for (size_t j = (size_t)c * 32; j < std::min(order.size(), (size_t)c * 32 + 32); ++j)
+                    w = std::max<int64_t>(w, rlen(order[j]));
                 tot += 32 * w;
             }
             return tot;
         };
         int64_t short_nnz = 0;
-        for (int r : short_rows) short_nnz += rlen(r);
+        const int64_t nshort = (int64_t)short_rows.size();
+#pragma omp parallel for schedule(static) reduction(+ : short_nnz)
+        for (int64_t j = 0; j < nshort; ++j) short_nnz += rlen(short_rows[(size_t)j]);
         std::vector<int> order = short_rows;
         h->sigma = 1;
         if (!short_rows.empty() && (double)padded(order) > 1.05 * (double)std::max<int64_t>(short_nnz, 1)) {
             // sort by decreasing length inside windows of 4096 consecutive row indices (stable)
             // (a stable counting sort: row lengths are <= AJM_SELL_MAX here)
             h->sigma = 4096;
-            std::vector<int> tmp;
-            size_t lo = 0;
-            while (lo < order.size()) {
+            std::vector<size_t> wlo;  // window boundaries in `order` (ascending row index)
+            for (size_t lo = 0; lo < order.size();) {
+                wlo.push_back(lo);
                 const int wbase = order[lo] / h->sigma;
-                size_t hi = lo;
-                while (hi < order.size() && order[hi] / h->sigma == wbase) ++hi;
-                int cnt[AJM_SELL_MAX + 2] = {0};
-                for (size_t j = lo; j < hi; ++j) ++cnt[AJM_SELL_MAX - rlen(order[j]) + 1];
-                for (int b2 = 1; b2 <= AJM_SELL_MAX + 1; ++b2) cnt[b2] += cnt[b2 - 1];
-                tmp.resize(hi - lo);
-                for (size_t j = lo; j < hi; ++j) tmp[(size_t)cnt[AJM_SELL_MAX - rlen(order[j])]++] = order[j];
-                std::copy(tmp.begin(), tmp.end(), order.begin() + lo);
-                lo = hi;
+                while (lo < order.size() && order[lo] / h->sigma == wbase) ++lo;
+            }
+            wlo.push_back(order.size());
+            const int64_t nwin = (int64_t)wlo.size() - 1;
+#pragma omp parallel
+            {
+                std::vector<int> tmp;
+#pragma omp for schedule(static)
+                for (int64_t wi = 0; wi < nwin; ++wi) {
+                    const size_t lo = wlo[(size_t)wi], hi = wlo[(size_t)wi + 1];
+                    int cnt[AJM_SELL_MAX + 2] = {0};
+                    for (size_t j = lo; j < hi; ++j) ++cnt[AJM_SELL_MAX - rlen(order[j]) + 1];
+                    for (int b2 = 1; b2 <= AJM_SELL_MAX + 1; ++b2) cnt[b2] += cnt[b2 - 1];
+                    tmp.resize(hi - lo);
+                    for (size_t j = lo; j < hi; ++j) tmp[(size_t)cnt[AJM_SELL_MAX - rlen(order[j])]++] = order[j];
+                    std::copy(tmp.begin(), tmp.end(), order.begin() + (long)lo);
+                }
             }
         }
         mark("L-sort", (cudaStream_t)-1);
@@ -577,7 +594,9 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         h->relabel = !(h->sigma == 1 && split_rows.empty() && whole_rows.empty());
         h->ident = true;  // SELL slot == internal row
         perm_h.assign((size_t)n, 0);
-        for (size_t j = 0; j < order.size(); ++j) perm_h[j] = order[j];
+        const int64_t nord = (int64_t)order.size();
+#pragma omp parallel for schedule(static)
+        for (int64_t j = 0; j < nord; ++j) perm_h[(size_t)j] = order[(size_t)j];
         {
             size_t k = order.size();
             for (int r : split_rows) perm_h[k++] = r;
@@ -586,21 +605,25 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         std::vector<int> inv_h;
         if (h->relabel) {
             inv_h.assign((size_t)n, 0);
+#pragma omp parallel for schedule(static)
             for (int64_t k = 0; k < n; ++k) inv_h[(size_t)perm_h[(size_t)k]] = (int)k;
         }
         auto irow = [&](int r) { return h->relabel ? inv_h[(size_t)r] : r; };
         mark("L-perm", (cudaStream_t)-1);
         choff.assign((size_t)h->nchunks + 1, 0);
         chcost.assign((size_t)h->nchunks, 0.0);
-        for (int64_t c = 0; c < h->nchunks; ++c) {
+        const int64_t nchk_h = h->nchunks, nsell_h = h->n_sell;
+#pragma omp parallel for schedule(static)
+        for (int64_t c = 0; c < nchk_h; ++c) {
             int64_t w = 1, rows = 0;
-            for (int64_t j = c * 32; j < std::min<int64_t>(h->n_sell, c * 32 + 32); ++j) {
+            for (int64_t j = c * 32; j < std::min<int64_t>(nsell_h, c * 32 + 32); ++j) {
                 w = std::max<int64_t>(w, rlen(order[(size_t)j]));
                 ++rows;
             }
-            choff[(size_t)c + 1] = choff[(size_t)c] + 32 * w;
+            choff[(size_t)c + 1] = 32 * w;
             chcost[(size_t)c] = 12.0 * 32 * w + 56.0 * rows + 64.0;
         }
+        for (int64_t c = 0; c < nchk_h; ++c) choff[(size_t)c + 1] += choff[(size_t)c];
         h->sell_elems = choff.back();
         mark("L-chunks", (cudaStream_t)-1);
         // segments: split rows first (consecutive per row), then whole rows
