@@ -323,6 +323,9 @@ def run_ours(args):
     tr = None if args.jblock else load_traffic(p.name)
     traffic = None if tr is None else tr["dram_bytes_per_pass"] * passes / args.steps
     cpu = cpu_baseline_run(p, args.config) if (world == 1 and not args.no_cpu_baseline) else None
+    # the same oracle on ONE host thread (SURVEY §8(d) oracle timing (i)), a shorter sample
+    cpu1 = cpu_baseline_run(p, args.config, budget_s=4.0, nthreads=1) \
+        if (world == 1 and not args.no_cpu_baseline) else None
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
     l2_note = (f"inputs larger than L2: {model_bytes / 1e6:.1f} MB algorithmic traffic per pass vs "
                f"{l2_bytes / 1e6:.0f} MB L2" if model_bytes > l2_bytes else
@@ -375,6 +378,7 @@ def run_ours(args):
         "gpu_launches": int(info["launches_per_solve"]) * args.steps,
         "clocks": clk,
         "cpu_baseline": cpu,
+        "cpu_baseline_1thread": cpu1,
     }
     print(json.dumps(line), flush=True)
     solver.close()
