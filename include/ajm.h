@@ -138,9 +138,9 @@ typedef struct {
  * Ownership: the handle deep-copies (and re-lays-out) Q, b and D into device memory it owns; the
  * caller's buffers may be freed when the call returns.
  * Side effects: device memory comes from a library-owned stream-ordered pool that keeps up to
- * 16 GiB of freed memory for later creates; when the six iterate vectors fit the L2 (but not the
- * persisting carve-out's 3/4) the call raises the device's cudaLimitPersistingL2CacheSize to hold
- * them (a device-wide setting).
+ * 16 GiB of freed memory for later creates; when the six iterate vectors fit the L2 the call
+ * raises the device's cudaLimitPersistingL2CacheSize to min(their size, the device maximum) so a
+ * persisting access-policy window can keep them resident (a device-wide setting).
  */
 ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t* row_ptr,
                         const int32_t* col_idx, const double* vals, const double* b,
