@@ -46,7 +46,7 @@ typedef enum {
     AJM_ERR_ZERO_RHS = 7,      /* ||b|| = 0: the relative-residual stopping rule is undefined */
     AJM_ERR_CUDA = 8,          /* a CUDA runtime call failed (message in ajm_last_error)              */
     AJM_ERR_OOM = 9,           /* device allocation failed                                            */
-    AJM_ERR_UNSUPPORTED = 10   /* e.g. nnz >= 2^31 (device column/offset type is int32)              */
+    AJM_ERR_UNSUPPORTED = 10   /* e.g. n >= 2^31, or nnz >= 2^31 with rows of > 64 nonzeros          */
 } ajm_status_t;
 
 /* The diagonal metric D of the Jacobi-type step x = y + D^{-1}(b - Q y). */
@@ -127,7 +127,8 @@ typedef struct {
 /*
  * ajm_create -- validate Q, b (and d), build the device layout and the diagonal metric D.
  *   out       : receives the handle (written only on AJM_OK)
- *   n, nnz    : 1 <= n < 2^31, 0 <= nnz < 2^31
+ *   n, nnz    : 1 <= n < 2^31, nnz >= 0 (nnz >= 2^31 only when every row has <= 64 nonzeros,
+ *               else AJM_ERR_UNSUPPORTED)
  *   row_ptr   : int64[n+1], canonical CSR offsets (row_ptr[0] = 0, nondecreasing, row_ptr[n] = nnz)
  *   col_idx   : int32[nnz], strictly increasing within each row, 0 <= col < n
  *   vals      : double[nnz]; BOTH triangles of the symmetric Q are stored

@@ -98,7 +98,7 @@ struct ajm_ctx {
     int grid = 0;
     uint32_t flags = 0;
     // device arrays
-    int* rp = nullptr;
+    long long* rp = nullptr;   // int64 row offsets (create-time kernels; nnz may exceed 2^31)
     int* col = nullptr;
     double* val = nullptr;
     double* b = nullptr;
@@ -377,8 +377,8 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     };
     if (!out) return fail(nullptr, AJM_ERR_INVALID_ARG, "out is NULL");
     if (n < 1 || nnz < 0) return fail(nullptr, AJM_ERR_INVALID_ARG, "n must be >= 1 and nnz >= 0");
-    if (n >= (int64_t)1 << 31 || nnz >= (int64_t)1 << 31)
-        return fail(nullptr, AJM_ERR_UNSUPPORTED, "n and nnz must be < 2^31 (int32 device offsets)");
+    if (n >= (int64_t)1 << 31)
+        return fail(nullptr, AJM_ERR_UNSUPPORTED, "n must be < 2^31 (int32 column indices)");
     if (!row_ptr || !b || (nnz > 0 && (!col_idx || !vals)))
         return fail(nullptr, AJM_ERR_INVALID_ARG, "NULL array argument");
     if (dmode < 0 || dmode > 3) return fail(nullptr, AJM_ERR_INVALID_ARG, "bad dmode %d", dmode);
@@ -453,17 +453,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(dalloc(&h->col, nnz + 8, st));
     CC(dalloc(&h->val, nnz + 8, st));
     CC(dalloc(&h->b_in, n, st));
-    if (rp_dev) {
-        ajm_rowptr_narrow_kernel<<<1024, 256, 0, st>>>(n + 1, (const long long*)row_ptr, h->rp);
-        CC(cudaGetLastError());
-    } else {
-        int64_t* rp64 = nullptr;
-        CC(dalloc(&rp64, n + 1, st));
-        CC(cudaMemcpyAsync(rp64, hrp, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
-        ajm_rowptr_narrow_kernel<<<1024, 256, 0, st>>>(n + 1, (const long long*)rp64, h->rp);
-        CC(cudaGetLastError());
-        CC(cudaFreeAsync(rp64, st));
-    }
+    CC(cudaMemcpyAsync(h->rp, row_ptr, sizeof(int64_t) * (n + 1), kind_to_device(row_ptr), st));
     if (nnz > 0) {
         CC(cudaMemcpyAsync(h->col, col_idx, sizeof(int32_t) * nnz, kind_to_device(col_idx), st));
         CC(cudaMemcpyAsync(h->val, vals, sizeof(double) * nnz, kind_to_device(vals), st));
@@ -538,6 +528,10 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             else split_rows.push_back((int)i);
         }
         h->long_rows = (int64_t)split_rows.size();
+        // the SELL path indexes with 64-bit offsets; warp segments keep int32 CSR offsets
+        if (nnz >= ((int64_t)1 << 31) && !(split_rows.empty() && whole_rows.empty()))
+            return bail(fail(h, AJM_ERR_UNSUPPORTED, "nnz >= 2^31 needs every row to have <= %d nonzeros",
+                             AJM_SELL_MAX));
         mark("L-bins", (cudaStream_t)-1);
         auto padded = [&](const std::vector<int>& order) {
             int64_t tot = 0;

@@ -79,7 +79,7 @@ struct AjmCtrl {
 
 struct AjmPass {
     // CSR (segment rows)
-    const int* __restrict__ rp;
+    const long long* __restrict__ rp;        // (create-time kernels only)
     const int* __restrict__ col;
     const double* __restrict__ val;
     // SELL-32-sigma of the short rows: chunk c, element k of slot l at chunk_off[c] + 32 k + l
@@ -1111,7 +1111,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
 
 // Column range / strict order / finiteness / diagonal, and D per dmode.  One thread per row,
 // ascending-column sequential sums: D_kk = Q_kk + sum_{j != k}|Q_kj| (eq-J-diag).
-__global__ void ajm_validate_diag_kernel(int n, const int* __restrict__ rp, const int* __restrict__ col,
+__global__ void ajm_validate_diag_kernel(int n, const long long* __restrict__ rp, const int* __restrict__ col,
                                          const double* __restrict__ val, int dmode,
                                          const double* __restrict__ duser, double* __restrict__ D,
                                          int* __restrict__ err) {
@@ -1120,7 +1120,7 @@ __global__ void ajm_validate_diag_kernel(int n, const int* __restrict__ rp, cons
     int e = 0;
     double qkk = 0.0, off = 0.0;
     int last = -1;
-    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+    for (long long k = rp[i]; k < rp[i + 1]; ++k) {
         const int j = col[k];
         const double v = val[k];
         if (j < 0 || j >= n || j <= last) e |= AJM_EB_CSR;
@@ -1144,15 +1144,15 @@ __global__ void ajm_validate_diag_kernel(int n, const int* __restrict__ rp, cons
 }
 
 // Q_ij == Q_ji for every stored entry (binary search of column i in row j).
-__global__ void ajm_symmetry_kernel(int n, const int* __restrict__ rp, const int* __restrict__ col,
+__global__ void ajm_symmetry_kernel(int n, const long long* __restrict__ rp, const int* __restrict__ col,
                                     const double* __restrict__ val, int* __restrict__ err) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+    for (long long k = rp[i]; k < rp[i + 1]; ++k) {
         const int j = col[k];
-        int lo = rp[j], hi = rp[j + 1] - 1, found = -1;
+        long long lo = rp[j], hi = rp[j + 1] - 1, found = -1;
         while (lo <= hi) {
-            const int mid = (lo + hi) >> 1;
+            const long long mid = (lo + hi) >> 1;
             const int cm = col[mid];
             if (cm == i) { found = mid; break; }
             if (cm < i) lo = mid + 1; else hi = mid - 1;
@@ -1165,13 +1165,6 @@ __global__ void ajm_finite_kernel(long long n, const double* __restrict__ v, int
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         if (!isfinite(v[i])) { atomicOr(err, AJM_EB_NONFINITE); return; }
-}
-
-__global__ void ajm_rowptr_narrow_kernel(long long n1, const long long* __restrict__ src,
-                                         int* __restrict__ dst) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n1;
-         i += (long long)gridDim.x * blockDim.x)
-        dst[i] = (int)src[i];
 }
 
 // ||b||^2: fixed grid of 256 CTAs, grid-strided sequential per thread, then fixed trees.
@@ -1203,7 +1196,7 @@ __global__ void ajm_sum_final_kernel(int m, const double* __restrict__ part, dou
 // (k >= row length, and tail slots) is val 0 / col = the slot's own internal row (or 0),
 // appended AFTER the row's entries so the sequential sum order is unchanged.
 __global__ void ajm_sell_fill_kernel(int nslots_padded, int n_sell, const int* __restrict__ perm,
-                                     int ident, const int* __restrict__ rp, const int* __restrict__ col,
+                                     int ident, const long long* __restrict__ rp, const int* __restrict__ col,
                                      const double* __restrict__ val, const long long* __restrict__ chunk_off,
                                      double* __restrict__ sval, int* __restrict__ scol) {
     const int slot = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1213,8 +1206,9 @@ __global__ void ajm_sell_fill_kernel(int nslots_padded, int n_sell, const int* _
     const int w = (int)((chunk_off[ch + 1] - base) >> 5);
     // slot -> caller's row (perm has n_sell entries; slots past them are chunk tail padding)
     const int row = slot < n_sell ? (ident ? slot : perm[slot]) : -1;
-    int k0 = 0, len = 0;
-    if (row >= 0) { k0 = rp[row]; len = rp[row + 1] - k0; }
+    long long k0 = 0;
+    int len = 0;
+    if (row >= 0) { k0 = rp[row]; len = (int)(rp[row + 1] - k0); }
     for (int k = 0; k < w; ++k) {
         const long long e = base + (long long)k * 32 + lane;
         if (k < len) { sval[e] = val[k0 + k]; scol[e] = col[k0 + k]; }
@@ -1282,7 +1276,7 @@ __device__ double ajm_spectral_norm(const double* B) {
 }
 
 template <int BS>
-__global__ void ajm_jblock_build_kernel(int n, const int* __restrict__ rp, const int* __restrict__ col,
+__global__ void ajm_jblock_build_kernel(int n, const long long* __restrict__ rp, const int* __restrict__ col,
                                         const double* __restrict__ val, double* __restrict__ Jout,
                                         double* __restrict__ Jinv, double* __restrict__ D, int* __restrict__ err) {
     const int blk = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1291,7 +1285,7 @@ __global__ void ajm_jblock_build_kernel(int n, const int* __restrict__ rp, const
     const int r0 = blk * BS;
     const int m = min(BS, n - r0);
     double A[BS * BS], B[BS * BS];
-    int cur[BS], end[BS];
+    long long cur[BS], end[BS];
     for (int k = 0; k < BS * BS; ++k) A[k] = 0.0;
     for (int r = 0; r < BS; ++r) {
         cur[r] = r < m ? rp[r0 + r] : 0;
