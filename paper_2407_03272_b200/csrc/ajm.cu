@@ -88,6 +88,11 @@ struct ajm_ctx {
     int direct = 0;
     int gring = 0;                     // kMode 3 gather ring
     int cluster = 0;                   // grid <= 16 CTAs launched as one cluster (DSMEM barrier)
+    int gmeta = 0;                     // per-CTA unit/chunk tables in global memory (huge layouts)
+    int* g_uc0 = nullptr;
+    int* g_coff = nullptr;
+    long long* g_ubase = nullptr;
+    long long* g_cbase = nullptr;
     unsigned long long* ts = nullptr;  // debug phase timestamps (AJM_TS=1)
     double* vecs = nullptr;            // X0 X1 X2 Qxp b D, one allocation
     int l2persist = 1;
@@ -238,7 +243,8 @@ void free_all(ajm_ctx* h) {
                     h->sval, h->scol, h->chunk_off, h->perm, h->seg_row, h->seg_k0, h->seg_k1,
                     h->seg_split, h->seg_part, h->split_row, h->split_seg0, h->split_cnt,
                     h->cta_split, h->owner_split, h->unit_c0, h->cta_seg, h->seg_list, h->cta_unit, h->partials, h->ctrl,
-                    h->hist, h->scratch, h->err, h->ts, h->perm_fwd, h->perm_inv, h->b_in, h->Jblk, h->Jinv, h->seg_order, h->seg_grp};
+                    h->hist, h->scratch, h->err, h->ts, h->perm_fwd, h->perm_inv, h->b_in, h->Jblk, h->Jinv, h->seg_order, h->seg_grp,
+                    h->g_uc0, h->g_coff, h->g_ubase, h->g_cbase};
     for (void* p : ptrs) dfree(p);
     if (h->h_ctrl) free(h->h_ctrl);
     if (h->ev0) cudaEventDestroy(h->ev0);
@@ -290,6 +296,10 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.vstage = h->vstage;
     p.ts = h->ts;
     p.bid_rev = getenv("AJM_BID_REV") ? atoi(getenv("AJM_BID_REV")) : 0;
+    p.g_uc0 = h->g_uc0;
+    p.g_coff = h->g_coff;
+    p.g_ubase = h->g_ubase;
+    p.g_cbase = h->g_cbase;
     p.Jinv = h->Jinv;
     p.jbs = h->jbs;
     p.direct_interleave = getenv("AJM_DIRECT_INTERLEAVE") ? atoi(getenv("AJM_DIRECT_INTERLEAVE")) : 0;
@@ -799,8 +809,18 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
                           : (size_t)(h->vstage ? kVariants[h->variant].vstages : kVariants[h->variant].stages) *
                             ((size_t)AJM_UNIT_EL * 12 + (h->vstage ? (size_t)5 * AJM_UNIT_ROWS * 8 : 0));
         size_t meta = 4096;  // initial allowance, grown until the plan fits
+        int smem_optin = 0;
+        CC(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
         for (int iter = 0;; ++iter) {
-            h->dyn_smem = ring + meta;
+            // tables too large for shared memory next to the ring: read them from global memory
+            if (!h->gmeta && (ring + meta + 2048 > (size_t)smem_optin || getenv("AJM_FORCE_GMETA")) && !h->direct &&
+                !h->gring && !h->vstage && !h->jbs) {
+                h->gmeta = 1;
+                h->fn = h->nseg == 0 ? ajm_solve_kernel<4, 96, 0, false, false, 0, true>
+                                     : ajm_solve_kernel<4, 96, 0, true, false, 0, true>;
+                CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            }
+            h->dyn_smem = ring + (h->gmeta ? 0 : meta);
             CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem));
             int occ = 0;
             CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->fn, block_threads(h),
@@ -815,8 +835,8 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
                 h->grid = (int)std::max<int64_t>(1, (nitems + AJM_WARPS - 1) / AJM_WARPS);
             plan(h->grid);
             const size_t need = (size_t)(h->meta_units + h->meta_chunks) * sizeof(int);
-            if (need <= meta) break;
-            if (iter > 4) return bail(fail(h, AJM_ERR_UNSUPPORTED, "layout metadata does not fit shared memory"));
+            if (h->gmeta || need <= meta) break;
+            if (iter > 6) return bail(fail(h, AJM_ERR_UNSUPPORTED, "layout metadata does not fit shared memory"));
             meta = need;
         }
         const int G = h->grid;
@@ -991,6 +1011,29 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(h2d(h->seg_order, seg_order_h.data(), sizeof(int) * seg_order_h.size()));
     CC(h2d(h->seg_grp, seg_grp_h.data(), sizeof(int) * seg_grp_h.size()));
     CC(h2d(h->cta_unit, cta_unit_h.data(), sizeof(int) * cta_unit_h.size()));
+    if (h->gmeta) {  // the per-CTA tables the kernel would otherwise stage in shared memory
+        std::vector<int> guc, gco;
+        std::vector<long long> gub((size_t)h->grid), gcb((size_t)h->grid);
+        for (int cc = 0; cc < h->grid; ++cc) {
+            const int u0 = cta_unit_h[(size_t)cc], u1 = cta_unit_h[(size_t)cc + 1];
+            const int cf = u1 > u0 ? unit_c0_h[(size_t)u0] : 0;
+            const int cl = u1 > u0 ? unit_c0_h[(size_t)u1] : 0;
+            const long long ef = u1 > u0 ? choff[(size_t)cf] : 0;
+            gub[(size_t)cc] = (long long)guc.size();
+            for (int i = 0; i <= u1 - u0; ++i) guc.push_back(unit_c0_h[(size_t)(u0 + i)] - cf);
+            gcb[(size_t)cc] = (long long)gco.size();
+            for (int i = 0; i <= cl - cf; ++i) gco.push_back((int)(choff[(size_t)(cf + i)] - ef));
+        }
+        CC(dalloc(&h->g_uc0, guc.size(), st));
+        CC(dalloc(&h->g_coff, gco.size(), st));
+        CC(dalloc(&h->g_ubase, gub.size(), st));
+        CC(dalloc(&h->g_cbase, gcb.size(), st));
+        CC(h2d(h->g_uc0, guc.data(), sizeof(int) * guc.size()));
+        CC(h2d(h->g_coff, gco.data(), sizeof(int) * gco.size()));
+        CC(h2d(h->g_ubase, gub.data(), sizeof(long long) * gub.size()));
+        CC(h2d(h->g_cbase, gcb.data(), sizeof(long long) * gcb.size()));
+        CC(cudaStreamSynchronize(st));  // the host vectors die here
+    }
     CC(cudaMemsetAsync(h->err, 0, sizeof(int), st));
 
     mark("copies", st);

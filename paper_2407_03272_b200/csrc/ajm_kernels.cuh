@@ -126,6 +126,10 @@ struct AjmPass {
     int vstage;                              // stage the rows' vector slices too (needs ident)
     unsigned long long* ts;                  // debug: per-pass phase timestamps of CTA 0 (or null)
     int direct_interleave;                   // direct mode: chunk j -> warp j%8 (else contiguous)
+    const int* __restrict__ g_uc0;           // (kGMeta) per-CTA unit -> first chunk tables, CTA-relative
+    const int* __restrict__ g_coff;          // (kGMeta) per-CTA chunk -> element offset tables
+    const long long* __restrict__ g_ubase;   // [grid] start of each CTA's unit table in g_uc0
+    const long long* __restrict__ g_cbase;   // [grid] start of each CTA's chunk table in g_coff
     int bid_rev;                             // experiment: CTA g takes work range G-1-g
     const double* __restrict__ Jinv;         // AJM_D_JBLOCK: rows of the block inverses, per chunk [bs][32]
     int jbs;                                 // AJM_D_JBLOCK block size (0: diagonal D)
@@ -654,7 +658,11 @@ __device__ __forceinline__ double ajm_chunk_dot_smem(const double* sv, const dou
 // per-pass barrier and the exchange of the CTA partials go through distributed shared memory
 // (remote mbarrier arrivals, ld.shared::cluster) instead of global memory.  Same reduction order
 // as the global path, so the results are bitwise those of the cooperative launch with the same grid.
-template <int kStages, int kMaxReg, int kMode, bool kSeg = true, bool kCluster = false, int kJB = 0>
+// kGMeta = true: the per-CTA unit/chunk tables are read from global memory (precomputed per CTA
+// on the host) instead of being staged in shared memory -- for layouts whose tables do not fit
+// next to the ring (hundreds of millions of rows).
+template <int kStages, int kMaxReg, int kMode, bool kSeg = true, bool kCluster = false, int kJB = 0,
+          bool kGMeta = false>
 __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     extern __shared__ __align__(128) unsigned char s_dyn[];
     __shared__ double s_red[AJM_WARPS][AJM_NPART];
@@ -700,13 +708,16 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     };
     // static per-CTA SELL metadata, loaded once: unit -> first chunk, chunk -> element offset
     // (relative to this CTA's first chunk / element), so the pass never chases global pointers
-    int* s_uc0 = reinterpret_cast<int*>(s_dyn + (direct ? (size_t)0 : (size_t)kStages * stage_bytes));
-    int* s_coff = s_uc0 + p.meta_units;
+    int* s_uc0 = kGMeta ? const_cast<int*>(p.g_uc0 + p.g_ubase[bid])
+                        : reinterpret_cast<int*>(s_dyn + (direct ? (size_t)0 : (size_t)kStages * stage_bytes));
+    int* s_coff = kGMeta ? const_cast<int*>(p.g_coff + p.g_cbase[bid]) : s_uc0 + p.meta_units;
     const int cfirst = nunits > 0 ? p.unit_c0[u0] : 0;
     const int nchk = nunits > 0 ? p.unit_c0[u1] - cfirst : 0;
     const long long efirst = nunits > 0 ? p.chunk_off[cfirst] : 0;
-    for (int i = tid; i <= nunits; i += blockDim.x) s_uc0[i] = p.unit_c0[u0 + i] - cfirst;
-    for (int i = tid; i <= nchk; i += blockDim.x) s_coff[i] = (int)(p.chunk_off[cfirst + i] - efirst);
+    if (!kGMeta) {
+        for (int i = tid; i <= nunits; i += blockDim.x) s_uc0[i] = p.unit_c0[u0 + i] - cfirst;
+        for (int i = tid; i <= nchk; i += blockDim.x) s_coff[i] = (int)(p.chunk_off[cfirst + i] - efirst);
+    }
     if (tid == 0) {
         s_st = c->s;
         s_stop = 0;

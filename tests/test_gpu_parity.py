@@ -254,3 +254,17 @@ def test_many_handles_pool_reuse(monkeypatch):
             if rep == 0:
                 o, _ = oracle_matching(Q, b, g, tol=0.0, maxit=100)
                 assert max_rel(g.x, o.x) <= PARITY_TOL, n
+
+
+def test_global_metadata_variant(monkeypatch):
+    """Layouts whose per-CTA unit/chunk tables do not fit shared memory read them from global
+    memory (a kernel instantiation for hundreds of millions of rows); forced here on oracle-sized
+    stencil and graph cases it must give bitwise the iterates of the shared-memory tables."""
+    for cfg, scale in ((2, 0.25), (4, 0.0125)):
+        p = synth.config_problem(cfg, scale)
+        a = gpu_solve(p.Q, p.b, tol=0.0, maxit=300, restart=True)
+        monkeypatch.setenv("AJM_FORCE_GMETA", "1")
+        g = gpu_solve(p.Q, p.b, tol=0.0, maxit=300, restart=True)
+        monkeypatch.delenv("AJM_FORCE_GMETA")
+        np.testing.assert_array_equal(a.x, g.x)
+        np.testing.assert_array_equal(a.res_hist, g.res_hist)
