@@ -121,7 +121,9 @@ typedef struct {
     int32_t mode;             /* 0 TMA ring, 1 ring + vector slices, 2 direct SELL loads       */
     int32_t l2_mode;          /* L2 policy: 2 all vectors persist, 3 only the x~ buffers persist */
     int32_t launches_per_solve; /* kernel launches of one ajm_solve (L2 priming + init + solver)   */
-    int32_t pad1;
+    int32_t col_bytes;        /* bytes streamed per SELL column index: 4 (int32), or 1 when the
+                                 column offsets col - row take <= 256 values and the layout stores
+                                 byte codes into an offset table (stencils)        */
 } ajm_info_t;
 
 /*

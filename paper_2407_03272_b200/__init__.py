@@ -71,7 +71,7 @@ class ajm_info_t(ctypes.Structure):
                 ("sigma", ctypes.c_int32), ("variant", ctypes.c_int32),
                 ("l2_window_bytes", ctypes.c_int64), ("l2_hit_ratio", ctypes.c_double),
                 ("mode", ctypes.c_int32), ("l2_mode", ctypes.c_int32),
-                ("launches_per_solve", ctypes.c_int32), ("pad1", ctypes.c_int32)]
+                ("launches_per_solve", ctypes.c_int32), ("col_bytes", ctypes.c_int32)]
 
 
 _lib = None

@@ -144,6 +144,9 @@ struct ajm_ctx {
     int jbs = 0;                // AJM_D_JBLOCK block size (0: diagonal metric)
     double* Jblk = nullptr;     // [s][bs][bs] blocks of eq-J-blkdiag
     double* Jinv = nullptr;     // rows of their inverses, per SELL chunk [bs][32]
+    uint8_t* scode = nullptr;   // byte-coded SELL columns (col = row + ctab[code]), replaces scol
+    int* ctab = nullptr;        // [AJM_CTAB] ascending column offsets of the codes
+    int col_bytes = 4;          // bytes per streamed column index: 4 (int32) or 1 (byte code)
     double nb = 0.0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double last_loop_ms = 0.0;
@@ -244,7 +247,7 @@ void free_all(ajm_ctx* h) {
                     h->seg_split, h->seg_part, h->split_row, h->split_seg0, h->split_cnt,
                     h->cta_split, h->owner_split, h->unit_c0, h->cta_seg, h->seg_list, h->cta_unit, h->partials, h->ctrl,
                     h->hist, h->scratch, h->err, h->ts, h->perm_fwd, h->perm_inv, h->b_in, h->Jblk, h->Jinv, h->seg_order, h->seg_grp,
-                    h->g_uc0, h->g_coff, h->g_ubase, h->g_cbase};
+                    h->g_uc0, h->g_coff, h->g_ubase, h->g_cbase, h->scode, h->ctab};
     for (void* p : ptrs) dfree(p);
     if (h->h_ctrl) free(h->h_ctrl);
     if (h->ev0) cudaEventDestroy(h->ev0);
@@ -302,6 +305,8 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.g_cbase = h->g_cbase;
     p.Jinv = h->Jinv;
     p.jbs = h->jbs;
+    p.scode = h->scode;
+    p.ctab = h->ctab;
     p.direct_interleave = getenv("AJM_DIRECT_INTERLEAVE") ? atoi(getenv("AJM_DIRECT_INTERLEAVE")) : 0;
     return p;
 }
@@ -1096,6 +1101,59 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
                                                                h->rp, h->col, h->val, h->chunk_off, h->sval, h->scol);
         CC(cudaGetLastError());
     }
+    // byte-coded columns: when the offsets col - row of the SELL entries take at most
+    // AJM_CTAB distinct values (stencils: 7 / 27), stream one byte per entry instead of an int32
+    // column (12 -> 9 bytes per stored entry) -- plain-ring variant-0 layouts only
+    if (h->nchunks > 0 && h->ident && h->variant == 0 && !h->cluster && !h->gmeta && !h->direct && !h->gring &&
+        !h->vstage && !h->jbs && (h->fn == kVariants[0].fn0 || h->fn == kVariants[0].fn) && !getenv("AJM_NO_COL8")) {
+        const int ns = (int)(h->nchunks * 32);
+        int* tmp = nullptr;
+        CC(dalloc(&tmp, AJM_CTAB_HASH + 2, st));
+        std::vector<int> htab(AJM_CTAB_HASH + 2, INT_MIN);
+        htab[AJM_CTAB_HASH] = htab[AJM_CTAB_HASH + 1] = 0;
+        CC(cudaMemcpyAsync(tmp, htab.data(), sizeof(int) * htab.size(), cudaMemcpyHostToDevice, st));
+        ajm_coloff_collect_kernel<<<(ns + 255) / 256, 256, 0, st>>>(ns, (int)h->n_sell, h->chunk_off, h->scol, tmp,
+                                                                     tmp + AJM_CTAB_HASH);
+        CC(cudaGetLastError());
+        CC(cudaMemcpyAsync(htab.data(), tmp, sizeof(int) * htab.size(), cudaMemcpyDeviceToHost, st));
+        CC(cudaStreamSynchronize(st));
+        // the 9-byte entries leave room for a 5th stage in the same shared-memory footprint: taken
+        // by the wide-row variant (config 5: 1150 -> 1127 us/pass), not by the narrow one (config
+        // 2: 43.5 -> 43.9); AJM_COL8_STAGES=4|5 overrides
+        const char* es = getenv("AJM_COL8_STAGES");
+        const bool s5 = es ? atoi(es) == 5 : h->fn == kVariants[0].fn;
+        SolveFn f8 = h->fn == kVariants[0].fn0
+                         ? (s5 ? ajm_solve_kernel<5, 96, 0, false, false, 0, false, true>
+                               : ajm_solve_kernel<4, 96, 0, false, false, 0, false, true>)
+                         : (s5 ? ajm_solve_kernel<5, 96, 0, true, false, 0, false, true>
+                               : ajm_solve_kernel<4, 96, 0, true, false, 0, false, true>);
+        int occ8 = 0;
+        if (htab[AJM_CTAB_HASH + 1] == 0 && htab[AJM_CTAB_HASH] <= AJM_CTAB) {
+            CC(cudaFuncSetAttribute((const void*)f8, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            CC(cudaFuncSetAttribute((const void*)f8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem));
+            CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ8, f8, block_threads(h), h->dyn_smem));
+        }
+        if (occ8 >= h->ctas_per_sm && occ8 > 0) {
+            std::vector<int> keys;
+            for (int i = 0; i < AJM_CTAB_HASH; ++i)
+                if (htab[(size_t)i] != INT_MIN) keys.push_back(htab[(size_t)i]);
+            std::sort(keys.begin(), keys.end());
+            const int m = (int)keys.size();
+            keys.resize(AJM_CTAB, keys.empty() ? 0 : keys.back());
+            CC(dalloc(&h->ctab, AJM_CTAB, st));
+            CC(cudaMemcpyAsync(h->ctab, keys.data(), sizeof(int) * AJM_CTAB, cudaMemcpyHostToDevice, st));
+            CC(dalloc(&h->scode, (size_t)h->sell_elems, st));
+            ajm_coloff_encode_kernel<<<(ns + 255) / 256, 256, 0, st>>>(ns, (int)h->n_sell, h->chunk_off, h->scol,
+                                                                        h->ctab, m, h->scode);
+            CC(cudaGetLastError());
+            CC(cudaFreeAsync(h->scol, st));
+            h->scol = nullptr;
+            h->fn = f8;
+            h->col_bytes = 1;
+        }
+        CC(cudaStreamSynchronize(st));  // keys / htab live until the copies have run
+        CC(cudaFreeAsync(tmp, st));
+    }
     // ||b||
     ajm_sumsq_partial_kernel<<<256, 256, 0, st>>>(n, h->b, h->scratch);
     ajm_sum_final_kernel<<<1, 32, 0, st>>>(256, h->scratch, h->scratch + 256);
@@ -1348,7 +1406,7 @@ ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info) {
     info->sell_elems = h->sell_elems;
     info->l2_mode = h->l2_mode;
     info->launches_per_solve = (int32_t)(1 + (h->prime_bytes ? 1 : 0) + std::max<int64_t>(h->last_launches, 1));
-    info->pad1 = 0;
+    info->col_bytes = h->col_bytes;
     return AJM_OK;
 }
 

@@ -42,6 +42,8 @@
 #define AJM_UNIT_ROWS (AJM_WARPS * 32)  // rows per staging unit (<= 8 chunks)
 #define AJM_LOG_CAP 64
 #define AJM_GWARPS 4     // gather warps per CTA in kMode 3
+#define AJM_CTAB 256     // byte-coded columns: at most this many distinct offsets col - row
+#define AJM_CTAB_HASH 2048  // create-time hash set of the offsets
 
 // Iteration state: identical copies in every CTA (shared memory) and in global memory.
 struct AjmState {
@@ -133,6 +135,8 @@ struct AjmPass {
     int bid_rev;                             // experiment: CTA g takes work range G-1-g
     const double* __restrict__ Jinv;         // AJM_D_JBLOCK: rows of the block inverses, per chunk [bs][32]
     int jbs;                                 // AJM_D_JBLOCK block size (0: diagonal D)
+    const uint8_t* __restrict__ scode;       // (kCol8) SELL column codes: col = row + ctab[code]
+    const int* __restrict__ ctab;            // (kCol8) [256] distinct offsets col - row, ascending
 };
 
 __device__ __forceinline__ unsigned long long ajm_gtime() {
@@ -551,6 +555,29 @@ __device__ __forceinline__ double ajm_chunk_dot(const double* sv, const int* sc,
     return s;
 }
 
+// Byte-coded columns (kCol8): element k of the lane's row has column row + tab[code[32 k]]; xb is
+// x~ already offset by the row, so the gathers and the ascending-column sum are those of
+// ajm_chunk_dot (same columns, same order: bitwise the same q).
+__device__ __forceinline__ double ajm_chunk_dot8(const double* sv, const uint8_t* sc, int w, const double* xb,
+                                                 const int* tab) {
+    double s = 0.0;
+    for (int k0 = 0; k0 < w; k0 += 8) {
+        double xg[8];
+        int cc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) cc[j] = (k0 + j < w) ? (int)sc[(k0 + j) * 32] : 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) cc[j] = tab[cc[j]];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (k0 + j < w) xg[j] = ajm_ld(xb + cc[j]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (k0 + j < w) s += sv[(k0 + j) * 32] * xg[j];  // ascending column order
+    }
+    return s;
+}
+
 // A SELL chunk read directly from global memory (no staging): used for sorted-window layouts,
 // whose variable chunk widths make the shared-memory units small.
 __device__ __forceinline__ void ajm_chunk_direct(const AjmPass& p, int ch, int w, long long base, int lane,
@@ -662,7 +689,7 @@ __device__ __forceinline__ double ajm_chunk_dot_smem(const double* sv, const dou
 // on the host) instead of being staged in shared memory -- for layouts whose tables do not fit
 // next to the ring (hundreds of millions of rows).
 template <int kStages, int kMaxReg, int kMode, bool kSeg = true, bool kCluster = false, int kJB = 0,
-          bool kGMeta = false>
+          bool kGMeta = false, bool kCol8 = false>
 __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     extern __shared__ __align__(128) unsigned char s_dyn[];
     __shared__ double s_red[AJM_WARPS][AJM_NPART];
@@ -680,6 +707,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     __shared__ __align__(8) uint64_t s_cexit;  // (kCluster) every CTA done with the others' smem
     __shared__ double s_part[2][AJM_NPART];    // (kCluster) this CTA's partials by pass parity
     __shared__ int s_to;
+    __shared__ int s_ctab[kCol8 ? AJM_CTAB : 1];  // (kCol8) column offsets of the byte codes
 
     AjmCtrl* c = p.ctrl;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -692,12 +720,15 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     constexpr bool vstage = (kMode == 1);  // the unit's rows are contiguous (internal numbering)
     constexpr bool vecs = vstage || gring; // row operands staged in shared memory
     constexpr bool direct = (kMode == 2);
-    // stage s: val[UNIT_EL] f64 | col[UNIT_EL] i32 | (vecs) b, D, x~, x^{t-1}, Qx^{t-1} [256] f64
-    //          | (gring) gathered x~[col] [UNIT_EL] f64
-    const size_t stage_bytes = (size_t)AJM_UNIT_EL * 12 + (vecs ? (size_t)5 * AJM_UNIT_ROWS * 8 : 0) +
+    // stage s: val[UNIT_EL] f64 | col[UNIT_EL] i32 (kCol8: code[UNIT_EL] u8)
+    //          | (vecs) b, D, x~, x^{t-1}, Qx^{t-1} [256] f64 | (gring) gathered x~[col] [UNIT_EL] f64
+    constexpr unsigned el_bytes = kCol8 ? 9u : 12u;
+    const size_t stage_bytes = (size_t)AJM_UNIT_EL * el_bytes + (vecs ? (size_t)5 * AJM_UNIT_ROWS * 8 : 0) +
                                (gring ? (size_t)AJM_UNIT_EL * 8 : 0);
+    static_assert(!kCol8 || (kMode == 0 && !kCluster && !kGMeta), "byte-coded columns: plain ring variant only");
     auto st_val = [&](int k) { return reinterpret_cast<double*>(s_dyn + (size_t)k * stage_bytes); };
     auto st_col = [&](int k) { return reinterpret_cast<int*>(s_dyn + (size_t)k * stage_bytes + (size_t)AJM_UNIT_EL * 8); };
+    auto st_code = [&](int k) { return s_dyn + (size_t)k * stage_bytes + (size_t)AJM_UNIT_EL * 8; };
     auto st_vec = [&](int k, int which) {
         return reinterpret_cast<double*>(s_dyn + (size_t)k * stage_bytes + (size_t)AJM_UNIT_EL * 12 +
                                          (size_t)which * AJM_UNIT_ROWS * 8);
@@ -718,6 +749,8 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         for (int i = tid; i <= nunits; i += blockDim.x) s_uc0[i] = p.unit_c0[u0 + i] - cfirst;
         for (int i = tid; i <= nchk; i += blockDim.x) s_coff[i] = (int)(p.chunk_off[cfirst + i] - efirst);
     }
+    if (kCol8)
+        for (int i = tid; i < AJM_CTAB; i += blockDim.x) s_ctab[i] = p.ctab[i];
     if (tid == 0) {
         s_st = c->s;
         s_stop = 0;
@@ -777,9 +810,12 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                         const int e0 = s_coff[s_uc0[uu]], e1 = s_coff[s_uc0[uu + 1]];
                         const unsigned ne = (unsigned)(e1 - e0);
                         const unsigned vbytes = vecs ? (unsigned)(s_uc0[uu + 1] - s_uc0[uu]) * 32u * 8u : 0u;
-                        ajm_mbar_expect_tx(&s_full[stage], ne * 12u + (vstage ? 5u : 2u) * vbytes);
+                        ajm_mbar_expect_tx(&s_full[stage], ne * el_bytes + (vstage ? 5u : 2u) * vbytes);
                         ajm_bulk_g2s(st_val(stage), p.sval + efirst + e0, ne * 8u, &s_full[stage], qpol);
-                        ajm_bulk_g2s(st_col(stage), p.scol + efirst + e0, ne * 4u, &s_full[stage], qpol);
+                        if (kCol8)
+                            ajm_bulk_g2s(st_code(stage), p.scode + efirst + e0, ne, &s_full[stage], qpol);
+                        else
+                            ajm_bulk_g2s(st_col(stage), p.scol + efirst + e0, ne * 4u, &s_full[stage], qpol);
                         if (vecs) {
                             const int r0 = (cfirst + s_uc0[uu]) * 32;
                             ajm_bulk_g2s(st_vec(stage, 0), p.b + r0, vbytes, &s_full[stage], vpol);
@@ -973,6 +1009,8 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                     }
                     const int off = (e0 - s_coff[s_uc0[uu]]) + lane;
                     const double q = gring ? ajm_chunk_dot_smem(st_val(stage) + off, st_xg(stage) + off, w)
+                                   : kCol8 ? ajm_chunk_dot8(st_val(stage) + off, st_code(stage) + off, w,
+                                                            xc + (row >= 0 ? row : 0), s_ctab)
                                            : ajm_chunk_dot<kCluster>(st_val(stage) + off, st_col(stage) + off, w, xc);
                     if (jblk)  // every lane takes part (shuffles); tail lanes store nothing
                         ajm_row_update_blk<kJB>(p.Qxp, xf, row, q, bi, jr, jbs, jv, xt, xpi, qxp, beta, restart_t,
@@ -1224,6 +1262,69 @@ __global__ void ajm_sell_fill_kernel(int nslots_padded, int n_sell, const int* _
         const long long e = base + (long long)k * 32 + lane;
         if (k < len) { sval[e] = val[k0 + k]; scol[e] = col[k0 + k]; }
         else { sval[e] = 0.0; scol[e] = slot < n_sell ? slot : 0; }  // padding: own (internal) row
+    }
+}
+
+// Byte-coded columns, create time.  Every SELL entry's offset col - base(slot)
+// (base = the slot's own row, 0 for chunk-tail slots, matching the padding columns of
+// ajm_sell_fill_kernel) goes into a hash set of AJM_CTAB_HASH int32 keys (INT_MIN = empty;
+// |offset| < 2^31 - 1, so INT_MIN never occurs).  cnt[0] counts the distinct keys, cnt[1] is set
+// once more than AJM_CTAB are seen or a probe sequence runs out: the layout then keeps int32
+// columns.  Any order of insertion gives the same set.
+__global__ void ajm_coloff_collect_kernel(int nslots_padded, int n_sell, const long long* __restrict__ chunk_off,
+                                          const int* __restrict__ scol, int* tab, int* cnt) {
+    const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+    if (slot >= nslots_padded) return;
+    const int ch = slot >> 5, lane = slot & 31;
+    const long long base_e = chunk_off[ch];
+    const int w = (int)((chunk_off[ch + 1] - base_e) >> 5);
+    const int base = slot < n_sell ? slot : 0;
+    int last = INT_MIN;
+    for (int k = 0; k < w; ++k) {
+        if (*(volatile int*)(cnt + 1)) return;
+        const int d = scol[base_e + (long long)k * 32 + lane] - base;
+        if (d == last) continue;
+        last = d;
+        unsigned hsh = ((unsigned)d * 2654435761u) >> 21;  // 11 bits: AJM_CTAB_HASH slots
+        bool ok = false;
+        for (int pr = 0; pr < 64 && !ok; ++pr, hsh = (hsh + 1) & (AJM_CTAB_HASH - 1)) {
+            int v = *(volatile int*)(tab + hsh);
+            if (v == INT_MIN) {
+                v = atomicCAS(tab + hsh, INT_MIN, d);
+                if (v == INT_MIN) {
+                    if (atomicAdd(cnt, 1) >= AJM_CTAB) atomicExch(cnt + 1, 1);
+                    ok = true;
+                }
+            }
+            if (v == d) ok = true;
+        }
+        if (!ok) atomicExch(cnt + 1, 1);
+    }
+}
+
+// code[e] = index of col - base(slot) in the ascending offset table ctab[0..m) (m <= AJM_CTAB)
+__global__ void ajm_coloff_encode_kernel(int nslots_padded, int n_sell, const long long* __restrict__ chunk_off,
+                                         const int* __restrict__ scol, const int* __restrict__ ctab, int m,
+                                         uint8_t* __restrict__ code) {
+    __shared__ int t[AJM_CTAB];
+    for (int i = threadIdx.x; i < AJM_CTAB; i += blockDim.x) t[i] = i < m ? ctab[i] : INT_MAX;
+    __syncthreads();
+    const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+    if (slot >= nslots_padded) return;
+    const int ch = slot >> 5, lane = slot & 31;
+    const long long base_e = chunk_off[ch];
+    const int w = (int)((chunk_off[ch + 1] - base_e) >> 5);
+    const int base = slot < n_sell ? slot : 0;
+    for (int k = 0; k < w; ++k) {
+        const long long e = base_e + (long long)k * 32 + lane;
+        const int d = scol[e] - base;
+        int lo = 0, hi = AJM_CTAB;  // first index with t[idx] >= d (present by construction)
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (t[mid] < d) lo = mid + 1;
+            else hi = mid;
+        }
+        code[e] = (uint8_t)lo;
     }
 }
 

@@ -27,6 +27,7 @@ def test_config2_full_1000_iterations(cfg2):
     iterations (restart on)."""
     p = cfg2
     g = gpu_solve(p.Q, p.b, tol=0.0, maxit=1000, restart=True)
+    assert g.info["col_bytes"] == 1  # byte-coded columns (7 offsets), as bench.py runs it
     o, nforced = oracle_matching(p.Q, p.b, g, tol=0.0, maxit=1000, restart=True)
     assert g.iterations == o.iterations == 1000
     assert max_rel(g.x, o.x) <= PARITY_TOL, (max_rel(g.x, o.x), nforced)
@@ -73,6 +74,7 @@ def test_config5_full_bounded_and_thm23():
     f(x^t) - f* <= 2 ||x0 - x*||_S^2 / (t+1)^2 with f* = -1/2 <b, x*> and S = J - Q."""
     p = synth.config_problem(5)
     g = gpu_solve(p.Q, p.b, tol=0.0, maxit=20, restart=True)
+    assert g.info["col_bytes"] == 1 and g.info["sigma"] == 1  # byte-coded columns (27 offsets)
     o, _ = oracle_matching(p.Q, p.b, g, tol=0.0, maxit=20, restart=True)
     assert max_rel(g.x, o.x) <= PARITY_TOL
     g = gpu_solve(p.Q, p.b, tol=0.0, maxit=300, restart=False)

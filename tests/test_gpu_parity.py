@@ -268,3 +268,46 @@ def test_global_metadata_variant(monkeypatch):
         monkeypatch.delenv("AJM_FORCE_GMETA")
         np.testing.assert_array_equal(a.x, g.x)
         np.testing.assert_array_equal(a.res_hist, g.res_hist)
+
+
+def _banded_offsets(nd, R=2048, regions=4, seed=0):
+    """SPD Laplacian (+1e-2 I) of 4 diagonal blocks of R rows; block r couples rows j and j+d for
+    the offsets d of its share of 1..nd (pairs (j, j+d) with floor(j/d) even), so every row has
+    <= 33 entries and the matrix has exactly 2 nd + 1 distinct offsets col - row."""
+    ds = np.array_split(np.arange(1, nd + 1), regions)
+    us, vs = [], []
+    for r, D in enumerate(ds):
+        j = np.arange(R)
+        for d in D:
+            m = ((j // d) % 2 == 0) & (j + d < R)
+            us.append(r * R + j[m])
+            vs.append(r * R + j[m] + d)
+    u, v = np.concatenate(us), np.concatenate(vs)
+    w = np.random.Generator(np.random.PCG64(seed)).uniform(0.1, 1.0, u.size)
+    return synth._laplacian_from_edges(R * regions, u, v, w, shift=1e-2)
+
+
+@pytest.mark.parametrize("case", ["cfg2", "ragged17", "band255", "band257"])
+def test_byte_coded_columns(case, monkeypatch):
+    """Layouts whose column offsets col - row take <= 256 values stream byte codes into an offset
+    table instead of int32 columns.  Same columns, same summation order: the
+    iterates are BITWISE those of the int32 layout (AJM_NO_COL8) and match the oracle; 257 distinct
+    offsets keep the int32 layout.  (cfg2 runs the variant without segment phases, the banded
+    cases (width 33) the one with them, as config 5 does at full size: test_gpu_fullsize.)"""
+    if case == "cfg2":
+        p = synth.config_problem(2, 0.25)
+    elif case == "ragged17":  # n = 4913: a ragged last chunk (tail slots), > 128 chunks (no cluster)
+        p = synth.make_problem("p3d17", synth.poisson3d(17), 4)
+    else:
+        p = synth.make_problem(case, _banded_offsets(127 if case == "band255" else 128), 5)
+    a = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True)
+    assert a.info["col_bytes"] == (4 if case == "band257" else 1), a.info
+    assert a.info["sigma"] == 1
+    monkeypatch.setenv("AJM_NO_COL8", "1")
+    b = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True)
+    monkeypatch.delenv("AJM_NO_COL8")
+    assert b.info["col_bytes"] == 4
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.res_hist, b.res_hist)
+    o, _ = oracle_matching(p.Q, p.b, a, tol=0.0, maxit=400, restart=True)
+    assert max_rel(a.x, o.x) <= PARITY_TOL
