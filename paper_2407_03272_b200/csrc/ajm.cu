@@ -64,6 +64,30 @@ const SolveVariant kVariants[] = {
 };
 const int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
+// variant-0 ring kernels by ring depth (the depth sets how much of the SM's unified L1/shared
+// memory is left to the L1, which holds the x~ gathers' lines in flight: DESIGN.md §4)
+SolveFn plain_fn(bool seg, int stages) {
+    switch (stages) {
+        case 2: return seg ? ajm_solve_kernel<2, 96, 0> : ajm_solve_kernel<2, 96, 0, false>;
+        case 3: return seg ? ajm_solve_kernel<3, 96, 0> : ajm_solve_kernel<3, 96, 0, false>;
+        default: return seg ? ajm_solve_kernel<4, 96, 0> : ajm_solve_kernel<4, 96, 0, false>;
+    }
+}
+SolveFn col8_fn(bool seg, int stages) {
+    switch (stages) {
+        case 2: return seg ? ajm_solve_kernel<2, 96, 0, true, false, 0, false, true>
+                           : ajm_solve_kernel<2, 96, 0, false, false, 0, false, true>;
+        case 3: return seg ? ajm_solve_kernel<3, 96, 0, true, false, 0, false, true>
+                           : ajm_solve_kernel<3, 96, 0, false, false, 0, false, true>;
+        case 5: return seg ? ajm_solve_kernel<5, 96, 0, true, false, 0, false, true>
+                           : ajm_solve_kernel<5, 96, 0, false, false, 0, false, true>;
+        case 6: return seg ? ajm_solve_kernel<6, 96, 0, true, false, 0, false, true>
+                           : ajm_solve_kernel<6, 96, 0, false, false, 0, false, true>;
+        default: return seg ? ajm_solve_kernel<4, 96, 0, true, false, 0, false, true>
+                            : ajm_solve_kernel<4, 96, 0, false, false, 0, false, true>;
+    }
+}
+
 }  // namespace
 
 struct ajm_ctx {
@@ -147,6 +171,11 @@ struct ajm_ctx {
     uint8_t* scode = nullptr;   // byte-coded SELL columns (col = row + ctab[code]), replaces scol
     int* ctab = nullptr;        // [AJM_CTAB] ascending column offsets of the codes
     int col_bytes = 4;          // bytes per streamed column index: 4 (int32) or 1 (byte code)
+    int ring_stages = 4;        // TMA ring depth of the chosen solver kernel
+    bool seg_fn = true;         // the chosen plain/col8 ring kernel has the segment phases
+    bool ring_fn = false;       // h->fn is a plain_fn/col8_fn kernel (ring depth selectable)
+    size_t meta_bytes = 0;      // shared-memory unit/chunk tables behind the ring
+    int carveout = 100;         // preferred shared-memory carve-out (%), set before every launch
     double nb = 0.0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double last_loop_ms = 0.0;
@@ -317,6 +346,11 @@ int block_threads(const ajm_ctx* h) { return h->direct ? AJM_BLOCK : (h->gring ?
 // cooperative launch of the persistent solver kernel, with the L2 access-policy window over the
 // iterate vectors (persisting hits, streaming misses)
 cudaError_t launch_solver(ajm_ctx* h, AjmPass& p, cudaStream_t st) {
+    // the attributes belong to the kernel, which other handles share: set this handle's own
+    cudaError_t e = cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributePreferredSharedMemoryCarveout, h->carveout);
+    if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(h->grid);
     cfg.blockDim = dim3(block_threads(h));
@@ -809,9 +843,26 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             h->fn = kVariants[h->variant].fnd;
             h->vstage = 0;
         }
+        // ring depth of the variant-0 ring kernels: a shallower ring leaves more of the SM's
+        // unified L1/shared memory to the L1; AJM_STAGES=2|3|4 overrides
+        int ring_stages = h->vstage ? kVariants[h->variant].vstages : kVariants[h->variant].stages;
+        if (h->variant == 0 && (h->fn == kVariants[0].fn || h->fn == kVariants[0].fn0)) {
+            h->seg_fn = h->fn == kVariants[0].fn;
+            h->ring_fn = true;
+            // 3 stages and the L1 they free win where the gathers are scattered (sorted-window graph
+            // layouts: config 3 135 -> 82, config 4 880 -> 535 us/pass) and on narrow natural-order
+            // rows (config 2 int32: 45.7 -> 44.7); natural-order wide rows (units of 2-3 chunks) keep
+            // 4 (config 5 int32: 1189 vs 1350 at 3)
+            int sv = (!h->relabel && avg_w >= 16.0) ? 4 : 3;
+            if (const char* ev = getenv("AJM_STAGES")) sv = std::min(4, std::max(2, atoi(ev)));
+            h->fn = plain_fn(h->seg_fn, sv);
+            ring_stages = sv;
+            CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        }
+        h->ring_stages = ring_stages;
         // ring: val/col of a unit (+ the rows' five vector slices for natural-order layouts)
-        const size_t ring = h->direct ? 0 : h->gring ? (size_t)kVariants[h->variant].gstages * ((size_t)AJM_UNIT_EL * 20 + (size_t)5 * AJM_UNIT_ROWS * 8)
-                          : (size_t)(h->vstage ? kVariants[h->variant].vstages : kVariants[h->variant].stages) *
+        size_t ring = h->direct ? 0 : h->gring ? (size_t)kVariants[h->variant].gstages * ((size_t)AJM_UNIT_EL * 20 + (size_t)5 * AJM_UNIT_ROWS * 8)
+                          : (size_t)ring_stages *
                             ((size_t)AJM_UNIT_EL * 12 + (h->vstage ? (size_t)5 * AJM_UNIT_ROWS * 8 : 0));
         size_t meta = 4096;  // initial allowance, grown until the plan fits
         int smem_optin = 0;
@@ -823,9 +874,13 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
                 h->gmeta = 1;
                 h->fn = h->nseg == 0 ? ajm_solve_kernel<4, 96, 0, false, false, 0, true>
                                      : ajm_solve_kernel<4, 96, 0, true, false, 0, true>;
+                h->ring_fn = false;
+                h->ring_stages = 4;
+                ring = (size_t)4 * AJM_UNIT_EL * 12;
                 CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
             }
             h->dyn_smem = ring + (h->gmeta ? 0 : meta);
+            h->meta_bytes = h->gmeta ? 0 : meta;
             CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem));
             int occ = 0;
             CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->fn, block_threads(h),
@@ -853,16 +908,17 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
                            : h->jbs == 4 ? ajm_solve_kernel<4, 96, 4, false, true, 4>
                            : h->jbs == 8 ? ajm_solve_kernel<4, 96, 4, false, true, 8>
                                          : ajm_solve_kernel<4, 96, 4, false, true>;
-            else if (h->fn == kVariants[0].fn0) cf = ajm_solve_kernel<4, 96, 0, false, true>;
-            else if (h->fn == kVariants[0].fn) cf = ajm_solve_kernel<4, 96, 0, true, true>;
+            else if (h->ring_fn) cf = h->seg_fn ? ajm_solve_kernel<4, 96, 0, true, true> : ajm_solve_kernel<4, 96, 0, false, true>;
+            // (the cluster kernels keep a 4-deep ring: per-pass latency, not L1, bounds them)
+            const size_t cdyn = h->ring_fn ? (size_t)4 * AJM_UNIT_EL * 12 + h->meta_bytes : h->dyn_smem;
             if (cf) {
-                cudaFuncSetAttribute((const void*)cf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem);
+                cudaFuncSetAttribute((const void*)cf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cdyn);
                 cudaFuncSetAttribute((const void*)cf, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
                 if (G > 8) cudaFuncSetAttribute((const void*)cf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
                 cudaLaunchConfig_t qc = {};
                 qc.gridDim = dim3(G);
                 qc.blockDim = dim3(block_threads(h));
-                qc.dynamicSmemBytes = h->dyn_smem;
+                qc.dynamicSmemBytes = cdyn;
                 cudaLaunchAttribute qa[1];
                 qa[0].id = cudaLaunchAttributeClusterDimension;
                 qa[0].val.clusterDim.x = (unsigned)G;
@@ -874,6 +930,9 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
                 if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)cf, &qc) == cudaSuccess && ncl >= 1) {
                     h->fn = cf;
                     h->cluster = 1;
+                    h->dyn_smem = cdyn;
+                    if (h->ring_fn) h->ring_stages = 4;
+                    h->ring_fn = false;
                 }
                 cudaGetLastError();
             }
@@ -1104,8 +1163,8 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     // byte-coded columns: when the offsets col - row of the SELL entries take at most
     // AJM_CTAB distinct values (stencils: 7 / 27), stream one byte per entry instead of an int32
     // column (12 -> 9 bytes per stored entry) -- plain-ring variant-0 layouts only
-    if (h->nchunks > 0 && h->ident && h->variant == 0 && !h->cluster && !h->gmeta && !h->direct && !h->gring &&
-        !h->vstage && !h->jbs && (h->fn == kVariants[0].fn0 || h->fn == kVariants[0].fn) && !getenv("AJM_NO_COL8")) {
+    if (h->nchunks > 0 && h->ident && h->ring_fn && !h->cluster && !h->gmeta && !h->direct && !h->gring &&
+        !h->vstage && !h->jbs && !getenv("AJM_NO_COL8")) {
         const int ns = (int)(h->nchunks * 32);
         int* tmp = nullptr;
         CC(dalloc(&tmp, AJM_CTAB_HASH + 2, st));
@@ -1117,21 +1176,19 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         CC(cudaGetLastError());
         CC(cudaMemcpyAsync(htab.data(), tmp, sizeof(int) * htab.size(), cudaMemcpyDeviceToHost, st));
         CC(cudaStreamSynchronize(st));
-        // the 9-byte entries leave room for a 5th stage in the same shared-memory footprint: taken
-        // by the wide-row variant (config 5: 1150 -> 1127 us/pass), not by the narrow one (config
-        // 2: 43.5 -> 43.9); AJM_COL8_STAGES=4|5 overrides
-        const char* es = getenv("AJM_COL8_STAGES");
-        const bool s5 = es ? atoi(es) == 5 : h->fn == kVariants[0].fn;
-        SolveFn f8 = h->fn == kVariants[0].fn0
-                         ? (s5 ? ajm_solve_kernel<5, 96, 0, false, false, 0, false, true>
-                               : ajm_solve_kernel<4, 96, 0, false, false, 0, false, true>)
-                         : (s5 ? ajm_solve_kernel<5, 96, 0, true, false, 0, false, true>
-                               : ajm_solve_kernel<4, 96, 0, true, false, 0, false, true>);
+        // ring depth of the byte-coded kernels (18 KB stages): stencils' gathers hit L1 anyway, so
+        // the depth goes to the ring -- 4 for narrow rows (config 2: 43.7 -> 43.0 us/pass vs 3), 5
+        // for wide ones, whose units hold only 2-3 chunks (config 5: 1414 / 1139 / 1126 us/pass
+        // at 3 / 4 / 5); AJM_COL8_STAGES=2..6 overrides
+        int st8 = h->seg_fn ? 5 : 4;
+        if (const char* es = getenv("AJM_COL8_STAGES")) st8 = std::min(6, std::max(2, atoi(es)));
+        SolveFn f8 = col8_fn(h->seg_fn, st8);
+        const size_t dyn8 = (size_t)st8 * AJM_UNIT_EL * 9 + h->meta_bytes;
         int occ8 = 0;
         if (htab[AJM_CTAB_HASH + 1] == 0 && htab[AJM_CTAB_HASH] <= AJM_CTAB) {
             CC(cudaFuncSetAttribute((const void*)f8, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-            CC(cudaFuncSetAttribute((const void*)f8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem));
-            CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ8, f8, block_threads(h), h->dyn_smem));
+            CC(cudaFuncSetAttribute((const void*)f8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn8));
+            CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ8, f8, block_threads(h), dyn8));
         }
         if (occ8 >= h->ctas_per_sm && occ8 > 0) {
             std::vector<int> keys;
@@ -1149,10 +1206,33 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             CC(cudaFreeAsync(h->scol, st));
             h->scol = nullptr;
             h->fn = f8;
+            h->dyn_smem = dyn8;
+            h->ring_stages = st8;
             h->col_bytes = 1;
         }
         CC(cudaStreamSynchronize(st));  // keys / htab live until the copies have run
         CC(cudaFreeAsync(tmp, st));
+    }
+    // shared-memory carve-out: the smallest that keeps ctas_per_sm CTAs resident, so the rest of
+    // the SM's 256 KB stays L1 for the gathers; AJM_CARVEOUT=<pct> overrides
+    {
+        cudaFuncAttributes fa = {};
+        CC(cudaFuncGetAttributes(&fa, (const void*)h->fn));
+        int smem_sm = 0;
+        CC(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device));
+        const double need = (double)h->ctas_per_sm * ((double)h->dyn_smem + (double)fa.sharedSizeBytes + 1024.0);
+        int pct = (int)std::ceil(100.0 * need / std::max(1, smem_sm)) + 1;
+        if (const char* ev = getenv("AJM_CARVEOUT")) pct = atoi(ev);
+        pct = std::min(100, std::max(0, pct));
+        CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem));
+        CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        int occ = 0;
+        CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->fn, block_threads(h), h->dyn_smem));
+        if (occ < h->ctas_per_sm && !h->cluster) {
+            pct = 100;
+            CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        }
+        h->carveout = pct;
     }
     // ||b||
     ajm_sumsq_partial_kernel<<<256, 256, 0, st>>>(n, h->b, h->scratch);
