@@ -1213,6 +1213,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         CC(cudaStreamSynchronize(st));  // keys / htab live until the copies have run
         CC(cudaFreeAsync(tmp, st));
     }
+    mark("col8", st);
     // shared-memory carve-out: the smallest that keeps ctas_per_sm CTAs resident, so the rest of
     // the SM's 256 KB stays L1 for the gathers; AJM_CARVEOUT=<pct> overrides
     {

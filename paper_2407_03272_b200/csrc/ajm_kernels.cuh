@@ -1274,21 +1274,21 @@ __global__ void ajm_sell_fill_kernel(int nslots_padded, int n_sell, const int* _
 __global__ void ajm_coloff_collect_kernel(int nslots_padded, int n_sell, const long long* __restrict__ chunk_off,
                                           const int* __restrict__ scol, int* tab, int* cnt) {
     const int slot = blockIdx.x * blockDim.x + threadIdx.x;
-    if (slot >= nslots_padded) return;
+    if (slot >= nslots_padded) return;  // whole warps (nslots_padded is a multiple of 32)
     const int ch = slot >> 5, lane = slot & 31;
     const long long base_e = chunk_off[ch];
     const int w = (int)((chunk_off[ch + 1] - base_e) >> 5);
     const int base = slot < n_sell ? slot : 0;
-    int last = INT_MIN;
     for (int k = 0; k < w; ++k) {
-        if (*(volatile int*)(cnt + 1)) return;
+        if (__ldcg(cnt + 1)) return;  // warp-uniform
         const int d = scol[base_e + (long long)k * 32 + lane] - base;
-        if (d == last) continue;
-        last = d;
+        // one insert per distinct offset of the warp (stencil chunks: usually one)
+        const unsigned same = __match_any_sync(0xffffffffu, d);
+        if (lane != __ffs(same) - 1) continue;
         unsigned hsh = ((unsigned)d * 2654435761u) >> 21;  // 11 bits: AJM_CTAB_HASH slots
         bool ok = false;
         for (int pr = 0; pr < 64 && !ok; ++pr, hsh = (hsh + 1) & (AJM_CTAB_HASH - 1)) {
-            int v = *(volatile int*)(tab + hsh);
+            int v = __ldcg(tab + hsh);  // a key never changes once set; a stale EMPTY goes to the CAS
             if (v == INT_MIN) {
                 v = atomicCAS(tab + hsh, INT_MIN, d);
                 if (v == INT_MIN) {
