@@ -918,6 +918,8 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         //     the rows are finished by their fixed owner CTA in (3), so the arithmetic does not
         //     depend on which warp ran a segment.  The other parity's queue was last used in pass
         //     t-1 (finished before the last grid barrier) and is reset here for pass t+1.
+        //     Static mode: warp w runs the CTA's segments w, w+8, ... (split rows first, then
+        //     longest first).
         if (p.dynseg && bid == 0 && tid == 0) c->seg_q[(t + 1) & 1] = 0u;
         int gk = 0, gend = 0;  // dynamic mode: current claim group [gk, gend) of seg_order
         for (int sk = sg0 + warp;; sk += AJM_WARPS) {
