@@ -311,3 +311,23 @@ def test_byte_coded_columns(case, monkeypatch):
     np.testing.assert_array_equal(a.res_hist, b.res_hist)
     o, _ = oracle_matching(p.Q, p.b, a, tol=0.0, maxit=400, restart=True)
     assert max_rel(a.x, o.x) <= PARITY_TOL
+
+
+def test_interleaved_handles_kernel_attributes():
+    """Handles whose solver kernels differ in ring depth, shared-memory size and carve-out (graph:
+    3-deep int32 ring; stencil: byte-coded 4-deep ring; tiny: single cluster) stay alive together
+    and solve alternately: each launch sets its own kernel attributes, so every solve is bitwise
+    the one it gives alone."""
+    probs = [synth.config_problem(3, 0.02), synth.config_problem(2, 0.25), synth.config_problem(1)]
+    alone = [gpu_solve(p.Q, p.b, tol=0.0, maxit=150, restart=True) for p in probs]
+    import paper_2407_03272_b200 as ajm
+    solvers = [ajm.Solver.from_csr(p.Q, p.b) for p in probs]
+    try:
+        for rep in range(2):
+            for s, a in zip(solvers, alone):
+                r = s.solve(tol=0.0, maxit=150, restart=True)
+                np.testing.assert_array_equal(r.x.cpu().numpy(), a.x)
+        assert len({(s.info()["col_bytes"], s.info()["grid"]) for s in solvers}) == 3
+    finally:
+        for s in solvers:
+            s.close()
