@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
+#include <omp.h>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -437,25 +439,23 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     if (dmode == AJM_D_USER && !d) return fail(nullptr, AJM_ERR_INVALID_ARG, "AJM_D_USER needs d");
     cudaStream_t st = (cudaStream_t)cuda_stream;
 
-    // host scan of row_ptr (needed anyway for the layout); read in place when it is host memory
-    const bool rp_dev = is_device_ptr(row_ptr);
-    std::vector<int64_t> hrp_copy;
-    const int64_t* hrp = row_ptr;
-    if (rp_dev) {
-        hrp_copy.resize((size_t)n + 1);
-        cudaError_t e = cudaMemcpyAsync(hrp_copy.data(), row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        if (e != cudaSuccess) return fail(nullptr, AJM_ERR_CUDA, "row_ptr copy: %s", cudaGetErrorString(e));
-        hrp = hrp_copy.data();
+    // the O(1) consistency checks before any copy: with row_ptr[0] = 0 and row_ptr[n] = nnz the
+    // arrays the copies below read have the sizes the caller declared
+    {
+        int64_t ends[2] = {0, 0};
+        if (is_device_ptr(row_ptr)) {
+            cudaError_t e = cudaMemcpyAsync(&ends[0], row_ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(&ends[1], row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) return fail(nullptr, AJM_ERR_CUDA, "row_ptr copy: %s", cudaGetErrorString(e));
+        } else {
+            ends[0] = row_ptr[0];
+            ends[1] = row_ptr[n];
+        }
+        if (ends[0] != 0) return fail(nullptr, AJM_ERR_CSR_INVALID, "row_ptr[0] = %lld != 0", (long long)ends[0]);
+        if (ends[1] != nnz)
+            return fail(nullptr, AJM_ERR_CSR_INVALID, "row_ptr[n] = %lld != nnz = %lld", (long long)ends[1], (long long)nnz);
     }
-    if (hrp[0] != 0) return fail(nullptr, AJM_ERR_CSR_INVALID, "row_ptr[0] = %lld != 0", (long long)hrp[0]);
-    for (int64_t i = 0; i < n; ++i)
-        if (hrp[i + 1] < hrp[i])
-            return fail(nullptr, AJM_ERR_CSR_INVALID, "row_ptr decreases at row %lld", (long long)i);
-    if (hrp[n] != nnz)
-        return fail(nullptr, AJM_ERR_CSR_INVALID, "row_ptr[n] = %lld != nnz = %lld", (long long)hrp[n], (long long)nnz);
-
-    mark("rowptr", st);
     ajm_ctx* h = new ajm_ctx();
     h->n = n;
     h->nnz = nnz;
@@ -463,6 +463,8 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     h->dmode = dmode;
     h->jbs = jbs;
     auto bail = [&](ajm_status_t s) {
+        cudaStreamSynchronize(st);  // no copy into the handle's memory still in flight
+        cudaGetLastError();
         g_create_error = h->err_msg;
         free_all(h);
         delete h;
@@ -510,6 +512,30 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(cudaMemcpyAsync(h->b_in, b, sizeof(double) * n, kind_to_device(b), st));
     mark("h2d-issue", st);
 
+    // host scan of row_ptr (needed anyway for the layout) while the copies above run; read in
+    // place when it is host memory.  (The copies move exactly the nnz / n entries the caller
+    // declared, so a row_ptr rejected here never made them read out of bounds.)
+    const bool rp_dev = is_device_ptr(row_ptr);
+    std::vector<int64_t> hrp_copy;
+    const int64_t* hrp = row_ptr;
+    if (rp_dev) {
+        hrp_copy.resize((size_t)n + 1);
+        CC(cudaMemcpyAsync(hrp_copy.data(), row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+        CC(cudaStreamSynchronize(st));
+        hrp = hrp_copy.data();
+    }
+    {
+        int64_t bad = n;  // first row whose offsets decrease (n: none)
+#pragma omp parallel for reduction(min : bad) schedule(static)
+        for (int64_t i = 0; i < n; ++i)
+            if (hrp[i + 1] < hrp[i] && i < bad) bad = i;
+        if (bad < n) return bail(fail(h, AJM_ERR_CSR_INVALID, "row_ptr decreases at row %lld", (long long)bad));
+    }
+    mark("rowptr", st);
+
+    // rows validated by a warp each (ajm_validate_long_kernel), caller's numbering
+    constexpr int64_t kValidateLong = 2048;
+    std::vector<int> vlong_h;
     // ---- row-length-binned layout (host, O(n log sigma)) ----
     auto rlen = [&](int64_t r) { return hrp[(size_t)r + 1] - hrp[(size_t)r]; };
     std::vector<int> perm_h, seg_row_h, seg_k0_h, seg_k1_h, seg_split_h, split_row_h, split_seg0_h;
@@ -570,11 +596,31 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             h->dynseg = (double)long_nnz >= 0.9 * (double)std::max<int64_t>(nnz, 1) ? 1 : 0;
             if (const char* ev = getenv("AJM_DYNSEG")) h->dynseg = atoi(ev) ? 1 : 0;
         }
-        for (int64_t i = 0; i < n; ++i) {
-            const int64_t len = rlen(i);
-            if (len <= AJM_SELL_MAX) short_rows.push_back((int)i);
-            else if (len <= seg_len) whole_rows.push_back((int)i);
-            else split_rows.push_back((int)i);
+        {
+            // per-thread bins over contiguous row ranges, concatenated in thread order (so every
+            // list stays in ascending row order, as a serial pass would give)
+            std::vector<std::vector<int>> tb[4];
+            int nt = 1;
+#pragma omp parallel
+            {
+#pragma omp single
+                {
+                    nt = omp_get_num_threads();
+                    for (auto& v : tb) v.resize((size_t)nt);
+                }
+                const int tid = omp_get_thread_num();
+                const int64_t lo = n * tid / nt, hi = n * (tid + 1) / nt;
+                for (int64_t i = lo; i < hi; ++i) {
+                    const int64_t len = rlen(i);
+                    if (len <= AJM_SELL_MAX) tb[0][(size_t)tid].push_back((int)i);
+                    else if (len <= seg_len) tb[1][(size_t)tid].push_back((int)i);
+                    else tb[2][(size_t)tid].push_back((int)i);
+                    if (len > kValidateLong) tb[3][(size_t)tid].push_back((int)i);
+                }
+            }
+            std::vector<int>* dst[4] = {&short_rows, &whole_rows, &split_rows, &vlong_h};
+            for (int q = 0; q < 4; ++q)
+                for (auto& v : tb[q]) dst[q]->insert(dst[q]->end(), v.begin(), v.end());
         }
         h->long_rows = (int64_t)split_rows.size();
         // the SELL path indexes with 64-bit offsets; warp segments keep int32 CSR offsets
@@ -605,10 +651,9 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             // (a stable counting sort: row lengths are <= AJM_SELL_MAX here)
             h->sigma = 4096;
             std::vector<size_t> wlo;  // window boundaries in `order` (ascending row index)
-            for (size_t lo = 0; lo < order.size();) {
-                wlo.push_back(lo);
-                const int wbase = order[lo] / h->sigma;
-                while (lo < order.size() && order[lo] / h->sigma == wbase) ++lo;
+            for (int64_t wb = 0; wb * h->sigma < n; ++wb) {
+                const size_t lo = (size_t)(std::lower_bound(order.begin(), order.end(), (int)(wb * h->sigma)) - order.begin());
+                if (lo < order.size() && (wlo.empty() || lo > wlo.back())) wlo.push_back(lo);
             }
             wlo.push_back(order.size());
             const int64_t nwin = (int64_t)wlo.size() - 1;
@@ -747,6 +792,22 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         for (int64_t c2 = 0; c2 < h->nchunks; ++c2) cost.push_back(chcost[(size_t)c2]);
         double total = 0.0;
         for (double x : cost) total += x;
+        mark("P-cost", (cudaStream_t)-1);
+        // LPT order of the segments (largest cost first, index order among equals): independent
+        // of the grid size, so computed once for every plan() call below
+        std::vector<int64_t> lpt_order;
+        if (!h->dynseg) {
+            // the cost is increasing in the segment length: a counting sort by length
+            int64_t seg_len_max = 0;
+            for (int64_t k = 0; k < h->nseg; ++k) seg_len_max = std::max<int64_t>(seg_len_max, seg_k1_h[(size_t)k] - seg_k0_h[(size_t)k]);
+            lpt_order.resize((size_t)h->nseg);
+            std::vector<int64_t> cnt((size_t)seg_len_max + 2, 0);
+            for (int64_t k = 0; k < h->nseg; ++k) ++cnt[(size_t)(seg_len_max - (seg_k1_h[(size_t)k] - seg_k0_h[(size_t)k]) + 1)];
+            for (size_t q = 1; q < cnt.size(); ++q) cnt[q] += cnt[q - 1];
+            for (int64_t k = 0; k < h->nseg; ++k)
+                lpt_order[(size_t)cnt[(size_t)(seg_len_max - (seg_k1_h[(size_t)k] - seg_k0_h[(size_t)k]))]++] = k;
+        }
+        mark("P-lptsort", (cudaStream_t)-1);
         auto plan = [&](int G) {
             // (a) segments: largest first onto the least-loaded CTA (LPT), so the latency-bound
             //     long rows spread over every SM; (b) SELL chunks: contiguous ranges topping every
@@ -755,39 +816,34 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             std::vector<double> segload((size_t)G, 0.0);
             std::vector<std::vector<int>> segs((size_t)G);
             if (!h->dynseg) {
-                std::vector<int64_t> order((size_t)h->nseg);
-                for (int64_t k = 0; k < h->nseg; ++k) order[(size_t)k] = k;
-                std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return cost[(size_t)x] > cost[(size_t)y]; });
-                std::vector<std::pair<double, int>> heap;
-                for (int cc = 0; cc < G; ++cc) heap.push_back({0.0, cc});
-                auto cmp = [](const std::pair<double, int>& x, const std::pair<double, int>& y) {
-                    return x.first > y.first || (x.first == y.first && x.second > y.second);
-                };
-                std::make_heap(heap.begin(), heap.end(), cmp);
-                for (int64_t k : order) {
-                    std::pop_heap(heap.begin(), heap.end(), cmp);
-                    auto& top = heap.back();
-                    top.first += cost[(size_t)k];
-                    segload[(size_t)top.second] += cost[(size_t)k];
-                    segs[(size_t)top.second].push_back((int)k);
-                    std::push_heap(heap.begin(), heap.end(), cmp);
+                // least-loaded CTA first, lower index among equal loads; the costs are integers,
+                // so (load << 10 | cta) orders exactly like (load, cta) in one 64-bit key
+                std::vector<uint64_t> heap;
+                for (int cc = 0; cc < G; ++cc) heap.push_back((uint64_t)cc);
+                std::make_heap(heap.begin(), heap.end(), std::greater<uint64_t>());
+                for (int64_t k : lpt_order) {
+                    std::pop_heap(heap.begin(), heap.end(), std::greater<uint64_t>());
+                    const int cc = (int)(heap.back() & 1023u);
+                    segload[(size_t)cc] += cost[(size_t)k];
+                    heap.back() = ((uint64_t)segload[(size_t)cc] << 10) | (uint64_t)cc;
+                    segs[(size_t)cc].push_back((int)k);
+                    std::push_heap(heap.begin(), heap.end(), std::greater<uint64_t>());
                 }
             }
+            mark("p-lpt", (cudaStream_t)-1);
             seg_list_h.clear();
             cta_seg_h.assign((size_t)G + 1, 0);
             for (int cc = 0; cc < G; ++cc) {
                 // split-row segments first (their owners wait for them), then longest first
-                // (round robin over the warps; config 4: 500.6 -> 496.1 us/pass vs segment order)
-                std::sort(segs[(size_t)cc].begin(), segs[(size_t)cc].end(), [&](int x, int y) {
-                    const bool sx = seg_split_h[(size_t)x] >= 0, sy = seg_split_h[(size_t)y] >= 0;
-                    if (sx != sy) return sx;
-                    const int lx = seg_k1_h[(size_t)x] - seg_k0_h[(size_t)x], ly = seg_k1_h[(size_t)y] - seg_k0_h[(size_t)y];
-                    return lx != ly ? lx > ly : x < y;
-                });
+                // (round robin over the warps; config 4: 500.6 -> 496.1 us/pass vs segment order);
+                // LPT handed them out longest first already, so a stable partition suffices
+                std::stable_partition(segs[(size_t)cc].begin(), segs[(size_t)cc].end(),
+                                      [&](int x) { return seg_split_h[(size_t)x] >= 0; });
                 cta_seg_h[(size_t)cc] = (int)seg_list_h.size();
                 for (int k : segs[(size_t)cc]) seg_list_h.push_back(k);
             }
             cta_seg_h[(size_t)G] = (int)seg_list_h.size();
+            mark("p-segsort", (cudaStream_t)-1);
             std::vector<int64_t> cstart((size_t)G + 1, h->nchunks);
             int64_t i = 0;
             double pref = 0.0, cumseg = 0.0;
@@ -876,6 +932,8 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         size_t meta = 4096;  // initial allowance, grown until the plan fits
         int smem_optin = 0;
         CC(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+        mark("P-pre", (cudaStream_t)-1);
+        int planned_grid = -1;
         for (int iter = 0;; ++iter) {
             // tables too large for shared memory next to the ring: read them from global memory
             if (!h->gmeta && (ring + meta + 2048 > (size_t)smem_optin || getenv("AJM_FORCE_GMETA")) && !h->direct &&
@@ -902,12 +960,16 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             // single cluster whose barrier lives in distributed shared memory
             if (nitems <= 16 * AJM_WARPS && h->variant == 0 && !getenv("AJM_NO_CLUSTER"))
                 h->grid = (int)std::max<int64_t>(1, (nitems + AJM_WARPS - 1) / AJM_WARPS);
-            plan(h->grid);
+            if (h->grid != planned_grid) {  // plan() depends on the grid size only
+                plan(h->grid);
+                planned_grid = h->grid;
+            }
             const size_t need = (size_t)(h->meta_units + h->meta_chunks) * sizeof(int);
             if (h->gmeta || need <= meta) break;
             if (iter > 6) return bail(fail(h, AJM_ERR_UNSUPPORTED, "layout metadata does not fit shared memory"));
             meta = need;
         }
+        mark("P-loop", (cudaStream_t)-1);
         const int G = h->grid;
         // small problems: the grid as ONE thread-block cluster, barrier and partial exchange in
         // distributed shared memory (variant 0 kernels only; AJM_NO_CLUSTER disables)
@@ -946,6 +1008,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
                 cudaGetLastError();
             }
         }
+        mark("P-cluster", (cudaStream_t)-1);
         // owner of a split row = the CTA that runs its last segment
         std::vector<int> seg_cta((size_t)h->nseg, 0);
         for (int cc = 0; cc < G; ++cc)
@@ -1113,8 +1176,21 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     // ---- validation + D (device) ----
     const int nblk = (int)((n + 255) / 256);
     ajm_validate_diag_kernel<<<nblk, 256, 0, st>>>((int)n, h->rp, h->col, h->val, dmode == AJM_D_JBLOCK ? 0 : dmode, dtmp,
-                                                   h->relabel ? h->X[2] : h->D, h->err);
+                                                   h->relabel ? h->X[2] : h->D, h->err,
+                                                   vlong_h.empty() ? LLONG_MAX : (long long)kValidateLong);
     CC(cudaGetLastError());
+    if (!vlong_h.empty()) {
+        int* vl = nullptr;
+        CC(dalloc(&vl, vlong_h.size(), st));
+        CC(cudaMemcpyAsync(vl, vlong_h.data(), sizeof(int) * vlong_h.size(), cudaMemcpyHostToDevice, st));
+        const int nl = (int)vlong_h.size();
+        ajm_validate_long_kernel<<<(nl + 7) / 8, 256, 0, st>>>((int)n, vl, nl, h->rp, h->col, h->val,
+                                                               dmode == AJM_D_JBLOCK ? 0 : dmode, dtmp,
+                                                               h->relabel ? h->X[2] : h->D, h->err);
+        CC(cudaGetLastError());
+        CC(cudaStreamSynchronize(st));  // vlong_h lives until the copy has run
+        CC(cudaFreeAsync(vl, st));
+    }
     if (h->relabel) {
         ajm_gather_kernel<<<1024, 256, 0, st>>>(n, h->perm_fwd, h->X[2], h->D);
         CC(cudaGetLastError());
@@ -1157,11 +1233,13 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         if (herr & AJM_EB_JBLOCK)
             return bail(fail(h, AJM_ERR_ZERO_DIAG, "a block J^{ii} of eq-J-blkdiag is not positive definite"));
     }
+    mark("validate", st);
     // columns in internal numbering (after validation, which needs the caller's order)
     if (h->relabel && nnz > 0) {
         ajm_remap_kernel<<<2048, 256, 0, st>>>(nnz, h->perm_inv, h->col);
         CC(cudaGetLastError());
     }
+    mark("remap", st);
     // SELL copy of the short rows (slot -> caller's row through perm_fwd when relabelled)
     if (h->nchunks > 0) {
         const int ns = (int)(h->nchunks * 32);
@@ -1169,6 +1247,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
                                                                h->rp, h->col, h->val, h->chunk_off, h->sval, h->scol);
         CC(cudaGetLastError());
     }
+    mark("fill", st);
     // byte-coded columns: when the offsets col - row of the SELL entries take at most
     // AJM_CTAB distinct values (stencils: 7 / 27), stream one byte per entry instead of an int32
     // column (12 -> 9 bytes per stored entry) -- plain-ring variant-0 layouts only

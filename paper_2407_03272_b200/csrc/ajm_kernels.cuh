@@ -1165,9 +1165,10 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
 __global__ void ajm_validate_diag_kernel(int n, const long long* __restrict__ rp, const int* __restrict__ col,
                                          const double* __restrict__ val, int dmode,
                                          const double* __restrict__ duser, double* __restrict__ D,
-                                         int* __restrict__ err) {
+                                         int* __restrict__ err, long long skip_len) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    if (rp[i + 1] - rp[i] > skip_len) return;  // a long row: ajm_validate_long_kernel
     int e = 0;
     double qkk = 0.0, off = 0.0;
     int last = -1;
@@ -1180,6 +1181,59 @@ __global__ void ajm_validate_diag_kernel(int n, const long long* __restrict__ rp
         if (j == i) qkk = v;
         else off += fabs(v);
     }
+    if (qkk < 0.0) e |= AJM_EB_NEGDIAG;
+    double d;
+    if (dmode == 0) d = qkk + off;
+    else if (dmode == 2) d = qkk;
+    else {
+        d = duser[i];
+        if (!isfinite(d)) e |= AJM_EB_NONFINITE;
+        if (!(d > 0.0)) e |= AJM_EB_ZERODIAG;
+    }
+    if (d == 0.0) e |= AJM_EB_ZERODIAG;
+    D[i] = d;
+    if (e) atomicOr(err, e);
+}
+
+// The same for the long rows (> skip_len entries), one warp per row: the checks run on 32 entries at
+// a time, and lane 0 still adds |Q_kj| in ascending column order (the values arrive by shuffles
+// in lane order), so D is bitwise the one-thread result -- without one thread streaming a whole
+// 1e5-entry hub row alone.
+__global__ void ajm_validate_long_kernel(int n, const int* __restrict__ rows, int nrows,
+                                         const long long* __restrict__ rp, const int* __restrict__ col,
+                                         const double* __restrict__ val, int dmode,
+                                         const double* __restrict__ duser, double* __restrict__ D,
+                                         int* __restrict__ err) {
+    const int wid = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (wid >= nrows) return;  // whole warps
+    const int i = rows[wid];
+    const long long k0 = rp[i], k1 = rp[i + 1];
+    int e = 0, last = -1;
+    double qkk = 0.0, off = 0.0;
+    for (long long kb = k0; kb < k1; kb += 32) {
+        const long long k = kb + lane;
+        const bool in = k < k1;
+        const int j = in ? col[k] : INT_MAX;
+        const double v = in ? val[k] : 0.0;
+        int jp = __shfl_up_sync(0xffffffffu, j, 1);
+        if (lane == 0) jp = last;
+        if (in && (j < 0 || j >= n || j <= jp)) e |= AJM_EB_CSR;
+        if (in && !isfinite(v)) e |= AJM_EB_NONFINITE;
+        const double a = (in && j != i) ? fabs(v) : 0.0;
+        const double dq = (in && j == i) ? v : 0.0;
+#pragma unroll
+        for (int l = 0; l < 32; ++l) {
+            const double al = __shfl_sync(0xffffffffu, a, l);
+            const double ql = __shfl_sync(0xffffffffu, dq, l);
+            if (kb + l < k1) {
+                if (ql != 0.0) qkk = ql;  // the diagonal entry (a second one is a CSR error anyway)
+                off += al;                // 0.0 for the diagonal: adding +0 is exact
+            }
+        }
+        last = __shfl_sync(0xffffffffu, j, 31);
+    }
+    e = __reduce_or_sync(0xffffffffu, e);
+    if (lane != 0) return;
     if (qkk < 0.0) e |= AJM_EB_NEGDIAG;
     double d;
     if (dmode == 0) d = qkk + off;

@@ -331,3 +331,50 @@ def test_interleaved_handles_kernel_attributes():
     finally:
         for s in solvers:
             s.close()
+
+
+def test_long_row_validation():
+    """Rows of > 2048 entries are validated by a warp each (create-time): eq-J-diag still bitwise
+    the oracle's ascending-column sum, and CSR / non-finite / negative-diagonal errors inside a
+    long row are still caught."""
+    import paper_2407_03272_b200 as ajm
+    n = 9000
+    g = np.random.Generator(np.random.PCG64(11))
+    hubs = [0, 4500, 8999]  # three hubs joined to 3000-6000 random nodes each
+    u, v = [], []
+    for h, deg in zip(hubs, (6000, 3000, 4097)):
+        nb = g.choice(np.setdiff1d(np.arange(n), hubs), deg, replace=False)
+        u.append(np.full(deg, h)), v.append(nb)
+    path = np.arange(n - 1)  # plus a path, so every node has a neighbour
+    u.append(path), v.append(path + 1)
+    u, v = np.concatenate(u), np.concatenate(v)
+    lo, hi = np.minimum(u, v), np.maximum(u, v)
+    key = np.unique(lo * n + hi)
+    w = g.uniform(0.1, 1.0, key.size) * 10.0 ** g.integers(-3, 4, key.size)  # spread magnitudes
+    Q = synth._laplacian_from_edges(n, key // n, key % n, w, shift=1e-3)
+    assert np.diff(Q.row_ptr).max() > 6000
+    p = synth.make_problem("hubs", Q, 12)
+    r = gpu_solve(p.Q, p.b, tol=0.0, maxit=50, restart=True)
+    np.testing.assert_array_equal(r.D, oracle.build_jdiag(p.Q))
+    o, _ = oracle_matching(p.Q, p.b, r, tol=0.0, maxit=50, restart=True)
+    assert max_rel(r.x, o.x) <= PARITY_TOL
+    h0, h1 = int(Q.row_ptr[0]), int(Q.row_ptr[1])  # row 0: a hub row (diagonal first)
+
+    def create(col, val):
+        with pytest.raises(ajm.AjmError) as e:
+            ajm.Solver(n, Q.row_ptr, col, val, p.b)
+        return e.value.status_name
+
+    bad = Q.col.copy()
+    bad[h0 + 3000], bad[h0 + 3001] = bad[h0 + 3001], bad[h0 + 3000]
+    assert create(bad, Q.val) == "AJM_ERR_CSR_INVALID"
+    bad = Q.col.copy()
+    bad[h1 - 1] = n  # out of range, last entry of the row
+    assert create(bad, Q.val) == "AJM_ERR_CSR_INVALID"
+    vv = Q.val.copy()
+    vv[h0 + 5000] = np.inf
+    assert create(Q.col, vv) == "AJM_ERR_NONFINITE"
+    vv = Q.val.copy()
+    assert Q.col[h0] == 0
+    vv[h0] = -1.0
+    assert create(Q.col, vv) == "AJM_ERR_NEGATIVE_DIAG"
