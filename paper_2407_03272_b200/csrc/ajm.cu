@@ -176,6 +176,7 @@ struct ajm_ctx {
     int ring_stages = 4;        // TMA ring depth of the chosen solver kernel
     bool seg_fn = true;         // the chosen plain/col8 ring kernel has the segment phases
     bool ring_fn = false;       // h->fn is a plain_fn/col8_fn kernel (ring depth selectable)
+    bool wide_rows = false;     // SELL chunks average >= 16 entries per row
     size_t meta_bytes = 0;      // shared-memory unit/chunk tables behind the ring
     int carveout = 100;         // preferred shared-memory carve-out (%), set before every launch
     double nb = 0.0;
@@ -888,6 +889,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         // width 27: 1174 -> 1197), so only below an average width of 16
         const double avg_w = h->nchunks ? (double)h->sell_elems / (32.0 * (double)h->nchunks) : 0.0;
         if (h->nseg == 0 && !h->vstage && avg_w < 16.0 && !getenv("AJM_NO_NOSEG")) h->fn = kVariants[h->variant].fn0;
+        h->wide_rows = avg_w >= 16.0;
         if (const char* ev = getenv("AJM_GRING")) h->gring = atoi(ev) ? 1 : 0;
         if (h->vstage) h->fn = kVariants[h->variant].fnv;
         if (h->jbs) {  // block-diagonal J: its own instantiation (natural order, no segments)
@@ -1268,9 +1270,12 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         // the depth goes to the ring -- 4 for narrow rows (config 2: 43.7 -> 43.0 us/pass vs 3), 5
         // for wide ones, whose units hold only 2-3 chunks (config 5: 1414 / 1139 / 1126 us/pass
         // at 3 / 4 / 5); AJM_COL8_STAGES=2..6 overrides
-        int st8 = h->seg_fn ? 5 : 4;
+        // Without warp segments the byte-coded kernel is always the variant compiled without the
+        // segment phases (config 5: 1104 -> 1088 us/pass; the int32 layouts keep the seg variant
+        // for wide rows, where it measured faster)
+        int st8 = h->wide_rows ? 5 : 4;
         if (const char* es = getenv("AJM_COL8_STAGES")) st8 = std::min(6, std::max(2, atoi(es)));
-        SolveFn f8 = col8_fn(h->seg_fn, st8);
+        SolveFn f8 = col8_fn(h->nseg > 0, st8);
         const size_t dyn8 = (size_t)st8 * AJM_UNIT_EL * 9 + h->meta_bytes;
         int occ8 = 0;
         if (htab[AJM_CTAB_HASH + 1] == 0 && htab[AJM_CTAB_HASH] <= AJM_CTAB) {
