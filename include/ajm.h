@@ -16,7 +16,9 @@
  *   - `cuda_stream` is a cudaStream_t (NULL = the legacy default stream); all device work of a call
  *     is ordered on it.  ajm_create and ajm_solve return only after the stream reaches the end of
  *     their work (their results are host-visible).
- *   - A handle is not thread-safe; distinct handles are independent.
+ *   - A handle is not thread-safe; distinct handles are independent and may be used from different
+ *     host threads at the same time (the solver kernels' launch attributes are set and the kernel
+ *     launched under one library lock).
  *   - On error a call returns a non-zero ajm_status_t and ajm_last_error() explains it; no output
  *     argument is written except where stated.
  */

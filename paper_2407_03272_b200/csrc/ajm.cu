@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -234,7 +235,9 @@ cudaMemcpyKind kind_from_device(const void* dst) {
 // destroy costs no synchronising cudaFree.
 cudaMemPool_t ajm_pool(int dev) {
     static cudaMemPool_t pools[64] = {};
+    static std::mutex mu;  // first use from several threads at once
     if (dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
     if (!pools[dev]) {
         cudaMemPoolProps pp = {};
         pp.allocType = cudaMemAllocationTypePinned;
@@ -349,7 +352,10 @@ int block_threads(const ajm_ctx* h) { return h->direct ? AJM_BLOCK : (h->gring ?
 // cooperative launch of the persistent solver kernel, with the L2 access-policy window over the
 // iterate vectors (persisting hits, streaming misses)
 cudaError_t launch_solver(ajm_ctx* h, AjmPass& p, cudaStream_t st) {
-    // the attributes belong to the kernel, which other handles share: set this handle's own
+    // the attributes belong to the kernel, which other handles share: set this handle's own, and
+    // launch before another thread's handle can change them (the launch itself is asynchronous)
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
     cudaError_t e = cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributePreferredSharedMemoryCarveout, h->carveout);

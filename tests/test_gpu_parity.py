@@ -378,3 +378,35 @@ def test_long_row_validation():
     assert Q.col[h0] == 0
     vv[h0] = -1.0
     assert create(Q.col, vv) == "AJM_ERR_NEGATIVE_DIAG"
+
+
+def test_threads_with_own_handles_and_streams():
+    """Two host threads, each with its own handles and CUDA stream, create and solve different
+    layouts at the same time (the C ABI releases the GIL): every result is bitwise the
+    single-threaded one (kernel attributes are set and the kernel launched under one lock)."""
+    import threading
+    import torch
+    import paper_2407_03272_b200 as ajm
+    probs = [synth.config_problem(3, 0.02), synth.config_problem(2, 0.25)]
+    ref = [gpu_solve(p.Q, p.b, tol=0.0, maxit=120, restart=True).x for p in probs]
+    errs = []
+
+    def work(k):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                for _ in range(4):
+                    p = probs[k]
+                    with ajm.Solver.from_csr(p.Q, p.b, stream=st) as s:
+                        r = s.solve(tol=0.0, maxit=120, restart=True)
+                        st.synchronize()
+                        np.testing.assert_array_equal(r.x.cpu().numpy(), ref[k])
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in (0, 1, 0, 1)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
