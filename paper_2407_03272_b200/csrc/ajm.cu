@@ -708,6 +708,15 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         choff.assign((size_t)h->nchunks + 1, 0);
         chcost.assign((size_t)h->nchunks, 0.0);
         const int64_t nchk_h = h->nchunks, nsell_h = h->n_sell;
+        // A wide chunk fills a staging unit alone (<= 2048 entries), so a ring of S stages keeps
+        // only S * floor(64 / w) of the CTA's 8 warps busy: weight such chunks by the idle share
+        // (config 4: the first sorted windows hold the 40-64-wide rows, and the CTAs planned on
+        // them finished ~90 us after the median)
+        const double par_stages = getenv("AJM_COST_PAR") && !atoi(getenv("AJM_COST_PAR")) ? 0.0 : (h->relabel ? 3.0 : 4.0);
+        // softened to (8 / busy)^0.5: config 4 495 -> 444 us/pass, config 3 79.1 -> 79.7 (exponent
+        // 1: 452 / 81.0; 0.7: 440 / 80.3; the idle-share weight on one-chunk units only: 452 / 79.1)
+        const double par_alpha = getenv("AJM_COST_ALPHA") ? atof(getenv("AJM_COST_ALPHA")) : 0.5;
+        const bool par_only1 = getenv("AJM_COST_ONLY1") && atoi(getenv("AJM_COST_ONLY1"));
 #pragma omp parallel for schedule(static)
         for (int64_t c = 0; c < nchk_h; ++c) {
             int64_t w = 1, rows = 0;
@@ -716,7 +725,10 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
                 ++rows;
             }
             choff[(size_t)c + 1] = 32 * w;
-            chcost[(size_t)c] = 12.0 * 32 * w + 56.0 * rows + 64.0;
+            double busy = par_stages > 0.0 ? std::min<double>(AJM_WARPS, par_stages * std::max<int64_t>(1, AJM_UNIT_EL / (32 * w)))
+                                            : (double)AJM_WARPS;
+            if (par_only1 && AJM_UNIT_EL / (32 * w) >= 2) busy = AJM_WARPS;
+            chcost[(size_t)c] = (12.0 * 32 * w + 56.0 * rows + 64.0) * std::pow((double)AJM_WARPS / busy, par_alpha);
         }
         for (int64_t c = 0; c < nchk_h; ++c) choff[(size_t)c + 1] += choff[(size_t)c];
         h->sell_elems = choff.back();
@@ -1112,8 +1124,8 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(dalloc(&h->scratch, 512, st));
     CC(dalloc(&h->err, 1, st));
     if (getenv("AJM_TS")) {
-        CC(dalloc(&h->ts, 512 + 2 * (size_t)h->grid, st));
-        CC(cudaMemsetAsync(h->ts, 0, (512 + 2 * (size_t)h->grid) * sizeof(unsigned long long), st));
+        CC(dalloc(&h->ts, 512 + 4 * (size_t)h->grid, st));
+        CC(cudaMemsetAsync(h->ts, 0, (512 + 4 * (size_t)h->grid) * sizeof(unsigned long long), st));
     }
     h->h_ctrl = (AjmCtrl*)malloc(sizeof(AjmCtrl));
     if (!h->h_ctrl) return bail(fail(h, AJM_ERR_OOM, "host allocation failed"));
@@ -1474,12 +1486,12 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
             ctl += (double)(hts[k * 8 + 5] - hts[k * 8 + 4]);
             ++np;
         }
-        std::vector<unsigned long long> cta((size_t)2 * h->grid);
+        std::vector<unsigned long long> cta((size_t)4 * h->grid);
         AJM_CUDA(h, cudaMemcpy(cta.data(), h->ts + 512, sizeof(unsigned long long) * cta.size(), cudaMemcpyDeviceToHost));
         if (c.s.iterations >= 6 && hts[5 * 8]) {  // pass-5 work-end of every CTA relative to the pass start
             std::vector<std::pair<double, int>> endt;
             for (int g = 0; g < h->grid; ++g)
-                endt.push_back({(double)(cta[(size_t)2 * g] - hts[5 * 8]) / 1e3, (int)cta[(size_t)2 * g + 1]});
+                endt.push_back({(double)(cta[(size_t)4 * g] - hts[5 * 8]) / 1e3, (int)cta[(size_t)4 * g + 1]});
             std::sort(endt.begin(), endt.end());
             auto q = [&](double f) { return endt[(size_t)std::min<double>(endt.size() - 1, f * (endt.size() - 1))]; };
             fprintf(stderr, "[ajm ts] pass 5 CTA work-end us: min %.2f (sm %d) p10 %.2f p50 %.2f p90 %.2f max %.2f (sm %d)\n",
@@ -1487,8 +1499,9 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
                     endt.back().first, endt.back().second);
             if (getenv("AJM_TS_ALL")) {
                 for (int g = 0; g < h->grid; ++g)
-                    fprintf(stderr, "[ajm cta] %d sm %d end %.2f\n", g, (int)cta[(size_t)2 * g + 1],
-                            (double)(cta[(size_t)2 * g] - hts[5 * 8]) / 1e3);
+                    fprintf(stderr, "[ajm cta] %d sm %d seg-end %.2f chunk-end %.2f end %.2f\n", g, (int)cta[(size_t)4 * g + 1],
+                            (double)(cta[(size_t)4 * g + 2] - hts[5 * 8]) / 1e3, (double)(cta[(size_t)4 * g + 3] - hts[5 * 8]) / 1e3,
+                            (double)(cta[(size_t)4 * g] - hts[5 * 8]) / 1e3);
             }
         }
         if (np)

@@ -953,6 +953,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         }
         }
         if (tsw) p.ts[pass * 8 + 6] = ajm_gtime();
+        if (p.ts && tid == 0 && pass == 5) p.ts[512 + 4 * bid + 2] = ajm_gtime();  // warp 0's segments done
         if (direct) {
             // (2') SELL chunks straight from global memory; chunk j of the CTA -> warp j % 8
             const int jb = (int)((long long)nchk * warp / AJM_WARPS);
@@ -1028,6 +1029,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
             ucnt += nunits;
         }
         if (tsw) p.ts[pass * 8 + 7] = ajm_gtime();
+        if (p.ts && tid == 0 && pass == 5) p.ts[512 + 4 * bid + 3] = ajm_gtime();  // warp 0's chunks done
         if (kSeg) {
         // (3) segment rows owned by this CTA (one per lane, 256 in flight per CTA): wait for all
         //     segments of this pass, sum their partials in segment order, run the row epilogue
@@ -1050,8 +1052,8 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         if (p.ts && tid == 0 && pass == 5) {  // debug: every CTA's work-end time and SM of pass 5
             unsigned smid;
             asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-            p.ts[512 + 2 * bid] = ajm_gtime();
-            p.ts[512 + 2 * bid + 1] = smid;
+            p.ts[512 + 4 * bid] = ajm_gtime();
+            p.ts[512 + 4 * bid + 1] = smid;
         }
         ajm_block_reduce(acc, s_red);
         if (tsw) p.ts[pass * 8 + 2] = ajm_gtime();
