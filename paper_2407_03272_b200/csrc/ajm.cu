@@ -159,6 +159,7 @@ struct ajm_ctx {
     int64_t nsegq = 0;              // claim groups
     int dynseg = 0;                 // segments claimed dynamically by warps (else static LPT plan)
     int* cta_unit = nullptr;
+    int* seg_meta = nullptr;        // int4 {row, k0, k1, split} per static seg_list position
     double* partials = nullptr;
     AjmCtrl* ctrl = nullptr;
     double* hist = nullptr;  // 4 x hist_cap: res, f, d, dabs
@@ -282,7 +283,7 @@ void free_all(ajm_ctx* h) {
                     h->seg_split, h->seg_part, h->split_row, h->split_seg0, h->split_cnt,
                     h->cta_split, h->owner_split, h->unit_c0, h->cta_seg, h->seg_list, h->cta_unit, h->partials, h->ctrl,
                     h->hist, h->scratch, h->err, h->ts, h->perm_fwd, h->perm_inv, h->b_in, h->Jblk, h->Jinv, h->seg_order, h->seg_grp,
-                    h->g_uc0, h->g_coff, h->g_ubase, h->g_cbase, h->scode, h->ctab};
+                    h->g_uc0, h->g_coff, h->g_ubase, h->g_cbase, h->scode, h->ctab, h->seg_meta};
     for (void* p : ptrs) dfree(p);
     if (h->h_ctrl) free(h->h_ctrl);
     if (h->ev0) cudaEventDestroy(h->ev0);
@@ -341,6 +342,7 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.Jinv = h->Jinv;
     p.jbs = h->jbs;
     p.scode = h->scode;
+    p.seg_meta = reinterpret_cast<const int4*>(h->seg_meta);
     p.ctab = h->ctab;
     p.direct_interleave = getenv("AJM_DIRECT_INTERLEAVE") ? atoi(getenv("AJM_DIRECT_INTERLEAVE")) : 0;
     return p;
@@ -902,11 +904,11 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         if (!h->ident) h->vstage = 0;
         h->direct = 0;  // direct mode measured slower than the ring on every config so far
         if (const char* ev = getenv("AJM_DIRECT")) h->direct = atoi(ev) ? 1 : 0;
-        // no long rows: the variant without the segment phases -- measured faster for narrow
-        // chunks (config 2, width 7: 47.5 -> 45.5 us/pass) but not for wide ones (config 5,
-        // width 27: 1174 -> 1197), so only below an average width of 16
         const double avg_w = h->nchunks ? (double)h->sell_elems / (32.0 * (double)h->nchunks) : 0.0;
-        if (h->nseg == 0 && !h->vstage && avg_w < 16.0 && !getenv("AJM_NO_NOSEG")) h->fn = kVariants[h->variant].fn0;
+        // no long rows: the variant without the segment phases (its ring loop has more registers to
+        // spare: config 2 47.5 -> 45.5 us/pass, config 3 81.5 -> 76.2; config 5 with int32 columns
+        // 1197 vs 1200, even)
+        if (h->nseg == 0 && !h->vstage && !getenv("AJM_NO_NOSEG")) h->fn = kVariants[h->variant].fn0;
         h->wide_rows = avg_w >= 16.0;
         if (const char* ev = getenv("AJM_GRING")) h->gring = atoi(ev) ? 1 : 0;
         if (h->vstage) h->fn = kVariants[h->variant].fnv;
@@ -1115,6 +1117,15 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(dalloc(&h->owner_split, h->nsplit, st));
     CC(dalloc(&h->unit_c0, unit_c0_h.size(), st));
     CC(dalloc(&h->cta_seg, cta_seg_h.size(), st));
+    std::vector<int> seg_meta_h(4 * seg_list_h.size());
+    for (size_t k = 0; k < seg_list_h.size(); ++k) {
+        const int sg = seg_list_h[k];
+        seg_meta_h[4 * k + 0] = seg_row_h[(size_t)sg];
+        seg_meta_h[4 * k + 1] = seg_k0_h[(size_t)sg];
+        seg_meta_h[4 * k + 2] = seg_k1_h[(size_t)sg];
+        seg_meta_h[4 * k + 3] = seg_split_h[(size_t)sg];
+    }
+    CC(dalloc(&h->seg_meta, seg_meta_h.size(), st));
     CC(dalloc(&h->seg_list, seg_list_h.size(), st));
     CC(dalloc(&h->seg_order, seg_order_h.size(), st));
     CC(dalloc(&h->seg_grp, seg_grp_h.size(), st));
@@ -1163,6 +1174,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(h2d(h->owner_split, owner_split_h.data(), sizeof(int) * owner_split_h.size()));
     CC(h2d(h->unit_c0, unit_c0_h.data(), sizeof(int) * unit_c0_h.size()));
     CC(h2d(h->cta_seg, cta_seg_h.data(), sizeof(int) * cta_seg_h.size()));
+    CC(h2d(h->seg_meta, seg_meta_h.data(), sizeof(int) * seg_meta_h.size()));
     CC(h2d(h->seg_list, seg_list_h.data(), sizeof(int) * seg_list_h.size()));
     CC(h2d(h->seg_order, seg_order_h.data(), sizeof(int) * seg_order_h.size()));
     CC(h2d(h->seg_grp, seg_grp_h.data(), sizeof(int) * seg_grp_h.size()));

@@ -137,6 +137,7 @@ struct AjmPass {
     int jbs;                                 // AJM_D_JBLOCK block size (0: diagonal D)
     const uint8_t* __restrict__ scode;       // (kCol8) SELL column codes: col = row + ctab[code]
     const int* __restrict__ ctab;            // (kCol8) [256] distinct offsets col - row, ascending
+    const int4* __restrict__ seg_meta;       // static plan: {row, k0, k1, split} of seg_list[k]
 };
 
 __device__ __forceinline__ unsigned long long ajm_gtime() {
@@ -922,6 +923,30 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         //     longest first).
         if (p.dynseg && bid == 0 && tid == 0) c->seg_q[(t + 1) & 1] = 0u;
         int gk = 0, gend = 0;  // dynamic mode: current claim group [gk, gend) of seg_order
+        if (!p.dynseg) {
+            // static plan: the next segment's metadata is loaded while this one runs (one 16-byte
+            // record in list order, no index chase)
+            int sk = sg0 + warp;
+            int4 m = make_int4(0, 0, 0, -1);
+            int msg = 0;
+            if (sk < sg1) { m = __ldg(p.seg_meta + sk); msg = __ldg(p.seg_list + sk); }
+            while (sk < sg1) {
+                const int4 cm = m;
+                const int csg = msg;
+                sk += AJM_WARPS;
+                if (sk < sg1) { m = __ldg(p.seg_meta + sk); msg = __ldg(p.seg_list + sk); }
+                const double s = ajm_seg_dot(p, cm.y, cm.z, xc, lane);
+                if (lane == 0) {
+                    if (cm.w < 0) {
+                        ajm_row_epilogue(p, cm.x, s, beta, restart_t, xc, xp, xf, acc);
+                    } else {
+                        __stcg(p.seg_part + csg, s);
+                        __threadfence();
+                        atomicAdd(p.split_cnt + cm.w, 1u);
+                    }
+                }
+            }
+        } else
         for (int sk = sg0 + warp;; sk += AJM_WARPS) {
             int sg;
             if (p.dynseg) {
