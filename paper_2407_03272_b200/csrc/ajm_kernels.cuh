@@ -1124,18 +1124,18 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         if (tsw) p.ts[pass * 8 + 3] = ajm_gtime();
         if (warp < AJM_NPART) {
             // warp j reduces component j of all CTA partials: lane l sums records l, l+32, ... in
-            // order (8 loads in flight), then a fixed xor tree -- identical bits in every CTA
+            // order (16 loads in flight), then a fixed xor tree -- identical bits in every CTA
             const double* src = part + (size_t)warp * G;
             double v = 0.0;
             if (kCluster) {  // G <= 16: lane l holds CTA l's record (the global path's order)
                 if (lane < (int)G) v = ajm_ld_cluster(&s_part[t & 1][warp], (unsigned)lane);
             } else
-            for (int k0 = lane; k0 < (int)G; k0 += 8 * 32) {
-                double r[8];
+            for (int k0 = lane; k0 < (int)G; k0 += 16 * 32) {  // one round trip for G <= 512
+                double r[16];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) r[j] = (k0 + j * 32 < (int)G) ? __ldcg(src + k0 + j * 32) : 0.0;
+                for (int j = 0; j < 16; ++j) r[j] = (k0 + j * 32 < (int)G) ? __ldcg(src + k0 + j * 32) : 0.0;
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
+                for (int j = 0; j < 16; ++j)
                     if (k0 + j * 32 < (int)G) v += r[j];
             }
             v = ajm_warp_sum(v);
