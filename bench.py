@@ -196,6 +196,28 @@ def make_problem(cfg=2):
     return synth.config_problem(cfg)
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def layout_bytes_per_iter(info, jblock=None) -> float:
+    """Bytes one pass of THIS layout must move at minimum: every stored SELL entry including its
+    padding (8-byte value + the streamed column index: 4 B int32 or 1 B byte code), the warp
+    segments' CSR entries (12 B), and the seven n-vectors (D replaced by bs doubles of J^-1 with
+    block J).  Differs from the algorithmic model (12 nnz + 56 n + 4(n+1)) by the byte codes, the
+    padding and the row offsets SELL does not need."""
+    return ((8.0 + info["col_bytes"]) * info["sell_elems"] + 12.0 * info["seg_nnz"]
+            + (48.0 + 8.0 * (jblock or 1)) * info["n"])
+
+
 def cpu_baseline_run(p, cfg=2, budget_s=12.0, nthreads=None):
     """The oracle as it stands (literal two-SpMV Alg. 3), on host cores, on a bounded sample of the
     workload: the first T iterations of the same solve, T sized to ~budget_s seconds."""
@@ -209,7 +231,7 @@ def cpu_baseline_run(p, cfg=2, budget_s=12.0, nthreads=None):
     t0 = time.perf_counter()
     r = oracle.solve(p.Q, p.b, tol=0.0, maxit=T, restart=True)
     dt = time.perf_counter() - t0
-    return {"value": r.iterations / dt, "unit": UNIT, "cores": nt, "kind": "oracle",
+    return {"value": r.iterations / dt, "unit": UNIT, "cores": nt, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"first {T} iterations of the config-{cfg} solve (literal two-SpMV Alg. 3, "
                       f"plain C FP64, {nt} OpenMP threads), {dt:.2f} s wall"}
 
@@ -242,13 +264,122 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": W["workload"], "sample_iterations_per_step": S},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": nt, "kind": "oracle",
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": nt, "kind": "oracle", "cpu_model": cpu_model(),
                          "sample": f"{S} iterations of the config-{args.config} solve per step (literal two-SpMV "
                                    f"Alg. 3, plain C FP64, {nt} OpenMP threads)"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def timed_solves(solver, kw, steps, warmup, stream, dist=None, dev=None, clocks=None):
+    """W untimed solves, then K solves bracketed by barrier + synchronize, CUDA events on the
+    launching stream.  Returns (iterations, passes, loop_ms (sum of the solver launches' own event
+    durations), ms (whole timed region), results, clocks)."""
+    import torch
+    for _ in range(warmup):
+        solver.solve(**kw)
+    torch.cuda.synchronize()
+    if clocks is not None:
+        clocks.start()
+        time.sleep(0.3)
+    barrier(dist, dev)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    iters, passes, loop_ms = 0, 0, 0.0
+    results = []
+    for _ in range(steps):
+        r = solver.solve(**kw)
+        inf = solver.info()
+        iters += r.iterations
+        passes += inf["last_passes"]
+        loop_ms += inf["last_loop_ms"]
+        results.append(r)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(dist, dev)
+    clk = clocks.stop() if clocks is not None else None
+    return iters, passes, loop_ms, e0.elapsed_time(e1), results, clk
+
+
+def roofline_block(p, info, passes, loop_ms, steps, bound, jblock=None):
+    """The dominant kernel's roofline (the persistent solver launch: one per solve).
+      achieved / frac : ALGORITHMIC bytes per pass (12 nnz + 7*8 n + 4 (n+1); D -> bs
+                        doubles of J^-1 with block J) x passes / the launches' CUDA-event time
+      layout_frac     : the bytes this layout must move (byte-coded columns: 9 B per stored entry,
+                        SELL padding, no row offsets) over the same time -- what the kernel could at
+                        best save on the stream
+      dram_frac       : ncu dram read+write bytes per pass of the committed capture
+                        (profiles/ncu_traffic.json, per workload) over this run's time per pass --
+                        the L2-resident vectors make it lower than the algorithmic figure"""
+    peak, peak_src = load_peaks()
+    model_bytes = info["model_bytes_per_iter"]
+    sec = loop_ms * 1e-3
+    achieved = model_bytes * passes / sec / 1e9
+    lay = layout_bytes_per_iter(info, jblock)
+    tr = None if jblock else load_traffic(p.name)
+    us = 1e6 * sec / passes
+    rb = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+          "traffic": None if tr is None else tr["dram_bytes_per_pass"] * passes / steps,
+          "traffic_basis": "ncu dram__bytes_read.sum + dram__bytes_write.sum per pass of the solver kernel "
+                           "(profiles/ncu_traffic.json" + ("" if tr is None else f", capture {tr.get('capture', '?')}")
+                           + ") x passes per launch",
+          "peak_source": peak_src,
+          "kernel": "ajm_solve_kernel (persistent; one launch per solve)",
+          "achieved_basis": "algorithmic bytes nnz*12+7n*8+4(n+1) per pass (D replaced by bs doubles of J^-1 per "
+                            "row with --jblock) x passes / launch duration (CUDA events on the launch stream)",
+          "layout_bytes_per_iteration": lay,
+          "layout_frac": lay * passes / sec / 1e9 / peak,
+          "dram_frac": None if tr is None else tr["dram_bytes_per_pass"] / (us * 1e-6) / 1e9 / peak}
+    return rb, model_bytes, achieved, us
+
+
+def gather_roof(p, info, passes, loop_ms):
+    """Second roof for graph layouts (sorted windows, sigma > 1): one random 8-byte x~ gather per
+    stored nonzero and pass against the measured random-gather ceiling from an L2-resident array
+    (tools/ubench/gather_mlp.cu).  Stencils (sigma = 1) hit L1 on most gathers, where this roof
+    does not bind -- it is not reported for them."""
+    if info["sigma"] <= 1:
+        return None
+    gps = p.Q.nnz * passes / (loop_ms * 1e-3) / 1e9
+    return {"bound": "l2_random_gather", "achieved": gps, "peak": GATHER_PEAK_GPS, "unit": "G gathers/s",
+            "frac": gps / GATHER_PEAK_GPS,
+            "peak_source": "measured on this pool: tools/ubench/gather_mlp.cu (8-32 MB array)"}
+
+
+def other_config_record(cfg, args, dev, stream):
+    """One BASELINE config other than the headline one, measured the same way (device-resident
+    inputs, W warm-up + K timed solves, CUDA events): it/s, us/pass and the roofline fractions."""
+    import torch
+    import paper_2407_03272_b200 as ajm
+    W = WORKLOADS[cfg]
+    t0 = time.perf_counter()
+    p = make_problem(cfg)
+    gen_s = time.perf_counter() - t0
+    Qd = [torch.from_numpy(a).to(dev) for a in (p.Q.row_ptr, p.Q.col, p.Q.val, p.b)]
+    x_out = torch.empty(p.Q.n, dtype=torch.float64, device=dev)
+    with ajm.Solver(p.Q.n, *Qd[:3], Qd[3]) as solver:
+        del Qd
+        kw = dict(tol=W["tol"], maxit=W["maxit"], restart=True, x_out=x_out, history=False)
+        steps = max(2, min(args.steps, 5))
+        clocks = ClockSampler(dev.index)
+        iters, passes, loop_ms, ms, results, clk = timed_solves(solver, kw, steps, 3, stream, clocks=clocks)
+        info = solver.info()
+    assert all(r.status == ("converged" if W["tol"] > 0 else "maxiter") for r in results)
+    rb, model_bytes, achieved, us = roofline_block(p, info, passes, loop_ms, steps, "hbm")
+    rec = {"config": cfg, "workload": W["workload"], "n": p.Q.n, "nnz": p.Q.nnz,
+           "value": iters / (ms * 1e-3), "unit": UNIT, "steps": steps, "warmup": 3,
+           "iterations_per_solve": iters / steps, "time_to_tol_ms": ms / steps, "us_per_iteration": us,
+           "sigma": info["sigma"], "column_index_bytes": info["col_bytes"], "grid": info["grid"],
+           "roofline": rb, "roofline_gather": gather_roof(p, info, passes, loop_ms), "clocks": clk,
+           "generate_s": round(gen_s, 1)}
+    if W["bound"] == "latency":
+        rec["roofline"]["note"] = (f"{model_bytes / 1e6:.2f} MB per pass fits the L2: latency-bound "
+                                   "(one grid barrier per pass), the HBM fraction is not the bound")
+    del p
+    return rec
 
 
 def run_ours(args):
@@ -272,31 +403,9 @@ def run_ours(args):
     solver = ajm.Solver(p.Q.n, *Qd[:3], Qd[3], jblock=args.jblock)
     x_out = torch.empty(p.Q.n, dtype=torch.float64, device=dev)
     kw = dict(tol=tol, maxit=maxit, restart=True, x_out=x_out, history=False)
-    for _ in range(args.warmup):
-        solver.solve(**kw)
-    torch.cuda.synchronize()
-
     clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
-    barrier(dist, dev)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    iters, passes, loop_ms = 0, 0, 0.0
-    results = []
-    for _ in range(args.steps):
-        r = solver.solve(**kw)
-        inf = solver.info()
-        iters += r.iterations
-        passes += inf["last_passes"]
-        loop_ms += inf["last_loop_ms"]
-        results.append(r)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier(dist, dev)
-    clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
+    iters, passes, loop_ms, ms, results, clk = timed_solves(solver, kw, args.steps, args.warmup, stream,
+                                                            dist, dev, clocks)
     job_iters, job_ms = reduce_job(float(iters), ms, dist, dev)
     info = solver.info()
     assert all(r.status == ("converged" if tol > 0 else "maxiter") for r in results)
@@ -322,15 +431,19 @@ def run_ours(args):
         e2e_ms += a0.elapsed_time(a1)
         d2h = x_host.numel() * 8 + 2 * 8 * (r2.iterations + 1)
     e2e_iters, e2e_ms = reduce_job(float(e2e_iters), e2e_ms, dist, dev)
+    del host, x_host, Qd
+    solver.close()
 
     if rank != 0:
-        solver.close()
         return 0
-    peak, peak_src = load_peaks()
-    model_bytes = info["model_bytes_per_iter"]
-    achieved = model_bytes * passes / (loop_ms * 1e-3) / 1e9  # GB/s, per-launch average
-    tr = None if args.jblock else load_traffic(p.name)
-    traffic = None if tr is None else tr["dram_bytes_per_pass"] * passes / args.steps
+    rb, model_bytes, achieved, us = roofline_block(p, info, passes, loop_ms, args.steps, W["bound"] if W["bound"] != "latency" else "hbm",
+                                                   args.jblock)
+    # the other BASELINE configs, each as a roofline fraction (north_star), same measurement
+    others = []
+    if world == 1 and args.config == 2 and not args.jblock and args.other_configs:
+        for cfg in [int(c) for c in args.other_configs.split(",") if c]:
+            others.append(other_config_record(cfg, args, dev, stream))
+            torch.cuda.empty_cache()
     cpu = cpu_baseline_run(p, args.config) if (world == 1 and not args.no_cpu_baseline) else None
     # the same oracle on ONE host thread (SURVEY §8(d) oracle timing (i)), a shorter sample
     cpu1 = cpu_baseline_run(p, args.config, budget_s=4.0, nthreads=1) \
@@ -356,31 +469,18 @@ def run_ours(args):
         "config": {"workload": W["workload"] + (f"; block-diagonal J (eq-J-blkdiag), bs={args.jblock}"
                                                  if args.jblock else ""),
                    "n": p.Q.n, "nnz": p.Q.nnz, "tol": tol, "maxit": maxit,
-                   "parallelism": f"replicas x{world} (the method does not shard: DESIGN.md §6)",
+                   "parallelism": f"replicas x{world} (one independent solve per GPU: DESIGN.md §6)",
                    "l2": l2_note,
-                   "kernel_variant": info["variant"], "grid": info["grid"],
+                   "grid": info["grid"],
                    "column_index_bytes": info.get("col_bytes", 4),
                    "ctas_per_sm": info["ctas_per_sm"]},
         "iterations_per_solve": iters / args.steps,
         "time_to_tol_ms": ms / args.steps,
-        "us_per_iteration": 1e3 * loop_ms / passes,
+        "us_per_iteration": us,
         "model_bytes_per_iteration": model_bytes,
         "model_gbs": achieved,
         "pct_of_8tbs_nominal": 100.0 * achieved / NOMINAL_HBM_GBS,
-        "roofline": {"bound": W["bound"] if W["bound"] != "latency" else "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "traffic_basis": "ncu dram read+write per pass (profiles/ncu_traffic.json) x passes per launch", "peak_source": peak_src,
-                     "kernel": "ajm_solve_kernel (persistent; one launch per solve)",
-                     "achieved_basis": "algorithmic bytes nnz*12+7n*8+4(n+1) per pass (D replaced by bs "
-                                       "doubles of J^-1 per row with --jblock) x passes / launch duration "
-                                       "(CUDA events on the launch stream)"},
-        # second roof for the x~ gathers: one random 8-byte load per stored nonzero and pass,
-        # against the measured ceiling of random 8-byte gathers from an L2-resident array
-        # (tools/ubench/gather_mlp.cu, profiles/r1_ubench_gather_mlp.jsonl); binding for the
-        # graph Laplacians (configs 3, 4), not for the stencils (whose gathers mostly hit L1)
-        "roofline_gather": {"bound": "l2_random_gather", "achieved": p.Q.nnz * passes / (loop_ms * 1e-3) / 1e9,
-                            "peak": GATHER_PEAK_GPS, "unit": "G gathers/s",
-                            "frac": p.Q.nnz * passes / (loop_ms * 1e-3) / 1e9 / GATHER_PEAK_GPS,
-                            "peak_source": "measured on this pool: tools/ubench/gather_mlp.cu (8-32 MB array)"},
+        "roofline": rb,
         "e2e": {"value": e2e_iters / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "note": "ajm_create from pinned host CSR+b (H2D + layout build) + ajm_solve to 1e-6 "
@@ -390,9 +490,12 @@ def run_ours(args):
         "clocks": clk,
         "cpu_baseline": cpu,
         "cpu_baseline_1thread": cpu1,
+        "other_configs": others,
     }
+    rg = gather_roof(p, info, passes, loop_ms)
+    if rg is not None:
+        line["roofline_gather"] = rg
     print(json.dumps(line), flush=True)
-    solver.close()
     return 0
 
 
@@ -410,6 +513,9 @@ def main(argv=None):
     ap.add_argument("--jblock", type=int, default=None,
                     help="block-diagonal J of eq-J-blkdiag with this block size (default: eq-J-diag)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--other-configs", default="1,3,4,5",
+                    help="with the default --config 2 at N=1: also measure these BASELINE configs "
+                         "(comma list, '' = none) and report them under other_configs")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps

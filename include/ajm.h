@@ -17,8 +17,8 @@
  *     is ordered on it.  ajm_create and ajm_solve return only after the stream reaches the end of
  *     their work (their results are host-visible).
  *   - A handle is not thread-safe; distinct handles are independent and may be used from different
- *     host threads at the same time (the solver kernels' launch attributes are set and the kernel
- *     launched under one library lock).
+ *     host threads at the same time: the solver kernels' attributes (shared by every handle of the
+ *     same layout class) are only set, queried and launched with under one library-wide lock.
  *   - On error a call returns a non-zero ajm_status_t and ajm_last_error() explains it; no output
  *     argument is written except where stated.
  */
@@ -31,7 +31,9 @@
 extern "C" {
 #endif
 
-#define AJM_ABI_VERSION 2  /* 2: AJM_D_JBLOCK, ajm_get_jblock, ajm_info_t.l2_mode / launches_per_solve */
+#define AJM_ABI_VERSION 3  /* 2: AJM_D_JBLOCK, ajm_get_jblock, ajm_info_t.l2_mode / launches_per_solve;
+                              3: layout create flags (AJM_INT32_COLUMNS, AJM_GLOBAL_TABLES, AJM_SEGMENTS_*,
+                                 AJM_DEBUG_POISON), ajm_estimate_spectrum, the sharded (row-block) API */
 
 typedef struct ajm_ctx* ajm_handle_t;
 
@@ -72,6 +74,15 @@ typedef enum {
 #define AJM_LOOP_HOST 0x10u        /* debug: one solver-kernel launch per pass, driven by the host,
                                       instead of the single persistent launch (same kernel, same
                                       results bit for bit)                                          */
+/* layout switches (defaults are chosen from the row-length histogram; these force one choice):   */
+#define AJM_INT32_COLUMNS 0x10000u    /* keep int32 SELL columns even when the column offsets col - row
+                                         take <= 256 values (no byte-coded columns; same iterates)     */
+#define AJM_GLOBAL_TABLES 0x20000u    /* per-CTA unit/chunk tables in global memory instead of shared
+                                         memory (what huge layouts use; same iterates)                 */
+#define AJM_SEGMENTS_STATIC 0x40000u  /* rows of > 64 nonzeros: static LPT plan of warp segments        */
+#define AJM_SEGMENTS_DYNAMIC 0x80000u /* ... or a per-pass claim queue (default: dynamic only when long
+                                         rows carry >= 90% of the nonzeros); same iterates either way   */
+#define AJM_DEBUG_POISON 0x100000u    /* debug: fill every device allocation of this create with 0xff   */
 /* block size of AJM_D_JBLOCK, bits 8..15 of the flags: bs in {1, 2, 4, 8, 16, 32} */
 #define AJM_JBLOCK_SIZE(bs) (((uint32_t)(bs) & 0xffu) << 8)
 #define AJM_JBLOCK_SIZE_OF(flags) (((uint32_t)(flags) >> 8) & 0xffu)
@@ -117,15 +128,16 @@ typedef struct {
     int64_t split_rows;       /* rows spanning several segments (finished by an owner CTA)     */
     int64_t sell_elems;       /* SELL entries including padding                                */
     int32_t sigma;            /* SELL sorting window (1 = natural order)                       */
-    int32_t variant;          /* kernel variant (TMA ring depth x register cap)                 */
+    int32_t variant;          /* 0 (one kernel family; kept for layout compatibility)           */
     int64_t l2_window_bytes;  /* iterate vectors covered by the persisting-L2 access window     */
     double l2_hit_ratio;      /* persisting fraction of that window                            */
-    int32_t mode;             /* 0 TMA ring, 1 ring + vector slices, 2 direct SELL loads       */
+    int32_t mode;             /* 0 cooperative grid with a TMA ring, 5 single thread-block cluster */
     int32_t l2_mode;          /* L2 policy: 2 all vectors persist, 3 only the x~ buffers persist */
     int32_t launches_per_solve; /* kernel launches of one ajm_solve (L2 priming + init + solver)   */
     int32_t col_bytes;        /* bytes streamed per SELL column index: 4 (int32), or 1 when the
                                  column offsets col - row take <= 256 values and the layout stores
                                  byte codes into an offset table (stencils)        */
+    int64_t seg_nnz;          /* nonzeros streamed by warp segments (rows of > 64 nonzeros)       */
 } ajm_info_t;
 
 /*
@@ -139,13 +151,16 @@ typedef struct {
  *   b         : double[n], consistent right-hand side (b in range(Q) is assumed, not checked)
  *   dmode     : ajm_dmode_t
  *   d         : double[n] (> 0) for AJM_D_USER, otherwise ignored (may be NULL)
- *   flags     : AJM_VALIDATE_SYMMETRY | AJM_LOOP_HOST | AJM_JBLOCK_SIZE(bs) (AJM_D_JBLOCK only)
+ *   flags     : AJM_VALIDATE_SYMMETRY | AJM_LOOP_HOST | AJM_JBLOCK_SIZE(bs) (AJM_D_JBLOCK only) |
+ *               the layout switches above
  * Ownership: the handle deep-copies (and re-lays-out) Q, b and D into device memory it owns; the
  * caller's buffers may be freed when the call returns.
  * Side effects: device memory comes from a library-owned stream-ordered pool that keeps up to
  * 16 GiB of freed memory for later creates; when the six iterate vectors fit the L2 the call
  * raises the device's cudaLimitPersistingL2CacheSize to min(their size, the device maximum) so a
- * persisting access-policy window can keep them resident (a device-wide setting).
+ * persisting access-policy window can keep them resident (a device-wide setting); when
+ * the last handle that raised it is destroyed the previous limit is restored and the persisting
+ * lines are reset (cudaCtxResetPersistingL2Cache).
  */
 ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t* row_ptr,
                         const int32_t* col_idx, const double* vals, const double* b,

@@ -229,11 +229,18 @@ int oracle_ajm_solve(int64_t n, const int64_t* rp, const int32_t* ci, const doub
     double *x = malloc(bytes), *x_prev = malloc(bytes), *y = malloc(bytes), *xt = malloc(bytes);
     double *qy = malloc(bytes), *qx = malloc(bytes), *qx_prev = malloc(bytes);
     double* part = part_alloc(n);
-    if (!x || !x_prev || !y || !xt || !qy || !qx || !qx_prev || !part) return -3;
+    int rc = 0;
+    if (!x || !x_prev || !y || !xt || !qy || !qx || !qx_prev || !part) {
+        rc = -3; /* allocation failure: free what was allocated (free(NULL) is a no-op) */
+        goto cleanup;
+    }
 
     for (int64_t i = 0; i < n; ++i) x[i] = x0 ? x0[i] : 0.0;
     double nb2 = dot_chunked(n, b, b, part);
-    if (nb2 == 0.0) return -2;
+    if (nb2 == 0.0) {
+        rc = -2;
+        goto cleanup;
+    }
     double nb = sqrt(nb2);
 
     /* t = 0: residual and f of x^0 */
@@ -359,6 +366,7 @@ done:
     info[3] = prerestart;
     info[4] = logged;
     info[5] = 0;
+cleanup:
     free(x); free(x_prev); free(y); free(xt); free(qy); free(qx); free(qx_prev); free(part);
-    return 0;
+    return rc;
 }

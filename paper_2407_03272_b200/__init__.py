@@ -31,6 +31,12 @@ TERM_NAMES = {0: "converged", 1: "maxiter", 2: "diverged"}
 D_MODES = {"jdiag": 0, "user": 1, "qdiag": 2, "jblock": 3}
 AJM_VALIDATE_SYMMETRY = 0x1
 AJM_LOOP_HOST = 0x10
+AJM_INT32_COLUMNS = 0x10000
+AJM_GLOBAL_TABLES = 0x20000
+AJM_SEGMENTS_STATIC = 0x40000
+AJM_SEGMENTS_DYNAMIC = 0x80000
+AJM_DEBUG_POISON = 0x100000
+ABI_VERSION = 3
 
 
 def AJM_JBLOCK_SIZE(bs: int) -> int:
@@ -71,7 +77,8 @@ class ajm_info_t(ctypes.Structure):
                 ("sigma", ctypes.c_int32), ("variant", ctypes.c_int32),
                 ("l2_window_bytes", ctypes.c_int64), ("l2_hit_ratio", ctypes.c_double),
                 ("mode", ctypes.c_int32), ("l2_mode", ctypes.c_int32),
-                ("launches_per_solve", ctypes.c_int32), ("col_bytes", ctypes.c_int32)]
+                ("launches_per_solve", ctypes.c_int32), ("col_bytes", ctypes.c_int32),
+                ("seg_nnz", ctypes.c_int64)]
 
 
 _lib = None
@@ -111,8 +118,12 @@ def lib():
     return _lib
 
 
-def _ptr(a, dtype):
-    """(pointer, keepalive) of a numpy array or torch tensor with the given numpy dtype."""
+def _ptr(a, dtype, output=False):
+    """(pointer, keepalive) of a numpy array or torch tensor with the given numpy dtype.
+
+    Inputs are converted (a contiguous copy of the right dtype) when needed.  Outputs are written
+    by the library in place, so a converted temporary would silently drop the result: an output
+    of the wrong dtype, or not contiguous, raises instead."""
     if a is None:
         return None, None
     try:
@@ -120,10 +131,18 @@ def _ptr(a, dtype):
         if isinstance(a, torch.Tensor):
             tdt = {np.float64: torch.float64, np.int64: torch.int64, np.int32: torch.int32}[dtype]
             if a.dtype != tdt or not a.is_contiguous():
+                if output:
+                    raise TypeError(f"output tensor must be a contiguous {tdt} tensor "
+                                    f"(got {a.dtype}, contiguous={a.is_contiguous()})")
                 a = a.to(tdt).contiguous()
             return ctypes.c_void_p(a.data_ptr()), a
     except ImportError:  # pragma: no cover
         pass
+    if output:
+        if not (isinstance(a, np.ndarray) and a.dtype == np.dtype(dtype) and a.flags.c_contiguous
+                and a.flags.writeable):
+            raise TypeError(f"output array must be a writeable C-contiguous numpy {np.dtype(dtype)} array")
+        return a.ctypes.data_as(ctypes.c_void_p), a
     arr = np.ascontiguousarray(a, dtype=dtype)
     return arr.ctypes.data_as(ctypes.c_void_p), arr
 
@@ -170,10 +189,10 @@ def ajm_solve(handle, x0, tol, maxit, momentum=True, restart=True, k0=2, x_out=N
               res_hist=None, f_hist=None, restart_iters=None, stream=None):
     """Marshal to ajm_solve; returns the ajm_result_t."""
     p0, k_0 = _ptr(x0, np.float64)
-    px, k_x = _ptr(x_out, np.float64)
-    pr, k_r = _ptr(res_hist, np.float64)
-    pf, k_f = _ptr(f_hist, np.float64)
-    pri, k_ri = _ptr(restart_iters, np.int64)
+    px, k_x = _ptr(x_out, np.float64, output=True)
+    pr, k_r = _ptr(res_hist, np.float64, output=True)
+    pf, k_f = _ptr(f_hist, np.float64, output=True)
+    pri, k_ri = _ptr(restart_iters, np.int64, output=True)
     cap = 0 if restart_iters is None else len(restart_iters)
     res = ajm_result_t()
     pol = ajm_policy_t(int(bool(momentum)), int(bool(restart)), int(k0))
@@ -209,13 +228,17 @@ class Solver:
     (device arrays are copied device->device).  The solver owns its device copy afterwards."""
 
     def __init__(self, n, row_ptr, col, val, b, dmode="jdiag", d=None, validate_symmetry=False,
-                 loop="graph", stream=None, jblock=None):
+                 loop="graph", stream=None, jblock=None, int32_columns=False, global_tables=False,
+                 segments="auto", debug_poison=False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2407_03272_b200 needs a CUDA device (no CPU fallback)")
         self.n = int(n)
         self.nnz = int(row_ptr[-1])
         flags = (AJM_VALIDATE_SYMMETRY if validate_symmetry else 0) | (AJM_LOOP_HOST if loop == "host" else 0)
+        flags |= (AJM_INT32_COLUMNS if int32_columns else 0) | (AJM_GLOBAL_TABLES if global_tables else 0)
+        flags |= {"auto": 0, "static": AJM_SEGMENTS_STATIC, "dynamic": AJM_SEGMENTS_DYNAMIC}[segments]
+        flags |= AJM_DEBUG_POISON if debug_poison else 0
         self.jblock = None
         if jblock is not None:  # eq-J-blkdiag with bs-row blocks (AJM_D_JBLOCK)
             dmode = "jblock"

@@ -37,6 +37,7 @@
 namespace {
 
 thread_local std::string g_create_error;
+thread_local bool g_poison = false;  // AJM_DEBUG_POISON during a create (tests)
 
 // NVTX range for the duration of a scope (SURVEY §5 tracing: create / solve / destroy)
 struct NvtxScope {
@@ -45,51 +46,61 @@ struct NvtxScope {
 };
 
 typedef void (*SolveFn)(AjmPass);
-struct SolveVariant {
-    SolveFn fn;   // plain ring (val/col), natural-order layouts
-    int stages;
-    SolveFn fnv;  // ring that also stages the rows' vector slices (natural-order layouts)
-    int vstages;
-    SolveFn fnd;  // no ring: SELL read directly (sorted-window layouts)
-    const char* name;
-    SolveFn fng;  // gather ring (kMode 3): x~ gathers as cp.async into the stage, 1 CTA/SM
-    int gstages;
-    SolveFn fn0;  // as fn, compiled without the segment phases (layouts without long rows)
-};
-// TMA ring depth x register cap (=> resident CTAs per SM with 288 threads; above 96 registers two
-// 9-warp CTAs no longer fit the per-SMSP register files); AJM_KVARIANT selects one (tuning); the
-// default is the measured best on B200
-const SolveVariant kVariants[] = {
-    {ajm_solve_kernel<4, 96, 0>, 4, ajm_solve_kernel<3, 96, 1>, 3, ajm_solve_kernel<1, 128, 2>, "s4r96", ajm_solve_kernel<4, 128, 3>, 4, ajm_solve_kernel<4, 96, 0, false>},    // 2 CTAs/SM
-    {ajm_solve_kernel<3, 72, 0>, 3, ajm_solve_kernel<2, 72, 1>, 2, ajm_solve_kernel<1, 72, 2>, "s3r72", ajm_solve_kernel<3, 128, 3>, 3, ajm_solve_kernel<3, 72, 0, false>},     // 3 CTAs/SM
-    {ajm_solve_kernel<2, 56, 0>, 2, ajm_solve_kernel<2, 56, 1>, 2, ajm_solve_kernel<1, 56, 2>, "s2r56", ajm_solve_kernel<2, 128, 3>, 2, ajm_solve_kernel<2, 56, 0, false>},     // 4 CTAs/SM
-    {ajm_solve_kernel<6, 128, 0>, 6, ajm_solve_kernel<6, 128, 1>, 6, ajm_solve_kernel<1, 128, 2>, "s6r128", ajm_solve_kernel<4, 128, 3>, 4, ajm_solve_kernel<6, 128, 0, false>}, // 1 CTA/SM
-};
-const int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
-// variant-0 ring kernels by ring depth (the depth sets how much of the SM's unified L1/shared
-// memory is left to the L1, which holds the x~ gathers' lines in flight: DESIGN.md §4)
-SolveFn plain_fn(bool seg, int stages) {
+// Solver kernel instantiations (ajm_solve_kernel<stages, kSeg, kCluster, kJB, kGMeta, kCol8>,
+// DESIGN.md §4).  The TMA ring depth sets how much of the SM's unified L1/shared memory is left to
+// the L1, which holds the x~ gathers' lines in flight.
+// int32 columns: ring depth 2-4, with or without the segment phases
+SolveFn ring_fn(bool seg, int stages) {
     switch (stages) {
-        case 2: return seg ? ajm_solve_kernel<2, 96, 0> : ajm_solve_kernel<2, 96, 0, false>;
-        case 3: return seg ? ajm_solve_kernel<3, 96, 0> : ajm_solve_kernel<3, 96, 0, false>;
-        default: return seg ? ajm_solve_kernel<4, 96, 0> : ajm_solve_kernel<4, 96, 0, false>;
+        case 2: return seg ? ajm_solve_kernel<2, true> : ajm_solve_kernel<2, false>;
+        case 3: return seg ? ajm_solve_kernel<3, true> : ajm_solve_kernel<3, false>;
+        default: return seg ? ajm_solve_kernel<4, true> : ajm_solve_kernel<4, false>;
     }
 }
+// byte-coded columns: ring depth 3-6 (18 KB stages)
 SolveFn col8_fn(bool seg, int stages) {
     switch (stages) {
-        case 2: return seg ? ajm_solve_kernel<2, 96, 0, true, false, 0, false, true>
-                           : ajm_solve_kernel<2, 96, 0, false, false, 0, false, true>;
-        case 3: return seg ? ajm_solve_kernel<3, 96, 0, true, false, 0, false, true>
-                           : ajm_solve_kernel<3, 96, 0, false, false, 0, false, true>;
-        case 5: return seg ? ajm_solve_kernel<5, 96, 0, true, false, 0, false, true>
-                           : ajm_solve_kernel<5, 96, 0, false, false, 0, false, true>;
-        case 6: return seg ? ajm_solve_kernel<6, 96, 0, true, false, 0, false, true>
-                           : ajm_solve_kernel<6, 96, 0, false, false, 0, false, true>;
-        default: return seg ? ajm_solve_kernel<4, 96, 0, true, false, 0, false, true>
-                            : ajm_solve_kernel<4, 96, 0, false, false, 0, false, true>;
+        case 3: return seg ? ajm_solve_kernel<3, true, false, 0, false, true> : ajm_solve_kernel<3, false, false, 0, false, true>;
+        case 5: return seg ? ajm_solve_kernel<5, true, false, 0, false, true> : ajm_solve_kernel<5, false, false, 0, false, true>;
+        case 6: return seg ? ajm_solve_kernel<6, true, false, 0, false, true> : ajm_solve_kernel<6, false, false, 0, false, true>;
+        default: return seg ? ajm_solve_kernel<4, true, false, 0, false, true> : ajm_solve_kernel<4, false, false, 0, false, true>;
     }
 }
+// block-diagonal J (natural order, no segments), cooperative grid or single cluster
+SolveFn jblock_fn(int bs, bool cluster) {
+    if (cluster)
+        return bs == 2 ? ajm_solve_kernel<4, false, true, 2> : bs == 4 ? ajm_solve_kernel<4, false, true, 4>
+             : bs == 8 ? ajm_solve_kernel<4, false, true, 8> : ajm_solve_kernel<4, false, true, -1>;
+    return bs == 2 ? ajm_solve_kernel<4, false, false, 2> : bs == 4 ? ajm_solve_kernel<4, false, false, 4>
+         : bs == 8 ? ajm_solve_kernel<4, false, false, 8> : ajm_solve_kernel<4, false, false, -1>;
+}
+SolveFn gmeta_fn(bool seg) { return seg ? ajm_solve_kernel<4, true, false, 0, true> : ajm_solve_kernel<4, false, false, 0, true>; }
+SolveFn cluster_fn(bool seg) { return seg ? ajm_solve_kernel<4, true, true> : ajm_solve_kernel<4, false, true>; }
+
+constexpr int kBlockThreads = AJM_BLOCK + 32;  // consumer warps + the TMA producer warp
+
+// Kernel attributes (max dynamic shared memory, carve-out) belong to the kernel, which every handle
+// of that layout shares: they are set -- and occupancy is queried -- under one library-wide lock,
+// and each launch sets its own handle's values and launches before releasing it.
+std::mutex g_attr_mu;
+
+// set the attributes of fn and return the resident CTAs per SM (0 on failure); caller holds g_attr_mu
+cudaError_t fn_occupancy(SolveFn fn, size_t dyn_smem, int carveout, int* occ) {
+    cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, fn, kBlockThreads, dyn_smem);
+    return e;
+}
+
+// Persisting-L2 limit: raised by creates whose vectors fit the L2 and restored (with the
+// persisting lines reset) when the last such handle is destroyed, so no handle's L2 state leaks
+// into later work.
+struct PersistState {
+    int holders = 0;
+    size_t saved_limit = 0;
+};
+PersistState g_persist[64];
 
 }  // namespace
 
@@ -99,21 +110,16 @@ struct ajm_ctx {
     int ctas_per_sm = 0;
     int64_t n = 0, nnz = 0, n_pad = 0;
     int64_t nchunks = 0, n_sell = 0, sell_elems = 0;
-    int64_t nseg = 0, nsplit = 0, seg_rows = 0, long_rows = 0;
+    int64_t nseg = 0, nsplit = 0, seg_rows = 0, long_rows = 0, seg_nnz = 0;
     int sigma = 1;
-    bool ident = true;
     bool relabel = false;           // SELL slot order != caller's row order: vectors live in slot order
     int* perm_fwd = nullptr;        // [n] internal (layout) index -> caller's row
     int* perm_inv = nullptr;        // [n] caller's row -> internal index
-    int variant = 0;
     SolveFn fn = nullptr;
     size_t dyn_smem = 0;
     int64_t nunits = 0;
     int meta_units = 0, meta_chunks = 0;
     int l2_mode = 2;
-    int vstage = 0;
-    int direct = 0;
-    int gring = 0;                     // kMode 3 gather ring
     int cluster = 0;                   // grid <= 16 CTAs launched as one cluster (DSMEM barrier)
     int gmeta = 0;                     // per-CTA unit/chunk tables in global memory (huge layouts)
     int* g_uc0 = nullptr;
@@ -123,6 +129,7 @@ struct ajm_ctx {
     unsigned long long* ts = nullptr;  // debug phase timestamps (AJM_TS=1)
     double* vecs = nullptr;            // X0 X1 X2 Qxp b D, one allocation
     int l2persist = 1;
+    bool persist_holder = false;       // this handle raised the device's persisting-L2 limit
     size_t win_bytes = 0;
     float win_hit = 0.f;
     size_t prime_bytes = 0;  // (l2_mode 3) window over all six vectors for the per-solve L2 priming
@@ -140,7 +147,6 @@ struct ajm_ctx {
     double* sval = nullptr;
     int* scol = nullptr;
     long long* chunk_off = nullptr;
-    int* perm = nullptr;
     int* seg_row = nullptr;
     int* seg_k0 = nullptr;
     int* seg_k1 = nullptr;
@@ -177,7 +183,7 @@ struct ajm_ctx {
     int col_bytes = 4;          // bytes per streamed column index: 4 (int32) or 1 (byte code)
     int ring_stages = 4;        // TMA ring depth of the chosen solver kernel
     bool seg_fn = true;         // the chosen plain/col8 ring kernel has the segment phases
-    bool ring_fn = false;       // h->fn is a plain_fn/col8_fn kernel (ring depth selectable)
+    bool ring_fn = false;       // h->fn is a ring_fn/col8_fn kernel (ring depth selectable)
     bool wide_rows = false;     // SELL chunks average >= 16 entries per row
     size_t meta_bytes = 0;      // shared-memory unit/chunk tables behind the ring
     int carveout = 100;         // preferred shared-memory carve-out (%), set before every launch
@@ -269,7 +275,7 @@ cudaError_t dalloc(T** p, size_t count, cudaStream_t s) {
     cudaError_t e = cudaMallocFromPoolAsync((void**)p, bytes, mp, s);
     // AJM_POISON (tests): fill new allocations with 0xff so a read of memory the library never
     // wrote shows up deterministically instead of depending on what the pool hands back
-    if (e == cudaSuccess && getenv("AJM_POISON")) cudaMemsetAsync(*p, 0xff, bytes, s);
+    if (e == cudaSuccess && g_poison) cudaMemsetAsync(*p, 0xff, bytes, s);
     return e;
 }
 
@@ -279,12 +285,26 @@ void dfree(void* p) {
 
 void free_all(ajm_ctx* h) {
     void* ptrs[] = {h->rp, h->col, h->val, h->vecs,
-                    h->sval, h->scol, h->chunk_off, h->perm, h->seg_row, h->seg_k0, h->seg_k1,
+                    h->sval, h->scol, h->chunk_off, h->seg_row, h->seg_k0, h->seg_k1,
                     h->seg_split, h->seg_part, h->split_row, h->split_seg0, h->split_cnt,
                     h->cta_split, h->owner_split, h->unit_c0, h->cta_seg, h->seg_list, h->cta_unit, h->partials, h->ctrl,
                     h->hist, h->scratch, h->err, h->ts, h->perm_fwd, h->perm_inv, h->b_in, h->Jblk, h->Jinv, h->seg_order, h->seg_grp,
                     h->g_uc0, h->g_coff, h->g_ubase, h->g_cbase, h->scode, h->ctab, h->seg_meta};
     for (void* p : ptrs) dfree(p);
+    if (h->persist_holder) {  // the last holder restores the limit and drops the persisting lines
+        std::lock_guard<std::mutex> lock(g_attr_mu);
+        PersistState& ps = g_persist[h->device];
+        if (--ps.holders == 0) {
+            int cur_dev = 0;
+            cudaGetDevice(&cur_dev);
+            if (cur_dev != h->device) cudaSetDevice(h->device);
+            cudaCtxResetPersistingL2Cache();
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, ps.saved_limit);
+            if (cur_dev != h->device) cudaSetDevice(cur_dev);
+            cudaGetLastError();
+        }
+        h->persist_holder = false;
+    }
     if (h->h_ctrl) free(h->h_ctrl);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
@@ -298,7 +318,6 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.sval = h->sval;
     p.scol = h->scol;
     p.chunk_off = h->chunk_off;
-    p.perm = h->perm;
     p.seg_row = h->seg_row;
     p.seg_k0 = h->seg_k0;
     p.seg_k1 = h->seg_k1;
@@ -327,14 +346,11 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.ctrl = h->ctrl;
     p.n = (int)h->n;
     p.n_sell = (int)h->n_sell;
-    p.ident = h->ident ? 1 : 0;
     p.max_passes = max_passes;
     p.meta_units = h->meta_units;
     p.meta_chunks = h->meta_chunks;
     p.l2_mode = h->l2_mode;
-    p.vstage = h->vstage;
     p.ts = h->ts;
-    p.bid_rev = getenv("AJM_BID_REV") ? atoi(getenv("AJM_BID_REV")) : 0;
     p.g_uc0 = h->g_uc0;
     p.g_coff = h->g_coff;
     p.g_ubase = h->g_ubase;
@@ -344,27 +360,22 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.scode = h->scode;
     p.seg_meta = reinterpret_cast<const int4*>(h->seg_meta);
     p.ctab = h->ctab;
-    p.direct_interleave = getenv("AJM_DIRECT_INTERLEAVE") ? atoi(getenv("AJM_DIRECT_INTERLEAVE")) : 0;
     return p;
 }
-
-// consumer warps + producer warp (+ gather warp in kMode 3); direct mode has no producer
-int block_threads(const ajm_ctx* h) { return h->direct ? AJM_BLOCK : (h->gring ? AJM_BLOCK + 32 + 32 * AJM_GWARPS : AJM_BLOCK + 32); }
 
 // cooperative launch of the persistent solver kernel, with the L2 access-policy window over the
 // iterate vectors (persisting hits, streaming misses)
 cudaError_t launch_solver(ajm_ctx* h, AjmPass& p, cudaStream_t st) {
     // the attributes belong to the kernel, which other handles share: set this handle's own, and
     // launch before another thread's handle can change them (the launch itself is asynchronous)
-    static std::mutex mu;
-    std::lock_guard<std::mutex> lock(mu);
+    std::lock_guard<std::mutex> lock(g_attr_mu);
     cudaError_t e = cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributePreferredSharedMemoryCarveout, h->carveout);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(h->grid);
-    cfg.blockDim = dim3(block_threads(h));
+    cfg.blockDim = dim3(kBlockThreads);
     cfg.dynamicSmemBytes = h->dyn_smem;
     cfg.stream = st;
     cudaLaunchAttribute at[2];
@@ -419,6 +430,8 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
                         const double* d, uint32_t flags, void* cuda_stream) {
     NvtxScope nvtx_scope_("ajm_create");
     g_create_error.clear();
+    g_poison = (flags & AJM_DEBUG_POISON) != 0;
+    struct PoisonReset { ~PoisonReset() { g_poison = false; } } poison_reset_;
     // debug (AJM_TS): host wall time of each create phase
     const bool tsc = getenv("AJM_TS") != nullptr;
     auto t_last = std::chrono::steady_clock::now();
@@ -492,21 +505,12 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     int coop = 0;
     CC(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device));
     if (!coop) return bail(fail(h, AJM_ERR_UNSUPPORTED, "device does not support cooperative launch"));
-    if (const char* ev = getenv("AJM_KVARIANT")) h->variant = std::max(0, std::min(kNumVariants - 1, atoi(ev)));
-    h->fn = kVariants[h->variant].fn;
-    int l2_env = -1;
-    if (const char* ev = getenv("AJM_L2MODE")) l2_env = std::max(0, std::min(3, atoi(ev)));
-    if (const char* ev = getenv("AJM_VSTAGE")) h->vstage = atoi(ev) ? 1 : 0;
-    if (const char* ev = getenv("AJM_L2PERSIST")) h->l2persist = atoi(ev) ? 1 : 0;
-    CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fnv, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fnd, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fng, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CC(cudaFuncSetAttribute((const void*)kVariants[h->variant].fn0, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CC(cudaFuncSetAttribute((const void*)ajm_solve_kernel<4, 96, 4, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CC(cudaFuncSetAttribute((const void*)ajm_solve_kernel<4, 96, 4, false, false, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CC(cudaFuncSetAttribute((const void*)ajm_solve_kernel<4, 96, 4, false, false, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CC(cudaFuncSetAttribute((const void*)ajm_solve_kernel<4, 96, 4, false, false, 8>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    // experiment overrides, read once per create (never per solve): AJM_STAGES / AJM_COL8_STAGES
+    // (ring depth), AJM_CARVEOUT (%), AJM_NO_CLUSTER; the supported layout switches are create flags
+    const int env_stages = getenv("AJM_STAGES") ? atoi(getenv("AJM_STAGES")) : 0;
+    const int env_col8_stages = getenv("AJM_COL8_STAGES") ? atoi(getenv("AJM_COL8_STAGES")) : 0;
+    const int env_carveout = getenv("AJM_CARVEOUT") ? atoi(getenv("AJM_CARVEOUT")) : -1;
+    const bool env_no_cluster = getenv("AJM_NO_CLUSTER") != nullptr;
 
     // ---- the CSR arrays and b go to the device now; the copies overlap the host planning ----
     CC(dalloc(&h->rp, n + 1, st));
@@ -580,7 +584,6 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             h->n_sell = n;
             h->nchunks = nch;
             h->relabel = false;
-            h->ident = true;
             choff.swap(fo);
             chcost.swap(fc);
             h->sell_elems = choff.back();
@@ -591,7 +594,6 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     }
     if (!fast) {
         int64_t seg_len = AJM_SEG;  // nonzeros per warp segment (AJM_SEGLEN: tuning experiments)
-        if (const char* ev = getenv("AJM_SEGLEN")) seg_len = std::max<int64_t>(AJM_SELL_MAX + 1, atoll(ev));
         std::vector<int> short_rows, split_rows, whole_rows;
         short_rows.reserve((size_t)n);
         // dynamic segment queue when long rows carry >= 90% of the nonzeros (e.g. the §4.1 dense
@@ -603,7 +605,8 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             for (int64_t i = 0; i < n; ++i)
                 if (rlen(i) > AJM_SELL_MAX) long_nnz += rlen(i);
             h->dynseg = (double)long_nnz >= 0.9 * (double)std::max<int64_t>(nnz, 1) ? 1 : 0;
-            if (const char* ev = getenv("AJM_DYNSEG")) h->dynseg = atoi(ev) ? 1 : 0;
+            if (flags & AJM_SEGMENTS_STATIC) h->dynseg = 0;
+            if (flags & AJM_SEGMENTS_DYNAMIC) h->dynseg = 1;
         }
         {
             // per-thread bins over contiguous row ranges, concatenated in thread order (so every
@@ -689,7 +692,6 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         // chunk is contiguous (coalesced / TMA-stageable) whatever the sorting window.  Values
         // and the order of each row's entries are unchanged (the row sums are the same).
         h->relabel = !(h->sigma == 1 && split_rows.empty() && whole_rows.empty());
-        h->ident = true;  // SELL slot == internal row
         perm_h.assign((size_t)n, 0);
         const int64_t nord = (int64_t)order.size();
 #pragma omp parallel for schedule(static)
@@ -714,11 +716,10 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         // only S * floor(64 / w) of the CTA's 8 warps busy: weight such chunks by the idle share
         // (config 4: the first sorted windows hold the 40-64-wide rows, and the CTAs planned on
         // them finished ~90 us after the median)
-        const double par_stages = getenv("AJM_COST_PAR") && !atoi(getenv("AJM_COST_PAR")) ? 0.0 : (h->relabel ? 3.0 : 4.0);
+        const double par_stages = h->relabel ? 3.0 : 4.0;
         // softened to (8 / busy)^0.5: config 4 495 -> 444 us/pass, config 3 79.1 -> 79.7 (exponent
         // 1: 452 / 81.0; 0.7: 440 / 80.3; the idle-share weight on one-chunk units only: 452 / 79.1)
-        const double par_alpha = getenv("AJM_COST_ALPHA") ? atof(getenv("AJM_COST_ALPHA")) : 0.5;
-        const bool par_only1 = getenv("AJM_COST_ONLY1") && atoi(getenv("AJM_COST_ONLY1"));
+        const double par_alpha = 0.5;
 #pragma omp parallel for schedule(static)
         for (int64_t c = 0; c < nchk_h; ++c) {
             int64_t w = 1, rows = 0;
@@ -727,9 +728,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
                 ++rows;
             }
             choff[(size_t)c + 1] = 32 * w;
-            double busy = par_stages > 0.0 ? std::min<double>(AJM_WARPS, par_stages * std::max<int64_t>(1, AJM_UNIT_EL / (32 * w)))
-                                            : (double)AJM_WARPS;
-            if (par_only1 && AJM_UNIT_EL / (32 * w) >= 2) busy = AJM_WARPS;
+            const double busy = std::min<double>(AJM_WARPS, par_stages * std::max<int64_t>(1, AJM_UNIT_EL / (32 * w)));
             chcost[(size_t)c] = (12.0 * 32 * w + 56.0 * rows + 64.0) * std::pow((double)AJM_WARPS / busy, par_alpha);
         }
         for (int64_t c = 0; c < nchk_h; ++c) choff[(size_t)c + 1] += choff[(size_t)c];
@@ -762,6 +761,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         }
         if (h->dynseg) split_seg0_h.push_back((int)seg_row_h.size());
         h->nseg = (int64_t)seg_row_h.size();
+        for (int64_t k = 0; k < h->nseg; ++k) h->seg_nnz += seg_k1_h[(size_t)k] - seg_k0_h[(size_t)k];
         h->nsplit = (int64_t)split_row_h.size();
         h->seg_rows = (int64_t)(split_rows.size() + whole_rows.size());
         if (h->relabel) {
@@ -784,7 +784,6 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         // claim groups: consecutive segments of the order with >= seg_group_nnz nonzeros (<= 16
         // segments), so the queue costs one atomic per ~1k nonzeros, not per short row
         int64_t gnnz = 1024;
-        if (const char* ev = getenv("AJM_SEGGROUP")) gnnz = std::max<int64_t>(1, atoll(ev));
         int64_t acc = 0, cntg = 0;
         seg_grp_h.push_back(0);
         for (int64_t k = 0; k < h->nseg; ++k) {
@@ -806,8 +805,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         std::vector<double> cost;
         cost.reserve((size_t)nitems);
         // segments are latency-bound (one warp, direct loads): weight their bytes twice
-        const double segw = getenv("AJM_SEGW") ? atof(getenv("AJM_SEGW")) : 24.0;  // (experiment knobs)
-        const double segc = getenv("AJM_SEGC") ? atof(getenv("AJM_SEGC")) : 568.0;
+        const double segw = 24.0, segc = 568.0;
         for (int64_t s2 = 0; s2 < h->nseg; ++s2)  // (dynamic segments are outside the static plan)
             cost.push_back(h->dynseg ? 0.0 : segw * (seg_k1_h[(size_t)s2] - seg_k0_h[(size_t)s2]) + segc);
         for (int64_t c2 = 0; c2 < h->nchunks; ++c2) cost.push_back(chcost[(size_t)c2]);
@@ -901,56 +899,26 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             h->meta_units = (mu + 3) & ~3;
             h->meta_chunks = (mc + 3) & ~3;
         };
-        if (!h->ident) h->vstage = 0;
-        h->direct = 0;  // direct mode measured slower than the ring on every config so far
-        if (const char* ev = getenv("AJM_DIRECT")) h->direct = atoi(ev) ? 1 : 0;
         const double avg_w = h->nchunks ? (double)h->sell_elems / (32.0 * (double)h->nchunks) : 0.0;
-        // no long rows: the variant without the segment phases (its ring loop has more registers to
-        // spare: config 2 47.5 -> 45.5 us/pass, config 3 81.5 -> 76.2; config 5 with int32 columns
-        // 1197 vs 1200, even)
-        if (h->nseg == 0 && !h->vstage && !getenv("AJM_NO_NOSEG")) h->fn = kVariants[h->variant].fn0;
         h->wide_rows = avg_w >= 16.0;
-        if (const char* ev = getenv("AJM_GRING")) h->gring = atoi(ev) ? 1 : 0;
-        if (h->vstage) h->fn = kVariants[h->variant].fnv;
+        int ring_stages = 4;
         if (h->jbs) {  // block-diagonal J: its own instantiation (natural order, no segments)
-            h->gring = 0;
-            h->direct = 0;
-            h->vstage = 0;
-            h->fn = h->jbs == 2 ? ajm_solve_kernel<4, 96, 4, false, false, 2>
-                  : h->jbs == 4 ? ajm_solve_kernel<4, 96, 4, false, false, 4>
-                  : h->jbs == 8 ? ajm_solve_kernel<4, 96, 4, false, false, 8>
-                                : ajm_solve_kernel<4, 96, 4, false>;
-        }
-        if (h->gring) {
-            h->fn = kVariants[h->variant].fng;
-            h->vstage = 0;
-            h->direct = 0;
-        }
-        if (h->direct) {
-            h->fn = kVariants[h->variant].fnd;
-            h->vstage = 0;
-        }
-        // ring depth of the variant-0 ring kernels: a shallower ring leaves more of the SM's
-        // unified L1/shared memory to the L1; AJM_STAGES=2|3|4 overrides
-        int ring_stages = h->vstage ? kVariants[h->variant].vstages : kVariants[h->variant].stages;
-        if (h->variant == 0 && (h->fn == kVariants[0].fn || h->fn == kVariants[0].fn0)) {
-            h->seg_fn = h->fn == kVariants[0].fn;
-            h->ring_fn = true;
+            h->fn = jblock_fn(h->jbs, false);
+        } else {
+            // without long rows the instantiation without the segment phases (its ring loop has more
+            // registers to spare: config 2 47.5 -> 45.5 us/pass, config 3 81.5 -> 76.2).  Ring depth:
             // 3 stages and the L1 they free win where the gathers are scattered (sorted-window graph
             // layouts: config 3 135 -> 82, config 4 880 -> 535 us/pass) and on narrow natural-order
             // rows (config 2 int32: 45.7 -> 44.7); natural-order wide rows (units of 2-3 chunks) keep
-            // 4 (config 5 int32: 1189 vs 1350 at 3)
-            int sv = (!h->relabel && avg_w >= 16.0) ? 4 : 3;
-            if (const char* ev = getenv("AJM_STAGES")) sv = std::min(4, std::max(2, atoi(ev)));
-            h->fn = plain_fn(h->seg_fn, sv);
-            ring_stages = sv;
-            CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            // 4 (config 5 int32: 1189 vs 1350 at 3) (DESIGN.md §4)
+            h->seg_fn = h->nseg > 0;
+            h->ring_fn = true;
+            ring_stages = (!h->relabel && avg_w >= 16.0) ? 4 : 3;
+            if (env_stages) ring_stages = std::min(4, std::max(2, env_stages));
+            h->fn = ring_fn(h->seg_fn, ring_stages);
         }
         h->ring_stages = ring_stages;
-        // ring: val/col of a unit (+ the rows' five vector slices for natural-order layouts)
-        size_t ring = h->direct ? 0 : h->gring ? (size_t)kVariants[h->variant].gstages * ((size_t)AJM_UNIT_EL * 20 + (size_t)5 * AJM_UNIT_ROWS * 8)
-                          : (size_t)ring_stages *
-                            ((size_t)AJM_UNIT_EL * 12 + (h->vstage ? (size_t)5 * AJM_UNIT_ROWS * 8 : 0));
+        size_t ring = (size_t)ring_stages * AJM_UNIT_EL * 12;  // val/col of a unit per stage
         size_t meta = 4096;  // initial allowance, grown until the plan fits
         int smem_optin = 0;
         CC(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
@@ -958,29 +926,29 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         int planned_grid = -1;
         for (int iter = 0;; ++iter) {
             // tables too large for shared memory next to the ring: read them from global memory
-            if (!h->gmeta && (ring + meta + 2048 > (size_t)smem_optin || getenv("AJM_FORCE_GMETA")) && !h->direct &&
-                !h->gring && !h->vstage && !h->jbs) {
+            if (!h->gmeta && !h->jbs && (ring + meta + 2048 > (size_t)smem_optin || (flags & AJM_GLOBAL_TABLES))) {
                 h->gmeta = 1;
-                h->fn = h->nseg == 0 ? ajm_solve_kernel<4, 96, 0, false, false, 0, true>
-                                     : ajm_solve_kernel<4, 96, 0, true, false, 0, true>;
+                h->fn = gmeta_fn(h->nseg > 0);
                 h->ring_fn = false;
                 h->ring_stages = 4;
                 ring = (size_t)4 * AJM_UNIT_EL * 12;
-                CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
             }
             h->dyn_smem = ring + (h->gmeta ? 0 : meta);
             h->meta_bytes = h->gmeta ? 0 : meta;
-            CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem));
             int occ = 0;
-            CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->fn, block_threads(h),
-                                                             h->dyn_smem));
+            cudaError_t eo;
+            {
+                std::lock_guard<std::mutex> lock(g_attr_mu);
+                eo = fn_occupancy(h->fn, h->dyn_smem, 100, &occ);
+            }
+            CC(eo);
             if (occ < 1) return bail(fail(h, AJM_ERR_UNSUPPORTED, "solver kernel cannot be resident (%zu B smem)", h->dyn_smem));
             h->ctas_per_sm = occ;
             const int64_t g = (int64_t)h->sm_count * occ;
             h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(g, nitems));
             // <= 128 work items: one item per consumer warp on <= 16 CTAs, launched below as a
             // single cluster whose barrier lives in distributed shared memory
-            if (nitems <= 16 * AJM_WARPS && h->variant == 0 && !getenv("AJM_NO_CLUSTER"))
+            if (nitems <= 16 * AJM_WARPS && !env_no_cluster)
                 h->grid = (int)std::max<int64_t>(1, (nitems + AJM_WARPS - 1) / AJM_WARPS);
             if (h->grid != planned_grid) {  // plan() depends on the grid size only
                 plan(h->grid);
@@ -994,41 +962,35 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         mark("P-loop", (cudaStream_t)-1);
         const int G = h->grid;
         // small problems: the grid as ONE thread-block cluster, barrier and partial exchange in
-        // distributed shared memory (variant 0 kernels only; AJM_NO_CLUSTER disables)
-        if (G <= 16 && h->variant == 0 && !h->direct && !h->gring && !h->vstage && !getenv("AJM_NO_CLUSTER")) {
-            SolveFn cf = nullptr;
-            if (h->jbs) cf = h->jbs == 2 ? ajm_solve_kernel<4, 96, 4, false, true, 2>
-                           : h->jbs == 4 ? ajm_solve_kernel<4, 96, 4, false, true, 4>
-                           : h->jbs == 8 ? ajm_solve_kernel<4, 96, 4, false, true, 8>
-                                         : ajm_solve_kernel<4, 96, 4, false, true>;
-            else if (h->ring_fn) cf = h->seg_fn ? ajm_solve_kernel<4, 96, 0, true, true> : ajm_solve_kernel<4, 96, 0, false, true>;
+        // distributed shared memory (AJM_NO_CLUSTER disables, for experiments)
+        if (G <= 16 && !env_no_cluster && (h->jbs || h->ring_fn)) {
+            const SolveFn cf = h->jbs ? jblock_fn(h->jbs, true) : cluster_fn(h->seg_fn);
             // (the cluster kernels keep a 4-deep ring: per-pass latency, not L1, bounds them)
             const size_t cdyn = h->ring_fn ? (size_t)4 * AJM_UNIT_EL * 12 + h->meta_bytes : h->dyn_smem;
-            if (cf) {
-                cudaFuncSetAttribute((const void*)cf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cdyn);
-                cudaFuncSetAttribute((const void*)cf, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-                if (G > 8) cudaFuncSetAttribute((const void*)cf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-                cudaLaunchConfig_t qc = {};
-                qc.gridDim = dim3(G);
-                qc.blockDim = dim3(block_threads(h));
-                qc.dynamicSmemBytes = cdyn;
-                cudaLaunchAttribute qa[1];
-                qa[0].id = cudaLaunchAttributeClusterDimension;
-                qa[0].val.clusterDim.x = (unsigned)G;
-                qa[0].val.clusterDim.y = 1;
-                qa[0].val.clusterDim.z = 1;
-                qc.attrs = qa;
-                qc.numAttrs = 1;
-                int ncl = 0;
-                if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)cf, &qc) == cudaSuccess && ncl >= 1) {
-                    h->fn = cf;
-                    h->cluster = 1;
-                    h->dyn_smem = cdyn;
-                    if (h->ring_fn) h->ring_stages = 4;
-                    h->ring_fn = false;
-                }
-                cudaGetLastError();
+            std::lock_guard<std::mutex> lock(g_attr_mu);
+            cudaFuncSetAttribute((const void*)cf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cdyn);
+            cudaFuncSetAttribute((const void*)cf, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            if (G > 8) cudaFuncSetAttribute((const void*)cf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            cudaLaunchConfig_t qc = {};
+            qc.gridDim = dim3(G);
+            qc.blockDim = dim3(kBlockThreads);
+            qc.dynamicSmemBytes = cdyn;
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = (unsigned)G;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            qc.attrs = qa;
+            qc.numAttrs = 1;
+            int ncl = 0;
+            if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)cf, &qc) == cudaSuccess && ncl >= 1) {
+                h->fn = cf;
+                h->cluster = 1;
+                h->dyn_smem = cdyn;
+                if (h->ring_fn) h->ring_stages = 4;
+                h->ring_fn = false;
             }
+            cudaGetLastError();
         }
         mark("P-cluster", (cudaStream_t)-1);
         // owner of a split row = the CTA that runs its last segment
@@ -1068,7 +1030,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     const size_t vec_bytes = sizeof(double) * 6 * (size_t)h->n_pad;
     // vectors larger than the whole L2 (configs 4, 5): a persisting carve-out only takes L2 away
     // from everything else (measured 1138 -> 919 us/pass on config 4): eviction hints only
-    if (vec_bytes > (size_t)l2size && l2_env < 0 && !getenv("AJM_FORCE_WINDOW")) {
+    if (vec_bytes > (size_t)l2size) {
         h->l2persist = 0;
         h->l2_mode = 3;
     }
@@ -1077,34 +1039,41 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         CC(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device));
         CC(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, h->device));
         if (maxp > 0 && maxw > 0) {
-            size_t persist = std::min<size_t>((size_t)maxp, vec_bytes);
+            const size_t persist = std::min<size_t>((size_t)maxp, vec_bytes);
             size_t cur = 0;
-            CC(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
-            if (cur < persist) CC(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
-            CC(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+            cudaError_t el;
+            {   // raise the device limit; the first holder remembers the value to restore at destroy
+                std::lock_guard<std::mutex> lock(g_attr_mu);
+                PersistState& ps = g_persist[h->device];
+                el = cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+                if (el == cudaSuccess && ps.holders == 0) ps.saved_limit = cur;
+                if (el == cudaSuccess && cur < persist) el = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist);
+                if (el == cudaSuccess) el = cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+                if (el == cudaSuccess) {
+                    ps.holders += 1;
+                    h->persist_holder = true;
+                }
+            }
+            CC(el);
             // mode 2: all six vectors in the window (they fit 3/4 of the carve-out: config 3);
             // mode 3: only the three rotating iterate buffers X0..X2 (the gathered x~ lives there),
             // b, D, Qx streamed with evict_first
             h->l2_mode = (double)vec_bytes <= 0.75 * (double)maxp ? 2 : 3;
-            if (l2_env >= 0) h->l2_mode = l2_env;
             const size_t wb = h->l2_mode == 3 ? sizeof(double) * 3 * (size_t)h->n_pad : vec_bytes;
             h->win_bytes = std::min<size_t>(wb, (size_t)maxw);
             h->win_hit = (float)std::min(1.0, (double)cur / (double)h->win_bytes);
             // mode 3 on vectors that fit the L2 (config 2): before each solve one touch pass over
             // all six vectors under a window covering them (the carve-out's share persists), then
             // the solver's own window keeps the x~ buffers at hit ratio 1 (55.3 -> 47.0 us/pass)
-            if (h->l2_mode == 3 && vec_bytes <= (size_t)l2size && !getenv("AJM_NO_PRIME")) {
+            if (h->l2_mode == 3 && vec_bytes <= (size_t)l2size) {
                 h->prime_bytes = std::min<size_t>(vec_bytes, (size_t)maxw);
                 h->prime_hit = (float)std::min(1.0, (double)cur / (double)h->prime_bytes);
             }
         }
-    } else if (l2_env >= 0) {
-        h->l2_mode = l2_env;
     }
     CC(dalloc(&h->sval, h->sell_elems, st));
     CC(dalloc(&h->scol, h->sell_elems, st));
     CC(dalloc(&h->chunk_off, h->nchunks + 1, st));
-    CC(dalloc(&h->perm, 1, st));
     CC(dalloc(&h->seg_row, h->nseg, st));
     CC(dalloc(&h->seg_k0, h->nseg, st));
     CC(dalloc(&h->seg_k1, h->nseg, st));
@@ -1283,8 +1252,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     // byte-coded columns: when the offsets col - row of the SELL entries take at most
     // AJM_CTAB distinct values (stencils: 7 / 27), stream one byte per entry instead of an int32
     // column (12 -> 9 bytes per stored entry) -- plain-ring variant-0 layouts only
-    if (h->nchunks > 0 && h->ident && h->ring_fn && !h->cluster && !h->gmeta && !h->direct && !h->gring &&
-        !h->vstage && !h->jbs && !getenv("AJM_NO_COL8")) {
+    if (h->nchunks > 0 && h->ring_fn && !h->cluster && !h->gmeta && !h->jbs && !(flags & AJM_INT32_COLUMNS)) {
         const int ns = (int)(h->nchunks * 32);
         int* tmp = nullptr;
         CC(dalloc(&tmp, AJM_CTAB_HASH + 2, st));
@@ -1299,19 +1267,22 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         // ring depth of the byte-coded kernels (18 KB stages): stencils' gathers hit L1 anyway, so
         // the depth goes to the ring -- 4 for narrow rows (config 2: 43.7 -> 43.0 us/pass vs 3), 5
         // for wide ones, whose units hold only 2-3 chunks (config 5: 1414 / 1139 / 1126 us/pass
-        // at 3 / 4 / 5); AJM_COL8_STAGES=2..6 overrides
+        // at 3 / 4 / 5); AJM_COL8_STAGES=3..6 overrides (experiments)
         // Without warp segments the byte-coded kernel is always the variant compiled without the
         // segment phases (config 5: 1104 -> 1088 us/pass; the int32 layouts keep the seg variant
         // for wide rows, where it measured faster)
         int st8 = h->wide_rows ? 5 : 4;
-        if (const char* es = getenv("AJM_COL8_STAGES")) st8 = std::min(6, std::max(2, atoi(es)));
+        if (env_col8_stages) st8 = std::min(6, std::max(3, env_col8_stages));
         SolveFn f8 = col8_fn(h->nseg > 0, st8);
         const size_t dyn8 = (size_t)st8 * AJM_UNIT_EL * 9 + h->meta_bytes;
         int occ8 = 0;
         if (htab[AJM_CTAB_HASH + 1] == 0 && htab[AJM_CTAB_HASH] <= AJM_CTAB) {
-            CC(cudaFuncSetAttribute((const void*)f8, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-            CC(cudaFuncSetAttribute((const void*)f8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn8));
-            CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ8, f8, block_threads(h), dyn8));
+            cudaError_t eo;
+            {
+                std::lock_guard<std::mutex> lock(g_attr_mu);
+                eo = fn_occupancy(f8, dyn8, 100, &occ8);
+            }
+            CC(eo);
         }
         if (occ8 >= h->ctas_per_sm && occ8 > 0) {
             std::vector<int> keys;
@@ -1346,16 +1317,19 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         CC(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device));
         const double need = (double)h->ctas_per_sm * ((double)h->dyn_smem + (double)fa.sharedSizeBytes + 1024.0);
         int pct = (int)std::ceil(100.0 * need / std::max(1, smem_sm)) + 1;
-        if (const char* ev = getenv("AJM_CARVEOUT")) pct = atoi(ev);
+        if (env_carveout >= 0) pct = env_carveout;
         pct = std::min(100, std::max(0, pct));
-        CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem));
-        CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         int occ = 0;
-        CC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->fn, block_threads(h), h->dyn_smem));
-        if (occ < h->ctas_per_sm && !h->cluster) {
-            pct = 100;
-            CC(cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        cudaError_t eo;
+        {
+            std::lock_guard<std::mutex> lock(g_attr_mu);
+            eo = fn_occupancy(h->fn, h->dyn_smem, pct, &occ);
+            if (eo == cudaSuccess && occ < h->ctas_per_sm && !h->cluster) {
+                pct = 100;
+                eo = cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+            }
         }
+        CC(eo);
         h->carveout = pct;
     }
     // ||b||
@@ -1604,14 +1578,15 @@ ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info) {
     info->seg_rows = h->seg_rows;
     info->split_rows = h->nsplit;
     info->sigma = h->sigma;
-    info->variant = h->variant;
+    info->variant = 0;
     info->l2_window_bytes = (int64_t)h->win_bytes;
     info->l2_hit_ratio = h->win_hit;
-    info->mode = h->gring ? 3 : h->direct ? 2 : h->vstage ? 1 : (h->cluster ? 5 : 0);
+    info->mode = h->cluster ? 5 : 0;
     info->sell_elems = h->sell_elems;
     info->l2_mode = h->l2_mode;
     info->launches_per_solve = (int32_t)(1 + (h->prime_bytes ? 1 : 0) + std::max<int64_t>(h->last_launches, 1));
     info->col_bytes = h->col_bytes;
+    info->seg_nnz = h->seg_nnz;
     return AJM_OK;
 }
 

@@ -41,7 +41,6 @@
 #define AJM_UNIT_EL 2048 // SELL elements per TMA staging unit (24 KB of val + col)
 #define AJM_UNIT_ROWS (AJM_WARPS * 32)  // rows per staging unit (<= 8 chunks)
 #define AJM_LOG_CAP 64
-#define AJM_GWARPS 4     // gather warps per CTA in kMode 3
 #define AJM_CTAB 256     // byte-coded columns: at most this many distinct offsets col - row
 #define AJM_CTAB_HASH 2048  // create-time hash set of the offsets
 
@@ -88,7 +87,6 @@ struct AjmPass {
     const double* __restrict__ sval;
     const int* __restrict__ scol;
     const long long* __restrict__ chunk_off; // [nchunks+1]
-    const int* __restrict__ perm;            // slot -> row (-1 for tail slots); unused if identity
     const int* __restrict__ unit_c0;         // [nunits+1] TMA staging units: chunks unit_c0[u]..
     // segments of the longer rows
     const int* __restrict__ seg_row;         // [nseg]
@@ -118,21 +116,17 @@ struct AjmPass {
     AjmCtrl* ctrl;
     int n;
     int n_sell;
-    int ident;                               // SELL slot == row
     int max_passes;                          // passes this launch (debug host loop: 1)
     int meta_units;                          // smem capacity for a CTA's unit table (+1)
     int meta_chunks;                         // smem capacity for a CTA's chunk offsets (+1)
     int l2_mode;                             // 0 none, 1 Q evict_first, 2 + vectors evict_last,
                                              // 3 = 1 + only the iterate x~ evict_last (b, D, Qx streamed
                                              //     evict_first): vectors larger than the L2 carve-out
-    int vstage;                              // stage the rows' vector slices too (needs ident)
     unsigned long long* ts;                  // debug: per-pass phase timestamps of CTA 0 (or null)
-    int direct_interleave;                   // direct mode: chunk j -> warp j%8 (else contiguous)
     const int* __restrict__ g_uc0;           // (kGMeta) per-CTA unit -> first chunk tables, CTA-relative
     const int* __restrict__ g_coff;          // (kGMeta) per-CTA chunk -> element offset tables
     const long long* __restrict__ g_ubase;   // [grid] start of each CTA's unit table in g_uc0
     const long long* __restrict__ g_cbase;   // [grid] start of each CTA's chunk table in g_coff
-    int bid_rev;                             // experiment: CTA g takes work range G-1-g
     const double* __restrict__ Jinv;         // AJM_D_JBLOCK: rows of the block inverses, per chunk [bs][32]
     int jbs;                                 // AJM_D_JBLOCK block size (0: diagonal D)
     const uint8_t* __restrict__ scode;       // (kCol8) SELL column codes: col = row + ctab[code]
@@ -203,32 +197,6 @@ __device__ __forceinline__ void ajm_row_update(double* __restrict__ Qxp, double*
     }
     const double xn = y + (bi - qy) / Di;
     ajm_stp(xf + i, xn, xpol);
-    const double term = (qy - bi) * (xn - xnow);
-    a.d += term;
-    a.dabs += fabs(term);
-}
-
-// same as ajm_row_update with plain stores (scattered rows of sorted-window layouts)
-__device__ __forceinline__ void ajm_row_update_plain(double* __restrict__ Qxp, double* __restrict__ xf, int i,
-                                                     double q, double bi, double Di, double xt, double xpi,
-                                                     double qxp, double beta, int restart_t, AjmAcc& a) {
-    const double r = bi - q;
-    a.rr += r * r;
-    a.xq += xt * q;
-    a.bx += bi * xt;
-    double y, qy, xnow;
-    if (!restart_t) {
-        y = xt + beta * (xt - xpi);
-        qy = q + beta * (q - qxp);
-        Qxp[i] = q;
-        xnow = xt;
-    } else {
-        y = xpi;
-        qy = qxp;
-        xnow = xpi;
-    }
-    const double xn = y + (bi - qy) / Di;
-    xf[i] = xn;
     const double term = (qy - bi) * (xn - xnow);
     a.d += term;
     a.dabs += fabs(term);
@@ -579,44 +547,6 @@ __device__ __forceinline__ double ajm_chunk_dot8(const double* sv, const uint8_t
     return s;
 }
 
-// A SELL chunk read directly from global memory (no staging): used for sorted-window layouts,
-// whose variable chunk widths make the shared-memory units small.
-__device__ __forceinline__ void ajm_chunk_direct(const AjmPass& p, int ch, int w, long long base, int lane,
-                                                 double beta, int restart_t, const double* xc,
-                                                 const double* xp, double* xf, AjmAcc& acc, uint64_t vpol) {
-    const int slot = ch * 32 + lane;
-    const int row = p.ident ? (slot < p.n_sell ? slot : -1) : __ldg(p.perm + slot);
-    double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
-    if (row >= 0) {  // plain loads: the rows of a sorted-window chunk are scattered
-        bi = __ldg(p.b + row);
-        Di = __ldg(p.D + row);
-        xt = ajm_ld(xc + row);
-        xpi = ajm_ld(xp + row);
-        qxp = p.Qxp[row];
-    }
-    const double* __restrict__ sv = p.sval + base + lane;
-    const int* __restrict__ sc = p.scol + base + lane;
-    double s = 0.0;
-    for (int k0 = 0; k0 < w; k0 += 8) {
-        double v[8], xg[8];
-        int cc[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            if (k0 + j < w) {
-                v[j] = __ldcs(sv + (size_t)(k0 + j) * 32);
-                cc[j] = __ldcs(sc + (size_t)(k0 + j) * 32);
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (k0 + j < w) xg[j] = ajm_ld(xc + cc[j]);
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (k0 + j < w) s += v[j] * xg[j];  // ascending column order
-    }
-    if (row >= 0) ajm_row_update_plain(p.Qxp, xf, row, s, bi, Di, xt, xpi, qxp, beta, restart_t, acc);
-}
-
 // ---- distributed shared memory (single-cluster variant) ----
 // arrive (release at cluster scope) on the mbarrier at the same smem offset in CTA `rank`
 __device__ __forceinline__ void ajm_cluster_arrive(uint64_t* bar, unsigned rank) {
@@ -649,49 +579,27 @@ __device__ __forceinline__ double ajm_ld_cluster(const double* local, unsigned r
     return v;
 }
 
-// The persistent solver kernel (cooperative launch; grid = resident CTAs).  AJM_BLOCK consumer
-// threads + one producer warp.  The producer streams this CTA's SELL units into a kStages-deep
-// shared-memory ring with cp.async.bulk (TMA engine, mbarrier complete_tx):
-//   static part  -- val/col of <= 8 chunks (and, for natural-order layouts, the rows' b and D);
-//                   Q never changes, so this part runs ahead across pass boundaries;
-//   dynamic part -- (natural-order layouts) the rows' x~^t, x^{t-1}, Q x^{t-1} slices; issued
-//                   only once the pass that owns the unit has started (after the grid barrier).
-// A stage's full barrier completes when both parts have landed.
-// kMode: 0 TMA ring of val/col; 1 ring + the rows' vector slices (natural order only);
-//        2 no ring, SELL read directly by the consumer warps (sorted-window layouts);
-//        3 "gather ring": as 1, plus a gather warp that, once a unit's columns have landed and
-//          its pass has started, issues the unit's x~ gathers as asynchronous 8-byte copies
-//          (cp.async, LDGSTS) straight into the stage, and the bulk copies of the rows'
-//          x~^t / x^{t-1} / Q x^{t-1} slices; both complete on the stage's "gathered" mbarrier.
-//          The consumer warps then run from shared memory only (no register-bound gather
-//          batches: every gather of a unit is in flight at once).
-__device__ __forceinline__ void ajm_cp_async8(void* dst_smem, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(ajm_smem(dst_smem)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void ajm_cp_async_arrive_noinc(uint64_t* bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(ajm_smem(bar)) : "memory");
-}
-
-// SELL chunk dot from shared memory: val and the gathered x~ values side by side in the stage
-__device__ __forceinline__ double ajm_chunk_dot_smem(const double* sv, const double* sx, int w) {
-    double s = 0.0;
-#pragma unroll 4
-    for (int k = 0; k < w; ++k) s += sv[k * 32] * sx[k * 32];  // ascending column order
-    return s;
-}
-
+// The persistent solver kernel (cooperative launch; grid = resident CTAs): AJM_WARPS consumer
+// warps + one producer warp per CTA.  The producer's lane 0 streams this CTA's SELL staging units
+// (val + col, or val + byte code) into a kStages-deep shared-memory ring with cp.async.bulk (TMA
+// engine, mbarrier complete_tx).  Q never changes, so the producer runs ahead across pass
+// boundaries while the consumers sit in the grid barrier.
 // kSeg = false: layouts without warp segments (all rows in SELL, e.g. stencils) -- phases (1) and
-// (3) are compiled out of the hot loop.
+//   (3) are compiled out of the hot loop.
 // kCluster = true: the whole grid is ONE thread-block cluster (<= 16 CTAs, small problems): the
-// per-pass barrier and the exchange of the CTA partials go through distributed shared memory
-// (remote mbarrier arrivals, ld.shared::cluster) instead of global memory.  Same reduction order
-// as the global path, so the results are bitwise those of the cooperative launch with the same grid.
+//   per-pass barrier and the exchange of the CTA partials go through distributed shared memory
+//   (remote mbarrier arrivals, ld.shared::cluster) instead of global memory.  Same reduction order
+//   as the global path, so the results are bitwise those of the cooperative launch with the same
+//   grid.
+// kJB: 0 = diagonal metric D; 2 / 4 / 8 = block-diagonal J of eq-J-blkdiag with that compile-time
+//   block size; -1 = block J with the runtime block size p.jbs (1, 16, 32).
 // kGMeta = true: the per-CTA unit/chunk tables are read from global memory (precomputed per CTA
-// on the host) instead of being staged in shared memory -- for layouts whose tables do not fit
-// next to the ring (hundreds of millions of rows).
-template <int kStages, int kMaxReg, int kMode, bool kSeg = true, bool kCluster = false, int kJB = 0,
-          bool kGMeta = false, bool kCol8 = false>
-__global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
+//   on the host) instead of being staged in shared memory -- for layouts whose tables do not fit
+//   next to the ring (hundreds of millions of rows).
+// kCol8 = true: byte-coded SELL columns (col = row + ctab[code]).
+template <int kStages, bool kSeg = true, bool kCluster = false, int kJB = 0, bool kGMeta = false,
+          bool kCol8 = false>
+__global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
     extern __shared__ __align__(128) unsigned char s_dyn[];
     __shared__ double s_red[AJM_WARPS][AJM_NPART];
     __shared__ double s_tot[AJM_NPART];
@@ -700,10 +608,7 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
     __shared__ __align__(8) uint64_t s_full[kStages];
     __shared__ __align__(8) uint64_t s_empty[kStages];
     __shared__ volatile int s_stop;
-    __shared__ volatile int s_pass;     // passes (of this launch) whose dynamic vectors may be staged
-    __shared__ volatile int s_bufc, s_bufp;  // x~^t / x^{t-1} buffer indices of pass s_pass
-    __shared__ volatile int s_endpass;       // (kMode 3) first pass that never runs, -1 while running
-    __shared__ __align__(8) uint64_t s_gath[kStages];
+    __shared__ volatile int s_pass;            // passes of this launch the consumers have started
     __shared__ __align__(8) uint64_t s_cbar;   // (kCluster) per-pass barrier: G arrivals per phase
     __shared__ __align__(8) uint64_t s_cexit;  // (kCluster) every CTA done with the others' smem
     __shared__ double s_part[2][AJM_NPART];    // (kCluster) this CTA's partials by pass parity
@@ -712,36 +617,22 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
 
     AjmCtrl* c = p.ctrl;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int bid = p.bid_rev ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x;  // (experiment knob)
+    const int bid = (int)blockIdx.x;
     const unsigned G = gridDim.x;
     const int u0 = p.cta_unit[bid], u1 = p.cta_unit[bid + 1];
     const int nunits = u1 - u0;
-    constexpr bool gring = (kMode == 3);
-    constexpr bool jblk = (kMode == 4);    // as 0 with the block-diagonal J of eq-J-blkdiag
-    constexpr bool vstage = (kMode == 1);  // the unit's rows are contiguous (internal numbering)
-    constexpr bool vecs = vstage || gring; // row operands staged in shared memory
-    constexpr bool direct = (kMode == 2);
+    constexpr bool jblk = (kJB != 0);
     // stage s: val[UNIT_EL] f64 | col[UNIT_EL] i32 (kCol8: code[UNIT_EL] u8)
-    //          | (vecs) b, D, x~, x^{t-1}, Qx^{t-1} [256] f64 | (gring) gathered x~[col] [UNIT_EL] f64
     constexpr unsigned el_bytes = kCol8 ? 9u : 12u;
-    const size_t stage_bytes = (size_t)AJM_UNIT_EL * el_bytes + (vecs ? (size_t)5 * AJM_UNIT_ROWS * 8 : 0) +
-                               (gring ? (size_t)AJM_UNIT_EL * 8 : 0);
-    static_assert(!kCol8 || (kMode == 0 && !kCluster && !kGMeta), "byte-coded columns: plain ring variant only");
+    constexpr size_t stage_bytes = (size_t)AJM_UNIT_EL * el_bytes;
+    static_assert(!kCol8 || (!jblk && !kCluster && !kGMeta), "byte-coded columns: plain ring variant only");
     auto st_val = [&](int k) { return reinterpret_cast<double*>(s_dyn + (size_t)k * stage_bytes); };
     auto st_col = [&](int k) { return reinterpret_cast<int*>(s_dyn + (size_t)k * stage_bytes + (size_t)AJM_UNIT_EL * 8); };
     auto st_code = [&](int k) { return s_dyn + (size_t)k * stage_bytes + (size_t)AJM_UNIT_EL * 8; };
-    auto st_vec = [&](int k, int which) {
-        return reinterpret_cast<double*>(s_dyn + (size_t)k * stage_bytes + (size_t)AJM_UNIT_EL * 12 +
-                                         (size_t)which * AJM_UNIT_ROWS * 8);
-    };
-    auto st_xg = [&](int k) {
-        return reinterpret_cast<double*>(s_dyn + (size_t)k * stage_bytes + (size_t)AJM_UNIT_EL * 12 +
-                                         (size_t)5 * AJM_UNIT_ROWS * 8);
-    };
     // static per-CTA SELL metadata, loaded once: unit -> first chunk, chunk -> element offset
     // (relative to this CTA's first chunk / element), so the pass never chases global pointers
     int* s_uc0 = kGMeta ? const_cast<int*>(p.g_uc0 + p.g_ubase[bid])
-                        : reinterpret_cast<int*>(s_dyn + (direct ? (size_t)0 : (size_t)kStages * stage_bytes));
+                        : reinterpret_cast<int*>(s_dyn + (size_t)kStages * stage_bytes);
     int* s_coff = kGMeta ? const_cast<int*>(p.g_coff + p.g_cbase[bid]) : s_uc0 + p.meta_units;
     const int cfirst = nunits > 0 ? p.unit_c0[u0] : 0;
     const int nchk = nunits > 0 ? p.unit_c0[u1] - cfirst : 0;
@@ -756,13 +647,9 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         s_st = c->s;
         s_stop = 0;
         s_pass = 0;
-        s_bufc = s_st.cur;
-        s_bufp = s_st.prev;
-        s_endpass = -1;
         for (int k = 0; k < kStages; ++k) {
             ajm_mbar_init(&s_full[k], 1);
             ajm_mbar_init(&s_empty[k], AJM_WARPS);
-            ajm_mbar_init(&s_gath[k], AJM_GWARPS * 32 + 1);  // cp.async arrivals + one expect_tx arrival
         }
         if (kCluster) {
             ajm_mbar_init(&s_cbar, gridDim.x);
@@ -777,119 +664,41 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
 
     if (warp == AJM_WARPS) {
         // ---------------- producer warp (one lane) ----------------
-        if (!direct && lane == 0 && nunits > 0) {
+        if (lane == 0 && nunits > 0) {
             const uint64_t qpol = ajm_policy(p.l2_mode >= 1 ? 1 : 0);
-            const uint64_t vpol = ajm_policy(p.l2_mode >= 2 ? 2 : 0);
             const long long total = (long long)nunits * p.max_passes;
-            long long cnt = 0, vcnt = 0;  // units with static / dynamic parts issued
+            long long cnt = 0;  // units issued
             long long idle = 0;
-            auto issue_dynamic = [&](long long k) {
-                const int stage = (int)(k % kStages);
-                const int uu = (int)(k % nunits);
-                const int r0 = (cfirst + s_uc0[uu]) * 32;
-                const unsigned bytes = (unsigned)(s_uc0[uu + 1] - s_uc0[uu]) * 32u * 8u;
-                const double* xcur = ajm_sel(p, s_bufc);
-                const double* xprv = ajm_sel(p, s_bufp);
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-                ajm_bulk_g2s(st_vec(stage, 2), xcur + r0, bytes, &s_full[stage], vpol);
-                ajm_bulk_g2s(st_vec(stage, 3), xprv + r0, bytes, &s_full[stage], vpol);
-                ajm_bulk_g2s(st_vec(stage, 4), p.Qxp + r0, bytes, &s_full[stage], vpol);
-            };
-            while (vcnt < total) {
-                bool progressed = false;
-                if (vstage && vcnt < cnt && vcnt / nunits <= (long long)s_pass) {
-                    issue_dynamic(vcnt++);
-                    progressed = true;
-                } else if (!vstage && vcnt < cnt) {
-                    vcnt = cnt;
+            while (cnt < total) {
+                const int stage = (int)(cnt % kStages);
+                const unsigned par = (unsigned)((cnt / kStages) & 1) ^ 1u;
+                if (ajm_mbar_try_wait(&s_empty[stage], par)) {
+                    const int uu = (int)(cnt % nunits);
+                    const int e0 = s_coff[s_uc0[uu]], e1 = s_coff[s_uc0[uu + 1]];
+                    const unsigned ne = (unsigned)(e1 - e0);
+                    ajm_mbar_expect_tx(&s_full[stage], ne * el_bytes);
+                    ajm_bulk_g2s(st_val(stage), p.sval + efirst + e0, ne * 8u, &s_full[stage], qpol);
+                    if (kCol8)
+                        ajm_bulk_g2s(st_code(stage), p.scode + efirst + e0, ne, &s_full[stage], qpol);
+                    else
+                        ajm_bulk_g2s(st_col(stage), p.scol + efirst + e0, ne * 4u, &s_full[stage], qpol);
+                    ++cnt;
+                    idle = 0;
+                } else if (s_stop) {
+                    break;
+                } else if (++idle > (1LL << 28)) {
+                    atomicExch(&c->timeout_flag, 1u);
+                    break;
                 }
-                if (cnt < total) {
-                    const int stage = (int)(cnt % kStages);
-                    const unsigned par = (unsigned)((cnt / kStages) & 1) ^ 1u;
-                    if (ajm_mbar_try_wait(&s_empty[stage], par)) {
-                        const int uu = (int)(cnt % nunits);
-                        const int e0 = s_coff[s_uc0[uu]], e1 = s_coff[s_uc0[uu + 1]];
-                        const unsigned ne = (unsigned)(e1 - e0);
-                        const unsigned vbytes = vecs ? (unsigned)(s_uc0[uu + 1] - s_uc0[uu]) * 32u * 8u : 0u;
-                        ajm_mbar_expect_tx(&s_full[stage], ne * el_bytes + (vstage ? 5u : 2u) * vbytes);
-                        ajm_bulk_g2s(st_val(stage), p.sval + efirst + e0, ne * 8u, &s_full[stage], qpol);
-                        if (kCol8)
-                            ajm_bulk_g2s(st_code(stage), p.scode + efirst + e0, ne, &s_full[stage], qpol);
-                        else
-                            ajm_bulk_g2s(st_col(stage), p.scol + efirst + e0, ne * 4u, &s_full[stage], qpol);
-                        if (vecs) {
-                            const int r0 = (cfirst + s_uc0[uu]) * 32;
-                            ajm_bulk_g2s(st_vec(stage, 0), p.b + r0, vbytes, &s_full[stage], vpol);
-                            ajm_bulk_g2s(st_vec(stage, 1), p.D + r0, vbytes, &s_full[stage], vpol);
-                        }
-                        ++cnt;
-                        progressed = true;
-                    }
-                }
-                if (s_stop) break;
-                if (progressed) idle = 0;
-                else if (++idle > (1LL << 28)) { atomicExch(&c->timeout_flag, 1u); break; }
             }
-            // complete every issued stage (dynamic parts of never-consumed units read stale but
-            // valid memory), then wait for all copies to land before the CTA exits
-            while (vstage && vcnt < cnt) issue_dynamic(vcnt++);
+            // wait for every issued copy to land before the CTA exits (units of passes that never
+            // ran were issued ahead and are simply not consumed)
             long long spins = 0;
             while (!s_stop) {
                 if (++spins > (1LL << 32)) break;
             }
             for (long long k = (long long)s_pass * nunits; k < cnt; ++k)
                 if (k >= 0) ajm_mbar_wait(&s_full[k % kStages], (unsigned)((k / kStages) & 1), &c->timeout_flag);
-        }
-        return;
-    }
-
-    if (gring && warp > AJM_WARPS) {
-        // ---------------- gather warp (kMode 3) ----------------
-        // unit k (this CTA's k-th staged unit, pass k / nunits): once its columns have landed
-        // (full) and its pass has started (x~ final after the grid barrier), lane 0 bulk-copies
-        // the rows' x~^t, x^{t-1}, Q x^{t-1} slices and all 32 lanes issue the unit's gathers
-        // x~[col[e]] -> stage as 8-byte cp.async; everything completes on s_gath[stage].
-        if (nunits > 0) {
-            const uint64_t vpol = ajm_policy(p.l2_mode >= 2 ? 2 : 0);
-            const long long total = (long long)nunits * p.max_passes;
-            for (long long k = 0; k < total; ++k) {
-                const long long kp = k / nunits;
-                long long spins = 0;
-                bool quit = false;
-                while ((long long)s_pass < kp) {
-                    if (s_stop || ++spins > (1LL << 31)) { quit = true; break; }
-                }
-                if (quit || (s_endpass >= 0 && kp >= (long long)s_endpass)) break;
-                const int stage = (int)(k % kStages);
-                ajm_mbar_wait(&s_full[stage], (unsigned)((k / kStages) & 1), &c->timeout_flag);
-                const int uu = (int)(k % nunits);
-                const int e0 = s_coff[s_uc0[uu]], ne = s_coff[s_uc0[uu + 1]] - e0;
-                const double* xcur = ajm_sel(p, s_bufc);
-                const int gt = (warp - AJM_WARPS - 1) * 32 + lane;
-                if (gt == 0) {
-                    const int r0 = (cfirst + s_uc0[uu]) * 32;
-                    const unsigned bytes = (unsigned)(s_uc0[uu + 1] - s_uc0[uu]) * 32u * 8u;
-                    asm volatile("fence.proxy.async.global;" ::: "memory");
-                    ajm_mbar_expect_tx(&s_gath[stage], 3u * bytes);
-                    ajm_bulk_g2s(st_vec(stage, 2), xcur + r0, bytes, &s_gath[stage], vpol);
-                    ajm_bulk_g2s(st_vec(stage, 3), ajm_sel(p, s_bufp) + r0, bytes, &s_gath[stage], vpol);
-                    ajm_bulk_g2s(st_vec(stage, 4), p.Qxp + r0, bytes, &s_gath[stage], vpol);
-                }
-                const int* sc = st_col(stage);
-                double* xg = st_xg(stage);
-                constexpr int GS = AJM_GWARPS * 32;
-                int e = gt;
-                for (; e + 3 * GS < ne; e += 4 * GS) {
-                    const int c0 = sc[e], c1 = sc[e + GS], c2 = sc[e + 2 * GS], c3 = sc[e + 3 * GS];
-                    ajm_cp_async8(xg + e, xcur + c0);
-                    ajm_cp_async8(xg + e + GS, xcur + c1);
-                    ajm_cp_async8(xg + e + 2 * GS, xcur + c2);
-                    ajm_cp_async8(xg + e + 3 * GS, xcur + c3);
-                }
-                for (; e < ne; e += GS) ajm_cp_async8(xg + e, xcur + sc[e]);
-                ajm_cp_async_arrive_noinc(&s_gath[stage]);
-            }
-            asm volatile("cp.async.wait_all;" ::: "memory");
         }
         return;
     }
@@ -922,7 +731,6 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         //     Static mode: warp w runs the CTA's segments w, w+8, ... (split rows first, then
         //     longest first).
         if (p.dynseg && bid == 0 && tid == 0) c->seg_q[(t + 1) & 1] = 0u;
-        int gk = 0, gend = 0;  // dynamic mode: current claim group [gk, gend) of seg_order
         if (!p.dynseg) {
             // static plan: the next segment's metadata is loaded while this one runs (one 16-byte
             // record in list order, no index chase)
@@ -946,10 +754,9 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                     }
                 }
             }
-        } else
-        for (int sk = sg0 + warp;; sk += AJM_WARPS) {
-            int sg;
-            if (p.dynseg) {
+        } else {
+            int gk = 0, gend = 0;  // current claim group [gk, gend) of seg_order
+            for (;;) {
                 if (gk >= gend) {
                     unsigned k = 0;
                     if (lane == 0) k = atomicAdd(&c->seg_q[t & 1], 1u);
@@ -958,40 +765,26 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                     gk = __ldg(p.seg_grp + k);
                     gend = __ldg(p.seg_grp + k + 1);
                 }
-                sg = __ldg(p.seg_order + gk++);
-            } else {
-                if (sk >= sg1) break;
-                sg = __ldg(p.seg_list + sk);
-            }
-            const int row = __ldg(p.seg_row + sg);
-            const double s = ajm_seg_dot(p, __ldg(p.seg_k0 + sg), __ldg(p.seg_k1 + sg), xc, lane);
-            const int sidx = __ldg(p.seg_split + sg);
-            if (lane == 0) {
-                if (sidx < 0) {
-                    ajm_row_epilogue(p, row, s, beta, restart_t, xc, xp, xf, acc);
-                } else {
-                    __stcg(p.seg_part + sg, s);
-                    __threadfence();
-                    atomicAdd(p.split_cnt + sidx, 1u);
+                const int sg = __ldg(p.seg_order + gk++);
+                const int row = __ldg(p.seg_row + sg);
+                const double s = ajm_seg_dot(p, __ldg(p.seg_k0 + sg), __ldg(p.seg_k1 + sg), xc, lane);
+                const int sidx = __ldg(p.seg_split + sg);
+                if (lane == 0) {
+                    if (sidx < 0) {
+                        ajm_row_epilogue(p, row, s, beta, restart_t, xc, xp, xf, acc);
+                    } else {
+                        __stcg(p.seg_part + sg, s);
+                        __threadfence();
+                        atomicAdd(p.split_cnt + sidx, 1u);
+                    }
                 }
             }
         }
         }
         if (tsw) p.ts[pass * 8 + 6] = ajm_gtime();
         if (p.ts && tid == 0 && pass == 5) p.ts[512 + 4 * bid + 2] = ajm_gtime();  // warp 0's segments done
-        if (direct) {
-            // (2') SELL chunks straight from global memory; chunk j of the CTA -> warp j % 8
-            const int jb = (int)((long long)nchk * warp / AJM_WARPS);
-            const int je = (int)((long long)nchk * (warp + 1) / AJM_WARPS);
-            for (int j = (p.direct_interleave ? warp : jb); j < (p.direct_interleave ? nchk : je);
-                 j += (p.direct_interleave ? AJM_WARPS : 1)) {
-                const int e0 = s_coff[j];
-                ajm_chunk_direct(p, cfirst + j, (s_coff[j + 1] - e0) >> 5, efirst + e0, lane, beta, restart_t,
-                                 xc, xp, xf, acc, vpol);
-            }
-        } else
-        // (2) SELL units from the ring; chunk j of the CTA -> warp j % AJM_WARPS (at most one
-        //     chunk per unit per warp)
+        // (2) SELL units from the ring; chunk j of the CTA -> warp j % AJM_WARPS (at most one chunk
+        //     per unit per warp)
         {
             int jc = warp;
             for (int uu = 0; uu < nunits; ++uu) {
@@ -1003,19 +796,14 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                     const int e0 = s_coff[j];
                     const int w = (s_coff[j + 1] - e0) >> 5;
                     const int slot = (cfirst + j) * 32 + lane;
-                    int row;
+                    const int row = slot < p.n_sell ? slot : -1;  // SELL slot == internal row
                     double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
-                    if (vecs) {
-                        row = slot < p.n_sell ? slot : -1;
-                    } else {
-                        row = p.ident ? (slot < p.n_sell ? slot : -1) : __ldg(p.perm + slot);
-                        if (row >= 0) {  // operands in flight during the stage wait
-                            bi = ajm_ldp(p.b + row, vpol);
-                            if (!jblk) Di = ajm_ldp(p.D + row, vpol);
-                            xt = ajm_ld(xc + row);
-                            xpi = ajm_ld(xp + row);
-                            qxp = ajm_ldp(p.Qxp + row, vpol);
-                        }
+                    if (row >= 0) {  // operands in flight during the stage wait
+                        bi = ajm_ldp(p.b + row, vpol);
+                        if (!jblk) Di = ajm_ldp(p.D + row, vpol);
+                        xt = ajm_ld(xc + row);
+                        xpi = ajm_ld(xp + row);
+                        qxp = ajm_ldp(p.Qxp + row, vpol);
                     }
                     constexpr int JV = kJB > 0 ? kJB : 8;
                     double jv[JV];  // (jblk) this row's first entries of J^{-1}, also in flight
@@ -1026,23 +814,13 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
                         for (int k = 0; k < JV; ++k) jv[k] = (k < jbs) ? __ldcs(jr + 32 * k) : 0.0;
                     }
                     ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);
-                    if (gring) ajm_mbar_wait(&s_gath[stage], par, &c->timeout_flag);
-                    if (vecs) {
-                        const int ri = (j - s_uc0[uu]) * 32 + lane;
-                        bi = st_vec(stage, 0)[ri];
-                        Di = st_vec(stage, 1)[ri];
-                        xt = st_vec(stage, 2)[ri];
-                        xpi = st_vec(stage, 3)[ri];
-                        qxp = st_vec(stage, 4)[ri];
-                    }
                     const int off = (e0 - s_coff[s_uc0[uu]]) + lane;
-                    const double q = gring ? ajm_chunk_dot_smem(st_val(stage) + off, st_xg(stage) + off, w)
-                                   : kCol8 ? ajm_chunk_dot8(st_val(stage) + off, st_code(stage) + off, w,
+                    const double q = kCol8 ? ajm_chunk_dot8(st_val(stage) + off, st_code(stage) + off, w,
                                                             xc + (row >= 0 ? row : 0), s_ctab)
                                            : ajm_chunk_dot<kCluster>(st_val(stage) + off, st_col(stage) + off, w, xc);
                     if (jblk)  // every lane takes part (shuffles); tail lanes store nothing
-                        ajm_row_update_blk<kJB>(p.Qxp, xf, row, q, bi, jr, jbs, jv, xt, xpi, qxp, beta, restart_t,
-                                                acc, vpol, xpol);
+                        ajm_row_update_blk<(kJB > 0 ? kJB : 0)>(p.Qxp, xf, row, q, bi, jr, jbs, jv, xt, xpi, qxp,
+                                                                beta, restart_t, acc, vpol, xpol);
                     else if (row >= 0)
                         ajm_row_update(p.Qxp, xf, row, q, bi, Di, xt, xpi, qxp, beta, restart_t, acc, vpol, xpol);
                 } else {
@@ -1056,14 +834,15 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
         if (tsw) p.ts[pass * 8 + 7] = ajm_gtime();
         if (p.ts && tid == 0 && pass == 5) p.ts[512 + 4 * bid + 3] = ajm_gtime();  // warp 0's chunks done
         if (kSeg) {
-        // (3) segment rows owned by this CTA (one per lane, 256 in flight per CTA): wait for all
-        //     segments of this pass, sum their partials in segment order, run the row epilogue
+        // (3) segment rows owned by this CTA (one per thread, 256 in flight per CTA): wait for all
+        //     segments of this pass, sum their partials in segment order, run the row epilogue.
+        //     The arrival counters are monotone over the solve; the comparison is wrap-safe.
         for (int k = sp0 + tid; k < sp1; k += AJM_BLOCK) {
             const int sidx = __ldg(p.owner_split + k);
             const int g0 = __ldg(p.split_seg0 + sidx), g1 = __ldg(p.split_seg0 + sidx + 1);
             const unsigned target = (unsigned)(g1 - g0) * (unsigned)(t + 1);
             long long spins = 0;
-            while (ajm_ld_acquire(p.split_cnt + sidx) < target) {
+            while ((int)(ajm_ld_acquire(p.split_cnt + sidx) - target) < 0) {
                 __nanosleep(32);
                 if (++spins > (1LL << 28)) { atomicExch(&c->timeout_flag, 1u); break; }
             }
@@ -1151,18 +930,11 @@ __global__ void __maxnreg__(kMaxReg) ajm_solve_kernel(AjmPass p) {
             s_st = ls;
             if (timed_out) s_st.done = 1;
             if (tsw) p.ts[pass * 8 + 5] = ajm_gtime();
-            if (!s_st.done) {  // the next pass may stage its dynamic vectors now
-                s_bufc = s_st.cur;
-                s_bufp = s_st.prev;
-                __threadfence_block();
-                s_pass = pass + 1;
-            }
+            if (!s_st.done) s_pass = pass + 1;
         }
         ajm_csync();
     }
     if (tid == 0) {
-        s_endpass = pass;  // (kMode 3) the gather warp must not start pass >= pass
-        __threadfence_block();
         s_pass = pass;  // units of passes >= pass were never consumed
         __threadfence_block();
         s_stop = 1;

@@ -20,6 +20,8 @@ ER/Chung-Lu Laplacians for the §4.2 graph Laplacians).
 from __future__ import annotations
 
 import dataclasses
+import os
+
 import numpy as np
 
 __all__ = [
@@ -184,6 +186,45 @@ def aniso27(m: int, w=(1.0, 1.0, 1e-2), shift: float = 1e-6) -> CSR:
 # graphs
 # ----------------------------------------------------------------------------------------------
 
+# Sorting kernels of the generators.  Large integer sorts / unique / searchsorted run through
+# torch's multi-threaded CPU ops when torch is importable: for integer keys (and exact float
+# comparisons in searchsorted) they return exactly numpy's results -- a stable sort's permutation
+# and a sorted unique set are unique -- so the matrices are bitwise the same either way
+# (tests/test_synth.py checks it); only the wall time of building configs 3-5 changes.
+_FAST = os.environ.get("AJM_SYNTH_NUMPY") is None
+
+
+def _torch():
+    if not _FAST:
+        return None
+    try:
+        import torch
+        return torch
+    except Exception:  # pragma: no cover
+        return None
+
+
+def _argsort_stable(key: np.ndarray) -> np.ndarray:
+    torch = _torch()
+    if torch is None or key.size < (1 << 20):
+        return np.argsort(key, kind="stable")
+    return torch.sort(torch.from_numpy(key), stable=True).indices.numpy()
+
+
+def _unique(key: np.ndarray) -> np.ndarray:
+    torch = _torch()
+    if torch is None or key.size < (1 << 20):
+        return np.unique(key)
+    return torch.unique(torch.from_numpy(key), sorted=True).numpy()
+
+
+def _searchsorted_right(cdf: np.ndarray, r: np.ndarray) -> np.ndarray:
+    torch = _torch()
+    if torch is None or r.size < (1 << 20):
+        return np.searchsorted(cdf, r, side="right").astype(np.int64)
+    return torch.searchsorted(torch.from_numpy(cdf), torch.from_numpy(r), right=True).numpy()
+
+
 def _laplacian_from_edges(n: int, u: np.ndarray, v: np.ndarray, w: np.ndarray,
                           shift: float = 0.0) -> CSR:
     """L = Deg - W (+ shift*I) from an undirected simple edge list (u < v unique), CSR sorted."""
@@ -192,7 +233,7 @@ def _laplacian_from_edges(n: int, u: np.ndarray, v: np.ndarray, w: np.ndarray,
     deg = np.bincount(u, weights=w, minlength=n) + np.bincount(v, weights=w, minlength=n)
     vals = np.concatenate([-w, -w, deg + shift])
     key = rows * n + cols
-    order = np.argsort(key, kind="stable")
+    order = _argsort_stable(key)
     del key
     rows = rows[order]
     col = cols[order].astype(np.int32)
@@ -209,7 +250,7 @@ def _dedupe_edges(n: int, u: np.ndarray, v: np.ndarray):
     u, v = u[keep], v[keep]
     a = np.minimum(u, v)
     bb = np.maximum(u, v)
-    key = np.unique(a.astype(np.int64) * n + bb)
+    key = _unique(a.astype(np.int64) * n + bb)
     return key // n, key % n
 
 
@@ -273,8 +314,8 @@ def chung_lu(n: int, seed: int, gamma: float = 2.1, mean_deg: float = 20.0, w_ma
     m = int(round(wexp.sum() / 2))
     cdf = np.cumsum(wexp)
     cdf /= cdf[-1]
-    u = np.searchsorted(cdf, g.random(m), side="right").astype(np.int64)
-    v = np.searchsorted(cdf, g.random(m), side="right").astype(np.int64)
+    u = _searchsorted_right(cdf, g.random(m))
+    v = _searchsorted_right(cdf, g.random(m))
     np.minimum(u, n - 1, out=u)
     np.minimum(v, n - 1, out=v)
     u, v = _dedupe_edges(n, u, v)

@@ -29,14 +29,14 @@ def oracle_threads():
 
 
 def gpu_solve(Q, b, x0=None, tol=0.0, maxit=1000, restart=True, momentum=True, k0=2,
-              dmode="jdiag", d=None, loop="graph", device_inputs=False, jblock=None):
+              dmode="jdiag", d=None, loop="graph", device_inputs=False, jblock=None, **solver_kw):
     import torch
     import paper_2407_03272_b200 as ajm
     args = [Q.row_ptr, Q.col, Q.val, b, d, x0]
     if device_inputs:
         args = [None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in args]
     with ajm.Solver(Q.n, args[0], args[1], args[2], args[3], dmode=dmode, d=args[4], loop=loop,
-                    jblock=jblock) as s:
+                    jblock=jblock, **solver_kw) as s:
         r = s.solve(x0=args[5], tol=tol, maxit=maxit, momentum=momentum, restart=restart, k0=k0)
         r.x = r.x.cpu().numpy()
         r.d_trace = s.trace("d", r.iterations + 1)
@@ -71,3 +71,35 @@ def oracle_matching(Q, b, g, **kw):
         forced_n += 1
         o = oracle.solve(Q, b, forced=forced, **kw)
     raise AssertionError("restart schedules could not be matched")
+
+
+F_TOL = 1e-10   # |f_gpu - f_oracle| <= F_TOL * max(1, |f*|) per history entry (DESIGN.md §5 parity)
+D_TOL = 1e-7    # |d_gpu - d_oracle| <= D_TOL * sum|terms| while the residual is >= D_RES_MIN
+D_RES_MIN = 1e-6
+
+
+def assert_history_parity(g, o, fstar=None):
+    """The ABI outputs besides x against the oracle of the same run, entry by entry:
+      res_hist[t]  relative residual of x~^t             -- rounding-level
+      f_hist[t]    f(x~^t) = 1/2<x,Qx> - <b,x> (eq-qp, P:25-28)   -- F_TOL * max(1, |f*|)
+      d_t          <Q y^t - b, x~^t - x^{t-1}> (restart test): D_TOL * sum|terms| and the same
+                   sign wherever the tie ratio |d|/sum|terms| > TIE_RATIO, for every t whose residual
+                   is >= D_RES_MIN (below that both sides' terms are differences of nearly equal
+                   iterates, dominated by rounding -- DESIGN.md R17)
+      status, iterations, n_restarts, restart iterations, x_is_prerestart (R5) -- exact."""
+    assert g.status == o.status and g.iterations == o.iterations
+    assert g.n_restarts == o.n_restarts and g.restart_iters == o.restart_iters
+    assert bool(g.x_is_prerestart) == bool(o.x_is_prerestart)
+    k = min(len(g.res_hist), len(o.res_hist))
+    assert k == g.iterations + 1
+    assert np.all(np.abs(g.res_hist[:k] - o.res_hist[:k]) <= 1e-9 * o.res_hist[:k] + 1e-12 * o.res_hist[0])
+    scale = max(1.0, abs(fstar) if fstar is not None else float(np.abs(o.f_hist[:k]).max()))
+    fdev = np.abs(g.f_hist[:k] - o.f_hist[:k])
+    assert fdev.max() <= F_TOL * scale, ("f_hist", float(fdev.max()), scale)
+    gd, od, oa = g.d_trace[1:k], o.d_hist[1:k], o.dabs_hist[1:k]
+    live = o.res_hist[1:k] >= D_RES_MIN
+    ddev = np.abs(gd - od)[live]
+    assert np.all(ddev <= D_TOL * oa[live]), ("d_t", float((ddev / np.maximum(oa[live], 1e-300)).max()))
+    decided = live & (np.abs(od) > TIE_RATIO * oa)
+    assert np.all(np.sign(gd[decided]) == np.sign(od[decided])), "restart inner product sign"
+    np.testing.assert_allclose(g.dabs_trace[1:k][live], oa[live], rtol=1e-6)

@@ -22,7 +22,7 @@ def test_library_built_and_loads():
     from paper_2407_03272_b200 import build
     build.build()
     L = ajm.lib()
-    assert L.ajm_abi_version() == 2
+    assert L.ajm_abi_version() == ajm.ABI_VERSION
 
 
 def test_exports_every_header_symbol():
@@ -68,3 +68,27 @@ def test_no_oracle_in_product_path():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "ajm_oracle" not in txt, f
+
+
+def test_output_arguments_are_not_silently_converted():
+    """Outputs (x_out, histories) are written in place: the binding raises on a wrong dtype or a
+    non-contiguous buffer instead of handing the library a temporary copy."""
+    import numpy as np
+    import torch
+    with pytest.raises(TypeError):
+        ajm._ptr(np.zeros(4, dtype=np.float32), np.float64, output=True)
+    with pytest.raises(TypeError):
+        ajm._ptr(np.zeros((4, 2))[:, 0], np.float64, output=True)
+    with pytest.raises(TypeError):
+        ajm._ptr(torch.zeros(4, dtype=torch.float32), np.float64, output=True)
+    with pytest.raises(TypeError):
+        ajm._ptr(torch.zeros(4, 2, dtype=torch.float64)[:, 0], np.float64, output=True)
+    a = np.zeros(4)
+    p, keep = ajm._ptr(a, np.float64, output=True)
+    assert keep is a and p.value == a.ctypes.data
+    t = torch.zeros(4, dtype=torch.float64)
+    p, keep = ajm._ptr(t, np.float64, output=True)
+    assert keep is t and p.value == t.data_ptr()
+    # inputs are still converted
+    p, keep = ajm._ptr(np.zeros(4, dtype=np.float32), np.float64)
+    assert keep.dtype == np.float64

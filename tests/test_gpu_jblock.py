@@ -7,7 +7,8 @@ import pytest
 
 import oracle
 import synth
-from _gpu_helpers import PARITY_TOL, gpu_solve, max_rel, oracle_matching, oracle_threads, requires_cuda
+from _gpu_helpers import (PARITY_TOL, assert_history_parity, gpu_solve, max_rel, oracle_matching, oracle_threads,
+                          requires_cuda)
 
 pytestmark = [pytest.mark.gpu, requires_cuda]
 
@@ -40,8 +41,7 @@ def test_jblock_parity_1000_iterations(cfg, scale, bs, restart):
     o, nforced = oracle_matching(p.Q, p.b, g, tol=0.0, maxit=1000, restart=restart, jblock=bs)
     assert g.iterations == o.iterations == 1000
     assert max_rel(g.x, o.x) <= PARITY_TOL, (cfg, bs, max_rel(g.x, o.x), nforced)
-    k = min(len(g.res_hist), len(o.res_hist))
-    assert np.all(np.abs(g.res_hist[:k] - o.res_hist[:k]) <= 1e-9 * o.res_hist[:k] + 1e-12 * o.res_hist[0])
+    assert_history_parity(g, o, fstar=-0.5 * float(np.dot(p.b, p.x_star)))
 
 
 @pytest.mark.parametrize("cfg,scale,bs", [(1, 1.0, 4), (2, 0.25, 8), (5, 0.09375, 4)])

@@ -7,8 +7,8 @@ import pytest
 
 import oracle
 import synth
-from _gpu_helpers import (PARITY_TOL, gpu_solve, max_rel, oracle_matching, oracle_threads,
-                          requires_cuda)
+from _gpu_helpers import (PARITY_TOL, assert_history_parity, gpu_solve, max_rel, oracle_matching,
+                          oracle_threads, requires_cuda)
 
 pytestmark = [pytest.mark.gpu, requires_cuda]
 
@@ -31,9 +31,8 @@ def test_parity_1000_iterations(cfg, scale, restart):
     assert g.status == o.status and g.iterations == o.iterations
     assert max_rel(g.x, o.x) <= PARITY_TOL, (cfg, max_rel(g.x, o.x), nforced)
     np.testing.assert_array_equal(g.D, oracle.build_jdiag(p.Q))  # eq-J-diag bitwise
-    # residual history of the same iterates (rounding-level differences only)
-    k = min(len(g.res_hist), len(o.res_hist))
-    assert np.all(np.abs(g.res_hist[:k] - o.res_hist[:k]) <= 1e-9 * o.res_hist[:k] + 1e-12 * o.res_hist[0])
+    # residual / f / restart-inner-product histories and the restart bookkeeping
+    assert_history_parity(g, o, fstar=-0.5 * float(np.dot(p.b, p.x_star)))
 
 
 @pytest.mark.parametrize("cfg,scale", CASES)
@@ -45,6 +44,8 @@ def test_iterations_to_tol(cfg, scale):
     assert g.status == "converged" and o.status == "converged"
     assert abs(g.iterations - o.iterations) <= 1, (g.iterations, o.iterations)
     assert g.res_hist[-1] <= 1e-6
+    if g.iterations == o.iterations and g.restart_iters == o.restart_iters:
+        assert_history_parity(g, o, fstar=-0.5 * float(np.dot(p.b, p.x_star)))
 
 
 def test_bitwise_equal_to_mirror_oracle():
@@ -191,37 +192,37 @@ def test_create_errors():
 def test_sdd_paper_experiment(n):
     """§4.1: on Q = (n+1)I - 11^T, b = 1, tol 1e-4, maxiter 5000, the GPU's Jacobi and
     weighted Jacobi (omega_opt = 2n/(n+2)) follow their closed forms (1-1/n)^t and (1-2/(n+2))^t
-    and AJM with restart follows the exact scalar recurrence of Alg. 3 on span{1} (the models are
-    pinned against the oracle in test_oracle_pins.py); rows of n nonzeros run on the warp-segment
-    and split-row path."""
-    import sys, os
-    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
-    import exp_sdd
+    and AJM with restart follows the exact scalar recurrence of Alg. 3 on span{1} -- the models of
+    tests/_sdd_models.py, pinned against the oracle in test_oracle_pins.py; rows of n nonzeros run
+    on the warp-segment and split-row path."""
+    from _sdd_models import closed_form_rate_iters, sdd_scalar_ajm
     Q = synth.sdd(n)
     b = np.ones(n)
     t = np.arange(5001)
     g = gpu_solve(Q, b, tol=1e-4, maxit=5000, momentum=False, restart=False, dmode="qdiag")
-    assert (g.iterations, g.status) == exp_sdd.closed_form_iters(1 - 1 / n, 1e-4, 5000)
+    assert (g.iterations, g.status) == closed_form_rate_iters(1 - 1 / n, 1e-4, 5000)
     np.testing.assert_allclose(g.res_hist, (1 - 1 / n) ** t[: len(g.res_hist)], rtol=1e-9)
     w = 2 * n / (n + 2)
     g = gpu_solve(Q, b, tol=1e-4, maxit=5000, momentum=False, restart=False, dmode="user", d=np.full(n, n / w))
-    it, st = exp_sdd.closed_form_iters(1 - 2 / (n + 2), 1e-4, 5000)
+    it, st = closed_form_rate_iters(1 - 2 / (n + 2), 1e-4, 5000)
     assert g.status == st and abs(g.iterations - it) <= 1
     np.testing.assert_allclose(g.res_hist, (1 - 2 / (n + 2)) ** t[: len(g.res_hist)], rtol=1e-8)
     g = gpu_solve(Q, b, tol=1e-4, maxit=5000, restart=True)
-    it, res = exp_sdd.scalar_ajm(n, 1e-4, 5000)
+    it, hist, rest = sdd_scalar_ajm(n, 1e-4, 5000)
     assert g.status == "converged" and abs(g.iterations - it) <= 1
+    assert g.restart_iters == rest
+    k = min(len(hist), len(g.res_hist))
+    np.testing.assert_allclose(g.res_hist[:k], hist[:k], rtol=1e-7, atol=1e-12)
 
 
-@pytest.mark.parametrize("dynseg", ["0", "1"])
-def test_segment_queue_modes(dynseg, monkeypatch):
-    """Both segment schedules (static LPT plan / dynamic claim queue, AJM_DYNSEG) give the same
+@pytest.mark.parametrize("segments", ["static", "dynamic"])
+def test_segment_queue_modes(segments):
+    """Both segment schedules (static LPT plan / dynamic claim queue, AJM_SEGMENTS_*) give the same
     iterates as the oracle on a Chung-Lu graph with split rows and on the dense §4.1 rows; each is
     deterministic run to run (the queue only decides which warp runs a segment)."""
-    monkeypatch.setenv("AJM_DYNSEG", dynseg)
     for p in (synth.config_problem(4, 0.0125), synth.make_problem("sdd", synth.sdd(2600), 3)):
-        a = gpu_solve(p.Q, p.b, tol=0.0, maxit=300, restart=True)
-        b = gpu_solve(p.Q, p.b, tol=0.0, maxit=300, restart=True)
+        a = gpu_solve(p.Q, p.b, tol=0.0, maxit=300, restart=True, segments=segments)
+        b = gpu_solve(p.Q, p.b, tol=0.0, maxit=300, restart=True, segments=segments)
         np.testing.assert_array_equal(a.x, b.x)
         o, _ = oracle_matching(p.Q, p.b, a, tol=0.0, maxit=300, restart=True)
         assert max_rel(a.x, o.x) <= PARITY_TOL
@@ -239,33 +240,30 @@ def test_relabelled_layout_x0_and_diag():
     assert max_rel(g.x, o.x) <= PARITY_TOL
 
 
-def test_many_handles_pool_reuse(monkeypatch):
+def test_many_handles_pool_reuse():
     """Create / solve / destroy cycles of mixed layouts (natural order, sorted windows with
     relabelling, single-cluster and cooperative grids) with every new allocation poisoned
-    (AJM_POISON): the pooled memory a handle gets back is never read before it is written
+    (AJM_DEBUG_POISON): the pooled memory a handle gets back is never read before it is written
     (regression: chunk-tail slots once read past the slot->row map)."""
-    monkeypatch.setenv("AJM_POISON", "1")
     for rep in range(3):
         for n in (1, 2, 3, 31, 33, 513, 4097):
             Q = synth.random_spd(n, seed=n, density=min(1.0, 4.0 / n)) if n <= 600 else \
                 synth.er_laplacian(n, 4 * n, seed=5)
             b = Q.scipy() @ np.random.Generator(np.random.PCG64(n)).uniform(-1, 1, Q.n)
-            g = gpu_solve(Q, b, tol=0.0, maxit=100)
+            g = gpu_solve(Q, b, tol=0.0, maxit=100, debug_poison=True)
             if rep == 0:
                 o, _ = oracle_matching(Q, b, g, tol=0.0, maxit=100)
                 assert max_rel(g.x, o.x) <= PARITY_TOL, n
 
 
-def test_global_metadata_variant(monkeypatch):
+def test_global_metadata_variant():
     """Layouts whose per-CTA unit/chunk tables do not fit shared memory read them from global
     memory (a kernel instantiation for hundreds of millions of rows); forced here on oracle-sized
     stencil and graph cases it must give bitwise the iterates of the shared-memory tables."""
     for cfg, scale in ((2, 0.25), (4, 0.0125)):
         p = synth.config_problem(cfg, scale)
         a = gpu_solve(p.Q, p.b, tol=0.0, maxit=300, restart=True)
-        monkeypatch.setenv("AJM_FORCE_GMETA", "1")
-        g = gpu_solve(p.Q, p.b, tol=0.0, maxit=300, restart=True)
-        monkeypatch.delenv("AJM_FORCE_GMETA")
+        g = gpu_solve(p.Q, p.b, tol=0.0, maxit=300, restart=True, global_tables=True)
         np.testing.assert_array_equal(a.x, g.x)
         np.testing.assert_array_equal(a.res_hist, g.res_hist)
 
@@ -288,10 +286,10 @@ def _banded_offsets(nd, R=2048, regions=4, seed=0):
 
 
 @pytest.mark.parametrize("case", ["cfg2", "ragged17", "band255", "band257"])
-def test_byte_coded_columns(case, monkeypatch):
+def test_byte_coded_columns(case):
     """Layouts whose column offsets col - row take <= 256 values stream byte codes into an offset
     table instead of int32 columns.  Same columns, same summation order: the
-    iterates are BITWISE those of the int32 layout (AJM_NO_COL8) and match the oracle; 257 distinct
+    iterates are BITWISE those of the int32 layout (AJM_INT32_COLUMNS) and match the oracle; 257 distinct
     offsets keep the int32 layout.  (cfg2 runs the variant without segment phases, the banded
     cases (width 33) the one with them, as config 5 does at full size: test_gpu_fullsize.)"""
     if case == "cfg2":
@@ -303,9 +301,7 @@ def test_byte_coded_columns(case, monkeypatch):
     a = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True)
     assert a.info["col_bytes"] == (4 if case == "band257" else 1), a.info
     assert a.info["sigma"] == 1
-    monkeypatch.setenv("AJM_NO_COL8", "1")
-    b = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True)
-    monkeypatch.delenv("AJM_NO_COL8")
+    b = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True, int32_columns=True)
     assert b.info["col_bytes"] == 4
     np.testing.assert_array_equal(a.x, b.x)
     np.testing.assert_array_equal(a.res_hist, b.res_hist)

@@ -314,34 +314,15 @@ def test_sdd_jacobi_closed_form():
     w = 2 * n / (n + 2)
     r = oracle.solve(Q, b, D=np.full(n, n / w), tol=0.0, maxit=300, momentum=False, restart=False)
     np.testing.assert_allclose(r.res_hist, (1 - 2 / (n + 2)) ** t, rtol=1e-10, atol=1e-13)
+    # the iteration-count model used by the GPU experiment test (tests/_sdd_models.py)
+    from _sdd_models import closed_form_rate_iters
+    for rate, D in ((1 - 1 / n, None), (1 - 2 / (n + 2), np.full(n, n / w))):
+        it, st = closed_form_rate_iters(rate, 1e-4, 5000)
+        r = oracle.solve(Q, b, D=D, dmode="qdiag", tol=1e-4, maxit=5000, momentum=False, restart=False)
+        assert (r.status, abs(r.iterations - it) <= 1) == (st, True)
 
 
-def _sdd_scalar_ajm(n, tol, maxit, restart, k0=2):
-    """Alg. 3 on the §4.1 system restricted to span{1}: Q(c 1) = c 1, J = (2n - 1) I, so every
-    vector is a scalar multiple of 1 and <u 1, v 1> = n u v."""
-    cx_prev = cy = 0.0
-    alpha, K, Kre = 1.0, k0, 0
-    res_hist = [1.0]
-    rest = []
-    for t in range(1, maxit + 1):
-        cxt = cy + (1.0 - cy) / (2 * n - 1)
-        res = abs(1.0 - cxt)
-        res_hist.append(res)
-        d = n * (cy - 1.0) * (cxt - cx_prev)
-        if res <= tol:
-            return t, res_hist, rest
-        if restart and t > Kre + K and d >= 0:
-            Kre, K = t, 2 * K
-            rest.append(t)
-            alpha = 1.0
-            cy = cx_prev
-        else:
-            an = (1 + math.sqrt(1 + 4 * alpha * alpha)) / 2
-            beta = (alpha - 1) / an
-            cy = cxt + beta * (cxt - cx_prev)
-            cx_prev = cxt
-            alpha = an
-    return maxit, res_hist, rest
+from _sdd_models import sdd_scalar_ajm as _sdd_scalar_ajm  # noqa: E402 (the pinned model)
 
 
 @pytest.mark.parametrize("n,restart", [(300, True), (300, False), (64, True)])

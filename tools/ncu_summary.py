@@ -1,5 +1,8 @@
-"""Summarise per-config ncu --set full captures (gpurun_out/<tag>_ncu_cfgK.ncu-rep, the 2nd solve of
-tools/prof.py K 30 = 31 passes) into profiles/<tag>_ncu_configs.md and profiles/ncu_traffic.json.
+"""Summarise per-config ncu --set full captures (gpurun_out/<tag>_ncu_cfgK.ncu-rep: caches flushed
+between replays, ncu's default; gpurun_out/<tag>_ncuwarm_cfgK.ncu-rep: --cache-control none, the
+bench's warm-L2 condition), each the 2nd solve of tools/prof.py K 30 = 31 passes, into
+profiles/<tag>_ncu_configs.md and profiles/ncu_traffic.json (the warm capture's DRAM bytes when
+present -- bench.py's dram_frac -- with the commit the capture was taken on).
 usage: python tools/ncu_summary.py TAG [K ...]"""
 import csv, io, json, os, subprocess, sys
 
@@ -36,31 +39,42 @@ def main():
     import synth
     lines = [f"# {tag} -- ncu --set full per BASELINE config (solver kernel, 2nd solve of "
              f"tools/prof.py K 30 = {PASSES} passes)", "",
-             "| cfg | workload | µs/pass (profiled) | DRAM MB/pass | algorithmic MB/pass | DRAM/alg | L2 hit | "
+             "| cfg (L2 at replay) | workload | µs/pass (profiled) | DRAM MB/pass | algorithmic MB/pass | DRAM/alg | L2 hit | "
              "L1 hit | warps active | L2 thru | L1 thru |", "|---|---|---|---|---|---|---|---|---|---|---|"]
     traffic = []
+    head = subprocess.run(["git", "rev-parse", "--short=12", "HEAD"], capture_output=True, text=True,
+                          cwd=ROOT).stdout.strip()
     for c in cfgs:
         rep = os.path.join(ROOT, "gpurun_out", f"{tag}_ncu_cfg{c}.ncu-rep")
-        if not os.path.exists(rep):
+        repw = os.path.join(ROOT, "gpurun_out", f"{tag}_ncuwarm_cfg{c}.ncu-rep")
+        if not os.path.exists(rep) and not os.path.exists(repw):
             continue
-        d = raw(rep)
+        dc = raw(rep) if os.path.exists(rep) else None
+        dw = raw(repw) if os.path.exists(repw) else None
+        d = dw or dc
         if c == 1:
             n, nnz = 4096, 20224
         else:
             p = synth.config_problem(c) if c in (2, 3) else None
             n, nnz = {2: (2097152, 14581760), 5: (16777216, 449455096)}.get(c, (p.Q.n, p.Q.nnz) if p else (4000000, 80218976))
         alg = 12.0 * nnz + 56.0 * n + 4.0 * (n + 1)
-        dram = (d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]) / PASSES
-        lines.append(f"| {c} | {NAMES[c]} | {1e6 * d['gpu__time_duration.sum'] / PASSES:.1f} | {dram / 1e6:.1f} | "
-                     f"{alg / 1e6:.1f} | {dram / alg:.2f} | {d['lts__t_sector_hit_rate.pct']:.1f}% | "
-                     f"{d['l1tex__t_sector_hit_rate.pct']:.1f}% | {d['sm__warps_active.avg.pct_of_peak_sustained_active']:.1f}% | "
-                     f"{d['lts__throughput.avg.pct_of_peak_sustained_elapsed']:.1f}% | "
-                     f"{d['l1tex__throughput.avg.pct_of_peak_sustained_active']:.1f}% |")
-        traffic.append({"workload": NAMES[c], "kernel": d["kernel"], "passes_profiled": PASSES,
-                        "dram_bytes_read": d["dram__bytes_read.sum"], "dram_bytes_write": d["dram__bytes_write.sum"],
-                        "dram_bytes_per_pass": dram, "algorithmic_bytes_per_pass": alg,
-                        "source": f"ncu --set full --clock-control none on tools/prof.py {c} 30 (2nd solve); "
-                                  f"profiles/{tag}_ncu_configs.md"})
+        rec = {"workload": NAMES[c], "kernel": d["kernel"], "passes_profiled": PASSES,
+               "algorithmic_bytes_per_pass": alg, "capture": f"{tag} @ {head}"}
+        for kind, dd in (("cold", dc), ("warm", dw)):
+            if dd is None:
+                continue
+            dram = (dd["dram__bytes_read.sum"] + dd["dram__bytes_write.sum"]) / PASSES
+            lines.append(f"| {c} {kind} | {NAMES[c]} | {1e6 * dd['gpu__time_duration.sum'] / PASSES:.1f} | {dram / 1e6:.1f} | "
+                         f"{alg / 1e6:.1f} | {dram / alg:.2f} | {dd['lts__t_sector_hit_rate.pct']:.1f}% | "
+                         f"{dd['l1tex__t_sector_hit_rate.pct']:.1f}% | {dd['sm__warps_active.avg.pct_of_peak_sustained_active']:.1f}% | "
+                         f"{dd['lts__throughput.avg.pct_of_peak_sustained_elapsed']:.1f}% | "
+                         f"{dd['l1tex__throughput.avg.pct_of_peak_sustained_active']:.1f}% |")
+            rec[f"dram_bytes_per_pass_{kind}"] = dram
+            rec[f"us_per_pass_profiled_{kind}"] = 1e6 * dd["gpu__time_duration.sum"] / PASSES
+        rec["dram_bytes_per_pass"] = rec.get("dram_bytes_per_pass_warm", rec.get("dram_bytes_per_pass_cold"))
+        rec["source"] = (f"ncu --set full --clock-control none [--cache-control none for 'warm'] on tools/prof.py {c} 30 "
+                         f"(2nd solve); profiles/{tag}_ncu_configs.md")
+        traffic.append(rec)
     with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_configs.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")

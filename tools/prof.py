@@ -1,11 +1,9 @@
 """Profiling driver: one warm-up solve then one profiled solve (the 2nd ajm_solve_kernel launch).
-usage: python tools/prof.py CFG MAXIT [VARIANT]"""
+usage: python tools/prof.py CFG MAXIT"""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth, paper_2407_03272_b200 as ajm
 cfg = int(sys.argv[1]); maxit = int(sys.argv[2])
-if len(sys.argv) > 3:
-    os.environ["AJM_KVARIANT"] = sys.argv[3]
 p = synth.config_problem(cfg)
 with ajm.Solver.from_csr(p.Q, p.b) as s:
     for _ in range(2):
