@@ -206,6 +206,40 @@ ajm_status_t ajm_get_diag(ajm_handle_t h, double* out);
  * last block is padded with the identity.  Other handles: AJM_ERR_INVALID_ARG. */
 ajm_status_t ajm_get_jblock(ajm_handle_t h, double* out);
 
+/* Extreme eigenvalues of D^{-1} Q for the handle's metric D (AJM_D_QDIAG: the Jacobi metric diag(Q)
+ * of P:54-69, whose omega_opt = 2 / (lambda_min + lambda_max)(D^{-1} Q) is the optimal weight of
+ * weighted Jacobi, eq-weighted-jacobi P:61-69; AJM_D_JDIAG: J^{-1} Q, whose lambda_max <= 1 since
+ * S = J - Q is PSD). */
+typedef struct {
+    double lambda_min, lambda_max; /* extreme Ritz values of the Lanczos tridiagonal T_k            */
+    double err_min, err_max;       /* residual bounds beta_k |s_k|: |lambda - theta| <= err (each
+                                      extreme Ritz value is within err of an eigenvalue)            */
+    double omega_opt;              /* 2 / (lambda_min + lambda_max)                                 */
+    int64_t steps;                 /* k, the Lanczos steps in T_k (one SpMV pass each, plus one)    */
+    int32_t converged;             /* err_min, err_max <= tol * max(|lambda_min|, |lambda_max|)     */
+    int32_t breakdown;             /* beta_k = 0: an invariant subspace, the values are exact       */
+} ajm_spectrum_t;
+
+/*
+ * ajm_estimate_spectrum -- Lanczos on M = D^{-1} Q in the D-inner product (M is similar to the
+ * symmetric D^{-1/2} Q D^{-1/2}) without reorthogonalisation (the extreme Ritz values
+ * converge regardless), running on the handle's own SpMV: one fused persistent pass per step with
+ * the Lanczos recurrence in the epilogue, launched in chunks of passes; between
+ * chunks the host computes the extreme eigenvalues of T_k (Sturm bisection) and their residual
+ * bounds (inverse iteration), and stops once both bounds are <= tol * max|lambda| or at max_steps.
+ *   v0        : double[n] start vector (host/device, caller's row order), or NULL = a fixed
+ *               counter-based pseudo-random vector of `seed` (independent of the layout)
+ *   max_steps : 1 .. 2^20;  tol >= 0 (0: run max_steps)
+ *   out       : host, the estimate;  alpha, beta: host double[max_steps] or NULL, receive the
+ *               coefficients alpha_1..alpha_k (diagonal of T_k) and beta_1..beta_k
+ * Errors: AJM_ERR_UNSUPPORTED for AJM_D_JBLOCK handles; AJM_ERR_NONFINITE for a non-finite v0 or
+ * coefficient.  The handle's solver state is not touched (a workspace of 8 n-vectors is allocated
+ * on first use and kept).
+ */
+ajm_status_t ajm_estimate_spectrum(ajm_handle_t h, const double* v0, uint64_t seed, int64_t max_steps,
+                                   double tol, ajm_spectrum_t* out, double* alpha, double* beta,
+                                   void* cuda_stream);
+
 /* ajm_get_info -- layout and last-solve timing facts. */
 ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info);
 

@@ -14,6 +14,7 @@ Each function cites the passage it follows (PAPER.md = P, SPEC.md = S, DESIGN.md
   objective       f(x) = 1/2<x,Qx> - <b,x>
   rel_residual    ||b - Qx|| / ||b||                                   (P:505)
   solve           Alg. 3, s = 1, literal two-SpMV form                 (R5-R10, R19)
+  spectrum        extreme eigenvalues of D^{-1} Q and omega_opt = 2/(lmin + lmax)
 
 Pins: tests/test_oracle_pins.py ties every function above to something other than itself (SPEC
 worked values, dense Cholesky / pseudo-inverse solves, Thm 2.3 / Lemma 2.2 / Lemma 2.4 / Thm 2.5,
@@ -263,3 +264,45 @@ def solve(Q, b, D=None, x0=None, tol=1e-6, maxit=1000, momentum=True, restart=Tr
         res_hist=res_hist[:k], f_hist=f_hist[:k], d_hist=d_hist[:k], dabs_hist=dabs_hist[:k],
         xt_hist=None if xt_hist is None else xt_hist.reshape(m1, n)[:k],
         alpha_hist=None if alpha_hist is None else alpha_hist[:k])
+
+
+@dataclasses.dataclass
+class OracleSpectrum:
+    lambda_min: float
+    lambda_max: float
+    omega_opt: float
+    method: str
+
+
+def spectrum(Q, D=None, dmode: str = "qdiag", dense_max: int = 3000, tol: float = 1e-12) -> OracleSpectrum:
+    """Extreme eigenvalues of D^{-1} Q for a positive diagonal metric D (default D = diag(Q), the
+    Jacobi metric of P:54) and the optimal weighted-Jacobi weight
+        omega_opt = 2 / (lambda_min(D^{-1} Q) + lambda_max(D^{-1} Q))        (P:65-69).
+    D^{-1} Q is similar to the symmetric D^{-1/2} Q D^{-1/2}, whose eigenvalues are
+    computed by a library routine: LAPACK (numpy eigvalsh) on the dense matrix for n <= dense_max,
+    else ARPACK (scipy eigsh, Lanczos with implicit restarts) for the two ends to `tol`."""
+    if D is None:
+        D = build_jdiag(Q) if dmode == "jdiag" else diag(Q)
+    D = np.asarray(D, dtype=np.float64)
+    if not np.all(D > 0):
+        raise OracleError("the metric D must be positive")
+    s = 1.0 / np.sqrt(D)
+    n = int(Q.n)
+    if n <= dense_max:
+        A = np.zeros((n, n))
+        rows = np.repeat(np.arange(n), np.diff(np.asarray(Q.row_ptr)))
+        A[rows, np.asarray(Q.col)] = np.asarray(Q.val)
+        A = s[:, None] * A * s[None, :]
+        lam = np.linalg.eigvalsh(0.5 * (A + A.T))
+        lmin, lmax, method = float(lam[0]), float(lam[-1]), "dense eigvalsh"
+    else:
+        import scipy.sparse as sp
+        import scipy.sparse.linalg as spla
+        A = sp.csr_matrix((np.asarray(Q.val), np.asarray(Q.col), np.asarray(Q.row_ptr)), shape=(n, n))
+        A = sp.diags(s) @ A @ sp.diags(s)
+        lmax = float(spla.eigsh(A, k=1, which="LA", tol=tol, return_eigenvectors=False)[0])
+        # the low end by shift-and-invert around a point just below the spectrum (lmin >= 0: SPSD)
+        lmin = float(spla.eigsh(A, k=1, sigma=-1e-3 * lmax, which="LM", tol=tol,
+                                return_eigenvectors=False)[0])
+        method = "ARPACK eigsh"
+    return OracleSpectrum(lmin, lmax, 2.0 / (lmin + lmax), method)

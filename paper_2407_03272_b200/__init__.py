@@ -16,7 +16,7 @@ import os
 
 import numpy as np
 
-__all__ = ["AjmError", "Result", "Solver", "ajm_create", "ajm_solve", "ajm_destroy", "lib",
+__all__ = ["AjmError", "Result", "Solver", "Spectrum", "ajm_create", "ajm_solve", "ajm_destroy", "lib",
            "LIB_PATH", "STATUS_NAMES", "TERM_NAMES", "D_MODES", "model_bytes_per_iter"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libajm.so")
@@ -45,7 +45,8 @@ def AJM_JBLOCK_SIZE(bs: int) -> int:
 
 # every symbol include/ajm.h declares (tests check the .so exports all of them)
 ABI_SYMBOLS = ["ajm_create", "ajm_solve", "ajm_get_trace", "ajm_get_diag", "ajm_get_jblock",
-               "ajm_get_info", "ajm_destroy", "ajm_last_error", "ajm_abi_version"]
+               "ajm_estimate_spectrum", "ajm_get_info", "ajm_destroy", "ajm_last_error",
+               "ajm_abi_version"]
 
 
 class AjmError(RuntimeError):
@@ -81,6 +82,28 @@ class ajm_info_t(ctypes.Structure):
                 ("seg_nnz", ctypes.c_int64)]
 
 
+class ajm_spectrum_t(ctypes.Structure):
+    _fields_ = [("lambda_min", ctypes.c_double), ("lambda_max", ctypes.c_double),
+                ("err_min", ctypes.c_double), ("err_max", ctypes.c_double),
+                ("omega_opt", ctypes.c_double), ("steps", ctypes.c_int64),
+                ("converged", ctypes.c_int32), ("breakdown", ctypes.c_int32)]
+
+
+@dataclasses.dataclass
+class Spectrum:
+    """Extreme eigenvalues of D^{-1} Q (ajm_estimate_spectrum) and omega_opt = 2/(lmin + lmax)."""
+    lambda_min: float
+    lambda_max: float
+    err_min: float
+    err_max: float
+    omega_opt: float
+    steps: int
+    converged: bool
+    breakdown: bool
+    alpha: np.ndarray
+    beta: np.ndarray
+
+
 _lib = None
 
 
@@ -107,6 +130,10 @@ def lib():
         if hasattr(L, "ajm_get_jblock"):  # (AJM_LIB_OVERRIDE A/B builds may predate it)
             L.ajm_get_jblock.argtypes = [P, P]
             L.ajm_get_jblock.restype = ctypes.c_int
+        if hasattr(L, "ajm_estimate_spectrum"):
+            L.ajm_estimate_spectrum.argtypes = [P, P, ctypes.c_uint64, I64, ctypes.c_double,
+                                                ctypes.POINTER(ajm_spectrum_t), P, P, P]
+            L.ajm_estimate_spectrum.restype = ctypes.c_int
         L.ajm_get_info.argtypes = [P, ctypes.POINTER(ajm_info_t)]
         L.ajm_get_info.restype = ctypes.c_int
         L.ajm_destroy.argtypes = [P]
@@ -267,6 +294,22 @@ class Solver:
                       x_is_prerestart=bool(r.x_is_prerestart),
                       restart_iters=[int(v) for v in ri[: r.restarts_logged]],
                       res_hist=None if rh is None else rh[:k], f_hist=None if fh is None else fh[:k])
+
+    def estimate_spectrum(self, v0=None, seed: int = 0, max_steps: int = 2000, tol: float = 1e-8) -> Spectrum:
+        """Extreme eigenvalues of D^{-1} Q by Lanczos on the handle's own SpMV (ajm_estimate_spectrum)
+        and omega_opt = 2 / (lambda_min + lambda_max), the optimal weighted-Jacobi weight for
+        D = diag(Q) (create the solver with dmode="qdiag" for that metric)."""
+        out = ajm_spectrum_t()
+        a = np.zeros(max_steps)
+        b = np.zeros(max_steps)
+        p0, k0 = _ptr(v0, np.float64)
+        _check(lib().ajm_estimate_spectrum(ctypes.c_void_p(self.handle), p0, int(seed), int(max_steps),
+                                           float(tol), ctypes.byref(out), a.ctypes.data_as(ctypes.c_void_p),
+                                           b.ctypes.data_as(ctypes.c_void_p), _stream(self._stream)),
+               ctypes.c_void_p(self.handle))
+        k = int(out.steps)
+        return Spectrum(out.lambda_min, out.lambda_max, out.err_min, out.err_max, out.omega_opt, k,
+                        bool(out.converged), bool(out.breakdown), a[:k].copy(), b[:k].copy())
 
     def trace(self, which: str, count: int) -> np.ndarray:
         out = np.empty(count)

@@ -78,6 +78,22 @@ SolveFn jblock_fn(int bs, bool cluster) {
 SolveFn gmeta_fn(bool seg) { return seg ? ajm_solve_kernel<4, true, false, 0, true> : ajm_solve_kernel<4, false, false, 0, true>; }
 SolveFn cluster_fn(bool seg) { return seg ? ajm_solve_kernel<4, true, true> : ajm_solve_kernel<4, false, true>; }
 
+// The Lanczos twin (kLz) of a handle's solver kernel: same template arguments, same ring and shared
+// memory, Lanczos epilogue (ajm_estimate_spectrum).  Instantiated for the layouts create picks by
+// default; nullptr for block-J handles and experiment-only ring depths.
+SolveFn lanczos_fn(bool seg, bool cluster, bool gmeta, int col_bytes, int stages) {
+    if (cluster) return seg ? ajm_solve_kernel<4, true, true, 0, false, false, true> : ajm_solve_kernel<4, false, true, 0, false, false, true>;
+    if (gmeta) return seg ? ajm_solve_kernel<4, true, false, 0, true, false, true> : ajm_solve_kernel<4, false, false, 0, true, false, true>;
+    if (col_bytes == 1) {
+        if (stages == 4) return seg ? ajm_solve_kernel<4, true, false, 0, false, true, true> : ajm_solve_kernel<4, false, false, 0, false, true, true>;
+        if (stages == 5) return seg ? ajm_solve_kernel<5, true, false, 0, false, true, true> : ajm_solve_kernel<5, false, false, 0, false, true, true>;
+        return nullptr;
+    }
+    if (stages == 3) return seg ? ajm_solve_kernel<3, true, false, 0, false, false, true> : ajm_solve_kernel<3, false, false, 0, false, false, true>;
+    if (stages == 4) return seg ? ajm_solve_kernel<4, true, false, 0, false, false, true> : ajm_solve_kernel<4, false, false, 0, false, false, true>;
+    return nullptr;
+}
+
 constexpr int kBlockThreads = AJM_BLOCK + 32;  // consumer warps + the TMA producer warp
 
 // Kernel attributes (max dynamic shared memory, carve-out) belong to the kernel, which every handle
@@ -116,6 +132,8 @@ struct ajm_ctx {
     int* perm_fwd = nullptr;        // [n] internal (layout) index -> caller's row
     int* perm_inv = nullptr;        // [n] caller's row -> internal index
     SolveFn fn = nullptr;
+    SolveFn fn_lz = nullptr;           // Lanczos twin of fn (ajm_estimate_spectrum), or nullptr
+    double* lzw = nullptr;             // Lanczos workspace: p x3, Qp x3, g x2 (n_pad each)
     size_t dyn_smem = 0;
     int64_t nunits = 0;
     int meta_units = 0, meta_chunks = 0;
@@ -289,7 +307,7 @@ void free_all(ajm_ctx* h) {
                     h->seg_split, h->seg_part, h->split_row, h->split_seg0, h->split_cnt,
                     h->cta_split, h->owner_split, h->unit_c0, h->cta_seg, h->seg_list, h->cta_unit, h->partials, h->ctrl,
                     h->hist, h->scratch, h->err, h->ts, h->perm_fwd, h->perm_inv, h->b_in, h->Jblk, h->Jinv, h->seg_order, h->seg_grp,
-                    h->g_uc0, h->g_coff, h->g_ubase, h->g_cbase, h->scode, h->ctab, h->seg_meta};
+                    h->g_uc0, h->g_coff, h->g_ubase, h->g_cbase, h->scode, h->ctab, h->seg_meta, h->lzw};
     for (void* p : ptrs) dfree(p);
     if (h->persist_holder) {  // the last holder restores the limit and drops the persisting lines
         std::lock_guard<std::mutex> lock(g_attr_mu);
@@ -365,13 +383,16 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
 
 // cooperative launch of the persistent solver kernel, with the L2 access-policy window over the
 // iterate vectors (persisting hits, streaming misses)
-cudaError_t launch_solver(ajm_ctx* h, AjmPass& p, cudaStream_t st) {
+cudaError_t launch_solver(ajm_ctx* h, AjmPass& p, cudaStream_t st, SolveFn fn = nullptr) {
+    if (!fn) fn = h->fn;
     // the attributes belong to the kernel, which other handles share: set this handle's own, and
     // launch before another thread's handle can change them (the launch itself is asynchronous)
     std::lock_guard<std::mutex> lock(g_attr_mu);
-    cudaError_t e = cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem);
+    cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributePreferredSharedMemoryCarveout, h->carveout);
+        e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributePreferredSharedMemoryCarveout, h->carveout);
+    if (e == cudaSuccess && h->cluster && h->grid > 8)
+        e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(h->grid);
@@ -400,7 +421,7 @@ cudaError_t launch_solver(ajm_ctx* h, AjmPass& p, cudaStream_t st) {
     }
     cfg.attrs = at;
     cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, h->fn, p);
+    return cudaLaunchKernelEx(&cfg, fn, p);
 }
 
 ajm_status_t ensure_hist(ajm_ctx* h, int64_t need, cudaStream_t st) {
@@ -413,6 +434,88 @@ ajm_status_t ensure_hist(ajm_ctx* h, int64_t need, cudaStream_t st) {
     AJM_CUDA(h, dalloc(&h->hist, (size_t)cap * 4, st));
     h->hist_cap = cap;
     return AJM_OK;
+}
+
+// ---- symmetric tridiagonal T_k (Lanczos coefficients) on the host: k <= a few thousand ----
+// Sturm count: eigenvalues of T (diag a[0..k), off-diagonal b[0..k-1)) strictly below x
+int tri_sturm(const std::vector<double>& a, const std::vector<double>& b, int k, double x) {
+    int cnt = 0;
+    double d = 1.0;
+    for (int i = 0; i < k; ++i) {
+        const double bb = i ? b[(size_t)i - 1] * b[(size_t)i - 1] : 0.0;
+        d = a[(size_t)i] - x - (i ? bb / d : 0.0);
+        if (d == 0.0) d = -1e-300;  // x is (numerically) an eigenvalue: count it as below
+        if (d < 0.0) ++cnt;
+    }
+    return cnt;
+}
+
+// the m-th smallest eigenvalue (m = 0 .. k-1) by bisection on the Sturm count, to full precision
+double tri_eig(const std::vector<double>& a, const std::vector<double>& b, int k, int m) {
+    double lo = a[0], hi = a[0];
+    for (int i = 0; i < k; ++i) {  // Gershgorin
+        const double r = (i ? std::fabs(b[(size_t)i - 1]) : 0.0) + (i + 1 < k ? std::fabs(b[(size_t)i]) : 0.0);
+        lo = std::min(lo, a[(size_t)i] - r);
+        hi = std::max(hi, a[(size_t)i] + r);
+    }
+    for (int it = 0; it < 200; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (mid <= lo || mid >= hi) break;
+        if (tri_sturm(a, b, k, mid) > m) hi = mid;
+        else lo = mid;
+    }
+    return 0.5 * (lo + hi);
+}
+
+// |last component| of the unit eigenvector of T for the eigenvalue theta: two steps of inverse
+// iteration with a tridiagonal LU with partial pivoting (shift perturbed off the exact eigenvalue)
+double tri_last_component(const std::vector<double>& a, const std::vector<double>& b, int k, double theta) {
+    if (k == 1) return 1.0;
+    double scale = 0.0;
+    for (int i = 0; i < k; ++i) scale = std::max(scale, std::fabs(a[(size_t)i]) + (i + 1 < k ? std::fabs(b[(size_t)i]) : 0.0));
+    const double sh = theta + 1e-13 * std::max(scale, 1e-300);
+    std::vector<double> y((size_t)k, 1.0);
+    for (int rep = 0; rep < 3; ++rep) {
+        // (T - sh I) x = y: rows i of the banded system, partial pivoting (dgtsv-style)
+        std::vector<double> dl((size_t)k, 0.0), d((size_t)k), du((size_t)k, 0.0), du2((size_t)k, 0.0), x = y;
+        for (int i = 0; i < k; ++i) {
+            d[(size_t)i] = a[(size_t)i] - sh;
+            if (i + 1 < k) { du[(size_t)i] = b[(size_t)i]; dl[(size_t)i] = b[(size_t)i]; }
+        }
+        for (int i = 0; i + 1 < k; ++i) {
+            if (std::fabs(d[(size_t)i]) >= std::fabs(dl[(size_t)i])) {  // no interchange
+                if (d[(size_t)i] == 0.0) d[(size_t)i] = 1e-300;
+                const double f = dl[(size_t)i] / d[(size_t)i];
+                d[(size_t)i + 1] -= f * du[(size_t)i];
+                x[(size_t)i + 1] -= f * x[(size_t)i];
+                du2[(size_t)i] = 0.0;
+            } else {  // swap rows i and i+1
+                const double f = d[(size_t)i] / dl[(size_t)i];
+                d[(size_t)i] = dl[(size_t)i];
+                const double tmp = d[(size_t)i + 1];
+                d[(size_t)i + 1] = du[(size_t)i] - f * tmp;
+                if (i + 2 < k) {
+                    du2[(size_t)i] = du[(size_t)i + 1];
+                    du[(size_t)i + 1] = -f * du2[(size_t)i];
+                }
+                du[(size_t)i] = tmp;
+                const double tx = x[(size_t)i];
+                x[(size_t)i] = x[(size_t)i + 1];
+                x[(size_t)i + 1] = tx - f * x[(size_t)i + 1];
+            }
+        }
+        if (d[(size_t)k - 1] == 0.0) d[(size_t)k - 1] = 1e-300;
+        x[(size_t)k - 1] /= d[(size_t)k - 1];
+        if (k >= 2) x[(size_t)k - 2] = (x[(size_t)k - 2] - du[(size_t)k - 2] * x[(size_t)k - 1]) / d[(size_t)k - 2];
+        for (int i = k - 3; i >= 0; --i)
+            x[(size_t)i] = (x[(size_t)i] - du[(size_t)i] * x[(size_t)i + 1] - du2[(size_t)i] * x[(size_t)i + 2]) / d[(size_t)i];
+        double nrm = 0.0;
+        for (double v : x) nrm += v * v;
+        nrm = std::sqrt(nrm);
+        if (!(nrm > 0.0) || !std::isfinite(nrm)) return 1.0;  // no information: the worst case
+        for (int i = 0; i < k; ++i) y[(size_t)i] = x[(size_t)i] / nrm;
+    }
+    return std::fabs(y[(size_t)k - 1]);
 }
 
 }  // namespace
@@ -1349,6 +1452,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         h->col = nullptr;
         h->val = nullptr;
     }
+    if (!h->jbs) h->fn_lz = lanczos_fn(h->nseg > 0, h->cluster != 0, h->gmeta != 0, h->col_bytes, h->ring_stages);
     mark("validate+fill+norm", st);
     if (tsc) fprintf(stderr, "[ajm create ms]%s\n", tsc_log.c_str());
     *out = h;
@@ -1520,6 +1624,125 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
         res->x_is_prerestart = c.s.prerestart;
         res->restarts_logged = (int32_t)nlog;
     }
+    return AJM_OK;
+}
+
+ajm_status_t ajm_estimate_spectrum(ajm_handle_t h, const double* v0, uint64_t seed, int64_t max_steps,
+                                   double tol, ajm_spectrum_t* out, double* alpha, double* beta,
+                                   void* cuda_stream) {
+    NvtxScope nvtx_scope_("ajm_estimate_spectrum");
+    if (!h) return fail(nullptr, AJM_ERR_INVALID_ARG, "NULL handle");
+    h->err_msg.clear();
+    if (!out) return fail(h, AJM_ERR_INVALID_ARG, "out is NULL");
+    if (max_steps < 1 || max_steps > (1 << 20)) return fail(h, AJM_ERR_INVALID_ARG, "max_steps must be in [1, 2^20]");
+    if (!(tol >= 0.0)) return fail(h, AJM_ERR_INVALID_ARG, "tol must be >= 0");
+    if (!h->fn_lz)
+        return fail(h, AJM_ERR_UNSUPPORTED, "no Lanczos pass for this layout (block-J handles, experiment ring depths)");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const int64_t n = h->n;
+    const size_t np = (size_t)h->n_pad;
+    if (!h->lzw) AJM_CUDA(h, dalloc(&h->lzw, 8 * np, st));
+    AJM_CUDA(h, cudaMemsetAsync(h->lzw, 0, sizeof(double) * 8 * np, st));
+    double* Lg0 = h->lzw + 6 * np;
+    // start vector in the g buffer 0 (internal order)
+    if (v0) {
+        const cudaMemcpyKind k = kind_to_device(v0);
+        if (h->relabel) {
+            AJM_CUDA(h, cudaMemcpyAsync(h->lzw + 7 * np, v0, sizeof(double) * n, k, st));
+            ajm_gather_kernel<<<1024, 256, 0, st>>>(n, h->perm_fwd, h->lzw + 7 * np, Lg0);
+            AJM_CUDA(h, cudaGetLastError());
+        } else {
+            AJM_CUDA(h, cudaMemcpyAsync(Lg0, v0, sizeof(double) * n, k, st));
+        }
+        AJM_CUDA(h, cudaMemsetAsync(h->err, 0, sizeof(int), st));
+        ajm_finite_kernel<<<1024, 256, 0, st>>>(n, Lg0, h->err);
+        AJM_CUDA(h, cudaGetLastError());
+        int herr = 0;
+        AJM_CUDA(h, cudaMemcpyAsync(&herr, h->err, sizeof(int), cudaMemcpyDeviceToHost, st));
+        AJM_CUDA(h, cudaStreamSynchronize(st));
+        if (herr) return fail(h, AJM_ERR_NONFINITE, "v0 has a non-finite entry");
+        AJM_CUDA(h, cudaMemsetAsync(h->lzw + 7 * np, 0, sizeof(double) * np, st));
+    } else {
+        ajm_start_vector_kernel<<<1024, 256, 0, st>>>(n, h->relabel ? h->perm_fwd : nullptr, seed, Lg0);
+        AJM_CUDA(h, cudaGetLastError());
+    }
+    // passes: pass 0 normalises the start, pass j >= 1 is Lanczos step j; T_k needs k + 1 passes
+    // (alpha_1..alpha_k and beta_1..beta_k, the last one for the residual bounds)
+    const int64_t passes = max_steps + 1;
+    {
+        const ajm_status_t hs = ensure_hist(h, passes + 2, st);
+        if (hs != AJM_OK) return hs;
+    }
+    double* ha = h->hist;                 // alpha_{t+1} at [t]
+    double* hb = h->hist + h->hist_cap;   // beta_t at [t] (t = 0: ||v0||_D)
+    if (h->nsplit) AJM_CUDA(h, cudaMemsetAsync(h->split_cnt, 0, sizeof(unsigned) * h->nsplit, st));
+    ajm_init_lanczos_kernel<<<1, 32, 0, st>>>(h->ctrl, passes, ha, hb, h->hist + 2 * h->hist_cap,
+                                              h->hist + 3 * h->hist_cap);
+    AJM_CUDA(h, cudaGetLastError());
+    AjmPass p = make_pass(h, 0);
+    p.Lp0 = h->lzw;
+    p.Lp1 = h->lzw + np;
+    p.Lp2 = h->lzw + 2 * np;
+    p.Lq0 = h->lzw + 3 * np;
+    p.Lq1 = h->lzw + 4 * np;
+    p.Lq2 = h->lzw + 5 * np;
+    p.Lg0 = Lg0;
+    p.Lg1 = h->lzw + 7 * np;
+    std::vector<double> va, vb;
+    int64_t done_passes = 0, chunk = 32;
+    ajm_spectrum_t r = {};
+    AJM_CUDA(h, cudaEventRecord(h->ev0, st));
+    int64_t launches = 0;
+    for (;;) {
+        // a chunk of passes in one persistent launch; the state continues across launches
+        p.max_passes = (int)std::min<int64_t>(chunk, passes - done_passes);
+        AJM_CUDA(h, launch_solver(h, p, st, h->fn_lz));
+        ++launches;
+        AJM_CUDA(h, cudaMemcpyAsync(h->h_ctrl, h->ctrl, sizeof(AjmCtrl), cudaMemcpyDeviceToHost, st));
+        AJM_CUDA(h, cudaStreamSynchronize(st));
+        const AjmCtrl& c = *h->h_ctrl;
+        if (c.timeout_flag) return fail(h, AJM_ERR_CUDA, "device barrier wait timed out (internal error)");
+        done_passes = c.s.iterations;
+        va.resize((size_t)done_passes);
+        vb.resize((size_t)done_passes);
+        AJM_CUDA(h, cudaMemcpy(va.data(), ha, sizeof(double) * done_passes, cudaMemcpyDeviceToHost));
+        AJM_CUDA(h, cudaMemcpy(vb.data(), hb, sizeof(double) * done_passes, cudaMemcpyDeviceToHost));
+        if (c.s.done && c.s.status == 2) return fail(h, AJM_ERR_NONFINITE, "non-finite Lanczos coefficient");
+        const bool breakdown = c.s.done && c.s.status == 0;  // beta = 0: invariant subspace
+        // T_k: alpha_1..alpha_k = va[0..k), beta_1..beta_{k-1} = vb[1..k), residual coefficient
+        // beta_k = vb[k] (0 at a breakdown)
+        const int k = (int)(breakdown ? done_passes : done_passes - 1);
+        if (k >= 1) {
+            std::vector<double> ta(va.begin(), va.begin() + k), tb;
+            for (int i = 1; i < k; ++i) tb.push_back(vb[(size_t)i]);
+            tb.push_back(0.0);
+            const double bk = breakdown ? 0.0 : vb[(size_t)k];
+            const double lmin = tri_eig(ta, tb, k, 0), lmax = tri_eig(ta, tb, k, k - 1);
+            r.lambda_min = lmin;
+            r.lambda_max = lmax;
+            r.err_min = bk * tri_last_component(ta, tb, k, lmin);
+            r.err_max = bk * tri_last_component(ta, tb, k, lmax);
+            r.steps = k;
+            r.breakdown = breakdown ? 1 : 0;
+            const double scale = std::max(std::fabs(lmax), std::fabs(lmin));
+            r.converged = (r.err_min <= tol * scale && r.err_max <= tol * scale) ? 1 : 0;
+            r.omega_opt = 2.0 / (lmin + lmax);
+            if (r.converged || breakdown) break;
+        }
+        if (c.s.done || done_passes >= passes) break;
+        chunk = std::min<int64_t>(2 * chunk, 1024);
+    }
+    AJM_CUDA(h, cudaEventRecord(h->ev1, st));
+    AJM_CUDA(h, cudaEventSynchronize(h->ev1));
+    float ms = 0.f;
+    AJM_CUDA(h, cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    h->last_loop_ms = ms;
+    h->last_passes = done_passes;
+    h->last_launches = launches;
+    const int64_t kk = std::min<int64_t>(r.steps, done_passes);
+    if (alpha) for (int64_t i = 0; i < kk; ++i) alpha[i] = va[(size_t)i];
+    if (beta) for (int64_t i = 0; i < kk; ++i) beta[i] = (size_t)i + 1 < vb.size() ? vb[(size_t)i + 1] : 0.0;
+    *out = r;
     return AJM_OK;
 }
 

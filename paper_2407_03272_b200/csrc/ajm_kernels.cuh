@@ -63,6 +63,14 @@ struct AjmState {
     int answer;         // buffer index holding the answer when done
     int prerestart;
     int nres, nlogged;
+    // Lanczos mode (ajm_estimate_spectrum, kLz): p/q buffers rotate through cur/prev/fre, the
+    // gathered g buffers through gcur; every stored vector carries a scale applied on reading
+    int gcur;
+    double lz_alpha;    // alpha_j of the current pass's three-term recurrence
+    double lz_beta;     // beta_{j-1}
+    double lz_sg;       // scale of the gathered g buffer (g = M p^_j = D^{-1} Q p^_j)
+    double lz_sp;       // scale of the p/q buffers cur (p^_j, Q p^_j)
+    double lz_spp;      // scale of the p/q buffers prev (p^_{j-1}, Q p^_{j-1})
 };
 
 struct AjmCtrl {
@@ -132,6 +140,10 @@ struct AjmPass {
     const uint8_t* __restrict__ scode;       // (kCol8) SELL column codes: col = row + ctab[code]
     const int* __restrict__ ctab;            // (kCol8) [256] distinct offsets col - row, ascending
     const int4* __restrict__ seg_meta;       // static plan: {row, k0, k1, split} of seg_list[k]
+    // Lanczos mode (kLz): rotating p / Q p buffers and the two gathered g = D^{-1} Q p buffers
+    double* Lp0; double* Lp1; double* Lp2;
+    double* Lq0; double* Lq1; double* Lq2;
+    double* Lg0; double* Lg1;
 };
 
 __device__ __forceinline__ unsigned long long ajm_gtime() {
@@ -363,6 +375,77 @@ __device__ void ajm_control_step(AjmState& s, const double* tot, AjmCtrl* c, boo
     }
     s.restart_t = rs;
     s.t = tn;
+}
+
+// ---- Lanczos mode (ajm_estimate_spectrum; NEXT-3: omega_opt of weighted Jacobi) ----
+// Lanczos on M = D^{-1} Q, self-adjoint in the D-inner product <u, v>_D = u^T D v (M is similar to
+// the symmetric D^{-1/2} Q D^{-1/2}), with ONE SpMV per step, as in the AJM pass: pass j
+// multiplies the stored g_j = M p^_j (so the SpMV gives Q g_j) and, by linearity,
+//   z   = M p^_j - alpha_j p^_j - beta_{j-1} p^_{j-1}          ( = beta_j p^_{j+1} )
+//   Q z = Q g_j  - alpha_j Q p^_j - beta_{j-1} Q p^_{j-1}
+// per row, with Q p^_j, Q p^_{j-1} stored by the previous passes.  Partials A = <z, Q z>,
+// B = <z, z>_D give beta_j = sqrt(B) and alpha_{j+1} = A / B after the grid barrier; z, Q z and
+// g_{j+1} = Q z / D are stored unnormalised and scaled by 1/beta_j when read (the pass that writes
+// them does not know beta_j yet).  Pass 0 runs the same epilogue on the start vector (z = x0).
+struct AjmLz {
+    const double* pc; const double* pp; const double* qc; const double* qp;
+    double* pn; double* qn; double* gn;
+    double sg, c1, c2;  // scale of the gathered g; alpha_j * scale(p cur); beta_{j-1} * scale(p prev)
+};
+
+__device__ __forceinline__ double* ajm_lsel(double* a, double* b, double* c, int k) {
+    return k == 0 ? a : (k == 1 ? b : c);
+}
+
+__device__ __forceinline__ void ajm_row_lanczos(const AjmLz& L, int i, double qg, double Di, double gi,
+                                                double pci, double ppi, double qci, double qpi, AjmAcc& a) {
+    const double z = L.sg * gi - L.c1 * pci - L.c2 * ppi;
+    const double Qz = L.sg * qg - L.c1 * qci - L.c2 * qpi;
+    L.pn[i] = z;
+    L.qn[i] = Qz;
+    L.gn[i] = Qz / Di;
+    a.rr += z * Qz;      // A = <z, Q z>
+    a.xq += Di * z * z;  // B = <z, z>_D
+}
+
+__device__ __forceinline__ void ajm_row_lanczos_ld(const AjmPass& p, const AjmLz& L, const double* g, int i,
+                                                   double qg, AjmAcc& a) {
+    ajm_row_lanczos(L, i, qg, p.D[i], ajm_ld(g + i), ajm_ld(L.pc + i), ajm_ld(L.pp + i), ajm_ld(L.qc + i),
+                    ajm_ld(L.qp + i), a);
+}
+
+// Lanczos control step (thread 0 of every CTA, identical inputs -> identical outputs; CTA 0 writes
+// the coefficient histories: res_hist[t] = alpha_{t+1}, f_hist[t] = beta_t (t = 0: ||x0||_D)).
+__device__ void ajm_lanczos_control(AjmState& s, const double* tot, AjmCtrl* c, bool writer) {
+    const long long t = s.t;
+    const double A = tot[0], B = tot[1];
+    const double beta = sqrt(B);
+    const double alpha = A / B;
+    if (writer) {
+        c->res_hist[t] = alpha;
+        c->f_hist[t] = beta;
+    }
+    s.iterations = t + 1;  // passes run
+    if (!(B > 0.0) || !isfinite(B) || !isfinite(A)) {  // exact breakdown (invariant subspace) / failure
+        s.done = 1;
+        s.status = (B == 0.0) ? 0 : 2;
+        return;
+    }
+    const int cur = s.cur, prev = s.prev, fre = s.fre;
+    s.prev = cur;
+    s.cur = fre;
+    s.fre = prev;
+    s.gcur ^= 1;
+    s.lz_spp = s.lz_sp;
+    s.lz_sp = 1.0 / beta;
+    s.lz_sg = 1.0 / beta;
+    s.lz_alpha = alpha;
+    s.lz_beta = beta;
+    s.t = t + 1;
+    if (s.t >= s.maxit) {
+        s.done = 1;
+        s.status = 1;
+    }
 }
 
 // Grid barrier over all CTAs of the cooperative launch: a monotone 64-bit arrival counter (reset
@@ -597,8 +680,10 @@ __device__ __forceinline__ double ajm_ld_cluster(const double* local, unsigned r
 //   on the host) instead of being staged in shared memory -- for layouts whose tables do not fit
 //   next to the ring (hundreds of millions of rows).
 // kCol8 = true: byte-coded SELL columns (col = row + ctab[code]).
+// kLz = true: the Lanczos pass of ajm_estimate_spectrum (same SpMV, epilogue ajm_row_lanczos,
+//   control ajm_lanczos_control) instead of the AJM pass.
 template <int kStages, bool kSeg = true, bool kCluster = false, int kJB = 0, bool kGMeta = false,
-          bool kCol8 = false>
+          bool kCol8 = false, bool kLz = false>
 __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
     extern __shared__ __align__(128) unsigned char s_dyn[];
     __shared__ double s_red[AJM_WARPS][AJM_NPART];
@@ -715,7 +800,20 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
         const long long t = s_st.t;
         const int restart_t = s_st.restart_t;
         const double beta = s_st.beta;
-        const double* xc = ajm_sel(p, s_st.cur);
+        AjmLz L;
+        if constexpr (kLz) {
+            L.pc = ajm_lsel(p.Lp0, p.Lp1, p.Lp2, s_st.cur);
+            L.pp = ajm_lsel(p.Lp0, p.Lp1, p.Lp2, s_st.prev);
+            L.pn = ajm_lsel(p.Lp0, p.Lp1, p.Lp2, s_st.fre);
+            L.qc = ajm_lsel(p.Lq0, p.Lq1, p.Lq2, s_st.cur);
+            L.qp = ajm_lsel(p.Lq0, p.Lq1, p.Lq2, s_st.prev);
+            L.qn = ajm_lsel(p.Lq0, p.Lq1, p.Lq2, s_st.fre);
+            L.gn = s_st.gcur ? p.Lg0 : p.Lg1;
+            L.sg = s_st.lz_sg;
+            L.c1 = s_st.lz_alpha * s_st.lz_sp;
+            L.c2 = s_st.lz_beta * s_st.lz_spp;
+        }
+        const double* xc = kLz ? (s_st.gcur ? p.Lg1 : p.Lg0) : ajm_sel(p, s_st.cur);
         const double* xp = ajm_sel(p, s_st.prev);
         double* xf = ajm_sel(p, s_st.fre);
         AjmAcc acc = {0.0, 0.0, 0.0, 0.0, 0.0};
@@ -746,7 +844,8 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
                 const double s = ajm_seg_dot(p, cm.y, cm.z, xc, lane);
                 if (lane == 0) {
                     if (cm.w < 0) {
-                        ajm_row_epilogue(p, cm.x, s, beta, restart_t, xc, xp, xf, acc);
+                        if constexpr (kLz) ajm_row_lanczos_ld(p, L, xc, cm.x, s, acc);
+                        else ajm_row_epilogue(p, cm.x, s, beta, restart_t, xc, xp, xf, acc);
                     } else {
                         __stcg(p.seg_part + csg, s);
                         __threadfence();
@@ -771,7 +870,8 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
                 const int sidx = __ldg(p.seg_split + sg);
                 if (lane == 0) {
                     if (sidx < 0) {
-                        ajm_row_epilogue(p, row, s, beta, restart_t, xc, xp, xf, acc);
+                        if constexpr (kLz) ajm_row_lanczos_ld(p, L, xc, row, s, acc);
+                        else ajm_row_epilogue(p, row, s, beta, restart_t, xc, xp, xf, acc);
                     } else {
                         __stcg(p.seg_part + sg, s);
                         __threadfence();
@@ -797,13 +897,22 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
                     const int w = (s_coff[j + 1] - e0) >> 5;
                     const int slot = (cfirst + j) * 32 + lane;
                     const int row = slot < p.n_sell ? slot : -1;  // SELL slot == internal row
-                    double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
+                    double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0, lqp = 0.0;
                     if (row >= 0) {  // operands in flight during the stage wait
-                        bi = ajm_ldp(p.b + row, vpol);
-                        if (!jblk) Di = ajm_ldp(p.D + row, vpol);
-                        xt = ajm_ld(xc + row);
-                        xpi = ajm_ld(xp + row);
-                        qxp = ajm_ldp(p.Qxp + row, vpol);
+                        if constexpr (kLz) {  // (bi, xpi, qxp, lqp) = (p^_j, p^_{j-1}, Q p^_j, Q p^_{j-1})
+                            Di = p.D[row];
+                            xt = ajm_ld(xc + row);
+                            bi = ajm_ld(L.pc + row);
+                            xpi = ajm_ld(L.pp + row);
+                            qxp = ajm_ld(L.qc + row);
+                            lqp = ajm_ld(L.qp + row);
+                        } else {
+                            bi = ajm_ldp(p.b + row, vpol);
+                            if (!jblk) Di = ajm_ldp(p.D + row, vpol);
+                            xt = ajm_ld(xc + row);
+                            xpi = ajm_ld(xp + row);
+                            qxp = ajm_ldp(p.Qxp + row, vpol);
+                        }
                     }
                     constexpr int JV = kJB > 0 ? kJB : 8;
                     double jv[JV];  // (jblk) this row's first entries of J^{-1}, also in flight
@@ -818,7 +927,9 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
                     const double q = kCol8 ? ajm_chunk_dot8(st_val(stage) + off, st_code(stage) + off, w,
                                                             xc + (row >= 0 ? row : 0), s_ctab)
                                            : ajm_chunk_dot<kCluster>(st_val(stage) + off, st_col(stage) + off, w, xc);
-                    if (jblk)  // every lane takes part (shuffles); tail lanes store nothing
+                    if constexpr (kLz) {
+                        if (row >= 0) ajm_row_lanczos(L, row, q, Di, xt, bi, xpi, qxp, lqp, acc);
+                    } else if (jblk)  // every lane takes part (shuffles); tail lanes store nothing
                         ajm_row_update_blk<(kJB > 0 ? kJB : 0)>(p.Qxp, xf, row, q, bi, jr, jbs, jv, xt, xpi, qxp,
                                                                 beta, restart_t, acc, vpol, xpol);
                     else if (row >= 0)
@@ -848,7 +959,8 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
             }
             double q = 0.0;
             for (int g = g0; g < g1; ++g) q += __ldcg(p.seg_part + g);
-            ajm_row_epilogue(p, __ldg(p.split_row + sidx), q, beta, restart_t, xc, xp, xf, acc);
+            if constexpr (kLz) ajm_row_lanczos_ld(p, L, xc, __ldg(p.split_row + sidx), q, acc);
+            else ajm_row_epilogue(p, __ldg(p.split_row + sidx), q, beta, restart_t, xc, xp, xf, acc);
         }
         }
         // (4) CTA partial -> grid barrier -> every CTA reduces all partials in the same order
@@ -926,7 +1038,8 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
         if (tsw) p.ts[pass * 8 + 4] = ajm_gtime();
         if (tid == 0) {
             AjmState ls = s_st;  // the control step on a register copy of the shared state
-            ajm_control_step(ls, s_tot, c, bid == 0, an_c, beta_c, s_res);
+            if constexpr (kLz) ajm_lanczos_control(ls, s_tot, c, bid == 0);
+            else ajm_control_step(ls, s_tot, c, bid == 0, an_c, beta_c, s_res);
             s_st = ls;
             if (timed_out) s_st.done = 1;
             if (tsw) p.ts[pass * 8 + 5] = ajm_gtime();
@@ -1381,4 +1494,51 @@ __global__ void ajm_init_ctrl_kernel(AjmCtrl* c, double tol, long long maxit, in
     c->timeout_flag = 0;
     d_hist[0] = 0.0;
     dabs_hist[0] = 0.0;
+}
+
+// ---- Lanczos (ajm_estimate_spectrum) setup ----
+// Default start vector: a counter-based hash (splitmix64) of (seed, the caller's row index) mapped
+// to U(-1, 1), so the start -- and every Lanczos coefficient -- is independent of the layout's
+// internal row order.
+__global__ void ajm_start_vector_kernel(long long n, const int* __restrict__ perm_fwd, unsigned long long seed,
+                                        double* __restrict__ x) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        unsigned long long z = seed + 0x9E3779B97F4A7C15ull * (unsigned long long)((perm_fwd ? perm_fwd[i] : i) + 1);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        x[i] = 2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0;
+    }
+}
+
+// Control block of a Lanczos run: t = 0 (pass 0 multiplies the start vector, held in the g buffer
+// 0 with scale 1), p/q buffers 0/1/2 as cur/prev/fre with scale 0 (p^_0 = p^_{-1} = 0),
+// histories res_hist = alpha, f_hist = beta; `passes` passes in total.
+__global__ void ajm_init_lanczos_kernel(AjmCtrl* c, long long passes, double* alpha_hist, double* beta_hist,
+                                        double* d_hist, double* dabs_hist) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    AjmState& s = c->s;
+    s = AjmState{};
+    s.t = 0;
+    s.maxit = passes;
+    s.iterations = 0;
+    s.nb = 1.0;
+    s.cur = 0;
+    s.prev = 1;
+    s.fre = 2;
+    s.gcur = 0;
+    s.lz_sg = 1.0;
+    s.lz_sp = 0.0;
+    s.lz_spp = 0.0;
+    s.lz_alpha = 0.0;
+    s.lz_beta = 0.0;
+    s.done = 0;
+    s.status = 1;
+    c->res_hist = alpha_hist;
+    c->f_hist = beta_hist;
+    c->d_hist = d_hist;
+    c->dabs_hist = dabs_hist;
+    c->bar_count = 0ull;
+    c->seg_q[0] = c->seg_q[1] = 0u;
+    c->timeout_flag = 0;
 }

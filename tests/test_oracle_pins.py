@@ -91,6 +91,70 @@ def test_golden_omega_opt(golden):
 
 
 # ------------------------------------------------------------------------------------------------
+# spectrum / omega_opt
+# ------------------------------------------------------------------------------------------------
+
+def test_spectrum_golden_and_sdd_closed_form(golden):
+    """§4.1 matrix with D = diag(Q) = nI: D^{-1}Q has eigenvalues 1/n and (n+1)/n, so omega_opt =
+    2n/(n+2) (golden 4/3 at n = 4)."""
+    for e in golden["omega_opt"]:
+        r = oracle.spectrum(synth.sdd(e["n"]))
+        assert r.omega_opt == pytest.approx(e["expected"], rel=1e-12), e["cite"]
+    for n in (4, 50, 700):
+        r = oracle.spectrum(synth.sdd(n))
+        assert r.lambda_min == pytest.approx(1 / n, rel=1e-11)
+        assert r.lambda_max == pytest.approx((n + 1) / n, rel=1e-12)
+        assert r.omega_opt == pytest.approx(2 * n / (n + 2), rel=1e-12)
+
+
+def _poisson_closed_form(m, dim):
+    """Dirichlet Laplacian on an m^dim grid, D = diag(Q) = 2 dim I: the eigenvalues of D^{-1}Q are
+    (1/(2 dim)) sum_a 4 sin^2(k_a pi / (2(m+1))), k_a = 1..m."""
+    s = 4 * np.sin(np.arange(1, m + 1) * np.pi / (2 * (m + 1))) ** 2
+    return dim * s[0] / (2 * dim), dim * s[-1] / (2 * dim)
+
+
+@pytest.mark.parametrize("dim,m", [(2, 12), (2, 64), (3, 9), (3, 40)])
+def test_spectrum_poisson_closed_form(dim, m):
+    """Dense (n <= 3000) and ARPACK (larger n) paths against the closed form."""
+    Q = synth.poisson2d(m) if dim == 2 else synth.poisson3d(m)
+    lo, hi = _poisson_closed_form(m, dim)
+    r = oracle.spectrum(Q)
+    assert r.lambda_min == pytest.approx(lo, rel=1e-9)
+    assert r.lambda_max == pytest.approx(hi, rel=1e-12)
+    assert r.method == ("dense eigvalsh" if Q.n <= 3000 else "ARPACK eigsh")
+
+
+def test_spectrum_diagonal_and_jdiag_bound():
+    """Q diagonal: D^{-1}Q = I, omega_opt = 1; with D = J of eq-J-diag, S = J - Q is PSD
+    (P:482), so lambda_max(J^{-1}Q) <= 1 -- and = 1 exactly for a bipartite Laplacian (a path)."""
+    r = oracle.spectrum(synth.diag_matrix(np.array([1.0, 3.0, 0.25, 8.0])))
+    assert r.lambda_min == pytest.approx(1.0) and r.lambda_max == pytest.approx(1.0) and r.omega_opt == pytest.approx(1.0)
+    for seed in range(3):
+        Q = synth.random_spd(40, seed=seed)
+        assert oracle.spectrum(Q, dmode="jdiag").lambda_max <= 1.0 + 1e-12
+    P = synth.from_dense(np.diag([1.0, 2.0, 2.0, 1.0]) - np.diag([1.0] * 3, 1) - np.diag([1.0] * 3, -1))
+    r = oracle.spectrum(P, dmode="jdiag")
+    assert r.lambda_min == pytest.approx(0.0, abs=1e-14) and r.lambda_max == pytest.approx(1.0, rel=1e-13)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_omega_opt_minimises_spectral_radius(seed):
+    """omega_opt is the minimiser of rho(I - omega D^{-1} Q): a brute-force scan of the
+    spectral radius (nonsymmetric dense eigenvalues of I - omega D^{-1}Q) over omega never beats it,
+    and rho at omega_opt equals (kappa - 1)/(kappa + 1)."""
+    Q = synth.random_spd(12, seed=seed)
+    A = synth.to_dense(Q)
+    M = A / np.diag(A)[:, None]
+    r = oracle.spectrum(Q)
+    rho = lambda w: float(np.abs(np.linalg.eigvals(np.eye(12) - w * M)).max())
+    best = min(rho(w) for w in np.linspace(1e-3, 2.0 / r.lambda_max, 4001))
+    kappa = r.lambda_max / r.lambda_min
+    assert rho(r.omega_opt) <= best + 1e-12
+    assert rho(r.omega_opt) == pytest.approx((kappa - 1) / (kappa + 1), rel=1e-10)
+
+
+# ------------------------------------------------------------------------------------------------
 # building blocks against dense brute force
 # ------------------------------------------------------------------------------------------------
 

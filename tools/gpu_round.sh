@@ -11,7 +11,7 @@ mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,driver_version,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${TAG}_smi.txt 2>&1
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${TAG}_build.log 2>&1 || { cat gpurun_out/${TAG}_build.log; exit 1; }
 if [ "$TESTS" = "1" ]; then
-  timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/${TAG}_gpu_tests.log 2>&1
+  timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_gpu_tests.log 2>&1
   echo "tests rc=$?"; tail -3 gpurun_out/${TAG}_gpu_tests.log
   timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke rc=$?"
 fi
@@ -32,4 +32,13 @@ for c in $WARM_CFGS; do
       -o gpurun_out/${TAG}_ncuwarm_cfg$c -f python tools/prof.py $c 30 > gpurun_out/${TAG}_ncuwarm_cfg$c.log 2>&1
   echo "ncu warm cfg$c rc=$?"
 done
-ls gpurun_out | grep "^${TAG}_" | head -50
+# gpurun brings back <= 64 MiB: export the raw / source pages as CSV here and drop the reports
+for r in gpurun_out/${TAG}_ncu*_cfg*.ncu-rep; do
+  [ -f "$r" ] || continue
+  ncu -i "$r" --page raw --csv > "${r%.ncu-rep}.raw.csv" 2>/dev/null
+  ncu -i "$r" --page source --csv > "${r%.ncu-rep}.source.csv" 2>/dev/null
+  gzip -f "${r%.ncu-rep}.source.csv"
+  rm -f "$r"
+done
+du -sh gpurun_out
+ls gpurun_out | grep "^${TAG}_" | head -60

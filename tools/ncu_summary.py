@@ -19,7 +19,11 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "us": 1e-6, "ms": 
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    csvp = rep[: -len(".ncu-rep")] + ".raw.csv"
+    if os.path.exists(csvp):  # exported on the GPU box (tools/gpu_round.sh)
+        out = open(csvp).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units, vals = rows[0], rows[1], rows[2]
     d = {}
@@ -47,10 +51,11 @@ def main():
     for c in cfgs:
         rep = os.path.join(ROOT, "gpurun_out", f"{tag}_ncu_cfg{c}.ncu-rep")
         repw = os.path.join(ROOT, "gpurun_out", f"{tag}_ncuwarm_cfg{c}.ncu-rep")
-        if not os.path.exists(rep) and not os.path.exists(repw):
+        have = lambda r: os.path.exists(r) or os.path.exists(r[: -len(".ncu-rep")] + ".raw.csv")
+        if not have(rep) and not have(repw):
             continue
-        dc = raw(rep) if os.path.exists(rep) else None
-        dw = raw(repw) if os.path.exists(repw) else None
+        dc = raw(rep) if have(rep) else None
+        dw = raw(repw) if have(repw) else None
         d = dw or dc
         if c == 1:
             n, nnz = 4096, 20224
