@@ -9,8 +9,10 @@ value = whole-job AJM iterations/s (sum over ranks of iterations / max-over-rank
 
 --impl reference times the CPU oracle (oracle/, plain C, literal two-SpMV Alg. 3) on this box's
 host cores on a bounded sample of the same workload (this tier's reference arm).
-Multi-GPU: the path does not shard (single-GPU method): N independent replicas,
-"scaling": "weak".
+Multi-GPU (torchrun, one process per GPU): the paper's row-block partition (Alg. 3 lines 3-5,
+§4.4) -- ONE solve of the same system sharded over the N GPUs, halo entries and the
+five partial sums exchanged every pass over peer memory (CUDA IPC / NVLink) by the solver kernel
+itself, "scaling": "strong".  --parallel replicas runs N independent solves instead ("weak").
 """
 from __future__ import annotations
 
@@ -382,6 +384,88 @@ def other_config_record(cfg, args, dev, stream):
     return rec
 
 
+def run_sharded(args, rank, world, local, dev, dist):
+    """N > 1: one solve of the config sharded by contiguous row blocks over the N ranks (strong
+    scaling).  value = the solve's iterations / max-over-ranks device time."""
+    import numpy as np
+    import torch
+    import paper_2407_03272_b200 as ajm
+    W = WORKLOADS[args.config]
+    tol = W["tol"] if args.tol is None else args.tol
+    maxit = W["maxit"] if args.maxit is None else args.maxit
+    p = make_problem(args.config)
+    Q = p.Q
+    starts = ajm.ajm_partition_rows(Q.row_ptr, world)
+    rp, cg, vv = ajm.shard_rows(Q.row_ptr, Q.col, Q.val, starts, rank)
+    r0, r1 = int(starts[rank]), int(starts[rank + 1])
+    bl = np.ascontiguousarray(p.b[r0:r1])
+    stream = torch.cuda.current_stream()
+    Qd = [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (rp, cg, vv, bl)]
+    solver = ajm.ShardSolver(rank, world, starts, *Qd[:3], Qd[3])
+    x_out = torch.empty(r1 - r0, dtype=torch.float64, device=dev)
+    kw = dict(tol=tol, maxit=maxit, restart=True, x_out=x_out, history=False)
+    clocks = ClockSampler(local)
+    iters, passes, loop_ms, ms, results, clk = timed_solves(solver, kw, args.steps, args.warmup, stream,
+                                                            dist, dev, clocks)
+    _, job_ms = reduce_job(0.0, ms, dist, dev)
+    _, job_loop_ms = reduce_job(0.0, loop_ms, dist, dev)
+    info = solver.info()
+    assert all(r.status == ("converged" if tol > 0 else "maxiter") for r in results)
+    # e2e: this rank's rows from pinned host buffers (create + connect + solve + x to host + destroy)
+    host = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (rp, cg, vv, bl)]
+    x_host = torch.empty(r1 - r0, dtype=torch.float64).pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in host)
+    e2e_ms, e2e_iters, d2h = 0.0, 0, 0
+    for k in range(1 + args.e2e_steps):
+        barrier(dist, dev)
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        with ajm.ShardSolver(rank, world, starts, host[0], host[1], host[2], host[3]) as s2:
+            r2 = s2.solve(tol=tol, maxit=maxit, restart=True, x_out=x_host, history=True)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        if k == 0:
+            continue
+        e2e_iters += r2.iterations
+        e2e_ms += a0.elapsed_time(a1)
+        d2h = x_host.numel() * 8 + 2 * 8 * (r2.iterations + 1)
+    _, e2e_ms = reduce_job(0.0, e2e_ms, dist, dev)
+    solver.close()
+    if rank != 0:
+        return 0
+    peak, peak_src = load_peaks()
+    model_bytes = ajm.model_bytes_per_iter(Q.n, Q.nnz)
+    achieved = model_bytes * passes / (job_loop_ms * 1e-3) / 1e9
+    nz = np.diff(Q.row_ptr[starts])
+    line = {
+        "metric": METRIC, "value": iters / (job_ms * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": job_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": W["workload"], "n": Q.n, "nnz": Q.nnz, "tol": tol, "maxit": maxit,
+                   "parallelism": f"row-block shards x{world} (Alg. 3 lines 3-5 / §4.4 partition; halo + partials "
+                                  "exchanged in-kernel over peer memory each pass: DESIGN.md §6)",
+                   "row_starts": [int(v) for v in starts], "halo_entries_rank0": info["halo"],
+                   "load_imbalance": float(world * nz.max() / Q.nnz), "grid": info["grid"],
+                   "column_index_bytes": info["col_bytes"]},
+        "iterations_per_solve": iters / args.steps, "time_to_tol_ms": job_ms / args.steps,
+        "us_per_iteration": 1e3 * job_loop_ms / passes,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": world * peak, "unit": "GB/s",
+                     "frac": achieved / (world * peak), "traffic": None, "peak_source": f"{world} x {peak_src}",
+                     "achieved_basis": "whole-matrix algorithmic bytes nnz*12+7n*8+4(n+1) per pass x passes / "
+                                       "max-over-ranks launch time"},
+        "e2e": {"value": e2e_iters / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "note": "per rank: ajm_shard_create from pinned host rows + connect + solve + x rows to host + "
+                        "destroy; time = max over ranks"},
+        "gpu_launches": int(info["launches_per_solve"]) * args.steps,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -393,6 +477,8 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = init_dist(world, "nccl")
+    if world > 1 and args.parallel == "shard":
+        return run_sharded(args, rank, world, local, dev, dist)
     W = WORKLOADS[args.config]
     tol = W["tol"] if args.tol is None else args.tol
     maxit = W["maxit"] if args.maxit is None else args.maxit
@@ -513,6 +599,8 @@ def main(argv=None):
     ap.add_argument("--jblock", type=int, default=None,
                     help="block-diagonal J of eq-J-blkdiag with this block size (default: eq-J-diag)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--parallel", default="shard", choices=["shard", "replicas"],
+                    help="N > 1: one row-block sharded solve (strong scaling) or N independent replicas")
     ap.add_argument("--other-configs", default="1,3,4,5",
                     help="with the default --config 2 at N=1: also measure these BASELINE configs "
                          "(comma list, '' = none) and report them under other_configs")

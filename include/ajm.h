@@ -31,9 +31,11 @@
 extern "C" {
 #endif
 
-#define AJM_ABI_VERSION 3  /* 2: AJM_D_JBLOCK, ajm_get_jblock, ajm_info_t.l2_mode / launches_per_solve;
+#define AJM_ABI_VERSION 4  /* 2: AJM_D_JBLOCK, ajm_get_jblock, ajm_info_t.l2_mode / launches_per_solve;
                               3: layout create flags (AJM_INT32_COLUMNS, AJM_GLOBAL_TABLES, AJM_SEGMENTS_*,
-                                 AJM_DEBUG_POISON), ajm_estimate_spectrum, the sharded (row-block) API */
+                                 AJM_DEBUG_POISON), ajm_estimate_spectrum;
+                              4: the row-block sharded API (ajm_partition_rows, ajm_shard_*,
+                                 ajm_group_solve), ajm_info_t.nranks / halo */
 
 typedef struct ajm_ctx* ajm_handle_t;
 
@@ -138,6 +140,10 @@ typedef struct {
                                  column offsets col - row take <= 256 values and the layout stores
                                  byte codes into an offset table (stencils)        */
     int64_t seg_nnz;          /* nonzeros streamed by warp segments (rows of > 64 nonzeros)       */
+    int32_t rank, nranks;     /* sharded handles: this rank / group size (1 for ajm_create)        */
+    int64_t halo;             /* sharded handles: halo entries H_lo + H_hi received per pass       */
+    int64_t send;             /* sharded handles: entries pushed to other ranks per pass           */
+    int64_t group_rows;       /* rows of 65..256 nonzeros run four to a warp (8-lane sub-warp groups) */
 } ajm_info_t;
 
 /*
@@ -239,6 +245,99 @@ typedef struct {
 ajm_status_t ajm_estimate_spectrum(ajm_handle_t h, const double* v0, uint64_t seed, int64_t max_steps,
                                    double tol, ajm_spectrum_t* out, double* alpha, double* beta,
                                    void* cuda_stream);
+
+/*
+ * ---- Row-block sharded solve (NEXT-2): the paper's own parallel design ----
+ * Alg. 3 lines 3-5 ("for i = 1, ..., s parallel") with the row partition of
+ * §3 and §4.4 (Q, x, y partitioned by rows, J built locally): rank r of an
+ * s = nranks group owns the contiguous global rows [row_starts[r], row_starts[r+1]) of Q, b, D and
+ * of every iterate.  Each pass, every rank multiplies its rows by x~^t -- its own entries plus a
+ * halo of the entries its rows reference on other ranks -- and the ranks exchange (a) the halo
+ * entries of x~^{t+1}, pushed straight into the readers' buffers by the producing CTA (peer stores
+ * over NVLink / NVSwitch; IPC-mapped between processes), and (b) the five partial sums of the
+ * residual / f / restart reductions, summed in rank order so every rank takes the same (bitwise)
+ * control decisions.  One persistent kernel per rank runs the whole solve; there is no host round
+ * trip per pass.  D = eq-J-diag needs only the rank's own rows (J built locally), so the
+ * iterates are those of the single-GPU solve up to the summation order of the reductions.
+ * Local numbering of a rank with n_loc own rows: own row i (global row_starts[r] + i) is i; the
+ * halo entries, sorted by global index, are -H_lo .. -1 (owned by lower ranks) and
+ * n_loc .. n_loc + H_hi - 1 (higher ranks), so a contiguous slab of a stencil keeps its offsets.
+ * Q must be structurally symmetric across the partition (it is, being symmetric): rank r's send
+ * list to rank s (the rows of r that s's rows reference) is derived from r's own rows.
+ * Supported metrics: AJM_D_JDIAG, AJM_D_USER, AJM_D_QDIAG (not AJM_D_JBLOCK).  Not thread-safe
+ * across the ranks of one group except as described per call.
+ */
+#define AJM_MAX_RANKS 8
+#define AJM_SHARD_BLOB_BYTES 1024      /* size of the opaque connection record of one rank            */
+#define AJM_SHARD_COLOCATED 0x200000u  /* create flag: every rank of the group lives on this device
+                                          (an emulated group, run by ajm_group_solve as ONE launch over
+                                          all ranks); the rank's grid is 1/nranks of the device       */
+
+/* ajm_partition_rows -- host only (no GPU): contiguous row blocks balanced by the per-pass bytes
+ * 12 B per nonzero + 56 B per row, every block non-empty.
+ *   row_ptr    : host int64[n+1] of the whole matrix
+ *   row_starts : host int64[nranks+1] out: block r is [row_starts[r], row_starts[r+1])
+ * The paper's load imbalance p * max_i nnz(Q^{i,:}) / nnz(Q) follows from it.
+ * Errors: INVALID_ARG for nranks < 1, nranks > AJM_MAX_RANKS or nranks > n; CSR_INVALID for a bad
+ * row_ptr. */
+ajm_status_t ajm_partition_rows(int64_t n, const int64_t* row_ptr, int32_t nranks, int64_t* row_starts);
+
+/* ajm_shard_plan -- host only (no GPU): rank `rank`'s local numbering and exchange lists.
+ *   row_starts : host int64[nranks+1] (row_starts[0] = 0, increasing; row_starts[nranks] = n)
+ *   row_ptr    : host int64[n_loc+1] of the rank's rows (local offsets, row_ptr[0] = 0)
+ *   col_glob   : host int32[nnz_loc] global columns of those rows
+ *   col_loc    : host int32[nnz_loc] out (or NULL): local columns in [-H_lo, n_loc + H_hi)
+ *   halo_glob  : host int64[H_lo + H_hi] out (or NULL): global index of local -H_lo + k, in order
+ *   send_rows  : host int64[sum send] out (or NULL): local rows to send, grouped by destination rank
+ *                (ascending), ascending within a group -- the order of the destination's halo
+ *   counts     : host int64[2 + 2*nranks] out: H_lo, H_hi, then halo entries per source rank, then
+ *                send entries per destination rank (by symmetry: the rows of this rank that have a
+ *                column in the destination's block)
+ * Errors: INVALID_ARG, CSR_INVALID (column out of [0, n) or row_ptr inconsistent). */
+ajm_status_t ajm_shard_plan(int32_t rank, int32_t nranks, const int64_t* row_starts, const int64_t* row_ptr,
+                            const int32_t* col_glob, int32_t* col_loc, int64_t* halo_glob, int64_t* send_rows,
+                            int64_t* counts);
+
+/* ajm_shard_create -- rank `rank`'s handle of a sharded group, on the current device.
+ *   row_starts        : host int64[nranks+1], the same on every rank (e.g. ajm_partition_rows)
+ *   nnz, row_ptr, col_idx, vals : the rank's rows row_starts[rank] .. row_starts[rank+1] as CSR with
+ *                       GLOBAL int32 column indices (host or device memory)
+ *   b, d              : the rank's slices (d: AJM_D_USER only)
+ *   flags             : AJM_SHARD_COLOCATED | the layout switches of ajm_create
+ * The handle can be solved only after ajm_shard_connect.  Ownership and errors as ajm_create
+ * (a zero local b is allowed; ||b|| = 0 of the whole b is reported by ajm_shard_connect). */
+ajm_status_t ajm_shard_create(ajm_handle_t* out, int32_t rank, int32_t nranks, const int64_t* row_starts,
+                              int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx, const double* vals,
+                              const double* b, int32_t dmode, const double* d, uint32_t flags,
+                              void* cuda_stream);
+
+/* ajm_shard_export -- write this rank's connection record (AJM_SHARD_BLOB_BYTES, host) to blob:
+ * CUDA IPC handles and offsets of its iterate buffers and exchange block, its halo layout per
+ * source rank and its local ||b||^2.  The caller all-gathers the records (e.g. torch.distributed). */
+ajm_status_t ajm_shard_export(ajm_handle_t h, void* blob);
+
+/* ajm_shard_connect -- map every rank's buffers (same process: the pointers themselves, with peer
+ * access enabled across devices; another process: cudaIpcOpenMemHandle) from the nranks records
+ * `blobs` (host, rank order, AJM_SHARD_BLOB_BYTES each), check that each rank's halo from this rank
+ * matches this rank's send list (else AJM_ERR_NOT_SYMMETRIC), and set ||b||_2 = sqrt of the ranks'
+ * ||b_r||^2 summed in rank order (AJM_ERR_ZERO_RHS if 0).  Once per handle. */
+ajm_status_t ajm_shard_connect(ajm_handle_t h, const void* blobs);
+
+/* ajm_solve on a connected shard handle: the same call on every rank of the group, concurrently
+ * (one process per GPU), with the same tol / maxit / policy; x0 and x_out are the rank's own rows
+ * (n_loc); res, res_hist, f_hist and restart_iters are the whole solve's (identical on every rank).
+ * A rank that cannot reach the others fails with AJM_ERR_CUDA after a bounded wait (seconds). */
+
+/* ajm_group_solve -- an AJM_SHARD_COLOCATED group (all ranks on this device, connected): run the
+ * sharded solve as ONE cooperative launch over every rank's CTAs (the same kernel and exchange as a
+ * multi-GPU group; peers are plain device pointers).
+ *   hs     : host array of the nranks handles in rank order
+ *   x0     : double[n] of the WHOLE system (host/device) or NULL = zeros;  x_out : double[n] out
+ *   other arguments as ajm_solve. */
+ajm_status_t ajm_group_solve(const ajm_handle_t* hs, int32_t nranks, const double* x0, double tol,
+                             int64_t maxit, ajm_policy_t policy, double* x_out, ajm_result_t* res,
+                             double* res_hist, double* f_hist, int64_t* restart_iters, int64_t restart_cap,
+                             void* cuda_stream);
 
 /* ajm_get_info -- layout and last-solve timing facts. */
 ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info);

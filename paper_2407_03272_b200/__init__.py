@@ -16,8 +16,9 @@ import os
 
 import numpy as np
 
-__all__ = ["AjmError", "Result", "Solver", "Spectrum", "ajm_create", "ajm_solve", "ajm_destroy", "lib",
-           "LIB_PATH", "STATUS_NAMES", "TERM_NAMES", "D_MODES", "model_bytes_per_iter"]
+__all__ = ["AjmError", "Result", "Solver", "Spectrum", "ShardGroup", "ShardSolver", "ajm_create", "ajm_solve",
+           "ajm_destroy", "ajm_partition_rows", "ajm_shard_plan", "shard_rows", "lib", "LIB_PATH",
+           "STATUS_NAMES", "TERM_NAMES", "D_MODES", "model_bytes_per_iter"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libajm.so")
 if os.environ.get("AJM_LIB_OVERRIDE"):  # A/B experiments against another build of the same ABI
@@ -36,7 +37,10 @@ AJM_GLOBAL_TABLES = 0x20000
 AJM_SEGMENTS_STATIC = 0x40000
 AJM_SEGMENTS_DYNAMIC = 0x80000
 AJM_DEBUG_POISON = 0x100000
-ABI_VERSION = 3
+AJM_SHARD_COLOCATED = 0x200000
+AJM_MAX_RANKS = 8
+AJM_SHARD_BLOB_BYTES = 1024
+ABI_VERSION = 4
 
 
 def AJM_JBLOCK_SIZE(bs: int) -> int:
@@ -46,7 +50,8 @@ def AJM_JBLOCK_SIZE(bs: int) -> int:
 # every symbol include/ajm.h declares (tests check the .so exports all of them)
 ABI_SYMBOLS = ["ajm_create", "ajm_solve", "ajm_get_trace", "ajm_get_diag", "ajm_get_jblock",
                "ajm_estimate_spectrum", "ajm_get_info", "ajm_destroy", "ajm_last_error",
-               "ajm_abi_version"]
+               "ajm_abi_version", "ajm_partition_rows", "ajm_shard_plan", "ajm_shard_create",
+               "ajm_shard_export", "ajm_shard_connect", "ajm_group_solve"]
 
 
 class AjmError(RuntimeError):
@@ -79,7 +84,8 @@ class ajm_info_t(ctypes.Structure):
                 ("l2_window_bytes", ctypes.c_int64), ("l2_hit_ratio", ctypes.c_double),
                 ("mode", ctypes.c_int32), ("l2_mode", ctypes.c_int32),
                 ("launches_per_solve", ctypes.c_int32), ("col_bytes", ctypes.c_int32),
-                ("seg_nnz", ctypes.c_int64)]
+                ("seg_nnz", ctypes.c_int64), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
+                ("halo", ctypes.c_int64), ("send", ctypes.c_int64), ("group_rows", ctypes.c_int64)]
 
 
 class ajm_spectrum_t(ctypes.Structure):
@@ -141,6 +147,21 @@ def lib():
         L.ajm_last_error.argtypes = [P]
         L.ajm_last_error.restype = ctypes.c_char_p
         L.ajm_abi_version.restype = ctypes.c_int32
+        if hasattr(L, "ajm_shard_create"):
+            L.ajm_partition_rows.argtypes = [I64, P, ctypes.c_int32, P]
+            L.ajm_partition_rows.restype = ctypes.c_int
+            L.ajm_shard_plan.argtypes = [ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, P]
+            L.ajm_shard_plan.restype = ctypes.c_int
+            L.ajm_shard_create.argtypes = [ctypes.POINTER(P), ctypes.c_int32, ctypes.c_int32, P, I64, P, P, P,
+                                           P, ctypes.c_int32, P, ctypes.c_uint32, P]
+            L.ajm_shard_create.restype = ctypes.c_int
+            L.ajm_shard_export.argtypes = [P, P]
+            L.ajm_shard_export.restype = ctypes.c_int
+            L.ajm_shard_connect.argtypes = [P, P]
+            L.ajm_shard_connect.restype = ctypes.c_int
+            L.ajm_group_solve.argtypes = [P, ctypes.c_int32, P, ctypes.c_double, I64, ajm_policy_t, P,
+                                          ctypes.POINTER(ajm_result_t), P, P, P, I64, P]
+            L.ajm_group_solve.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -357,3 +378,229 @@ class Solver:
             self.close()
         except Exception:
             pass
+
+
+# ---- row-block sharded solve (NEXT-2; include/ajm.h "Row-block sharded solve") ----
+
+def ajm_partition_rows(row_ptr, nranks: int) -> np.ndarray:
+    """Contiguous row blocks balanced by the per-pass bytes (host only, no GPU): int64[nranks+1]."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    out = np.zeros(int(nranks) + 1, dtype=np.int64)
+    _check(lib().ajm_partition_rows(len(rp) - 1, rp.ctypes.data_as(ctypes.c_void_p), int(nranks),
+                                    out.ctypes.data_as(ctypes.c_void_p)))
+    return out
+
+
+def shard_rows(row_ptr, col, val, starts, rank: int):
+    """The rows of block `rank` as (row_ptr rebased to 0, global columns, values): slicing only."""
+    rp = np.asarray(row_ptr, dtype=np.int64)
+    r0, r1 = int(starts[rank]), int(starts[rank + 1])
+    k0, k1 = int(rp[r0]), int(rp[r1])
+    return rp[r0:r1 + 1] - k0, np.asarray(col)[k0:k1], np.asarray(val)[k0:k1]
+
+
+def ajm_shard_plan(rank: int, nranks: int, starts, row_ptr_loc, col_glob) -> dict:
+    """Host-only plan of one rank (no GPU): local columns, halo (global indices in local order), send
+    lists grouped by destination rank, and the per-rank counts (include/ajm.h ajm_shard_plan)."""
+    st = np.ascontiguousarray(starts, dtype=np.int64)
+    rp = np.ascontiguousarray(row_ptr_loc, dtype=np.int64)
+    cg = np.ascontiguousarray(col_glob, dtype=np.int32)
+    R = int(nranks)
+    counts = np.zeros(2 + 2 * R, dtype=np.int64)
+    P = ctypes.c_void_p
+    _check(lib().ajm_shard_plan(int(rank), R, st.ctypes.data_as(P), rp.ctypes.data_as(P), cg.ctypes.data_as(P),
+                                None, None, None, counts.ctypes.data_as(P)))
+    h_lo, h_hi = int(counts[0]), int(counts[1])
+    col_loc = np.empty(len(cg), dtype=np.int32)
+    halo = np.empty(h_lo + h_hi, dtype=np.int64)
+    send = np.empty(int(counts[2 + R:].sum()), dtype=np.int64)
+    _check(lib().ajm_shard_plan(int(rank), R, st.ctypes.data_as(P), rp.ctypes.data_as(P), cg.ctypes.data_as(P),
+                                col_loc.ctypes.data_as(P), halo.ctypes.data_as(P), send.ctypes.data_as(P),
+                                counts.ctypes.data_as(P)))
+    return {"col_loc": col_loc, "halo_glob": halo, "send_rows": send, "h_lo": h_lo, "h_hi": h_hi,
+            "halo_cnt": counts[2:2 + R].copy(), "send_cnt": counts[2 + R:].copy()}
+
+
+def _shard_create(rank, nranks, starts, row_ptr_loc, col_glob, val, b_loc, dmode, d_loc, flags, stream):
+    keep = []
+    ptrs = []
+    for a, dt in ((starts, np.int64), (row_ptr_loc, np.int64), (col_glob, np.int32), (val, np.float64),
+                  (b_loc, np.float64), (d_loc, np.float64)):
+        p, k = _ptr(a, dt)
+        ptrs.append(p)
+        keep.append(k)
+    h = ctypes.c_void_p()
+    dm = D_MODES[dmode] if isinstance(dmode, str) else int(dmode)
+    nnz = int(np.asarray(row_ptr_loc[-1].cpu() if hasattr(row_ptr_loc, "cpu") else row_ptr_loc[-1]))
+    _check(lib().ajm_shard_create(ctypes.byref(h), int(rank), int(nranks), ptrs[0], nnz, ptrs[1], ptrs[2],
+                                  ptrs[3], ptrs[4], dm, ptrs[5], int(flags), _stream(stream)), None)
+    return h.value
+
+
+def _shard_export(handle) -> bytes:
+    buf = ctypes.create_string_buffer(AJM_SHARD_BLOB_BYTES)
+    _check(lib().ajm_shard_export(ctypes.c_void_p(handle), ctypes.cast(buf, ctypes.c_void_p)),
+           ctypes.c_void_p(handle))
+    return buf.raw
+
+
+def _shard_connect(handle, blobs) -> None:
+    joined = b"".join(blobs)
+    assert len(joined) == AJM_SHARD_BLOB_BYTES * len(blobs)
+    buf = ctypes.create_string_buffer(joined, len(joined))
+    _check(lib().ajm_shard_connect(ctypes.c_void_p(handle), ctypes.cast(buf, ctypes.c_void_p)),
+           ctypes.c_void_p(handle))
+
+
+def _result(r, x_out, rh, fh, ri) -> Result:
+    k = r.iterations + 1
+    return Result(x=x_out, status=TERM_NAMES[r.status], iterations=int(r.iterations),
+                  rel_residual=r.rel_residual, f=r.f, n_restarts=int(r.n_restarts),
+                  x_is_prerestart=bool(r.x_is_prerestart),
+                  restart_iters=[int(v) for v in ri[: r.restarts_logged]],
+                  res_hist=None if rh is None else rh[:k], f_hist=None if fh is None else fh[:k])
+
+
+class _ShardHandles:
+    def _info(self, h) -> dict:
+        inf = ajm_info_t()
+        _check(lib().ajm_get_info(ctypes.c_void_p(h), ctypes.byref(inf)), ctypes.c_void_p(h))
+        return {f: getattr(inf, f) for f, _ in ajm_info_t._fields_}
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class ShardGroup(_ShardHandles):
+    """All ranks of a row-block sharded solve on THIS device (AJM_SHARD_COLOCATED), solved as one
+    cooperative launch (ajm_group_solve): the multi-GPU kernel and exchange with the peers being
+    ordinary device pointers -- how the sharded path runs and is tested on a single GPU."""
+
+    def __init__(self, n, row_ptr, col, val, b, nranks: int, starts=None, dmode="jdiag", d=None,
+                 int32_columns=False, segments="auto", stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2407_03272_b200 needs a CUDA device (no CPU fallback)")
+        self.n = int(n)
+        self.nranks = int(nranks)
+        self._stream = stream
+        self.starts = ajm_partition_rows(row_ptr, nranks) if starts is None else np.asarray(starts, dtype=np.int64)
+        flags = AJM_SHARD_COLOCATED | (AJM_INT32_COLUMNS if int32_columns else 0)
+        flags |= {"auto": 0, "static": AJM_SEGMENTS_STATIC, "dynamic": AJM_SEGMENTS_DYNAMIC}[segments]
+        self.handles = []
+        bb = np.asarray(b, dtype=np.float64)
+        dd = None if d is None else np.asarray(d, dtype=np.float64)
+
+        def create_all(fl):
+            for r in range(self.nranks):
+                rp, cg, vv = shard_rows(row_ptr, col, val, self.starts, r)
+                r0, r1 = int(self.starts[r]), int(self.starts[r + 1])
+                self.handles.append(_shard_create(r, self.nranks, self.starts, rp, cg, vv, bb[r0:r1], dmode,
+                                                  None if dd is None else dd[r0:r1], fl, stream))
+        create_all(flags)
+        # one launch runs every rank: they must share the column encoding (byte codes need every
+        # rank's offsets to fit one table each -- a rank whose do not keeps int32 columns)
+        if len({self._info(h)["col_bytes"] for h in self.handles}) > 1:
+            self.close()
+            create_all(flags | AJM_INT32_COLUMNS)
+        blobs = [_shard_export(h) for h in self.handles]
+        for h in self.handles:
+            _shard_connect(h, blobs)
+
+    @classmethod
+    def from_csr(cls, Q, b, nranks, **kw):
+        return cls(Q.n, Q.row_ptr, Q.col, Q.val, b, nranks, **kw)
+
+    def solve(self, x0=None, tol=1e-6, maxit=1000, momentum=True, restart=True, k0=2, x_out=None,
+              history=True, restart_cap=64) -> Result:
+        import torch
+        if x_out is None:
+            x_out = torch.empty(self.n, dtype=torch.float64, device="cuda")
+        rh = np.empty(maxit + 1) if history else None
+        fh = np.empty(maxit + 1) if history else None
+        ri = np.zeros(restart_cap, dtype=np.int64)
+        p0, k_0 = _ptr(x0, np.float64)
+        px, k_x = _ptr(x_out, np.float64, output=True)
+        pr, k_r = _ptr(rh, np.float64, output=True)
+        pf, k_f = _ptr(fh, np.float64, output=True)
+        pri, k_ri = _ptr(ri, np.int64, output=True)
+        arr = (ctypes.c_void_p * self.nranks)(*self.handles)
+        res = ajm_result_t()
+        pol = ajm_policy_t(int(bool(momentum)), int(bool(restart)), int(k0))
+        _check(lib().ajm_group_solve(ctypes.cast(arr, ctypes.c_void_p), self.nranks, p0, float(tol), int(maxit), pol,
+                                     px, ctypes.byref(res), pr, pf, pri, len(ri), _stream(self._stream)),
+               ctypes.c_void_p(self.handles[0]))
+        return _result(res, x_out, rh, fh, ri)
+
+    def info(self, rank: int = 0) -> dict:
+        return self._info(self.handles[rank])
+
+    def load_imbalance(self, row_ptr) -> float:
+        """p * max_i nnz(Q^{i,:}) / nnz(Q), the paper's load-imbalance measure."""
+        rp = np.asarray(row_ptr, dtype=np.int64)
+        nz = rp[self.starts[1:]] - rp[self.starts[:-1]]
+        return float(self.nranks * nz.max() / max(int(rp[-1]), 1))
+
+    def close(self):
+        for h in getattr(self, "handles", []):
+            if h:
+                ajm_destroy(h)
+        self.handles = []
+
+
+def allgather_bytes(blob: bytes, group=None) -> list:
+    """All ranks' connection records in rank order over torch.distributed (plumbing only)."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, blob, group=group)
+    return out
+
+
+class ShardSolver(_ShardHandles):
+    """One rank of a multi-process (one process per GPU) row-block sharded solve: create from this
+    rank's rows, exchange connection records with the other ranks (``exchange(blob) -> [blobs]``,
+    default torch.distributed all_gather_object), connect, then ``solve`` concurrently on every rank."""
+
+    def __init__(self, rank: int, nranks: int, starts, row_ptr_loc, col_glob, val, b_loc, dmode="jdiag",
+                 d_loc=None, int32_columns=False, segments="auto", exchange=None, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2407_03272_b200 needs a CUDA device (no CPU fallback)")
+        self.rank, self.nranks = int(rank), int(nranks)
+        self.starts = np.asarray(starts, dtype=np.int64)
+        self.n = int(self.starts[rank + 1] - self.starts[rank])
+        self._stream = stream
+        flags = (AJM_INT32_COLUMNS if int32_columns else 0)
+        flags |= {"auto": 0, "static": AJM_SEGMENTS_STATIC, "dynamic": AJM_SEGMENTS_DYNAMIC}[segments]
+        self.handle = _shard_create(rank, nranks, self.starts, row_ptr_loc, col_glob, val, b_loc, dmode, d_loc,
+                                    flags, stream)
+        blobs = (exchange or allgather_bytes)(_shard_export(self.handle))
+        _shard_connect(self.handle, blobs)
+
+    def solve(self, x0=None, tol=1e-6, maxit=1000, momentum=True, restart=True, k0=2, x_out=None,
+              history=True, restart_cap=64) -> Result:
+        import torch
+        if x_out is None:
+            x_out = torch.empty(self.n, dtype=torch.float64, device="cuda")
+        rh = np.empty(maxit + 1) if history else None
+        fh = np.empty(maxit + 1) if history else None
+        ri = np.zeros(restart_cap, dtype=np.int64)
+        r = ajm_solve(self.handle, x0, tol, maxit, momentum, restart, k0, x_out, rh, fh, ri, self._stream)
+        return _result(r, x_out, rh, fh, ri)
+
+    def info(self) -> dict:
+        return self._info(self.handle)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            ajm_destroy(self.handle)
+            self.handle = None

@@ -14,6 +14,7 @@
 //          Alg. 3 with a grid barrier per pass and device-side control (no host round trip, no
 //          relaunch) -> copy-out of the answer buffer, histories and the control block.
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <functional>
@@ -94,7 +95,21 @@ SolveFn lanczos_fn(bool seg, bool cluster, bool gmeta, int col_bytes, int stages
     return nullptr;
 }
 
-constexpr int kBlockThreads = AJM_BLOCK + 32;  // consumer warps + the TMA producer warp
+// One rank of a row-block sharded solve (kShard): int32 columns at ring depth 3 / 4 or byte-coded
+// columns at 4 / 5, with or without the segment phases -- the layouts create picks for shards.
+SolveFn shard_fn(int col_bytes, bool seg, int stages) {
+    if (col_bytes == 1) {
+        if (stages == 5) return seg ? ajm_solve_kernel<5, true, false, 0, false, true, false, true> : ajm_solve_kernel<5, false, false, 0, false, true, false, true>;
+        return seg ? ajm_solve_kernel<4, true, false, 0, false, true, false, true> : ajm_solve_kernel<4, false, false, 0, false, true, false, true>;
+    }
+    if (stages == 4) return seg ? ajm_solve_kernel<4, true, false, 0, false, false, false, true> : ajm_solve_kernel<4, false, false, 0, false, false, false, true>;
+    return seg ? ajm_solve_kernel<3, true, false, 0, false, false, false, true> : ajm_solve_kernel<3, false, false, 0, false, false, false, true>;
+}
+
+// Threads per CTA of a solver kernel: 8 consumer warps + the TMA producer warp (kProd, layouts
+// without warp segments), or the 8 warps alone (segment layouts: the last warp to release a stage
+// refills it, and 128 registers per thread fit).  Every kernel a handle uses shares its nseg > 0.
+int block_threads(bool seg) { return seg ? AJM_BLOCK : AJM_BLOCK + 32; }
 
 // Kernel attributes (max dynamic shared memory, carve-out) belong to the kernel, which every handle
 // of that layout shares: they are set -- and occupancy is queried -- under one library-wide lock,
@@ -102,10 +117,10 @@ constexpr int kBlockThreads = AJM_BLOCK + 32;  // consumer warps + the TMA produ
 std::mutex g_attr_mu;
 
 // set the attributes of fn and return the resident CTAs per SM (0 on failure); caller holds g_attr_mu
-cudaError_t fn_occupancy(SolveFn fn, size_t dyn_smem, int carveout, int* occ) {
+cudaError_t fn_occupancy(SolveFn fn, size_t dyn_smem, int carveout, int* occ, int threads) {
     cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, fn, kBlockThreads, dyn_smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, fn, threads, dyn_smem);
     return e;
 }
 
@@ -184,6 +199,8 @@ struct ajm_ctx {
     int dynseg = 0;                 // segments claimed dynamically by warps (else static LPT plan)
     int* cta_unit = nullptr;
     int* seg_meta = nullptr;        // int4 {row, k0, k1, split} per static seg_list position
+    int4* grp = nullptr;            // sub-warp groups: 3 int4 per group ({rows}, {k0}, {k1})
+    int64_t ngrp = 0, grp_rows = 0;
     double* partials = nullptr;
     AjmCtrl* ctrl = nullptr;
     double* hist = nullptr;  // 4 x hist_cap: res, f, d, dabs
@@ -212,6 +229,27 @@ struct ajm_ctx {
     int64_t last_launches = 0;
     int64_t last_iterations = -1;
     std::string err_msg;
+    // ---- row-block shard (NEXT-2; ajm_shard_create) ----
+    int shard = 0;                     // 1: one rank of a sharded group
+    int rank = 0, nranks = 1;
+    int colocated = 0;                 // AJM_SHARD_COLOCATED: the group runs as one launch here
+    int64_t n_glob = 0, row0 = 0;
+    int64_t h_lo = 0, h_hi = 0;        // halo entries below / above the own rows
+    int64_t lo_pad = 0, xstride = 0;   // X_k = vecs + k * xstride + lo_pad
+    double bsq_local = 0.0;            // ||b_r||^2 of the own rows
+    std::vector<int64_t> halo_cnt, send_cnt;  // [nranks]
+    std::vector<int4> snd_host;        // per CTA: {internal row, peer, k-th entry of the list to peer, 0}
+    std::vector<int> snd_cta_host;     // [grid+1]
+    int* snd_cta = nullptr;
+    int4* snd = nullptr;
+    double* xch = nullptr;             // cudaMalloc (IPC-exportable): slots [2][MAXR][NPART] + counter
+    AjmPeer* peers = nullptr;          // [nranks] device
+    std::vector<AjmPeer> peers_host;
+    std::vector<void*> ipc_opened;     // peer allocations opened through CUDA IPC
+    bool connected = false;
+    bool broken = false;               // a cross-rank wait timed out: the counters are out of step
+    unsigned long long bar_base = 0;   // cross-rank arrivals of earlier solves
+    AjmPass* emu = nullptr;            // (colocated, rank 0) device array of the group's pass structs
 };
 
 namespace {
@@ -302,13 +340,24 @@ void dfree(void* p) {
 }
 
 void free_all(ajm_ctx* h) {
-    void* ptrs[] = {h->rp, h->col, h->val, h->vecs,
+    void* ptrs[] = {h->rp, h->col, h->val, h->shard ? nullptr : h->vecs,
                     h->sval, h->scol, h->chunk_off, h->seg_row, h->seg_k0, h->seg_k1,
                     h->seg_split, h->seg_part, h->split_row, h->split_seg0, h->split_cnt,
                     h->cta_split, h->owner_split, h->unit_c0, h->cta_seg, h->seg_list, h->cta_unit, h->partials, h->ctrl,
                     h->hist, h->scratch, h->err, h->ts, h->perm_fwd, h->perm_inv, h->b_in, h->Jblk, h->Jinv, h->seg_order, h->seg_grp,
-                    h->g_uc0, h->g_coff, h->g_ubase, h->g_cbase, h->scode, h->ctab, h->seg_meta, h->lzw};
+                    h->g_uc0, h->g_coff, h->g_ubase, h->g_cbase, h->scode, h->ctab, h->seg_meta, h->lzw, h->grp};
     for (void* p : ptrs) dfree(p);
+    dfree(h->snd_cta);
+    dfree(h->snd);
+    dfree(h->peers);
+    dfree(h->emu);
+    for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
+    h->ipc_opened.clear();
+    if (h->xch) cudaFree(h->xch);
+    if (h->shard && h->vecs) {  // cudaMalloc'd (IPC-exportable), not from the pool
+        cudaFree(h->vecs);
+        h->vecs = nullptr;
+    }
     if (h->persist_holder) {  // the last holder restores the limit and drops the persisting lines
         std::lock_guard<std::mutex> lock(g_attr_mu);
         PersistState& ps = g_persist[h->device];
@@ -377,7 +426,20 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.jbs = h->jbs;
     p.scode = h->scode;
     p.seg_meta = reinterpret_cast<const int4*>(h->seg_meta);
+    p.grp = h->grp;
     p.ctab = h->ctab;
+    p.sh = AjmShard{};
+    p.sh.nranks = 1;
+    if (h->shard) {
+        p.sh.rank = h->rank;
+        p.sh.nranks = h->nranks;
+        p.sh.peers = h->peers;
+        p.sh.snd_cta = h->snd_cta;
+        p.sh.snd = h->snd;
+        p.sh.slot = h->xch;
+        p.sh.bar = reinterpret_cast<unsigned long long*>(h->xch + 2 * AJM_MAX_RANKS * AJM_NPART);
+        p.sh.bar_base = h->bar_base;
+    }
     return p;
 }
 
@@ -396,7 +458,7 @@ cudaError_t launch_solver(ajm_ctx* h, AjmPass& p, cudaStream_t st, SolveFn fn = 
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(h->grid);
-    cfg.blockDim = dim3(kBlockThreads);
+    cfg.blockDim = dim3(block_threads(h->nseg > 0));
     cfg.dynamicSmemBytes = h->dyn_smem;
     cfg.stream = st;
     cudaLaunchAttribute at[2];
@@ -518,6 +580,16 @@ double tri_last_component(const std::vector<double>& a, const std::vector<double
     return std::fabs(y[(size_t)k - 1]);
 }
 
+// What ajm_shard_create hands to the common create path (host data of the rank's plan)
+struct ShardIn {
+    int rank = 0, nranks = 1;
+    int colocated = 0;
+    int64_t n_glob = 0, row0 = 0;
+    int64_t h_lo = 0, h_hi = 0;
+    std::vector<int64_t> halo_cnt, send_cnt;  // [nranks]
+    std::vector<int64_t> send_rows;           // own local rows, grouped by destination rank
+};
+
 }  // namespace
 
 extern "C" {
@@ -528,10 +600,12 @@ const char* ajm_last_error(ajm_handle_t h) {
     return h ? h->err_msg.c_str() : g_create_error.c_str();
 }
 
-ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t* row_ptr,
-                        const int32_t* col_idx, const double* vals, const double* b, int32_t dmode,
-                        const double* d, uint32_t flags, void* cuda_stream) {
-    NvtxScope nvtx_scope_("ajm_create");
+// The create path of ajm_create and (sh != NULL) ajm_shard_create: a shard's rows are an ordinary
+// n-row matrix whose columns may also reach its halo, [-H_lo, n + H_hi).
+static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t* row_ptr,
+                                const int32_t* col_idx, const double* vals, const double* b, int32_t dmode,
+                                const double* d, uint32_t flags, void* cuda_stream, const ShardIn* sh) {
+    NvtxScope nvtx_scope_(sh ? "ajm_shard_create" : "ajm_create");
     g_create_error.clear();
     g_poison = (flags & AJM_DEBUG_POISON) != 0;
     struct PoisonReset { ~PoisonReset() { g_poison = false; } } poison_reset_;
@@ -562,6 +636,11 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     if (dmode == AJM_D_JBLOCK && (jbs < 1 || jbs > 32 || (jbs & (jbs - 1))))
         return fail(nullptr, AJM_ERR_INVALID_ARG, "AJM_D_JBLOCK needs AJM_JBLOCK_SIZE(bs) with bs in {1,2,4,8,16,32}");
     if (dmode == AJM_D_USER && !d) return fail(nullptr, AJM_ERR_INVALID_ARG, "AJM_D_USER needs d");
+    if (sh && dmode == AJM_D_JBLOCK) return fail(nullptr, AJM_ERR_UNSUPPORTED, "sharded handles support diagonal metrics only");
+    if (sh && (flags & (AJM_VALIDATE_SYMMETRY | AJM_GLOBAL_TABLES | AJM_LOOP_HOST)))
+        return fail(nullptr, AJM_ERR_UNSUPPORTED, "AJM_VALIDATE_SYMMETRY / AJM_GLOBAL_TABLES / AJM_LOOP_HOST are not available for shards");
+    const int64_t clo = sh ? -sh->h_lo : 0, chi = sh ? n + sh->h_hi : n;  // column range
+    if (chi >= ((int64_t)1 << 31) - 1) return fail(nullptr, AJM_ERR_UNSUPPORTED, "n + halo must be < 2^31");
     cudaStream_t st = (cudaStream_t)cuda_stream;
 
     // the O(1) consistency checks before any copy: with row_ptr[0] = 0 and row_ptr[n] = nnz the
@@ -584,6 +663,19 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     ajm_ctx* h = new ajm_ctx();
     h->n = n;
     h->nnz = nnz;
+    if (sh) {
+        h->shard = 1;
+        h->rank = sh->rank;
+        h->nranks = sh->nranks;
+        h->colocated = sh->colocated;
+        h->n_glob = sh->n_glob;
+        h->row0 = sh->row0;
+        h->h_lo = sh->h_lo;
+        h->h_hi = sh->h_hi;
+        h->halo_cnt = sh->halo_cnt;
+        h->send_cnt = sh->send_cnt;
+        h->l2persist = 0;  // no persisting window: the group's buffers are other ranks' too
+    }
     h->flags = flags;
     h->dmode = dmode;
     h->jbs = jbs;
@@ -655,6 +747,9 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     // ---- row-length-binned layout (host, O(n log sigma)) ----
     auto rlen = [&](int64_t r) { return hrp[(size_t)r + 1] - hrp[(size_t)r]; };
     std::vector<int> perm_h, seg_row_h, seg_k0_h, seg_k1_h, seg_split_h, split_row_h, split_seg0_h;
+    std::vector<int> inv_keep;  // (shards, relabelled) caller's local row -> internal row
+    std::vector<int> row_cta;   // (shards) internal row -> the CTA that computes it
+    std::vector<int4> grp_h;    // sub-warp groups: {rows}, {k0}, {k1} per group
     std::vector<long long> choff;
     std::vector<double> chcost;
     // fast path (stencil-like matrices): every row short and natural order pads < 5% -> SELL-32
@@ -850,7 +945,16 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             }
         }
         if (!h->dynseg) split_seg0_h.push_back((int)seg_row_h.size());
+        // sub-warp groups (static plan): rows of 65 .. AJM_GRP_MAX nonzeros four to a warp, 8 lanes
+        // per row, so four rows' latency chains (operands, gathers, epilogue) overlap in one warp
+        // (north_star "one warp or sub-warp per row, chosen by row-length histogram")
+        std::vector<int> grp_members;
+        const bool use_groups = !h->dynseg && !getenv("AJM_NO_GROUPS");
         for (int r : whole_rows) {
+            if (use_groups && rlen(r) <= AJM_GRP_MAX) {
+                grp_members.push_back(r);
+                continue;
+            }
             // dynamic segments: every segment row is finished by a fixed owner CTA (one segment)
             const int sidx = h->dynseg ? (int)split_row_h.size() : -1;
             if (h->dynseg) {
@@ -863,6 +967,34 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             seg_split_h.push_back(sidx);
         }
         if (h->dynseg) split_seg0_h.push_back((int)seg_row_h.size());
+        if (!grp_members.empty()) {
+            // longest first, so the rows of a group have similar lengths (balanced 8-lane groups)
+            std::stable_sort(grp_members.begin(), grp_members.end(), [&](int x, int y) { return rlen(x) > rlen(y); });
+            const int64_t ng = ((int64_t)grp_members.size() + AJM_GRP_ROWS - 1) / AJM_GRP_ROWS;
+            grp_h.assign((size_t)ng * 3, make_int4(-1, -1, -1, -1));
+            for (int64_t g = 0; g < ng; ++g) {
+                int rr[4] = {-1, -1, -1, -1}, k0[4] = {0, 0, 0, 0}, k1[4] = {0, 0, 0, 0};
+                int64_t tot = 0;
+                for (int q = 0; q < AJM_GRP_ROWS; ++q) {
+                    const int64_t m = g * AJM_GRP_ROWS + q;
+                    if (m >= (int64_t)grp_members.size()) break;
+                    const int r = grp_members[(size_t)m];
+                    rr[q] = irow(r);
+                    k0[q] = (int)hrp[(size_t)r];
+                    k1[q] = (int)hrp[(size_t)r + 1];
+                    tot += rlen(r);
+                }
+                grp_h[(size_t)g * 3 + 0] = make_int4(rr[0], rr[1], rr[2], rr[3]);
+                grp_h[(size_t)g * 3 + 1] = make_int4(k0[0], k0[1], k0[2], k0[3]);
+                grp_h[(size_t)g * 3 + 2] = make_int4(k1[0], k1[1], k1[2], k1[3]);
+                seg_row_h.push_back((int)g);  // a group item: {group id, 0, its nonzeros, -2}
+                seg_k0_h.push_back(0);
+                seg_k1_h.push_back((int)tot);
+                seg_split_h.push_back(-2);
+            }
+            h->ngrp = ng;
+            h->grp_rows = (int64_t)grp_members.size();
+        }
         h->nseg = (int64_t)seg_row_h.size();
         for (int64_t k = 0; k < h->nseg; ++k) h->seg_nnz += seg_k1_h[(size_t)k] - seg_k0_h[(size_t)k];
         h->nsplit = (int64_t)split_row_h.size();
@@ -873,6 +1005,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             CC(cudaMemcpyAsync(h->perm_fwd, perm_h.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
             CC(cudaMemcpyAsync(h->perm_inv, inv_h.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
             CC(cudaStreamSynchronize(st));
+            if (sh) inv_keep.swap(inv_h);
         }
     }
     mark("layout", st);
@@ -1030,6 +1163,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         for (int iter = 0;; ++iter) {
             // tables too large for shared memory next to the ring: read them from global memory
             if (!h->gmeta && !h->jbs && (ring + meta + 2048 > (size_t)smem_optin || (flags & AJM_GLOBAL_TABLES))) {
+                if (sh) return bail(fail(h, AJM_ERR_UNSUPPORTED, "shard layout tables do not fit shared memory"));
                 h->gmeta = 1;
                 h->fn = gmeta_fn(h->nseg > 0);
                 h->ring_fn = false;
@@ -1042,16 +1176,19 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             cudaError_t eo;
             {
                 std::lock_guard<std::mutex> lock(g_attr_mu);
-                eo = fn_occupancy(h->fn, h->dyn_smem, 100, &occ);
+                eo = fn_occupancy(h->fn, h->dyn_smem, 100, &occ, block_threads(h->nseg > 0));
             }
             CC(eo);
             if (occ < 1) return bail(fail(h, AJM_ERR_UNSUPPORTED, "solver kernel cannot be resident (%zu B smem)", h->dyn_smem));
             h->ctas_per_sm = occ;
             const int64_t g = (int64_t)h->sm_count * occ;
             h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(g, nitems));
+            // an emulated group shares the device: every rank takes the same 1/nranks of the
+            // resident CTAs (one launch runs them all)
+            if (sh && sh->colocated) h->grid = (int)std::max<int64_t>(1, g / sh->nranks);
             // <= 128 work items: one item per consumer warp on <= 16 CTAs, launched below as a
             // single cluster whose barrier lives in distributed shared memory
-            if (nitems <= 16 * AJM_WARPS && !env_no_cluster)
+            if (!sh && nitems <= 16 * AJM_WARPS && !env_no_cluster)
                 h->grid = (int)std::max<int64_t>(1, (nitems + AJM_WARPS - 1) / AJM_WARPS);
             if (h->grid != planned_grid) {  // plan() depends on the grid size only
                 plan(h->grid);
@@ -1066,7 +1203,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         const int G = h->grid;
         // small problems: the grid as ONE thread-block cluster, barrier and partial exchange in
         // distributed shared memory (AJM_NO_CLUSTER disables, for experiments)
-        if (G <= 16 && !env_no_cluster && (h->jbs || h->ring_fn)) {
+        if (!sh && G <= 16 && !env_no_cluster && (h->jbs || h->ring_fn)) {
             const SolveFn cf = h->jbs ? jblock_fn(h->jbs, true) : cluster_fn(h->seg_fn);
             // (the cluster kernels keep a 4-deep ring: per-pass latency, not L1, bounds them)
             const size_t cdyn = h->ring_fn ? (size_t)4 * AJM_UNIT_EL * 12 + h->meta_bytes : h->dyn_smem;
@@ -1076,7 +1213,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             if (G > 8) cudaFuncSetAttribute((const void*)cf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             cudaLaunchConfig_t qc = {};
             qc.gridDim = dim3(G);
-            qc.blockDim = dim3(kBlockThreads);
+            qc.blockDim = dim3(block_threads(h->nseg > 0));
             qc.dynamicSmemBytes = cdyn;
             cudaLaunchAttribute qa[1];
             qa[0].id = cudaLaunchAttributeClusterDimension;
@@ -1112,6 +1249,26 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
             cta_split_h[(size_t)cc + 1] = cta_split_h[(size_t)cc] + (int)per[(size_t)cc].size();
             for (int sp : per[(size_t)cc]) owner_split_h.push_back(sp);
         }
+        if (sh) {  // which CTA writes each row's x~^{t+1} (and so pushes its halo entries)
+            row_cta.assign((size_t)n, 0);
+            for (int cc = 0; cc < G; ++cc) {
+                const int u0 = cta_unit_h[(size_t)cc], u1 = cta_unit_h[(size_t)cc + 1];
+                if (u1 <= u0) continue;
+                const int64_t r0 = (int64_t)unit_c0_h[(size_t)u0] * 32;
+                const int64_t r1 = std::min<int64_t>(h->n_sell, (int64_t)unit_c0_h[(size_t)u1] * 32);
+                for (int64_t r = r0; r < r1; ++r) row_cta[(size_t)r] = cc;
+            }
+            for (int64_t k = 0; k < h->nseg; ++k) {
+                if (seg_split_h[(size_t)k] == -1) row_cta[(size_t)seg_row_h[(size_t)k]] = seg_cta[(size_t)k];
+                if (seg_split_h[(size_t)k] == -2) {
+                    const int4 gr = grp_h[(size_t)seg_row_h[(size_t)k] * 3];
+                    for (int r2 : {gr.x, gr.y, gr.z, gr.w})
+                        if (r2 >= 0) row_cta[(size_t)r2] = seg_cta[(size_t)k];
+                }
+            }
+            for (int cc = 0; cc < G; ++cc)
+                for (int sp : per[(size_t)cc]) row_cta[(size_t)split_row_h[(size_t)sp]] = cc;
+        }
     }
 
     mark("plan", st);
@@ -1119,18 +1276,36 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     // the six n-vectors in ONE allocation [X0 X1 X2 Qxp b D] (each padded to whole SELL chunks,
     // 256-byte aligned): the L2 persistence window below covers them with a single range
     h->n_pad = (std::max<int64_t>(n, h->nchunks * 32) + 31) / 32 * 32;
-    CC(dalloc(&h->vecs, (size_t)6 * h->n_pad, st));
-    CC(cudaMemsetAsync(h->vecs, 0, sizeof(double) * 6 * h->n_pad, st));
-    for (int k = 0; k < 3; ++k) h->X[k] = h->vecs + (size_t)k * h->n_pad;
-    h->Qxp = h->vecs + (size_t)3 * h->n_pad;
-    h->b = h->vecs + (size_t)4 * h->n_pad;
-    h->D = h->vecs + (size_t)5 * h->n_pad;
+    size_t vec_elems = (size_t)6 * h->n_pad;
+    if (sh) {
+        // a shard's iterate buffers carry its halo around the own rows: X_k = base + lo_pad, the
+        // lower halo at X_k[-H_lo .. -1], the upper at X_k[n .. n + H_hi - 1]; cudaMalloc (not the
+        // pool) so the allocation can be exported through CUDA IPC to the other ranks' processes
+        h->lo_pad = (h->h_lo + 31) / 32 * 32;
+        h->xstride = h->lo_pad + h->n_pad + (h->h_hi + 31) / 32 * 32;
+        vec_elems = (size_t)3 * h->xstride + (size_t)3 * h->n_pad;
+        CC(cudaMalloc((void**)&h->vecs, sizeof(double) * vec_elems));
+        for (int k = 0; k < 3; ++k) h->X[k] = h->vecs + (size_t)k * h->xstride + h->lo_pad;
+        double* rest = h->vecs + (size_t)3 * h->xstride;
+        h->Qxp = rest;
+        h->b = rest + (size_t)h->n_pad;
+        h->D = rest + (size_t)2 * h->n_pad;
+        CC(cudaMalloc((void**)&h->xch, sizeof(double) * (2 * AJM_MAX_RANKS * AJM_NPART + 1)));
+        CC(cudaMemsetAsync(h->xch, 0, sizeof(double) * (2 * AJM_MAX_RANKS * AJM_NPART + 1), st));
+    } else {
+        CC(dalloc(&h->vecs, vec_elems, st));
+        for (int k = 0; k < 3; ++k) h->X[k] = h->vecs + (size_t)k * h->n_pad;
+        h->Qxp = h->vecs + (size_t)3 * h->n_pad;
+        h->b = h->vecs + (size_t)4 * h->n_pad;
+        h->D = h->vecs + (size_t)5 * h->n_pad;
+    }
+    CC(cudaMemsetAsync(h->vecs, 0, sizeof(double) * vec_elems, st));
     // L2 residency: keep as much of the iterate vectors as the device allows in a
     // persisting L2 carve-out; the matrix stream goes through with evict_first hints
     h->win_bytes = 0;
     int l2size = 0;
     CC(cudaDeviceGetAttribute(&l2size, cudaDevAttrL2CacheSize, h->device));
-    const size_t vec_bytes = sizeof(double) * 6 * (size_t)h->n_pad;
+    const size_t vec_bytes = sizeof(double) * vec_elems;
     // vectors larger than the whole L2 (configs 4, 5): a persisting carve-out only takes L2 away
     // from everything else (measured 1138 -> 919 us/pass on config 4): eviction hints only
     if (vec_bytes > (size_t)l2size) {
@@ -1247,6 +1422,10 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     CC(h2d(h->unit_c0, unit_c0_h.data(), sizeof(int) * unit_c0_h.size()));
     CC(h2d(h->cta_seg, cta_seg_h.data(), sizeof(int) * cta_seg_h.size()));
     CC(h2d(h->seg_meta, seg_meta_h.data(), sizeof(int) * seg_meta_h.size()));
+    if (!grp_h.empty()) {
+        CC(dalloc(&h->grp, grp_h.size(), st));
+        CC(h2d(h->grp, grp_h.data(), sizeof(int4) * grp_h.size()));
+    }
     CC(h2d(h->seg_list, seg_list_h.data(), sizeof(int) * seg_list_h.size()));
     CC(h2d(h->seg_order, seg_order_h.data(), sizeof(int) * seg_order_h.size()));
     CC(h2d(h->seg_grp, seg_grp_h.data(), sizeof(int) * seg_grp_h.size()));
@@ -1279,7 +1458,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     mark("copies", st);
     // ---- validation + D (device) ----
     const int nblk = (int)((n + 255) / 256);
-    ajm_validate_diag_kernel<<<nblk, 256, 0, st>>>((int)n, h->rp, h->col, h->val, dmode == AJM_D_JBLOCK ? 0 : dmode, dtmp,
+    ajm_validate_diag_kernel<<<nblk, 256, 0, st>>>((int)n, (int)clo, (int)chi, h->rp, h->col, h->val, dmode == AJM_D_JBLOCK ? 0 : dmode, dtmp,
                                                    h->relabel ? h->X[2] : h->D, h->err,
                                                    vlong_h.empty() ? LLONG_MAX : (long long)kValidateLong);
     CC(cudaGetLastError());
@@ -1288,7 +1467,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         CC(dalloc(&vl, vlong_h.size(), st));
         CC(cudaMemcpyAsync(vl, vlong_h.data(), sizeof(int) * vlong_h.size(), cudaMemcpyHostToDevice, st));
         const int nl = (int)vlong_h.size();
-        ajm_validate_long_kernel<<<(nl + 7) / 8, 256, 0, st>>>((int)n, vl, nl, h->rp, h->col, h->val,
+        ajm_validate_long_kernel<<<(nl + 7) / 8, 256, 0, st>>>((int)clo, (int)chi, vl, nl, h->rp, h->col, h->val,
                                                                dmode == AJM_D_JBLOCK ? 0 : dmode, dtmp,
                                                                h->relabel ? h->X[2] : h->D, h->err);
         CC(cudaGetLastError());
@@ -1340,7 +1519,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     mark("validate", st);
     // columns in internal numbering (after validation, which needs the caller's order)
     if (h->relabel && nnz > 0) {
-        ajm_remap_kernel<<<2048, 256, 0, st>>>(nnz, h->perm_inv, h->col);
+        ajm_remap_kernel<<<2048, 256, 0, st>>>(nnz, (int)n, h->perm_inv, h->col);
         CC(cudaGetLastError());
     }
     mark("remap", st);
@@ -1377,13 +1556,14 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         int st8 = h->wide_rows ? 5 : 4;
         if (env_col8_stages) st8 = std::min(6, std::max(3, env_col8_stages));
         SolveFn f8 = col8_fn(h->nseg > 0, st8);
+
         const size_t dyn8 = (size_t)st8 * AJM_UNIT_EL * 9 + h->meta_bytes;
         int occ8 = 0;
         if (htab[AJM_CTAB_HASH + 1] == 0 && htab[AJM_CTAB_HASH] <= AJM_CTAB) {
             cudaError_t eo;
             {
                 std::lock_guard<std::mutex> lock(g_attr_mu);
-                eo = fn_occupancy(f8, dyn8, 100, &occ8);
+                eo = fn_occupancy(f8, dyn8, 100, &occ8, block_threads(h->nseg > 0));
             }
             CC(eo);
         }
@@ -1426,7 +1606,7 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         cudaError_t eo;
         {
             std::lock_guard<std::mutex> lock(g_attr_mu);
-            eo = fn_occupancy(h->fn, h->dyn_smem, pct, &occ);
+            eo = fn_occupancy(h->fn, h->dyn_smem, pct, &occ, block_threads(h->nseg > 0));
             if (eo == cudaSuccess && occ < h->ctas_per_sm && !h->cluster) {
                 pct = 100;
                 eo = cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
@@ -1442,8 +1622,12 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     double bb = 0.0;
     CC(cudaMemcpyAsync(&bb, h->scratch + 256, sizeof(double), cudaMemcpyDeviceToHost, st));
     CC(cudaStreamSynchronize(st));
-    if (!(bb > 0.0)) return bail(fail(h, AJM_ERR_ZERO_RHS, "||b|| = 0: relative residual undefined"));
-    h->nb = std::sqrt(bb);
+    if (sh) {
+        h->bsq_local = bb;  // ||b|| of the whole system: ajm_shard_connect, in rank order
+    } else {
+        if (!(bb > 0.0)) return bail(fail(h, AJM_ERR_ZERO_RHS, "||b|| = 0: relative residual undefined"));
+        h->nb = std::sqrt(bb);
+    }
     // without warp segments the solver never reads the CSR copy again (everything is in the SELL
     // copy): release it, halving the matrix footprint (config 5: 5.4 GB)
     if (h->nseg == 0) {
@@ -1452,7 +1636,40 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
         h->col = nullptr;
         h->val = nullptr;
     }
-    if (!h->jbs) h->fn_lz = lanczos_fn(h->nseg > 0, h->cluster != 0, h->gmeta != 0, h->col_bytes, h->ring_stages);
+    if (!h->jbs && !sh) h->fn_lz = lanczos_fn(h->nseg > 0, h->cluster != 0, h->gmeta != 0, h->col_bytes, h->ring_stages);
+    if (sh) {
+        // the rank's kernel: the same layout class with the halo exchange compiled in
+        h->fn = shard_fn(h->col_bytes, h->nseg > 0, h->ring_stages);
+        {
+            std::lock_guard<std::mutex> lock(g_attr_mu);
+            int occ = 0;
+            cudaError_t eo = fn_occupancy(h->fn, h->dyn_smem, h->carveout, &occ, block_threads(h->nseg > 0));
+            if (eo == cudaSuccess && occ < h->ctas_per_sm) {  // (its pass-struct copy in shared memory)
+                h->carveout = 100;
+                eo = fn_occupancy(h->fn, h->dyn_smem, h->carveout, &occ, block_threads(h->nseg > 0));
+            }
+            if (eo == cudaSuccess && occ < h->ctas_per_sm)
+                return bail(fail(h, AJM_ERR_UNSUPPORTED, "shard kernel cannot keep %d CTAs per SM resident", h->ctas_per_sm));
+            CC(eo);
+        }
+        // send entries grouped by the CTA that writes the row: {internal row, peer, k, 0}, k = the
+        // entry's position in this rank's list to that peer (turned into an offset at connect)
+        std::vector<std::vector<int4>> per_cta((size_t)h->grid);
+        size_t pos = 0;
+        for (int r = 0; r < sh->nranks; ++r)
+            for (int64_t k = 0; k < sh->send_cnt[(size_t)r]; ++k, ++pos) {
+                const int64_t j = sh->send_rows[pos];
+                const int ir = h->relabel ? inv_keep[(size_t)j] : (int)j;
+                per_cta[(size_t)row_cta[(size_t)ir]].push_back(make_int4(ir, r, (int)k, 0));
+            }
+        h->snd_cta_host.assign((size_t)h->grid + 1, 0);
+        h->snd_host.clear();
+        for (int cc = 0; cc < h->grid; ++cc) {
+            h->snd_cta_host[(size_t)cc] = (int)h->snd_host.size();
+            h->snd_host.insert(h->snd_host.end(), per_cta[(size_t)cc].begin(), per_cta[(size_t)cc].end());
+        }
+        h->snd_cta_host[(size_t)h->grid] = (int)h->snd_host.size();
+    }
     mark("validate+fill+norm", st);
     if (tsc) fprintf(stderr, "[ajm create ms]%s\n", tsc_log.c_str());
     *out = h;
@@ -1460,12 +1677,9 @@ ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t
     return AJM_OK;
 }
 
-ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t maxit,
-                       ajm_policy_t policy, double* x_out, ajm_result_t* res, double* res_hist,
-                       double* f_hist, int64_t* restart_iters, int64_t restart_cap,
-                       void* cuda_stream) {
-    NvtxScope nvtx_scope_("ajm_solve");
-    if (!h) return fail(nullptr, AJM_ERR_INVALID_ARG, "NULL handle");
+// ---- ajm_solve in phases (shared with ajm_group_solve) ----
+static ajm_status_t solve_check(ajm_ctx* h, const double* x_out, double tol, int64_t maxit, ajm_policy_t policy,
+                                const int64_t* restart_iters, int64_t restart_cap) {
     h->err_msg.clear();
     if (!x_out) return fail(h, AJM_ERR_INVALID_ARG, "x_out is NULL");
     if (!(tol >= 0.0)) return fail(h, AJM_ERR_INVALID_ARG, "tol must be >= 0");
@@ -1475,7 +1689,15 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
     if (policy.restart && !policy.momentum)
         return fail(h, AJM_ERR_INVALID_ARG, "restart requires momentum (Alg. 2/3)");
     if (restart_iters && restart_cap < 0) return fail(h, AJM_ERR_INVALID_ARG, "restart_cap < 0");
-    cudaStream_t st = (cudaStream_t)cuda_stream;
+    if (h->shard && !h->connected) return fail(h, AJM_ERR_INVALID_ARG, "shard handle is not connected (ajm_shard_connect)");
+    if (h->broken) return fail(h, AJM_ERR_CUDA, "an earlier solve of this shard group timed out: re-create the group");
+    return AJM_OK;
+}
+
+// x~^0, x^{-1}, Q x^{-1}, the control block (the own rows; a shard's halo of x~^0 is exchanged by
+// the kernel's round 0)
+static ajm_status_t solve_prep(ajm_ctx* h, const double* x0, double tol, int64_t maxit, ajm_policy_t policy,
+                               cudaStream_t st) {
     const int64_t n = h->n;
     ajm_status_t s = ensure_hist(h, maxit + 2, st);
     if (s != AJM_OK) return s;
@@ -1529,39 +1751,29 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
                                            policy.restart ? 1 : 0, policy.k0, h->nb, hr, hf, hd, hda);
     AJM_CUDA(h, cudaGetLastError());
 
-    AJM_CUDA(h, cudaEventRecord(h->ev0, st));
-    int64_t launches = 0;
-    if (!(h->flags & AJM_LOOP_HOST)) {
-        // the whole Alg. 3 loop: one cooperative launch
-        AjmPass p = make_pass(h, (int)(maxit + 1));
-        AJM_CUDA(h, launch_solver(h, p, st));
-        launches = 1;
-    } else {
-        // debug host loop: one pass per launch, the control state round-trips through global memory
-        AjmPass p = make_pass(h, 1);
-        int64_t issued = 0;
-        for (;;) {
-            const int64_t chunk = std::min<int64_t>(64, maxit + 1 - issued);
-            for (int64_t i = 0; i < chunk; ++i) AJM_CUDA(h, launch_solver(h, p, st));
-            issued += chunk;
-            AJM_CUDA(h, cudaMemcpyAsync(h->h_ctrl, h->ctrl, sizeof(AjmCtrl), cudaMemcpyDeviceToHost, st));
-            AJM_CUDA(h, cudaStreamSynchronize(st));
-            if (h->h_ctrl->s.done || issued >= maxit + 1) break;
-        }
-        launches = issued;
-    }
-    AJM_CUDA(h, cudaEventRecord(h->ev1, st));
+    return AJM_OK;
+}
+
+// after the loop: the control block, the answer in the caller's order and the histories
+static ajm_status_t solve_post(ajm_ctx* h, int64_t launches, float ms, double* x_out, ajm_result_t* res,
+                               double* res_hist, double* f_hist, int64_t* restart_iters, int64_t restart_cap,
+                               cudaStream_t st) {
+    const int64_t n = h->n;
     AJM_CUDA(h, cudaMemcpyAsync(h->h_ctrl, h->ctrl, sizeof(AjmCtrl), cudaMemcpyDeviceToHost, st));
     AJM_CUDA(h, cudaStreamSynchronize(st));
     const AjmCtrl& c = *h->h_ctrl;
+    if (h->shard) {  // every rank added one arrival per round to every rank's counter
+        if (c.timeout_flag || !c.s.done) h->broken = true;
+        else h->bar_base += (unsigned long long)h->nranks * (unsigned long long)(c.s.iterations + 2);
+    }
     if (c.timeout_flag) return fail(h, AJM_ERR_CUDA, "device barrier wait timed out (internal error)");
     if (!c.s.done) return fail(h, AJM_ERR_CUDA, "iteration loop ended without a termination decision");
-    float ms = 0.f;
-    AJM_CUDA(h, cudaEventElapsedTime(&ms, h->ev0, h->ev1));
     h->last_loop_ms = ms;
     h->last_passes = c.s.iterations + 1;
     h->last_launches = launches;
     h->last_iterations = c.s.iterations;
+    double* hr = h->hist;
+    double* hf = h->hist + h->hist_cap;
     if (h->ts) {  // debug: mean phase durations of CTA 0 over the first passes
         unsigned long long hts[64 * 8];
         AJM_CUDA(h, cudaMemcpy(hts, h->ts, sizeof(hts), cudaMemcpyDeviceToHost));
@@ -1627,6 +1839,456 @@ ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t max
     return AJM_OK;
 }
 
+
+ajm_status_t ajm_solve(ajm_handle_t h, const double* x0, double tol, int64_t maxit,
+                       ajm_policy_t policy, double* x_out, ajm_result_t* res, double* res_hist,
+                       double* f_hist, int64_t* restart_iters, int64_t restart_cap,
+                       void* cuda_stream) {
+    NvtxScope nvtx_scope_("ajm_solve");
+    if (!h) return fail(nullptr, AJM_ERR_INVALID_ARG, "NULL handle");
+    ajm_status_t s = solve_check(h, x_out, tol, maxit, policy, restart_iters, restart_cap);
+    if (s != AJM_OK) return s;
+    if (h->colocated) return fail(h, AJM_ERR_INVALID_ARG, "an AJM_SHARD_COLOCATED group is solved by ajm_group_solve");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    s = solve_prep(h, x0, tol, maxit, policy, st);
+    if (s != AJM_OK) return s;
+    AJM_CUDA(h, cudaEventRecord(h->ev0, st));
+    int64_t launches = 0;
+    if (!(h->flags & AJM_LOOP_HOST)) {
+        // the whole Alg. 3 loop: one cooperative launch
+        AjmPass p = make_pass(h, (int)(maxit + 1));
+        AJM_CUDA(h, launch_solver(h, p, st));
+        launches = 1;
+    } else {
+        // debug host loop: one pass per launch, the control state round-trips through global memory
+        AjmPass p = make_pass(h, 1);
+        int64_t issued = 0;
+        for (;;) {
+            const int64_t chunk = std::min<int64_t>(64, maxit + 1 - issued);
+            for (int64_t i = 0; i < chunk; ++i) AJM_CUDA(h, launch_solver(h, p, st));
+            issued += chunk;
+            AJM_CUDA(h, cudaMemcpyAsync(h->h_ctrl, h->ctrl, sizeof(AjmCtrl), cudaMemcpyDeviceToHost, st));
+            AJM_CUDA(h, cudaStreamSynchronize(st));
+            if (h->h_ctrl->s.done || issued >= maxit + 1) break;
+        }
+        launches = issued;
+    }
+    AJM_CUDA(h, cudaEventRecord(h->ev1, st));
+    AJM_CUDA(h, cudaEventSynchronize(h->ev1));
+    float ms = 0.f;
+    AJM_CUDA(h, cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    return solve_post(h, launches, ms, x_out, res, res_hist, f_hist, restart_iters, restart_cap, st);
+}
+
+// ------------------------------------------------------------------------------------------------
+// Row-block sharded solve (NEXT-2; include/ajm.h)
+// ------------------------------------------------------------------------------------------------
+
+ajm_status_t ajm_create(ajm_handle_t* out, int64_t n, int64_t nnz, const int64_t* row_ptr,
+                        const int32_t* col_idx, const double* vals, const double* b, int32_t dmode,
+                        const double* d, uint32_t flags, void* cuda_stream) {
+    return create_impl(out, n, nnz, row_ptr, col_idx, vals, b, dmode, d, flags, cuda_stream, nullptr);
+}
+
+ajm_status_t ajm_partition_rows(int64_t n, const int64_t* row_ptr, int32_t nranks, int64_t* row_starts) {
+    g_create_error.clear();
+    if (!row_ptr || !row_starts) return fail(nullptr, AJM_ERR_INVALID_ARG, "NULL argument");
+    if (nranks < 1 || nranks > AJM_MAX_RANKS || n < nranks)
+        return fail(nullptr, AJM_ERR_INVALID_ARG, "need 1 <= nranks <= min(%d, n)", AJM_MAX_RANKS);
+    if (row_ptr[0] != 0) return fail(nullptr, AJM_ERR_CSR_INVALID, "row_ptr[0] != 0");
+    for (int64_t i = 0; i < n; ++i)
+        if (row_ptr[i + 1] < row_ptr[i]) return fail(nullptr, AJM_ERR_CSR_INVALID, "row_ptr decreases at row %lld", (long long)i);
+    // block r starts at the first row whose prefix cost reaches r/nranks of the total (12 B per
+    // nonzero + 56 B per row: the pass's bytes), at least one row per block
+    const double total = 12.0 * (double)row_ptr[n] + 56.0 * (double)n;
+    row_starts[0] = 0;
+    int64_t i = 0;
+    for (int r = 1; r < nranks; ++r) {
+        const double lim = total * (double)r / (double)nranks;
+        while (i < n && 12.0 * (double)row_ptr[i] + 56.0 * (double)i < lim) ++i;
+        row_starts[r] = std::min<int64_t>(std::max<int64_t>(i, row_starts[r - 1] + 1), n - (nranks - r));
+        i = row_starts[r];
+    }
+    row_starts[nranks] = n;
+    return AJM_OK;
+}
+
+namespace {
+// The plan of one rank (host only): local columns, halo (sorted global indices), send lists.
+ajm_status_t shard_plan_host(int rank, int R, const int64_t* starts, const int64_t* rp, const int32_t* colg,
+                             std::vector<int32_t>* col_loc, std::vector<int64_t>* halo_glob,
+                             std::vector<int64_t>* send_rows, ShardIn& out) {
+    if (R < 1 || R > AJM_MAX_RANKS || rank < 0 || rank >= R || !starts || !rp)
+        return fail(nullptr, AJM_ERR_INVALID_ARG, "bad rank / nranks / NULL argument");
+    if (starts[0] != 0) return fail(nullptr, AJM_ERR_INVALID_ARG, "row_starts[0] != 0");
+    for (int r = 0; r < R; ++r)
+        if (starts[r + 1] <= starts[r]) return fail(nullptr, AJM_ERR_INVALID_ARG, "row_starts must increase (every block non-empty)");
+    const int64_t n = starts[R], r0 = starts[rank], r1 = starts[rank + 1], nl = r1 - r0;
+    if (n >= ((int64_t)1 << 31)) return fail(nullptr, AJM_ERR_UNSUPPORTED, "n must be < 2^31");
+    if (rp[0] != 0) return fail(nullptr, AJM_ERR_CSR_INVALID, "row_ptr[0] != 0");
+    for (int64_t i = 0; i < nl; ++i)
+        if (rp[i + 1] < rp[i]) return fail(nullptr, AJM_ERR_CSR_INVALID, "row_ptr decreases at local row %lld", (long long)i);
+    const int64_t nnz = rp[nl];
+    if (nnz > 0 && !colg) return fail(nullptr, AJM_ERR_INVALID_ARG, "col_idx is NULL");
+    auto owner = [&](int64_t j) { return (int)(std::upper_bound(starts, starts + R + 1, j) - starts) - 1; };
+    // halo: the distinct out-of-block columns, sorted (lower ranks' entries first)
+    int bad = 0;
+    std::vector<int32_t> hal;
+    {
+        std::vector<std::vector<int32_t>> th;
+#pragma omp parallel
+        {
+#pragma omp single
+            th.resize((size_t)omp_get_num_threads());
+            std::vector<int32_t>& v = th[(size_t)omp_get_thread_num()];
+#pragma omp for schedule(static) reduction(| : bad)
+            for (int64_t k = 0; k < nnz; ++k) {
+                const int64_t j = colg[k];
+                if (j < 0 || j >= n) bad |= 1;
+                else if (j < r0 || j >= r1) v.push_back((int32_t)j);
+            }
+        }
+        for (auto& v : th) hal.insert(hal.end(), v.begin(), v.end());
+    }
+    if (bad) return fail(nullptr, AJM_ERR_CSR_INVALID, "column index out of [0, n)");
+    std::sort(hal.begin(), hal.end());
+    hal.erase(std::unique(hal.begin(), hal.end()), hal.end());
+    const int64_t hlo = (int64_t)(std::lower_bound(hal.begin(), hal.end(), (int32_t)r0) - hal.begin());
+    out.rank = rank;
+    out.nranks = R;
+    out.n_glob = n;
+    out.row0 = r0;
+    out.h_lo = hlo;
+    out.h_hi = (int64_t)hal.size() - hlo;
+    out.halo_cnt.assign((size_t)R, 0);
+    for (int32_t j : hal) ++out.halo_cnt[(size_t)owner(j)];
+    if (halo_glob) halo_glob->assign(hal.begin(), hal.end());
+    if (col_loc) {
+        col_loc->resize((size_t)nnz);
+#pragma omp parallel for schedule(static)
+        for (int64_t k = 0; k < nnz; ++k) {
+            const int32_t j = colg[k];
+            int64_t l;
+            if (j >= r0 && j < r1) l = j - r0;
+            else {
+                const int64_t pos = (int64_t)(std::lower_bound(hal.begin(), hal.end(), j) - hal.begin());
+                l = pos < hlo ? pos - hlo : nl + (pos - hlo);
+            }
+            (*col_loc)[(size_t)k] = (int32_t)l;
+        }
+    }
+    // send lists: by symmetry of the structure, rank s reads own row i iff row i has a column in s's block
+    std::vector<std::vector<std::vector<int64_t>>> ts;  // [thread][dest] rows, contiguous row ranges
+    int nt = 1;
+#pragma omp parallel
+    {
+#pragma omp single
+        {
+            nt = omp_get_num_threads();
+            ts.assign((size_t)nt, std::vector<std::vector<int64_t>>((size_t)R));
+        }
+        const int tid = omp_get_thread_num();
+        const int64_t lo = nl * tid / nt, hi = nl * (tid + 1) / nt;
+        std::vector<int64_t> last((size_t)R, -1);
+        for (int64_t i = lo; i < hi; ++i)
+            for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+                const int64_t j = colg[k];
+                if (j >= r0 && j < r1) continue;
+                const int s = owner(j);
+                if (last[(size_t)s] != i) {
+                    last[(size_t)s] = i;
+                    ts[(size_t)tid][(size_t)s].push_back(i);
+                }
+            }
+    }
+    out.send_cnt.assign((size_t)R, 0);
+    std::vector<int64_t> sr;
+    for (int s = 0; s < R; ++s)
+        for (int t2 = 0; t2 < nt; ++t2) {
+            out.send_cnt[(size_t)s] += (int64_t)ts[(size_t)t2][(size_t)s].size();
+            sr.insert(sr.end(), ts[(size_t)t2][(size_t)s].begin(), ts[(size_t)t2][(size_t)s].end());
+        }
+    out.send_rows = sr;
+    if (send_rows) send_rows->swap(sr);
+    return AJM_OK;
+}
+
+// The connection record of one rank (ajm_shard_export / ajm_shard_connect)
+struct ShardBlob {
+    uint32_t magic;
+    int32_t version, rank, nranks;
+    int32_t device, pid, colocated, grid;
+    int64_t n_loc, row0, n_glob;
+    cudaIpcMemHandle_t vec_h, xch_h;
+    int32_t ipc_ok, carveout;
+    uint64_t vec_ptr, xch_ptr, fn;
+    int64_t x_off[3];
+    int64_t dyn_smem;
+    int64_t halo_off[AJM_MAX_RANKS], halo_cnt[AJM_MAX_RANKS], send_cnt[AJM_MAX_RANKS];
+    double bsq;
+};
+static_assert(sizeof(ShardBlob) <= AJM_SHARD_BLOB_BYTES, "shard record size");
+constexpr uint32_t kBlobMagic = 0x414a4d53u;  // "AJMS"
+}  // namespace
+
+ajm_status_t ajm_shard_plan(int32_t rank, int32_t nranks, const int64_t* row_starts, const int64_t* row_ptr,
+                            const int32_t* col_glob, int32_t* col_loc, int64_t* halo_glob, int64_t* send_rows,
+                            int64_t* counts) {
+    g_create_error.clear();
+    if (!counts) return fail(nullptr, AJM_ERR_INVALID_ARG, "counts is NULL");
+    ShardIn sp;
+    std::vector<int32_t> cl;
+    std::vector<int64_t> hg, sr;
+    ajm_status_t s = shard_plan_host(rank, nranks, row_starts, row_ptr, col_glob, col_loc ? &cl : nullptr,
+                                     halo_glob ? &hg : nullptr, send_rows ? &sr : nullptr, sp);
+    if (s != AJM_OK) return s;
+    counts[0] = sp.h_lo;
+    counts[1] = sp.h_hi;
+    for (int r = 0; r < nranks; ++r) {
+        counts[2 + r] = sp.halo_cnt[(size_t)r];
+        counts[2 + nranks + r] = sp.send_cnt[(size_t)r];
+    }
+    if (col_loc) std::copy(cl.begin(), cl.end(), col_loc);
+    if (halo_glob) std::copy(hg.begin(), hg.end(), halo_glob);
+    if (send_rows) std::copy(sr.begin(), sr.end(), send_rows);
+    return AJM_OK;
+}
+
+ajm_status_t ajm_shard_create(ajm_handle_t* out, int32_t rank, int32_t nranks, const int64_t* row_starts,
+                              int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx, const double* vals,
+                              const double* b, int32_t dmode, const double* d, uint32_t flags,
+                              void* cuda_stream) {
+    g_create_error.clear();
+    if (!out || !row_starts || !row_ptr || !b || (nnz > 0 && (!col_idx || !vals)))
+        return fail(nullptr, AJM_ERR_INVALID_ARG, "NULL argument");
+    if (nranks < 1 || nranks > AJM_MAX_RANKS || rank < 0 || rank >= nranks)
+        return fail(nullptr, AJM_ERR_INVALID_ARG, "bad rank / nranks (1 <= nranks <= %d)", AJM_MAX_RANKS);
+    if (nnz < 0) return fail(nullptr, AJM_ERR_INVALID_ARG, "nnz < 0");
+    for (int r = 0; r < nranks; ++r)
+        if (row_starts[r + 1] <= row_starts[r]) return fail(nullptr, AJM_ERR_INVALID_ARG, "row_starts must increase");
+    const int64_t nl = row_starts[rank + 1] - row_starts[rank];
+    // the plan needs the rank's structure on the host
+    std::vector<int64_t> rph;
+    std::vector<int32_t> colh;
+    const int64_t* rpp = row_ptr;
+    const int32_t* cp = col_idx;
+    if (is_device_ptr(row_ptr)) {
+        rph.resize((size_t)nl + 1);
+        if (cudaMemcpy(rph.data(), row_ptr, sizeof(int64_t) * (nl + 1), cudaMemcpyDeviceToHost) != cudaSuccess)
+            return fail(nullptr, AJM_ERR_CUDA, "row_ptr copy failed");
+        rpp = rph.data();
+    }
+    if (rpp[nl] != nnz) return fail(nullptr, AJM_ERR_CSR_INVALID, "row_ptr[n_loc] != nnz");
+    if (nnz > 0 && is_device_ptr(col_idx)) {
+        colh.resize((size_t)nnz);
+        if (cudaMemcpy(colh.data(), col_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return fail(nullptr, AJM_ERR_CUDA, "col_idx copy failed");
+        cp = colh.data();
+    }
+    ShardIn sp;
+    std::vector<int32_t> cl;
+    ajm_status_t s = shard_plan_host(rank, nranks, row_starts, rpp, cp, &cl, nullptr, nullptr, sp);
+    if (s != AJM_OK) return s;
+    sp.colocated = (flags & AJM_SHARD_COLOCATED) ? 1 : 0;
+    return create_impl(out, nl, nnz, rpp, cl.data(), vals, b, dmode, d, flags & ~AJM_SHARD_COLOCATED, cuda_stream, &sp);
+}
+
+ajm_status_t ajm_shard_export(ajm_handle_t h, void* blob) {
+    if (!h || !blob) return fail(h, AJM_ERR_INVALID_ARG, "NULL argument");
+    if (!h->shard) return fail(h, AJM_ERR_INVALID_ARG, "not a shard handle");
+    ShardBlob bl;
+    memset(&bl, 0, sizeof bl);
+    bl.magic = kBlobMagic;
+    bl.version = AJM_ABI_VERSION;
+    bl.rank = h->rank;
+    bl.nranks = h->nranks;
+    bl.device = h->device;
+    bl.pid = (int32_t)getpid();
+    bl.colocated = h->colocated;
+    bl.grid = h->grid;
+    bl.n_loc = h->n;
+    bl.row0 = h->row0;
+    bl.n_glob = h->n_glob;
+    bl.ipc_ok = (cudaIpcGetMemHandle(&bl.vec_h, h->vecs) == cudaSuccess &&
+                 cudaIpcGetMemHandle(&bl.xch_h, h->xch) == cudaSuccess) ? 1 : 0;
+    cudaGetLastError();
+    bl.carveout = h->carveout;
+    bl.vec_ptr = (uint64_t)(uintptr_t)h->vecs;
+    bl.xch_ptr = (uint64_t)(uintptr_t)h->xch;
+    bl.fn = (uint64_t)(uintptr_t)h->fn;
+    for (int k = 0; k < 3; ++k) bl.x_off[k] = (int64_t)(h->X[k] - h->vecs);
+    bl.dyn_smem = (int64_t)h->dyn_smem;
+    int64_t lo = -h->h_lo, hi = h->n;  // where each source rank's entries start in this rank's halo
+    for (int r = 0; r < h->nranks; ++r) {
+        bl.halo_cnt[r] = h->halo_cnt[(size_t)r];
+        bl.send_cnt[r] = h->send_cnt[(size_t)r];
+        if (r < h->rank) { bl.halo_off[r] = lo; lo += h->halo_cnt[(size_t)r]; }
+        else if (r > h->rank) { bl.halo_off[r] = hi; hi += h->halo_cnt[(size_t)r]; }
+    }
+    bl.bsq = h->bsq_local;
+    memset(blob, 0, AJM_SHARD_BLOB_BYTES);
+    memcpy(blob, &bl, sizeof bl);
+    return AJM_OK;
+}
+
+ajm_status_t ajm_shard_connect(ajm_handle_t h, const void* blobs) {
+    if (!h || !blobs) return fail(h, AJM_ERR_INVALID_ARG, "NULL argument");
+    if (!h->shard) return fail(h, AJM_ERR_INVALID_ARG, "not a shard handle");
+    if (h->connected) return fail(h, AJM_ERR_INVALID_ARG, "already connected");
+    h->err_msg.clear();
+    const int R = h->nranks, me = h->rank;
+    std::vector<ShardBlob> bl((size_t)R);
+    for (int r = 0; r < R; ++r) memcpy(&bl[(size_t)r], (const char*)blobs + (size_t)r * AJM_SHARD_BLOB_BYTES, sizeof(ShardBlob));
+    for (int r = 0; r < R; ++r) {
+        const ShardBlob& b = bl[(size_t)r];
+        if (b.magic != kBlobMagic || b.version != AJM_ABI_VERSION || b.rank != r || b.nranks != R || b.n_glob != h->n_glob)
+            return fail(h, AJM_ERR_INVALID_ARG, "record %d is not rank %d of this group", r, r);
+        if (r + 1 < R && b.row0 + b.n_loc != bl[(size_t)r + 1].row0)
+            return fail(h, AJM_ERR_INVALID_ARG, "records disagree on the row partition");
+        if (r != me && (b.halo_cnt[me] != h->send_cnt[(size_t)r] || b.send_cnt[me] != h->halo_cnt[(size_t)r]))
+            return fail(h, AJM_ERR_NOT_SYMMETRIC, "rank %d's halo from rank %d (%lld entries) differs from rank %d's send "
+                        "list (%lld): Q is not structurally symmetric", r, me, (long long)b.halo_cnt[me], me,
+                        (long long)h->send_cnt[(size_t)r]);
+        if (h->colocated && (b.pid != (int32_t)getpid() || b.device != h->device || !b.colocated))
+            return fail(h, AJM_ERR_INVALID_ARG, "an AJM_SHARD_COLOCATED group must live in one process on one device");
+    }
+    // ||b||^2 summed in rank order: the same bits on every rank
+    double bb = 0.0;
+    for (int r = 0; r < R; ++r) bb += bl[(size_t)r].bsq;
+    if (!(bb > 0.0)) return fail(h, AJM_ERR_ZERO_RHS, "||b|| = 0: relative residual undefined");
+    h->peers_host.assign((size_t)R, AjmPeer{});
+    for (int r = 0; r < R; ++r) {
+        const ShardBlob& b = bl[(size_t)r];
+        double* vec = nullptr;
+        double* xch = nullptr;
+        if (r == me) {
+            vec = h->vecs;
+            xch = h->xch;
+        } else if (b.pid == (int32_t)getpid()) {
+            vec = (double*)(uintptr_t)b.vec_ptr;
+            xch = (double*)(uintptr_t)b.xch_ptr;
+            if (b.device != h->device) {
+                cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                    return fail(h, AJM_ERR_CUDA, "peer access to device %d: %s", b.device, cudaGetErrorString(e));
+                cudaGetLastError();
+            }
+        } else {
+            if (!b.ipc_ok) return fail(h, AJM_ERR_CUDA, "rank %d could not export CUDA IPC handles", r);
+            void* pv = nullptr;
+            void* px = nullptr;
+            AJM_CUDA(h, cudaIpcOpenMemHandle(&pv, b.vec_h, cudaIpcMemLazyEnablePeerAccess));
+            h->ipc_opened.push_back(pv);
+            AJM_CUDA(h, cudaIpcOpenMemHandle(&px, b.xch_h, cudaIpcMemLazyEnablePeerAccess));
+            h->ipc_opened.push_back(px);
+            vec = (double*)pv;
+            xch = (double*)px;
+        }
+        AjmPeer& pe = h->peers_host[(size_t)r];
+        for (int k = 0; k < 3; ++k) pe.x[k] = vec + b.x_off[k];
+        pe.slot = xch;
+        pe.bar = reinterpret_cast<unsigned long long*>(xch + 2 * AJM_MAX_RANKS * AJM_NPART);
+    }
+    // the send entries' positions become offsets into the destination's buffers
+    std::vector<int4> snd = h->snd_host;
+    for (int4& e : snd) e.z = (int)(bl[(size_t)e.y].halo_off[me] + e.z);
+    AJM_CUDA(h, cudaMalloc((void**)&h->peers, sizeof(AjmPeer) * R));
+    AJM_CUDA(h, cudaMemcpy(h->peers, h->peers_host.data(), sizeof(AjmPeer) * R, cudaMemcpyHostToDevice));
+    AJM_CUDA(h, cudaMalloc((void**)&h->snd_cta, sizeof(int) * h->snd_cta_host.size()));
+    AJM_CUDA(h, cudaMemcpy(h->snd_cta, h->snd_cta_host.data(), sizeof(int) * h->snd_cta_host.size(), cudaMemcpyHostToDevice));
+    AJM_CUDA(h, cudaMalloc((void**)&h->snd, sizeof(int4) * std::max<size_t>(1, snd.size())));
+    if (!snd.empty()) AJM_CUDA(h, cudaMemcpy(h->snd, snd.data(), sizeof(int4) * snd.size(), cudaMemcpyHostToDevice));
+    h->nb = std::sqrt(bb);
+    h->connected = true;
+    return AJM_OK;
+}
+
+ajm_status_t ajm_group_solve(const ajm_handle_t* hs, int32_t nranks, const double* x0, double tol,
+                             int64_t maxit, ajm_policy_t policy, double* x_out, ajm_result_t* res,
+                             double* res_hist, double* f_hist, int64_t* restart_iters, int64_t restart_cap,
+                             void* cuda_stream) {
+    NvtxScope nvtx_scope_("ajm_group_solve");
+    if (!hs || nranks < 1 || nranks > AJM_MAX_RANKS || !hs[0]) return fail(nullptr, AJM_ERR_INVALID_ARG, "bad handle array");
+    ajm_ctx* h0 = hs[0];
+    for (int r = 0; r < nranks; ++r) {
+        ajm_ctx* h = hs[r];
+        if (!h || !h->shard || !h->colocated || h->rank != r || h->nranks != nranks)
+            return fail(h0, AJM_ERR_INVALID_ARG, "handle %d is not rank %d of an AJM_SHARD_COLOCATED group of %d", r, r, nranks);
+        if (h->col_bytes != h0->col_bytes || h->grid != h0->grid)
+            return fail(h0, AJM_ERR_UNSUPPORTED, "ranks 0 and %d chose different column encodings / grids: one launch "
+                        "cannot run both (create the group with AJM_INT32_COLUMNS)", r);
+        ajm_status_t s = solve_check(h, x_out, tol, maxit, policy, restart_iters, restart_cap);
+        if (s != AJM_OK) return s == AJM_OK ? s : fail(h0, s, "rank %d: %s", r, h->err_msg.c_str());
+    }
+    // ONE kernel for every rank: the segment phases if any rank has long rows, the deepest ring of
+    // the ranks (each rank's tables sit behind the ring in shared memory)
+    bool any_seg = false;
+    int stages = 0;
+    size_t meta = 0;
+    for (int r = 0; r < nranks; ++r) {
+        any_seg = any_seg || hs[r]->nseg > 0;
+        stages = std::max(stages, hs[r]->ring_stages);
+        meta = std::max(meta, hs[r]->meta_bytes);
+    }
+    if (h0->col_bytes == 1) stages = std::max(4, std::min(5, stages));
+    else stages = std::max(3, std::min(4, stages));
+    const SolveFn gfn = shard_fn(h0->col_bytes, any_seg, stages);
+    const size_t gdyn = (size_t)stages * AJM_UNIT_EL * (h0->col_bytes == 1 ? 9 : 12) + meta;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    for (int r = 0; r < nranks; ++r) {
+        ajm_ctx* h = hs[r];
+        ajm_status_t s = solve_prep(h, x0 ? x0 + h->row0 : nullptr, tol, maxit, policy, st);
+        if (s != AJM_OK) return fail(h0, s, "rank %d: %s", r, h->err_msg.c_str());
+    }
+    std::vector<AjmPass> ps((size_t)nranks);
+    for (int r = 0; r < nranks; ++r) ps[(size_t)r] = make_pass(hs[r], (int)(maxit + 1));
+    if (!h0->emu) AJM_CUDA(h0, cudaMalloc((void**)&h0->emu, sizeof(AjmPass) * AJM_MAX_RANKS));
+    AJM_CUDA(h0, cudaMemcpyAsync(h0->emu, ps.data(), sizeof(AjmPass) * nranks, cudaMemcpyHostToDevice, st));
+    AjmPass p = ps[0];
+    p.sh.emu = h0->emu;
+    p.sh.emu_grid = h0->grid;
+    AJM_CUDA(h0, cudaStreamSynchronize(st));  // ps lives until the copy has run
+    AJM_CUDA(h0, cudaEventRecord(h0->ev0, st));
+    {
+        std::lock_guard<std::mutex> lock(g_attr_mu);
+        int occ = 0;
+        cudaError_t e = fn_occupancy(gfn, gdyn, 100, &occ, block_threads(any_seg));
+        if (e == cudaSuccess && (int64_t)occ * h0->sm_count < (int64_t)h0->grid * nranks)
+            return fail(h0, AJM_ERR_UNSUPPORTED, "the group's %d CTAs cannot be co-resident (%d per SM)", h0->grid * nranks, occ);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(h0->grid * nranks));
+        cfg.blockDim = dim3(block_threads(any_seg));
+        cfg.dynamicSmemBytes = gdyn;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;  // every rank's CTAs co-resident
+        at[0].val.cooperative = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, gfn, p);
+        AJM_CUDA(h0, e);
+    }
+    AJM_CUDA(h0, cudaEventRecord(h0->ev1, st));
+    AJM_CUDA(h0, cudaEventSynchronize(h0->ev1));
+    float ms = 0.f;
+    AJM_CUDA(h0, cudaEventElapsedTime(&ms, h0->ev0, h0->ev1));
+    // every rank took the same decisions: its own control block says so
+    ajm_result_t r0res = {};
+    for (int r = 0; r < nranks; ++r) {
+        ajm_ctx* h = hs[r];
+        ajm_result_t rr = {};
+        ajm_status_t s = solve_post(h, 1, ms, x_out + h->row0, &rr, r == 0 ? res_hist : nullptr, r == 0 ? f_hist : nullptr,
+                                    r == 0 ? restart_iters : nullptr, restart_cap, st);
+        if (s != AJM_OK) return fail(h0, s, "rank %d: %s", r, h->err_msg.c_str());
+        if (r == 0) r0res = rr;
+        else if (rr.iterations != r0res.iterations || rr.status != r0res.status || rr.n_restarts != r0res.n_restarts ||
+                 memcmp(&rr.rel_residual, &r0res.rel_residual, sizeof(double)) != 0)
+            return fail(h0, AJM_ERR_CUDA, "rank %d's control decisions differ from rank 0's (internal error)", r);
+    }
+    if (res) *res = r0res;
+    return AJM_OK;
+}
+
 ajm_status_t ajm_estimate_spectrum(ajm_handle_t h, const double* v0, uint64_t seed, int64_t max_steps,
                                    double tol, ajm_spectrum_t* out, double* alpha, double* beta,
                                    void* cuda_stream) {
@@ -1644,7 +2306,7 @@ ajm_status_t ajm_estimate_spectrum(ajm_handle_t h, const double* v0, uint64_t se
     if (!h->lzw) AJM_CUDA(h, dalloc(&h->lzw, 8 * np, st));
     AJM_CUDA(h, cudaMemsetAsync(h->lzw, 0, sizeof(double) * 8 * np, st));
     double* Lg0 = h->lzw + 6 * np;
-    // start vector in the g buffer 0 (internal order)
+    // start vector (internal order)
     if (v0) {
         const cudaMemcpyKind k = kind_to_device(v0);
         if (h->relabel) {
@@ -1666,9 +2328,10 @@ ajm_status_t ajm_estimate_spectrum(ajm_handle_t h, const double* v0, uint64_t se
         ajm_start_vector_kernel<<<1024, 256, 0, st>>>(n, h->relabel ? h->perm_fwd : nullptr, seed, Lg0);
         AJM_CUDA(h, cudaGetLastError());
     }
-    // passes: pass 0 normalises the start, pass j >= 1 is Lanczos step j; T_k needs k + 1 passes
-    // (alpha_1..alpha_k and beta_1..beta_k, the last one for the residual bounds)
-    const int64_t passes = max_steps + 1;
+    // steps: step 0 normalises the start, step j >= 1 is Lanczos step j (an SpMV pass for alpha_j
+    // and a vector pass for beta_j); T_k needs k + 1 steps (alpha_1..alpha_k and beta_1..beta_k, the
+    // last one for the residual bounds)
+    const int64_t passes = max_steps + 1;  // Lanczos steps
     {
         const ajm_status_t hs = ensure_hist(h, passes + 2, st);
         if (hs != AJM_OK) return hs;
@@ -1683,19 +2346,19 @@ ajm_status_t ajm_estimate_spectrum(ajm_handle_t h, const double* v0, uint64_t se
     p.Lp0 = h->lzw;
     p.Lp1 = h->lzw + np;
     p.Lp2 = h->lzw + 2 * np;
-    p.Lq0 = h->lzw + 3 * np;
-    p.Lq1 = h->lzw + 4 * np;
-    p.Lq2 = h->lzw + 5 * np;
-    p.Lg0 = Lg0;
-    p.Lg1 = h->lzw + 7 * np;
+    p.Lq = h->lzw + 3 * np;
+    p.Lv = Lg0;
     std::vector<double> va, vb;
     int64_t done_passes = 0, chunk = 32;
+    int64_t kchk = 0;    // beta_1 .. beta_kchk checked for a (numerical) breakdown
+    double tnorm = 0.0;  // max |alpha_i|, beta_i seen so far (the scale of T_k)
     ajm_spectrum_t r = {};
     AJM_CUDA(h, cudaEventRecord(h->ev0, st));
     int64_t launches = 0;
     for (;;) {
-        // a chunk of passes in one persistent launch; the state continues across launches
-        p.max_passes = (int)std::min<int64_t>(chunk, passes - done_passes);
+        // a chunk of steps (two passes each) in one persistent launch; the state continues across
+        // launches
+        p.max_passes = (int)(2 * std::min<int64_t>(chunk, passes - done_passes + 1));
         AJM_CUDA(h, launch_solver(h, p, st, h->fn_lz));
         ++launches;
         AJM_CUDA(h, cudaMemcpyAsync(h->h_ctrl, h->ctrl, sizeof(AjmCtrl), cudaMemcpyDeviceToHost, st));
@@ -1708,15 +2371,27 @@ ajm_status_t ajm_estimate_spectrum(ajm_handle_t h, const double* v0, uint64_t se
         AJM_CUDA(h, cudaMemcpy(va.data(), ha, sizeof(double) * done_passes, cudaMemcpyDeviceToHost));
         AJM_CUDA(h, cudaMemcpy(vb.data(), hb, sizeof(double) * done_passes, cudaMemcpyDeviceToHost));
         if (c.s.done && c.s.status == 2) return fail(h, AJM_ERR_NONFINITE, "non-finite Lanczos coefficient");
-        const bool breakdown = c.s.done && c.s.status == 0;  // beta = 0: invariant subspace
+        bool breakdown = c.s.done && c.s.status == 0;  // beta = 0: invariant subspace
         // T_k: alpha_1..alpha_k = va[0..k), beta_1..beta_{k-1} = vb[1..k), residual coefficient
         // beta_k = vb[k] (0 at a breakdown)
-        const int k = (int)(breakdown ? done_passes : done_passes - 1);
+        int k = (int)(breakdown ? done_passes : done_passes - 1);
+        // a NUMERICAL breakdown -- beta_k at rounding level against ||T_k|| (the Krylov space is
+        // invariant: e.g. the §4.1 matrix has two distinct eigenvalues) -- ends the run at T_k: the
+        // steps after it are rounding noise without reorthogonalisation, not more information
+        for (int64_t kk = kchk + 1; kk < done_passes && !breakdown; ++kk) {
+            tnorm = std::max(tnorm, std::fabs(va[(size_t)kk - 1]));
+            if (kk >= 2) tnorm = std::max(tnorm, vb[(size_t)kk - 1]);
+            if (vb[(size_t)kk] <= 1e-12 * tnorm) {
+                breakdown = true;
+                k = (int)kk;
+            }
+            kchk = kk;
+        }
         if (k >= 1) {
             std::vector<double> ta(va.begin(), va.begin() + k), tb;
             for (int i = 1; i < k; ++i) tb.push_back(vb[(size_t)i]);
             tb.push_back(0.0);
-            const double bk = breakdown ? 0.0 : vb[(size_t)k];
+            const double bk = (breakdown && (int64_t)k >= done_passes) ? 0.0 : vb[(size_t)k];
             const double lmin = tri_eig(ta, tb, k, 0), lmax = tri_eig(ta, tb, k, k - 1);
             r.lambda_min = lmin;
             r.lambda_max = lmax;
@@ -1801,7 +2476,7 @@ ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info) {
     info->seg_rows = h->seg_rows;
     info->split_rows = h->nsplit;
     info->sigma = h->sigma;
-    info->variant = 0;
+    info->variant = h->nseg > 0 ? 1 : 0;  // 1: no producer warp, 128 registers (layouts with segments)
     info->l2_window_bytes = (int64_t)h->win_bytes;
     info->l2_hit_ratio = h->win_hit;
     info->mode = h->cluster ? 5 : 0;
@@ -1810,6 +2485,11 @@ ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info) {
     info->launches_per_solve = (int32_t)(1 + (h->prime_bytes ? 1 : 0) + std::max<int64_t>(h->last_launches, 1));
     info->col_bytes = h->col_bytes;
     info->seg_nnz = h->seg_nnz;
+    info->rank = h->rank;
+    info->nranks = h->nranks;
+    info->halo = h->h_lo + h->h_hi;
+    info->send = (int64_t)h->snd_host.size();
+    info->group_rows = h->grp_rows;
     return AJM_OK;
 }
 

@@ -37,6 +37,8 @@
 #define AJM_WARPS (AJM_BLOCK / 32)
 #define AJM_SELL_MAX 64  // rows up to this length go to SELL (thread per row)
 #define AJM_SEG 2048     // max nonzeros per warp segment of a longer row
+#define AJM_GRP_MAX 256  // rows of AJM_SELL_MAX+1 .. this many nonzeros: sub-warp groups (static plan)
+#define AJM_GRP_ROWS 4   // rows per group (8 lanes each)
 #define AJM_NPART 5      // rr, <x,q>, <b,x>, d, sum|d terms|
 #define AJM_UNIT_EL 2048 // SELL elements per TMA staging unit (24 KB of val + col)
 #define AJM_UNIT_ROWS (AJM_WARPS * 32)  // rows per staging unit (<= 8 chunks)
@@ -63,14 +65,12 @@ struct AjmState {
     int answer;         // buffer index holding the answer when done
     int prerestart;
     int nres, nlogged;
-    // Lanczos mode (ajm_estimate_spectrum, kLz): p/q buffers rotate through cur/prev/fre, the
-    // gathered g buffers through gcur; every stored vector carries a scale applied on reading
-    int gcur;
-    double lz_alpha;    // alpha_j of the current pass's three-term recurrence
-    double lz_beta;     // beta_{j-1}
-    double lz_sg;       // scale of the gathered g buffer (g = M p^_j = D^{-1} Q p^_j)
-    double lz_sp;       // scale of the p/q buffers cur (p^_j, Q p^_j)
-    double lz_spp;      // scale of the p/q buffers prev (p^_{j-1}, Q p^_{j-1})
+    // Lanczos mode (ajm_estimate_spectrum, kLz): the w buffers rotate through cur/prev/fre; each
+    // holds an unnormalised Lanczos vector, p^_j = lz_sp * w_cur, p^_{j-1} = lz_spp * w_prev
+    double lz_alpha;    // alpha_j (after the SpMV pass of step j)
+    double lz_beta;     // beta_{j-1}: the coupling of p^_{j-1} in the next three-term step
+    double lz_sp;       // 1 / beta_{j-1}: scale of w_cur
+    double lz_spp;      // scale of w_prev
 };
 
 struct AjmCtrl {
@@ -84,6 +84,33 @@ struct AjmCtrl {
     unsigned int timeout_flag;     // set if a barrier/arrival wait timed out (never expected)
     unsigned int pad;
     long long restart_log[AJM_LOG_CAP];
+};
+
+// Row-block sharding (NEXT-2; Alg. 3 lines 3-5 "for i = 1..s parallel"; §4.4):
+// rank r owns the contiguous global rows [r0, r1).  Its iterate buffers hold its own rows at
+// [0, n) and the halo -- the entries of x~ its rows reference on other ranks, sorted by global
+// index -- at [-H_lo, 0) (lower ranks) and [n, n + H_hi) (higher ranks), so a contiguous slab of a
+// stencil keeps its column offsets.  What a rank can reach of each member of its group (peer
+// device pointers: NVLink P2P / IPC on a multi-GPU node, plain pointers when the ranks are
+// emulated on one device):
+#define AJM_MAX_RANKS 8
+struct AjmPeer {
+    double* x[3];                 // X0..X2 base (own row 0) of that rank's iterate buffers
+    double* slot;                 // [2][AJM_MAX_RANKS][AJM_NPART] rank partials it receives
+    unsigned long long* bar;      // its monotone cross-rank arrival counter
+};
+
+struct AjmPass;
+struct AjmShard {
+    const AjmPass* emu;           // emulated group (all ranks in ONE launch): per-rank pass structs
+    int rank, nranks;
+    int emu_grid;                 // CTAs per rank in an emulated launch
+    const AjmPeer* peers;         // [nranks]
+    const int* snd_cta;           // [G+1] this CTA's range of send entries
+    const int4* snd;              // {own internal row, peer, offset in the peer's X, 0}
+    double* slot;                 // own [2][AJM_MAX_RANKS][AJM_NPART]
+    unsigned long long* bar;      // own cross-rank counter (peers add 1 per round)
+    unsigned long long bar_base;  // arrivals of earlier solves (never reset: no reset race)
 };
 
 struct AjmPass {
@@ -140,10 +167,13 @@ struct AjmPass {
     const uint8_t* __restrict__ scode;       // (kCol8) SELL column codes: col = row + ctab[code]
     const int* __restrict__ ctab;            // (kCol8) [256] distinct offsets col - row, ascending
     const int4* __restrict__ seg_meta;       // static plan: {row, k0, k1, split} of seg_list[k]
-    // Lanczos mode (kLz): rotating p / Q p buffers and the two gathered g = D^{-1} Q p buffers
+                                             // (split -2: sub-warp group `row`, k1 its nonzeros)
+    const int4* __restrict__ grp;            // sub-warp groups: {rows}, {k0}, {k1} (3 int4 each)
+    // Lanczos mode (kLz): rotating unnormalised Lanczos vectors w, Q p^_j, the start vector
     double* Lp0; double* Lp1; double* Lp2;
-    double* Lq0; double* Lq1; double* Lq2;
-    double* Lg0; double* Lg1;
+    double* Lq;
+    const double* Lv;
+    AjmShard sh;                             // (kShard) row-block sharding
 };
 
 __device__ __forceinline__ unsigned long long ajm_gtime() {
@@ -285,7 +315,7 @@ __device__ __forceinline__ unsigned ajm_ld_acquire(const unsigned* p) {
     return v;
 }
 
-// barrier among the AJM_BLOCK consumer threads only (the TMA producer warp never joins)
+// CTA barrier of the AJM_BLOCK threads (named barrier 1)
 __device__ __forceinline__ void ajm_csync() { asm volatile("bar.sync 1, %0;" ::"n"(AJM_BLOCK) : "memory"); }
 
 // Fixed-order CTA reduction of the 5 accumulators over the consumer warps; valid in thread 0.
@@ -379,73 +409,88 @@ __device__ void ajm_control_step(AjmState& s, const double* tot, AjmCtrl* c, boo
 
 // ---- Lanczos mode (ajm_estimate_spectrum; NEXT-3: omega_opt of weighted Jacobi) ----
 // Lanczos on M = D^{-1} Q, self-adjoint in the D-inner product <u, v>_D = u^T D v (M is similar to
-// the symmetric D^{-1/2} Q D^{-1/2}), with ONE SpMV per step, as in the AJM pass: pass j
-// multiplies the stored g_j = M p^_j (so the SpMV gives Q g_j) and, by linearity,
-//   z   = M p^_j - alpha_j p^_j - beta_{j-1} p^_{j-1}          ( = beta_j p^_{j+1} )
-//   Q z = Q g_j  - alpha_j Q p^_j - beta_{j-1} Q p^_{j-1}
-// per row, with Q p^_j, Q p^_{j-1} stored by the previous passes.  Partials A = <z, Q z>,
-// B = <z, z>_D give beta_j = sqrt(B) and alpha_{j+1} = A / B after the grid barrier; z, Q z and
-// g_{j+1} = Q z / D are stored unnormalised and scaled by 1/beta_j when read (the pass that writes
-// them does not know beta_j yet).  Pass 0 runs the same epilogue on the start vector (z = x0).
+// the symmetric D^{-1/2} Q D^{-1/2}): the textbook three-term recurrence, two passes per
+// step on the solver's own SpMV and grid barrier (the pass index t alternates):
+//   t odd  (SpMV pass of step j = (t+1)/2):  q = Q p^_j (the gathered w_cur scaled by lz_sp),
+//          alpha_j = <p^_j, q> = <p^_j, M p^_j>_D                          (partial in acc.rr)
+//   t even (vector pass; t = 0 starts):      w = q / D - alpha_j p^_j - beta_{j-1} p^_{j-1}
+//          (t = 0: w = v0), beta_j = ||w||_D, p^_{j+1} = w / beta_j     (partial in acc.xq)
+// Q is multiplied by the Lanczos vector itself every step (a recurrence for Q p^ instead, one SpMV
+// per step by linearity, drifts from Q times the vector once orthogonality is lost and produced
+// Ritz values outside the spectrum).  The vector pass streams no matrix: its units are released
+// unread.
 struct AjmLz {
-    const double* pc; const double* pp; const double* qc; const double* qp;
-    double* pn; double* qn; double* gn;
-    double sg, c1, c2;  // scale of the gathered g; alpha_j * scale(p cur); beta_{j-1} * scale(p prev)
+    const double* pc; const double* pp;  // w_cur, w_prev
+    double* pn;                          // w_fre (vector pass output)
+    double* q;                           // Q p^_j
+    const double* v0;                    // start vector (t = 0)
+    double sp, spp, alpha, beta;
 };
 
 __device__ __forceinline__ double* ajm_lsel(double* a, double* b, double* c, int k) {
     return k == 0 ? a : (k == 1 ? b : c);
 }
 
-__device__ __forceinline__ void ajm_row_lanczos(const AjmLz& L, int i, double qg, double Di, double gi,
-                                                double pci, double ppi, double qci, double qpi, AjmAcc& a) {
-    const double z = L.sg * gi - L.c1 * pci - L.c2 * ppi;
-    const double Qz = L.sg * qg - L.c1 * qci - L.c2 * qpi;
-    L.pn[i] = z;
-    L.qn[i] = Qz;
-    L.gn[i] = Qz / Di;
-    a.rr += z * Qz;      // A = <z, Q z>
-    a.xq += Di * z * z;  // B = <z, z>_D
+// SpMV pass, row i: qv = (Q w_cur)_i, wi = (w_cur)_i
+__device__ __forceinline__ void ajm_row_lanczos(const AjmLz& L, int i, double qv, double wi, AjmAcc& a) {
+    const double q = L.sp * qv;
+    L.q[i] = q;
+    a.rr += (L.sp * wi) * q;  // alpha_j = <p^_j, Q p^_j>
 }
 
-__device__ __forceinline__ void ajm_row_lanczos_ld(const AjmPass& p, const AjmLz& L, const double* g, int i,
-                                                   double qg, AjmAcc& a) {
-    ajm_row_lanczos(L, i, qg, p.D[i], ajm_ld(g + i), ajm_ld(L.pc + i), ajm_ld(L.pp + i), ajm_ld(L.qc + i),
-                    ajm_ld(L.qp + i), a);
+__device__ __forceinline__ void ajm_row_lanczos_ld(const AjmPass& p, const AjmLz& L, const double* w, int i,
+                                                   double qv, AjmAcc& a) {
+    ajm_row_lanczos(L, i, qv, ajm_ld(w + i), a);
+}
+
+// vector pass, row i (t0: the start vector)
+__device__ __forceinline__ void ajm_row_lanczos_axpy(const AjmPass& p, const AjmLz& L, int i, bool t0, AjmAcc& a) {
+    const double Di = p.D[i];
+    const double w = t0 ? L.v0[i]
+                        : ajm_ld(L.q + i) / Di - L.alpha * (L.sp * ajm_ld(L.pc + i)) - L.beta * (L.spp * ajm_ld(L.pp + i));
+    L.pn[i] = w;
+    a.xq += Di * w * w;  // beta_j^2 = ||w||_D^2
 }
 
 // Lanczos control step (thread 0 of every CTA, identical inputs -> identical outputs; CTA 0 writes
-// the coefficient histories: res_hist[t] = alpha_{t+1}, f_hist[t] = beta_t (t = 0: ||x0||_D)).
+// the coefficient histories: res_hist[j-1] = alpha_j, f_hist[j] = beta_j (j = 0: ||v0||_D)).
+// s.iterations = j after the vector pass of step j: alpha_1..alpha_j and beta_0..beta_j are known.
 __device__ void ajm_lanczos_control(AjmState& s, const double* tot, AjmCtrl* c, bool writer) {
     const long long t = s.t;
-    const double A = tot[0], B = tot[1];
-    const double beta = sqrt(B);
-    const double alpha = A / B;
-    if (writer) {
-        c->res_hist[t] = alpha;
-        c->f_hist[t] = beta;
+    if (t & 1) {  // SpMV pass of step j = (t + 1) / 2
+        const double alpha = tot[0];
+        if (writer) c->res_hist[(t - 1) / 2] = alpha;
+        s.lz_alpha = alpha;
+        if (!isfinite(alpha)) {
+            s.done = 1;
+            s.status = 2;
+            return;
+        }
+    } else {      // vector pass: beta_j, j = t / 2
+        const double B = tot[1];
+        const double beta = sqrt(B);
+        const long long j = t / 2;
+        if (writer) c->f_hist[j] = beta;
+        s.iterations = j;
+        if (!(B > 0.0) || !isfinite(B)) {  // exact breakdown (invariant subspace) / failure
+            s.done = 1;
+            s.status = (B == 0.0) ? 0 : 2;
+            return;
+        }
+        const int cur = s.cur, prev = s.prev, fre = s.fre;
+        s.prev = cur;
+        s.cur = fre;
+        s.fre = prev;
+        s.lz_spp = s.lz_sp;
+        s.lz_sp = 1.0 / beta;
+        s.lz_beta = beta;
+        if (j >= s.maxit) {
+            s.done = 1;
+            s.status = 1;
+            return;
+        }
     }
-    s.iterations = t + 1;  // passes run
-    if (!(B > 0.0) || !isfinite(B) || !isfinite(A)) {  // exact breakdown (invariant subspace) / failure
-        s.done = 1;
-        s.status = (B == 0.0) ? 0 : 2;
-        return;
-    }
-    const int cur = s.cur, prev = s.prev, fre = s.fre;
-    s.prev = cur;
-    s.cur = fre;
-    s.fre = prev;
-    s.gcur ^= 1;
-    s.lz_spp = s.lz_sp;
-    s.lz_sp = 1.0 / beta;
-    s.lz_sg = 1.0 / beta;
-    s.lz_alpha = alpha;
-    s.lz_beta = beta;
     s.t = t + 1;
-    if (s.t >= s.maxit) {
-        s.done = 1;
-        s.status = 1;
-    }
 }
 
 // Grid barrier over all CTAs of the cooperative launch: a monotone 64-bit arrival counter (reset
@@ -478,6 +523,56 @@ __device__ __forceinline__ bool ajm_grid_wait(AjmCtrl* c, unsigned nblocks, long
         }
     }
     __threadfence();
+    return to;
+}
+
+// ---- row-block sharding (kShard): halo push and the cross-rank barrier ----
+__device__ __forceinline__ unsigned long long ajm_ld_acquire_sys64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// Halo push (consumer threads of one CTA): every x~ entry this CTA computed that another rank's
+// rows reference is stored straight into that rank's buffer `buf` (a peer store over NVLink on a
+// multi-GPU node), then fenced at system scope, so the CTA's arrival on the local grid barrier
+// orders it before the rank's cross-rank signal.
+__device__ __forceinline__ void ajm_shard_push(const AjmShard& sh, int bid, const double* src, int buf) {
+    const int k1 = __ldg(sh.snd_cta + bid + 1);
+    for (int k = __ldg(sh.snd_cta + bid) + (int)threadIdx.x; k < k1; k += AJM_BLOCK) {
+        const int4 e = __ldg(sh.snd + k);
+        double* dst = sh.peers[e.y].x[buf];
+        dst[e.z] = ajm_ld(src + e.x);
+    }
+    __threadfence_system();
+}
+// Cross-rank exchange of round `rnd` (after the local grid barrier; called by all consumer threads,
+// rank partial in rk[0..4] valid in CTA 0's warp 0): CTA 0's lane s writes the rank partial into
+// rank s's slot array and release-adds rank s's counter (system scope); every CTA then waits until
+// all ranks have arrived for this round.  Returns true on a (never expected) timeout.
+__device__ __forceinline__ bool ajm_shard_cross(const AjmShard& sh, int bid, long long rnd, const double* rk,
+                                                unsigned* timeout_flag) {
+    const int lane = threadIdx.x & 31;
+    if (bid == 0 && threadIdx.x < 32 && lane < sh.nranks) {
+        const AjmPeer& pe = sh.peers[lane];
+        double* d = pe.slot + ((size_t)(rnd & 1) * AJM_MAX_RANKS + sh.rank) * AJM_NPART;
+#pragma unroll
+        for (int j = 0; j < AJM_NPART; ++j) d[j] = rk[j];
+        __threadfence_system();
+        asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(pe.bar) : "memory");
+    }
+    bool to = false;
+    if (threadIdx.x == 0) {
+        const unsigned long long target = sh.bar_base + (unsigned long long)sh.nranks * (unsigned long long)(rnd + 1);
+        long long spins = 0;
+        while (ajm_ld_acquire_sys64(sh.bar) < target) {
+            if (++spins > (1LL << 30)) {
+                atomicExch(timeout_flag, 1u);
+                to = true;
+                break;
+            }
+        }
+        __threadfence_system();
+    }
     return to;
 }
 
@@ -520,6 +615,56 @@ __device__ __forceinline__ double ajm_seg_dot(const AjmPass& p, int k0, int k1, 
         }
     }
     return ajm_warp_sum(s);
+}
+
+// Sub-warp group (rows of 65 .. AJM_GRP_MAX nonzeros, four to a warp): lanes 8q .. 8q+7 run row q
+// -- lane-strided by 8, 8 loads per lane per step, then a fixed 3-level xor tree inside the 8 lanes --
+// and lane 8q finishes it with the row epilogue, whose five operands it loaded before the dot.  The
+// four rows' latency chains overlap instead of running one after another.
+template <bool kLz>
+__device__ __forceinline__ void ajm_group_rows(const AjmPass& p, const AjmLz& L, int gid, const double* xc,
+                                               const double* xp, double* xf, double beta, int restart_t,
+                                               AjmAcc& a, int lane) {
+    const int sub = lane >> 3, li = lane & 7;
+    const int4* gm = p.grp + 3 * gid;
+    const int4 R = __ldg(gm), K0 = __ldg(gm + 1), K1 = __ldg(gm + 2);
+    const int row = sub == 0 ? R.x : sub == 1 ? R.y : sub == 2 ? R.z : R.w;
+    const int k0 = sub == 0 ? K0.x : sub == 1 ? K0.y : sub == 2 ? K0.z : K0.w;
+    const int k1 = sub == 0 ? K1.x : sub == 1 ? K1.y : sub == 2 ? K1.z : K1.w;
+    const bool lead = li == 0 && row >= 0;
+    const uint64_t pol = ajm_policy(p.l2_mode == 3 ? 1 : (p.l2_mode >= 2 ? 2 : 0));
+    double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
+    if (!kLz && lead) {  // epilogue operands in flight during the dot
+        bi = ajm_ldp(p.b + row, pol);
+        Di = ajm_ldp(p.D + row, pol);
+        xt = ajm_ld(xc + row);
+        xpi = ajm_ld(xp + row);
+        qxp = ajm_ldp(p.Qxp + row, pol);
+    }
+    double s = 0.0;
+    for (int kb = k0 + li; kb < k1; kb += 64) {
+        double v[8], xg[8];
+        int cc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int kk = kb + 8 * j;
+            v[j] = kk < k1 ? __ldcs(p.val + kk) : 0.0;
+            cc[j] = kk < k1 ? __ldcs(p.col + kk) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) xg[j] = (kb + 8 * j < k1) ? ajm_ld(xc + cc[j]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (kb + 8 * j < k1) s += v[j] * xg[j];
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    if (lead) {
+        if constexpr (kLz) ajm_row_lanczos_ld(p, L, xc, row, s, a);
+        else ajm_row_update(p.Qxp, xf, row, s, bi, Di, xt, xpi, qxp, beta, restart_t, a, pol,
+                            ajm_policy(p.l2_mode >= 2 ? 2 : 0));
+    }
 }
 
 // ---- mbarrier / bulk-copy (TMA engine) helpers --------------------------------------------------
@@ -662,11 +807,11 @@ __device__ __forceinline__ double ajm_ld_cluster(const double* local, unsigned r
     return v;
 }
 
-// The persistent solver kernel (cooperative launch; grid = resident CTAs): AJM_WARPS consumer
-// warps + one producer warp per CTA.  The producer's lane 0 streams this CTA's SELL staging units
-// (val + col, or val + byte code) into a kStages-deep shared-memory ring with cp.async.bulk (TMA
-// engine, mbarrier complete_tx).  Q never changes, so the producer runs ahead across pass
-// boundaries while the consumers sit in the grid barrier.
+// The persistent solver kernel (cooperative launch; grid = resident CTAs): AJM_WARPS warps per CTA.
+// The CTA's SELL staging units (val + col, or val + byte code) stream through a kStages-deep
+// shared-memory ring with cp.async.bulk (TMA engine, mbarrier complete_tx); the last warp to release
+// a stage refills it (no producer warp).  Q never changes, so the ring runs ahead across pass
+// boundaries while the warps sit in the grid barrier.
 // kSeg = false: layouts without warp segments (all rows in SELL, e.g. stencils) -- phases (1) and
 //   (3) are compiled out of the hot loop.
 // kCluster = true: the whole grid is ONE thread-block cluster (<= 16 CTAs, small problems): the
@@ -682,28 +827,61 @@ __device__ __forceinline__ double ajm_ld_cluster(const double* local, unsigned r
 // kCol8 = true: byte-coded SELL columns (col = row + ctab[code]).
 // kLz = true: the Lanczos pass of ajm_estimate_spectrum (same SpMV, epilogue ajm_row_lanczos,
 //   control ajm_lanczos_control) instead of the AJM pass.
+// kShard = true: one rank of a row-block sharded solve (NEXT-2; AjmShard above): before the loop a
+//   round 0 pushes x~^0's halo entries, and every pass pushes x~^{t+1}'s, then the rank's partial is
+//   exchanged with every rank (rank order, bitwise the same totals everywhere) before the control
+//   step.  With sh.emu set, ONE cooperative launch runs every rank (CTA block r*emu_grid.. is rank
+//   r) on one device -- the same code, peers being ordinary device pointers.
+// kProd: how the TMA ring is refilled.
+//   true  -- a 9th (producer) warp waits on each stage's "empty" mbarrier and refills it; two CTAs of
+//            9 warps fit the SM's register files at 96 registers per thread.  The layouts without
+//            warp segments (stencils, ER) use it: their 8 consumer warps never wait on a refill.
+//   false -- no producer warp: the last of the 8 warps to release a stage refills it, and two CTAs of
+//            8 warps fit 128 registers per thread -- what the segment phases (the long-row dot, the
+//            sub-warp groups, the epilogue operand prefetch) need to run without spills.
 template <int kStages, bool kSeg = true, bool kCluster = false, int kJB = 0, bool kGMeta = false,
-          bool kCol8 = false, bool kLz = false>
-__global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
+          bool kCol8 = false, bool kLz = false, bool kShard = false, bool kProd = !kSeg>
+__global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
+    static_assert(!kShard || (!kCluster && !kJB && !kGMeta && !kLz), "sharded solve: plain ring variants only");
+    // (kShard) this CTA's rank's pass struct, in shared memory (the emulated launch serves all ranks)
+    __shared__ __align__(16) unsigned char s_pp[kShard ? sizeof(AjmPass) : 16];
+    int bid = (int)blockIdx.x;
+    unsigned G = gridDim.x;
+    if constexpr (kShard) {
+        int rk = p0.sh.rank;
+        const AjmPass* srcp = &p0;
+        if (p0.sh.emu) {
+            rk = (int)blockIdx.x / p0.sh.emu_grid;
+            bid = (int)blockIdx.x - rk * p0.sh.emu_grid;
+            G = (unsigned)p0.sh.emu_grid;
+            srcp = p0.sh.emu + rk;
+        }
+        const unsigned long long* s8 = reinterpret_cast<const unsigned long long*>(srcp);
+        unsigned long long* d8 = reinterpret_cast<unsigned long long*>(s_pp);
+        static_assert(sizeof(AjmPass) % 8 == 0, "AjmPass copy");
+        for (int i = threadIdx.x; i < (int)(sizeof(AjmPass) / 8); i += blockDim.x) d8[i] = s8[i];
+        __syncthreads();
+    }
+    const AjmPass& p = kShard ? *reinterpret_cast<const AjmPass*>(s_pp) : p0;
     extern __shared__ __align__(128) unsigned char s_dyn[];
     __shared__ double s_red[AJM_WARPS][AJM_NPART];
     __shared__ double s_tot[AJM_NPART];
     __shared__ double s_res;
     __shared__ AjmState s_st;
     __shared__ __align__(8) uint64_t s_full[kStages];
-    __shared__ __align__(8) uint64_t s_empty[kStages];
-    __shared__ volatile int s_stop;
-    __shared__ volatile int s_pass;            // passes of this launch the consumers have started
+    __shared__ __align__(8) uint64_t s_empty[kStages];  // the 8 consumer warps released the stage's unit
+    __shared__ unsigned s_rel[kStages];        // (!kProd) warps done with the stage's unit (monotone)
+    __shared__ volatile int s_stop;            // (kProd) the consumers left the pass loop
+    __shared__ volatile int s_pass;            // (kProd) passes of this launch the consumers have started
     __shared__ __align__(8) uint64_t s_cbar;   // (kCluster) per-pass barrier: G arrivals per phase
     __shared__ __align__(8) uint64_t s_cexit;  // (kCluster) every CTA done with the others' smem
-    __shared__ double s_part[2][AJM_NPART];    // (kCluster) this CTA's partials by pass parity
+    __shared__ double s_part[2][AJM_NPART];    // (kCluster) this CTA's partials by the parity of the
+                                               // launch's pass count (the barrier is fresh per launch)
     __shared__ int s_to;
     __shared__ int s_ctab[kCol8 ? AJM_CTAB : 1];  // (kCol8) column offsets of the byte codes
 
     AjmCtrl* c = p.ctrl;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int bid = (int)blockIdx.x;
-    const unsigned G = gridDim.x;
     const int u0 = p.cta_unit[bid], u1 = p.cta_unit[bid + 1];
     const int nunits = u1 - u0;
     constexpr bool jblk = (kJB != 0);
@@ -730,12 +908,13 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
         for (int i = tid; i < AJM_CTAB; i += blockDim.x) s_ctab[i] = p.ctab[i];
     if (tid == 0) {
         s_st = c->s;
-        s_stop = 0;
-        s_pass = 0;
         for (int k = 0; k < kStages; ++k) {
             ajm_mbar_init(&s_full[k], 1);
             ajm_mbar_init(&s_empty[k], AJM_WARPS);
+            s_rel[k] = 0u;
         }
+        s_stop = 0;
+        s_pass = 0;
         if (kCluster) {
             ajm_mbar_init(&s_cbar, gridDim.x);
             ajm_mbar_init(&s_cexit, gridDim.x);
@@ -747,46 +926,87 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
 
-    if (warp == AJM_WARPS) {
-        // ---------------- producer warp (one lane) ----------------
-        if (lane == 0 && nunits > 0) {
-            const uint64_t qpol = ajm_policy(p.l2_mode >= 1 ? 1 : 0);
-            const long long total = (long long)nunits * p.max_passes;
-            long long cnt = 0;  // units issued
-            long long idle = 0;
-            while (cnt < total) {
-                const int stage = (int)(cnt % kStages);
-                const unsigned par = (unsigned)((cnt / kStages) & 1) ^ 1u;
-                if (ajm_mbar_try_wait(&s_empty[stage], par)) {
-                    const int uu = (int)(cnt % nunits);
-                    const int e0 = s_coff[s_uc0[uu]], e1 = s_coff[s_uc0[uu + 1]];
-                    const unsigned ne = (unsigned)(e1 - e0);
-                    ajm_mbar_expect_tx(&s_full[stage], ne * el_bytes);
-                    ajm_bulk_g2s(st_val(stage), p.sval + efirst + e0, ne * 8u, &s_full[stage], qpol);
-                    if (kCol8)
-                        ajm_bulk_g2s(st_code(stage), p.scode + efirst + e0, ne, &s_full[stage], qpol);
-                    else
-                        ajm_bulk_g2s(st_col(stage), p.scol + efirst + e0, ne * 4u, &s_full[stage], qpol);
-                    ++cnt;
-                    idle = 0;
-                } else if (s_stop) {
-                    break;
-                } else if (++idle > (1LL << 28)) {
-                    atomicExch(&c->timeout_flag, 1u);
-                    break;
-                }
-            }
-            // wait for every issued copy to land before the CTA exits (units of passes that never
-            // ran were issued ahead and are simply not consumed)
-            long long spins = 0;
-            while (!s_stop) {
-                if (++spins > (1LL << 32)) break;
-            }
-            for (long long k = (long long)s_pass * nunits; k < cnt; ++k)
-                if (k >= 0) ajm_mbar_wait(&s_full[k % kStages], (unsigned)((k / kStages) & 1), &c->timeout_flag);
+    // ---------------- the TMA ring ----------------
+    // Unit g (counted over all passes of the launch) goes to stage g % kStages (cp.async.bulk +
+    // mbarrier complete_tx, L2 evict_first).  Q never changes, so the ring runs ahead across pass
+    // boundaries while the consumers sit in the grid barrier.  kProd: the producer warp refills a
+    // stage once its "empty" barrier completes.  !kProd: thread 0 issues the first kStages units and
+    // the LAST of the 8 warps to release unit g's stage issues unit g + kStages into it.
+    const long long total_units = (long long)nunits * p.max_passes;
+    // (stage, unit index within the pass): no 64-bit division on the refill path, which runs on the
+    // critical path of the warp that releases a unit last
+    auto issue_unit = [&](int stage, int uu) {
+        const int e0 = s_coff[s_uc0[uu]], e1 = s_coff[s_uc0[uu + 1]];
+        const unsigned ne = (unsigned)(e1 - e0);
+        const uint64_t qpol = ajm_policy(p.l2_mode >= 1 ? 1 : 0);
+        ajm_mbar_expect_tx(&s_full[stage], ne * el_bytes);
+        ajm_bulk_g2s(st_val(stage), p.sval + efirst + e0, ne * 8u, &s_full[stage], qpol);
+        if (kCol8)
+            ajm_bulk_g2s(st_code(stage), p.scode + efirst + e0, ne, &s_full[stage], qpol);
+        else
+            ajm_bulk_g2s(st_col(stage), p.scol + efirst + e0, ne * 4u, &s_full[stage], qpol);
+    };
+    // lane 0 of a warp, after __syncwarp: this warp is done reading unit g's stage.  It arrives on the
+    // stage's "empty" mbarrier (the ordering of its shared-memory reads before the TMA's writes, as a
+    // producer waiting on it would get) and counts itself on a RELAXED shared atomic that elects the
+    // last of the 8 warps, which waits for the (by then complete) phase and refills the stage.
+    // Acquire/release atomics or a proxy fence would compile to MEMBAR.ALL.CTA, which waits for the
+    // warp's x~ gathers still in flight (measured: config 2 42.6 -> 62.3 us/pass with the two-chunk
+    // pipeline).
+    auto release_unit = [&](long long g, int uu) {
+        const int stage = (int)(g % kStages);
+        ajm_mbar_arrive(&s_empty[stage]);
+        unsigned old;
+        asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;"
+                     : "=r"(old) : "r"(ajm_smem(&s_rel[stage])) : "memory");
+        if ((old & (AJM_WARPS - 1)) == AJM_WARPS - 1 && g + kStages < total_units) {
+            ajm_mbar_wait(&s_empty[stage], (unsigned)((g / kStages) & 1), &c->timeout_flag);
+            int un = uu + kStages;
+            while (un >= nunits) un -= nunits;
+            issue_unit(stage, un);
         }
-        return;
+    };
+    if constexpr (kProd) {
+        if (warp == AJM_WARPS) {
+            // ---------------- producer warp (one lane) ----------------
+            if (lane == 0 && nunits > 0) {
+                long long cnt = 0;  // units issued
+                int uu = 0;         // cnt % nunits
+                long long idle = 0;
+                while (cnt < total_units) {
+                    const int stage = (int)(cnt % kStages);
+                    const unsigned par = (unsigned)((cnt / kStages) & 1) ^ 1u;
+                    if (ajm_mbar_try_wait(&s_empty[stage], par)) {
+                        issue_unit(stage, uu);
+                        ++cnt;
+                        if (++uu == nunits) uu = 0;
+                        idle = 0;
+                    } else if (s_stop) {
+                        break;
+                    } else if (++idle > (1LL << 28)) {
+                        atomicExch(&c->timeout_flag, 1u);
+                        break;
+                    }
+                }
+                // wait for every issued copy to land before the CTA exits (units of passes that never
+                // ran were issued ahead and are simply not consumed)
+                long long spins = 0;
+                while (!s_stop) {
+                    if (++spins > (1LL << 32)) break;
+                }
+                for (long long k = (long long)s_pass * nunits; k < cnt; ++k)
+                    if (k >= 0) ajm_mbar_wait(&s_full[k % kStages], (unsigned)((k / kStages) & 1), &c->timeout_flag);
+            }
+            return;
+        }
+    } else if (tid == 0) {
+        for (long long g = 0; g < total_units && g < kStages; ++g) issue_unit((int)g, (int)(g % nunits));
     }
+    // a consumer warp is done reading unit g (index uu in its pass): release its stage
+    auto release = [&](long long g, int uu) {
+        if constexpr (kProd) ajm_mbar_arrive(&s_empty[(int)(g % kStages)]);
+        else release_unit(g, uu);
+    };
 
     // ---------------- consumer warps ----------------
     const uint64_t vpol = ajm_policy(p.l2_mode == 3 ? 1 : (p.l2_mode >= 2 ? 2 : 0));  // b, D, Qx
@@ -794,6 +1014,22 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
     const int sg0 = p.cta_seg[bid], sg1 = p.cta_seg[bid + 1];
     const int sp0 = p.cta_split[bid], sp1 = p.cta_split[bid + 1];
     long long ucnt = 0;  // units consumed by this CTA (all passes)
+    if constexpr (kShard) {
+        // round 0: the halo of x~^0 (own rows written by the host before the launch)
+        ajm_shard_push(p.sh, bid, ajm_sel(p, s_st.cur), s_st.cur);
+        ajm_csync();
+        if (tid == 0) {
+            ajm_grid_arrive(c);
+            s_to = ajm_grid_wait(c, G, 0) ? 1 : 0;
+        }
+        ajm_csync();
+        if (tid < AJM_NPART) s_tot[tid] = 0.0;
+        ajm_csync();
+        if (ajm_shard_cross(p.sh, bid, 0, s_tot, &c->timeout_flag)) s_to = 1;
+        ajm_csync();
+        if (tid == 0 && s_to) s_st.done = 1;
+        ajm_csync();
+    }
     int pass = 0;
     for (; pass < p.max_passes; ++pass) {
         if (s_st.done) break;
@@ -801,26 +1037,28 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
         const int restart_t = s_st.restart_t;
         const double beta = s_st.beta;
         AjmLz L;
+        // (kLz) even passes are the Lanczos vector passes: no SpMV (units released unread)
+        const bool lz_vec = kLz && !(t & 1);
         if constexpr (kLz) {
             L.pc = ajm_lsel(p.Lp0, p.Lp1, p.Lp2, s_st.cur);
             L.pp = ajm_lsel(p.Lp0, p.Lp1, p.Lp2, s_st.prev);
             L.pn = ajm_lsel(p.Lp0, p.Lp1, p.Lp2, s_st.fre);
-            L.qc = ajm_lsel(p.Lq0, p.Lq1, p.Lq2, s_st.cur);
-            L.qp = ajm_lsel(p.Lq0, p.Lq1, p.Lq2, s_st.prev);
-            L.qn = ajm_lsel(p.Lq0, p.Lq1, p.Lq2, s_st.fre);
-            L.gn = s_st.gcur ? p.Lg0 : p.Lg1;
-            L.sg = s_st.lz_sg;
-            L.c1 = s_st.lz_alpha * s_st.lz_sp;
-            L.c2 = s_st.lz_beta * s_st.lz_spp;
+            L.q = p.Lq;
+            L.v0 = p.Lv;
+            L.sp = s_st.lz_sp;
+            L.spp = s_st.lz_spp;
+            L.alpha = s_st.lz_alpha;
+            L.beta = s_st.lz_beta;
         }
-        const double* xc = kLz ? (s_st.gcur ? p.Lg1 : p.Lg0) : ajm_sel(p, s_st.cur);
+        const double* xc = kLz ? L.pc : ajm_sel(p, s_st.cur);
         const double* xp = ajm_sel(p, s_st.prev);
         double* xf = ajm_sel(p, s_st.fre);
         AjmAcc acc = {0.0, 0.0, 0.0, 0.0, 0.0};
         const bool tsw = p.ts && bid == 0 && tid == 0 && pass < 64;
         if (tsw) p.ts[pass * 8 + 0] = ajm_gtime();
 
-        if (kSeg) {
+        if (kSeg && p.dynseg && bid == 0 && tid == 0) c->seg_q[(t + 1) & 1] = 0u;  // (see below)
+        if (kSeg && !lz_vec) {
         // (1) row segments (direct loads).  Dynamic mode: every warp of every CTA claims segments
         //     (longest first) from this pass's queue until it is empty; results go to seg_part and
         //     the rows are finished by their fixed owner CTA in (3), so the arithmetic does not
@@ -828,7 +1066,7 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
         //     t-1 (finished before the last grid barrier) and is reset here for pass t+1.
         //     Static mode: warp w runs the CTA's segments w, w+8, ... (split rows first, then
         //     longest first).
-        if (p.dynseg && bid == 0 && tid == 0) c->seg_q[(t + 1) & 1] = 0u;
+
         if (!p.dynseg) {
             // static plan: the next segment's metadata is loaded while this one runs (one 16-byte
             // record in list order, no index chase)
@@ -841,11 +1079,26 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
                 const int csg = msg;
                 sk += AJM_WARPS;
                 if (sk < sg1) { m = __ldg(p.seg_meta + sk); msg = __ldg(p.seg_list + sk); }
+                if (cm.w == -2) {  // a sub-warp group of four rows
+                    ajm_group_rows<kLz>(p, L, cm.x, xc, xp, xf, beta, restart_t, acc, lane);
+                    continue;
+                }
+                // a whole row: lane 0 loads its epilogue operands before the dot
+                const uint64_t pol = ajm_policy(p.l2_mode == 3 ? 1 : (p.l2_mode >= 2 ? 2 : 0));
+                double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
+                if (!kLz && cm.w == -1 && lane == 0) {
+                    bi = ajm_ldp(p.b + cm.x, pol);
+                    Di = ajm_ldp(p.D + cm.x, pol);
+                    xt = ajm_ld(xc + cm.x);
+                    xpi = ajm_ld(xp + cm.x);
+                    qxp = ajm_ldp(p.Qxp + cm.x, pol);
+                }
                 const double s = ajm_seg_dot(p, cm.y, cm.z, xc, lane);
                 if (lane == 0) {
                     if (cm.w < 0) {
                         if constexpr (kLz) ajm_row_lanczos_ld(p, L, xc, cm.x, s, acc);
-                        else ajm_row_epilogue(p, cm.x, s, beta, restart_t, xc, xp, xf, acc);
+                        else ajm_row_update(p.Qxp, xf, cm.x, s, bi, Di, xt, xpi, qxp, beta, restart_t, acc, pol,
+                                            ajm_policy(p.l2_mode >= 2 ? 2 : 0));
                     } else {
                         __stcg(p.seg_part + csg, s);
                         __threadfence();
@@ -890,22 +1143,17 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
             for (int uu = 0; uu < nunits; ++uu) {
                 const int stage = (int)((ucnt + uu) % kStages);
                 const unsigned par = (unsigned)(((ucnt + uu) / kStages) & 1);
-                if (jc < s_uc0[uu + 1]) {
+                if (!lz_vec && jc < s_uc0[uu + 1]) {
                     const int j = jc;
                     jc += AJM_WARPS;
                     const int e0 = s_coff[j];
                     const int w = (s_coff[j + 1] - e0) >> 5;
                     const int slot = (cfirst + j) * 32 + lane;
                     const int row = slot < p.n_sell ? slot : -1;  // SELL slot == internal row
-                    double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0, lqp = 0.0;
+                    double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
                     if (row >= 0) {  // operands in flight during the stage wait
-                        if constexpr (kLz) {  // (bi, xpi, qxp, lqp) = (p^_j, p^_{j-1}, Q p^_j, Q p^_{j-1})
-                            Di = p.D[row];
+                        if constexpr (kLz) {  // the row's own entry of the multiplied w
                             xt = ajm_ld(xc + row);
-                            bi = ajm_ld(L.pc + row);
-                            xpi = ajm_ld(L.pp + row);
-                            qxp = ajm_ld(L.qc + row);
-                            lqp = ajm_ld(L.qp + row);
                         } else {
                             bi = ajm_ldp(p.b + row, vpol);
                             if (!jblk) Di = ajm_ldp(p.D + row, vpol);
@@ -928,7 +1176,7 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
                                                             xc + (row >= 0 ? row : 0), s_ctab)
                                            : ajm_chunk_dot<kCluster>(st_val(stage) + off, st_col(stage) + off, w, xc);
                     if constexpr (kLz) {
-                        if (row >= 0) ajm_row_lanczos(L, row, q, Di, xt, bi, xpi, qxp, lqp, acc);
+                        if (row >= 0) ajm_row_lanczos(L, row, q, xt, acc);
                     } else if (jblk)  // every lane takes part (shuffles); tail lanes store nothing
                         ajm_row_update_blk<(kJB > 0 ? kJB : 0)>(p.Qxp, xf, row, q, bi, jr, jbs, jv, xt, xpi, qxp,
                                                                 beta, restart_t, acc, vpol, xpol);
@@ -938,20 +1186,22 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
                     ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);  // keep the phases in step
                 }
                 __syncwarp();
-                if (lane == 0) ajm_mbar_arrive(&s_empty[stage]);
+                if (lane == 0) release(ucnt + uu, uu);
             }
             ucnt += nunits;
         }
         if (tsw) p.ts[pass * 8 + 7] = ajm_gtime();
         if (p.ts && tid == 0 && pass == 5) p.ts[512 + 4 * bid + 3] = ajm_gtime();  // warp 0's chunks done
-        if (kSeg) {
+        if (kSeg && !lz_vec) {
         // (3) segment rows owned by this CTA (one per thread, 256 in flight per CTA): wait for all
         //     segments of this pass, sum their partials in segment order, run the row epilogue.
         //     The arrival counters are monotone over the solve; the comparison is wrap-safe.
         for (int k = sp0 + tid; k < sp1; k += AJM_BLOCK) {
             const int sidx = __ldg(p.owner_split + k);
             const int g0 = __ldg(p.split_seg0 + sidx), g1 = __ldg(p.split_seg0 + sidx + 1);
-            const unsigned target = (unsigned)(g1 - g0) * (unsigned)(t + 1);
+            // passes that ran the segments so far (the Lanczos vector passes do not)
+            const unsigned nsp = kLz ? (unsigned)((t + 1) / 2) : (unsigned)(t + 1);
+            const unsigned target = (unsigned)(g1 - g0) * nsp;
             long long spins = 0;
             while ((int)(ajm_ld_acquire(p.split_cnt + sidx) - target) < 0) {
                 __nanosleep(32);
@@ -963,7 +1213,21 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
             else ajm_row_epilogue(p, __ldg(p.split_row + sidx), q, beta, restart_t, xc, xp, xf, acc);
         }
         }
+        if constexpr (kLz) {
+            // the Lanczos vector pass: a contiguous slice of the rows per CTA (after the grid
+            // barrier every q / w entry is final)
+            if (lz_vec) {
+                const long long r0 = (long long)p.n * bid / G, r1 = (long long)p.n * (bid + 1) / G;
+                for (long long i = r0 + tid; i < r1; i += AJM_BLOCK) ajm_row_lanczos_axpy(p, L, (int)i, t == 0, acc);
+            }
+        }
         // (4) CTA partial -> grid barrier -> every CTA reduces all partials in the same order
+        // (kShard: rounds are passes + 1, round 0 being the x~^0 halo exchange)
+        const long long rnd = t + (kShard ? 1 : 0);
+        if constexpr (kShard) {  // every x~^{t+1} row of this CTA is written: push the halo entries
+            ajm_csync();
+            ajm_shard_push(p.sh, bid, xf, s_st.fre);
+        }
         if (tsw) p.ts[pass * 8 + 1] = ajm_gtime();
         if (p.ts && tid == 0 && pass == 5) {  // debug: every CTA's work-end time and SM of pass 5
             unsigned smid;
@@ -974,11 +1238,11 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
         ajm_block_reduce(acc, s_red);
         if (tsw) p.ts[pass * 8 + 2] = ajm_gtime();
         // partials as 5 arrays of G (SoA) so the all-CTA read below is coalesced
-        double* part = p.partials + (size_t)(t & 1) * G * AJM_NPART;
+        double* part = p.partials + (size_t)(rnd & 1) * G * AJM_NPART;
         double an_c = 0.0, beta_c = 0.0;
         if (kCluster && warp == 0) {
             if (lane == 0) {
-                double* sp = s_part[t & 1];
+                double* sp = s_part[pass & 1];
                 sp[0] = acc.rr;
                 sp[1] = acc.xq;
                 sp[2] = acc.bx;
@@ -994,7 +1258,7 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
             const double a = s_st.alpha;
             an_c = (1.0 + sqrt(1.0 + 4.0 * a * a)) / 2.0;
             beta_c = s_st.momentum ? (a - 1.0) / an_c : 0.0;
-            s_to = ajm_cluster_wait(&s_cbar, (unsigned)(t & 1), &c->timeout_flag) ? 1 : 0;
+            s_to = ajm_cluster_wait(&s_cbar, (unsigned)(pass & 1), &c->timeout_flag) ? 1 : 0;
             __threadfence();  // invalidate this SM's L1 before re-reading x~ written by other SMs
         } else if (!kCluster && tid == 0) {
             part[0 * G + bid] = acc.rr;
@@ -1008,10 +1272,9 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
             const double a = s_st.alpha;
             an_c = (1.0 + sqrt(1.0 + 4.0 * a * a)) / 2.0;
             beta_c = s_st.momentum ? (a - 1.0) / an_c : 0.0;
-            s_to = ajm_grid_wait(c, G, t) ? 1 : 0;
+            s_to = ajm_grid_wait(c, G, rnd) ? 1 : 0;
         }
         ajm_csync();
-        const bool timed_out = s_to != 0;
         if (tsw) p.ts[pass * 8 + 3] = ajm_gtime();
         if (warp < AJM_NPART) {
             // warp j reduces component j of all CTA partials: lane l sums records l, l+32, ... in
@@ -1019,7 +1282,7 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
             const double* src = part + (size_t)warp * G;
             double v = 0.0;
             if (kCluster) {  // G <= 16: lane l holds CTA l's record (the global path's order)
-                if (lane < (int)G) v = ajm_ld_cluster(&s_part[t & 1][warp], (unsigned)lane);
+                if (lane < (int)G) v = ajm_ld_cluster(&s_part[pass & 1][warp], (unsigned)lane);
             } else
             for (int k0 = lane; k0 < (int)G; k0 += 16 * 32) {  // one round trip for G <= 512
                 double r[16];
@@ -1032,9 +1295,24 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
             v = ajm_warp_sum(v);
             if (lane == 0) s_tot[warp] = v;
             // the relative residual ||b - Q x~||/||b|| off the serial control path
-            if (warp == 0 && lane == 0) s_res = sqrt(v) / s_st.nb;
+            if (!kShard && warp == 0 && lane == 0) s_res = sqrt(v) / s_st.nb;
         }
         ajm_csync();
+        if constexpr (kShard) {
+            // s_tot holds this rank's partial: exchange with every rank, then the totals are the
+            // rank partials summed by a fixed lane tree in rank order -- the same bits on every rank
+            if (ajm_shard_cross(p.sh, bid, rnd, s_tot, &c->timeout_flag)) s_to = 1;
+            ajm_csync();
+            if (warp < AJM_NPART) {
+                const double* sl = p.sh.slot + (size_t)(rnd & 1) * AJM_MAX_RANKS * AJM_NPART;
+                double v = lane < p.sh.nranks ? __ldcg(sl + lane * AJM_NPART + warp) : 0.0;
+                v = ajm_warp_sum(v);
+                if (lane == 0) s_tot[warp] = v;
+                if (warp == 0 && lane == 0) s_res = sqrt(v) / s_st.nb;
+            }
+            ajm_csync();
+        }
+        const bool timed_out = s_to != 0;
         if (tsw) p.ts[pass * 8 + 4] = ajm_gtime();
         if (tid == 0) {
             AjmState ls = s_st;  // the control step on a register copy of the shared state
@@ -1043,15 +1321,22 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
             s_st = ls;
             if (timed_out) s_st.done = 1;
             if (tsw) p.ts[pass * 8 + 5] = ajm_gtime();
-            if (!s_st.done) s_pass = pass + 1;
+            if (kProd && !s_st.done) s_pass = pass + 1;
         }
         ajm_csync();
     }
     if (tid == 0) {
-        s_pass = pass;  // units of passes >= pass were never consumed
-        __threadfence_block();
-        s_stop = 1;
         if (bid == 0) c->s = s_st;
+        if constexpr (kProd) {
+            s_pass = pass;  // units of passes >= pass were never consumed
+            __threadfence_block();
+            s_stop = 1;
+        } else {
+            // units [ucnt, ucnt + kStages) were issued ahead for passes that never ran: let the
+            // copies land before the CTA's shared memory goes away
+            for (long long g = ucnt; g < total_units && g < ucnt + kStages; ++g)
+                ajm_mbar_wait(&s_full[g % kStages], (unsigned)((g / kStages) & 1), &c->timeout_flag);
+        }
     }
     if (kCluster && warp == 0) {  // no CTA leaves while another may still read its partials
         __syncwarp();
@@ -1074,8 +1359,10 @@ __global__ void __maxnreg__(96) ajm_solve_kernel(AjmPass p) {
 
 // Column range / strict order / finiteness / diagonal, and D per dmode.  One thread per row,
 // ascending-column sequential sums: D_kk = Q_kk + sum_{j != k}|Q_kj| (eq-J-diag).
-__global__ void ajm_validate_diag_kernel(int n, const long long* __restrict__ rp, const int* __restrict__ col,
-                                         const double* __restrict__ val, int dmode,
+// Columns must lie in [clo, chi): [0, n) for a whole matrix, [-H_lo, n + H_hi) for a shard's local
+// numbering (own rows at [0, n), halo around them).
+__global__ void ajm_validate_diag_kernel(int n, int clo, int chi, const long long* __restrict__ rp,
+                                         const int* __restrict__ col, const double* __restrict__ val, int dmode,
                                          const double* __restrict__ duser, double* __restrict__ D,
                                          int* __restrict__ err, long long skip_len) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1083,11 +1370,11 @@ __global__ void ajm_validate_diag_kernel(int n, const long long* __restrict__ rp
     if (rp[i + 1] - rp[i] > skip_len) return;  // a long row: ajm_validate_long_kernel
     int e = 0;
     double qkk = 0.0, off = 0.0;
-    int last = -1;
+    int last = INT_MIN;
     for (long long k = rp[i]; k < rp[i + 1]; ++k) {
         const int j = col[k];
         const double v = val[k];
-        if (j < 0 || j >= n || j <= last) e |= AJM_EB_CSR;
+        if (j < clo || j >= chi || j <= last) e |= AJM_EB_CSR;
         last = j;
         if (!isfinite(v)) e |= AJM_EB_NONFINITE;
         if (j == i) qkk = v;
@@ -1111,7 +1398,7 @@ __global__ void ajm_validate_diag_kernel(int n, const long long* __restrict__ rp
 // a time, and lane 0 still adds |Q_kj| in ascending column order (the values arrive by shuffles
 // in lane order), so D is bitwise the one-thread result -- without one thread streaming a whole
 // 1e5-entry hub row alone.
-__global__ void ajm_validate_long_kernel(int n, const int* __restrict__ rows, int nrows,
+__global__ void ajm_validate_long_kernel(int clo, int chi, const int* __restrict__ rows, int nrows,
                                          const long long* __restrict__ rp, const int* __restrict__ col,
                                          const double* __restrict__ val, int dmode,
                                          const double* __restrict__ duser, double* __restrict__ D,
@@ -1120,7 +1407,7 @@ __global__ void ajm_validate_long_kernel(int n, const int* __restrict__ rows, in
     if (wid >= nrows) return;  // whole warps
     const int i = rows[wid];
     const long long k0 = rp[i], k1 = rp[i + 1];
-    int e = 0, last = -1;
+    int e = 0, last = INT_MIN;
     double qkk = 0.0, off = 0.0;
     for (long long kb = k0; kb < k1; kb += 32) {
         const long long k = kb + lane;
@@ -1129,7 +1416,7 @@ __global__ void ajm_validate_long_kernel(int n, const int* __restrict__ rows, in
         const double v = in ? val[k] : 0.0;
         int jp = __shfl_up_sync(0xffffffffu, j, 1);
         if (lane == 0) jp = last;
-        if (in && (j < 0 || j >= n || j <= jp)) e |= AJM_EB_CSR;
+        if (in && (j < clo || j >= chi || j <= jp)) e |= AJM_EB_CSR;
         if (in && !isfinite(v)) e |= AJM_EB_NONFINITE;
         const double a = (in && j != i) ? fabs(v) : 0.0;
         const double dq = (in && j == i) ? v : 0.0;
@@ -1441,10 +1728,13 @@ __global__ void ajm_gather_kernel(long long n, const int* __restrict__ idx, cons
         dst[i] = src[idx[i]];
 }
 
-// col[k] = inv[col[k]]: column indices in the layout's row numbering (values and entry order unchanged)
-__global__ void ajm_remap_kernel(long long nnz, const int* __restrict__ inv, int* __restrict__ col) {
-    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < nnz; k += (long long)gridDim.x * blockDim.x)
-        col[k] = inv[col[k]];
+// col[k] = inv[col[k]]: column indices in the layout's row numbering (values and entry order
+// unchanged); a shard's halo columns (outside [0, n)) keep their numbering
+__global__ void ajm_remap_kernel(long long nnz, int n, const int* __restrict__ inv, int* __restrict__ col) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < nnz; k += (long long)gridDim.x * blockDim.x) {
+        const int j = col[k];
+        if (j >= 0 && j < n) col[k] = inv[j];
+    }
 }
 
 // L2 priming: read every line of the vectors once (launched under an access-policy window)
@@ -1511,23 +1801,21 @@ __global__ void ajm_start_vector_kernel(long long n, const int* __restrict__ per
     }
 }
 
-// Control block of a Lanczos run: t = 0 (pass 0 multiplies the start vector, held in the g buffer
-// 0 with scale 1), p/q buffers 0/1/2 as cur/prev/fre with scale 0 (p^_0 = p^_{-1} = 0),
-// histories res_hist = alpha, f_hist = beta; `passes` passes in total.
-__global__ void ajm_init_lanczos_kernel(AjmCtrl* c, long long passes, double* alpha_hist, double* beta_hist,
+// Control block of a Lanczos run: t = 0 (the vector pass that normalises the start vector), w
+// buffers 0/1/2 as cur/prev/fre with scale 0 (p^_0 = p^_{-1} = 0), histories res_hist = alpha,
+// f_hist = beta; at most `steps` Lanczos steps.
+__global__ void ajm_init_lanczos_kernel(AjmCtrl* c, long long steps, double* alpha_hist, double* beta_hist,
                                         double* d_hist, double* dabs_hist) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     AjmState& s = c->s;
     s = AjmState{};
     s.t = 0;
-    s.maxit = passes;
+    s.maxit = steps;
     s.iterations = 0;
     s.nb = 1.0;
     s.cur = 0;
     s.prev = 1;
     s.fre = 2;
-    s.gcur = 0;
-    s.lz_sg = 1.0;
     s.lz_sp = 0.0;
     s.lz_spp = 0.0;
     s.lz_alpha = 0.0;
