@@ -755,6 +755,9 @@ __device__ __forceinline__ double ajm_chunk_dot(const double* sv, const int* sc,
 // Byte-coded columns (kCol8): element k of the lane's row has column row + tab[code[32 k]]; xb is
 // x~ already offset by the row, so the gathers and the ascending-column sum are those of
 // ajm_chunk_dot (same columns, same order: bitwise the same q).
+#ifndef AJM_DOT8_MODE
+#define AJM_DOT8_MODE 2
+#endif
 __device__ __forceinline__ double ajm_chunk_dot8(const double* sv, const uint8_t* sc, int w, const double* xb,
                                                  const int* tab) {
     double s = 0.0;
@@ -771,6 +774,85 @@ __device__ __forceinline__ double ajm_chunk_dot8(const double* sv, const uint8_t
 #pragma unroll
         for (int j = 0; j < 8; ++j)
             if (k0 + j < w) s += sv[(k0 + j) * 32] * xg[j];  // ascending column order
+    }
+    return s;
+}
+
+// The same sum with the stage addressed as 32-bit shared-window offsets (sva: this lane's first
+// value, sca: its first code byte, taba: the offset table): the generic-pointer form compiled to an
+// S2R SR_CgaCtaId + address rebuild per element, and ptxas interleaved the sum with the gathers,
+// issuing gathers 5-8 only after the first product (two gather latencies per chunk; ncu r2a: 20 %
+// of all stall samples on the first DMUL).  Here every code, offset and gather of a batch is issued
+// before the first product.  Same columns, same ascending order: bitwise ajm_chunk_dot8.
+__device__ __forceinline__ uint32_t ajm_lds_u8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int ajm_lds_s32(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double ajm_lds_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+template <int W>  // W <= 8 entries per row, known at compile time
+__device__ __forceinline__ double ajm_chunk_dot8_w(uint32_t sva, uint32_t sca, const double* xb, uint32_t taba) {
+    int cc[W];
+    double xg[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) cc[k] = (int)ajm_lds_u8(sca + 32u * k);
+#pragma unroll
+    for (int k = 0; k < W; ++k) cc[k] = ajm_lds_s32(taba + 4u * (uint32_t)cc[k]);
+#pragma unroll
+    for (int k = 0; k < W; ++k) xg[k] = ajm_ld(xb + cc[k]);
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < W; ++k) s += ajm_lds_f64(sva + 256u * k) * xg[k];  // ascending column order
+    return s;
+}
+__device__ __forceinline__ double ajm_chunk_dot8s(uint32_t sva, uint32_t sca, int w, const double* xb, uint32_t taba) {
+    if (AJM_DOT8_MODE >= 2) {
+        switch (w) {  // the stencils' widths: 7-point (7), 5-point (5), 27-point chunks are w > 8
+            case 7: return ajm_chunk_dot8_w<7>(sva, sca, xb, taba);
+            case 5: return ajm_chunk_dot8_w<5>(sva, sca, xb, taba);
+            default: break;
+        }
+    }
+    double s = 0.0;
+    for (int k0 = 0; k0 < w; k0 += 8) {
+        int cc[8];
+        double xg[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) cc[j] = (k0 + j < w) ? (int)ajm_lds_u8(sca + 32u * (k0 + j)) : 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) cc[j] = ajm_lds_s32(taba + 4u * (uint32_t)cc[j]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) xg[j] = (k0 + j < w) ? ajm_ld(xb + cc[j]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (k0 + j < w) s += ajm_lds_f64(sva + 256u * (k0 + j)) * xg[j];  // ascending column order
+    }
+    return s;
+}
+
+// int32 columns, the same treatment: 32-bit shared-window addresses, every column and gather of a
+// batch of 8 issued before the batch's first product (bitwise ajm_chunk_dot)
+__device__ __forceinline__ double ajm_chunk_dots(uint32_t sva, uint32_t sca, int w, const double* xc) {
+    double s = 0.0;
+    for (int k0 = 0; k0 < w; k0 += 8) {
+        int cc[8];
+        double xg[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) cc[j] = (k0 + j < w) ? ajm_lds_s32(sca + 128u * (k0 + j)) : 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) xg[j] = (k0 + j < w) ? ajm_ld(xc + cc[j]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (k0 + j < w) s += ajm_lds_f64(sva + 256u * (k0 + j)) * xg[j];  // ascending column order
     }
     return s;
 }
@@ -1036,7 +1118,7 @@ __global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
         const long long t = s_st.t;
         const int restart_t = s_st.restart_t;
         const double beta = s_st.beta;
-        AjmLz L;
+        AjmLz L{};
         // (kLz) even passes are the Lanczos vector passes: no SpMV (units released unread)
         const bool lz_vec = kLz && !(t & 1);
         if constexpr (kLz) {
@@ -1172,9 +1254,14 @@ __global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
                     }
                     ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);
                     const int off = (e0 - s_coff[s_uc0[uu]]) + lane;
-                    const double q = kCol8 ? ajm_chunk_dot8(st_val(stage) + off, st_code(stage) + off, w,
-                                                            xc + (row >= 0 ? row : 0), s_ctab)
-                                           : ajm_chunk_dot<kCluster>(st_val(stage) + off, st_col(stage) + off, w, xc);
+                    const double q = kCol8 ? (AJM_DOT8_MODE == 0
+                                                  ? ajm_chunk_dot8(st_val(stage) + off, st_code(stage) + off, w,
+                                                                   xc + (row >= 0 ? row : 0), s_ctab)
+                                                  : ajm_chunk_dot8s(ajm_smem(st_val(stage) + off), ajm_smem(st_code(stage) + off), w,
+                                                                    xc + (row >= 0 ? row : 0), ajm_smem(s_ctab)))
+                                           : (kCluster || kProd || AJM_DOT8_MODE == 0  // (int32 + producer: config 3 measured 0.6 % faster with the generic form)
+                                                  ? ajm_chunk_dot<kCluster>(st_val(stage) + off, st_col(stage) + off, w, xc)
+                                                  : ajm_chunk_dots(ajm_smem(st_val(stage) + off), ajm_smem(st_col(stage) + off), w, xc));
                     if constexpr (kLz) {
                         if (row >= 0) ajm_row_lanczos(L, row, q, xt, acc);
                     } else if (jblk)  // every lane takes part (shuffles); tail lanes store nothing

@@ -11,7 +11,7 @@ mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,driver_version,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${TAG}_smi.txt 2>&1
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${TAG}_build.log 2>&1 || { cat gpurun_out/${TAG}_build.log; exit 1; }
 if [ "$TESTS" = "1" ]; then
-  timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_gpu_tests.log 2>&1
+  timeout 2700 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/${TAG}_gpu_tests.log 2>&1
   echo "tests rc=$?"; tail -3 gpurun_out/${TAG}_gpu_tests.log
   timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke rc=$?"
 fi
