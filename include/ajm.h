@@ -133,7 +133,8 @@ typedef struct {
     int32_t variant;          /* 0 (one kernel family; kept for layout compatibility)           */
     int64_t l2_window_bytes;  /* iterate vectors covered by the persisting-L2 access window     */
     double l2_hit_ratio;      /* persisting fraction of that window                            */
-    int32_t mode;             /* 0 cooperative grid with a TMA ring, 5 single thread-block cluster */
+    int32_t mode;             /* 0 cooperative grid with a TMA ring, 5 single thread-block cluster,
+                                 6 single cluster with the whole solve resident on chip            */
     int32_t l2_mode;          /* L2 policy: 2 all vectors persist, 3 only the x~ buffers persist */
     int32_t launches_per_solve; /* kernel launches of one ajm_solve (L2 priming + init + solver)   */
     int32_t col_bytes;        /* bytes streamed per SELL column index: 4 (int32), or 1 when the

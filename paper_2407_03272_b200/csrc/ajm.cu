@@ -230,6 +230,8 @@ struct ajm_ctx {
     int64_t last_iterations = -1;
     std::string err_msg;
     // ---- row-block shard (NEXT-2; ajm_shard_create) ----
+    int resident = 0;                  // the resident single-cluster kernel (ajm_resident_kernel)
+    size_t lz_dyn_smem = 0;            // dynamic shared memory of the Lanczos twin
     int shard = 0;                     // 1: one rank of a sharded group
     int rank = 0, nranks = 1;
     int colocated = 0;                 // AJM_SHARD_COLOCATED: the group runs as one launch here
@@ -446,11 +448,16 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
 // cooperative launch of the persistent solver kernel, with the L2 access-policy window over the
 // iterate vectors (persisting hits, streaming misses)
 cudaError_t launch_solver(ajm_ctx* h, AjmPass& p, cudaStream_t st, SolveFn fn = nullptr) {
+    // the solver kernel, or its Lanczos twin (which keeps the ring kernel's shared-memory layout and
+    // block when the solver is the resident single-cluster kernel)
+    const bool lz = fn != nullptr && fn != h->fn;
     if (!fn) fn = h->fn;
+    const size_t dyn = lz ? h->lz_dyn_smem : h->dyn_smem;
+    const int threads = (h->resident && !lz) ? AJM_BLOCK : block_threads(h->nseg > 0);
     // the attributes belong to the kernel, which other handles share: set this handle's own, and
     // launch before another thread's handle can change them (the launch itself is asynchronous)
     std::lock_guard<std::mutex> lock(g_attr_mu);
-    cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->dyn_smem);
+    cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributePreferredSharedMemoryCarveout, h->carveout);
     if (e == cudaSuccess && h->cluster && h->grid > 8)
@@ -458,8 +465,8 @@ cudaError_t launch_solver(ajm_ctx* h, AjmPass& p, cudaStream_t st, SolveFn fn = 
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(h->grid);
-    cfg.blockDim = dim3(block_threads(h->nseg > 0));
-    cfg.dynamicSmemBytes = h->dyn_smem;
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = dyn;
     cfg.stream = st;
     cudaLaunchAttribute at[2];
     if (h->cluster) {  // the grid is one thread-block cluster (co-scheduled by construction)
@@ -1232,6 +1239,42 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
             }
             cudaGetLastError();
         }
+        h->lz_dyn_smem = h->dyn_smem;
+        // natural-order SELL rows only, diagonal D: the whole solve resident in the cluster
+        // (ajm_resident_kernel: matrix slices and an x~ replica in shared memory, row state in
+        // registers); AJM_NO_RESIDENT=1 keeps the kCluster ring kernel (experiments)
+        if (h->cluster && !h->relabel && h->nseg == 0 && !h->jbs && !getenv("AJM_NO_RESIDENT")) {
+            int64_t max_el = 0;
+            for (int cc = 0; cc < G; ++cc) {
+                const int ua = cta_unit_h[(size_t)cc], ub = cta_unit_h[(size_t)cc + 1];
+                if (ub > ua) max_el = std::max<int64_t>(max_el, choff[(size_t)unit_c0_h[(size_t)ub]] - choff[(size_t)unit_c0_h[(size_t)ua]]);
+            }
+            const size_t rdyn = (size_t)2 * 8 * (size_t)((n + 31) / 32 * 32) + (size_t)max_el * 12 + 64;
+            const SolveFn rf = ajm_resident_kernel;
+            std::lock_guard<std::mutex> lock(g_attr_mu);
+            if (rdyn <= (size_t)smem_optin &&
+                cudaFuncSetAttribute((const void*)rf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rdyn) == cudaSuccess) {
+                if (G > 8) cudaFuncSetAttribute((const void*)rf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                cudaLaunchConfig_t qc = {};
+                qc.gridDim = dim3(G);
+                qc.blockDim = dim3(AJM_BLOCK);
+                qc.dynamicSmemBytes = rdyn;
+                cudaLaunchAttribute qa[1];
+                qa[0].id = cudaLaunchAttributeClusterDimension;
+                qa[0].val.clusterDim.x = (unsigned)G;
+                qa[0].val.clusterDim.y = 1;
+                qa[0].val.clusterDim.z = 1;
+                qc.attrs = qa;
+                qc.numAttrs = 1;
+                int ncl = 0;
+                if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)rf, &qc) == cudaSuccess && ncl >= 1) {
+                    h->fn = rf;
+                    h->resident = 1;
+                    h->dyn_smem = rdyn;
+                }
+            }
+            cudaGetLastError();
+        }
         mark("P-cluster", (cudaStream_t)-1);
         // owner of a split row = the CTA that runs its last segment
         std::vector<int> seg_cta((size_t)h->nseg, 0);
@@ -1606,7 +1649,8 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
         cudaError_t eo;
         {
             std::lock_guard<std::mutex> lock(g_attr_mu);
-            eo = fn_occupancy(h->fn, h->dyn_smem, pct, &occ, block_threads(h->nseg > 0));
+            if (h->resident) pct = 100;  // one CTA per SM of the cluster: all of it to shared memory
+            eo = fn_occupancy(h->fn, h->dyn_smem, pct, &occ, h->resident ? AJM_BLOCK : block_threads(h->nseg > 0));
             if (eo == cudaSuccess && occ < h->ctas_per_sm && !h->cluster) {
                 pct = 100;
                 eo = cudaFuncSetAttribute((const void*)h->fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
@@ -2479,7 +2523,7 @@ ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info) {
     info->variant = h->nseg > 0 ? 1 : 0;  // 1: no producer warp, 128 registers (layouts with segments)
     info->l2_window_bytes = (int64_t)h->win_bytes;
     info->l2_hit_ratio = h->win_hit;
-    info->mode = h->cluster ? 5 : 0;
+    info->mode = h->resident ? 6 : (h->cluster ? 5 : 0);
     info->sell_elems = h->sell_elems;
     info->l2_mode = h->l2_mode;
     info->launches_per_solve = (int32_t)(1 + (h->prime_bytes ? 1 : 0) + std::max<int64_t>(h->last_launches, 1));

@@ -506,6 +506,8 @@ __device__ __forceinline__ unsigned long long ajm_ld_acquire64(const unsigned lo
 // Arrival (thread 0, right after ajm_block_reduce, whose CTA barrier already ordered every thread's
 // stores of this pass): a release-add orders them before the arrival without waiting for the
 // atomic's round trip.
+// (Measured and rejected: the counter split over 8 L2 lines, CTAs arriving on bid % 8 and the waiters
+// summing relaxed reads of all 8 -- config 2 39.9 -> 40.9 us/pass.)
 __device__ __forceinline__ void ajm_grid_arrive(AjmCtrl* c) {
     asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&c->bar_count) : "memory");
 }
@@ -819,6 +821,7 @@ __device__ __forceinline__ double ajm_chunk_dot8s(uint32_t sva, uint32_t sca, in
         switch (w) {  // the stencils' widths: 7-point (7), 5-point (5), 27-point chunks are w > 8
             case 7: return ajm_chunk_dot8_w<7>(sva, sca, xb, taba);
             case 5: return ajm_chunk_dot8_w<5>(sva, sca, xb, taba);
+            // (27, fully unrolled: measured config 5 1068 -> 1131 us/pass, rejected)
             default: break;
         }
     }
@@ -1426,6 +1429,188 @@ __global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
         }
     }
     if (kCluster && warp == 0) {  // no CTA leaves while another may still read its partials
+        __syncwarp();
+        if (lane < (int)G) ajm_cluster_arrive(&s_cexit, (unsigned)lane);
+        if (lane == 0) ajm_cluster_wait(&s_cexit, 0u, &c->timeout_flag);
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Small problems, resident in one thread-block cluster (config 1: the whole pass is latency)
+// ------------------------------------------------------------------------------------------------
+// The grid is ONE cluster of G <= 16 CTAs, 8 warps each, one 32-row SELL chunk per warp (natural
+// order, rows <= 64 nonzeros, diagonal D).  Everything stays on chip for the whole solve:
+//   - the CTA's chunks (values + int32 columns) are copied into shared memory once;
+//   - every lane keeps its row's b_i, D_i, x~^t_i, x^{t-1}_i and (Q x^{t-1})_i in registers;
+//   - every CTA holds a full replica of x~ in shared memory (double-buffered by pass parity): a lane
+//     publishes x~^{t+1}_i to all G replicas with st.shared::cluster, so the gathers of the next pass
+//     are local shared-memory loads;
+//   - the CTA partials and the per-pass barrier go through distributed shared memory as in the
+//     kCluster path (remote mbarrier arrivals, ld.shared::cluster).
+// Per pass nothing touches global memory except CTA 0's history entries.  The row sums (ascending
+// column, from 0.0), the update, the CTA and cluster reduction orders and the control step are
+// those of ajm_solve_kernel's kCluster path: the iterates are bitwise the same.
+__global__ void __launch_bounds__(AJM_BLOCK, 1) ajm_resident_kernel(AjmPass p) {
+    extern __shared__ __align__(128) unsigned char s_dyn[];
+    __shared__ double s_red[AJM_WARPS][AJM_NPART];
+    __shared__ double s_tot[AJM_NPART];
+    __shared__ double s_part[2][AJM_NPART];
+    __shared__ double s_res;
+    __shared__ AjmState s_st;
+    __shared__ __align__(8) uint64_t s_cbar;
+    __shared__ __align__(8) uint64_t s_cexit;
+    __shared__ int s_to;
+    AjmCtrl* c = p.ctrl;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int bid = (int)blockIdx.x;
+    const unsigned G = gridDim.x;
+    const int npad = (p.n + 31) & ~31;
+    double* xs0 = reinterpret_cast<double*>(s_dyn);
+    double* xs1 = xs0 + npad;
+    const int u0 = p.cta_unit[bid], u1 = p.cta_unit[bid + 1];
+    const int cfirst = u1 > u0 ? p.unit_c0[u0] : 0;
+    const int nchk = u1 > u0 ? p.unit_c0[u1] - cfirst : 0;
+    const long long efirst = nchk > 0 ? p.chunk_off[cfirst] : 0;
+    const int nel = nchk > 0 ? (int)(p.chunk_off[cfirst + nchk] - efirst) : 0;
+    double* sv = xs1 + npad;
+    int* sc = reinterpret_cast<int*>(sv + nel);
+    for (int i = tid; i < nel; i += AJM_BLOCK) {
+        sv[i] = p.sval[efirst + i];
+        sc[i] = p.scol[efirst + i];
+    }
+    if (tid == 0) {
+        s_st = c->s;
+        ajm_mbar_init(&s_cbar, G);
+        ajm_mbar_init(&s_cexit, G);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    {
+        const double* x0 = ajm_sel(p, s_st.cur);
+        for (int i = tid; i < p.n; i += AJM_BLOCK) xs0[i] = x0[i];
+    }
+    // this lane's row and its chunk column
+    const bool has = warp < nchk;
+    int w = 0, e0 = 0, row = -1;
+    if (has) {
+        e0 = (int)(p.chunk_off[cfirst + warp] - efirst) + lane;
+        w = (int)((p.chunk_off[cfirst + warp + 1] - p.chunk_off[cfirst + warp]) >> 5);
+        const int slot = (cfirst + warp) * 32 + lane;
+        row = slot < p.n_sell ? slot : -1;
+    }
+    double bi = 0.0, Di = 1.0, xt = 0.0, xp = 0.0, qxp = 0.0;
+    if (row >= 0) {
+        bi = p.b[row];
+        Di = p.D[row];
+        xt = ajm_sel(p, s_st.cur)[row];
+        xp = ajm_sel(p, s_st.prev)[row];
+        qxp = p.Qxp[row];
+    }
+    __syncthreads();
+    // every CTA's barriers initialised (and its replica loaded) before any remote access
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    int pass = 0;
+    for (; pass < p.max_passes; ++pass) {
+        if (s_st.done) break;
+        const int restart_t = s_st.restart_t;
+        const double beta = s_st.beta;
+        const double* xr = (pass & 1) ? xs1 : xs0;  // x~^t, all rows
+        double* xw = (pass & 1) ? xs0 : xs1;        // receives x~^{t+1}
+        AjmAcc acc = {0.0, 0.0, 0.0, 0.0, 0.0};
+        double q = 0.0, xn = 0.0;
+        if (row >= 0) {
+            for (int k0 = 0; k0 < w; k0 += 8) {  // ascending column order; a batch's loads first
+                double v[8], xg[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const bool in = k0 + j < w;
+                    const int e = e0 + 32 * (k0 + j);
+                    v[j] = in ? sv[e] : 0.0;
+                    xg[j] = in ? xr[sc[e]] : 0.0;
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (k0 + j < w) q += v[j] * xg[j];
+            }
+            const double r = bi - q;
+            acc.rr += r * r;
+            acc.xq += xt * q;
+            acc.bx += bi * xt;
+            double y, qy, xnow;
+            if (!restart_t) {
+                y = xt + beta * (xt - xp);
+                qy = q + beta * (q - qxp);
+                xnow = xt;
+            } else {
+                y = xp;
+                qy = qxp;
+                xnow = xp;
+            }
+            xn = y + (bi - qy) / Di;
+            const double term = (qy - bi) * (xn - xnow);
+            acc.d += term;
+            acc.dabs += fabs(term);
+            // publish x~^{t+1}_row to every CTA's replica
+            const uint32_t la = ajm_smem(xw + row);
+            for (unsigned rk = 0; rk < G; ++rk)
+                asm volatile("{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\tst.shared::cluster.f64 [ra], %2;\n\t}"
+                             ::"r"(la), "r"(rk), "d"(xn) : "memory");
+        }
+        ajm_block_reduce(acc, s_red);
+        double an_c = 0.0, beta_c = 0.0;
+        if (warp == 0) {
+            if (lane == 0) {
+                double* sp = s_part[pass & 1];
+                sp[0] = acc.rr;
+                sp[1] = acc.xq;
+                sp[2] = acc.bx;
+                sp[3] = acc.d;
+                sp[4] = acc.dabs;
+            }
+            __syncwarp();
+            // lane r arrives (release, cluster scope) on CTA r's barrier: this CTA's replica stores
+            // (ordered by the CTA barrier in ajm_block_reduce) and its partials
+            if (lane < (int)G) ajm_cluster_arrive(&s_cbar, (unsigned)lane);
+        }
+        if (tid == 0) {
+            const double a = s_st.alpha;
+            an_c = (1.0 + sqrt(1.0 + 4.0 * a * a)) / 2.0;
+            beta_c = s_st.momentum ? (a - 1.0) / an_c : 0.0;
+            s_to = ajm_cluster_wait(&s_cbar, (unsigned)(pass & 1), &c->timeout_flag) ? 1 : 0;
+        }
+        ajm_csync();
+        if (warp < AJM_NPART) {  // lane l holds CTA l's record: the kCluster path's order
+            double v = 0.0;
+            if (lane < (int)G) v = ajm_ld_cluster(&s_part[pass & 1][warp], (unsigned)lane);
+            v = ajm_warp_sum(v);
+            if (lane == 0) s_tot[warp] = v;
+            if (warp == 0 && lane == 0) s_res = sqrt(v) / s_st.nb;
+        }
+        ajm_csync();
+        if (tid == 0) {
+            AjmState ls = s_st;
+            ajm_control_step(ls, s_tot, c, bid == 0, an_c, beta_c, s_res);
+            s_st = ls;
+            if (s_to) s_st.done = 1;
+        }
+        ajm_csync();
+        if (!s_st.done) {  // the rotation of the buffers, in registers
+            if (!restart_t) {
+                xp = xt;
+                qxp = q;
+            }
+            xt = xn;
+        }
+    }
+    // the state back to the buffers the control block names (the answer, and a later launch)
+    if (row >= 0) {
+        ajm_sel(p, s_st.cur)[row] = xt;
+        ajm_sel(p, s_st.prev)[row] = xp;
+        p.Qxp[row] = qxp;
+    }
+    if (tid == 0 && bid == 0) c->s = s_st;
+    if (warp == 0) {  // no CTA leaves while another may still read its partials
         __syncwarp();
         if (lane < (int)G) ajm_cluster_arrive(&s_cexit, (unsigned)lane);
         if (lane == 0) ajm_cluster_wait(&s_cexit, 0u, &c->timeout_flag);

@@ -35,4 +35,5 @@ def test_c_example_solves(tmp_path):
     assert out.returncode == 0, out.stderr
     r = json.loads(out.stdout)
     assert r["status"] == 0 and r["rel_residual"] <= 1e-10
-    assert r["max_abs_err"] <= 1e-6 and r["abi"] == 3
+    import paper_2407_03272_b200 as ajm
+    assert r["max_abs_err"] <= 1e-6 and r["abi"] == ajm.ABI_VERSION

@@ -406,3 +406,29 @@ def test_threads_with_own_handles_and_streams():
     for t in th:
         t.join()
     assert not errs, errs
+
+
+def test_resident_cluster_bitwise():
+    """Config 1 runs on the resident single-cluster kernel (mode 6: matrix slices and an x~ replica
+    in shared memory, row state in registers); its iterates and histories are bitwise those of the
+    kCluster ring kernel (mode 5, AJM_NO_RESIDENT=1) and of the host-driven loop (one launch per
+    pass: the state goes through global memory between launches)."""
+    import os
+    p = synth.config_problem(1)
+    for restart in (True, False):
+        a = gpu_solve(p.Q, p.b, tol=0.0, maxit=700, restart=restart)
+        os.environ["AJM_NO_RESIDENT"] = "1"
+        try:
+            b = gpu_solve(p.Q, p.b, tol=0.0, maxit=700, restart=restart)
+        finally:
+            del os.environ["AJM_NO_RESIDENT"]
+        c = gpu_solve(p.Q, p.b, tol=0.0, maxit=700, restart=restart, loop="host")
+        assert a.info["mode"] == 6 and b.info["mode"] == 5 and c.info["mode"] == 6
+        for o in (b, c):
+            np.testing.assert_array_equal(a.x, o.x)
+            np.testing.assert_array_equal(a.res_hist, o.res_hist)
+            np.testing.assert_array_equal(a.f_hist, o.f_hist)
+            assert a.restart_iters == o.restart_iters
+        d = gpu_solve(p.Q, p.b, tol=1e-6, maxit=5000, restart=restart)
+        od = oracle.solve(p.Q, p.b, tol=1e-6, maxit=5000, restart=restart)
+        assert abs(d.iterations - od.iterations) <= 1

@@ -51,7 +51,7 @@ def test_poisson_closed_form(cfg, scale):
     s = 4 * np.sin(np.arange(1, m + 1) * np.pi / (2 * (m + 1))) ** 2
     sp, info = _estimate(p.Q, "qdiag")
     _check(sp, dim * s[0] / (2 * dim), dim * s[-1] / (2 * dim))
-    assert info["mode"] == (5 if cfg == 1 else 0)
+    assert info["mode"] == (6 if cfg == 1 else 0)  # (the Lanczos twin of the resident kernel: kCluster)
 
 
 @pytest.mark.parametrize("cfg,scale", [(2, 0.25), (3, 0.0025), (4, 0.00075), (5, 0.039)])
