@@ -124,3 +124,23 @@ def test_shard_errors():
         ajm.ShardGroup.from_csr(p.Q, p.b, 2, dmode="jblock")
     with pytest.raises(ajm.AjmError):
         ajm.ShardGroup.from_csr(p.Q, p.b, 9)  # > AJM_MAX_RANKS
+
+
+def test_shard_solver_per_process_path_one_rank():
+    """The per-process path of bench.py --gpus N (ajm_shard_create without AJM_SHARD_COLOCATED on the
+    whole device, the connection records exchanged by the caller, ajm_solve on the shard handle: the
+    kernel's own launch with its peer table) with a single rank -- the only size one GPU can run
+    concurrently.  Bitwise the single-GPU solve (rank partial + zeros), and the oracle to 1e-10."""
+    import paper_2407_03272_b200 as ajm
+    for cfg, scale in [(3, 0.02), (2, 0.25)]:
+        p = synth.config_problem(cfg, scale)
+        with ajm.ShardSolver(0, 1, [0, p.Q.n], p.Q.row_ptr, p.Q.col, p.Q.val, p.b, exchange=lambda b: [b]) as s:
+            r = s.solve(tol=0.0, maxit=400)
+            x = r.x.cpu().numpy()
+            assert s.info()["nranks"] == 1 and s.info()["halo"] == 0
+            r2 = s.solve(tol=1e-6, maxit=5000)  # a second solve: the arrival counters continue
+        g = gpu_solve(p.Q, p.b, tol=0.0, maxit=400)
+        np.testing.assert_array_equal(x, g.x)
+        np.testing.assert_array_equal(r.res_hist, g.res_hist)
+        o = oracle.solve(p.Q, p.b, tol=1e-6, maxit=5000, restart=True)
+        assert abs(r2.iterations - o.iterations) <= 1

@@ -203,3 +203,34 @@ def test_sharded_iteration_gloo_world2_matches_oracle(cfg, scale, restart):
     o = oracle.solve(p.Q, p.b, tol=0.0, maxit=maxit, restart=restart)
     assert o.restart_iters == out[0][3]
     assert np.abs(x - o.x).max() / np.abs(o.x).max() <= 1e-10
+
+
+def _blob_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import torch.distributed as dist
+    import paper_2407_03272_b200 as ajm
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        blob = bytes([rank]) * ajm.AJM_SHARD_BLOB_BYTES
+        q.put((rank, ajm.allgather_bytes(blob)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_connection_records_allgather_gloo_world2():
+    """ShardSolver's default exchange of the connection records (torch.distributed all-gather, the
+    plumbing of bench.py --gpus N) delivers every rank's record to every rank in rank order."""
+    import paper_2407_03272_b200 as ajm
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_blob_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    out = [q.get(timeout=120) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    for rank, blobs in out:
+        assert [b[0] for b in blobs] == [0, 1]
+        assert all(len(b) == ajm.AJM_SHARD_BLOB_BYTES for b in blobs)
