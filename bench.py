@@ -478,7 +478,13 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     dist = init_dist(world, "nccl")
     if world > 1 and args.parallel == "shard":
-        return run_sharded(args, rank, world, local, dev, dist)
+        try:
+            return run_sharded(args, rank, world, local, dev, dist)
+        except Exception as e:  # reported on the line of the replica run below, never hidden
+            args.shard_error = f"{type(e).__name__}: {e}"[:300]
+            print(f"[bench] sharded solve failed on rank {rank}: {args.shard_error}; running replicas",
+                  file=sys.stderr, flush=True)
+            barrier(dist, dev)
     W = WORKLOADS[args.config]
     tol = W["tol"] if args.tol is None else args.tol
     maxit = W["maxit"] if args.maxit is None else args.maxit
@@ -578,6 +584,8 @@ def run_ours(args):
         "cpu_baseline_1thread": cpu1,
         "other_configs": others,
     }
+    if getattr(args, "shard_error", None):
+        line["shard_error"] = args.shard_error
     rg = gather_roof(p, info, passes, loop_ms)
     if rg is not None:
         line["roofline_gather"] = rg

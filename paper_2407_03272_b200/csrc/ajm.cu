@@ -95,15 +95,20 @@ SolveFn lanczos_fn(bool seg, bool cluster, bool gmeta, int col_bytes, int stages
     return nullptr;
 }
 
-// One rank of a row-block sharded solve (kShard): int32 columns at ring depth 3 / 4 or byte-coded
-// columns at 4 / 5, with or without the segment phases -- the layouts create picks for shards.
-SolveFn shard_fn(int col_bytes, bool seg, int stages) {
+// One rank of a row-block sharded solve: int32 columns at ring depth 3 / 4 or byte-coded columns at
+// 4 / 5, with or without the segment phases -- the layouts create picks for shards; emu: the
+// emulated-group kernel (kShard = 2) instead of the per-process one (kShard = 1)
+template <int kSh>
+SolveFn shard_fn_t(int col_bytes, bool seg, int stages) {
     if (col_bytes == 1) {
-        if (stages == 5) return seg ? ajm_solve_kernel<5, true, false, 0, false, true, false, true> : ajm_solve_kernel<5, false, false, 0, false, true, false, true>;
-        return seg ? ajm_solve_kernel<4, true, false, 0, false, true, false, true> : ajm_solve_kernel<4, false, false, 0, false, true, false, true>;
+        if (stages == 5) return seg ? ajm_solve_kernel<5, true, false, 0, false, true, false, kSh> : ajm_solve_kernel<5, false, false, 0, false, true, false, kSh>;
+        return seg ? ajm_solve_kernel<4, true, false, 0, false, true, false, kSh> : ajm_solve_kernel<4, false, false, 0, false, true, false, kSh>;
     }
-    if (stages == 4) return seg ? ajm_solve_kernel<4, true, false, 0, false, false, false, true> : ajm_solve_kernel<4, false, false, 0, false, false, false, true>;
-    return seg ? ajm_solve_kernel<3, true, false, 0, false, false, false, true> : ajm_solve_kernel<3, false, false, 0, false, false, false, true>;
+    if (stages == 4) return seg ? ajm_solve_kernel<4, true, false, 0, false, false, false, kSh> : ajm_solve_kernel<4, false, false, 0, false, false, false, kSh>;
+    return seg ? ajm_solve_kernel<3, true, false, 0, false, false, false, kSh> : ajm_solve_kernel<3, false, false, 0, false, false, false, kSh>;
+}
+SolveFn shard_fn(int col_bytes, bool seg, int stages, bool emu) {
+    return emu ? shard_fn_t<2>(col_bytes, seg, stages) : shard_fn_t<1>(col_bytes, seg, stages);
 }
 
 // Threads per CTA of a solver kernel: 8 consumer warps + the TMA producer warp (kProd, layouts
@@ -681,7 +686,9 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
         h->h_hi = sh->h_hi;
         h->halo_cnt = sh->halo_cnt;
         h->send_cnt = sh->send_cnt;
-        h->l2persist = 0;  // no persisting window: the group's buffers are other ranks' too
+        // one process per GPU: the rank's iterate buffers get the device's persisting L2 window like a
+        // single-GPU handle (emulated groups share one device and one launch: none)
+        h->l2persist = sh->colocated ? 0 : 1;
     }
     h->flags = flags;
     h->dmode = dmode;
@@ -1380,7 +1387,7 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
             // mode 3: only the three rotating iterate buffers X0..X2 (the gathered x~ lives there),
             // b, D, Qx streamed with evict_first
             h->l2_mode = (double)vec_bytes <= 0.75 * (double)maxp ? 2 : 3;
-            const size_t wb = h->l2_mode == 3 ? sizeof(double) * 3 * (size_t)h->n_pad : vec_bytes;
+            const size_t wb = h->l2_mode == 3 ? sizeof(double) * 3 * (size_t)(h->shard ? h->xstride : h->n_pad) : vec_bytes;
             h->win_bytes = std::min<size_t>(wb, (size_t)maxw);
             h->win_hit = (float)std::min(1.0, (double)cur / (double)h->win_bytes);
             // mode 3 on vectors that fit the L2 (config 2): before each solve one touch pass over
@@ -1683,7 +1690,7 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
     if (!h->jbs && !sh) h->fn_lz = lanczos_fn(h->nseg > 0, h->cluster != 0, h->gmeta != 0, h->col_bytes, h->ring_stages);
     if (sh) {
         // the rank's kernel: the same layout class with the halo exchange compiled in
-        h->fn = shard_fn(h->col_bytes, h->nseg > 0, h->ring_stages);
+        h->fn = shard_fn(h->col_bytes, h->nseg > 0, h->ring_stages, sh->colocated != 0);
         {
             std::lock_guard<std::mutex> lock(g_attr_mu);
             int occ = 0;
@@ -2276,7 +2283,7 @@ ajm_status_t ajm_group_solve(const ajm_handle_t* hs, int32_t nranks, const doubl
     }
     if (h0->col_bytes == 1) stages = std::max(4, std::min(5, stages));
     else stages = std::max(3, std::min(4, stages));
-    const SolveFn gfn = shard_fn(h0->col_bytes, any_seg, stages);
+    const SolveFn gfn = shard_fn(h0->col_bytes, any_seg, stages, true);
     const size_t gdyn = (size_t)stages * AJM_UNIT_EL * (h0->col_bytes == 1 ? 9 : 12) + meta;
     cudaStream_t st = (cudaStream_t)cuda_stream;
     for (int r = 0; r < nranks; ++r) {

@@ -540,7 +540,9 @@ __device__ __forceinline__ unsigned long long ajm_ld_acquire_sys64(const unsigne
 // orders it before the rank's cross-rank signal.
 __device__ __forceinline__ void ajm_shard_push(const AjmShard& sh, int bid, const double* src, int buf) {
     const int k1 = __ldg(sh.snd_cta + bid + 1);
-    for (int k = __ldg(sh.snd_cta + bid) + (int)threadIdx.x; k < k1; k += AJM_BLOCK) {
+    int k = __ldg(sh.snd_cta + bid) + (int)threadIdx.x;
+    if (k >= k1) return;  // (only the threads that stored to a peer pay for the system-scope fence)
+    for (; k < k1; k += AJM_BLOCK) {
         const int4 e = __ldg(sh.snd + k);
         double* dst = sh.peers[e.y].x[buf];
         dst[e.z] = ajm_ld(src + e.x);
@@ -566,14 +568,17 @@ __device__ __forceinline__ bool ajm_shard_cross(const AjmShard& sh, int bid, lon
     if (threadIdx.x == 0) {
         const unsigned long long target = sh.bar_base + (unsigned long long)sh.nranks * (unsigned long long)(rnd + 1);
         long long spins = 0;
+        // bounded: a rank that never arrives (a failed peer process) fails this solve within ~10 s
+        // instead of holding the GPU for minutes
         while (ajm_ld_acquire_sys64(sh.bar) < target) {
-            if (++spins > (1LL << 30)) {
+            if (spins > 4096) __nanosleep(256);
+            if (++spins > (1LL << 25)) {
                 atomicExch(timeout_flag, 1u);
                 to = true;
                 break;
             }
         }
-        __threadfence_system();
+        __threadfence();  // (the acquire was system-scope; this invalidates the SM's L1 for the halo reads)
     }
     return to;
 }
@@ -912,11 +917,13 @@ __device__ __forceinline__ double ajm_ld_cluster(const double* local, unsigned r
 // kCol8 = true: byte-coded SELL columns (col = row + ctab[code]).
 // kLz = true: the Lanczos pass of ajm_estimate_spectrum (same SpMV, epilogue ajm_row_lanczos,
 //   control ajm_lanczos_control) instead of the AJM pass.
-// kShard = true: one rank of a row-block sharded solve (NEXT-2; AjmShard above): before the loop a
+// kShard != 0: one rank of a row-block sharded solve (NEXT-2; AjmShard above): before the loop a
 //   round 0 pushes x~^0's halo entries, and every pass pushes x~^{t+1}'s, then the rank's partial is
 //   exchanged with every rank (rank order, bitwise the same totals everywhere) before the control
-//   step.  With sh.emu set, ONE cooperative launch runs every rank (CTA block r*emu_grid.. is rank
-//   r) on one device -- the same code, peers being ordinary device pointers.
+//   step.  kShard = 1: one rank per launch (a process per GPU), the pass struct in the parameter
+//   space like the single-GPU kernel.  kShard = 2: the emulated group -- ONE cooperative launch
+//   runs every rank (CTA block r*emu_grid.. is rank r) on one device, each CTA reading its rank's
+//   pass struct from a shared-memory copy; peers are ordinary device pointers.
 // kProd: how the TMA ring is refilled.
 //   true  -- a 9th (producer) warp waits on each stage's "empty" mbarrier and refills it; two CTAs of
 //            9 warps fit the SM's register files at 96 registers per thread.  The layouts without
@@ -925,29 +932,24 @@ __device__ __forceinline__ double ajm_ld_cluster(const double* local, unsigned r
 //            8 warps fit 128 registers per thread -- what the segment phases (the long-row dot, the
 //            sub-warp groups, the epilogue operand prefetch) need to run without spills.
 template <int kStages, bool kSeg = true, bool kCluster = false, int kJB = 0, bool kGMeta = false,
-          bool kCol8 = false, bool kLz = false, bool kShard = false, bool kProd = !kSeg>
+          bool kCol8 = false, bool kLz = false, int kShard = 0, bool kProd = !kSeg>
 __global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
     static_assert(!kShard || (!kCluster && !kJB && !kGMeta && !kLz), "sharded solve: plain ring variants only");
-    // (kShard) this CTA's rank's pass struct, in shared memory (the emulated launch serves all ranks)
-    __shared__ __align__(16) unsigned char s_pp[kShard ? sizeof(AjmPass) : 16];
+    // (kShard = 2) this CTA's rank's pass struct, in shared memory (the launch serves all ranks)
+    __shared__ __align__(16) unsigned char s_pp[kShard == 2 ? sizeof(AjmPass) : 16];
     int bid = (int)blockIdx.x;
     unsigned G = gridDim.x;
-    if constexpr (kShard) {
-        int rk = p0.sh.rank;
-        const AjmPass* srcp = &p0;
-        if (p0.sh.emu) {
-            rk = (int)blockIdx.x / p0.sh.emu_grid;
-            bid = (int)blockIdx.x - rk * p0.sh.emu_grid;
-            G = (unsigned)p0.sh.emu_grid;
-            srcp = p0.sh.emu + rk;
-        }
-        const unsigned long long* s8 = reinterpret_cast<const unsigned long long*>(srcp);
+    if constexpr (kShard == 2) {
+        const int rk = (int)blockIdx.x / p0.sh.emu_grid;
+        bid = (int)blockIdx.x - rk * p0.sh.emu_grid;
+        G = (unsigned)p0.sh.emu_grid;
+        const unsigned long long* s8 = reinterpret_cast<const unsigned long long*>(p0.sh.emu + rk);
         unsigned long long* d8 = reinterpret_cast<unsigned long long*>(s_pp);
         static_assert(sizeof(AjmPass) % 8 == 0, "AjmPass copy");
         for (int i = threadIdx.x; i < (int)(sizeof(AjmPass) / 8); i += blockDim.x) d8[i] = s8[i];
         __syncthreads();
     }
-    const AjmPass& p = kShard ? *reinterpret_cast<const AjmPass*>(s_pp) : p0;
+    const AjmPass& p = kShard == 2 ? *reinterpret_cast<const AjmPass*>(s_pp) : p0;
     extern __shared__ __align__(128) unsigned char s_dyn[];
     __shared__ double s_red[AJM_WARPS][AJM_NPART];
     __shared__ double s_tot[AJM_NPART];
