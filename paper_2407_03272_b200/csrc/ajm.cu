@@ -1813,9 +1813,9 @@ static ajm_status_t solve_post(ajm_ctx* h, int64_t launches, float ms, double* x
     AJM_CUDA(h, cudaMemcpyAsync(h->h_ctrl, h->ctrl, sizeof(AjmCtrl), cudaMemcpyDeviceToHost, st));
     AJM_CUDA(h, cudaStreamSynchronize(st));
     const AjmCtrl& c = *h->h_ctrl;
-    if (h->shard) {  // every rank added one arrival per round to every rank's counter
+    if (h->shard) {  // every other rank added one arrival per round to this rank's counter
         if (c.timeout_flag || !c.s.done) h->broken = true;
-        else h->bar_base += (unsigned long long)h->nranks * (unsigned long long)(c.s.iterations + 2);
+        else h->bar_base += (unsigned long long)(h->nranks - 1) * (unsigned long long)(c.s.iterations + 2);
     }
     if (c.timeout_flag) return fail(h, AJM_ERR_CUDA, "device barrier wait timed out (internal error)");
     if (!c.s.done) return fail(h, AJM_ERR_CUDA, "iteration loop ended without a termination decision");

@@ -556,17 +556,19 @@ __device__ __forceinline__ void ajm_shard_push(const AjmShard& sh, int bid, cons
 __device__ __forceinline__ bool ajm_shard_cross(const AjmShard& sh, int bid, long long rnd, const double* rk,
                                                 unsigned* timeout_flag) {
     const int lane = threadIdx.x & 31;
-    if (bid == 0 && threadIdx.x < 32 && lane < sh.nranks) {
+    // to the OTHER ranks only: every CTA of this rank holds this rank's partial already.  The
+    // system-scope release orders the slot stores and (cumulatively, through the rank's grid
+    // barrier) every CTA's fenced halo pushes before the arrival.
+    if (bid == 0 && threadIdx.x < 32 && lane < sh.nranks && lane != sh.rank) {
         const AjmPeer& pe = sh.peers[lane];
         double* d = pe.slot + ((size_t)(rnd & 1) * AJM_MAX_RANKS + sh.rank) * AJM_NPART;
 #pragma unroll
         for (int j = 0; j < AJM_NPART; ++j) d[j] = rk[j];
-        __threadfence_system();
         asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(pe.bar) : "memory");
     }
     bool to = false;
-    if (threadIdx.x == 0) {
-        const unsigned long long target = sh.bar_base + (unsigned long long)sh.nranks * (unsigned long long)(rnd + 1);
+    if (threadIdx.x == 0 && sh.nranks > 1) {
+        const unsigned long long target = sh.bar_base + (unsigned long long)(sh.nranks - 1) * (unsigned long long)(rnd + 1);
         long long spins = 0;
         // bounded: a rank that never arrives (a failed peer process) fails this solve within ~10 s
         // instead of holding the GPU for minutes
@@ -1397,7 +1399,8 @@ __global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
             ajm_csync();
             if (warp < AJM_NPART) {
                 const double* sl = p.sh.slot + (size_t)(rnd & 1) * AJM_MAX_RANKS * AJM_NPART;
-                double v = lane < p.sh.nranks ? __ldcg(sl + lane * AJM_NPART + warp) : 0.0;
+                const double own = s_tot[warp];  // this rank's partial (the bits the others received)
+                double v = lane < p.sh.nranks ? (lane == p.sh.rank ? own : __ldcg(sl + lane * AJM_NPART + warp)) : 0.0;
                 v = ajm_warp_sum(v);
                 if (lane == 0) s_tot[warp] = v;
                 if (warp == 0 && lane == 0) s_res = sqrt(v) / s_st.nb;
