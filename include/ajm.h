@@ -31,11 +31,12 @@
 extern "C" {
 #endif
 
-#define AJM_ABI_VERSION 4  /* 2: AJM_D_JBLOCK, ajm_get_jblock, ajm_info_t.l2_mode / launches_per_solve;
+#define AJM_ABI_VERSION 5  /* 2: AJM_D_JBLOCK, ajm_get_jblock, ajm_info_t.l2_mode / launches_per_solve;
                               3: layout create flags (AJM_INT32_COLUMNS, AJM_GLOBAL_TABLES, AJM_SEGMENTS_*,
                                  AJM_DEBUG_POISON), ajm_estimate_spectrum;
                               4: the row-block sharded API (ajm_partition_rows, ajm_shard_*,
-                                 ajm_group_solve), ajm_info_t.nranks / halo */
+                                 ajm_group_solve), ajm_info_t.nranks / halo;
+                              5: pair-coded SELL entries (AJM_VALUE_STREAM, ajm_info_t.val_bytes) */
 
 typedef struct ajm_ctx* ajm_handle_t;
 
@@ -85,6 +86,8 @@ typedef enum {
 #define AJM_SEGMENTS_DYNAMIC 0x80000u /* ... or a per-pass claim queue (default: dynamic only when long
                                          rows carry >= 90% of the nonzeros); same iterates either way   */
 #define AJM_DEBUG_POISON 0x100000u    /* debug: fill every device allocation of this create with 0xff   */
+#define AJM_VALUE_STREAM 0x400000u    /* keep streaming the SELL values even when the (column offset,
+                                         value) pairs take <= 256 values (no pair codes; same iterates) */
 /* block size of AJM_D_JBLOCK, bits 8..15 of the flags: bs in {1, 2, 4, 8, 16, 32} */
 #define AJM_JBLOCK_SIZE(bs) (((uint32_t)(bs) & 0xffu) << 8)
 #define AJM_JBLOCK_SIZE_OF(flags) (((uint32_t)(flags) >> 8) & 0xffu)
@@ -145,6 +148,10 @@ typedef struct {
     int64_t halo;             /* sharded handles: halo entries H_lo + H_hi received per pass       */
     int64_t send;             /* sharded handles: entries pushed to other ranks per pass           */
     int64_t group_rows;       /* rows of 65..256 nonzeros run four to a warp (8-lane sub-warp groups) */
+    int32_t val_bytes;        /* bytes streamed per SELL value: 8, or 0 when the byte code indexes a
+                                 table of <= 256 (value, column offset) pairs (pair-coded entries:
+                                 constant-coefficient stencils)                       */
+    int32_t pad_;
 } ajm_info_t;
 
 /*

@@ -38,9 +38,10 @@ AJM_SEGMENTS_STATIC = 0x40000
 AJM_SEGMENTS_DYNAMIC = 0x80000
 AJM_DEBUG_POISON = 0x100000
 AJM_SHARD_COLOCATED = 0x200000
+AJM_VALUE_STREAM = 0x400000
 AJM_MAX_RANKS = 8
 AJM_SHARD_BLOB_BYTES = 1024
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 
 def AJM_JBLOCK_SIZE(bs: int) -> int:
@@ -85,7 +86,8 @@ class ajm_info_t(ctypes.Structure):
                 ("mode", ctypes.c_int32), ("l2_mode", ctypes.c_int32),
                 ("launches_per_solve", ctypes.c_int32), ("col_bytes", ctypes.c_int32),
                 ("seg_nnz", ctypes.c_int64), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
-                ("halo", ctypes.c_int64), ("send", ctypes.c_int64), ("group_rows", ctypes.c_int64)]
+                ("halo", ctypes.c_int64), ("send", ctypes.c_int64), ("group_rows", ctypes.c_int64),
+                ("val_bytes", ctypes.c_int32), ("pad_", ctypes.c_int32)]
 
 
 class ajm_spectrum_t(ctypes.Structure):
@@ -277,7 +279,7 @@ class Solver:
 
     def __init__(self, n, row_ptr, col, val, b, dmode="jdiag", d=None, validate_symmetry=False,
                  loop="graph", stream=None, jblock=None, int32_columns=False, global_tables=False,
-                 segments="auto", debug_poison=False):
+                 segments="auto", debug_poison=False, value_stream=False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2407_03272_b200 needs a CUDA device (no CPU fallback)")
@@ -287,6 +289,7 @@ class Solver:
         flags |= (AJM_INT32_COLUMNS if int32_columns else 0) | (AJM_GLOBAL_TABLES if global_tables else 0)
         flags |= {"auto": 0, "static": AJM_SEGMENTS_STATIC, "dynamic": AJM_SEGMENTS_DYNAMIC}[segments]
         flags |= AJM_DEBUG_POISON if debug_poison else 0
+        flags |= AJM_VALUE_STREAM if value_stream else 0
         self.jblock = None
         if jblock is not None:  # eq-J-blkdiag with bs-row blocks (AJM_D_JBLOCK)
             dmode = "jblock"
@@ -509,7 +512,7 @@ class ShardGroup(_ShardHandles):
         create_all(flags)
         # one launch runs every rank: they must share the column encoding (byte codes need every
         # rank's offsets to fit one table each -- a rank whose do not keeps int32 columns)
-        if len({self._info(h)["col_bytes"] for h in self.handles}) > 1:
+        if len({(self._info(h)["col_bytes"], self._info(h)["val_bytes"]) for h in self.handles}) > 1:
             self.close()
             create_all(flags | AJM_INT32_COLUMNS)
         blobs = [_shard_export(h) for h in self.handles]

@@ -68,6 +68,12 @@ SolveFn col8_fn(bool seg, int stages) {
         default: return seg ? ajm_solve_kernel<4, true, false, 0, false, true> : ajm_solve_kernel<4, false, false, 0, false, true>;
     }
 }
+// pair-coded entries (1 byte per entry, no values streamed; 2 KB stages): ring depth 4 or 8,
+// with or without the segment phases
+SolveFn pair_fn(bool seg, int stages) {
+    if (stages == 8) return seg ? ajm_solve_kernel<8, true, false, 0, false, 2> : ajm_solve_kernel<8, false, false, 0, false, 2>;
+    return seg ? ajm_solve_kernel<4, true, false, 0, false, 2> : ajm_solve_kernel<4, false, false, 0, false, 2>;
+}
 // block-diagonal J (natural order, no segments), cooperative grid or single cluster
 SolveFn jblock_fn(int bs, bool cluster) {
     if (cluster)
@@ -82,7 +88,11 @@ SolveFn cluster_fn(bool seg) { return seg ? ajm_solve_kernel<4, true, true> : aj
 // The Lanczos twin (kLz) of a handle's solver kernel: same template arguments, same ring and shared
 // memory, Lanczos epilogue (ajm_estimate_spectrum).  Instantiated for the layouts create picks by
 // default; nullptr for block-J handles and experiment-only ring depths.
-SolveFn lanczos_fn(bool seg, bool cluster, bool gmeta, int col_bytes, int stages) {
+SolveFn lanczos_fn(bool seg, bool cluster, bool gmeta, int col_bytes, int stages, bool pair) {
+    if (pair) {
+        if (stages == 8) return seg ? ajm_solve_kernel<8, true, false, 0, false, 2, true> : ajm_solve_kernel<8, false, false, 0, false, 2, true>;
+        return seg ? ajm_solve_kernel<4, true, false, 0, false, 2, true> : ajm_solve_kernel<4, false, false, 0, false, 2, true>;
+    }
     if (cluster) return seg ? ajm_solve_kernel<4, true, true, 0, false, false, true> : ajm_solve_kernel<4, false, true, 0, false, false, true>;
     if (gmeta) return seg ? ajm_solve_kernel<4, true, false, 0, true, false, true> : ajm_solve_kernel<4, false, false, 0, true, false, true>;
     if (col_bytes == 1) {
@@ -99,7 +109,8 @@ SolveFn lanczos_fn(bool seg, bool cluster, bool gmeta, int col_bytes, int stages
 // 4 / 5, with or without the segment phases -- the layouts create picks for shards; emu: the
 // emulated-group kernel (kShard = 2) instead of the per-process one (kShard = 1)
 template <int kSh>
-SolveFn shard_fn_t(int col_bytes, bool seg, int stages) {
+SolveFn shard_fn_t(int col_bytes, bool seg, int stages, bool pair) {
+    if (pair) return ajm_solve_kernel<4, false, false, 0, false, 2, false, kSh>;  // (no segments)
     if (col_bytes == 1) {
         if (stages == 5) return seg ? ajm_solve_kernel<5, true, false, 0, false, true, false, kSh> : ajm_solve_kernel<5, false, false, 0, false, true, false, kSh>;
         return seg ? ajm_solve_kernel<4, true, false, 0, false, true, false, kSh> : ajm_solve_kernel<4, false, false, 0, false, true, false, kSh>;
@@ -107,8 +118,8 @@ SolveFn shard_fn_t(int col_bytes, bool seg, int stages) {
     if (stages == 4) return seg ? ajm_solve_kernel<4, true, false, 0, false, false, false, kSh> : ajm_solve_kernel<4, false, false, 0, false, false, false, kSh>;
     return seg ? ajm_solve_kernel<3, true, false, 0, false, false, false, kSh> : ajm_solve_kernel<3, false, false, 0, false, false, false, kSh>;
 }
-SolveFn shard_fn(int col_bytes, bool seg, int stages, bool emu) {
-    return emu ? shard_fn_t<2>(col_bytes, seg, stages) : shard_fn_t<1>(col_bytes, seg, stages);
+SolveFn shard_fn(int col_bytes, bool seg, int stages, bool emu, bool pair) {
+    return emu ? shard_fn_t<2>(col_bytes, seg, stages, pair) : shard_fn_t<1>(col_bytes, seg, stages, pair);
 }
 
 // Threads per CTA of a solver kernel: 8 consumer warps + the TMA producer warp (kProd, layouts
@@ -220,7 +231,9 @@ struct ajm_ctx {
     double* Jinv = nullptr;     // rows of their inverses, per SELL chunk [bs][32]
     uint8_t* scode = nullptr;   // byte-coded SELL columns (col = row + ctab[code]), replaces scol
     int* ctab = nullptr;        // [AJM_CTAB] ascending column offsets of the codes
+    long long* ptab = nullptr;  // [AJM_CTAB][2] pair-coded entries {value bits, offset}
     int col_bytes = 4;          // bytes per streamed column index: 4 (int32) or 1 (byte code)
+    int pair = 0;               // 1: the byte code carries the value too (no values streamed)
     int ring_stages = 4;        // TMA ring depth of the chosen solver kernel
     bool seg_fn = true;         // the chosen plain/col8 ring kernel has the segment phases
     bool ring_fn = false;       // h->fn is a ring_fn/col8_fn kernel (ring depth selectable)
@@ -352,7 +365,7 @@ void free_all(ajm_ctx* h) {
                     h->seg_split, h->seg_part, h->split_row, h->split_seg0, h->split_cnt,
                     h->cta_split, h->owner_split, h->unit_c0, h->cta_seg, h->seg_list, h->cta_unit, h->partials, h->ctrl,
                     h->hist, h->scratch, h->err, h->ts, h->perm_fwd, h->perm_inv, h->b_in, h->Jblk, h->Jinv, h->seg_order, h->seg_grp,
-                    h->g_uc0, h->g_coff, h->g_ubase, h->g_cbase, h->scode, h->ctab, h->seg_meta, h->lzw, h->grp};
+                    h->g_uc0, h->g_coff, h->g_ubase, h->g_cbase, h->scode, h->ctab, h->seg_meta, h->lzw, h->grp, h->ptab};
     for (void* p : ptrs) dfree(p);
     dfree(h->snd_cta);
     dfree(h->snd);
@@ -435,6 +448,7 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.seg_meta = reinterpret_cast<const int4*>(h->seg_meta);
     p.grp = h->grp;
     p.ctab = h->ctab;
+    p.ptab = h->ptab;
     p.sh = AjmShard{};
     p.sh.nranks = 1;
     if (h->shard) {
@@ -1116,7 +1130,14 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
             std::vector<int64_t> cstart((size_t)G + 1, h->nchunks);
             int64_t i = 0;
             double pref = 0.0, cumseg = 0.0;
+            // a small grid with a chunk per consumer warp (the single-cluster kernels): exactly
+            // AJM_WARPS consecutive chunks per CTA -- the pass lasts as long as its slowest warp
+            const bool one_per_warp = h->nseg == 0 && G <= 16 && (int64_t)G * AJM_WARPS >= h->nchunks;
             for (int cc = 0; cc < G; ++cc) {
+                if (one_per_warp) {
+                    cstart[(size_t)cc] = std::min<int64_t>((int64_t)cc * AJM_WARPS, h->nchunks);
+                    continue;
+                }
                 cstart[(size_t)cc] = i;
                 cumseg += segload[(size_t)cc];
                 if (cc == G - 1) break;
@@ -1252,14 +1273,18 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
         // registers); AJM_NO_RESIDENT=1 keeps the kCluster ring kernel (experiments)
         if (h->cluster && !h->relabel && h->nseg == 0 && !h->jbs && !getenv("AJM_NO_RESIDENT")) {
             int64_t max_el = 0;
+            int max_chk = 0;  // the kernel runs one chunk per warp: every CTA needs <= AJM_WARPS
             for (int cc = 0; cc < G; ++cc) {
                 const int ua = cta_unit_h[(size_t)cc], ub = cta_unit_h[(size_t)cc + 1];
-                if (ub > ua) max_el = std::max<int64_t>(max_el, choff[(size_t)unit_c0_h[(size_t)ub]] - choff[(size_t)unit_c0_h[(size_t)ua]]);
+                if (ub > ua) {
+                    max_el = std::max<int64_t>(max_el, choff[(size_t)unit_c0_h[(size_t)ub]] - choff[(size_t)unit_c0_h[(size_t)ua]]);
+                    max_chk = std::max(max_chk, unit_c0_h[(size_t)ub] - unit_c0_h[(size_t)ua]);
+                }
             }
             const size_t rdyn = (size_t)2 * 8 * (size_t)((n + 31) / 32 * 32) + (size_t)max_el * 12 + 64;
             const SolveFn rf = ajm_resident_kernel;
             std::lock_guard<std::mutex> lock(g_attr_mu);
-            if (rdyn <= (size_t)smem_optin &&
+            if (rdyn <= (size_t)smem_optin && max_chk <= AJM_WARPS &&
                 cudaFuncSetAttribute((const void*)rf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rdyn) == cudaSuccess) {
                 if (G > 8) cudaFuncSetAttribute((const void*)rf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
                 cudaLaunchConfig_t qc = {};
@@ -1641,6 +1666,88 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
         CC(cudaFreeAsync(tmp, st));
     }
     mark("col8", st);
+    // pair-coded entries: when the byte-coded layout's (offset, value) pairs take at
+    // most AJM_CTAB distinct values (constant-coefficient stencils: 7 / 27 / a few boundary
+    // diagonals), the code byte indexes a table of pairs and the values are not streamed at all
+    // (9 -> 1 byte per stored entry); the same values and columns in the same order, so bitwise the
+    // same iterates.  AJM_VALUE_STREAM keeps the values (experiments, tests).
+    if (h->col_bytes == 1 && !(flags & AJM_VALUE_STREAM) && !(sh && h->nseg > 0) && getenv("AJM_NO_PAIR") == nullptr) {
+        const long long ne = (long long)h->sell_elems;
+        unsigned long long* vt = nullptr;
+        CC(dalloc(&vt, AJM_VTAB_HASH + 1, st));
+        CC(cudaMemsetAsync(vt, 0xff, sizeof(unsigned long long) * AJM_VTAB_HASH, st));
+        CC(cudaMemsetAsync(vt + AJM_VTAB_HASH, 0, sizeof(unsigned long long), st));
+        int* vcnt = reinterpret_cast<int*>(vt + AJM_VTAB_HASH);
+        const int gblocks = (int)std::min<long long>((ne + 255) / 256, 148LL * 16);
+        ajm_val_collect_kernel<<<gblocks, 256, 0, st>>>(ne, h->sval, vt, vcnt);
+        CC(cudaGetLastError());
+        std::vector<unsigned long long> vh(AJM_VTAB_HASH + 1);
+        CC(cudaMemcpyAsync(vh.data(), vt, sizeof(unsigned long long) * vh.size(), cudaMemcpyDeviceToHost, st));
+        CC(cudaStreamSynchronize(st));
+        int cnt2[2];
+        std::memcpy(cnt2, &vh[AJM_VTAB_HASH], sizeof(cnt2));
+        if (cnt2[1] == 0 && cnt2[0] <= AJM_CTAB) {
+            std::vector<unsigned long long> vk;
+            for (int i = 0; i < AJM_VTAB_HASH; ++i)
+                if (vh[(size_t)i] != ~0ull) vk.push_back(vh[(size_t)i]);
+            std::sort(vk.begin(), vk.end());
+            const int mv = (int)vk.size();
+            vk.resize(AJM_CTAB, ~0ull);
+            // flags of the present (offset code, value code) pairs
+            uint8_t* fl = nullptr;
+            CC(dalloc(&fl, (size_t)AJM_CTAB * AJM_CTAB, st));
+            CC(cudaMemsetAsync(fl, 0, (size_t)AJM_CTAB * AJM_CTAB, st));
+            CC(cudaMemcpyAsync(vt, vk.data(), sizeof(unsigned long long) * AJM_CTAB, cudaMemcpyHostToDevice, st));
+            ajm_pair_code_kernel<<<gblocks, 256, 0, st>>>(ne, h->sval, vt, mv, h->scode, fl, 0);
+            CC(cudaGetLastError());
+            std::vector<uint8_t> fh((size_t)AJM_CTAB * AJM_CTAB);
+            std::vector<int> ch(AJM_CTAB);
+            CC(cudaMemcpyAsync(fh.data(), fl, fh.size(), cudaMemcpyDeviceToHost, st));
+            CC(cudaMemcpyAsync(ch.data(), h->ctab, sizeof(int) * AJM_CTAB, cudaMemcpyDeviceToHost, st));
+            CC(cudaStreamSynchronize(st));
+            std::vector<long long> pt;
+            std::vector<uint8_t> map((size_t)AJM_CTAB * AJM_CTAB, 0);
+            for (int k = 0; k < AJM_CTAB * AJM_CTAB; ++k)
+                if (fh[(size_t)k]) {
+                    if (pt.size() >= 2 * (size_t)AJM_CTAB) { pt.clear(); break; }
+                    map[(size_t)k] = (uint8_t)(pt.size() / 2);
+                    pt.push_back((long long)vk[(size_t)(k % AJM_CTAB)]);
+                    pt.push_back((long long)ch[(size_t)(k / AJM_CTAB)]);
+                }
+            // more than AJM_CTAB pairs (pt cleared) or none: keep the values streamed
+            if (!pt.empty()) {
+                const char* es = getenv("AJM_PAIR_STAGES");  // (experiments) 4 or 8
+                const int stp = es ? (std::atoi(es) >= 8 ? 8 : 4) : (h->wide_rows ? 8 : 4);
+                SolveFn fp = pair_fn(h->nseg > 0, stp);
+                const size_t dynp = (size_t)stp * AJM_UNIT_EL * 1 + h->meta_bytes;
+                int occp = 0;
+                cudaError_t eo;
+                {
+                    std::lock_guard<std::mutex> lock(g_attr_mu);
+                    eo = fn_occupancy(fp, dynp, 100, &occp, block_threads(h->nseg > 0));
+                }
+                CC(eo);
+                if (occp >= h->ctas_per_sm) {
+                    pt.resize(2 * (size_t)AJM_CTAB, 0);
+                    CC(dalloc(&h->ptab, 2 * (size_t)AJM_CTAB, st));
+                    CC(cudaMemcpyAsync(h->ptab, pt.data(), sizeof(long long) * pt.size(), cudaMemcpyHostToDevice, st));
+                    CC(cudaMemcpyAsync(fl, map.data(), map.size(), cudaMemcpyHostToDevice, st));
+                    ajm_pair_code_kernel<<<gblocks, 256, 0, st>>>(ne, h->sval, vt, mv, h->scode, fl, 1);
+                    CC(cudaGetLastError());
+                    CC(cudaFreeAsync(h->sval, st));
+                    h->sval = nullptr;
+                    h->fn = fp;
+                    h->dyn_smem = dynp;
+                    h->ring_stages = stp;
+                    h->pair = 1;
+                }
+            }
+            CC(cudaStreamSynchronize(st));  // map / pt live until the copies have run
+            CC(cudaFreeAsync(fl, st));
+        }
+        CC(cudaFreeAsync(vt, st));
+    }
+    mark("pair", st);
     // shared-memory carve-out: the smallest that keeps ctas_per_sm CTAs resident, so the rest of
     // the SM's 256 KB stays L1 for the gathers; AJM_CARVEOUT=<pct> overrides
     {
@@ -1687,10 +1794,10 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
         h->col = nullptr;
         h->val = nullptr;
     }
-    if (!h->jbs && !sh) h->fn_lz = lanczos_fn(h->nseg > 0, h->cluster != 0, h->gmeta != 0, h->col_bytes, h->ring_stages);
+    if (!h->jbs && !sh) h->fn_lz = lanczos_fn(h->nseg > 0, h->cluster != 0, h->gmeta != 0, h->col_bytes, h->ring_stages, h->pair != 0);
     if (sh) {
         // the rank's kernel: the same layout class with the halo exchange compiled in
-        h->fn = shard_fn(h->col_bytes, h->nseg > 0, h->ring_stages, sh->colocated != 0);
+        h->fn = shard_fn(h->col_bytes, h->nseg > 0, h->ring_stages, sh->colocated != 0, h->pair != 0);
         {
             std::lock_guard<std::mutex> lock(g_attr_mu);
             int occ = 0;
@@ -2265,7 +2372,7 @@ ajm_status_t ajm_group_solve(const ajm_handle_t* hs, int32_t nranks, const doubl
         ajm_ctx* h = hs[r];
         if (!h || !h->shard || !h->colocated || h->rank != r || h->nranks != nranks)
             return fail(h0, AJM_ERR_INVALID_ARG, "handle %d is not rank %d of an AJM_SHARD_COLOCATED group of %d", r, r, nranks);
-        if (h->col_bytes != h0->col_bytes || h->grid != h0->grid)
+        if (h->col_bytes != h0->col_bytes || h->pair != h0->pair || h->grid != h0->grid)
             return fail(h0, AJM_ERR_UNSUPPORTED, "ranks 0 and %d chose different column encodings / grids: one launch "
                         "cannot run both (create the group with AJM_INT32_COLUMNS)", r);
         ajm_status_t s = solve_check(h, x_out, tol, maxit, policy, restart_iters, restart_cap);
@@ -2281,10 +2388,11 @@ ajm_status_t ajm_group_solve(const ajm_handle_t* hs, int32_t nranks, const doubl
         stages = std::max(stages, hs[r]->ring_stages);
         meta = std::max(meta, hs[r]->meta_bytes);
     }
-    if (h0->col_bytes == 1) stages = std::max(4, std::min(5, stages));
+    if (h0->pair) stages = 4;
+    else if (h0->col_bytes == 1) stages = std::max(4, std::min(5, stages));
     else stages = std::max(3, std::min(4, stages));
-    const SolveFn gfn = shard_fn(h0->col_bytes, any_seg, stages, true);
-    const size_t gdyn = (size_t)stages * AJM_UNIT_EL * (h0->col_bytes == 1 ? 9 : 12) + meta;
+    const SolveFn gfn = shard_fn(h0->col_bytes, any_seg, stages, true, h0->pair != 0);
+    const size_t gdyn = (size_t)stages * AJM_UNIT_EL * (h0->pair ? 1 : h0->col_bytes == 1 ? 9 : 12) + meta;
     cudaStream_t st = (cudaStream_t)cuda_stream;
     for (int r = 0; r < nranks; ++r) {
         ajm_ctx* h = hs[r];
@@ -2535,6 +2643,7 @@ ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info) {
     info->l2_mode = h->l2_mode;
     info->launches_per_solve = (int32_t)(1 + (h->prime_bytes ? 1 : 0) + std::max<int64_t>(h->last_launches, 1));
     info->col_bytes = h->col_bytes;
+    info->val_bytes = h->pair ? 0 : 8;
     info->seg_nnz = h->seg_nnz;
     info->rank = h->rank;
     info->nranks = h->nranks;

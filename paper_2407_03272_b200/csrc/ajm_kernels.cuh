@@ -166,6 +166,8 @@ struct AjmPass {
     int jbs;                                 // AJM_D_JBLOCK block size (0: diagonal D)
     const uint8_t* __restrict__ scode;       // (kCol8) SELL column codes: col = row + ctab[code]
     const int* __restrict__ ctab;            // (kCol8) [256] distinct offsets col - row, ascending
+    const long long* __restrict__ ptab;      // (kCol8 == 2) [256][2] pair-coded entries: {bits of Q_ij,
+                                             //   offset col - row}; the code alone is streamed
     const int4* __restrict__ seg_meta;       // static plan: {row, k0, k1, split} of seg_list[k]
                                              // (split -2: sub-warp group `row`, k1 its nonzeros)
     const int4* __restrict__ grp;            // sub-warp groups: {rows}, {k0}, {k1} (3 int4 each)
@@ -849,6 +851,52 @@ __device__ __forceinline__ double ajm_chunk_dot8s(uint32_t sva, uint32_t sca, in
     return s;
 }
 
+// Pair-coded entries (kCol8 == 2): element k of the lane's row is (Q_ij, j - row) =
+// ptab[code[32 k]], one 16-byte table entry read by one ld.shared.v2 -- the same values and columns
+// in the same ascending order as ajm_chunk_dot8s / ajm_chunk_dots: bitwise the same q.
+__device__ __forceinline__ void ajm_lds_pair(uint32_t a, double& v, int& off) {
+    long long o;
+    asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=d"(v), "=l"(o) : "r"(a));
+    off = (int)o;
+}
+template <int W>  // W <= 8 entries per row, known at compile time
+__device__ __forceinline__ double ajm_chunk_dotp_w(uint32_t sca, const double* xb, uint32_t taba) {
+    int cc[W];
+    double vv[W], xg[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) cc[k] = (int)ajm_lds_u8(sca + 32u * k);
+#pragma unroll
+    for (int k = 0; k < W; ++k) ajm_lds_pair(taba + 16u * (uint32_t)cc[k], vv[k], cc[k]);
+#pragma unroll
+    for (int k = 0; k < W; ++k) xg[k] = ajm_ld(xb + cc[k]);
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < W; ++k) s += vv[k] * xg[k];  // ascending column order
+    return s;
+}
+__device__ __forceinline__ double ajm_chunk_dotp(uint32_t sca, int w, const double* xb, uint32_t taba) {
+    switch (w) {
+        case 7: return ajm_chunk_dotp_w<7>(sca, xb, taba);
+        case 5: return ajm_chunk_dotp_w<5>(sca, xb, taba);
+        default: break;
+    }
+    double s = 0.0;
+    for (int k0 = 0; k0 < w; k0 += 8) {
+        int cc[8];
+        double vv[8], xg[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) cc[j] = (k0 + j < w) ? (int)ajm_lds_u8(sca + 32u * (k0 + j)) : 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ajm_lds_pair(taba + 16u * (uint32_t)cc[j], vv[j], cc[j]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) xg[j] = (k0 + j < w) ? ajm_ld(xb + cc[j]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (k0 + j < w) s += vv[j] * xg[j];  // ascending column order
+    }
+    return s;
+}
+
 // int32 columns, the same treatment: 32-bit shared-window addresses, every column and gather of a
 // batch of 8 issued before the batch's first product (bitwise ajm_chunk_dot)
 __device__ __forceinline__ double ajm_chunk_dots(uint32_t sva, uint32_t sca, int w, const double* xc) {
@@ -916,7 +964,11 @@ __device__ __forceinline__ double ajm_ld_cluster(const double* local, unsigned r
 // kGMeta = true: the per-CTA unit/chunk tables are read from global memory (precomputed per CTA
 //   on the host) instead of being staged in shared memory -- for layouts whose tables do not fit
 //   next to the ring (hundreds of millions of rows).
-// kCol8 = true: byte-coded SELL columns (col = row + ctab[code]).
+// kCol8 = 1: byte-coded SELL columns (col = row + ctab[code]).
+// kCol8 = 2: pair-coded SELL entries: one byte per entry indexes a table of (value, column offset)
+//   pairs (when the SELL entries hold <= 256 distinct pairs, e.g. constant-coefficient stencils);
+//   the values are not streamed at all (1 byte per entry instead of 9).  Same values, columns and
+//   order: bitwise the iterates of kCol8 = 1 / int32 columns.
 // kLz = true: the Lanczos pass of ajm_estimate_spectrum (same SpMV, epilogue ajm_row_lanczos,
 //   control ajm_lanczos_control) instead of the AJM pass.
 // kShard != 0: one rank of a row-block sharded solve (NEXT-2; AjmShard above): before the loop a
@@ -934,7 +986,7 @@ __device__ __forceinline__ double ajm_ld_cluster(const double* local, unsigned r
 //            8 warps fit 128 registers per thread -- what the segment phases (the long-row dot, the
 //            sub-warp groups, the epilogue operand prefetch) need to run without spills.
 template <int kStages, bool kSeg = true, bool kCluster = false, int kJB = 0, bool kGMeta = false,
-          bool kCol8 = false, bool kLz = false, int kShard = 0, bool kProd = !kSeg>
+          int kCol8 = 0, bool kLz = false, int kShard = 0, bool kProd = !kSeg>
 __global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
     static_assert(!kShard || (!kCluster && !kJB && !kGMeta && !kLz), "sharded solve: plain ring variants only");
     // (kShard = 2) this CTA's rank's pass struct, in shared memory (the launch serves all ranks)
@@ -967,20 +1019,21 @@ __global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
     __shared__ double s_part[2][AJM_NPART];    // (kCluster) this CTA's partials by the parity of the
                                                // launch's pass count (the barrier is fresh per launch)
     __shared__ int s_to;
-    __shared__ int s_ctab[kCol8 ? AJM_CTAB : 1];  // (kCol8) column offsets of the byte codes
+    __shared__ int s_ctab[kCol8 == 1 ? AJM_CTAB : 1];  // (kCol8 1) column offsets of the byte codes
+    __shared__ __align__(16) long long s_ptab[kCol8 == 2 ? 2 * AJM_CTAB : 2];  // (kCol8 2) {value, offset}
 
     AjmCtrl* c = p.ctrl;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int u0 = p.cta_unit[bid], u1 = p.cta_unit[bid + 1];
     const int nunits = u1 - u0;
     constexpr bool jblk = (kJB != 0);
-    // stage s: val[UNIT_EL] f64 | col[UNIT_EL] i32 (kCol8: code[UNIT_EL] u8)
-    constexpr unsigned el_bytes = kCol8 ? 9u : 12u;
+    // stage s: val[UNIT_EL] f64 | col[UNIT_EL] i32 (kCol8 1: code[UNIT_EL] u8; kCol8 2: code only)
+    constexpr unsigned el_bytes = kCol8 == 2 ? 1u : (kCol8 ? 9u : 12u);
     constexpr size_t stage_bytes = (size_t)AJM_UNIT_EL * el_bytes;
     static_assert(!kCol8 || (!jblk && !kCluster && !kGMeta), "byte-coded columns: plain ring variant only");
     auto st_val = [&](int k) { return reinterpret_cast<double*>(s_dyn + (size_t)k * stage_bytes); };
     auto st_col = [&](int k) { return reinterpret_cast<int*>(s_dyn + (size_t)k * stage_bytes + (size_t)AJM_UNIT_EL * 8); };
-    auto st_code = [&](int k) { return s_dyn + (size_t)k * stage_bytes + (size_t)AJM_UNIT_EL * 8; };
+    auto st_code = [&](int k) { return s_dyn + (size_t)k * stage_bytes + (kCol8 == 2 ? (size_t)0 : (size_t)AJM_UNIT_EL * 8); };
     // static per-CTA SELL metadata, loaded once: unit -> first chunk, chunk -> element offset
     // (relative to this CTA's first chunk / element), so the pass never chases global pointers
     int* s_uc0 = kGMeta ? const_cast<int*>(p.g_uc0 + p.g_ubase[bid])
@@ -993,8 +1046,10 @@ __global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
         for (int i = tid; i <= nunits; i += blockDim.x) s_uc0[i] = p.unit_c0[u0 + i] - cfirst;
         for (int i = tid; i <= nchk; i += blockDim.x) s_coff[i] = (int)(p.chunk_off[cfirst + i] - efirst);
     }
-    if (kCol8)
+    if (kCol8 == 1)
         for (int i = tid; i < AJM_CTAB; i += blockDim.x) s_ctab[i] = p.ctab[i];
+    if (kCol8 == 2)
+        for (int i = tid; i < 2 * AJM_CTAB; i += blockDim.x) s_ptab[i] = p.ptab[i];
     if (tid == 0) {
         s_st = c->s;
         for (int k = 0; k < kStages; ++k) {
@@ -1029,7 +1084,7 @@ __global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
         const unsigned ne = (unsigned)(e1 - e0);
         const uint64_t qpol = ajm_policy(p.l2_mode >= 1 ? 1 : 0);
         ajm_mbar_expect_tx(&s_full[stage], ne * el_bytes);
-        ajm_bulk_g2s(st_val(stage), p.sval + efirst + e0, ne * 8u, &s_full[stage], qpol);
+        if (kCol8 != 2) ajm_bulk_g2s(st_val(stage), p.sval + efirst + e0, ne * 8u, &s_full[stage], qpol);
         if (kCol8)
             ajm_bulk_g2s(st_code(stage), p.scode + efirst + e0, ne, &s_full[stage], qpol);
         else
@@ -1261,7 +1316,9 @@ __global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
                     }
                     ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);
                     const int off = (e0 - s_coff[s_uc0[uu]]) + lane;
-                    const double q = kCol8 ? (AJM_DOT8_MODE == 0
+                    const double q = kCol8 == 2 ? ajm_chunk_dotp(ajm_smem(st_code(stage) + off), w,
+                                                                 xc + (row >= 0 ? row : 0), ajm_smem(s_ptab))
+                                   : kCol8 ? (AJM_DOT8_MODE == 0
                                                   ? ajm_chunk_dot8(st_val(stage) + off, st_code(stage) + off, w,
                                                                    xc + (row >= 0 ? row : 0), s_ctab)
                                                   : ajm_chunk_dot8s(ajm_smem(st_val(stage) + off), ajm_smem(st_code(stage) + off), w,
@@ -1460,12 +1517,12 @@ __global__ void __launch_bounds__(AJM_BLOCK, 1) ajm_resident_kernel(AjmPass p) {
     extern __shared__ __align__(128) unsigned char s_dyn[];
     __shared__ double s_red[AJM_WARPS][AJM_NPART];
     __shared__ double s_tot[AJM_NPART];
-    __shared__ double s_part[2][AJM_NPART];
-    __shared__ double s_res;
+    // every CTA's partials, pushed by their owners (st.shared::cluster) before the barrier arrival,
+    // by pass parity: after the barrier the reduction reads only local shared memory
+    __shared__ double s_pall[2][16][AJM_NPART];
     __shared__ AjmState s_st;
     __shared__ __align__(8) uint64_t s_cbar;
     __shared__ __align__(8) uint64_t s_cexit;
-    __shared__ int s_to;
     AjmCtrl* c = p.ctrl;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int bid = (int)blockIdx.x;
@@ -1562,42 +1619,42 @@ __global__ void __launch_bounds__(AJM_BLOCK, 1) ajm_resident_kernel(AjmPass p) {
                 asm volatile("{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\tst.shared::cluster.f64 [ra], %2;\n\t}"
                              ::"r"(la), "r"(rk), "d"(xn) : "memory");
         }
-        ajm_block_reduce(acc, s_red);
-        double an_c = 0.0, beta_c = 0.0;
+        ajm_block_reduce(acc, s_red);  // (lane 0 of warp 0 holds the CTA's sums)
         if (warp == 0) {
+            // lane r pushes this CTA's five partials into CTA r's s_pall and arrives (release,
+            // cluster scope) on CTA r's barrier: that orders the partials and this CTA's replica
+            // stores (ordered before by the CTA barrier in ajm_block_reduce)
+            const double pr[AJM_NPART] = {__shfl_sync(0xffffffffu, acc.rr, 0), __shfl_sync(0xffffffffu, acc.xq, 0),
+                                          __shfl_sync(0xffffffffu, acc.bx, 0), __shfl_sync(0xffffffffu, acc.d, 0),
+                                          __shfl_sync(0xffffffffu, acc.dabs, 0)};
+            if (lane < (int)G) {
+                const uint32_t la = ajm_smem(&s_pall[pass & 1][bid][0]);
+#pragma unroll
+                for (int k = 0; k < AJM_NPART; ++k)
+                    asm volatile("{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\tst.shared::cluster.f64 [ra], %2;\n\t}"
+                                 ::"r"(la + 8u * k), "r"((unsigned)lane), "d"(pr[k]) : "memory");
+                ajm_cluster_arrive(&s_cbar, (unsigned)lane);
+            }
+            double an_c = 0.0, beta_c = 0.0;
+            int to = 0;
             if (lane == 0) {
-                double* sp = s_part[pass & 1];
-                sp[0] = acc.rr;
-                sp[1] = acc.xq;
-                sp[2] = acc.bx;
-                sp[3] = acc.d;
-                sp[4] = acc.dabs;
+                const double a = s_st.alpha;
+                an_c = (1.0 + sqrt(1.0 + 4.0 * a * a)) / 2.0;
+                beta_c = s_st.momentum ? (a - 1.0) / an_c : 0.0;
+                to = ajm_cluster_wait(&s_cbar, (unsigned)(pass & 1), &c->timeout_flag) ? 1 : 0;
             }
             __syncwarp();
-            // lane r arrives (release, cluster scope) on CTA r's barrier: this CTA's replica stores
-            // (ordered by the CTA barrier in ajm_block_reduce) and its partials
-            if (lane < (int)G) ajm_cluster_arrive(&s_cbar, (unsigned)lane);
-        }
-        if (tid == 0) {
-            const double a = s_st.alpha;
-            an_c = (1.0 + sqrt(1.0 + 4.0 * a * a)) / 2.0;
-            beta_c = s_st.momentum ? (a - 1.0) / an_c : 0.0;
-            s_to = ajm_cluster_wait(&s_cbar, (unsigned)(pass & 1), &c->timeout_flag) ? 1 : 0;
-        }
-        ajm_csync();
-        if (warp < AJM_NPART) {  // lane l holds CTA l's record: the kCluster path's order
-            double v = 0.0;
-            if (lane < (int)G) v = ajm_ld_cluster(&s_part[pass & 1][warp], (unsigned)lane);
-            v = ajm_warp_sum(v);
-            if (lane == 0) s_tot[warp] = v;
-            if (warp == 0 && lane == 0) s_res = sqrt(v) / s_st.nb;
-        }
-        ajm_csync();
-        if (tid == 0) {
-            AjmState ls = s_st;
-            ajm_control_step(ls, s_tot, c, bid == 0, an_c, beta_c, s_res);
-            s_st = ls;
-            if (s_to) s_st.done = 1;
+            // the five totals: lane l holds CTA l's record, the same xor tree per component as the
+            // kCluster path's warp-per-component reduction (bitwise the same totals)
+            double tot[AJM_NPART];
+#pragma unroll
+            for (int k = 0; k < AJM_NPART; ++k) tot[k] = ajm_warp_sum(lane < (int)G ? s_pall[pass & 1][lane][k] : 0.0);
+            if (lane == 0) {
+                AjmState ls = s_st;
+                ajm_control_step(ls, tot, c, bid == 0, an_c, beta_c, sqrt(tot[0]) / ls.nb);
+                s_st = ls;
+                if (to) s_st.done = 1;
+            }
         }
         ajm_csync();
         if (!s_st.done) {  // the rotation of the buffers, in registers
@@ -1857,6 +1914,59 @@ __global__ void ajm_coloff_encode_kernel(int nslots_padded, int n_sell, const lo
             else hi = mid;
         }
         code[e] = (uint8_t)lo;
+    }
+}
+
+// Pair-coded entries, create time, after the byte-coded columns: (1) the distinct
+// values (bit patterns) of the SELL entries go into a hash set of AJM_VTAB_HASH 64-bit keys (all
+// ones = empty: a NaN, which validation excludes; cnt[0] distinct keys, cnt[1] set on overflow of
+// AJM_CTAB values or of a probe sequence); (2) every present (offset code, value code) pair is
+// flagged in a 256 x 256 byte map (value code = index in the ascending bit-pattern table);
+// (3) each entry's byte becomes the index of its pair in the host-built pair table.
+#define AJM_VTAB_HASH 4096
+__global__ void ajm_val_collect_kernel(long long ne, const double* __restrict__ sval, unsigned long long* tab,
+                                       int* cnt) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (long long)gridDim.x * blockDim.x) {
+        if (__ldcg(cnt + 1)) return;
+        const unsigned long long v = (unsigned long long)__double_as_longlong(sval[e]);
+        const unsigned same = __match_any_sync(__activemask(), v);
+        if ((threadIdx.x & 31) != __ffs(same) - 1) continue;
+        unsigned hsh = (unsigned)((v * 0x9E3779B97F4A7C15ull) >> 52);  // 12 bits: AJM_VTAB_HASH slots
+        bool ok = false;
+        for (int pr = 0; pr < 64 && !ok; ++pr, hsh = (hsh + 1) & (AJM_VTAB_HASH - 1)) {
+            unsigned long long k = __ldcg(tab + hsh);
+            if (k == ~0ull) {
+                k = atomicCAS(tab + hsh, ~0ull, v);
+                if (k == ~0ull) {
+                    if (atomicAdd(cnt, 1) >= AJM_CTAB) atomicExch(cnt + 1, 1);
+                    ok = true;
+                }
+            }
+            if (k == v) ok = true;
+        }
+        if (!ok) atomicExch(cnt + 1, 1);
+    }
+}
+__device__ __forceinline__ int ajm_vcode(const unsigned long long* t, unsigned long long v) {
+    int lo = 0, hi = AJM_CTAB;  // first index with t[idx] >= v (present by construction)
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (t[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+// mode 0: flag[code * 256 + vcode] = 1; mode 1: code = map[code * 256 + vcode]
+__global__ void ajm_pair_code_kernel(long long ne, const double* __restrict__ sval, const unsigned long long* vtab,
+                                     int m, uint8_t* __restrict__ code, uint8_t* __restrict__ flag_or_map, int mode) {
+    __shared__ unsigned long long t[AJM_CTAB];
+    for (int i = threadIdx.x; i < AJM_CTAB; i += blockDim.x) t[i] = i < m ? vtab[i] : ~0ull;
+    __syncthreads();
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (long long)gridDim.x * blockDim.x) {
+        const int vc = ajm_vcode(t, (unsigned long long)__double_as_longlong(sval[e]));
+        const int k = (int)code[e] * AJM_CTAB + vc;
+        if (mode == 0) flag_or_map[k] = 1;
+        else code[e] = flag_or_map[k];
     }
 }
 

@@ -285,7 +285,21 @@ def _banded_offsets(nd, R=2048, regions=4, seed=0):
     return synth._laplacian_from_edges(R * regions, u, v, w, shift=1e-2)
 
 
-@pytest.mark.parametrize("case", ["cfg2", "ragged17", "band255", "band257"])
+def _stencil_with_values(edge, nvals, seed=3):
+    """3D 7-point Dirichlet Laplacian whose off-diagonal couplings take `nvals` distinct values
+    (symmetric, diagonally dominant: SPD), so the (offset, value) pairs of its entries number about
+    6 nvals + the distinct diagonals."""
+    Q0 = synth.poisson3d(edge)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    levels = rng.uniform(0.1, 1.0, nvals)
+    n = Q0.n
+    rows = np.repeat(np.arange(n), np.diff(Q0.row_ptr))
+    u, v = rows[Q0.col > rows], Q0.col[Q0.col > rows]
+    w = levels[rng.integers(0, nvals, u.size)]  # one value per edge
+    return synth._laplacian_from_edges(n, u, v, w, shift=1e-2)
+
+
+@pytest.mark.parametrize("case", ["cfg2", "ragged17", "band255", "band257", "vals2", "vals300"])
 def test_byte_coded_columns(case):
     """Layouts whose column offsets col - row take <= 256 values stream byte codes into an offset
     table instead of int32 columns.  Same columns, same summation order: the
@@ -296,15 +310,27 @@ def test_byte_coded_columns(case):
         p = synth.config_problem(2, 0.25)
     elif case == "ragged17":  # n = 4913: a ragged last chunk (tail slots), > 128 chunks (no cluster)
         p = synth.make_problem("p3d17", synth.poisson3d(17), 4)
+    elif case.startswith("vals"):  # a 7-point stencil with 2 / 300 distinct coupling values
+        p = synth.make_problem(case, _stencil_with_values(24, int(case[4:])), 6)
     else:
         p = synth.make_problem(case, _banded_offsets(127 if case == "band255" else 128), 5)
     a = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True)
     assert a.info["col_bytes"] == (4 if case == "band257" else 1), a.info
     assert a.info["sigma"] == 1
+    # pair-coded entries (values not streamed) exactly when the (offset, value) pairs number <= 256
+    # (the banded cases' random weights do not, nor do 300 coupling levels; 2 levels do)
+    pairs = case in ("cfg2", "ragged17", "vals2")
+    assert a.info["val_bytes"] == (0 if pairs else 8), a.info
     b = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True, int32_columns=True)
-    assert b.info["col_bytes"] == 4
+    assert b.info["col_bytes"] == 4 and b.info["val_bytes"] == 8
     np.testing.assert_array_equal(a.x, b.x)
     np.testing.assert_array_equal(a.res_hist, b.res_hist)
+    np.testing.assert_array_equal(a.f_hist, b.f_hist)
+    if pairs:  # the byte-coded layout with the values streamed: bitwise the same too
+        c = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True, value_stream=True)
+        assert c.info["col_bytes"] == 1 and c.info["val_bytes"] == 8
+        np.testing.assert_array_equal(a.x, c.x)
+        np.testing.assert_array_equal(a.res_hist, c.res_hist)
     o, _ = oracle_matching(p.Q, p.b, a, tol=0.0, maxit=400, restart=True)
     assert max_rel(a.x, o.x) <= PARITY_TOL
 
