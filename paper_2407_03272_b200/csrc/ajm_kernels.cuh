@@ -859,8 +859,10 @@ __device__ __forceinline__ void ajm_lds_pair(uint32_t a, double& v, int& off) {
     asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=d"(v), "=l"(o) : "r"(a));
     off = (int)o;
 }
-template <int W>  // W <= 8 entries per row, known at compile time
-__device__ __forceinline__ double ajm_chunk_dotp_w(uint32_t sca, const double* xb, uint32_t taba) {
+// W consecutive entries k0..k0+W-1 (sca, xb at entry k0) added to s in ascending order: every
+// code, table entry and gather issued before the first product
+template <int W>
+__device__ __forceinline__ void ajm_dotp_part(uint32_t sca, const double* xb, uint32_t taba, double& s) {
     int cc[W];
     double vv[W], xg[W];
 #pragma unroll
@@ -869,30 +871,30 @@ __device__ __forceinline__ double ajm_chunk_dotp_w(uint32_t sca, const double* x
     for (int k = 0; k < W; ++k) ajm_lds_pair(taba + 16u * (uint32_t)cc[k], vv[k], cc[k]);
 #pragma unroll
     for (int k = 0; k < W; ++k) xg[k] = ajm_ld(xb + cc[k]);
-    double s = 0.0;
 #pragma unroll
     for (int k = 0; k < W; ++k) s += vv[k] * xg[k];  // ascending column order
-    return s;
 }
+// full batches of 8, then the remainder unrolled for its exact width -- no predicated slots (the
+// predicated generic batch made the 6-wide boundary chunks of the 7-point stencil ~25 % slower than
+// the 7-wide ones; the cost plan gives their CTAs more of them)
 __device__ __forceinline__ double ajm_chunk_dotp(uint32_t sca, int w, const double* xb, uint32_t taba) {
-    switch (w) {
-        case 7: return ajm_chunk_dotp_w<7>(sca, xb, taba);
-        case 5: return ajm_chunk_dotp_w<5>(sca, xb, taba);
-        default: break;
-    }
     double s = 0.0;
-    for (int k0 = 0; k0 < w; k0 += 8) {
-        int cc[8];
-        double vv[8], xg[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) cc[j] = (k0 + j < w) ? (int)ajm_lds_u8(sca + 32u * (k0 + j)) : 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) ajm_lds_pair(taba + 16u * (uint32_t)cc[j], vv[j], cc[j]);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) xg[j] = (k0 + j < w) ? ajm_ld(xb + cc[j]) : 0.0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (k0 + j < w) s += vv[j] * xg[j];  // ascending column order
+    int k0 = 0;
+    if (w == 7) {  // the 7-point stencil's interior chunks
+        ajm_dotp_part<7>(sca, xb, taba, s);
+        return s;
+    }
+    for (; k0 + 8 <= w; k0 += 8) ajm_dotp_part<8>(sca + 32u * k0, xb, taba, s);
+    const uint32_t sa = sca + 32u * k0;
+    switch (w - k0) {
+        case 1: ajm_dotp_part<1>(sa, xb, taba, s); break;
+        case 2: ajm_dotp_part<2>(sa, xb, taba, s); break;
+        case 3: ajm_dotp_part<3>(sa, xb, taba, s); break;
+        case 4: ajm_dotp_part<4>(sa, xb, taba, s); break;
+        case 5: ajm_dotp_part<5>(sa, xb, taba, s); break;
+        case 6: ajm_dotp_part<6>(sa, xb, taba, s); break;
+        case 7: ajm_dotp_part<7>(sa, xb, taba, s); break;
+        default: break;
     }
     return s;
 }
@@ -1284,6 +1286,12 @@ __global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
         //     per unit per warp)
         {
             int jc = warp;
+            // (kPre) the five row operands of this warp's NEXT chunk of the pass are loaded while the
+            // current chunk's gathers and update run: with the matrix stream down to a byte per entry
+            // the pass is the chain operands -> update, whose DRAM latency this takes off the path
+            constexpr bool kPre = (kCol8 == 2) && !kLz && !jblk;
+            double nb_ = 0.0, nD_ = 1.0, nxt_ = 0.0, nxp_ = 0.0, nqx_ = 0.0;
+            bool pre = false;
             for (int uu = 0; uu < nunits; ++uu) {
                 const int stage = (int)((ucnt + uu) % kStages);
                 const unsigned par = (unsigned)(((ucnt + uu) / kStages) & 1);
@@ -1295,7 +1303,9 @@ __global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
                     const int slot = (cfirst + j) * 32 + lane;
                     const int row = slot < p.n_sell ? slot : -1;  // SELL slot == internal row
                     double bi = 0.0, Di = 1.0, xt = 0.0, xpi = 0.0, qxp = 0.0;
-                    if (row >= 0) {  // operands in flight during the stage wait
+                    if (kPre && pre) {
+                        bi = nb_; Di = nD_; xt = nxt_; xpi = nxp_; qxp = nqx_;
+                    } else if (row >= 0) {  // operands in flight during the stage wait
                         if constexpr (kLz) {  // the row's own entry of the multiplied w
                             xt = ajm_ld(xc + row);
                         } else {
@@ -1304,6 +1314,17 @@ __global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
                             xt = ajm_ld(xc + row);
                             xpi = ajm_ld(xp + row);
                             qxp = ajm_ldp(p.Qxp + row, vpol);
+                        }
+                    }
+                    if constexpr (kPre) {
+                        pre = jc < nchk;
+                        const int nslot = (cfirst + jc) * 32 + lane;
+                        if (pre && nslot < p.n_sell) {
+                            nb_ = ajm_ldp(p.b + nslot, vpol);
+                            nD_ = ajm_ldp(p.D + nslot, vpol);
+                            nxt_ = ajm_ld(xc + nslot);
+                            nxp_ = ajm_ld(xp + nslot);
+                            nqx_ = ajm_ldp(p.Qxp + nslot, vpol);
                         }
                     }
                     constexpr int JV = kJB > 0 ? kJB : 8;

@@ -2,7 +2,7 @@
 
 usage: python tools/env_ab.py CFGS "ENV_A" "ENV_B" [...]   e.g.
        python tools/env_ab.py 2,5 "" "AJM_NO_PAIR=1"
-Each variant: create (the switches are read at create), 1 warm-up + 3 timed solves to the config's
+AB_ROUNDS=<k> sets the rounds (default 2).  Each variant: create (the switches are read at create), 1 warm-up + 3 timed solves to the config's
 tolerance, us/pass from the library's own CUDA-event loop time; the variants alternate twice."""
 import os
 import sys
@@ -42,7 +42,7 @@ def main():
     envs = sys.argv[2:] or [""]
     for cfg in cfgs:
         p = synth.config_problem(cfg)
-        for rnd in range(2):
+        for rnd in range(int(os.environ.get("AB_ROUNDS", "2"))):
             for env in envs:
                 info, r, us = run(p, cfg, env)
                 print(f"cfg{cfg} [{env or 'default'}] round {rnd}: its={r.iterations} us/pass "
