@@ -249,6 +249,7 @@ struct ajm_ctx {
     std::string err_msg;
     // ---- row-block shard (NEXT-2; ajm_shard_create) ----
     int resident = 0;                  // the resident single-cluster kernel (ajm_resident_kernel)
+    std::vector<int> cta_nchk;         // (AJM_TS_ALL diagnostics) SELL chunks planned per CTA
     size_t lz_dyn_smem = 0;            // dynamic shared memory of the Lanczos twin
     int shard = 0;                     // 1: one rank of a sharded group
     int rank = 0, nranks = 1;
@@ -451,6 +452,7 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.ptab = h->ptab;
     p.sh = AjmShard{};
     p.sh.nranks = 1;
+    p.rot = 0;
     if (h->shard) {
         p.sh.rank = h->rank;
         p.sh.nranks = h->nranks;
@@ -796,7 +798,9 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
             for (int64_t r = c * 32; r < r1; ++r) w = std::max<int64_t>(w, rlen(r));
             maxlen = std::max(maxlen, w);
             fo[(size_t)c + 1] = 32 * w;
-            fc[(size_t)c] = 12.0 * 32 * w + 56.0 * (double)(r1 - c * 32) + 64.0;
+            // a chunk costs its row operands plus one gather round trip per batch of 8 entries
+            // (the natural-order cost model below)
+            fc[(size_t)c] = 2600.0 * (double)((w + 7) / 8) + 56.0 * (double)(r1 - c * 32) + 64.0;
         }
         for (int64_t c = 0; c < nch; ++c) fo[(size_t)c + 1] += fo[(size_t)c];
         if (jbs && maxlen > AJM_SELL_MAX)
@@ -955,7 +959,13 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
             }
             choff[(size_t)c + 1] = 32 * w;
             const double busy = std::min<double>(AJM_WARPS, par_stages * std::max<int64_t>(1, AJM_UNIT_EL / (32 * w)));
-            chcost[(size_t)c] = (12.0 * 32 * w + 56.0 * rows + 64.0) * std::pow((double)AJM_WARPS / busy, par_alpha);
+            // natural-order layouts (stencils): a chunk costs its row operands plus one gather round
+            // trip per batch of 8 entries -- measured per chunk (config 2, pair-coded): 6-wide
+            // boundary chunks take as long as 7-wide ones (0.12 us per chunk and CTA; the byte model
+            // gave the boundary CTAs 242 chunks instead of 221 and they finished last), and on config
+            // 5 an 18-wide chunk (3 batches) takes 0.78 of a 27-wide one (4 batches)
+            const double body = h->relabel ? 12.0 * 32 * w : 2600.0 * (double)((w + 7) / 8);
+            chcost[(size_t)c] = (body + 56.0 * rows + 64.0) * std::pow((double)AJM_WARPS / busy, par_alpha);
         }
         for (int64_t c = 0; c < nchk_h; ++c) choff[(size_t)c + 1] += choff[(size_t)c];
         h->sell_elems = choff.back();
@@ -1306,6 +1316,11 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
                 }
             }
             cudaGetLastError();
+        }
+        if (getenv("AJM_TS_ALL")) {
+            h->cta_nchk.assign((size_t)G, 0);
+            for (int cc = 0; cc < G; ++cc)
+                h->cta_nchk[(size_t)cc] = unit_c0_h[(size_t)cta_unit_h[(size_t)cc + 1]] - unit_c0_h[(size_t)cta_unit_h[(size_t)cc]];
         }
         mark("P-cluster", (cudaStream_t)-1);
         // owner of a split row = the CTA that runs its last segment
@@ -1959,9 +1974,9 @@ static ajm_status_t solve_post(ajm_ctx* h, int64_t launches, float ms, double* x
                     endt.back().first, endt.back().second);
             if (getenv("AJM_TS_ALL")) {
                 for (int g = 0; g < h->grid; ++g)
-                    fprintf(stderr, "[ajm cta] %d sm %d seg-end %.2f chunk-end %.2f end %.2f\n", g, (int)cta[(size_t)4 * g + 1],
+                    fprintf(stderr, "[ajm cta] %d sm %d seg-end %.2f chunk-end %.2f end %.2f chunks %d\n", g, (int)cta[(size_t)4 * g + 1],
                             (double)(cta[(size_t)4 * g + 2] - hts[5 * 8]) / 1e3, (double)(cta[(size_t)4 * g + 3] - hts[5 * 8]) / 1e3,
-                            (double)(cta[(size_t)4 * g] - hts[5 * 8]) / 1e3);
+                            (double)(cta[(size_t)4 * g] - hts[5 * 8]) / 1e3, h->cta_nchk.empty() ? -1 : h->cta_nchk[(size_t)g]);
             }
         }
         if (np)

@@ -176,6 +176,7 @@ struct AjmPass {
     double* Lq;
     const double* Lv;
     AjmShard sh;                             // (kShard) row-block sharding
+    int rot;                                 // (experiment) CTA b runs the work planned for CTA (b + rot) % G
 };
 
 __device__ __forceinline__ unsigned long long ajm_gtime() {
@@ -810,8 +811,8 @@ __device__ __forceinline__ double ajm_lds_f64(uint32_t a) {
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
     return v;
 }
-template <int W>  // W <= 8 entries per row, known at compile time
-__device__ __forceinline__ double ajm_chunk_dot8_w(uint32_t sva, uint32_t sca, const double* xb, uint32_t taba) {
+template <int W>
+__device__ __forceinline__ void ajm_dot8_part(uint32_t sva, uint32_t sca, const double* xb, uint32_t taba, double& s) {
     int cc[W];
     double xg[W];
 #pragma unroll
@@ -820,33 +821,24 @@ __device__ __forceinline__ double ajm_chunk_dot8_w(uint32_t sva, uint32_t sca, c
     for (int k = 0; k < W; ++k) cc[k] = ajm_lds_s32(taba + 4u * (uint32_t)cc[k]);
 #pragma unroll
     for (int k = 0; k < W; ++k) xg[k] = ajm_ld(xb + cc[k]);
-    double s = 0.0;
 #pragma unroll
     for (int k = 0; k < W; ++k) s += ajm_lds_f64(sva + 256u * k) * xg[k];  // ascending column order
-    return s;
 }
+// full batches of 8 and an exactly unrolled remainder (no predicated slots)
 __device__ __forceinline__ double ajm_chunk_dot8s(uint32_t sva, uint32_t sca, int w, const double* xb, uint32_t taba) {
-    if (AJM_DOT8_MODE >= 2) {
-        switch (w) {  // the stencils' widths: 7-point (7), 5-point (5), 27-point chunks are w > 8
-            case 7: return ajm_chunk_dot8_w<7>(sva, sca, xb, taba);
-            case 5: return ajm_chunk_dot8_w<5>(sva, sca, xb, taba);
-            // (27, fully unrolled: measured config 5 1068 -> 1131 us/pass, rejected)
-            default: break;
-        }
-    }
     double s = 0.0;
-    for (int k0 = 0; k0 < w; k0 += 8) {
-        int cc[8];
-        double xg[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) cc[j] = (k0 + j < w) ? (int)ajm_lds_u8(sca + 32u * (k0 + j)) : 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) cc[j] = ajm_lds_s32(taba + 4u * (uint32_t)cc[j]);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) xg[j] = (k0 + j < w) ? ajm_ld(xb + cc[j]) : 0.0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (k0 + j < w) s += ajm_lds_f64(sva + 256u * (k0 + j)) * xg[j];  // ascending column order
+    int k0 = 0;
+    for (; k0 + 8 <= w; k0 += 8) ajm_dot8_part<8>(sva + 256u * k0, sca + 32u * k0, xb, taba, s);
+    const uint32_t va = sva + 256u * k0, ca = sca + 32u * k0;
+    switch (w - k0) {
+        case 1: ajm_dot8_part<1>(va, ca, xb, taba, s); break;
+        case 2: ajm_dot8_part<2>(va, ca, xb, taba, s); break;
+        case 3: ajm_dot8_part<3>(va, ca, xb, taba, s); break;
+        case 4: ajm_dot8_part<4>(va, ca, xb, taba, s); break;
+        case 5: ajm_dot8_part<5>(va, ca, xb, taba, s); break;
+        case 6: ajm_dot8_part<6>(va, ca, xb, taba, s); break;
+        case 7: ajm_dot8_part<7>(va, ca, xb, taba, s); break;
+        default: break;
     }
     return s;
 }
@@ -993,8 +985,8 @@ __global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
     static_assert(!kShard || (!kCluster && !kJB && !kGMeta && !kLz), "sharded solve: plain ring variants only");
     // (kShard = 2) this CTA's rank's pass struct, in shared memory (the launch serves all ranks)
     __shared__ __align__(16) unsigned char s_pp[kShard == 2 ? sizeof(AjmPass) : 16];
-    int bid = (int)blockIdx.x;
     unsigned G = gridDim.x;
+    int bid = (int)((blockIdx.x + (unsigned)p0.rot) % G);
     if constexpr (kShard == 2) {
         const int rk = (int)blockIdx.x / p0.sh.emu_grid;
         bid = (int)blockIdx.x - rk * p0.sh.emu_grid;
