@@ -88,6 +88,9 @@ typedef enum {
 #define AJM_DEBUG_POISON 0x100000u    /* debug: fill every device allocation of this create with 0xff   */
 #define AJM_VALUE_STREAM 0x400000u    /* keep streaming the SELL values even when the (column offset,
                                          value) pairs take <= 256 values (no pair codes; same iterates) */
+#define AJM_NO_BAND_STAGING 0x800000u /* pair-coded stencils: gather x~ from global memory instead of
+                                         staging its bands and the row operands through the TMA ring
+                                         (same iterates)                                              */
 /* block size of AJM_D_JBLOCK, bits 8..15 of the flags: bs in {1, 2, 4, 8, 16, 32} */
 #define AJM_JBLOCK_SIZE(bs) (((uint32_t)(bs) & 0xffu) << 8)
 #define AJM_JBLOCK_SIZE_OF(flags) (((uint32_t)(flags) >> 8) & 0xffu)
@@ -151,7 +154,8 @@ typedef struct {
     int32_t val_bytes;        /* bytes streamed per SELL value: 8, or 0 when the byte code indexes a
                                  table of <= 256 (value, column offset) pairs (pair-coded entries:
                                  constant-coefficient stencils)                       */
-    int32_t pad_;
+    int32_t band_staged;      /* 1: x~ bands and the row operands are staged by the TMA ring
+                                 (ajm_band_kernel; natural-order pair-coded stencils)              */
 } ajm_info_t;
 
 /*

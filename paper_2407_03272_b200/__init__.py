@@ -39,6 +39,7 @@ AJM_SEGMENTS_DYNAMIC = 0x80000
 AJM_DEBUG_POISON = 0x100000
 AJM_SHARD_COLOCATED = 0x200000
 AJM_VALUE_STREAM = 0x400000
+AJM_NO_BAND_STAGING = 0x800000
 AJM_MAX_RANKS = 8
 AJM_SHARD_BLOB_BYTES = 1024
 ABI_VERSION = 5
@@ -87,7 +88,7 @@ class ajm_info_t(ctypes.Structure):
                 ("launches_per_solve", ctypes.c_int32), ("col_bytes", ctypes.c_int32),
                 ("seg_nnz", ctypes.c_int64), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
                 ("halo", ctypes.c_int64), ("send", ctypes.c_int64), ("group_rows", ctypes.c_int64),
-                ("val_bytes", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+                ("val_bytes", ctypes.c_int32), ("band_staged", ctypes.c_int32)]
 
 
 class ajm_spectrum_t(ctypes.Structure):
@@ -279,7 +280,7 @@ class Solver:
 
     def __init__(self, n, row_ptr, col, val, b, dmode="jdiag", d=None, validate_symmetry=False,
                  loop="graph", stream=None, jblock=None, int32_columns=False, global_tables=False,
-                 segments="auto", debug_poison=False, value_stream=False):
+                 segments="auto", debug_poison=False, value_stream=False, band_staging=True):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2407_03272_b200 needs a CUDA device (no CPU fallback)")
@@ -290,6 +291,7 @@ class Solver:
         flags |= {"auto": 0, "static": AJM_SEGMENTS_STATIC, "dynamic": AJM_SEGMENTS_DYNAMIC}[segments]
         flags |= AJM_DEBUG_POISON if debug_poison else 0
         flags |= AJM_VALUE_STREAM if value_stream else 0
+        flags |= 0 if band_staging else AJM_NO_BAND_STAGING
         self.jblock = None
         if jblock is not None:  # eq-J-blkdiag with bs-row blocks (AJM_D_JBLOCK)
             dmode = "jblock"

@@ -74,6 +74,10 @@ SolveFn pair_fn(bool seg, int stages) {
     if (stages == 8) return seg ? ajm_solve_kernel<8, true, false, 0, false, 2> : ajm_solve_kernel<8, false, false, 0, false, 2>;
     return seg ? ajm_solve_kernel<4, true, false, 0, false, 2> : ajm_solve_kernel<4, false, false, 0, false, 2>;
 }
+// banded staging (natural-order pair-coded stencils): ring depth 2-4 (stages of 12-30 KB)
+SolveFn band_fn(int stages) {
+    return stages >= 4 ? ajm_band_kernel<4> : stages == 3 ? ajm_band_kernel<3> : ajm_band_kernel<2>;
+}
 // block-diagonal J (natural order, no segments), cooperative grid or single cluster
 SolveFn jblock_fn(int bs, bool cluster) {
     if (cluster)
@@ -234,6 +238,9 @@ struct ajm_ctx {
     long long* ptab = nullptr;  // [AJM_CTAB][2] pair-coded entries {value bits, offset}
     int col_bytes = 4;          // bytes per streamed column index: 4 (int32) or 1 (byte code)
     int pair = 0;               // 1: the byte code carries the value too (no values streamed)
+    int band = 0;               // 1: ajm_band_kernel (x~ bands and row operands staged by the TMA)
+    AjmBand bd = {};            // its band layout
+    long long* bptab = nullptr; // [AJM_CTAB][2] {value bits, stage offset} of the pair codes
     int ring_stages = 4;        // TMA ring depth of the chosen solver kernel
     bool seg_fn = true;         // the chosen plain/col8 ring kernel has the segment phases
     bool ring_fn = false;       // h->fn is a ring_fn/col8_fn kernel (ring depth selectable)
@@ -366,7 +373,7 @@ void free_all(ajm_ctx* h) {
                     h->seg_split, h->seg_part, h->split_row, h->split_seg0, h->split_cnt,
                     h->cta_split, h->owner_split, h->unit_c0, h->cta_seg, h->seg_list, h->cta_unit, h->partials, h->ctrl,
                     h->hist, h->scratch, h->err, h->ts, h->perm_fwd, h->perm_inv, h->b_in, h->Jblk, h->Jinv, h->seg_order, h->seg_grp,
-                    h->g_uc0, h->g_coff, h->g_ubase, h->g_cbase, h->scode, h->ctab, h->seg_meta, h->lzw, h->grp, h->ptab};
+                    h->g_uc0, h->g_coff, h->g_ubase, h->g_cbase, h->scode, h->ctab, h->seg_meta, h->lzw, h->grp, h->ptab, h->bptab};
     for (void* p : ptrs) dfree(p);
     dfree(h->snd_cta);
     dfree(h->snd);
@@ -452,7 +459,8 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.ptab = h->ptab;
     p.sh = AjmShard{};
     p.sh.nranks = 1;
-    p.rot = 0;
+    p.bd = h->bd;
+    p.bptab = h->bptab;
     if (h->shard) {
         p.sh.rank = h->rank;
         p.sh.nranks = h->nranks;
@@ -1402,6 +1410,7 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
         h->l2persist = 0;
         h->l2_mode = 3;
     }
+    if (getenv("AJM_NO_PERSIST")) h->l2persist = 0;  // (experiments)
     if (h->l2persist) {
         int maxp = 0, maxw = 0;
         CC(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device));
@@ -1763,6 +1772,98 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
         CC(cudaFreeAsync(vt, st));
     }
     mark("pair", st);
+    // banded staging (ajm_band_kernel): natural-order pair-coded layouts without long
+    // rows and with a diagonal D whose column offsets fall into <= AJM_MAX_BANDS bands of width
+    // <= 64 (offsets closer than 32 share a band): every operand of a 256-row unit is staged by
+    // the TMA -- x~ over each band, b, D, x^{t-1}, Q x^{t-1} -- next to its codes.  Same sums, same
+    // reduction order: bitwise the pair kernel (AJM_NO_BAND=1 keeps it, experiments / tests).
+    if (h->pair && !sh && h->nseg == 0 && !h->relabel && !h->jbs && !h->cluster && !h->gmeta && !h->resident &&
+        getenv("AJM_NO_BAND") == nullptr && !(flags & AJM_NO_BAND_STAGING)) {
+        std::vector<long long> pt(2 * (size_t)AJM_CTAB);
+        std::vector<int> offs(AJM_CTAB);
+        CC(cudaMemcpyAsync(pt.data(), h->ptab, sizeof(long long) * pt.size(), cudaMemcpyDeviceToHost, st));
+        CC(cudaMemcpyAsync(offs.data(), h->ctab, sizeof(int) * AJM_CTAB, cudaMemcpyDeviceToHost, st));
+        CC(cudaStreamSynchronize(st));
+        std::vector<int> ko(offs.begin(), offs.end());
+        ko.push_back(0);  // x~_row itself is always staged
+        std::sort(ko.begin(), ko.end());
+        ko.erase(std::unique(ko.begin(), ko.end()), ko.end());
+        AjmBand bd = {};
+        bool ok = true;
+        // two offset ranges share a band when the gap between them is below a unit's rows: the merged
+        // band is then no longer than the two (config 2: the y-neighbour bands join the centre one,
+        // 31.6 -> 28.5 us/pass; AJM_BAND_GAP overrides for experiments)
+        const long long gap = getenv("AJM_BAND_GAP") ? std::atoll(getenv("AJM_BAND_GAP")) : AJM_UNIT_ROWS;
+        for (size_t i = 0; i < ko.size() && ok; ++i) {
+            if (bd.nb > 0 && (long long)ko[i] - bd.hi[bd.nb - 1] <= gap) {
+                bd.hi[bd.nb - 1] = ko[i];
+            } else if (bd.nb < AJM_MAX_BANDS) {
+                bd.lo[bd.nb] = bd.hi[bd.nb] = ko[i];
+                bd.nb += 1;
+            } else {
+                ok = false;
+            }
+        }
+        int maxw = 0;
+        for (int64_t c = 0; c < h->nchunks; ++c) maxw = std::max<int>(maxw, (int)((choff[(size_t)c + 1] - choff[(size_t)c]) / 32));
+        int xd = 0;
+        for (int b = 0; b < bd.nb && ok; ++b) {
+            if (bd.hi[b] - bd.lo[b] > 1024) ok = false;
+            bd.pos[b] = xd;
+            int len = AJM_UNIT_ROWS + (bd.hi[b] - bd.lo[b]) + 2;
+            xd += len + (len & 1);
+        }
+        bd.xdoubles = xd;
+        bd.code_bytes = (AJM_UNIT_ROWS * maxw + 15) / 16 * 16;
+        bd.stage_bytes = bd.code_bytes + 8 * bd.xdoubles + 4 * AJM_UNIT_ROWS * 8;
+        bd.n_pad = (int)h->n_pad;
+        auto soff_of = [&](int off) {
+            for (int b = 0; b < bd.nb; ++b)
+                if (off >= bd.lo[b] && off <= bd.hi[b]) return bd.pos[b] + off - bd.lo[b] + (bd.lo[b] & 1);
+            return -1;
+        };
+        bd.xt_soff = soff_of(0);
+        int stb = 0;
+        size_t dynb = 0;
+        if (ok && h->n_pad < INT_MAX / 2) {
+            const int smax = getenv("AJM_BAND_STAGES") ? std::max(2, std::min(4, std::atoi(getenv("AJM_BAND_STAGES")))) : 4;
+            for (int sgs = smax; sgs >= 2 && !stb; --sgs) {
+                const size_t dyn = (size_t)sgs * (size_t)bd.stage_bytes + h->meta_bytes;
+                int occ = 0;
+                cudaError_t eo;
+                {
+                    std::lock_guard<std::mutex> lock(g_attr_mu);
+                    eo = fn_occupancy(band_fn(sgs), dyn, 100, &occ, block_threads(false));
+                }
+                CC(eo);
+                if (occ >= h->ctas_per_sm) {
+                    stb = sgs;
+                    dynb = dyn;
+                }
+            }
+        }
+        if (stb) {
+            bd.vpk = h->l2_mode == 3 ? 1 : (h->l2_mode >= 2 ? 2 : 0);
+            bd.xpk = h->l2_mode >= 2 ? 2 : 0;
+            if (getenv("AJM_BAND_VPK")) bd.vpk = std::atoi(getenv("AJM_BAND_VPK"));  // (experiments)
+            if (getenv("AJM_BAND_XPK")) bd.xpk = std::atoi(getenv("AJM_BAND_XPK"));
+            std::vector<long long> bp(2 * (size_t)AJM_CTAB, 0);
+            for (int cc = 0; cc < AJM_CTAB; ++cc) {
+                bp[2 * (size_t)cc] = pt[2 * (size_t)cc];
+                const int so = soff_of((int)pt[2 * (size_t)cc + 1]);
+                bp[2 * (size_t)cc + 1] = 8LL * (so < 0 ? bd.xt_soff : so);  // bytes (unused slots: any in-range offset)
+            }
+            CC(dalloc(&h->bptab, bp.size(), st));
+            CC(cudaMemcpyAsync(h->bptab, bp.data(), sizeof(long long) * bp.size(), cudaMemcpyHostToDevice, st));
+            CC(cudaStreamSynchronize(st));
+            h->bd = bd;
+            h->band = 1;
+            h->fn = band_fn(stb);
+            h->dyn_smem = dynb;
+            h->ring_stages = stb;
+        }
+    }
+    mark("band", st);
     // shared-memory carve-out: the smallest that keeps ctas_per_sm CTAs resident, so the rest of
     // the SM's 256 KB stays L1 for the gathers; AJM_CARVEOUT=<pct> overrides
     {
@@ -2659,6 +2760,7 @@ ajm_status_t ajm_get_info(ajm_handle_t h, ajm_info_t* info) {
     info->launches_per_solve = (int32_t)(1 + (h->prime_bytes ? 1 : 0) + std::max<int64_t>(h->last_launches, 1));
     info->col_bytes = h->col_bytes;
     info->val_bytes = h->pair ? 0 : 8;
+    info->band_staged = h->band;
     info->seg_nnz = h->seg_nnz;
     info->rank = h->rank;
     info->nranks = h->nranks;

@@ -45,6 +45,9 @@
 #define AJM_LOG_CAP 64
 #define AJM_CTAB 256     // byte-coded columns: at most this many distinct offsets col - row
 #define AJM_CTAB_HASH 2048  // create-time hash set of the offsets
+#ifndef AJM_PROD_SLEEP_NS
+#define AJM_PROD_SLEEP_NS 64  // producer polls of the consumers' pass count sleep this long
+#endif
 
 // Iteration state: identical copies in every CTA (shared memory) and in global memory.
 struct AjmState {
@@ -98,6 +101,22 @@ struct AjmPeer {
     double* x[3];                 // X0..X2 base (own row 0) of that rank's iterate buffers
     double* slot;                 // [2][AJM_MAX_RANKS][AJM_NPART] rank partials it receives
     unsigned long long* bar;      // its monotone cross-rank arrival counter
+};
+
+// Banded staging (ajm_band_kernel): the column offsets of a natural-order pair-coded layout fall
+// into nb bands [lo_b, hi_b]; for a staging unit of rows [r0, r0 + 256) the entries of x~ it gathers
+// are the nb contiguous ranges x~[r0 + lo_b, r0 + 255 + hi_b], which the TMA copies into the stage
+// next to the unit's codes and its rows' b, D, x^{t-1}, (Q x^{t-1}).
+#define AJM_MAX_BANDS 16
+struct AjmBand {
+    int nb;                        // bands
+    int code_bytes;                // code area per stage (16-byte multiple)
+    int xdoubles;                  // x~ area per stage (doubles; every band starts 16-byte aligned)
+    int stage_bytes;               // code_bytes + 8 xdoubles + 4 * 256 * 8
+    int xt_soff;                   // stage position of x~_row (offset 0) relative to the row's slot
+    int n_pad;                     // length of the vector buffers (copies are clamped to [0, n_pad))
+    int vpk, xpk;                  // L2 policy kinds (ajm_policy) of the b/D/Qx and x~/x^{t-1} copies
+    int lo[AJM_MAX_BANDS], hi[AJM_MAX_BANDS], pos[AJM_MAX_BANDS];
 };
 
 struct AjmPass;
@@ -176,7 +195,8 @@ struct AjmPass {
     double* Lq;
     const double* Lv;
     AjmShard sh;                             // (kShard) row-block sharding
-    int rot;                                 // (experiment) CTA b runs the work planned for CTA (b + rot) % G
+    AjmBand bd;                              // (ajm_band_kernel) banded x~ staging
+    const long long* __restrict__ bptab;     // (ajm_band_kernel) [256][2] {bits of Q_ij, stage offset}
 };
 
 __device__ __forceinline__ unsigned long long ajm_gtime() {
@@ -986,7 +1006,7 @@ __global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
     // (kShard = 2) this CTA's rank's pass struct, in shared memory (the launch serves all ranks)
     __shared__ __align__(16) unsigned char s_pp[kShard == 2 ? sizeof(AjmPass) : 16];
     unsigned G = gridDim.x;
-    int bid = (int)((blockIdx.x + (unsigned)p0.rot) % G);
+    int bid = (int)blockIdx.x;
     if constexpr (kShard == 2) {
         const int rk = (int)blockIdx.x / p0.sh.emu_grid;
         bid = (int)blockIdx.x - rk * p0.sh.emu_grid;
@@ -1512,6 +1532,297 @@ __global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
 }
 
 // ------------------------------------------------------------------------------------------------
+// Banded staging kernel (natural-order pair-coded layouts without long rows, diagonal D: stencils)
+// ------------------------------------------------------------------------------------------------
+// The persistent pass of ajm_solve_kernel<.., kCol8 = 2> with EVERY operand of a staging unit in
+// shared memory before its consumers start: a unit is 8 consecutive chunks (256 rows) of the CTA's
+// range, and the producer warp's single lane copies into its stage (cp.async.bulk, one mbarrier):
+//   - the unit's code bytes (1 per entry),
+//   - for every band b of the column offsets, x~^t[r0 + lo_b, r0 + 255 + hi_b] (clamped to the
+//     buffer),
+//   - the rows' b, D, x^{t-1} and (Q x^{t-1}).
+// A consumer lane then forms (Q x~)_row from shared memory only: code -> {Q_ij, stage offset of
+// x~_j} (the pair table; stage offset = band position + offset - lo_b, constant per code), and
+// the row update reads its operands from the stage; the only global accesses are the two stores.
+// The gathers' latency chain of the register kernel (one L1/L2 round trip per batch of 8 entries
+// after the operands) is replaced by the ring's run-ahead.  x~^t changes every pass, so the units
+// of pass t+1 are issued only after pass t's grid barrier: the producer waits for the consumers'
+// pass count (release/acquire in shared memory, after tid 0's acquire of the grid barrier) and
+// orders the async-proxy reads after the generic stores of every SM with fence.proxy.async.
+// Same chunk -> warp mapping (chunk j -> warp j % 8), same ascending-column sums, same CTA / grid
+// reduction order and control step as ajm_solve_kernel: bitwise the iterates of the pair kernel.
+__device__ __forceinline__ int ajm_lds_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(ajm_smem(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void ajm_sts_release(int* p, int v) {
+    asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(ajm_smem(p)), "r"(v) : "memory");
+}
+template <int W>
+__device__ __forceinline__ void ajm_dotb_part(uint32_t sca, uint32_t xrow, uint32_t taba, double& s) {
+    int cc[W];
+    double vv[W], xg[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) cc[k] = (int)ajm_lds_u8(sca + 32u * k);
+#pragma unroll
+    for (int k = 0; k < W; ++k) ajm_lds_pair(taba + 16u * (uint32_t)cc[k], vv[k], cc[k]);
+#pragma unroll
+    for (int k = 0; k < W; ++k) xg[k] = ajm_lds_f64(xrow + (uint32_t)cc[k]);
+#pragma unroll
+    for (int k = 0; k < W; ++k) s += vv[k] * xg[k];  // ascending column order
+}
+// sca: this lane's first code; xrow: stage address of the x~ area + 8 * (the row's slot in the unit);
+// the table holds the x~ stage offsets in BYTES
+__device__ __forceinline__ double ajm_chunk_dotb(uint32_t sca, int w, uint32_t xrow, uint32_t taba) {
+    double s = 0.0;
+    if (w == 7) {
+        ajm_dotb_part<7>(sca, xrow, taba, s);
+        return s;
+    }
+    int k0 = 0;
+    for (; k0 + 8 <= w; k0 += 8) ajm_dotb_part<8>(sca + 32u * k0, xrow, taba, s);
+    const uint32_t sa = sca + 32u * k0;
+    switch (w - k0) {
+        case 1: ajm_dotb_part<1>(sa, xrow, taba, s); break;
+        case 2: ajm_dotb_part<2>(sa, xrow, taba, s); break;
+        case 3: ajm_dotb_part<3>(sa, xrow, taba, s); break;
+        case 4: ajm_dotb_part<4>(sa, xrow, taba, s); break;
+        case 5: ajm_dotb_part<5>(sa, xrow, taba, s); break;
+        case 6: ajm_dotb_part<6>(sa, xrow, taba, s); break;
+        case 7: ajm_dotb_part<7>(sa, xrow, taba, s); break;
+        default: break;
+    }
+    return s;
+}
+
+template <int kStages>
+__global__ void __maxnreg__(96) ajm_band_kernel(AjmPass p) {
+    extern __shared__ __align__(128) unsigned char s_dyn[];
+    __shared__ double s_red[AJM_WARPS][AJM_NPART];
+    __shared__ double s_tot[AJM_NPART];
+    __shared__ double s_res;
+    __shared__ AjmState s_st;
+    __shared__ __align__(8) uint64_t s_full[kStages];
+    __shared__ __align__(8) uint64_t s_empty[kStages];
+    __shared__ volatile int s_stop;  // the consumers left the pass loop
+    __shared__ int s_pass;           // passes the consumers have started (release / acquire)
+    __shared__ volatile int s_fin;   // passes run, written before s_stop
+    __shared__ int s_to;
+    __shared__ __align__(16) long long s_bp[2 * AJM_CTAB];  // {Q_ij bits, stage byte offset} per code
+    AjmCtrl* c = p.ctrl;
+    const AjmBand& bd = p.bd;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int bid = (int)blockIdx.x;
+    const unsigned G = gridDim.x;
+    const int u0 = p.cta_unit[bid], u1 = p.cta_unit[bid + 1];
+    const int cfirst = u1 > u0 ? p.unit_c0[u0] : 0;
+    const int nchk = u1 > u0 ? p.unit_c0[u1] - cfirst : 0;
+    const long long efirst = nchk > 0 ? p.chunk_off[cfirst] : 0;
+    const int nun = (nchk + AJM_WARPS - 1) / AJM_WARPS;  // units of 8 chunks
+    const size_t SB = (size_t)bd.stage_bytes;
+    int* s_coff = reinterpret_cast<int*>(s_dyn + (size_t)kStages * SB);
+    for (int i = tid; i <= nchk; i += blockDim.x) s_coff[i] = (int)(p.chunk_off[cfirst + i] - efirst);
+    for (int i = tid; i < 2 * AJM_CTAB; i += blockDim.x) s_bp[i] = p.bptab[i];
+    if (tid == 0) {
+        s_st = c->s;
+        for (int k = 0; k < kStages; ++k) {
+            ajm_mbar_init(&s_full[k], 1);
+            ajm_mbar_init(&s_empty[k], AJM_WARPS);
+        }
+        s_stop = 0;
+        s_pass = 0;
+        s_fin = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const long long total_units = (long long)nun * p.max_passes;
+
+    if (warp == AJM_WARPS) {
+        // ---------------- producer warp (one lane) ----------------
+        if (lane == 0 && nun > 0) {
+            const uint64_t qpol = ajm_policy(p.l2_mode >= 1 ? 1 : 0);  // codes
+            const uint64_t vpol = ajm_policy(bd.vpk);                   // b, D, Qx
+            const uint64_t xpol = ajm_policy(bd.xpk);                   // x~, x^{t-1}
+            long long cnt = 0;
+            int uu = 0, pass = 0;
+            const double* xcur = ajm_sel(p, s_st.cur);
+            const double* xprv = ajm_sel(p, s_st.prev);
+            bool stop = false;
+            while (cnt < total_units && !stop) {
+                if (uu == 0 && cnt > 0) {
+                    // the first unit of the next pass: after that pass's grid barrier (x~^{t+1} and
+                    // Q x^t of every SM written) -- the consumers publish their pass count after it;
+                    // the spin sleeps between polls so it takes no issue slots from the consumers
+                    ++pass;
+                    long long spins = 0;
+                    while (ajm_lds_acquire(&s_pass) < pass) {
+                        if (s_stop) { stop = true; break; }  // (s_pass never reaches a pass that does not run)
+                        if (++spins > (1LL << 28)) { atomicExch(&c->timeout_flag, 1u); stop = true; break; }
+                        __nanosleep(AJM_PROD_SLEEP_NS);
+                    }
+                    if (stop) break;
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    xcur = ajm_sel(p, s_st.cur);
+                    xprv = ajm_sel(p, s_st.prev);
+                }
+                const int stage = (int)(cnt % kStages);
+                const unsigned par = (unsigned)((cnt / kStages) & 1) ^ 1u;
+                long long idle = 0;
+                while (!ajm_mbar_try_wait(&s_empty[stage], par)) {
+                    if (s_stop) { stop = true; break; }
+                    if (++idle > (1LL << 28)) { atomicExch(&c->timeout_flag, 1u); stop = true; break; }
+                }
+                if (stop) break;
+                // unit uu: chunks [8 uu, min(8 uu + 8, nchk)) of the CTA
+                const int c0 = uu * AJM_WARPS, c1 = min(c0 + AJM_WARPS, nchk);
+                const int e0 = s_coff[c0], e1 = s_coff[c1];
+                const int r0 = (cfirst + c0) * 32, nr = (c1 - c0) * 32;
+                unsigned char* sb = s_dyn + (size_t)stage * SB;
+                double* xa = reinterpret_cast<double*>(sb + bd.code_bytes);
+                double* so = xa + bd.xdoubles;
+                unsigned bytes = (unsigned)(e1 - e0) + 4u * 8u * (unsigned)nr;
+                for (int b = 0; b < bd.nb; ++b) {
+                    const int a = r0 + bd.lo[b] - (bd.lo[b] & 1);
+                    int e = r0 + nr + bd.hi[b];
+                    e += e & 1;
+                    const int ca = max(a, 0), ce = min(e, bd.n_pad);
+                    if (ce > ca) bytes += 8u * (unsigned)(ce - ca);
+                }
+                ajm_mbar_expect_tx(&s_full[stage], bytes);
+                ajm_bulk_g2s(sb, p.scode + efirst + e0, (unsigned)(e1 - e0), &s_full[stage], qpol);
+                for (int b = 0; b < bd.nb; ++b) {
+                    const int a = r0 + bd.lo[b] - (bd.lo[b] & 1);
+                    int e = r0 + nr + bd.hi[b];
+                    e += e & 1;
+                    const int ca = max(a, 0), ce = min(e, bd.n_pad);
+                    if (ce > ca)
+                        ajm_bulk_g2s(xa + bd.pos[b] + (ca - a), xcur + ca, 8u * (unsigned)(ce - ca), &s_full[stage], xpol);
+                }
+                ajm_bulk_g2s(so, p.b + r0, 8u * nr, &s_full[stage], vpol);
+                ajm_bulk_g2s(so + 256, p.D + r0, 8u * nr, &s_full[stage], vpol);
+                ajm_bulk_g2s(so + 512, xprv + r0, 8u * nr, &s_full[stage], xpol);
+                ajm_bulk_g2s(so + 768, p.Qxp + r0, 8u * nr, &s_full[stage], vpol);
+                ++cnt;
+                if (++uu == nun) uu = 0;
+            }
+            // every issued copy lands before the CTA exits (units of a pass that never ran included)
+            long long spins = 0;
+            while (!s_stop) {
+                if (++spins > (1LL << 28)) break;
+                __nanosleep(AJM_PROD_SLEEP_NS);
+            }
+            __threadfence_block();
+            for (long long k = (long long)s_fin * nun; k < cnt; ++k)
+                if (k >= 0) ajm_mbar_wait(&s_full[k % kStages], (unsigned)((k / kStages) & 1), &c->timeout_flag);
+        }
+        return;
+    }
+
+    // ---------------- consumer warps ----------------
+    const uint64_t vpol = ajm_policy(p.l2_mode == 3 ? 1 : (p.l2_mode >= 2 ? 2 : 0));
+    const uint64_t xpol = ajm_policy(p.l2_mode >= 2 ? 2 : 0);
+    const uint32_t taba = ajm_smem(s_bp);
+    long long ucnt = 0;
+    int pass = 0;
+    for (; pass < p.max_passes; ++pass) {
+        if (s_st.done) break;
+        const long long t = s_st.t;
+        const int restart_t = s_st.restart_t;
+        const double beta = s_st.beta;
+        double* xf = ajm_sel(p, s_st.fre);
+        AjmAcc acc = {0.0, 0.0, 0.0, 0.0, 0.0};
+        const bool tsw = p.ts && bid == 0 && tid == 0 && pass < 64;
+        if (tsw) p.ts[pass * 8 + 0] = ajm_gtime();
+        for (int uu = 0; uu < nun; ++uu) {
+            const int stage = (int)((ucnt + uu) % kStages);
+            const unsigned par = (unsigned)(((ucnt + uu) / kStages) & 1);
+            const int j = uu * AJM_WARPS + warp;
+            ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);
+            if (j < nchk) {
+                const unsigned char* sb = s_dyn + (size_t)stage * SB;
+                const double* xa = reinterpret_cast<const double*>(sb + bd.code_bytes);
+                const double* so = xa + bd.xdoubles;
+                const int lrow = warp * 32 + lane;  // the row's slot in the unit
+                const int row = (cfirst + j) * 32 + lane;
+                const int e0 = s_coff[j];
+                const int w = (s_coff[j + 1] - e0) >> 5;
+                const uint32_t sca = ajm_smem(sb) + (uint32_t)(e0 - s_coff[uu * AJM_WARPS]) + (uint32_t)lane;
+                const uint32_t xrow = ajm_smem(xa) + 8u * (uint32_t)lrow;
+                const double q = ajm_chunk_dotb(sca, w, xrow, taba);
+                if (row < p.n_sell) {
+                    const double bi = so[lrow], Di = so[256 + lrow], xpi = so[512 + lrow], qxp = so[768 + lrow];
+                    const double xt = xa[bd.xt_soff + lrow];
+                    ajm_row_update(p.Qxp, xf, row, q, bi, Di, xt, xpi, qxp, beta, restart_t, acc, vpol, xpol);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) ajm_mbar_arrive(&s_empty[stage]);
+        }
+        ucnt += nun;
+        if (tsw) p.ts[pass * 8 + 7] = ajm_gtime();
+        if (tsw) p.ts[pass * 8 + 1] = ajm_gtime();
+        if (p.ts && tid == 0 && pass == 5) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            p.ts[512 + 4 * bid] = ajm_gtime();
+            p.ts[512 + 4 * bid + 1] = smid;
+        }
+        // CTA partial -> grid barrier -> every CTA reduces all partials in the same order
+        ajm_block_reduce(acc, s_red);
+        if (tsw) p.ts[pass * 8 + 2] = ajm_gtime();
+        double* part = p.partials + (size_t)(t & 1) * G * AJM_NPART;
+        double an_c = 0.0, beta_c = 0.0;
+        if (tid == 0) {
+            part[0 * G + bid] = acc.rr;
+            part[1 * G + bid] = acc.xq;
+            part[2 * G + bid] = acc.bx;
+            part[3 * G + bid] = acc.d;
+            part[4 * G + bid] = acc.dabs;
+            ajm_grid_arrive(c);
+            const double a = s_st.alpha;
+            an_c = (1.0 + sqrt(1.0 + 4.0 * a * a)) / 2.0;
+            beta_c = s_st.momentum ? (a - 1.0) / an_c : 0.0;
+            s_to = ajm_grid_wait(c, G, t) ? 1 : 0;
+        }
+        ajm_csync();
+        if (tsw) p.ts[pass * 8 + 3] = ajm_gtime();
+        if (warp < AJM_NPART) {
+            const double* src = part + (size_t)warp * G;
+            double v = 0.0;
+            for (int k0 = lane; k0 < (int)G; k0 += 16 * 32) {
+                double r[16];
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) r[jj] = (k0 + jj * 32 < (int)G) ? __ldcg(src + k0 + jj * 32) : 0.0;
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj)
+                    if (k0 + jj * 32 < (int)G) v += r[jj];
+            }
+            v = ajm_warp_sum(v);
+            if (lane == 0) s_tot[warp] = v;
+            if (warp == 0 && lane == 0) s_res = sqrt(v) / s_st.nb;
+        }
+        ajm_csync();
+        if (tsw) p.ts[pass * 8 + 4] = ajm_gtime();
+        if (tid == 0) {
+            AjmState ls = s_st;
+            ajm_control_step(ls, s_tot, c, bid == 0, an_c, beta_c, s_res);
+            s_st = ls;
+            if (s_to) s_st.done = 1;
+            if (tsw) p.ts[pass * 8 + 5] = ajm_gtime();
+            if (!s_st.done) ajm_sts_release(&s_pass, pass + 1);  // the producer may stage pass + 1
+        }
+        ajm_csync();
+    }
+    if (tid == 0) {
+        if (bid == 0) c->s = s_st;
+        s_fin = pass;  // units of passes >= pass were never consumed
+        __threadfence_block();
+        s_stop = 1;
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
 // Small problems, resident in one thread-block cluster (config 1: the whole pass is latency)
 // ------------------------------------------------------------------------------------------------
 // The grid is ONE cluster of G <= 16 CTAs, 8 warps each, one 32-row SELL chunk per warp (natural
@@ -1529,7 +1840,6 @@ __global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
 __global__ void __launch_bounds__(AJM_BLOCK, 1) ajm_resident_kernel(AjmPass p) {
     extern __shared__ __align__(128) unsigned char s_dyn[];
     __shared__ double s_red[AJM_WARPS][AJM_NPART];
-    __shared__ double s_tot[AJM_NPART];
     // every CTA's partials, pushed by their owners (st.shared::cluster) before the barrier arrival,
     // by pass parity: after the barrier the reduction reads only local shared memory
     __shared__ double s_pall[2][16][AJM_NPART];

@@ -328,9 +328,18 @@ def test_byte_coded_columns(case):
     np.testing.assert_array_equal(a.f_hist, b.f_hist)
     if pairs:  # the byte-coded layout with the values streamed: bitwise the same too
         c = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True, value_stream=True)
-        assert c.info["col_bytes"] == 1 and c.info["val_bytes"] == 8
+        assert c.info["col_bytes"] == 1 and c.info["val_bytes"] == 8 and c.info["band_staged"] == 0
         np.testing.assert_array_equal(a.x, c.x)
         np.testing.assert_array_equal(a.res_hist, c.res_hist)
+        # natural-order pair-coded stencils stage x~'s bands and the row operands through the TMA
+        # ring (ajm_band_kernel); the register-gather pair kernel gives the same bits
+        assert a.info["band_staged"] == 1, a.info
+        d = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True, band_staging=False)
+        assert d.info["val_bytes"] == 0 and d.info["band_staged"] == 0
+        np.testing.assert_array_equal(a.x, d.x)
+        np.testing.assert_array_equal(a.res_hist, d.res_hist)
+        np.testing.assert_array_equal(a.f_hist, d.f_hist)
+        np.testing.assert_array_equal(a.d_trace, d.d_trace)
     o, _ = oracle_matching(p.Q, p.b, a, tol=0.0, maxit=400, restart=True)
     assert max_rel(a.x, o.x) <= PARITY_TOL
 

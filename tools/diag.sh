@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${TAG}_build.log 2>&1 || { tail gpurun_out/${TAG}_build.log; exit 1; }
 for c in $CFGS; do
   AJM_TS=1 timeout 300 python tools/prof.py $c $P 2>&1 | grep -v "^\[ajm create\]" | tail -4
-  timeout 600 ncu --set full --cache-control none --clock-control none --import-source on -k regex:ajm_solve_kernel -s 1 -c 1 \
+  timeout 600 ncu --set full --cache-control none --clock-control none --import-source on -k regex:"ajm_(solve|band|resident)_kernel" -s 1 -c 1 \
       -o gpurun_out/${TAG}_cfg$c -f python tools/prof.py $c $P > gpurun_out/${TAG}_ncu_cfg$c.log 2>&1
   echo "ncu cfg$c rc=$?"
   r=gpurun_out/${TAG}_cfg$c.ncu-rep

@@ -11,7 +11,7 @@ for c in $CFGS; do
 done
 for c in $CFGS; do
   python tools/prof.py $c 30 > gpurun_out/${TAG}_prof_cfg$c.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:ajm_solve_kernel -s 1 -c 1 \
+  ncu --set full --clock-control none --import-source on -k regex:"ajm_(solve|band|resident)_kernel" -s 1 -c 1 \
       -o gpurun_out/${TAG}_ncu_cfg$c -f python tools/prof.py $c 30 > gpurun_out/${TAG}_ncu_cfg$c.log 2>&1
 done
 ls -la gpurun_out

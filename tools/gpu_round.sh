@@ -23,12 +23,12 @@ timeout 600 python bench.py --other-configs "" --no-cpu-baseline --steps 2 --war
 echo "launch list rc=$?"
 for c in $NCU_CFGS; do
   timeout 300 python tools/prof.py $c 30 > gpurun_out/${TAG}_prof_cfg$c.log 2>&1 && \
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:ajm_solve_kernel -s 1 -c 1 \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"ajm_(solve|band|resident)_kernel" -s 1 -c 1 \
       -o gpurun_out/${TAG}_ncu_cfg$c -f python tools/prof.py $c 30 > gpurun_out/${TAG}_ncu_cfg$c.log 2>&1
   echo "ncu cfg$c rc=$?"
 done
 for c in $WARM_CFGS; do
-  timeout 600 ncu --set full --cache-control none --clock-control none --import-source on -k regex:ajm_solve_kernel -s 1 -c 1 \
+  timeout 600 ncu --set full --cache-control none --clock-control none --import-source on -k regex:"ajm_(solve|band|resident)_kernel" -s 1 -c 1 \
       -o gpurun_out/${TAG}_ncuwarm_cfg$c -f python tools/prof.py $c 30 > gpurun_out/${TAG}_ncuwarm_cfg$c.log 2>&1
   echo "ncu warm cfg$c rc=$?"
 done
