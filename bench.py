@@ -212,12 +212,24 @@ def cpu_model() -> str:
 
 def layout_bytes_per_iter(info, jblock=None) -> float:
     """Bytes one pass of THIS layout must move at minimum: every stored SELL entry including its
-    padding (8-byte value + the streamed column index: 4 B int32 or 1 B byte code), the warp
+    padding (8-byte value + the streamed column index: 4 B int32 or 1 B byte code; 1 B in all for
+    pair-coded entries, whose code also names the value), the warp
     segments' CSR entries (12 B), and the seven n-vectors (D replaced by bs doubles of J^-1 with
     block J).  Differs from the algorithmic model (12 nnz + 56 n + 4(n+1)) by the byte codes, the
     padding and the row offsets SELL does not need."""
-    return ((8.0 + info["col_bytes"]) * info["sell_elems"] + 12.0 * info["seg_nnz"]
+    return ((info["val_bytes"] + info["col_bytes"]) * info["sell_elems"] + 12.0 * info["seg_nnz"]
             + (48.0 + 8.0 * (jblock or 1)) * info["n"])
+
+
+def kernel_name(info) -> str:
+    """The persistent solver kernel the handle launches."""
+    if info["mode"] == 6:
+        return "ajm_resident_kernel (single thread-block cluster, whole solve on chip; one launch per solve)"
+    if info["band_staged"]:
+        return "ajm_band_kernel (pair-coded entries, x~ bands + row operands TMA-staged; one launch per solve)"
+    enc = "pair-coded entries" if info["val_bytes"] == 0 else ("byte-coded columns" if info["col_bytes"] == 1
+                                                              else "int32 columns")
+    return f"ajm_solve_kernel ({enc}; persistent, one launch per solve)"
 
 
 def cpu_baseline_run(p, cfg=2, budget_s=12.0, nthreads=None):
@@ -329,7 +341,7 @@ def roofline_block(p, info, passes, loop_ms, steps, bound, jblock=None):
                            "(profiles/ncu_traffic.json" + ("" if tr is None else f", capture {tr.get('capture', '?')}")
                            + ") x passes per launch",
           "peak_source": peak_src,
-          "kernel": "ajm_solve_kernel (persistent; one launch per solve)",
+          "kernel": kernel_name(info),
           "achieved_basis": "algorithmic bytes nnz*12+7n*8+4(n+1) per pass (D replaced by bs doubles of J^-1 per "
                             "row with --jblock) x passes / launch duration (CUDA events on the launch stream)",
           "layout_bytes_per_iteration": lay,
@@ -374,7 +386,7 @@ def other_config_record(cfg, args, dev, stream):
     rec = {"config": cfg, "workload": W["workload"], "n": p.Q.n, "nnz": p.Q.nnz,
            "value": iters / (ms * 1e-3), "unit": UNIT, "steps": steps, "warmup": 3,
            "iterations_per_solve": iters / steps, "time_to_tol_ms": ms / steps, "us_per_iteration": us,
-           "sigma": info["sigma"], "column_index_bytes": info["col_bytes"], "grid": info["grid"],
+           "sigma": info["sigma"], "column_index_bytes": info["col_bytes"], "value_bytes": info["val_bytes"], "band_staged": info["band_staged"], "grid": info["grid"],
            "roofline": rb, "roofline_gather": gather_roof(p, info, passes, loop_ms), "clocks": clk,
            "generate_s": round(gen_s, 1)}
     if W["bound"] == "latency":
@@ -565,6 +577,8 @@ def run_ours(args):
                    "l2": l2_note,
                    "grid": info["grid"],
                    "column_index_bytes": info.get("col_bytes", 4),
+                   "value_bytes": info.get("val_bytes", 8),
+                   "band_staged": info.get("band_staged", 0),
                    "ctas_per_sm": info["ctas_per_sm"]},
         "iterations_per_solve": iters / args.steps,
         "time_to_tol_ms": ms / args.steps,
