@@ -1846,6 +1846,8 @@ __global__ void __launch_bounds__(AJM_BLOCK, 1) ajm_resident_kernel(AjmPass p) {
     __shared__ AjmState s_st;
     __shared__ __align__(8) uint64_t s_cbar;
     __shared__ __align__(8) uint64_t s_cexit;
+    __shared__ int s_win[16][2];  // every CTA's x~ window [lo, hi] (the columns its rows gather)
+    __shared__ int s_wlo, s_whi;
     AjmCtrl* c = p.ctrl;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int bid = (int)blockIdx.x;
@@ -1892,9 +1894,42 @@ __global__ void __launch_bounds__(AJM_BLOCK, 1) ajm_resident_kernel(AjmPass p) {
         xp = ajm_sel(p, s_st.prev)[row];
         qxp = p.Qxp[row];
     }
+    // this CTA's x~ window: the range of the columns its rows gather (a stencil's own rows plus
+    // the halo); each CTA's replica needs only that window, so a row's x~^{t+1} is published to
+    // the CTAs whose windows hold it (a 5-point 64^2 grid: 1-2 CTAs instead of all 16)
+    {
+        int cmn = INT_MAX, cmx = INT_MIN;
+        if (row >= 0)
+            for (int k = 0; k < w; ++k) {
+                const int cc = sc[e0 + 32 * k];
+                cmn = min(cmn, cc);
+                cmx = max(cmx, cc);
+            }
+        cmn = __reduce_min_sync(0xffffffffu, cmn);
+        cmx = __reduce_max_sync(0xffffffffu, cmx);
+        if (tid == 0) {
+            s_wlo = INT_MAX;
+            s_whi = INT_MIN;
+        }
+        __syncthreads();
+        if (lane == 0) {
+            atomicMin(&s_wlo, cmn);
+            atomicMax(&s_whi, cmx);
+        }
+    }
     __syncthreads();
     // every CTA's barriers initialised (and its replica loaded) before any remote access
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (tid < (int)G) {  // this CTA's window into every CTA's s_win[bid]
+        const uint32_t la = ajm_smem(&s_win[bid][0]);
+        asm volatile("{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\tst.shared::cluster.v2.s32 [ra], {%2, %3};\n\t}"
+                     ::"r"(la), "r"((unsigned)tid), "r"(s_wlo), "r"(s_whi) : "memory");
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    unsigned dmask = 0;  // the CTAs whose windows hold this lane's row
+    if (row >= 0)
+        for (unsigned rk = 0; rk < G; ++rk)
+            if (row >= s_win[rk][0] && row <= s_win[rk][1]) dmask |= 1u << rk;
     int pass = 0;
     for (; pass < p.max_passes; ++pass) {
         if (s_st.done) break;
@@ -1936,11 +1971,13 @@ __global__ void __launch_bounds__(AJM_BLOCK, 1) ajm_resident_kernel(AjmPass p) {
             const double term = (qy - bi) * (xn - xnow);
             acc.d += term;
             acc.dabs += fabs(term);
-            // publish x~^{t+1}_row to every CTA's replica
+            // publish x~^{t+1}_row to the replicas whose windows hold it
             const uint32_t la = ajm_smem(xw + row);
-            for (unsigned rk = 0; rk < G; ++rk)
+            for (unsigned m = dmask; m; m &= m - 1u) {
+                const unsigned rk = (unsigned)__ffs(m) - 1u;
                 asm volatile("{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\tst.shared::cluster.f64 [ra], %2;\n\t}"
                              ::"r"(la), "r"(rk), "d"(xn) : "memory");
+            }
         }
         ajm_block_reduce(acc, s_red);  // (lane 0 of warp 0 holds the CTA's sums)
         if (warp == 0) {
