@@ -353,18 +353,24 @@ __device__ __forceinline__ void ajm_block_reduce(AjmAcc& a, double (*s_red)[AJM_
         for (int j = 0; j < AJM_NPART; ++j) s_red[warp][j] = v[j];
     }
     ajm_csync();
-    if (threadIdx.x == 0) {
-        double s[AJM_NPART] = {0, 0, 0, 0, 0};
-        for (int w = 0; w < AJM_WARPS; ++w)
+    if (warp == 0) {
+        // lane j < 5 sums component j over the warps in warp order (the order thread 0 used to
+        // take alone: same bits, a fifth of the serial chain)
+        double s = 0.0;
+        if (lane < AJM_NPART)
 #pragma unroll
-            for (int j = 0; j < AJM_NPART; ++j) s[j] += s_red[w][j];
-        a.rr = s[0]; a.xq = s[1]; a.bx = s[2]; a.d = s[3]; a.dabs = s[4];
+            for (int w = 0; w < AJM_WARPS; ++w) s += s_red[w][lane];
+        a.rr = __shfl_sync(0xffffffffu, s, 0);
+        a.xq = __shfl_sync(0xffffffffu, s, 1);
+        a.bx = __shfl_sync(0xffffffffu, s, 2);
+        a.d = __shfl_sync(0xffffffffu, s, 3);
+        a.dabs = __shfl_sync(0xffffffffu, s, 4);
     }
 }
 
 // a7 control step (thread 0 of every CTA, identical inputs -> identical outputs).  CTA 0 also
 // writes the histories and the restart log.
-__device__ void ajm_control_step(AjmState& s, const double* tot, AjmCtrl* c, bool writer, double an_c,
+__device__ __forceinline__ void ajm_control_step(AjmState& s, const double* tot, AjmCtrl* c, bool writer, double an_c,
                                  double beta_c, double res) {
     const long long t = s.t;
     const double f = 0.5 * tot[1] - tot[2];
