@@ -1843,6 +1843,18 @@ __global__ void __maxnreg__(96) ajm_band_kernel(AjmPass p) {
 // Per pass nothing touches global memory except CTA 0's history entries.  The row sums (ascending
 // column, from 0.0), the update, the CTA and cluster reduction orders and the control step are
 // those of ajm_solve_kernel's kCluster path: the iterates are bitwise the same.
+// W entries of a resident chunk (values / int32 columns in shared memory, x~ replica xr) added to q
+template <int W>
+__device__ __forceinline__ void ajm_res_part(const double* sv, const int* sc, const double* xr, double& q) {
+    double v[W], xg[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        v[j] = sv[32 * j];
+        xg[j] = xr[sc[32 * j]];
+    }
+#pragma unroll
+    for (int j = 0; j < W; ++j) q += v[j] * xg[j];  // ascending column order
+}
 __global__ void __launch_bounds__(AJM_BLOCK, 1) ajm_resident_kernel(AjmPass p) {
     extern __shared__ __align__(128) unsigned char s_dyn[];
     __shared__ double s_red[AJM_WARPS][AJM_NPART];
@@ -1936,28 +1948,33 @@ __global__ void __launch_bounds__(AJM_BLOCK, 1) ajm_resident_kernel(AjmPass p) {
     if (row >= 0)
         for (unsigned rk = 0; rk < G; ++rk)
             if (row >= s_win[rk][0] && row <= s_win[rk][1]) dmask |= 1u << rk;
+    // every thread keeps the control state in registers: every warp reduces the CTA records in the
+    // same order and runs the same control step, so no thread waits for another to publish it
+    AjmState ls = s_st;
     int pass = 0;
     for (; pass < p.max_passes; ++pass) {
-        if (s_st.done) break;
-        const int restart_t = s_st.restart_t;
-        const double beta = s_st.beta;
-        const double* xr = (pass & 1) ? xs1 : xs0;  // x~^t, all rows
+        if (ls.done) break;
+        const int restart_t = ls.restart_t;
+        const double beta = ls.beta;
+        const double* xr = (pass & 1) ? xs1 : xs0;  // x~^t (this CTA's window)
         double* xw = (pass & 1) ? xs0 : xs1;        // receives x~^{t+1}
         AjmAcc acc = {0.0, 0.0, 0.0, 0.0, 0.0};
         double q = 0.0, xn = 0.0;
         if (row >= 0) {
-            for (int k0 = 0; k0 < w; k0 += 8) {  // ascending column order; a batch's loads first
-                double v[8], xg[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const bool in = k0 + j < w;
-                    const int e = e0 + 32 * (k0 + j);
-                    v[j] = in ? sv[e] : 0.0;
-                    xg[j] = in ? xr[sc[e]] : 0.0;
-                }
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if (k0 + j < w) q += v[j] * xg[j];
+            // ascending column order, full batches of 8 then the exact remainder
+            int k0 = 0;
+            for (; k0 + 8 <= w; k0 += 8) ajm_res_part<8>(sv + e0 + 32 * k0, sc + e0 + 32 * k0, xr, q);
+            const double* sva = sv + e0 + 32 * k0;
+            const int* sca = sc + e0 + 32 * k0;
+            switch (w - k0) {
+                case 1: ajm_res_part<1>(sva, sca, xr, q); break;
+                case 2: ajm_res_part<2>(sva, sca, xr, q); break;
+                case 3: ajm_res_part<3>(sva, sca, xr, q); break;
+                case 4: ajm_res_part<4>(sva, sca, xr, q); break;
+                case 5: ajm_res_part<5>(sva, sca, xr, q); break;
+                case 6: ajm_res_part<6>(sva, sca, xr, q); break;
+                case 7: ajm_res_part<7>(sva, sca, xr, q); break;
+                default: break;
             }
             const double r = bi - q;
             acc.rr += r * r;
@@ -1985,45 +2002,29 @@ __global__ void __launch_bounds__(AJM_BLOCK, 1) ajm_resident_kernel(AjmPass p) {
                              ::"r"(la), "r"(rk), "d"(xn) : "memory");
             }
         }
-        ajm_block_reduce(acc, s_red);  // (lane 0 of warp 0 holds the CTA's sums)
-        if (warp == 0) {
-            // lane r pushes this CTA's five partials into CTA r's s_pall and arrives (release,
-            // cluster scope) on CTA r's barrier: that orders the partials and this CTA's replica
-            // stores (ordered before by the CTA barrier in ajm_block_reduce)
-            const double pr[AJM_NPART] = {__shfl_sync(0xffffffffu, acc.rr, 0), __shfl_sync(0xffffffffu, acc.xq, 0),
-                                          __shfl_sync(0xffffffffu, acc.bx, 0), __shfl_sync(0xffffffffu, acc.d, 0),
-                                          __shfl_sync(0xffffffffu, acc.dabs, 0)};
-            if (lane < (int)G) {
-                const uint32_t la = ajm_smem(&s_pall[pass & 1][bid][0]);
+        ajm_block_reduce(acc, s_red);  // (every lane of warp 0 holds the CTA's sums)
+        if (warp == 0 && lane < (int)G) {
+            // lane r pushes this CTA's five partials into CTA r's s_pall
+            const double pr[AJM_NPART] = {acc.rr, acc.xq, acc.bx, acc.d, acc.dabs};
+            const uint32_t la = ajm_smem(&s_pall[pass & 1][bid][0]);
 #pragma unroll
-                for (int k = 0; k < AJM_NPART; ++k)
-                    asm volatile("{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\tst.shared::cluster.f64 [ra], %2;\n\t}"
-                                 ::"r"(la + 8u * k), "r"((unsigned)lane), "d"(pr[k]) : "memory");
-                ajm_cluster_arrive(&s_cbar, (unsigned)lane);
-            }
-            double an_c = 0.0, beta_c = 0.0;
-            int to = 0;
-            if (lane == 0) {
-                const double a = s_st.alpha;
-                an_c = (1.0 + sqrt(1.0 + 4.0 * a * a)) / 2.0;
-                beta_c = s_st.momentum ? (a - 1.0) / an_c : 0.0;
-                to = ajm_cluster_wait(&s_cbar, (unsigned)(pass & 1), &c->timeout_flag) ? 1 : 0;
-            }
-            __syncwarp();
-            // the five totals: lane l holds CTA l's record, the same xor tree per component as the
-            // kCluster path's warp-per-component reduction (bitwise the same totals)
-            double tot[AJM_NPART];
-#pragma unroll
-            for (int k = 0; k < AJM_NPART; ++k) tot[k] = ajm_warp_sum(lane < (int)G ? s_pall[pass & 1][lane][k] : 0.0);
-            if (lane == 0) {
-                AjmState ls = s_st;
-                ajm_control_step(ls, tot, c, bid == 0, an_c, beta_c, sqrt(tot[0]) / ls.nb);
-                s_st = ls;
-                if (to) s_st.done = 1;
-            }
+            for (int k = 0; k < AJM_NPART; ++k)
+                asm volatile("{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\tst.shared::cluster.f64 [ra], %2;\n\t}"
+                             ::"r"(la + 8u * k), "r"((unsigned)lane), "d"(pr[k]) : "memory");
         }
-        ajm_csync();
-        if (!s_st.done) {  // the rotation of the buffers, in registers
+        // one cluster-wide barrier (release / acquire): every CTA's x~ stores and partials of this
+        // pass are visible everywhere after it.  (A hardware barrier: every CTA runs the same passes,
+        // so every CTA arrives; the launch-time exchange above uses it too.)
+        const double an_c = (1.0 + sqrt(1.0 + 4.0 * ls.alpha * ls.alpha)) / 2.0;
+        const double beta_c = ls.momentum ? (ls.alpha - 1.0) / an_c : 0.0;
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        // the five totals: lane l holds CTA l's record, the same xor tree per component as the
+        // kCluster path's warp-per-component reduction (bitwise the same totals), in every warp
+        double tot[AJM_NPART];
+#pragma unroll
+        for (int k = 0; k < AJM_NPART; ++k) tot[k] = ajm_warp_sum(lane < (int)G ? s_pall[pass & 1][lane][k] : 0.0);
+        ajm_control_step(ls, tot, c, bid == 0 && tid == 0, an_c, beta_c, sqrt(tot[0]) / ls.nb);
+        if (!ls.done) {  // the rotation of the buffers, in registers
             if (!restart_t) {
                 xp = xt;
                 qxp = q;
@@ -2033,11 +2034,11 @@ __global__ void __launch_bounds__(AJM_BLOCK, 1) ajm_resident_kernel(AjmPass p) {
     }
     // the state back to the buffers the control block names (the answer, and a later launch)
     if (row >= 0) {
-        ajm_sel(p, s_st.cur)[row] = xt;
-        ajm_sel(p, s_st.prev)[row] = xp;
+        ajm_sel(p, ls.cur)[row] = xt;
+        ajm_sel(p, ls.prev)[row] = xp;
         p.Qxp[row] = qxp;
     }
-    if (tid == 0 && bid == 0) c->s = s_st;
+    if (tid == 0 && bid == 0) c->s = ls;
     if (warp == 0) {  // no CTA leaves while another may still read its partials
         __syncwarp();
         if (lane < (int)G) ajm_cluster_arrive(&s_cexit, (unsigned)lane);
