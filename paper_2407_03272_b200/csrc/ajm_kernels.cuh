@@ -1614,6 +1614,7 @@ __global__ void __maxnreg__(96) ajm_band_kernel(AjmPass p) {
     __shared__ volatile int s_stop;  // the consumers left the pass loop
     __shared__ int s_pass;           // passes the consumers have started (release / acquire)
     __shared__ volatile int s_fin;   // passes run, written before s_stop
+    __shared__ int s_nbuf[2];        // x~ / x^{t-1} buffers of the pass the producer may stage next
     __shared__ int s_to;
     __shared__ __align__(16) long long s_bp[2 * AJM_CTAB];  // {Q_ij bits, stage byte offset} per code
     AjmCtrl* c = p.ctrl;
@@ -1669,8 +1670,8 @@ __global__ void __maxnreg__(96) ajm_band_kernel(AjmPass p) {
                     }
                     if (stop) break;
                     asm volatile("fence.proxy.async.global;" ::: "memory");
-                    xcur = ajm_sel(p, s_st.cur);
-                    xprv = ajm_sel(p, s_st.prev);
+                    xcur = ajm_sel(p, s_nbuf[0]);
+                    xprv = ajm_sel(p, s_nbuf[1]);
                 }
                 const int stage = (int)(cnt % kStages);
                 const unsigned par = (unsigned)((cnt / kStages) & 1) ^ 1u;
@@ -1790,6 +1791,15 @@ __global__ void __maxnreg__(96) ajm_band_kernel(AjmPass p) {
             an_c = (1.0 + sqrt(1.0 + 4.0 * a * a)) / 2.0;
             beta_c = s_st.momentum ? (a - 1.0) / an_c : 0.0;
             s_to = ajm_grid_wait(c, G, t) ? 1 : 0;
+            // every x~^{t+1} and Q x^t entry is written: the producer may stage the next pass now,
+            // overlapped with the partial reduction and the control step.  Its buffers follow from
+            // this pass's state alone (x~^{t+1} is in fre; x^t is x~^t, or x^{t-1} after a restart);
+            // if the control step ends the solve, the staged units are drained unread (s_fin).
+            if (!s_to && pass + 1 < p.max_passes) {
+                s_nbuf[0] = s_st.fre;
+                s_nbuf[1] = restart_t ? s_st.prev : s_st.cur;
+                ajm_sts_release(&s_pass, pass + 1);
+            }
         }
         ajm_csync();
         if (tsw) p.ts[pass * 8 + 3] = ajm_gtime();
@@ -1816,7 +1826,6 @@ __global__ void __maxnreg__(96) ajm_band_kernel(AjmPass p) {
             s_st = ls;
             if (s_to) s_st.done = 1;
             if (tsw) p.ts[pass * 8 + 5] = ajm_gtime();
-            if (!s_st.done) ajm_sts_release(&s_pass, pass + 1);  // the producer may stage pass + 1
         }
         ajm_csync();
     }
