@@ -75,8 +75,9 @@ SolveFn pair_fn(bool seg, int stages) {
     return seg ? ajm_solve_kernel<4, true, false, 0, false, 2> : ajm_solve_kernel<4, false, false, 0, false, 2>;
 }
 // banded staging (natural-order pair-coded stencils): ring depth 2-4 (stages of 12-30 KB)
-SolveFn band_fn(int stages) {
-    return stages >= 4 ? ajm_band_kernel<4> : stages == 3 ? ajm_band_kernel<3> : ajm_band_kernel<2>;
+SolveFn band_fn(int stages, int ku) {
+    if (ku == 16) return stages >= 3 ? ajm_band_kernel<3, 16> : ajm_band_kernel<2, 16>;
+    return stages >= 4 ? ajm_band_kernel<4, 8> : stages == 3 ? ajm_band_kernel<3, 8> : ajm_band_kernel<2, 8>;
 }
 // block-diagonal J (natural order, no segments), cooperative grid or single cluster
 SolveFn jblock_fn(int bs, bool cluster) {
@@ -1774,9 +1775,9 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
     mark("pair", st);
     // banded staging (ajm_band_kernel): natural-order pair-coded layouts without long
     // rows and with a diagonal D whose column offsets fall into <= AJM_MAX_BANDS bands of width
-    // <= 64 (offsets closer than 32 share a band): every operand of a 256-row unit is staged by
-    // the TMA -- x~ over each band, b, D, x^{t-1}, Q x^{t-1} -- next to its codes.  Same sums, same
-    // reduction order: bitwise the pair kernel (AJM_NO_BAND=1 keeps it, experiments / tests).
+    // <= 1024: every operand of a 256- or 512-row unit is staged by the TMA -- x~ over each band, b,
+    // D, x^{t-1}, Q x^{t-1} -- next to its codes.  Same sums, same reduction order: bitwise the pair
+    // kernel (AJM_NO_BAND=1 keeps it, experiments / tests).
     if (h->pair && !sh && h->nseg == 0 && !h->relabel && !h->jbs && !h->cluster && !h->gmeta && !h->resident &&
         getenv("AJM_NO_BAND") == nullptr && !(flags & AJM_NO_BAND_STAGING)) {
         std::vector<long long> pt(2 * (size_t)AJM_CTAB);
@@ -1789,59 +1790,76 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
         std::sort(ko.begin(), ko.end());
         ko.erase(std::unique(ko.begin(), ko.end()), ko.end());
         AjmBand bd = {};
-        bool ok = true;
+        int maxw = 0;
+        for (int64_t c = 0; c < h->nchunks; ++c) maxw = std::max<int>(maxw, (int)((choff[(size_t)c + 1] - choff[(size_t)c]) / 32));
         // two offset ranges share a band when the gap between them is below a unit's rows: the merged
         // band is then no longer than the two (config 2: the y-neighbour bands join the centre one,
         // 31.6 -> 28.5 us/pass; AJM_BAND_GAP overrides for experiments)
-        const long long gap = getenv("AJM_BAND_GAP") ? std::atoll(getenv("AJM_BAND_GAP")) : AJM_UNIT_ROWS;
-        for (size_t i = 0; i < ko.size() && ok; ++i) {
-            if (bd.nb > 0 && (long long)ko[i] - bd.hi[bd.nb - 1] <= gap) {
-                bd.hi[bd.nb - 1] = ko[i];
-            } else if (bd.nb < AJM_MAX_BANDS) {
-                bd.lo[bd.nb] = bd.hi[bd.nb] = ko[i];
-                bd.nb += 1;
-            } else {
-                ok = false;
+        // the band layout for units of ku chunks (32 ku rows); false if the offsets do not band
+        auto plan_band = [&](int ku, AjmBand& out) {
+            AjmBand q = {};
+            const int urows = 32 * ku;
+            const long long gap = getenv("AJM_BAND_GAP") ? std::atoll(getenv("AJM_BAND_GAP")) : urows;
+            for (size_t i = 0; i < ko.size(); ++i) {
+                if (q.nb > 0 && (long long)ko[i] - q.hi[q.nb - 1] <= gap) {
+                    q.hi[q.nb - 1] = ko[i];
+                } else if (q.nb < AJM_MAX_BANDS) {
+                    q.lo[q.nb] = q.hi[q.nb] = ko[i];
+                    q.nb += 1;
+                } else {
+                    return false;
+                }
             }
-        }
-        int maxw = 0;
-        for (int64_t c = 0; c < h->nchunks; ++c) maxw = std::max<int>(maxw, (int)((choff[(size_t)c + 1] - choff[(size_t)c]) / 32));
-        int xd = 0;
-        for (int b = 0; b < bd.nb && ok; ++b) {
-            if (bd.hi[b] - bd.lo[b] > 1024) ok = false;
-            bd.pos[b] = xd;
-            int len = AJM_UNIT_ROWS + (bd.hi[b] - bd.lo[b]) + 2;
-            xd += len + (len & 1);
-        }
-        bd.xdoubles = xd;
-        bd.code_bytes = (AJM_UNIT_ROWS * maxw + 15) / 16 * 16;
-        bd.stage_bytes = bd.code_bytes + 8 * bd.xdoubles + 4 * AJM_UNIT_ROWS * 8;
-        bd.n_pad = (int)h->n_pad;
+            int xd = 0;
+            for (int b = 0; b < q.nb; ++b) {
+                if (q.hi[b] - q.lo[b] > 1024) return false;
+                q.pos[b] = xd;
+                const int len = urows + (q.hi[b] - q.lo[b]) + 2;
+                xd += len + (len & 1);
+            }
+            q.urows = urows;
+            q.xdoubles = xd;
+            q.code_bytes = (urows * maxw + 15) / 16 * 16;
+            q.stage_bytes = q.code_bytes + 8 * q.xdoubles + 4 * urows * 8;
+            q.n_pad = (int)h->n_pad;
+            out = q;
+            return true;
+        };
         auto soff_of = [&](int off) {
             for (int b = 0; b < bd.nb; ++b)
                 if (off >= bd.lo[b] && off <= bd.hi[b]) return bd.pos[b] + off - bd.lo[b] + (bd.lo[b] & 1);
             return -1;
         };
-        bd.xt_soff = soff_of(0);
-        int stb = 0;
+        // (unit chunks, stages) in order of preference: the largest unit whose ring of >= 2 stages
+        // keeps ctas_per_sm CTAs resident (config 2: 16 x 3 22.3 us/pass, 16 x 2 22.9, 8 x 4 27.2;
+        // config 5's 27-wide 512-row stages do not fit, it takes 8 x 4); AJM_BAND_UNIT / AJM_BAND_STAGES
+        // restrict the search (experiments)
+        const int env_ku = getenv("AJM_BAND_UNIT") ? std::atoi(getenv("AJM_BAND_UNIT")) : 0;
+        const int smax = getenv("AJM_BAND_STAGES") ? std::max(2, std::min(4, std::atoi(getenv("AJM_BAND_STAGES")))) : 4;
+        const int cand[5][2] = {{16, 3}, {16, 2}, {8, 4}, {8, 3}, {8, 2}};
+        int stb = 0, kub = 0;
         size_t dynb = 0;
-        if (ok && h->n_pad < INT_MAX / 2) {
-            const int smax = getenv("AJM_BAND_STAGES") ? std::max(2, std::min(4, std::atoi(getenv("AJM_BAND_STAGES")))) : 4;
-            for (int sgs = smax; sgs >= 2 && !stb; --sgs) {
-                const size_t dyn = (size_t)sgs * (size_t)bd.stage_bytes + h->meta_bytes;
-                int occ = 0;
-                cudaError_t eo;
-                {
-                    std::lock_guard<std::mutex> lock(g_attr_mu);
-                    eo = fn_occupancy(band_fn(sgs), dyn, 100, &occ, block_threads(false));
-                }
-                CC(eo);
-                if (occ >= h->ctas_per_sm) {
-                    stb = sgs;
-                    dynb = dyn;
-                }
+        for (int ci = 0; ci < 5 && !stb && h->n_pad < INT_MAX / 2; ++ci) {
+            const int ku = cand[ci][0], sgs = cand[ci][1];
+            if ((env_ku && ku != env_ku) || sgs > smax) continue;
+            AjmBand q;
+            if (!plan_band(ku, q)) continue;
+            const size_t dyn = (size_t)sgs * (size_t)q.stage_bytes + h->meta_bytes;
+            int occ = 0;
+            cudaError_t eo;
+            {
+                std::lock_guard<std::mutex> lock(g_attr_mu);
+                eo = fn_occupancy(band_fn(sgs, ku), dyn, 100, &occ, block_threads(false));
+            }
+            CC(eo);
+            if (occ >= h->ctas_per_sm) {
+                stb = sgs;
+                kub = ku;
+                dynb = dyn;
+                bd = q;
             }
         }
+        bd.xt_soff = soff_of(0);
         if (stb) {
             bd.vpk = h->l2_mode == 3 ? 1 : (h->l2_mode >= 2 ? 2 : 0);
             bd.xpk = h->l2_mode >= 2 ? 2 : 0;
@@ -1858,7 +1876,7 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
             CC(cudaStreamSynchronize(st));
             h->bd = bd;
             h->band = 1;
-            h->fn = band_fn(stb);
+            h->fn = band_fn(stb, kub);
             h->dyn_smem = dynb;
             h->ring_stages = stb;
         }

@@ -115,6 +115,7 @@ struct AjmBand {
     int stage_bytes;               // code_bytes + 8 xdoubles + 4 * 256 * 8
     int xt_soff;                   // stage position of x~_row (offset 0) relative to the row's slot
     int n_pad;                     // length of the vector buffers (copies are clamped to [0, n_pad))
+    int urows;                     // rows per staging unit (32 kU)
     int vpk, xpk;                  // L2 policy kinds (ajm_policy) of the b/D/Qx and x~/x^{t-1} copies
     int lo[AJM_MAX_BANDS], hi[AJM_MAX_BANDS], pos[AJM_MAX_BANDS];
 };
@@ -1602,7 +1603,7 @@ __device__ __forceinline__ double ajm_chunk_dotb(uint32_t sca, int w, uint32_t x
     return s;
 }
 
-template <int kStages>
+template <int kStages, int kU>  // kU: chunks per staging unit (8 or 16; 256 or 512 rows)
 __global__ void __maxnreg__(96) ajm_band_kernel(AjmPass p) {
     extern __shared__ __align__(128) unsigned char s_dyn[];
     __shared__ double s_red[AJM_WARPS][AJM_NPART];
@@ -1626,7 +1627,8 @@ __global__ void __maxnreg__(96) ajm_band_kernel(AjmPass p) {
     const int cfirst = u1 > u0 ? p.unit_c0[u0] : 0;
     const int nchk = u1 > u0 ? p.unit_c0[u1] - cfirst : 0;
     const long long efirst = nchk > 0 ? p.chunk_off[cfirst] : 0;
-    const int nun = (nchk + AJM_WARPS - 1) / AJM_WARPS;  // units of 8 chunks
+    constexpr int UR = kU * 32;                    // rows per unit
+    const int nun = (nchk + kU - 1) / kU;          // units of kU chunks
     const size_t SB = (size_t)bd.stage_bytes;
     int* s_coff = reinterpret_cast<int*>(s_dyn + (size_t)kStages * SB);
     for (int i = tid; i <= nchk; i += blockDim.x) s_coff[i] = (int)(p.chunk_off[cfirst + i] - efirst);
@@ -1681,8 +1683,8 @@ __global__ void __maxnreg__(96) ajm_band_kernel(AjmPass p) {
                     if (++idle > (1LL << 28)) { atomicExch(&c->timeout_flag, 1u); stop = true; break; }
                 }
                 if (stop) break;
-                // unit uu: chunks [8 uu, min(8 uu + 8, nchk)) of the CTA
-                const int c0 = uu * AJM_WARPS, c1 = min(c0 + AJM_WARPS, nchk);
+                // unit uu: chunks [kU uu, min(kU uu + kU, nchk)) of the CTA
+                const int c0 = uu * kU, c1 = min(c0 + kU, nchk);
                 const int e0 = s_coff[c0], e1 = s_coff[c1];
                 const int r0 = (cfirst + c0) * 32, nr = (c1 - c0) * 32;
                 unsigned char* sb = s_dyn + (size_t)stage * SB;
@@ -1707,9 +1709,9 @@ __global__ void __maxnreg__(96) ajm_band_kernel(AjmPass p) {
                         ajm_bulk_g2s(xa + bd.pos[b] + (ca - a), xcur + ca, 8u * (unsigned)(ce - ca), &s_full[stage], xpol);
                 }
                 ajm_bulk_g2s(so, p.b + r0, 8u * nr, &s_full[stage], vpol);
-                ajm_bulk_g2s(so + 256, p.D + r0, 8u * nr, &s_full[stage], vpol);
-                ajm_bulk_g2s(so + 512, xprv + r0, 8u * nr, &s_full[stage], xpol);
-                ajm_bulk_g2s(so + 768, p.Qxp + r0, 8u * nr, &s_full[stage], vpol);
+                ajm_bulk_g2s(so + UR, p.D + r0, 8u * nr, &s_full[stage], vpol);
+                ajm_bulk_g2s(so + 2 * UR, xprv + r0, 8u * nr, &s_full[stage], xpol);
+                ajm_bulk_g2s(so + 3 * UR, p.Qxp + r0, 8u * nr, &s_full[stage], vpol);
                 ++cnt;
                 if (++uu == nun) uu = 0;
             }
@@ -1744,23 +1746,27 @@ __global__ void __maxnreg__(96) ajm_band_kernel(AjmPass p) {
         for (int uu = 0; uu < nun; ++uu) {
             const int stage = (int)((ucnt + uu) % kStages);
             const unsigned par = (unsigned)(((ucnt + uu) / kStages) & 1);
-            const int j = uu * AJM_WARPS + warp;
             ajm_mbar_wait(&s_full[stage], par, &c->timeout_flag);
-            if (j < nchk) {
-                const unsigned char* sb = s_dyn + (size_t)stage * SB;
-                const double* xa = reinterpret_cast<const double*>(sb + bd.code_bytes);
-                const double* so = xa + bd.xdoubles;
-                const int lrow = warp * 32 + lane;  // the row's slot in the unit
-                const int row = (cfirst + j) * 32 + lane;
-                const int e0 = s_coff[j];
-                const int w = (s_coff[j + 1] - e0) >> 5;
-                const uint32_t sca = ajm_smem(sb) + (uint32_t)(e0 - s_coff[uu * AJM_WARPS]) + (uint32_t)lane;
-                const uint32_t xrow = ajm_smem(xa) + 8u * (uint32_t)lrow;
-                const double q = ajm_chunk_dotb(sca, w, xrow, taba);
-                if (row < p.n_sell) {
-                    const double bi = so[lrow], Di = so[256 + lrow], xpi = so[512 + lrow], qxp = so[768 + lrow];
-                    const double xt = xa[bd.xt_soff + lrow];
-                    ajm_row_update(p.Qxp, xf, row, q, bi, Di, xt, xpi, qxp, beta, restart_t, acc, vpol, xpol);
+            const unsigned char* sb = s_dyn + (size_t)stage * SB;
+            const double* xa = reinterpret_cast<const double*>(sb + bd.code_bytes);
+            const double* so = xa + bd.xdoubles;
+            const int cu = uu * kU;  // the unit's first chunk
+#pragma unroll
+            for (int h = 0; h < kU / AJM_WARPS; ++h) {  // chunk j -> warp j % 8, as in the pair kernel
+                const int j = cu + h * AJM_WARPS + warp;
+                if (j < nchk) {
+                    const int lrow = (j - cu) * 32 + lane;  // the row's slot in the unit
+                    const int row = (cfirst + j) * 32 + lane;
+                    const int e0 = s_coff[j];
+                    const int w = (s_coff[j + 1] - e0) >> 5;
+                    const uint32_t sca = ajm_smem(sb) + (uint32_t)(e0 - s_coff[cu]) + (uint32_t)lane;
+                    const uint32_t xrow = ajm_smem(xa) + 8u * (uint32_t)lrow;
+                    const double q = ajm_chunk_dotb(sca, w, xrow, taba);
+                    if (row < p.n_sell) {
+                        const double bi = so[lrow], Di = so[UR + lrow], xpi = so[2 * UR + lrow], qxp = so[3 * UR + lrow];
+                        const double xt = xa[bd.xt_soff + lrow];
+                        ajm_row_update(p.Qxp, xf, row, q, bi, Di, xt, xpi, qxp, beta, restart_t, acc, vpol, xpol);
+                    }
                 }
             }
             __syncwarp();
