@@ -1583,9 +1583,12 @@ __device__ __forceinline__ void ajm_dotb_part(uint32_t sca, uint32_t xrow, uint3
 // the table holds the x~ stage offsets in BYTES
 __device__ __forceinline__ double ajm_chunk_dotb(uint32_t sca, int w, uint32_t xrow, uint32_t taba) {
     double s = 0.0;
-    if (w == 7) {
-        ajm_dotb_part<7>(sca, xrow, taba, s);
-        return s;
+    switch (w) {  // the stencils' narrow widths in one jump (7-point: 7, boundary planes 6 / 5 / 4)
+        case 4: ajm_dotb_part<4>(sca, xrow, taba, s); return s;
+        case 5: ajm_dotb_part<5>(sca, xrow, taba, s); return s;
+        case 6: ajm_dotb_part<6>(sca, xrow, taba, s); return s;
+        case 7: ajm_dotb_part<7>(sca, xrow, taba, s); return s;
+        default: break;
     }
     int k0 = 0;
     for (; k0 + 8 <= w; k0 += 8) ajm_dotb_part<8>(sca + 32u * k0, xrow, taba, s);
