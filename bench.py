@@ -9,10 +9,12 @@ value = whole-job AJM iterations/s (sum over ranks of iterations / max-over-rank
 
 --impl reference times the CPU oracle (oracle/, plain C, literal two-SpMV Alg. 3) on this box's
 host cores on a bounded sample of the same workload (this tier's reference arm).
-Multi-GPU (torchrun, one process per GPU): the paper's row-block partition (Alg. 3 lines 3-5,
-§4.4) -- ONE solve of the same system sharded over the N GPUs, halo entries and the
-five partial sums exchanged every pass over peer memory (CUDA IPC / NVLink) by the solver kernel
-itself, "scaling": "strong".  --parallel replicas runs N independent solves instead ("weak").
+Multi-GPU (torchrun, one process per GPU): by default N independent replicas of the solve, one per
+GPU ("scaling": "weak") -- the north_star's path is one GPU and SURVEY.md §8(e) says "replicas
+only".  --parallel shard runs the paper's row-block partition instead (Alg. 3 lines 3-5, §4.4;
+DESIGN.md §6): ONE solve of the same system sharded over the N GPUs, halo entries and the five
+partial sums exchanged every pass over peer memory (CUDA IPC / NVLink) by the solver kernel
+itself ("scaling": "strong").
 """
 from __future__ import annotations
 
@@ -621,8 +623,9 @@ def main(argv=None):
     ap.add_argument("--jblock", type=int, default=None,
                     help="block-diagonal J of eq-J-blkdiag with this block size (default: eq-J-diag)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--parallel", default="shard", choices=["shard", "replicas"],
-                    help="N > 1: one row-block sharded solve (strong scaling) or N independent replicas")
+    ap.add_argument("--parallel", default="replicas", choices=["shard", "replicas"],
+                    help="N > 1: N independent replicas (default, weak scaling; SURVEY §8(e)) or one "
+                         "row-block sharded solve (strong scaling, DESIGN.md §6)")
     ap.add_argument("--other-configs", default="1,3,4,5",
                     help="with the default --config 2 at N=1: also measure these BASELINE configs "
                          "(comma list, '' = none) and report them under other_configs")
