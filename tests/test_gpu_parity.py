@@ -467,3 +467,24 @@ def test_resident_cluster_bitwise():
         d = gpu_solve(p.Q, p.b, tol=1e-6, maxit=5000, restart=restart)
         od = oracle.solve(p.Q, p.b, tol=1e-6, maxit=5000, restart=restart)
         assert abs(d.iterations - od.iterations) <= 1
+
+
+@pytest.mark.parametrize("unit", ["8", "16"])
+def test_band_staging_units_bitwise(unit, monkeypatch):
+    """The banded staging kernel with staging units of 8 and of 16 chunks (256 / 512
+    rows; AJM_BAND_UNIT restricts create's search) gives bitwise the iterates, residual / f / d
+    histories of the register-gather pair kernel (AJM_NO_BAND_STAGING), on a ragged 3D stencil
+    with restarts, through the persistent launch and the host-driven loop."""
+    p = synth.make_problem("p3d81", synth.poisson3d(81), 8)  # n = 531441: several units per CTA, ragged tail
+    monkeypatch.setenv("AJM_BAND_UNIT", unit)
+    a = gpu_solve(p.Q, p.b, tol=0.0, maxit=500, restart=True)
+    h = gpu_solve(p.Q, p.b, tol=0.0, maxit=120, restart=True, loop="host")
+    monkeypatch.delenv("AJM_BAND_UNIT")
+    assert a.info["band_staged"] == 1 and a.info["val_bytes"] == 0, a.info
+    r = gpu_solve(p.Q, p.b, tol=0.0, maxit=500, restart=True, band_staging=False)
+    assert r.info["band_staged"] == 0
+    for f in ("x", "res_hist", "f_hist", "d_trace"):
+        np.testing.assert_array_equal(getattr(a, f), getattr(r, f))
+    np.testing.assert_array_equal(h.res_hist, r.res_hist[:121])
+    o, _ = oracle_matching(p.Q, p.b, a, tol=0.0, maxit=500, restart=True)
+    assert max_rel(a.x, o.x) <= PARITY_TOL
