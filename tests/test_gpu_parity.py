@@ -488,3 +488,25 @@ def test_band_staging_units_bitwise(unit, monkeypatch):
     np.testing.assert_array_equal(h.res_hist, r.res_hist[:121])
     o, _ = oracle_matching(p.Q, p.b, a, tol=0.0, maxit=500, restart=True)
     assert max_rel(a.x, o.x) <= PARITY_TOL
+
+
+@pytest.mark.parametrize("case", ["p2d400", "aniso27_40", "p3d_bands17"])
+def test_band_staging_stencils(case):
+    """Banded staging on other stencil shapes: a 2D 5-point grid whose +-400 rows stay separate
+    bands of a 512-row unit, the anisotropic 27-point stencil (nine offset lines in three bands,
+    several boundary diagonals among the pairs), and a 7-point 17^3 grid (ragged, few units per CTA)
+    -- bitwise the register-gather pair kernel, and at parity with the oracle."""
+    if case == "p2d400":
+        p = synth.make_problem(case, synth.poisson2d(400), 9)
+    elif case == "aniso27_40":
+        p = synth.make_problem(case, synth.aniso27(40), 10)
+    else:
+        p = synth.make_problem(case, synth.poisson3d(17), 11)
+    a = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True)
+    assert a.info["band_staged"] == 1 and a.info["val_bytes"] == 0, a.info
+    r = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True, band_staging=False)
+    for f in ("x", "res_hist", "f_hist", "d_trace"):
+        np.testing.assert_array_equal(getattr(a, f), getattr(r, f))
+    o, _ = oracle_matching(p.Q, p.b, a, tol=0.0, maxit=400, restart=True)
+    assert max_rel(a.x, o.x) <= PARITY_TOL
+    assert_history_parity(a, o)
