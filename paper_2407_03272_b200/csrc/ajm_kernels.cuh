@@ -1880,7 +1880,7 @@ __global__ void __launch_bounds__(AJM_BLOCK, 1) ajm_resident_kernel(AjmPass p) {
     // by pass parity: after the barrier the reduction reads only local shared memory
     __shared__ double s_pall[2][16][AJM_NPART];
     __shared__ AjmState s_st;
-    __shared__ __align__(8) uint64_t s_cbar;
+    __shared__ __align__(8) uint64_t s_xbar[2];  // per pass parity: the pass's remote data has landed
     __shared__ __align__(8) uint64_t s_cexit;
     __shared__ int s_win[16][2];  // every CTA's x~ window [lo, hi] (the columns its rows gather)
     __shared__ int s_wlo, s_whi;
@@ -1904,7 +1904,8 @@ __global__ void __launch_bounds__(AJM_BLOCK, 1) ajm_resident_kernel(AjmPass p) {
     }
     if (tid == 0) {
         s_st = c->s;
-        ajm_mbar_init(&s_cbar, G);
+        ajm_mbar_init(&s_xbar[0], 1);
+        ajm_mbar_init(&s_xbar[1], 1);
         ajm_mbar_init(&s_cexit, G);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -1966,12 +1967,20 @@ __global__ void __launch_bounds__(AJM_BLOCK, 1) ajm_resident_kernel(AjmPass p) {
     if (row >= 0)
         for (unsigned rk = 0; rk < G; ++rk)
             if (row >= s_win[rk][0] && row <= s_win[rk][1]) dmask |= 1u << rk;
+    // bytes this CTA receives per pass: the x~ entries of its window (each from its owner) and every
+    // CTA's five partials -- all as st.async stores completing on s_xbar, so the data and the
+    // synchronisation arrive together (no release fence, no cluster barrier per pass)
+    const int wl = max(s_wlo, 0), wh = min(s_whi, p.n_sell - 1);
+    const unsigned rx_bytes = 8u * (unsigned)max(0, wh - wl + 1) + 8u * AJM_NPART * G;
     // every thread keeps the control state in registers: every warp reduces the CTA records in the
     // same order and runs the same control step, so no thread waits for another to publish it
     AjmState ls = s_st;
     int pass = 0;
     for (; pass < p.max_passes; ++pass) {
         if (ls.done) break;
+        // arm this pass's barrier: one local arrival + the bytes the other CTAs' st.async deliver
+        // (complete_tx may already have run ahead; the phase needs the arrival too)
+        if (tid == 0) ajm_mbar_expect_tx(&s_xbar[pass & 1], rx_bytes);
         const int restart_t = ls.restart_t;
         const double beta = ls.beta;
         const double* xr = (pass & 1) ? xs1 : xs0;  // x~^t (this CTA's window)
@@ -2013,29 +2022,29 @@ __global__ void __launch_bounds__(AJM_BLOCK, 1) ajm_resident_kernel(AjmPass p) {
             acc.d += term;
             acc.dabs += fabs(term);
             // publish x~^{t+1}_row to the replicas whose windows hold it
-            const uint32_t la = ajm_smem(xw + row);
+            const uint32_t la = ajm_smem(xw + row), lb = ajm_smem(&s_xbar[pass & 1]);
             for (unsigned m = dmask; m; m &= m - 1u) {
                 const unsigned rk = (unsigned)__ffs(m) - 1u;
-                asm volatile("{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\tst.shared::cluster.f64 [ra], %2;\n\t}"
-                             ::"r"(la), "r"(rk), "d"(xn) : "memory");
+                asm volatile("{\n\t.reg .b32 ra, rb;\n\tmapa.shared::cluster.u32 ra, %0, %2;\n\tmapa.shared::cluster.u32 rb, %1, %2;\n\t"
+                             "st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [ra], %3, [rb];\n\t}"
+                             ::"r"(la), "r"(lb), "r"(rk), "d"(xn) : "memory");
             }
         }
         ajm_block_reduce(acc, s_red);  // (every lane of warp 0 holds the CTA's sums)
         if (warp == 0 && lane < (int)G) {
             // lane r pushes this CTA's five partials into CTA r's s_pall
             const double pr[AJM_NPART] = {acc.rr, acc.xq, acc.bx, acc.d, acc.dabs};
-            const uint32_t la = ajm_smem(&s_pall[pass & 1][bid][0]);
+            const uint32_t la = ajm_smem(&s_pall[pass & 1][bid][0]), lb = ajm_smem(&s_xbar[pass & 1]);
 #pragma unroll
             for (int k = 0; k < AJM_NPART; ++k)
-                asm volatile("{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\tst.shared::cluster.f64 [ra], %2;\n\t}"
-                             ::"r"(la + 8u * k), "r"((unsigned)lane), "d"(pr[k]) : "memory");
+                asm volatile("{\n\t.reg .b32 ra, rb;\n\tmapa.shared::cluster.u32 ra, %0, %2;\n\tmapa.shared::cluster.u32 rb, %1, %2;\n\t"
+                             "st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [ra], %3, [rb];\n\t}"
+                             ::"r"(la + 8u * k), "r"(lb), "r"((unsigned)lane), "d"(pr[k]) : "memory");
         }
-        // one cluster-wide barrier (release / acquire): every CTA's x~ stores and partials of this
-        // pass are visible everywhere after it.  (A hardware barrier: every CTA runs the same passes,
-        // so every CTA arrives; the launch-time exchange above uses it too.)
         const double an_c = (1.0 + sqrt(1.0 + 4.0 * ls.alpha * ls.alpha)) / 2.0;
         const double beta_c = ls.momentum ? (ls.alpha - 1.0) / an_c : 0.0;
-        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        // this pass's x~ entries of the window and all partials have landed (bounded wait)
+        ajm_mbar_wait(&s_xbar[pass & 1], (unsigned)((pass >> 1) & 1), &c->timeout_flag);
         // the five totals: lane l holds CTA l's record, the same xor tree per component as the
         // kCluster path's warp-per-component reduction (bitwise the same totals), in every warp
         double tot[AJM_NPART];
