@@ -543,6 +543,7 @@ __device__ __forceinline__ void ajm_grid_arrive(AjmCtrl* c) {
 }
 // Wait (thread 0) until pass t's arrivals reach (t+1)*G; the trailing gpu-scope fence also
 // invalidates this SM's L1.  Returns true on a (never expected) timeout.
+template <bool kFence = true>
 __device__ __forceinline__ bool ajm_grid_wait(AjmCtrl* c, unsigned nblocks, long long t) {
     const unsigned long long target = (unsigned long long)(t + 1) * nblocks;
     long long spins = 0;
@@ -554,7 +555,7 @@ __device__ __forceinline__ bool ajm_grid_wait(AjmCtrl* c, unsigned nblocks, long
             break;
         }
     }
-    __threadfence();
+    if (kFence) __threadfence();
     return to;
 }
 
@@ -1799,7 +1800,9 @@ __global__ void __maxnreg__(96) ajm_band_kernel(AjmPass p) {
             const double a = s_st.alpha;
             an_c = (1.0 + sqrt(1.0 + 4.0 * a * a)) / 2.0;
             beta_c = s_st.momentum ? (a - 1.0) / an_c : 0.0;
-            s_to = ajm_grid_wait(c, G, t) ? 1 : 0;
+            // (no trailing fence: this kernel reads other CTAs' data only through the TMA and
+            //  L2-only loads, never through this SM's L1)
+            s_to = ajm_grid_wait<false>(c, G, t) ? 1 : 0;
             // every x~^{t+1} and Q x^t entry is written: the producer may stage the next pass now,
             // overlapped with the partial reduction and the control step.  Its buffers follow from
             // this pass's state alone (x~^{t+1} is in fre; x^t is x~^t, or x^{t-1} after a restart);
