@@ -329,7 +329,10 @@ def roofline_block(p, info, passes, loop_ms, steps, bound, jblock=None):
                         best save on the stream
       dram_frac       : ncu dram read+write bytes per pass of the committed capture
                         (profiles/ncu_traffic.json, per workload) over this run's time per pass --
-                        the L2-resident vectors make it lower than the algorithmic figure"""
+                        the L2-resident vectors make it lower than the algorithmic figure
+      l2_throughput_frac / l1tex_throughput_frac : the same capture's lts / l1tex throughput (% of
+                        peak / 100): the graph configs lean on the L2 (random 32-byte gather
+                        sectors), the band-staged stencils on the L1/shared-memory pipe"""
     peak, peak_src = load_peaks()
     model_bytes = info["model_bytes_per_iter"]
     sec = loop_ms * 1e-3
@@ -348,7 +351,10 @@ def roofline_block(p, info, passes, loop_ms, steps, bound, jblock=None):
                             "row with --jblock) x passes / launch duration (CUDA events on the launch stream)",
           "layout_bytes_per_iteration": lay,
           "layout_frac": lay * passes / sec / 1e9 / peak,
-          "dram_frac": None if tr is None else tr["dram_bytes_per_pass"] / (us * 1e-6) / 1e9 / peak}
+          "dram_frac": None if tr is None else tr["dram_bytes_per_pass"] / (us * 1e-6) / 1e9 / peak,
+          # the capture's other roofs: which on-chip resource the kernel actually leans on
+          "l2_throughput_frac": None if tr is None or "l2_throughput_pct" not in tr else tr["l2_throughput_pct"] / 100.0,
+          "l1tex_throughput_frac": None if tr is None or "l1tex_throughput_pct" not in tr else tr["l1tex_throughput_pct"] / 100.0}
     return rb, model_bytes, achieved, us
 
 

@@ -77,6 +77,9 @@ def main():
             rec[f"dram_bytes_per_pass_{kind}"] = dram
             rec[f"us_per_pass_profiled_{kind}"] = 1e6 * dd["gpu__time_duration.sum"] / PASSES
         rec["dram_bytes_per_pass"] = rec.get("dram_bytes_per_pass_warm", rec.get("dram_bytes_per_pass_cold"))
+        # the other roofs of the same capture: L2 (lts) and L1/shared (l1tex) throughput, % of peak
+        rec["l2_throughput_pct"] = d["lts__throughput.avg.pct_of_peak_sustained_elapsed"]
+        rec["l1tex_throughput_pct"] = d["l1tex__throughput.avg.pct_of_peak_sustained_active"]
         rec["source"] = (f"ncu --set full --clock-control none [--cache-control none for 'warm'] on tools/prof.py {c} 30 "
                          f"(2nd solve); profiles/{tag}_ncu_configs.md")
         traffic.append(rec)
