@@ -510,3 +510,22 @@ def test_band_staging_stencils(case):
     o, _ = oracle_matching(p.Q, p.b, a, tol=0.0, maxit=400, restart=True)
     assert max_rel(a.x, o.x) <= PARITY_TOL
     assert_history_parity(a, o)
+
+
+def test_band_staging_x0_and_early_exits():
+    """Banded staging with a nonzero x0 (staged from the caller's buffer), a solve that converges at
+    t = 0 (the producer has already staged pass 1, drained unread), maxit = 1, and a converged solve
+    followed by another on the same handle: bitwise the pair kernel each time."""
+    p = synth.make_problem("p3d40", synth.poisson3d(40), 12)
+    x0 = synth.random_vector(p.Q.n, 5)
+    kws = [dict(x0=x0, tol=0.0, maxit=300), dict(tol=10.0, maxit=50), dict(tol=0.0, maxit=1),
+           dict(x0=x0, tol=1e-6, maxit=2000)]
+    import paper_2407_03272_b200 as ajm
+    with ajm.Solver.from_csr(p.Q, p.b) as a, ajm.Solver.from_csr(p.Q, p.b, band_staging=False) as r:
+        assert a.info()["band_staged"] == 1 and r.info()["band_staged"] == 0
+        for kw in kws:
+            ga, gr = a.solve(restart=True, **kw), r.solve(restart=True, **kw)
+            assert ga.status == gr.status and ga.iterations == gr.iterations, (kw, ga.iterations, gr.iterations)
+            np.testing.assert_array_equal(ga.x.cpu().numpy(), gr.x.cpu().numpy())
+            np.testing.assert_array_equal(ga.res_hist, gr.res_hist)
+    assert kws and ga.status == "converged"
