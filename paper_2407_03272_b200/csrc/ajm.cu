@@ -87,6 +87,11 @@ SolveFn jblock_fn(int bs, bool cluster) {
     return bs == 2 ? ajm_solve_kernel<4, false, false, 2> : bs == 4 ? ajm_solve_kernel<4, false, false, 4>
          : bs == 8 ? ajm_solve_kernel<4, false, false, 8> : ajm_solve_kernel<4, false, false, -1>;
 }
+// block-diagonal J on pair-coded entries (natural-order stencils; 1-byte stages)
+SolveFn jblock_pair_fn(int bs) {
+    return bs == 2 ? ajm_solve_kernel<4, false, false, 2, false, 2> : bs == 4 ? ajm_solve_kernel<4, false, false, 4, false, 2>
+         : bs == 8 ? ajm_solve_kernel<4, false, false, 8, false, 2> : ajm_solve_kernel<4, false, false, -1, false, 2>;
+}
 SolveFn gmeta_fn(bool seg) { return seg ? ajm_solve_kernel<4, true, false, 0, true> : ajm_solve_kernel<4, false, false, 0, true>; }
 SolveFn cluster_fn(bool seg) { return seg ? ajm_solve_kernel<4, true, true> : ajm_solve_kernel<4, false, true>; }
 
@@ -1634,7 +1639,11 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
     // byte-coded columns: when the offsets col - row of the SELL entries take at most
     // AJM_CTAB distinct values (stencils: 7 / 27), stream one byte per entry instead of an int32
     // column (12 -> 9 bytes per stored entry) -- plain-ring variant-0 layouts only
-    if (h->nchunks > 0 && h->ring_fn && !h->cluster && !h->gmeta && !h->jbs && !(flags & AJM_INT32_COLUMNS)) {
+    // (block J: there is no value-streamed byte-coded block-J kernel, so the codes are built with the
+    //  int32 columns kept, and committed only if the pair coding below succeeds)
+    bool jb_pending = false;
+    if (h->nchunks > 0 && (h->ring_fn || (h->jbs && !sh)) && !h->cluster && !h->gmeta && !(flags & AJM_INT32_COLUMNS) &&
+        !(h->jbs && (flags & AJM_VALUE_STREAM))) {
         const int ns = (int)(h->nchunks * 32);
         int* tmp = nullptr;
         CC(dalloc(&tmp, AJM_CTAB_HASH + 2, st));
@@ -1667,6 +1676,7 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
             }
             CC(eo);
         }
+        if (h->jbs && htab[AJM_CTAB_HASH + 1] == 0 && htab[AJM_CTAB_HASH] <= AJM_CTAB) occ8 = h->ctas_per_sm;
         if (occ8 >= h->ctas_per_sm && occ8 > 0) {
             std::vector<int> keys;
             for (int i = 0; i < AJM_CTAB_HASH; ++i)
@@ -1680,11 +1690,15 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
             ajm_coloff_encode_kernel<<<(ns + 255) / 256, 256, 0, st>>>(ns, (int)h->n_sell, h->chunk_off, h->scol,
                                                                         h->ctab, m, h->scode);
             CC(cudaGetLastError());
-            CC(cudaFreeAsync(h->scol, st));
-            h->scol = nullptr;
-            h->fn = f8;
-            h->dyn_smem = dyn8;
-            h->ring_stages = st8;
+            if (h->jbs) {
+                jb_pending = true;  // the int32 columns stay until the pair coding commits
+            } else {
+                CC(cudaFreeAsync(h->scol, st));
+                h->scol = nullptr;
+                h->fn = f8;
+                h->dyn_smem = dyn8;
+                h->ring_stages = st8;
+            }
             h->col_bytes = 1;
         }
         CC(cudaStreamSynchronize(st));  // keys / htab live until the copies have run
@@ -1742,8 +1756,8 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
             // more than AJM_CTAB pairs (pt cleared) or none: keep the values streamed
             if (!pt.empty()) {
                 const char* es = getenv("AJM_PAIR_STAGES");  // (experiments) 4 or 8
-                const int stp = es ? (std::atoi(es) >= 8 ? 8 : 4) : (h->wide_rows ? 8 : 4);
-                SolveFn fp = pair_fn(h->nseg > 0, stp);
+                const int stp = h->jbs ? 4 : es ? (std::atoi(es) >= 8 ? 8 : 4) : (h->wide_rows ? 8 : 4);
+                SolveFn fp = h->jbs ? jblock_pair_fn(h->jbs) : pair_fn(h->nseg > 0, stp);
                 const size_t dynp = (size_t)stp * AJM_UNIT_EL * 1 + h->meta_bytes;
                 int occp = 0;
                 cudaError_t eo;
@@ -1761,6 +1775,11 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
                     CC(cudaGetLastError());
                     CC(cudaFreeAsync(h->sval, st));
                     h->sval = nullptr;
+                    if (jb_pending) {  // block J: the pair coding commits, the int32 columns go
+                        CC(cudaFreeAsync(h->scol, st));
+                        h->scol = nullptr;
+                        jb_pending = false;
+                    }
                     h->fn = fp;
                     h->dyn_smem = dynp;
                     h->ring_stages = stp;
@@ -1771,6 +1790,14 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
             CC(cudaFreeAsync(fl, st));
         }
         CC(cudaFreeAsync(vt, st));
+    }
+    if (jb_pending) {  // block J without a pair coding: back to the int32 columns
+        CC(cudaStreamSynchronize(st));
+        CC(cudaFreeAsync(h->scode, st));
+        CC(cudaFreeAsync(h->ctab, st));
+        h->scode = nullptr;
+        h->ctab = nullptr;
+        h->col_bytes = 4;
     }
     mark("pair", st);
     // banded staging (ajm_band_kernel): natural-order pair-coded layouts without long

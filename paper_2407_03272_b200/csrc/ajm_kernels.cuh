@@ -1052,7 +1052,8 @@ __global__ void __maxnreg__(kProd ? 96 : 128) ajm_solve_kernel(AjmPass p0) {
     // stage s: val[UNIT_EL] f64 | col[UNIT_EL] i32 (kCol8 1: code[UNIT_EL] u8; kCol8 2: code only)
     constexpr unsigned el_bytes = kCol8 == 2 ? 1u : (kCol8 ? 9u : 12u);
     constexpr size_t stage_bytes = (size_t)AJM_UNIT_EL * el_bytes;
-    static_assert(!kCol8 || (!jblk && !kCluster && !kGMeta), "byte-coded columns: plain ring variant only");
+    static_assert(!kCol8 || (!kCluster && !kGMeta && (!jblk || kCol8 == 2)),
+                  "byte-coded columns: plain ring variants (block J: pair-coded only)");
     auto st_val = [&](int k) { return reinterpret_cast<double*>(s_dyn + (size_t)k * stage_bytes); };
     auto st_col = [&](int k) { return reinterpret_cast<int*>(s_dyn + (size_t)k * stage_bytes + (size_t)AJM_UNIT_EL * 8); };
     auto st_code = [&](int k) { return s_dyn + (size_t)k * stage_bytes + (kCol8 == 2 ? (size_t)0 : (size_t)AJM_UNIT_EL * 8); };

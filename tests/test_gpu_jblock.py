@@ -89,3 +89,19 @@ def test_jblock_errors():
     with pytest.raises(ajm.AjmError) as e:
         ajm.Solver.from_csr(P, np.ones(64), jblock=3)
     assert e.value.status_name == "AJM_ERR_INVALID_ARG"
+
+
+@pytest.mark.parametrize("bs", [2, 4, 8, 16])
+def test_jblock_pair_coded_bitwise(bs):
+    """Block J on a constant-coefficient stencil takes the pair-coded layout (one byte per entry
+    names value and column offset): bitwise the iterates and histories of the same
+    block-J solve on int32 columns, and at parity with the oracle."""
+    p = synth.make_problem("p3d36", synth.poisson3d(36), 13)  # n = 46656, several units per CTA
+    a = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True, jblock=bs)
+    assert a.info["val_bytes"] == 0 and a.info["col_bytes"] == 1, a.info
+    r = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True, jblock=bs, int32_columns=True)
+    assert r.info["val_bytes"] == 8 and r.info["col_bytes"] == 4
+    for f in ("x", "res_hist", "f_hist", "d_trace"):
+        np.testing.assert_array_equal(getattr(a, f), getattr(r, f))
+    o, _ = oracle_matching(p.Q, p.b, a, tol=0.0, maxit=400, restart=True, jblock=bs)
+    assert max_rel(a.x, o.x) <= PARITY_TOL
