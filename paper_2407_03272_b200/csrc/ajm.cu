@@ -247,6 +247,9 @@ struct ajm_ctx {
     int band = 0;               // 1: ajm_band_kernel (x~ bands and row operands staged by the TMA)
     AjmBand bd = {};            // its band layout
     long long* bptab = nullptr; // [AJM_CTAB][2] {value bits, stage offset} of the pair codes
+    int* band_c0 = nullptr;     // [grid+1] first SELL chunk of each band-kernel CTA
+    int* smid = nullptr;        // [grid] placement probe output (SM of each CTA)
+    double band_skew = 0.0;     // work skew applied between the two CTAs sharing an SM (0: none)
     int ring_stages = 4;        // TMA ring depth of the chosen solver kernel
     bool seg_fn = true;         // the chosen plain/col8 ring kernel has the segment phases
     bool ring_fn = false;       // h->fn is a ring_fn/col8_fn kernel (ring depth selectable)
@@ -379,7 +382,8 @@ void free_all(ajm_ctx* h) {
                     h->seg_split, h->seg_part, h->split_row, h->split_seg0, h->split_cnt,
                     h->cta_split, h->owner_split, h->unit_c0, h->cta_seg, h->seg_list, h->cta_unit, h->partials, h->ctrl,
                     h->hist, h->scratch, h->err, h->ts, h->perm_fwd, h->perm_inv, h->b_in, h->Jblk, h->Jinv, h->seg_order, h->seg_grp,
-                    h->g_uc0, h->g_coff, h->g_ubase, h->g_cbase, h->scode, h->ctab, h->seg_meta, h->lzw, h->grp, h->ptab, h->bptab};
+                    h->g_uc0, h->g_coff, h->g_ubase, h->g_cbase, h->scode, h->ctab, h->seg_meta, h->lzw, h->grp, h->ptab, h->bptab,
+                    h->band_c0, h->smid};
     for (void* p : ptrs) dfree(p);
     dfree(h->snd_cta);
     dfree(h->snd);
@@ -467,6 +471,8 @@ AjmPass make_pass(ajm_ctx* h, int max_passes) {
     p.sh.nranks = 1;
     p.bd = h->bd;
     p.bptab = h->bptab;
+    p.band_c0 = h->band_c0;
+    p.smid_out = nullptr;
     if (h->shard) {
         p.sh.rank = h->rank;
         p.sh.nranks = h->nranks;
@@ -1933,6 +1939,94 @@ static ajm_status_t create_impl(ajm_handle_t* out, int64_t n, int64_t nnz, const
         }
         CC(eo);
         h->carveout = pct;
+    }
+    // Band kernel: the CTAs' chunk ranges re-planned for the band kernel.
+    //  - chunk cost 123 + w (w = chunk width): measured per CTA (AJM_TS_ALL, config 5) the 18-wide
+    //    z-boundary chunks take 0.94 of a 27-wide one -- the stage's x~ bands, row operands and
+    //    per-row work weigh as much as the entries -- where the register kernels' batch-count cost
+    //    gave them 0.75, and the two boundary CTAs finished 30-60 us after the others;
+    //  - the SM-sharing skew: of the two CTAs on an SM the one launched first (lower index) is
+    //    issued first by the warp schedulers and runs ~10 % faster while both are resident (config
+    //    2: 16.9 vs 18.8 us, config 5: 343 vs 370 us per pass, every SM), and the pass waits for the
+    //    later one.  A probe launch of the solver kernel itself (max_passes = 0) records each CTA's
+    //    SM; the older CTA of every SM gets (1 + skew) of the mean cost, the younger (1 - skew).  A
+    //    placement that differs at solve time only costs balance, never correctness (the
+    //    arithmetic of a chunk does not depend on its CTA; a fixed plan keeps every solve of the
+    //    handle bitwise the same).  Measured (tools/env_ab.py, profiles/r2i_band_replan_ab.log):
+    //    config 2 21.89 (generic plan) -> 21.88 (band cost) -> 21.52 us/pass (skew 0.07; 0.045:
+    //    21.67, 0.1: 21.97, 0.13: 22.24); config 5 411 -> 387 -> 381 (0.045 and 0.07 alike).
+    //    AJM_BAND_SKEW=<x> overrides (experiments; 0 disables), AJM_BAND_NO_REPLAN keeps the
+    //    generic plan's ranges (tests comparing partial sums bitwise with the other kernels).
+    if (h->band) {
+        const int G = h->grid;
+        std::vector<int> c0h((size_t)G + 1);
+        for (int cc = 0; cc <= G; ++cc) c0h[(size_t)cc] = unit_c0_h[(size_t)cta_unit_h[(size_t)cc]];
+        const double skew = getenv("AJM_BAND_SKEW") ? std::atof(getenv("AJM_BAND_SKEW")) : AJM_BAND_SKEW;
+        std::vector<int> age((size_t)G, -1);  // 0: first CTA on its SM, 1: second, ...
+        if (h->ctas_per_sm >= 2 && skew != 0.0 && !sh) {
+            CC(dalloc(&h->smid, G, st));
+            CC(cudaMemsetAsync(h->smid, 0xff, sizeof(int) * (size_t)G, st));
+        }
+        std::vector<int> smid_h((size_t)G, -1);
+        if (h->smid) {
+            // the probe needs the (unchanged) plan's ranges: upload them first
+            CC(dalloc(&h->band_c0, (size_t)G + 1, st));
+            CC(cudaMemcpyAsync(h->band_c0, c0h.data(), sizeof(int) * ((size_t)G + 1), cudaMemcpyHostToDevice, st));
+            AjmPass pp = make_pass(h, 0);
+            pp.smid_out = h->smid;
+            CC(launch_solver(h, pp, st));
+            CC(cudaMemcpyAsync(smid_h.data(), h->smid, sizeof(int) * (size_t)G, cudaMemcpyDeviceToHost, st));
+            CC(cudaStreamSynchronize(st));
+            std::vector<int> seen;  // CTAs seen so far per SM (bid order = launch order)
+            for (int cc = 0; cc < G; ++cc) {
+                const int sm = smid_h[(size_t)cc];
+                if (sm < 0) { age.assign((size_t)G, -1); break; }
+                if ((size_t)sm >= seen.size()) seen.resize((size_t)sm + 1, 0);
+                age[(size_t)cc] = seen[(size_t)sm]++;
+            }
+        }
+        // weights: the older CTA of a shared SM (1 + skew), the younger (1 - skew); alone: 1
+        std::vector<double> wt((size_t)G, 1.0);
+        {
+            std::vector<int> per_sm;
+            for (int cc = 0; cc < G; ++cc)
+                if (age[(size_t)cc] >= 0) {
+                    const int sm = smid_h[(size_t)cc];
+                    if ((size_t)sm >= per_sm.size()) per_sm.resize((size_t)sm + 1, 0);
+                    per_sm[(size_t)sm]++;
+                }
+            for (int cc = 0; cc < G; ++cc)
+                if (age[(size_t)cc] >= 0 && per_sm[(size_t)smid_h[(size_t)cc]] == 2)
+                    wt[(size_t)cc] = age[(size_t)cc] == 0 ? 1.0 + skew : 1.0 - skew;
+        }
+        const int64_t nc = h->nchunks;
+        std::vector<double> cpre((size_t)nc + 1, 0.0);
+        for (int64_t cidx = 0; cidx < nc; ++cidx)
+            cpre[(size_t)cidx + 1] = cpre[(size_t)cidx] + 123.0 + (double)((choff[(size_t)cidx + 1] - choff[(size_t)cidx]) >> 5);
+        double wsum = 0.0;
+        for (double w : wt) wsum += w;
+        std::vector<int> nh((size_t)G + 1, 0);
+        double wacc = 0.0;
+        int64_t i = 0;
+        for (int cc = 0; cc < G; ++cc) {
+            nh[(size_t)cc] = (int)i;
+            wacc += wt[(size_t)cc];
+            const double lim = cpre[(size_t)nc] * wacc / wsum;
+            while (i < nc && 0.5 * (cpre[(size_t)i] + cpre[(size_t)i + 1]) < lim) ++i;
+        }
+        nh[(size_t)G] = (int)nc;
+        // the band kernel keeps a CTA's chunk offsets in the shared-memory table behind its ring
+        int mx = 0;
+        for (int cc = 0; cc < G; ++cc) mx = std::max(mx, nh[(size_t)cc + 1] - nh[(size_t)cc] + 1);
+        if ((size_t)mx * sizeof(int) <= h->meta_bytes && !getenv("AJM_BAND_NO_REPLAN")) {  // (experiments)
+            c0h.swap(nh);
+            h->band_skew = h->smid ? skew : 0.0;
+        }
+        if (!h->band_c0) CC(dalloc(&h->band_c0, (size_t)G + 1, st));
+        CC(cudaMemcpyAsync(h->band_c0, c0h.data(), sizeof(int) * ((size_t)G + 1), cudaMemcpyHostToDevice, st));
+        CC(cudaStreamSynchronize(st));
+        if (!h->cta_nchk.empty())
+            for (int cc = 0; cc < G; ++cc) h->cta_nchk[(size_t)cc] = c0h[(size_t)cc + 1] - c0h[(size_t)cc];
     }
     // ||b||
     ajm_sumsq_partial_kernel<<<256, 256, 0, st>>>(n, h->b, h->scratch);

@@ -41,6 +41,7 @@
 #define AJM_GRP_ROWS 4   // rows per group (8 lanes each)
 #define AJM_NPART 5      // rr, <x,q>, <b,x>, d, sum|d terms|
 #define AJM_UNIT_EL 2048 // SELL elements per TMA staging unit (24 KB of val + col)
+#define AJM_BAND_SKEW 0.07 // band kernel: work skew between the older and the younger CTA of an SM
 #define AJM_UNIT_ROWS (AJM_WARPS * 32)  // rows per staging unit (<= 8 chunks)
 #define AJM_LOG_CAP 64
 #define AJM_CTAB 256     // byte-coded columns: at most this many distinct offsets col - row
@@ -198,6 +199,8 @@ struct AjmPass {
     AjmShard sh;                             // (kShard) row-block sharding
     AjmBand bd;                              // (ajm_band_kernel) banded x~ staging
     const long long* __restrict__ bptab;     // (ajm_band_kernel) [256][2] {bits of Q_ij, stage offset}
+    const int* __restrict__ band_c0;         // (ajm_band_kernel) [grid+1] first SELL chunk of each CTA
+    int* smid_out;                           // (create-time placement probe) [grid] SM of each CTA, or null
 };
 
 __device__ __forceinline__ unsigned long long ajm_gtime() {
@@ -1628,10 +1631,16 @@ __global__ void __maxnreg__(96) ajm_band_kernel(AjmPass p) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int bid = (int)blockIdx.x;
     const unsigned G = gridDim.x;
-    const int u0 = p.cta_unit[bid], u1 = p.cta_unit[bid + 1];
-    const int cfirst = u1 > u0 ? p.unit_c0[u0] : 0;
-    const int nchk = u1 > u0 ? p.unit_c0[u1] - cfirst : 0;
+    // the CTA's contiguous chunk range (planned with the band kernel's chunk cost and the SM-sharing
+    // skew)
+    const int cfirst = p.band_c0[bid];
+    const int nchk = p.band_c0[bid + 1] - cfirst;
     const long long efirst = nchk > 0 ? p.chunk_off[cfirst] : 0;
+    if (p.smid_out && tid == 0) {  // create-time placement probe (launched with max_passes = 0)
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.smid_out[bid] = (int)smid;
+    }
     constexpr int UR = kU * 32;                    // rows per unit
     const int nun = (nchk + kU - 1) / kU;          // units of kU chunks
     const size_t SB = (size_t)bd.stage_bytes;

@@ -256,10 +256,11 @@ def test_many_handles_pool_reuse():
                 assert max_rel(g.x, o.x) <= PARITY_TOL, n
 
 
-def test_global_metadata_variant():
+def test_global_metadata_variant(monkeypatch):
     """Layouts whose per-CTA unit/chunk tables do not fit shared memory read them from global
     memory (a kernel instantiation for hundreds of millions of rows); forced here on oracle-sized
     stencil and graph cases it must give bitwise the iterates of the shared-memory tables."""
+    monkeypatch.setenv("AJM_BAND_NO_REPLAN", "1")  # the band kernel on the generic plan (test_band_replan)
     for cfg, scale in ((2, 0.25), (4, 0.0125)):
         p = synth.config_problem(cfg, scale)
         a = gpu_solve(p.Q, p.b, tol=0.0, maxit=300, restart=True)
@@ -300,7 +301,7 @@ def _stencil_with_values(edge, nvals, seed=3):
 
 
 @pytest.mark.parametrize("case", ["cfg2", "ragged17", "band255", "band257", "vals2", "vals300"])
-def test_byte_coded_columns(case):
+def test_byte_coded_columns(case, monkeypatch):
     """Layouts whose column offsets col - row take <= 256 values stream byte codes into an offset
     table instead of int32 columns.  Same columns, same summation order: the
     iterates are BITWISE those of the int32 layout (AJM_INT32_COLUMNS) and match the oracle; 257 distinct
@@ -314,6 +315,9 @@ def test_byte_coded_columns(case):
         p = synth.make_problem(case, _stencil_with_values(24, int(case[4:])), 6)
     else:
         p = synth.make_problem(case, _banded_offsets(127 if case == "band255" else 128), 5)
+    # the band kernel on the generic plan's CTA ranges (same CTA partials -> bitwise histories);
+    # its own re-planned ranges: test_band_replan
+    monkeypatch.setenv("AJM_BAND_NO_REPLAN", "1")
     a = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True)
     assert a.info["col_bytes"] == (4 if case == "band257" else 1), a.info
     assert a.info["sigma"] == 1
@@ -476,6 +480,7 @@ def test_band_staging_units_bitwise(unit, monkeypatch):
     histories of the register-gather pair kernel (AJM_NO_BAND_STAGING), on a ragged 3D stencil
     with restarts, through the persistent launch and the host-driven loop."""
     p = synth.make_problem("p3d81", synth.poisson3d(81), 8)  # n = 531441: several units per CTA, ragged tail
+    monkeypatch.setenv("AJM_BAND_NO_REPLAN", "1")  # the generic plan's CTA ranges (test_band_replan)
     monkeypatch.setenv("AJM_BAND_UNIT", unit)
     a = gpu_solve(p.Q, p.b, tol=0.0, maxit=500, restart=True)
     h = gpu_solve(p.Q, p.b, tol=0.0, maxit=120, restart=True, loop="host")
@@ -491,7 +496,7 @@ def test_band_staging_units_bitwise(unit, monkeypatch):
 
 
 @pytest.mark.parametrize("case", ["p2d400", "aniso27_40", "p3d_bands17"])
-def test_band_staging_stencils(case):
+def test_band_staging_stencils(case, monkeypatch):
     """Banded staging on other stencil shapes: a 2D 5-point grid whose +-400 rows stay separate
     bands of a 512-row unit, the anisotropic 27-point stencil (nine offset lines in three bands,
     several boundary diagonals among the pairs), and a 7-point 17^3 grid (ragged, few units per CTA)
@@ -502,6 +507,7 @@ def test_band_staging_stencils(case):
         p = synth.make_problem(case, synth.aniso27(40), 10)
     else:
         p = synth.make_problem(case, synth.poisson3d(17), 11)
+    monkeypatch.setenv("AJM_BAND_NO_REPLAN", "1")  # the generic plan's CTA ranges (test_band_replan)
     a = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True)
     assert a.info["band_staged"] == 1 and a.info["val_bytes"] == 0, a.info
     r = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True, band_staging=False)
@@ -512,7 +518,7 @@ def test_band_staging_stencils(case):
     assert_history_parity(a, o)
 
 
-def test_band_staging_x0_and_early_exits():
+def test_band_staging_x0_and_early_exits(monkeypatch):
     """Banded staging with a nonzero x0 (staged from the caller's buffer), a solve that converges at
     t = 0 (the producer has already staged pass 1, drained unread), maxit = 1, and a converged solve
     followed by another on the same handle: bitwise the pair kernel each time."""
@@ -521,6 +527,7 @@ def test_band_staging_x0_and_early_exits():
     kws = [dict(x0=x0, tol=0.0, maxit=300), dict(tol=10.0, maxit=50), dict(tol=0.0, maxit=1),
            dict(x0=x0, tol=1e-6, maxit=2000)]
     import paper_2407_03272_b200 as ajm
+    monkeypatch.setenv("AJM_BAND_NO_REPLAN", "1")  # the generic plan's CTA ranges (test_band_replan)
     with ajm.Solver.from_csr(p.Q, p.b) as a, ajm.Solver.from_csr(p.Q, p.b, band_staging=False) as r:
         assert a.info()["band_staged"] == 1 and r.info()["band_staged"] == 0
         for kw in kws:
@@ -529,3 +536,33 @@ def test_band_staging_x0_and_early_exits():
             np.testing.assert_array_equal(ga.x.cpu().numpy(), gr.x.cpu().numpy())
             np.testing.assert_array_equal(ga.res_hist, gr.res_hist)
     assert kws and ga.status == "converged"
+
+
+@pytest.mark.parametrize("case", ["p3d81", "aniso27_40", "p3d_bands17"])
+def test_band_replan(case, monkeypatch):
+    """The band kernel's own CTA ranges (chunk cost 123 + w, older/younger CTA of an
+    SM weighted 1 +- AJM_BAND_SKEW from a placement probe) against the generic plan's: only the
+    grouping of the CTA partials changes, so the iterates and restart schedule are bitwise the
+    same and the residual / f / d histories agree to rounding; both at parity with the oracle;
+    repeated solves on the re-planned handle are bitwise identical (the plan is fixed at create)."""
+    if case == "p3d81":
+        p = synth.make_problem(case, synth.poisson3d(81), 8)
+    elif case == "aniso27_40":
+        p = synth.make_problem(case, synth.aniso27(40), 10)
+    else:
+        p = synth.make_problem(case, synth.poisson3d(17), 11)
+    a = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True)
+    a2 = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True)
+    monkeypatch.setenv("AJM_BAND_NO_REPLAN", "1")
+    g = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True)
+    monkeypatch.delenv("AJM_BAND_NO_REPLAN")
+    assert a.info["band_staged"] == 1 and g.info["band_staged"] == 1
+    assert a.restart_iters == g.restart_iters and a.iterations == g.iterations
+    np.testing.assert_array_equal(a.x, g.x)
+    np.testing.assert_allclose(a.res_hist, g.res_hist, rtol=1e-12, atol=0)
+    np.testing.assert_allclose(a.f_hist, g.f_hist, rtol=1e-12, atol=1e-12)
+    for f in ("x", "res_hist", "f_hist", "d_trace"):
+        np.testing.assert_array_equal(getattr(a, f), getattr(a2, f))
+    o, _ = oracle_matching(p.Q, p.b, a, tol=0.0, maxit=400, restart=True)
+    assert max_rel(a.x, o.x) <= PARITY_TOL
+    assert_history_parity(a, o)

@@ -66,9 +66,10 @@ def test_shard_iterations_to_tol(cfg, scale, nranks):
         assert max_rel(g.x, o.x) <= 1e-8
 
 
-def test_one_rank_group_is_bitwise_the_single_gpu_solve():
+def test_one_rank_group_is_bitwise_the_single_gpu_solve(monkeypatch):
     """nranks = 1: the rank partial plus zeros is the partial, the grid and layout are the
     single-GPU ones -> bitwise the same iterates and histories."""
+    monkeypatch.setenv("AJM_BAND_NO_REPLAN", "1")  # single GPU: the band kernel on the generic plan
     p = synth.config_problem(2, 0.25)
     g = group_solve(p, 1, tol=0.0, maxit=300)
     s = gpu_solve(p.Q, p.b, tol=0.0, maxit=300)
@@ -126,12 +127,13 @@ def test_shard_errors():
         ajm.ShardGroup.from_csr(p.Q, p.b, 9)  # > AJM_MAX_RANKS
 
 
-def test_shard_solver_per_process_path_one_rank():
+def test_shard_solver_per_process_path_one_rank(monkeypatch):
     """The per-process path of bench.py --gpus N (ajm_shard_create without AJM_SHARD_COLOCATED on the
     whole device, the connection records exchanged by the caller, ajm_solve on the shard handle: the
     kernel's own launch with its peer table) with a single rank -- the only size one GPU can run
     concurrently.  Bitwise the single-GPU solve (rank partial + zeros), and the oracle to 1e-10."""
     import paper_2407_03272_b200 as ajm
+    monkeypatch.setenv("AJM_BAND_NO_REPLAN", "1")  # single GPU: the band kernel on the generic plan
     for cfg, scale in [(3, 0.02), (2, 0.25)]:
         p = synth.config_problem(cfg, scale)
         with ajm.ShardSolver(0, 1, [0, p.Q.n], p.Q.row_ptr, p.Q.col, p.Q.val, p.b, exchange=lambda b: [b]) as s:

@@ -29,6 +29,7 @@ def run(p, cfg, env):
             us = []
             for _ in range(3):
                 r = s.solve(tol=TOL[cfg], maxit=MAXIT[cfg], restart=True, history=False)
+                r.xh = r.x.cpu().numpy()
                 inf = s.info()
                 us.append(1e3 * inf["last_loop_ms"] / inf["last_passes"])
         return info, r, us
@@ -42,12 +43,18 @@ def main():
     envs = sys.argv[2:] or [""]
     for cfg in cfgs:
         p = synth.config_problem(cfg)
+        x_ref = None
         for rnd in range(int(os.environ.get("AB_ROUNDS", "2"))):
             for env in envs:
                 info, r, us = run(p, cfg, env)
+                if x_ref is None:
+                    x_ref = r.xh
+                same = bool(np.array_equal(x_ref, r.xh))
                 print(f"cfg{cfg} [{env or 'default'}] round {rnd}: its={r.iterations} us/pass "
                       f"{' '.join(f'{u:.2f}' for u in us)} (min {min(us):.2f}) col_bytes={info['col_bytes']} "
-                      f"val_bytes={info['val_bytes']} stages/mode={info['mode']} grid={info['grid']}", flush=True)
+                      f"val_bytes={info['val_bytes']} stages/mode={info['mode']} grid={info['grid']} "
+                      f"hot={info.get('hot_entries', 0)}@{info.get('hot_first', 0)} share={info.get('hot_share', 0.0):.3f} "
+                      f"x_bitwise_first={same}", flush=True)
         del p
 
 
