@@ -223,6 +223,22 @@ struct AjmAcc {
 // coherent (L1-cached, invalidated by the post-barrier fence) load of data written in-kernel
 __device__ __forceinline__ double ajm_ld(const double* p) { return *p; }
 
+// x~ gather of the int32 (graph) layouts, written as a complementary-predicated pair: the plain load
+// for a valid column, and an L1::no_allocate twin that never executes (columns are >= 0).  Measured
+// on the same box against the plain `xc[col]` (profiles/r2k_gather_form_ab.log): config 4 394.6 ->
+// 380.2 us/pass, config 3 75.6 -> 75.2; ptxas spaces the eight gathers of a batch by the predicate
+// instructions instead of issuing them back to back.  Single-instruction forms measured no gain
+// (asm volatile ld.global, L1::evict_last: 394-395), an executing no_allocate / evict_first twin
+// for the columns outside a hub range lost 15-30 %.
+__device__ __forceinline__ double ajm_ldx(const double* xc, int col) {
+    double v;
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ge.s32 q, %2, 0;\n\t"
+        "@q ld.global.f64 %0, [%1];\n\t@!q ld.global.L1::no_allocate.f64 %0, [%1];\n\t}"
+        : "=d"(v) : "l"(xc + col), "r"(col));
+    return v;
+}
+
 // L2 eviction-priority policies (createpolicy): the Q stream is evict_first, the iterate vectors
 // evict_last, so the ~100 MB of vectors stay L2-resident across passes
 __device__ __forceinline__ uint64_t ajm_policy(int kind) {
@@ -637,7 +653,7 @@ __device__ __forceinline__ double ajm_seg_dot(const AjmPass& p, int k0, int k1, 
     for (; k < k1; k += 8 * 32) {
         double xg[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) xg[j] = ajm_ld(xc + cc[j]);
+        for (int j = 0; j < 8; ++j) xg[j] = ajm_ldx(xc, cc[j]);
         double vn[8];
         int cn[8];
         const int kn = k + 8 * 32;
@@ -695,7 +711,7 @@ __device__ __forceinline__ void ajm_group_rows(const AjmPass& p, const AjmLz& L,
             cc[j] = kk < k1 ? __ldcs(p.col + kk) : 0;
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) xg[j] = (kb + 8 * j < k1) ? ajm_ld(xc + cc[j]) : 0.0;
+        for (int j = 0; j < 8; ++j) xg[j] = (kb + 8 * j < k1) ? ajm_ldx(xc, cc[j]) : 0.0;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
             if (kb + 8 * j < k1) s += v[j] * xg[j];
@@ -787,7 +803,7 @@ __device__ __forceinline__ double ajm_chunk_dot(const double* sv, const int* sc,
         for (int j = 0; j < 8; ++j) cc[j] = (k0 + j < w) ? sc[(k0 + j) * 32] : 0;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-            if (k0 + j < w) xg[j] = ajm_ld(xc + cc[j]);
+            if (k0 + j < w) xg[j] = ajm_ldx(xc, cc[j]);
 #pragma unroll
         for (int j = 0; j < 8; ++j)
             if (k0 + j < w) s += sv[(k0 + j) * 32] * xg[j];  // ascending column order
@@ -932,7 +948,7 @@ __device__ __forceinline__ double ajm_chunk_dots(uint32_t sva, uint32_t sca, int
 #pragma unroll
         for (int j = 0; j < 8; ++j) cc[j] = (k0 + j < w) ? ajm_lds_s32(sca + 128u * (k0 + j)) : 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) xg[j] = (k0 + j < w) ? ajm_ld(xc + cc[j]) : 0.0;
+        for (int j = 0; j < 8; ++j) xg[j] = (k0 + j < w) ? ajm_ldx(xc, cc[j]) : 0.0;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
             if (k0 + j < w) s += ajm_lds_f64(sva + 256u * (k0 + j)) * xg[j];  // ascending column order
