@@ -63,6 +63,25 @@ def test_bitwise_equal_to_mirror_oracle():
             assert m.res_hist[t] < 1e-13  # only at machine-precision residuals
 
 
+def test_bitwise_equal_to_mirror_oracle_graph_layout():
+    """The same on a sorted-window int32 layout (ER Laplacian, rows <= 64: the SELL chunk dot with
+    the predicated-pair gathers, relabelled rows): every row sum is sequential in ascending column
+    order, so the iterates are bitwise the mirror oracle's while the restart decisions agree."""
+    p = synth.config_problem(3, 0.02)
+    g = gpu_solve(p.Q, p.b, tol=0.0, maxit=400, restart=True)
+    assert g.info["sigma"] > 1 and g.info["col_bytes"] == 4 and g.info["seg_rows"] == 0
+    m = oracle.solve(p.Q, p.b, tol=0.0, maxit=400, restart=True, mirror=True)
+    if g.restart_iters == m.restart_iters:
+        np.testing.assert_array_equal(g.x, m.x)
+    else:
+        t = min(set(g.restart_iters) ^ set(m.restart_iters))
+        assert m.res_hist[t] < 1e-13  # only at machine-precision residuals
+        k = t - 1
+        g2 = gpu_solve(p.Q, p.b, tol=0.0, maxit=k, restart=True)
+        m2 = oracle.solve(p.Q, p.b, tol=0.0, maxit=k, restart=True, mirror=True)
+        np.testing.assert_array_equal(g2.x, m2.x)
+
+
 def test_determinism_and_loop_modes():
     p = synth.config_problem(2, 0.25)
     a = gpu_solve(p.Q, p.b, tol=0.0, maxit=300)
