@@ -35,12 +35,18 @@
 
 #define AJM_BLOCK 256
 #define AJM_WARPS (AJM_BLOCK / 32)
-#define AJM_SELL_MAX 64  // rows up to this length go to SELL (thread per row)
+#ifndef AJM_SELL_MAX
+#define AJM_SELL_MAX 64
+#endif
+// AJM_SELL_MAX: rows up to this length go to SELL (thread per row)
 #define AJM_SEG 2048     // max nonzeros per warp segment of a longer row
 #define AJM_GRP_MAX 256  // rows of AJM_SELL_MAX+1 .. this many nonzeros: sub-warp groups (static plan)
 #define AJM_GRP_ROWS 4   // rows per group (8 lanes each)
 #define AJM_NPART 5      // rr, <x,q>, <b,x>, d, sum|d terms|
-#define AJM_UNIT_EL 2048 // SELL elements per TMA staging unit (24 KB of val + col)
+#ifndef AJM_UNIT_EL
+#define AJM_UNIT_EL 2048
+#endif
+// AJM_UNIT_EL: SELL elements per TMA staging unit (24 KB of val + col)
 #define AJM_BAND_SKEW 0.07 // band kernel: work skew between the older and the younger CTA of an SM
 #define AJM_UNIT_ROWS (AJM_WARPS * 32)  // rows per staging unit (<= 8 chunks)
 #define AJM_LOG_CAP 64
